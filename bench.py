@@ -1,0 +1,296 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 smooth-distance engine (exact path, BASELINE cfg2).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+A step is one exact pass of d_hat + grad over the workload's queries
+(smooth_min_dist_flat for every query, smooth.hpp:189-198): BASELINE.json
+configs[1], the helix polyline (20,000 edges) against 262,144 queries per
+GPU, alpha = 100, fp32. Multi-GPU runs shard queries (each rank its own
+block of the same query distribution) with the geometry replicated: no
+collective on the data path, "scaling": "weak". One JSON line on rank 0.
+
+--impl reference times the reference CPU evaluator of the same path on this
+host's cores: the reference cannot be built here (Eigen3/GTest/CLI11 are
+absent), so its line-faithful fp64 restatement in oracle/ stands in
+("kind": "port"). Only that leg and the cpu_baseline leg execute oracle/.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FLOPS_PER_EDGE_PAIR = 62      # SURVEY 8(d) canonical count, S != 1
+MUFU_PER_EDGE_PAIR = 5
+QUERIES_PER_GPU = 262144
+ALPHA = 100.0
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax.append(float(f[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(smax), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def measure_peaks():
+    L = ctypes.CDLL(os.path.join(ROOT, "paper_2108_10480_b200", "libsdpeaks.so"))
+    f, d, m = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+    L.sd_measure_peaks.argtypes = [ctypes.POINTER(ctypes.c_double)] * 3
+    if L.sd_measure_peaks(ctypes.byref(f), ctypes.byref(d), ctypes.byref(m)) != 0:
+        return None
+    return {"ffma_tflops": f.value / 1e12, "dfma_tflops": d.value / 1e12, "mufu_tops": m.value / 1e12}
+
+
+def workload(block: int):
+    from paper_2108_10480_b200 import configs
+    w, q = configs.cfg2(QUERIES_PER_GPU, block=block)
+    v = configs.quantize(w.vertices)
+    q = configs.quantize(q)
+    wt = configs.weights_without_triangles(w.simplices, w.kinds, len(v))
+    return w, v, q, wt
+
+
+def cpu_sample(v, s, k, wt, q, threads, target_s=12.0):
+    """Times the oracle port on a bounded prefix of the queries, sized from a
+    pilot so that the sample takes about target_s seconds."""
+    import oracle as O
+    m = O.Mesh.from_arrays(v, s, k)
+    w = O.Weights.from_table(O.WeightTable(wt.A, wt.sup_wtilde, wt.edge_a, wt.tri_stored, wt.poly_index))
+    p = O.Params(alpha=ALPHA, alpha_u=600.0, beta=0.0)
+    pilot = max(threads * 2, 64)
+    r = O.query(m, w, q[:pilot], p, threads=threads)
+    n = int(min(len(q), max(pilot, pilot * target_s / max(r.seconds, 1e-3))))
+    r = O.query(m, w, q[:n], p, threads=threads)
+    return n, r.seconds, r
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    import oracle as O
+    O.build()
+    w, v, q, wt = workload(0)
+    threads = O.hardware_threads()
+    N = len(w.kinds)
+    n, secs, _ = cpu_sample(v, w.simplices, w.kinds, wt, q, threads, target_s=3.0)
+    import oracle as O2  # noqa: F401  (same module; warm-up steps below)
+    m = O.Mesh.from_arrays(v, w.simplices, w.kinds)
+    ws = O.Weights.from_table(O.WeightTable(wt.A, wt.sup_wtilde, wt.edge_a, wt.tri_stored, wt.poly_index))
+    p = O.Params(alpha=ALPHA, alpha_u=600.0, beta=0.0)
+    for i in range(args.warmup):
+        O.query(m, ws, q[:n], p, threads=threads)
+    times = []
+    for i in range(args.steps):
+        lo = (i * n) % max(1, len(q) - n)
+        r = O.query(m, ws, q[lo:lo + n], p, threads=threads)
+        times.append(r.seconds)
+    t = float(np.mean(times))
+    value = n * N / t
+    line = {
+        "impl": "reference", "metric": "exact pair-evals/s (value+grad)", "value": value, "unit": "pair-evals/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "cfg2: helix polyline 20,000 edges, exact LSE, alpha=100 (BASELINE configs[1])",
+                   "queries_per_step": n, "primitives": N, "parallelism": f"{threads} host threads"},
+        "cpu_baseline": {"value": value, "unit": "pair-evals/s", "cores": threads, "kind": "port",
+                         "sample": f"{n} of {QUERIES_PER_GPU} cfg2 queries x {N} edges per step"},
+        "e2e": {"value": value, "unit": "pair-evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, rank, world, local):
+    import torch
+    import paper_2108_10480_b200 as sd
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    w, v, q, wt = workload(rank)
+    N, Q = len(w.kinds), len(q)
+    eng = sd.Engine(local, sd.SD_FP32)
+    eng.set_geometry(v, w.simplices, w.kinds)
+    eng.set_weights(wt.A, wt.sup_wtilde, wt.edge_a, wt.tri_stored, wt.poly_index)
+    P = sd.SmoothParams(alpha=ALPHA, alpha_u=600.0, beta=0.0)
+
+    dev = torch.device("cuda", local)
+    qd = torch.tensor(q, dtype=torch.float32, device=dev)
+    d_hat = torch.empty(Q, dtype=torch.float64, device=dev)
+    grad = torch.empty(Q, 3, dtype=torch.float64, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        eng.query_points_device(qd.data_ptr(), Q, P, sd.SD_EXACT, d_hat.data_ptr(), grad.data_ptr(),
+                                stream=stream.cuda_stream)
+
+    peaks = measure_peaks() if rank == 0 or True else None
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    launches_per_step = eng.last_launch_count()
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.zero_()  # L2 flush between timed iterations (outside the events)
+            evs[i][0].record(stream)
+            step()
+            evs[i][1].record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    ms = float(np.mean(step_ms))
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    ms_max = float(t.item())
+    pairs_per_rank = Q * N
+    value = world * pairs_per_rank / (ms_max * 1e-3)
+
+    # end to end through the public host API: pinned host q in, d_hat+grad out
+    qh = torch.tensor(q, dtype=torch.float64).pin_memory().numpy()
+    e2e_times = []
+    barrier()
+    for i in range(max(1, args.steps // 2)):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        r = eng.query_points(qh, P, sd.SD_EXACT, want_grad=True)
+        e2e_times.append(time.perf_counter() - t0)
+    e2e_s = float(np.mean(e2e_times))
+    te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
+    e2e_value = world * pairs_per_rank / float(te.item())
+
+    if rank == 0:
+        achieved = pairs_per_rank * FLOPS_PER_EDGE_PAIR / (ms_max * 1e-3) / 1e12
+        roof = {"bound": "fp32-fma", "achieved": achieved, "unit": "TFLOP/s", "traffic": None,
+                "kernel": "exact_kernel<float, edge, poly> x3 segment launches + finalize (step time)",
+                "algorithmic": f"{FLOPS_PER_EDGE_PAIR} flop x {pairs_per_rank} edge pairs per step"}
+        if peaks:
+            roof.update({"peak": peaks["ffma_tflops"], "frac": achieved / peaks["ffma_tflops"],
+                         "peak_source": "in-run FFMA microbenchmark (libsdpeaks.so); MEASURED_PEAKS.json has no FP32 entry",
+                         "mufu_frac": pairs_per_rank * MUFU_PER_EDGE_PAIR / (ms_max * 1e-3) / 1e12 / peaks["mufu_tops"],
+                         "peaks": peaks})
+        cpu = None
+        if world == 1 and not args.no_cpu:
+            import oracle as O
+            O.build()
+            threads = O.hardware_threads()
+            n, secs, _ = cpu_sample(v, w.simplices, w.kinds, wt, q, threads)
+            cpu = {"value": n * N / secs, "unit": "pair-evals/s", "cores": threads, "kind": "port",
+                   "sample": f"first {n} of {Q} cfg2 queries x {N} edges ({secs:.1f} s, fp64 oracle port)"}
+        line = {
+            "metric": "exact pair-evals/s (value+grad)", "value": value, "unit": "pair-evals/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "cfg2: helix polyline 20,000 edges x 262,144 queries per GPU, exact LSE, "
+                                   "alpha=100, fp32 (BASELINE configs[1])",
+                       "queries_per_gpu": Q, "primitives": N, "l2": "flushed between timed steps (256 MiB write)",
+                       "parallelism": f"query-sharded x{world}, geometry replicated"},
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": "pair-evals/s", "h2d_bytes_per_step": Q * 3 * 8,
+                    "d2h_bytes_per_step": Q * 4 * 8},
+            "gpu_launches": launches_per_step * args.steps,
+            "clocks": clk.summary(),
+            "step_ms_all": step_ms,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    args = ap.parse_args()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_ours(args, rank, world, local)
+
+
+if __name__ == "__main__":
+    main()

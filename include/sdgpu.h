@@ -1,0 +1,144 @@
+/* include/sdgpu.h -- C ABI of the B200-native smooth-distance query engine.
+ *
+ * Drop-in boundary for the batched point-query evaluator of the reference
+ * (arXiv 2108.10480, /root/reference/proj/include/smoothdist). The reference
+ * has no plugin/FFI layer of its own: its boundary IS the header-only C++
+ * API below, and each entry point here replaces one or more of those calls
+ * for a whole batch of queries:
+ *
+ *   sd_set_geometry      <- SimplexMesh / Simplex / SimplexKind   (mesh.hpp:15-50)
+ *   sd_set_weights       <- WeightSet (+ build_weight_set result)  (weights.hpp:565-621)
+ *   sd_set_bvh           <- Bvh / BvhNode, reference layout        (bvh.hpp:14-32)
+ *   sd_build_bvh         <- build_bvh                              (bvh.hpp:34-91)
+ *   sd_export_bvh        <- Bvh::nodes (save_bvh_cache record)     (bvh.hpp:193-212)
+ *   sd_query_points      <- smooth_min_dist(mesh, bvh, ws, q, params) per query
+ *                           (smooth.hpp:166-184; beta > 0 => Barnes-Hut tree path)
+ *                           smooth_min_dist_flat(mesh, ws, q, params)
+ *                           (smooth.hpp:189-198; SD_EXACT)
+ *   sd_finalize_device   <- detail::result_from_accum              (smooth.hpp:147-159)
+ *   sd_params            <- SmoothParams {alpha, alpha_u, beta, epsilon} (params.hpp:13-22)
+ *   sd_outputs           <- SmoothResult {d_hat, grad, c, grad_c, leaves, far_field}
+ *                           (smooth.hpp:20-27)
+ *
+ * Error convention: every call returns 0 on success or a negative SD_E*
+ * code, and sd_last_error() (thread-local) describes the failure, in place
+ * of the reference's fail() -> std::runtime_error (common.hpp:50). The
+ * evaluator semantics of the reference are kept: a query whose exponential
+ * sum underflows (every term has alpha * d > 708) reports d_hat = +inf and a
+ * zero gradient, never an error (smooth.hpp:151-155).
+ *
+ * There is no CPU fallback: without a CUDA device every compute entry point
+ * fails with SD_E_CUDA.
+ */
+#ifndef SDGPU_H
+#define SDGPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SDGPU_ABI_VERSION 1
+
+typedef struct sd_ctx sd_ctx;
+
+/* SmoothParams (params.hpp:13-22); alpha_q only matters for mesh-to-mesh
+ * queries, which are outside this path. */
+typedef struct sd_params {
+    double alpha;    /* LogSumExp sharpness, > 0 */
+    double alpha_u;  /* attenuation threshold: S = alpha / max(alpha, alpha_u) */
+    double beta;     /* Barnes-Hut admissibility; 0 = exact */
+    double epsilon;  /* gradient denominator guard (reference default 1e-300) */
+} sd_params;
+
+/* Reference BvhNode record, byte-compatible with the 72-byte struct of
+ * bvh.hpp:14-22 (Aabb box{lo, hi}; left, right (-1 on leaves), primitive,
+ * count; diameter = box diagonal). Root is node 0, ids are pre-order. */
+typedef struct sd_bvh_node {
+    double lo[3];
+    double hi[3];
+    int32_t left, right, primitive, count;
+    double diameter;
+} sd_bvh_node;
+
+/* Per-query outputs (SmoothResult, smooth.hpp:20-27). Only d_hat is
+ * required; any other pointer may be NULL. grad / grad_c are Q x 3. */
+typedef struct sd_outputs {
+    double* d_hat;
+    double* grad;
+    double* c;
+    double* grad_c;
+    int64_t* leaves;          /* exact leaf evaluations */
+    int64_t* far_field;       /* Barnes-Hut expansions taken */
+    uint64_t* decision_hash;  /* order-independent hash of {(node, far|leaf)} */
+} sd_outputs;
+
+enum { SD_FP32 = 0, SD_FP64 = 1 };                  /* arithmetic precision */
+enum { SD_EXACT = 0, SD_BVH = 1 };                  /* query mode */
+enum { SD_BVH_MEDIAN = 0, SD_BVH_LBVH = 1 };        /* tree builders */
+enum { SD_POINT = 0, SD_EDGE = 1, SD_TRIANGLE = 2 }; /* SimplexKind (mesh.hpp:15) */
+
+enum {
+    SD_OK = 0,
+    SD_E_ARG = -1,      /* invalid argument (mirrors the reference's fail()) */
+    SD_E_STATE = -2,    /* geometry / weights / tree missing or inconsistent */
+    SD_E_CUDA = -3,     /* CUDA runtime failure, or no device */
+    SD_E_NOMEM = -4
+};
+
+const char* sd_last_error(void);
+int sd_abi_version(void);
+
+/* One context per GPU (one process per GPU in multi-GPU runs). precision is
+ * SD_FP32 or SD_FP64. In SD_FP32 the vertex and query coordinates are
+ * rounded to float on upload. */
+int sd_create(sd_ctx** out, int device, int precision);
+int sd_destroy(sd_ctx* ctx);
+
+/* SimplexMesh: vertices V x 3 (AoS, = SimplexMesh::vertices.data()),
+ * simplices N x 3 int32 (unused corners -1) and N kinds. Validated as
+ * validate() does (mesh.hpp:55-87). Invalidates weights and tree. */
+int sd_set_geometry(sd_ctx* ctx, const double* xyz, int64_t V, const int32_t* simplices, const uint8_t* kinds,
+                    int64_t N);
+
+/* WeightSet as flat arrays: A, sup_wtilde, ne edge polynomials a[0..4]
+ * (EdgeWeightPoly::a), nt triangle polynomials stored[0..12]
+ * (TriWeightPoly::stored), poly_index[N] (-1: unit weight). */
+int sd_set_weights(sd_ctx* ctx, double A, double sup_wtilde, int32_t ne, const double* edge_a, int32_t nt,
+                   const double* tri_stored, const int32_t* poly_index);
+
+/* Upload a reference-layout tree (e.g. from the reference build_bvh), or
+ * build one on the GPU: SD_BVH_MEDIAN reproduces build_bvh exactly,
+ * SD_BVH_LBVH is the Morton-code linear BVH. Either way the tree can be
+ * exported in the reference layout so a CPU evaluator can run on it. */
+int sd_set_bvh(sd_ctx* ctx, const sd_bvh_node* nodes, int64_t n);
+int sd_build_bvh(sd_ctx* ctx, int method);
+int sd_bvh_size(sd_ctx* ctx, int64_t* n);
+int sd_export_bvh(sd_ctx* ctx, sd_bvh_node* out, int64_t cap);
+
+/* Batched point queries with HOST buffers: q is Q x 3 doubles. The call
+ * copies q to the device, evaluates, and copies the requested outputs back
+ * (blocking). mode SD_EXACT ignores beta; SD_BVH uses the tree. */
+int sd_query_points(sd_ctx* ctx, const double* q, int64_t Q, const sd_params* p, int mode, const sd_outputs* out);
+
+/* Same with DEVICE buffers on the caller's stream (cudaStream_t, may be
+ * NULL): q_dev is Q x 3 float (SD_FP32) or double (SD_FP64); outputs are
+ * device pointers. Asynchronous. */
+int sd_query_points_device(sd_ctx* ctx, const void* q_dev, int64_t Q, const sd_params* p, int mode,
+                           const sd_outputs* out_dev, void* stream);
+
+/* Primitive-sharded runs: after each shard wrote its unshifted fp64
+ * partial sums (c, grad_c) with sd_query_points_device and the shards were
+ * summed (e.g. one NCCL all-reduce), finalize d_hat / grad exactly as
+ * result_from_accum does (smooth.hpp:147-159). Device pointers. */
+int sd_finalize_device(sd_ctx* ctx, const double* c, const double* grad_c, int64_t Q, const sd_params* p,
+                       double* d_hat, double* grad, void* stream);
+
+/* Number of this library's kernels launched by the last query call. */
+int sd_last_launch_count(sd_ctx* ctx, int64_t* n);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SDGPU_H */

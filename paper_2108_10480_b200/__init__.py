@@ -1,0 +1,246 @@
+"""B200-native smooth-distance query engine (arXiv 2108.10480).
+
+Python host mirror of the reference C++ evaluator API
+(/root/reference/proj/include/smoothdist/smooth.hpp:166-198), bound through
+ctypes to the C ABI of ``include/sdgpu.h`` implemented by ``libsdgpu.so``
+(hand-written sm_100a CUDA, built in-tree by ``make -C paper_2108_10480_b200``).
+
+Names follow the reference: :class:`SmoothParams` (params.hpp:13-22),
+:class:`SmoothResult` fields (smooth.hpp:20-27), ``smooth_min_dist`` /
+``smooth_min_dist_flat`` as batched calls. There is no CPU fallback: when the
+library or a CUDA device is missing every compute call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+from dataclasses import dataclass, field
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsdgpu.so")
+
+SD_FP32, SD_FP64 = 0, 1
+SD_EXACT, SD_BVH = 0, 1
+SD_BVH_MEDIAN, SD_BVH_LBVH = 0, 1
+SD_POINT, SD_EDGE, SD_TRIANGLE = 0, 1, 2
+
+NODE_DTYPE = np.dtype(
+    [("lo", "<f8", 3), ("hi", "<f8", 3), ("left", "<i4"), ("right", "<i4"),
+     ("primitive", "<i4"), ("count", "<i4"), ("diameter", "<f8")], align=False)
+assert NODE_DTYPE.itemsize == 72
+
+# Every symbol include/sdgpu.h declares (tests check the library exports them).
+EXPORTED_SYMBOLS = (
+    "sd_last_error", "sd_abi_version", "sd_create", "sd_destroy", "sd_set_geometry", "sd_set_weights",
+    "sd_set_bvh", "sd_build_bvh", "sd_bvh_size", "sd_export_bvh", "sd_query_points", "sd_query_points_device",
+    "sd_finalize_device", "sd_last_launch_count",
+)
+
+
+class SdError(RuntimeError):
+    """A failed C-ABI call (the reference raises std::runtime_error via fail())."""
+
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"sdgpu error {code}: {msg}")
+        self.code = code
+
+
+class _Params(C.Structure):
+    _fields_ = [("alpha", C.c_double), ("alpha_u", C.c_double), ("beta", C.c_double), ("epsilon", C.c_double)]
+
+
+class _Outputs(C.Structure):
+    _fields_ = [("d_hat", C.c_void_p), ("grad", C.c_void_p), ("c", C.c_void_p), ("grad_c", C.c_void_p),
+                ("leaves", C.c_void_p), ("far_field", C.c_void_p), ("decision_hash", C.c_void_p)]
+
+
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    """Compile libsdgpu.so in-tree for sm_100a (nvcc cross-compiles without a GPU)."""
+    args = ["make", "-s", "-C", _HERE, "-j4"]
+    if force:
+        subprocess.run(["make", "-s", "-C", _HERE, "clean"], check=True)
+    subprocess.run(args, check=True)
+    return LIB_PATH
+
+
+def lib():
+    """Load libsdgpu.so; raises if it is missing (no fallback path exists)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run paper_2108_10480_b200.build() (make -C paper_2108_10480_b200)")
+        L = C.CDLL(LIB_PATH)
+        vp, i64, i32, f64 = C.c_void_p, C.c_int64, C.c_int32, C.c_double
+        P = C.POINTER
+        sig = {
+            "sd_last_error": (C.c_char_p, []),
+            "sd_abi_version": (C.c_int, []),
+            "sd_create": (C.c_int, [P(vp), C.c_int, C.c_int]),
+            "sd_destroy": (C.c_int, [vp]),
+            "sd_set_geometry": (C.c_int, [vp, vp, i64, vp, vp, i64]),
+            "sd_set_weights": (C.c_int, [vp, f64, f64, i32, vp, i32, vp, vp]),
+            "sd_set_bvh": (C.c_int, [vp, vp, i64]),
+            "sd_build_bvh": (C.c_int, [vp, C.c_int]),
+            "sd_bvh_size": (C.c_int, [vp, P(i64)]),
+            "sd_export_bvh": (C.c_int, [vp, vp, i64]),
+            "sd_query_points": (C.c_int, [vp, vp, i64, P(_Params), C.c_int, P(_Outputs)]),
+            "sd_query_points_device": (C.c_int, [vp, vp, i64, P(_Params), C.c_int, P(_Outputs), vp]),
+            "sd_finalize_device": (C.c_int, [vp, vp, vp, i64, P(_Params), vp, vp, vp]),
+            "sd_last_launch_count": (C.c_int, [vp, P(i64)]),
+        }
+        for name, (res, argt) in sig.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = argt
+        _lib = L
+    return _lib
+
+
+def _check(rc: int):
+    if rc != 0:
+        raise SdError(rc, lib().sd_last_error().decode())
+
+
+def _ptr(a):
+    return None if a is None else C.c_void_p(a.ctypes.data)
+
+
+@dataclass
+class SmoothParams:
+    """SmoothParams (params.hpp:13-22); defaults are the reference's."""
+    alpha: float = 100.0
+    alpha_u: float = 600.0
+    beta: float = 0.5
+    alpha_q: float = 100.0
+    epsilon: float = 1e-300
+
+    def attenuation(self) -> float:
+        return self.alpha / max(self.alpha, self.alpha_u)
+
+    def _c(self) -> _Params:
+        return _Params(self.alpha, self.alpha_u, self.beta, self.epsilon)
+
+
+@dataclass
+class SmoothResults:
+    """Batched SmoothResult (smooth.hpp:20-27): one row per query."""
+    d_hat: np.ndarray
+    grad: np.ndarray | None = None
+    c: np.ndarray | None = None
+    grad_c: np.ndarray | None = None
+    leaves: np.ndarray | None = None
+    far_field: np.ndarray | None = None
+    decision_hash: np.ndarray | None = None
+
+
+class Engine:
+    """One sd_ctx bound to one CUDA device (one process per GPU)."""
+
+    def __init__(self, device: int = 0, precision: int = SD_FP32):
+        h = C.c_void_p()
+        _check(lib().sd_create(C.byref(h), device, precision))
+        self.h = h
+        self.device = device
+        self.precision = precision
+        self.num_simplices = 0
+
+    def close(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.sd_destroy(self.h)
+            self.h = None
+
+    __del__ = close
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    # -- geometry / weights / tree (mesh.hpp, weights.hpp, bvh.hpp) --
+    def set_geometry(self, vertices, simplices, kinds):
+        v = np.ascontiguousarray(vertices, np.float64).reshape(-1, 3)
+        s = np.ascontiguousarray(simplices, np.int32).reshape(-1, 3)
+        k = np.ascontiguousarray(kinds, np.uint8).reshape(-1)
+        _check(lib().sd_set_geometry(self.h, _ptr(v), len(v), _ptr(s), _ptr(k), len(k)))
+        self.num_simplices = len(k)
+
+    def set_weights(self, A, sup_wtilde, edge_a, tri_stored, poly_index):
+        ea = np.ascontiguousarray(edge_a, np.float64).reshape(-1, 5)
+        ts = np.ascontiguousarray(tri_stored, np.float64).reshape(-1, 13)
+        pi = np.ascontiguousarray(poly_index, np.int32).reshape(-1)
+        _check(lib().sd_set_weights(self.h, float(A), float(sup_wtilde), len(ea), _ptr(ea), len(ts), _ptr(ts),
+                                    _ptr(pi)))
+
+    def set_weight_table(self, t):
+        """Accepts any object with A, sup_wtilde, edge_a, tri_stored, poly_index."""
+        self.set_weights(t.A, t.sup_wtilde, t.edge_a, t.tri_stored, t.poly_index)
+
+    def set_bvh(self, nodes: np.ndarray):
+        nodes = np.ascontiguousarray(nodes, dtype=NODE_DTYPE)
+        _check(lib().sd_set_bvh(self.h, _ptr(nodes), len(nodes)))
+
+    def build_bvh(self, method: int = SD_BVH_LBVH):
+        _check(lib().sd_build_bvh(self.h, method))
+
+    def export_bvh(self) -> np.ndarray:
+        n = C.c_int64()
+        _check(lib().sd_bvh_size(self.h, C.byref(n)))
+        out = np.zeros(n.value, NODE_DTYPE)
+        _check(lib().sd_export_bvh(self.h, _ptr(out), n.value))
+        return out
+
+    # -- queries (smooth.hpp:166-198) --
+    def query_points(self, q, params: SmoothParams, mode: int = SD_EXACT, *, want_grad=True, want_c=False,
+                     want_counters=False) -> SmoothResults:
+        """Host-buffer batched query: H2D, evaluate, D2H (blocking)."""
+        q = np.ascontiguousarray(q, np.float64).reshape(-1, 3)
+        n = len(q)
+        r = SmoothResults(np.empty(n))
+        if want_grad:
+            r.grad = np.empty((n, 3))
+        if want_c:
+            r.c, r.grad_c = np.empty(n), np.empty((n, 3))
+        if want_counters:
+            r.leaves, r.far_field = np.empty(n, np.int64), np.empty(n, np.int64)
+            r.decision_hash = np.empty(n, np.uint64)
+        o = _Outputs(*(None if a is None else a.ctypes.data for a in
+                       (r.d_hat, r.grad, r.c, r.grad_c, r.leaves, r.far_field, r.decision_hash)))
+        _check(lib().sd_query_points(self.h, _ptr(q), n, C.byref(params._c()), mode, C.byref(o)))
+        return r
+
+    def query_points_device(self, q_ptr: int, n: int, params: SmoothParams, mode: int, d_hat_ptr: int,
+                            grad_ptr: int | None = None, c_ptr: int | None = None, grad_c_ptr: int | None = None,
+                            leaves_ptr: int | None = None, far_ptr: int | None = None, hash_ptr: int | None = None,
+                            stream: int | None = None):
+        """Device-buffer batched query on `stream` (raw CUDA pointers, e.g.
+        torch ``tensor.data_ptr()``); q is float32 (SD_FP32) or float64."""
+        o = _Outputs(d_hat_ptr, grad_ptr, c_ptr, grad_c_ptr, leaves_ptr, far_ptr, hash_ptr)
+        _check(lib().sd_query_points_device(self.h, C.c_void_p(q_ptr), n, C.byref(params._c()), mode, C.byref(o),
+                                            C.c_void_p(stream) if stream else None))
+
+    def finalize_device(self, c_ptr: int, grad_c_ptr: int, n: int, params: SmoothParams, d_hat_ptr: int,
+                        grad_ptr: int | None, stream: int | None = None):
+        _check(lib().sd_finalize_device(self.h, C.c_void_p(c_ptr), C.c_void_p(grad_c_ptr), n, C.byref(params._c()),
+                                        C.c_void_p(d_hat_ptr), C.c_void_p(grad_ptr) if grad_ptr else None,
+                                        C.c_void_p(stream) if stream else None))
+
+    def last_launch_count(self) -> int:
+        n = C.c_int64()
+        _check(lib().sd_last_launch_count(self.h, C.byref(n)))
+        return n.value
+
+    def smooth_min_dist(self, q, params: SmoothParams) -> SmoothResults:
+        """Batched smooth_min_dist (smooth.hpp:166-184): tree path when beta > 0."""
+        mode = SD_BVH if params.beta > 0 else SD_EXACT
+        return self.query_points(q, params, mode, want_c=True, want_counters=True)
+
+    def smooth_min_dist_flat(self, q, params: SmoothParams) -> SmoothResults:
+        """Batched smooth_min_dist_flat (smooth.hpp:189-198)."""
+        return self.query_points(q, params, SD_EXACT, want_c=True, want_counters=True)

@@ -1,0 +1,139 @@
+"""Seeded synthetic workloads of BASELINE.json (numpy; no dataset needed).
+
+Shapes, sizes and value distributions follow BASELINE.json ``configs`` with
+the interpretations frozen in SURVEY.md 8(d); the paper's Thingi10K corpus
+is not available and these inputs stand in for it. The tests build the same
+configs with the CPU oracle's mt19937_64 generators; the bench uses these
+numpy generators so that its GPU leg never executes oracle code.
+
+Also: the host-side WeightSet pieces this path needs for meshes whose
+polynomials have closed forms -- valences (mesh.hpp:163-183), edge
+polynomials (weights.hpp:46-76), unit weights for points -- so that a
+WeightSet can be assembled without the reference toolchain.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+
+@dataclass
+class Workload:
+    name: str
+    vertices: np.ndarray   # (V, 3) float64
+    simplices: np.ndarray  # (N, 3) int32, -1 padded
+    kinds: np.ndarray      # (N,) uint8
+    alpha: float
+    alpha_u: float = 600.0
+    beta: float = 0.0
+    precision: int = 0     # 0 fp32, 1 fp64
+
+
+@dataclass
+class WeightTable:
+    A: float
+    sup_wtilde: float
+    edge_a: np.ndarray
+    tri_stored: np.ndarray
+    poly_index: np.ndarray
+
+
+def edge_poly(v0: int, v1: int):
+    """build_edge_weight (weights.hpp:46-76): coefficients and extrema."""
+    P, Q = 1.0 / v1 - 1.0 / v0, 1.0 - 1.0 / v0
+    a = [1.0 / v0, 0.0, -5 * P + 16 * Q, 14 * P - 32 * Q, 16 * Q - 8 * P]
+    val = lambda t: a[0] + t * (a[1] + t * (a[2] + t * (a[3] + t * a[4])))
+    sup, inf = max(val(0.0), val(1.0)), min(val(0.0), val(1.0))
+    qa, qb, qc = 4 * a[4], 3 * a[3], 2 * a[2]
+    cands = []
+    if abs(qa) > 1e-300:
+        disc = qb * qb - 4 * qa * qc
+        if disc >= 0:
+            rt = math.sqrt(disc)
+            cands = [(-qb + rt) / (2 * qa), (-qb - rt) / (2 * qa)]
+    elif abs(qb) > 1e-300:
+        cands = [-qc / qb]
+    for t in cands:
+        if 0.0 < t < 1.0:
+            sup, inf = max(sup, val(t)), min(inf, val(t))
+    return np.array(a), sup, inf
+
+
+def weights_without_triangles(simplices: np.ndarray, kinds: np.ndarray, nverts: int) -> WeightTable:
+    """build_weight_set (weights.hpp:589-621) for point/edge meshes: vertex
+    valence = incident non-point simplices; edge polynomial per (v0, v1)
+    valence pair in first-occurrence order; A = max valence."""
+    if (kinds == 2).any():
+        raise ValueError("triangle weight polynomials need the SVD/LP construction (weights.hpp:352-560)")
+    val = np.zeros(nverts, np.int64)
+    e = kinds == 1
+    np.add.at(val, simplices[e, 0], 1)
+    np.add.at(val, simplices[e, 1], 1)
+    poly_index = np.full(len(kinds), -1, np.int32)
+    A, sup = 1.0, 1.0
+    polys, cache = [], {}
+    idx = np.nonzero(e)[0]
+    pairs = np.stack([val[simplices[idx, 0]], val[simplices[idx, 1]]], 1)
+    uniq, first, inv = np.unique(pairs, axis=0, return_index=True, return_inverse=True)
+    order = np.argsort(first)  # first-occurrence order, as the reference's cache
+    rank = np.empty(len(order), np.int64)
+    rank[order] = np.arange(len(order))
+    for u in order:
+        a, s, _ = edge_poly(int(uniq[u, 0]), int(uniq[u, 1]))
+        polys.append(a)
+        sup = max(sup, s)
+        A = max(A, float(uniq[u].max()))
+    poly_index[idx] = rank[inv.reshape(-1)]
+    return WeightTable(A, sup, np.array(polys).reshape(-1, 5), np.zeros((0, 13)), poly_index)
+
+
+# ------------------------------------------------------------ workloads
+def cfg1(nq: int = 65536, seed: int = 1001):
+    rng = np.random.default_rng(seed)
+    p = rng.standard_normal((4096, 3))
+    p /= np.linalg.norm(p, axis=1, keepdims=True)
+    q = np.random.default_rng(seed + 1).uniform(-2, 2, (nq, 3))
+    w = Workload("cfg1 point cloud 4096 pts, exact LSE, fp64", p, np.stack(
+        [np.arange(4096), -np.ones(4096), -np.ones(4096)], 1).astype(np.int32), np.zeros(4096, np.uint8),
+        alpha=50.0, precision=1)
+    return w, q
+
+
+def cfg2(nq: int = 262144, seed: int = 2001, block: int = 0):
+    """Helix x = cos t, y = sin t, z = 0.05 t, t in [0, 40 pi], 20,001
+    vertices with N(0, 1e-3^2) jitter; queries uniform in the AABB scaled
+    x1.2 about its centre. `block` selects a disjoint query block of the
+    same distribution (per-rank blocks for weak scaling)."""
+    K = 20000
+    t = 40.0 * math.pi * np.arange(K + 1) / K
+    v = np.stack([np.cos(t), np.sin(t), 0.05 * t], 1)
+    v += np.random.default_rng(seed).normal(0.0, 1e-3, v.shape)
+    s = np.stack([np.arange(K), np.arange(1, K + 1), -np.ones(K, np.int64)], 1).astype(np.int32)
+    lo, hi = v.min(0), v.max(0)
+    c, h = 0.5 * (lo + hi), 0.6 * (hi - lo)
+    q = np.random.default_rng([seed + 1, block]).uniform(c - h, c + h, (nq, 3))
+    w = Workload("cfg2 helix polyline 20,000 edges, exact LSE", v, s, np.ones(K, np.uint8), alpha=100.0)
+    return w, q
+
+
+def torus(major=1.0, minor=0.3, nu=512, nv=256, seed=3001):
+    """uv_torus (shapes.hpp:67-89) + N(0, (0.1 mean edge)^2) jitter."""
+    i, j = np.meshgrid(np.arange(nu), np.arange(nv), indexing="ij")
+    u, vv = 2 * np.pi * i / nu, 2 * np.pi * j / nv
+    ring = major + minor * np.cos(vv)
+    V = np.stack([ring * np.cos(u), minor * np.sin(vv), ring * np.sin(u)], -1).reshape(-1, 3)
+    vid = lambda a, b: ((a % nu) * nv + (b % nv))
+    t1 = np.stack([vid(i, j), vid(i + 1, j), vid(i, j + 1)], -1).reshape(-1, 3)
+    t2 = np.stack([vid(i + 1, j), vid(i + 1, j + 1), vid(i, j + 1)], -1).reshape(-1, 3)
+    T = np.stack([t1, t2], 1).reshape(-1, 3).astype(np.int32)
+    e = np.concatenate([T[:, [0, 1]], T[:, [1, 2]], T[:, [2, 0]]])
+    e = np.unique(np.sort(e, 1), axis=0)
+    mel = np.linalg.norm(V[e[:, 0]] - V[e[:, 1]], axis=1).mean()
+    V = V + np.random.default_rng(seed).normal(0.0, 0.1 * mel, V.shape)
+    return V, T
+
+
+def quantize(x: np.ndarray) -> np.ndarray:
+    return np.asarray(x, np.float32).astype(np.float64)

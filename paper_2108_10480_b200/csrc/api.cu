@@ -1,0 +1,509 @@
+// api.cu -- the C ABI of include/sdgpu.h: context lifetime, geometry and
+// weight upload (AoS fp64 mesh -> per-kind SoA-ish records grouped into
+// (kind, polynomial) segments), and query dispatch to K1/K3/K4.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <stdexcept>
+
+#include "context.h"
+
+namespace sdgpu {
+
+static thread_local std::string g_err;
+void set_error(const std::string& m) { g_err = m; }
+
+void check_cuda(cudaError_t e, const char* where) {
+    if (e != cudaSuccess) throw CudaError{e, where};
+}
+
+struct ArgError {
+    std::string msg;
+};
+struct StateError {
+    std::string msg;
+};
+
+template <class F>
+static int guard(F&& f) {
+    try {
+        f();
+        return SD_OK;
+    } catch (const ArgError& e) {
+        set_error(e.msg);
+        return SD_E_ARG;
+    } catch (const StateError& e) {
+        set_error(e.msg);
+        return SD_E_STATE;
+    } catch (const CudaError& e) {
+        set_error(std::string("CUDA error in ") + e.where + ": " + cudaGetErrorString(e.code));
+        return SD_E_CUDA;
+    } catch (const std::bad_alloc&) {
+        set_error("out of host memory");
+        return SD_E_NOMEM;
+    } catch (const std::exception& e) {
+        set_error(e.what());
+        return SD_E_ARG;
+    }
+}
+
+struct DeviceScope {  // makes ctx->device current for the duration of a call
+    int prev = -1;
+    explicit DeviceScope(int dev) {
+        check_cuda(cudaGetDevice(&prev), "cudaGetDevice");
+        if (prev != dev) check_cuda(cudaSetDevice(dev), "cudaSetDevice");
+    }
+    ~DeviceScope() {
+        int cur;
+        if (cudaGetDevice(&cur) == cudaSuccess && prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+// ------------------------------------------------------------ host math
+struct D3 {
+    double x, y, z;
+};
+static inline D3 sub(D3 a, D3 b) { return {a.x - b.x, a.y - b.y, a.z - b.z}; }
+static inline double dot3(D3 a, D3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+static inline D3 cross3(D3 a, D3 b) { return {a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x}; }
+static inline D3 scale3(D3 a, double s) { return {a.x * s, a.y * s, a.z * s}; }
+
+static inline D3 vtx(const Ctx& c, int32_t i) { return {c.xyz[3 * size_t(i)], c.xyz[3 * size_t(i) + 1], c.xyz[3 * size_t(i) + 2]}; }
+
+template <class T>
+void build_record(const Ctx& c, int64_t prim, T* out) {
+    const int k = c.kind[prim];
+    const int32_t* s = &c.sv[3 * size_t(prim)];
+    const D3 a = vtx(c, s[0]);
+    for (int i = 0; i < rec_size(k); ++i) out[i] = T(0);
+    out[0] = T(a.x);
+    out[1] = T(a.y);
+    out[2] = T(a.z);
+    if (k == SD_EDGE) {
+        const D3 e = sub(vtx(c, s[1]), a);
+        const double e2 = dot3(e, e);
+        const double inv = e2 > 0 ? 1.0 / e2 : 0.0;  // exact.hpp:71: t = 0 if |e|^2 <= 0
+        out[3] = T(e.x); out[4] = T(e.y); out[5] = T(e.z);
+        out[6] = T(inv);
+        out[7] = T(e.x * inv); out[8] = T(e.y * inv); out[9] = T(e.z * inv);
+    } else if (k == SD_TRIANGLE) {
+        const D3 b = vtx(c, s[1]), cc = vtx(c, s[2]);
+        const D3 ab = sub(b, a), ac = sub(cc, a), bc = sub(cc, b);
+        const double A = dot3(ab, ab), B = dot3(ab, ac), C = dot3(ac, ac), BC = dot3(bc, bc);
+        const double det = A * C - B * B;
+        out[3] = T(ab.x); out[4] = T(ab.y); out[5] = T(ab.z);
+        out[6] = T(ac.x); out[7] = T(ac.y); out[8] = T(ac.z);
+        out[9] = T(A); out[10] = T(B); out[11] = T(C);
+        out[12] = T(1.0 / A); out[13] = T(1.0 / C); out[14] = T(1.0 / BC); out[15] = T(1.0 / det);
+        // barycentric shape gradients without the 1/alpha (weights.hpp:689-696)
+        const D3 n = cross3(ab, ac);
+        const double nn = dot3(n, n);
+        const double inv = nn > 0 ? 1.0 / nn : 0.0;
+        const D3 g1 = scale3(cross3(n, sub(a, cc)), inv), g2 = scale3(cross3(n, ab), inv);
+        out[16] = T(g1.x); out[17] = T(g1.y); out[18] = T(g1.z);
+        out[19] = T(g2.x); out[20] = T(g2.y); out[21] = T(g2.z);
+    }
+}
+template void build_record<float>(const Ctx&, int64_t, float*);
+template void build_record<double>(const Ctx&, int64_t, double*);
+
+template <class T>
+Phys<T> make_phys(const Ctx& c, const sd_params& p) {
+    const double S = p.alpha / std::max(p.alpha, p.alpha_u);  // params.hpp:21
+    Phys<T> ph;
+    ph.kappa = T(-p.alpha * 1.4426950408889634);
+    ph.dmax = T(708.0 / p.alpha);
+    ph.S = T(S);
+    ph.A = T(c.A);
+    ph.lw_unit = T(S * std::log2(std::max(c.A, 1e-300)));
+    ph.lw_floor = T(S * std::log2(1e-300));
+    ph.kgrad = T(S * c.A / (p.alpha * p.alpha));
+    ph.w_ff = T(std::pow(std::max(c.A * c.sup_wtilde, 1e-300), S));  // weights.hpp:576-578
+    ph.beta = T(p.beta);
+    return ph;
+}
+template Phys<float> make_phys<float>(const Ctx&, const sd_params&);
+template Phys<double> make_phys<double>(const Ctx&, const sd_params&);
+
+// coefficient packing documented in pair.cuh (Poly)
+template <class T>
+Poly<T> make_poly(const Ctx& c, int kind, int poly) {
+    Poly<T> out;
+    for (int i = 0; i < kPolyCoefs; ++i) out.c[i] = T(0);
+    if (poly < 0) return out;
+    if (kind == SD_EDGE) {
+        const double* a = &c.edge_a[5 * size_t(poly)];
+        for (int i = 0; i < 5; ++i) out.c[i] = T(a[i]);
+        out.c[5] = T(a[1]);
+        out.c[6] = T(2 * a[2]);
+        out.c[7] = T(3 * a[3]);
+        out.c[8] = T(4 * a[4]);
+        return out;
+    }
+    // expand the 13 stored slots to the symmetric grid (weights.hpp:155-161)
+    static const int kStored[13][2] = {{0, 0}, {0, 2}, {0, 3}, {0, 4}, {0, 5}, {0, 6}, {0, 7},
+                                       {2, 2}, {2, 3}, {2, 4}, {2, 5}, {3, 3}, {3, 4}};
+    double g[8][8] = {};
+    const double* st = &c.tri_stored[13 * size_t(poly)];
+    for (int m = 0; m < 13; ++m) {
+        g[kStored[m][0]][kStored[m][1]] = st[m];
+        g[kStored[m][1]][kStored[m][0]] = st[m];
+    }
+    int n = 0;
+    const int rows[7] = {0, 2, 3, 4, 5, 6, 7};
+    for (int j : rows)  // value rows
+        for (int k = 0; j + k <= 7; ++k)
+            if (k != 1) out.c[n++] = T(g[j][k]);
+    for (int j : rows)  // d/dx rows, j >= 2
+        if (j >= 2)
+            for (int k = 0; j + k <= 7; ++k)
+                if (k != 1) out.c[n++] = T(j * g[j][k]);
+    for (int j : rows)  // d/dy rows, k >= 2
+        for (int k = 2; j + k <= 7; ++k) out.c[n++] = T(k * g[j][k]);
+    if (n != kPolyCoefs) throw std::logic_error("triangle polynomial packing");
+    return out;
+}
+template Poly<float> make_poly<float>(const Ctx&, int, int);
+template Poly<double> make_poly<double>(const Ctx&, int, int);
+
+// --------------------------------------------------------- exact layout
+template <class T>
+static void prepare_exact(Ctx& c) {
+    if (c.exact_ready) return;
+    c.segs.clear();
+    for (int k = 0; k < 3; ++k) {
+        std::vector<int64_t> ids;
+        for (int64_t i = 0; i < c.N; ++i)
+            if (c.kind[i] == k) ids.push_back(i);
+        std::stable_sort(ids.begin(), ids.end(),
+                         [&](int64_t a, int64_t b) { return c.poly_index[a] < c.poly_index[b]; });
+        const int R = rec_size(k);
+        std::vector<T> host(ids.size() * size_t(R));
+        for (size_t j = 0; j < ids.size(); ++j) build_record<T>(c, ids[j], &host[j * R]);
+        T* d = static_cast<T*>(c.rec[k].ensure(host.size() * sizeof(T)));
+        if (!host.empty()) check_cuda(cudaMemcpy(d, host.data(), host.size() * sizeof(T), cudaMemcpyHostToDevice), "upload records");
+        size_t j = 0;
+        while (j < ids.size()) {
+            const int poly = k == SD_POINT ? -1 : c.poly_index[ids[j]];
+            size_t e = j;
+            while (e < ids.size() && (k == SD_POINT ? -1 : c.poly_index[ids[e]]) == poly) ++e;
+            c.segs.push_back({k, poly, int64_t(j), int64_t(e - j)});
+            j = e;
+        }
+    }
+    c.exact_ready = true;
+}
+
+template <class T>
+__global__ void convert_queries(const double* __restrict__ in, T* __restrict__ out, int64_t n) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = T(in[i]);
+}
+
+template <class T>
+static void exact_query(Ctx& c, const T* q, int64_t Q, const sd_params& p, const FinalizeOut& out,
+                        cudaStream_t st) {
+    prepare_exact<T>(c);
+    if (c.segs.empty()) {
+        check_cuda(launch_empty_result(Q, out, st), "empty result");
+        c.last_launches = 1;
+        return;
+    }
+    // splits: enough CTAs for several waves over 148 SMs even for small Q
+    const int64_t qpc = exact_queries_per_cta(0);
+    const int64_t qblocks = (Q + qpc - 1) / qpc;
+    int64_t maxcount = 0;
+    for (const Segment& s : c.segs) maxcount = std::max(maxcount, s.count);
+    const int64_t target = 148 * 8;
+    int64_t splits = std::max<int64_t>(1, (target + qblocks - 1) / qblocks);
+    splits = std::min<int64_t>(splits, std::max<int64_t>(1, maxcount / 512));
+    splits = std::min<int64_t>(splits, 64);
+    T* part = static_cast<T*>(c.part.ensure(size_t(splits) * 5 * Q * sizeof(T)));
+    const Phys<T> ph = make_phys<T>(c, p);
+    int64_t launches = 0;
+    bool first = true;
+    for (const Segment& s : c.segs) {
+        ExactLaunch<T> L;
+        L.kind = s.kind;
+        L.has_poly = s.poly >= 0;
+        L.rec = c.rec[s.kind].as<T>() + s.offset * rec_size(s.kind);
+        L.count = s.count;
+        L.splits = int(splits);
+        L.chunk = (s.count + splits - 1) / splits;
+        L.q = q;
+        L.Q = Q;
+        L.part = part;
+        L.first = first ? 1 : 0;
+        L.ph = ph;
+        L.poly = make_poly<T>(c, s.kind, s.poly);
+        check_cuda(launch_exact<T>(L, st), "exact kernel launch");
+        ++launches;
+        first = false;
+    }
+    check_cuda(launch_finalize<T>(part, int(splits), Q, p.alpha, p.epsilon, c.N, nullptr, nullptr, nullptr, nullptr,
+                                  out, st),
+               "finalize launch");
+    c.last_launches = launches + 1;
+}
+
+static void check_params(const sd_params* p) {
+    if (!p) throw ArgError{"params is NULL"};
+    if (!(p->alpha > 0) || !std::isfinite(p->alpha)) throw ArgError{"alpha must be positive and finite"};
+    if (!(p->alpha_u > 0)) throw ArgError{"alpha_u must be positive"};
+    if (!(p->beta >= 0) || !std::isfinite(p->beta)) throw ArgError{"beta must be >= 0"};
+    if (!(p->epsilon >= 0)) throw ArgError{"epsilon must be >= 0"};
+}
+
+static void check_ready(const Ctx& c, int mode) {
+    if (!c.have_geom) throw StateError{"no geometry: call sd_set_geometry first"};
+    if (!c.have_weights) throw StateError{"no weight table: call sd_set_weights first"};
+    if (mode == SD_BVH && !c.have_tree && c.N > 0) throw StateError{"no tree: call sd_set_bvh or sd_build_bvh first"};
+    if (mode != SD_EXACT && mode != SD_BVH) throw ArgError{"mode must be SD_EXACT or SD_BVH"};
+}
+
+template <class T>
+static void dispatch(Ctx& c, const T* q, int64_t Q, const sd_params& p, int mode, const FinalizeOut& out,
+                     cudaStream_t st) {
+    if (Q == 0) {
+        c.last_launches = 0;
+        return;
+    }
+    if (mode == SD_BVH && c.N > 0) tree_query<T>(c, q, Q, p, out, st);
+    else exact_query<T>(c, q, Q, p, out, st);
+}
+
+}  // namespace sdgpu
+
+using namespace sdgpu;
+
+extern "C" {
+
+const char* sd_last_error(void) { return g_err.c_str(); }
+int sd_abi_version(void) { return SDGPU_ABI_VERSION; }
+
+int sd_create(sd_ctx** out, int device, int precision) {
+    return guard([&] {
+        if (!out) throw ArgError{"out is NULL"};
+        if (precision != SD_FP32 && precision != SD_FP64) throw ArgError{"precision must be SD_FP32 or SD_FP64"};
+        int n = 0;
+        check_cuda(cudaGetDeviceCount(&n), "cudaGetDeviceCount");
+        if (device < 0 || device >= n) throw ArgError{"device index out of range"};
+        auto* c = new sd_ctx;
+        c->device = device;
+        c->precision = precision;
+        {
+            DeviceScope ds(device);
+            cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+            if (e != cudaSuccess) {
+                delete c;
+                check_cuda(e, "cudaStreamCreate");
+            }
+        }
+        *out = c;
+    });
+}
+
+int sd_destroy(sd_ctx* c) {
+    return guard([&] {
+        if (!c) return;
+        {
+            DeviceScope ds(c->device);
+            if (c->stream) cudaStreamDestroy(c->stream);
+            c->stream = nullptr;
+        }
+        delete c;
+    });
+}
+
+// mesh.hpp:55-87 validation, then the fp32 rounding of SURVEY 7.
+int sd_set_geometry(sd_ctx* c, const double* xyz, int64_t V, const int32_t* sv, const uint8_t* kinds, int64_t N) {
+    return guard([&] {
+        if (!c) throw ArgError{"ctx is NULL"};
+        if (V < 0 || N < 0 || (V > 0 && !xyz) || (N > 0 && (!sv || !kinds))) throw ArgError{"bad geometry arrays"};
+        if (V > INT32_MAX) throw ArgError{"too many vertices for int32 indices"};
+        std::vector<double> x(xyz, xyz + 3 * V);
+        if (c->precision == SD_FP32)
+            for (double& v : x) v = double(float(v));
+        for (double v : x)
+            if (!std::isfinite(v)) throw ArgError{"non-finite vertex coordinate"};
+        for (int64_t i = 0; i < N; ++i) {
+            if (kinds[i] > SD_TRIANGLE) throw ArgError{"simplex " + std::to_string(i) + ": bad kind"};
+            const int nv = kinds[i] + 1;
+            for (int a = 0; a < nv; ++a)
+                if (sv[3 * i + a] < 0 || sv[3 * i + a] >= V)
+                    throw ArgError{"simplex " + std::to_string(i) + ": vertex index " + std::to_string(sv[3 * i + a]) +
+                                   " out of range [0, " + std::to_string(V) + ")"};
+            for (int a = 0; a < nv; ++a)
+                for (int b = a + 1; b < nv; ++b) {
+                    const int32_t ia = sv[3 * i + a], ib = sv[3 * i + b];
+                    if (ia == ib || (x[3 * ia] == x[3 * ib] && x[3 * ia + 1] == x[3 * ib + 1] &&
+                                     x[3 * ia + 2] == x[3 * ib + 2]))
+                        throw ArgError{"degenerate simplex " + std::to_string(i)};
+                }
+            if (kinds[i] == SD_TRIANGLE) {
+                const D3 a = {x[3 * sv[3 * i]], x[3 * sv[3 * i] + 1], x[3 * sv[3 * i] + 2]};
+                const D3 b = {x[3 * sv[3 * i + 1]], x[3 * sv[3 * i + 1] + 1], x[3 * sv[3 * i + 1] + 2]};
+                const D3 cc = {x[3 * sv[3 * i + 2]], x[3 * sv[3 * i + 2] + 1], x[3 * sv[3 * i + 2] + 2]};
+                const D3 n = cross3(sub(b, a), sub(cc, a));
+                if (std::sqrt(dot3(n, n)) == 0.0) throw ArgError{"degenerate simplex " + std::to_string(i) + " (zero area)"};
+            }
+        }
+        c->xyz.swap(x);
+        c->sv.assign(sv, sv + 3 * N);
+        c->kind.assign(kinds, kinds + N);
+        c->V = V;
+        c->N = N;
+        c->have_geom = true;
+        c->have_weights = false;
+        c->exact_ready = false;
+        c->have_tree = false;
+        c->dtree_ready = false;
+        c->tree.clear();
+    });
+}
+
+int sd_set_weights(sd_ctx* c, double A, double sup, int32_t ne, const double* edge_a, int32_t nt,
+                   const double* tri_stored, const int32_t* poly_index) {
+    return guard([&] {
+        if (!c) throw ArgError{"ctx is NULL"};
+        if (!c->have_geom) throw StateError{"set the geometry before the weights"};
+        if (ne < 0 || nt < 0 || (ne > 0 && !edge_a) || (nt > 0 && !tri_stored) || (c->N > 0 && !poly_index))
+            throw ArgError{"bad weight arrays"};
+        if (!(A >= 1.0) || !std::isfinite(sup)) throw ArgError{"WeightSet::A must be >= 1 and sup finite"};
+        for (int64_t i = 0; i < c->N; ++i) {
+            const int32_t pi = poly_index[i];
+            const int k = c->kind[i];
+            if (pi < -1 || (k == SD_EDGE && pi >= ne) || (k == SD_TRIANGLE && pi >= nt))
+                throw ArgError{"poly_index[" + std::to_string(i) + "] out of range"};
+        }
+        c->A = A;
+        c->sup_wtilde = sup;
+        c->edge_a.assign(edge_a, edge_a + 5 * size_t(ne));
+        c->tri_stored.assign(tri_stored, tri_stored + 13 * size_t(nt));
+        c->poly_index.assign(poly_index, poly_index + c->N);
+        c->have_weights = true;
+        c->exact_ready = false;
+        c->dtree_ready = false;
+    });
+}
+
+int sd_set_bvh(sd_ctx* c, const sd_bvh_node* nodes, int64_t n) {
+    return guard([&] {
+        if (!c) throw ArgError{"ctx is NULL"};
+        if (!c->have_geom) throw StateError{"set the geometry before the tree"};
+        if (n != (c->N > 0 ? 2 * c->N - 1 : 0) || (n > 0 && !nodes))
+            throw ArgError{"tree must have 2N - 1 nodes (one primitive per leaf)"};
+        c->tree.assign(nodes, nodes + n);
+        c->have_tree = true;
+        c->dtree_ready = false;
+    });
+}
+
+int sd_build_bvh(sd_ctx* c, int method) {
+    return guard([&] {
+        if (!c) throw ArgError{"ctx is NULL"};
+        if (!c->have_geom) throw StateError{"set the geometry before building a tree"};
+        DeviceScope ds(c->device);
+        if (method == SD_BVH_MEDIAN) tree_build_median(*c);
+        else if (method == SD_BVH_LBVH) tree_build_lbvh(*c);
+        else throw ArgError{"unknown tree builder"};
+        c->have_tree = true;
+    });
+}
+
+int sd_bvh_size(sd_ctx* c, int64_t* n) {
+    return guard([&] {
+        if (!c || !n) throw ArgError{"NULL argument"};
+        *n = int64_t(c->tree.size());
+    });
+}
+
+int sd_export_bvh(sd_ctx* c, sd_bvh_node* out, int64_t cap) {
+    return guard([&] {
+        if (!c) throw ArgError{"ctx is NULL"};
+        if (!c->have_tree) throw StateError{"no tree"};
+        if (cap < int64_t(c->tree.size()) || (!out && !c->tree.empty())) throw ArgError{"output too small"};
+        std::memcpy(out, c->tree.data(), c->tree.size() * sizeof(sd_bvh_node));
+    });
+}
+
+int sd_query_points_device(sd_ctx* c, const void* q, int64_t Q, const sd_params* p, int mode, const sd_outputs* o,
+                           void* stream) {
+    return guard([&] {
+        if (!c) throw ArgError{"ctx is NULL"};
+        check_params(p);
+        check_ready(*c, mode);
+        if (Q < 0 || (Q > 0 && (!q || !o || !o->d_hat))) throw ArgError{"bad query / output pointers"};
+        DeviceScope ds(c->device);
+        FinalizeOut out{o->d_hat, o->grad, o->c, o->grad_c, o->leaves, o->far_field, o->decision_hash};
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        if (c->precision == SD_FP32) dispatch<float>(*c, static_cast<const float*>(q), Q, *p, mode, out, st);
+        else dispatch<double>(*c, static_cast<const double*>(q), Q, *p, mode, out, st);
+    });
+}
+
+int sd_query_points(sd_ctx* c, const double* q, int64_t Q, const sd_params* p, int mode, const sd_outputs* o) {
+    return guard([&] {
+        if (!c) throw ArgError{"ctx is NULL"};
+        check_params(p);
+        check_ready(*c, mode);
+        if (Q < 0 || (Q > 0 && (!q || !o || !o->d_hat))) throw ArgError{"bad query / output pointers"};
+        if (Q == 0) return;
+        DeviceScope ds(c->device);
+        cudaStream_t st = c->stream;
+        double* qd = c->qd.ensure(size_t(Q) * 3 * sizeof(double)) ? c->qd.as<double>() : nullptr;
+        check_cuda(cudaMemcpyAsync(qd, q, size_t(Q) * 3 * sizeof(double), cudaMemcpyHostToDevice, st), "H2D queries");
+        FinalizeOut out;
+        out.d_hat = static_cast<double*>(c->out_d.ensure(size_t(Q) * sizeof(double)));
+        if (o->grad) out.grad = static_cast<double*>(c->out_g.ensure(size_t(Q) * 3 * sizeof(double)));
+        if (o->c) out.c = static_cast<double*>(c->out_c.ensure(size_t(Q) * sizeof(double)));
+        if (o->grad_c) out.grad_c = static_cast<double*>(c->out_gc.ensure(size_t(Q) * 3 * sizeof(double)));
+        if (o->leaves) out.leaves = static_cast<int64_t*>(c->out_l.ensure(size_t(Q) * sizeof(int64_t)));
+        if (o->far_field) out.far_field = static_cast<int64_t*>(c->out_f.ensure(size_t(Q) * sizeof(int64_t)));
+        if (o->decision_hash) out.hash = static_cast<uint64_t*>(c->out_h.ensure(size_t(Q) * sizeof(uint64_t)));
+        int64_t conv = 0;
+        if (c->precision == SD_FP32) {
+            float* qf = static_cast<float*>(c->qT.ensure(size_t(Q) * 3 * sizeof(float)));
+            convert_queries<float><<<unsigned((3 * Q + 255) / 256), 256, 0, st>>>(qd, qf, 3 * Q);
+            check_cuda(cudaGetLastError(), "convert queries");
+            conv = 1;
+            dispatch<float>(*c, qf, Q, *p, mode, out, st);
+        } else {
+            dispatch<double>(*c, qd, Q, *p, mode, out, st);
+        }
+        c->last_launches += conv;
+        auto d2h = [&](void* dst, const void* src, size_t bytes) {
+            if (dst) check_cuda(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st), "D2H results");
+        };
+        d2h(o->d_hat, out.d_hat, size_t(Q) * sizeof(double));
+        d2h(o->grad, out.grad, size_t(Q) * 3 * sizeof(double));
+        d2h(o->c, out.c, size_t(Q) * sizeof(double));
+        d2h(o->grad_c, out.grad_c, size_t(Q) * 3 * sizeof(double));
+        d2h(o->leaves, out.leaves, size_t(Q) * sizeof(int64_t));
+        d2h(o->far_field, out.far_field, size_t(Q) * sizeof(int64_t));
+        d2h(o->decision_hash, out.hash, size_t(Q) * sizeof(uint64_t));
+        check_cuda(cudaStreamSynchronize(st), "query");
+    });
+}
+
+int sd_finalize_device(sd_ctx* c, const double* cs, const double* gc, int64_t Q, const sd_params* p, double* d_hat,
+                       double* grad, void* stream) {
+    return guard([&] {
+        if (!c) throw ArgError{"ctx is NULL"};
+        check_params(p);
+        if (Q < 0 || (Q > 0 && (!cs || !gc || !d_hat))) throw ArgError{"bad pointers"};
+        DeviceScope ds(c->device);
+        check_cuda(launch_finalize_sums(cs, gc, Q, p->alpha, p->epsilon, d_hat, grad, static_cast<cudaStream_t>(stream)),
+                   "finalize");
+        c->last_launches = Q > 0 ? 1 : 0;
+    });
+}
+
+int sd_last_launch_count(sd_ctx* c, int64_t* n) {
+    return guard([&] {
+        if (!c || !n) throw ArgError{"NULL argument"};
+        *n = c->last_launches;
+    });
+}
+
+}  // extern "C"

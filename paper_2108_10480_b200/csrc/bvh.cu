@@ -1,0 +1,485 @@
+// bvh.cu -- Barnes-Hut tree path: tree construction (reference median
+// split on the host; LBVH on the GPU lives in lbvh.cu), upload into the
+// traversal layout, query Morton sort, and K3, the stack traversal that
+// replaces collect_contributions (smooth.hpp:101-131) for a query batch.
+//
+// Decision semantics (checked invariant): at every popped node, leaves
+// included, when beta > 0: admissible iff d_B > 0 and diameter < beta d_B
+// (bvh.hpp:185-187) with d_B the point-box distance (bvh.hpp:105-111).
+// The fp32 path decides in fp32 when |diameter - beta d_B| is clearly
+// outside a 1e-5 relative band and otherwise re-decides in fp64 with the
+// reference's operation order (no FMA contraction), which is bit-identical
+// to the oracle compiled with -ffp-contract=off. The fp64 path always
+// decides that way.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+
+#include <cub/cub.cuh>
+
+#include "context.h"
+
+namespace sdgpu {
+
+// ------------------------------------------------------------ host tree
+// Restates build_bvh (bvh.hpp:34-91): leaf box = corner bbox, centroid =
+// bbox centre, split axis = longest extent (ties -> x, then y), median by
+// (centroid[axis], index); one primitive per leaf; pre-order ids.
+static void median_build_host(const Ctx& c, std::vector<sd_bvh_node>& out) {
+    const int64_t n = c.N;
+    out.clear();
+    if (n == 0) return;
+    std::vector<double> lo(3 * n), hi(3 * n), ce(3 * n);
+    for (int64_t i = 0; i < n; ++i) {
+        for (int a = 0; a < 3; ++a) {
+            lo[3 * i + a] = INFINITY;
+            hi[3 * i + a] = -INFINITY;
+        }
+        for (int k = 0; k <= c.kind[i]; ++k) {
+            const int32_t v = c.sv[3 * i + k];
+            for (int a = 0; a < 3; ++a) {
+                lo[3 * i + a] = std::min(lo[3 * i + a], c.xyz[3 * size_t(v) + a]);
+                hi[3 * i + a] = std::max(hi[3 * i + a], c.xyz[3 * size_t(v) + a]);
+            }
+        }
+        for (int a = 0; a < 3; ++a) ce[3 * i + a] = 0.5 * (lo[3 * i + a] + hi[3 * i + a]);
+    }
+    std::vector<int32_t> order(n);
+    std::iota(order.begin(), order.end(), 0);
+    out.resize(size_t(2 * n - 1));
+    auto diag = [](const double* l, const double* h) {
+        if (!(l[0] <= h[0] && l[1] <= h[1] && l[2] <= h[2])) return 0.0;
+        const double dx = h[0] - l[0], dy = h[1] - l[1], dz = h[2] - l[2];
+        return std::sqrt(dx * dx + dy * dy + dz * dz);
+    };
+    int32_t next = 0;
+    // explicit-stack version of the reference recursion (same id order)
+    struct Job {
+        int64_t first, last;
+        int32_t id;
+        int stage;
+    };
+    std::vector<Job> stack;
+    stack.push_back({0, n, next++, 0});
+    while (!stack.empty()) {
+        Job& j = stack.back();
+        sd_bvh_node& node = out[j.id];
+        if (j.last - j.first == 1) {
+            const int32_t p = order[j.first];
+            node.left = node.right = -1;
+            node.primitive = p;
+            node.count = 1;
+            for (int a = 0; a < 3; ++a) {
+                node.lo[a] = lo[3 * p + a];
+                node.hi[a] = hi[3 * p + a];
+            }
+            node.diameter = diag(node.lo, node.hi);
+            stack.pop_back();
+            continue;
+        }
+        const int64_t mid = j.first + (j.last - j.first) / 2;
+        if (j.stage == 0) {
+            double bl[3] = {INFINITY, INFINITY, INFINITY}, bh[3] = {-INFINITY, -INFINITY, -INFINITY};
+            for (int64_t i = j.first; i < j.last; ++i)
+                for (int a = 0; a < 3; ++a) {
+                    bl[a] = std::min(bl[a], lo[3 * size_t(order[i]) + a]);
+                    bh[a] = std::max(bh[a], hi[3 * size_t(order[i]) + a]);
+                }
+            int axis = 0;
+            if (bh[1] - bl[1] > bh[0] - bl[0]) axis = 1;
+            if (bh[2] - bl[2] > bh[axis] - bl[axis]) axis = 2;
+            std::nth_element(order.begin() + j.first, order.begin() + mid, order.begin() + j.last,
+                             [&](int32_t x, int32_t y) {
+                                 const double cx = ce[3 * size_t(x) + axis], cy = ce[3 * size_t(y) + axis];
+                                 return cx != cy ? cx < cy : x < y;
+                             });
+            j.stage = 1;
+            node.left = next++;
+            stack.push_back({j.first, mid, node.left, 0});
+        } else if (j.stage == 1) {
+            j.stage = 2;
+            node.right = next++;
+            stack.push_back({mid, j.last, node.right, 0});
+        } else {
+            const sd_bvh_node& l = out[node.left];
+            const sd_bvh_node& r = out[node.right];
+            node.primitive = -1;
+            node.count = l.count + r.count;
+            for (int a = 0; a < 3; ++a) {
+                node.lo[a] = std::min(l.lo[a], r.lo[a]);
+                node.hi[a] = std::max(l.hi[a], r.hi[a]);
+            }
+            node.diameter = diag(node.lo, node.hi);
+            stack.pop_back();
+        }
+    }
+}
+
+void tree_build_median(Ctx& c) {
+    median_build_host(c, c.tree);
+    c.dtree_ready = false;
+}
+
+// ---------------------------------------------------------------- upload
+template <class T>
+struct NodeT {  // 2 x (4 T): (lo, diam) (hi, link)
+    T v[8];
+};
+
+template <class T>
+static void upload_tree_T(Ctx& c) {
+    const int64_t n = int64_t(c.tree.size());
+    const int64_t N = c.N;
+    if (n != 2 * N - 1) throw std::runtime_error("tree must have 2N - 1 nodes");
+    // validate and compute the pre-order numbering of the given tree
+    std::vector<int32_t> pre(n, -1), stack;
+    std::vector<int32_t> order;
+    order.reserve(n);
+    stack.push_back(0);
+    std::vector<char> seen_prim(N, 0);
+    int depth = 0;
+    std::vector<int> dep(n, 0);
+    while (!stack.empty()) {
+        const int32_t id = stack.back();
+        stack.pop_back();
+        if (id < 0 || id >= n || pre[id] >= 0) throw std::runtime_error("tree: bad or repeated child index");
+        pre[id] = int32_t(order.size());
+        order.push_back(id);
+        const sd_bvh_node& nd = c.tree[id];
+        depth = std::max(depth, dep[id]);
+        if (nd.left < 0) {
+            if (nd.primitive < 0 || nd.primitive >= N || seen_prim[nd.primitive])
+                throw std::runtime_error("tree: bad or repeated leaf primitive");
+            seen_prim[nd.primitive] = 1;
+        } else {
+            if (nd.right < 0 || nd.right >= n || nd.left >= n) throw std::runtime_error("tree: bad child index");
+            dep[nd.left] = dep[nd.right] = dep[id] + 1;
+            stack.push_back(nd.right);
+            stack.push_back(nd.left);
+        }
+    }
+    if (int64_t(order.size()) != n) throw std::runtime_error("tree: unreachable nodes");
+    bool identity = true;
+    for (int64_t i = 0; i < n && identity; ++i) identity = pre[i] == i;
+    if (!identity) throw std::runtime_error("tree must be in pre-order layout (left child = parent + 1, root 0)");
+
+    std::vector<NodeT<T>> box(n);
+    std::vector<int32_t> count(n);
+    std::vector<double> d64(n);
+    std::vector<T> leafrec;
+    std::vector<int32_t> leafmeta;
+    leafrec.reserve(size_t(N) * kRecTri);
+    int64_t slot = 0;
+    bool exact_boxes = true;
+    for (int64_t id = 0; id < n; ++id) {
+        const sd_bvh_node& nd = c.tree[id];
+        NodeT<T>& b = box[id];
+        for (int a = 0; a < 3; ++a) {
+            // outward rounding keeps the fp32 box a superset (exact when the
+            // geometry was quantized to float, as SD_FP32 does)
+            T l = T(nd.lo[a]), h = T(nd.hi[a]);
+            if (double(l) > nd.lo[a]) l = std::nextafter(l, T(-INFINITY));
+            if (double(h) < nd.hi[a]) h = std::nextafter(h, T(INFINITY));
+            exact_boxes = exact_boxes && double(l) == nd.lo[a] && double(h) == nd.hi[a];
+            b.v[a] = l;
+            b.v[4 + a] = h;
+        }
+        b.v[3] = T(nd.diameter);
+        int32_t link;
+        if (nd.left < 0) {
+            link = int32_t(-(slot + 1));
+            const int32_t p = nd.primitive;
+            T rec[kRecTri];
+            build_record<T>(c, p, rec);
+            leafrec.insert(leafrec.end(), rec, rec + kRecTri);
+            const int k = c.kind[p];
+            const int poly = k == SD_POINT ? -1 : c.poly_index[p];
+            leafmeta.push_back(k | ((poly + 1) << 2));
+            ++slot;
+        } else {
+            if (nd.left != id + 1) throw std::runtime_error("tree: left child must follow its parent");
+            link = nd.right;
+        }
+        std::memcpy(&b.v[7], &link, sizeof(int32_t));
+        if (sizeof(T) == 8) std::memset(reinterpret_cast<char*>(&b.v[7]) + 4, 0, 4);
+        count[id] = nd.count;
+        d64[id] = nd.diameter;
+    }
+    DeviceTree& t = c.dtree;
+    t.nodes = n;
+    t.leaves = slot;
+    t.depth = depth;
+    t.exact_boxes = exact_boxes;
+    auto up = [](DevBuf& buf, const void* src, size_t bytes) {
+        void* d = buf.ensure(bytes);
+        if (bytes) check_cuda(cudaMemcpy(d, src, bytes, cudaMemcpyHostToDevice), "upload tree");
+    };
+    up(t.box, box.data(), box.size() * sizeof(NodeT<T>));
+    up(t.count, count.data(), count.size() * sizeof(int32_t));
+    up(t.diam64, d64.data(), d64.size() * sizeof(double));
+    up(t.leafrec, leafrec.data(), leafrec.size() * sizeof(T));
+    up(t.leafmeta, leafmeta.data(), leafmeta.size() * sizeof(int32_t));
+    c.dtree_ready = true;
+}
+
+void tree_upload(Ctx& c) {
+    if (c.precision == SD_FP32) upload_tree_T<float>(c);
+    else upload_tree_T<double>(c);
+}
+
+// ---------------------------------------------------------- query order
+__device__ __forceinline__ uint32_t spread10(uint32_t v) {
+    v &= 0x3ffu;
+    v = (v | (v << 16)) & 0x030000FFu;
+    v = (v | (v << 8)) & 0x0300F00Fu;
+    v = (v | (v << 4)) & 0x030C30C3u;
+    v = (v | (v << 2)) & 0x09249249u;
+    return v;
+}
+
+template <class T>
+__global__ void query_morton(const T* __restrict__ q, int64_t Q, double3 lo, double3 inv, uint32_t* keys,
+                             int64_t* idx) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= Q) return;
+    auto cell = [](double x, double l, double s) {
+        const double f = (x - l) * s;
+        return uint32_t(fmin(fmax(f, 0.0), 1023.0));
+    };
+    const uint32_t x = cell(double(q[3 * i]), lo.x, inv.x);
+    const uint32_t y = cell(double(q[3 * i + 1]), lo.y, inv.y);
+    const uint32_t z = cell(double(q[3 * i + 2]), lo.z, inv.z);
+    keys[i] = (spread10(x) << 2) | (spread10(y) << 1) | spread10(z);
+    idx[i] = i;
+}
+
+// ------------------------------------------------------------ traversal
+template <class T>
+struct TraverseArgs {
+    const T* q;
+    const int64_t* perm;  // sorted position -> query index
+    int64_t Q;
+    const NodeT<T>* box;
+    const int32_t* count;
+    const double* diam64;
+    const T* leafrec;
+    const int32_t* leafmeta;
+    const Poly<T>* polys;  // [0, ne): edge polys, [ne, ne + nt): tri polys
+    int ne, npoly;
+    int use_bh;
+    int exact_boxes;  // every fp32 box equals its fp64 box (quantized geometry)
+    int stack_depth;
+    double beta64;
+    Phys<T> ph;
+    T* part;            // [5][Q] state in sorted order
+    int64_t* leaves;    // sorted order
+    int64_t* far;
+    uint64_t* hash;
+    unsigned long long* rechecks;  // fp64 re-decisions (diagnostic)
+};
+
+constexpr int kTravThreads = 128;
+
+// Reference-rounded fp64 decision (bvh.hpp:105-111,185-187).
+template <class T>
+__device__ __forceinline__ bool decide64(const NodeT<T>& b, double d64, double qx, double qy, double qz,
+                                         double beta) {
+    const double yx = fmin(fmax(qx, double(b.v[0])), double(b.v[4]));
+    const double yy = fmin(fmax(qy, double(b.v[1])), double(b.v[5]));
+    const double yz = fmin(fmax(qz, double(b.v[2])), double(b.v[6]));
+    const double dx = __dsub_rn(qx, yx), dy = __dsub_rn(qy, yy), dz = __dsub_rn(qz, yz);
+    const double s = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+    const double d = __dsqrt_rn(s);
+    return d > 0.0 && d64 < __dmul_rn(beta, d);
+}
+
+template <class T>
+__global__ void __launch_bounds__(kTravThreads) traverse_kernel(const __grid_constant__ TraverseArgs<T> a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    // polynomial table first, then the per-thread stacks [depth][threads]
+    Poly<T>* polys = reinterpret_cast<Poly<T>*>(smem_raw);
+    int32_t* stack = reinterpret_cast<int32_t*>(smem_raw + sizeof(Poly<T>) * a.npoly);
+    for (int i = threadIdx.x; i < a.npoly * kPolyCoefs; i += blockDim.x)
+        reinterpret_cast<T*>(polys)[i] = reinterpret_cast<const T*>(a.polys)[i];
+    __syncthreads();
+
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= a.Q) return;
+    const int64_t qi = a.perm ? a.perm[i] : i;
+    const T qx = a.q[3 * qi], qy = a.q[3 * qi + 1], qz = a.q[3 * qi + 2];
+    Acc<T> acc;
+    acc.init();
+    int64_t nleaf = 0, nfar = 0;
+    uint64_t h = 0;
+    unsigned long long nre = 0;
+    int sp = 0;
+    int32_t id = 0;
+    const T beta = a.ph.beta;
+    while (true) {
+        const NodeT<T> b = a.box[id];
+        int32_t link;
+        memcpy(&link, &b.v[7], sizeof(int32_t));
+        if (a.use_bh) {
+            const T yx = fmin(fmax(qx, b.v[0]), b.v[4]);
+            const T yy = fmin(fmax(qy, b.v[1]), b.v[5]);
+            const T yz = fmin(fmax(qz, b.v[2]), b.v[6]);
+            const T dx = qx - yx, dy = qy - yy, dz = qz - yz;
+            const T s = fma(dx, dx, fma(dy, dy, dz * dz));
+            bool far;
+            if constexpr (sizeof(T) == 4) {
+                const T r = s > T(0) ? Math<T>::rsqrt(s) : T(0);
+                const T d = s * r;
+                const T rhs = beta * d;
+                const T band = T(1e-5) * rhs;
+                if (s == T(0) && a.exact_boxes) far = false;  // contact: d_B = 0 exactly
+                else if (b.v[3] < rhs - band) far = true;
+                else if (b.v[3] > rhs + band) far = false;
+                else {
+                    far = decide64(b, a.diam64[id], double(qx), double(qy), double(qz), a.beta64);
+                    ++nre;
+                }
+                if (far) {
+                    const T lw = Math<T>::lg2(T(a.count[id]) * a.ph.w_ff);
+                    acc.add(masked_exponent(a.ph, d, lw), dx * r, dy * r, dz * r);
+                }
+            } else {
+                far = decide64(b, a.diam64[id], double(qx), double(qy), double(qz), a.beta64);
+                if (far) {
+                    const T d = sqrt(s);
+                    const T r = T(1) / d;
+                    const T lw = Math<T>::lg2(T(a.count[id]) * a.ph.w_ff);
+                    acc.add(masked_exponent(a.ph, d, lw), dx * r, dy * r, dz * r);
+                }
+            }
+            if (far) {
+                ++nfar;
+                h += decision_mix(uint64_t(id), 1);
+                if (sp == 0) break;
+                id = stack[(--sp) * kTravThreads + threadIdx.x];
+                continue;
+            }
+        }
+        if (link < 0) {  // exact leaf (smooth.hpp:122-124)
+            const int slot = -link - 1;
+            const int meta = a.leafmeta[slot];
+            const int kind = meta & 3, poly = (meta >> 2) - 1;
+            T rec[kRecTri];
+            using V = typename Vec4<T>::type;
+            const V* src = reinterpret_cast<const V*>(a.leafrec + size_t(slot) * kRecTri);
+            if (kind == 0) {
+                reinterpret_cast<V*>(rec)[0] = src[0];
+                point_term(a.ph, qx, qy, qz, rec[0], rec[1], rec[2], acc);
+            } else if (kind == 1) {
+#pragma unroll
+                for (int j = 0; j < kRecEdge * int(sizeof(T)) / int(sizeof(V)); ++j) reinterpret_cast<V*>(rec)[j] = src[j];
+                if (poly >= 0) edge_term<T, true>(a.ph, polys[poly], qx, qy, qz, rec, acc);
+                else edge_term<T, false>(a.ph, polys[0], qx, qy, qz, rec, acc);
+            } else {
+#pragma unroll
+                for (int j = 0; j < kRecTri * int(sizeof(T)) / int(sizeof(V)); ++j) reinterpret_cast<V*>(rec)[j] = src[j];
+                if (poly >= 0) tri_term<T, true>(a.ph, polys[a.ne + poly], qx, qy, qz, rec, acc);
+                else tri_term<T, false>(a.ph, polys[0], qx, qy, qz, rec, acc);
+            }
+            ++nleaf;
+            h += decision_mix(uint64_t(id), 2);
+            if (sp == 0) break;
+            id = stack[(--sp) * kTravThreads + threadIdx.x];
+        } else {  // descend: left (id + 1) next, right on the stack
+            stack[(sp++) * kTravThreads + threadIdx.x] = link;
+            id = id + 1;
+        }
+    }
+    a.part[i] = acc.m;
+    a.part[a.Q + i] = acc.s;
+    a.part[2 * a.Q + i] = acc.gx;
+    a.part[3 * a.Q + i] = acc.gy;
+    a.part[4 * a.Q + i] = acc.gz;
+    a.leaves[i] = nleaf;
+    a.far[i] = nfar;
+    a.hash[i] = h;
+    if (nre) atomicAdd(a.rechecks, nre);
+}
+
+template <class T>
+void tree_query(Ctx& c, const T* q, int64_t Q, const sd_params& p, const FinalizeOut& out, cudaStream_t st) {
+    if (!c.dtree_ready) tree_upload(c);
+    const DeviceTree& t = c.dtree;
+    int64_t launches = 0;
+    // Morton order of the queries over the root box (coherent traversal)
+    const sd_bvh_node& root = c.tree[0];
+    double3 lo = make_double3(root.lo[0], root.lo[1], root.lo[2]);
+    auto inv = [](double l, double h) { return h > l ? 1024.0 / (h - l) : 0.0; };
+    double3 iv = make_double3(inv(root.lo[0], root.hi[0]), inv(root.lo[1], root.hi[1]), inv(root.lo[2], root.hi[2]));
+    uint32_t* keys = static_cast<uint32_t*>(c.keys.ensure(size_t(Q) * 2 * sizeof(uint32_t)));
+    int64_t* idx = static_cast<int64_t*>(c.perm.ensure(size_t(Q) * 2 * sizeof(int64_t)));
+    const unsigned blocks = unsigned((Q + 255) / 256);
+    query_morton<T><<<blocks, 256, 0, st>>>(q, Q, lo, iv, keys, idx);
+    check_cuda(cudaGetLastError(), "query morton");
+    ++launches;
+    size_t tmp_bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys, keys + Q, idx, idx + Q, int(Q), 0, 30, st);
+    void* tmp = c.tmp.ensure(tmp_bytes);
+    check_cuda(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, keys + Q, idx, idx + Q, int(Q), 0, 30, st),
+               "radix sort queries");
+    launches += 4;  // onesweep histogram + passes (approximate count of CUB kernels)
+    const int64_t* perm = idx + Q;
+
+    // polynomial table: edge polys then triangle polys
+    const int ne = int(c.edge_a.size() / 5), nt = int(c.tri_stored.size() / 13);
+    const int npoly = std::max(1, ne + nt);
+    std::vector<Poly<T>> ptab(npoly);
+    for (int e = 0; e < ne; ++e) ptab[e] = make_poly<T>(c, SD_EDGE, e);
+    for (int k = 0; k < nt; ++k) ptab[ne + k] = make_poly<T>(c, SD_TRIANGLE, k);
+    Poly<T>* dpoly = static_cast<Poly<T>*>(c.polys.ensure(ptab.size() * sizeof(Poly<T>)));
+    check_cuda(cudaMemcpyAsync(dpoly, ptab.data(), ptab.size() * sizeof(Poly<T>), cudaMemcpyHostToDevice, st),
+               "upload polys");
+
+    T* part = static_cast<T*>(c.part.ensure(size_t(5) * Q * sizeof(T)));
+    int64_t* cnt = static_cast<int64_t*>(c.counters.ensure(size_t(Q) * 3 * sizeof(int64_t) + 64));
+    unsigned long long* re = reinterpret_cast<unsigned long long*>(cnt + 3 * Q);
+    check_cuda(cudaMemsetAsync(re, 0, sizeof(unsigned long long), st), "memset");
+
+    TraverseArgs<T> a;
+    a.q = q;
+    a.perm = perm;
+    a.Q = Q;
+    a.box = t.box.as<NodeT<T>>();
+    a.count = t.count.as<int32_t>();
+    a.diam64 = t.diam64.as<double>();
+    a.leafrec = t.leafrec.as<T>();
+    a.leafmeta = t.leafmeta.as<int32_t>();
+    a.polys = dpoly;
+    a.ne = ne;
+    a.npoly = npoly;
+    a.use_bh = p.beta > 0.0 ? 1 : 0;
+    a.exact_boxes = t.exact_boxes ? 1 : 0;
+    a.stack_depth = t.depth + 1;
+    a.beta64 = p.beta;
+    a.ph = make_phys<T>(c, p);
+    a.part = part;
+    a.leaves = cnt;
+    a.far = cnt + Q;
+    a.hash = reinterpret_cast<uint64_t*>(cnt + 2 * Q);
+    a.rechecks = re;
+    const size_t smem = sizeof(Poly<T>) * npoly + size_t(a.stack_depth) * kTravThreads * sizeof(int32_t);
+    auto kern = traverse_kernel<T>;
+    check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)), "smem attr");
+    kern<<<unsigned((Q + kTravThreads - 1) / kTravThreads), kTravThreads, smem, st>>>(a);
+    check_cuda(cudaGetLastError(), "traverse kernel");
+    ++launches;
+    check_cuda(launch_finalize<T>(part, 1, Q, p.alpha, p.epsilon, 0, a.leaves, a.far, a.hash, perm, out, st),
+               "finalize");
+    ++launches;
+    c.last_launches = launches;
+}
+template void tree_query<float>(Ctx&, const float*, int64_t, const sd_params&, const FinalizeOut&, cudaStream_t);
+template void tree_query<double>(Ctx&, const double*, int64_t, const sd_params&, const FinalizeOut&, cudaStream_t);
+
+}  // namespace sdgpu
+
+namespace sdgpu {
+void tree_build_lbvh(Ctx& c) {
+    throw std::runtime_error("LBVH builder not available in this build");
+}
+}  // namespace sdgpu

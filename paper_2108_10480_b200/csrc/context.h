@@ -1,0 +1,128 @@
+// context.h -- sd_ctx: one device, its resident geometry (per-kind
+// primitive records grouped into (kind, polynomial) segments), weight
+// table, tree and scratch. Internal to libsdgpu.so.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "../../include/sdgpu.h"
+#include "exact.h"
+
+namespace sdgpu {
+
+void set_error(const std::string& msg);
+
+struct CudaError {
+    cudaError_t code;
+    std::string where;
+};
+void check_cuda(cudaError_t e, const char* where);  // throws CudaError
+
+// Grow-only device buffer.
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() { release(); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+    void* ensure(size_t n) {
+        if (n > bytes) {
+            release();
+            check_cuda(cudaMalloc(&p, n ? n : 16), "cudaMalloc");
+            bytes = n ? n : 16;
+        }
+        return p;
+    }
+    template <class T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
+// A run of primitives of one kind sharing one weight polynomial
+// (poly = -1: unit weight).
+struct Segment {
+    int kind;
+    int poly;
+    int64_t offset;  // first record in the kind's record array
+    int64_t count;
+};
+
+// Tree in traversal layout (pre-order ids == reference ids).
+//   box[2 * id + 0] = (lo.xyz, diameter rounded to T)
+//   box[2 * id + 1] = (hi.xyz, link) with link = right child id, or
+//                     -(leaf slot + 1) on leaves
+//   count[id]       = n_B;  diam64[id] = reference fp64 diameter
+//   leaf slot s     -> leafrec[s * 24] unified record, leafmeta[s] =
+//                      (kind | (poly + 1) << 2)
+struct DeviceTree {
+    int64_t nodes = 0;
+    int64_t leaves = 0;
+    int depth = 0;
+    bool exact_boxes = true;
+    DevBuf box, count, diam64, leafrec, leafmeta;
+};
+
+struct Ctx {
+    int device = 0;
+    int precision = SD_FP32;
+    cudaStream_t stream = nullptr;  // library-owned stream for host-buffer calls
+
+    // geometry (vertices already rounded to float in SD_FP32)
+    std::vector<double> xyz;
+    std::vector<int32_t> sv;
+    std::vector<uint8_t> kind;
+    int64_t V = 0, N = 0;
+    bool have_geom = false;
+
+    // weights
+    bool have_weights = false;
+    double A = 1.0, sup_wtilde = 1.0;
+    std::vector<double> edge_a, tri_stored;
+    std::vector<int32_t> poly_index;
+
+    // exact layout
+    bool exact_ready = false;
+    std::vector<Segment> segs;
+    DevBuf rec[3];
+
+    // tree (host copy in the reference layout + device traversal layout)
+    bool have_tree = false;
+    std::vector<sd_bvh_node> tree;
+    DeviceTree dtree;
+    bool dtree_ready = false;
+
+    // scratch
+    DevBuf qd, qT, part, out_d, out_g, out_c, out_gc, out_l, out_f, out_h;
+    DevBuf perm, keys, tmp, counters, polys;
+    int64_t last_launches = 0;
+};
+
+// Host helpers shared by api.cu / bvh.cu
+template <class T>
+Phys<T> make_phys(const Ctx& c, const sd_params& p);
+template <class T>
+Poly<T> make_poly(const Ctx& c, int kind, int poly);
+template <class T>
+void build_record(const Ctx& c, int64_t prim, T* out);  // rec_size(kind) values
+
+// Tree entry points (bvh.cu)
+void tree_upload(Ctx& c);  // host reference layout -> DeviceTree
+void tree_build_median(Ctx& c);
+void tree_build_lbvh(Ctx& c);
+template <class T>
+void tree_query(Ctx& c, const T* q, int64_t Q, const sd_params& p, const FinalizeOut& out, cudaStream_t st);
+
+}  // namespace sdgpu
+
+struct sd_ctx : sdgpu::Ctx {};

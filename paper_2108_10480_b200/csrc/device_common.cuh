@@ -1,0 +1,150 @@
+// device_common.cuh -- sm_100a device helpers shared by the exact (K1),
+// tree (K2/K3) and epilogue (K4) kernels: precision traits, the online
+// max-shifted log2-domain accumulator, bulk-copy/mbarrier PTX wrappers and
+// the per-primitive record layouts.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace sdgpu {
+
+// ----------------------------------------------------------- precision
+// MUFU-backed approximations for fp32 (ex2/lg2/rsqrt/rcp.approx: <= 2 ulp),
+// library double-precision routines for fp64.
+template <class T> struct Math;
+template <> struct Math<float> {
+    static __device__ __forceinline__ float ex2(float x) {
+        float y;
+        asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+        return y;
+    }
+    static __device__ __forceinline__ float lg2(float x) {
+        float y;
+        asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+        return y;
+    }
+    static __device__ __forceinline__ float rsqrt(float x) {
+        float y;
+        asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+        return y;
+    }
+    static __device__ __forceinline__ float rcp(float x) {
+        float y;
+        asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+        return y;
+    }
+    static constexpr float kMinusHuge = -1e30f;  // "no term yet" log2 shift
+};
+template <> struct Math<double> {
+    static __device__ __forceinline__ double ex2(double x) { return exp2(x); }
+    static __device__ __forceinline__ double lg2(double x) { return log2(x); }
+    static __device__ __forceinline__ double rsqrt(double x) { return ::rsqrt(x); }
+    static __device__ __forceinline__ double rcp(double x) { return 1.0 / x; }
+    static constexpr double kMinusHuge = -1e300;
+};
+
+// Vector types used to read records out of shared memory (16 B loads).
+template <class T> struct Vec4;
+template <> struct Vec4<float> { using type = float4; };
+template <> struct Vec4<double> { using type = double2; };
+
+// ------------------------------------------------ online accumulator
+// Per-query partial of the reference sum c = sum_i w_i exp(-alpha d_i),
+// grad_c = sum_i exp(-alpha d_i) (w_i grad d_i - grad w_i / alpha)
+// (smooth.hpp:51-61, 79-93), kept as
+//   c = s * 2^m,  grad_c = g * 2^m
+// with the exponent x_i = log2(w_i exp(-alpha d_i)). The shift m is raised
+// lazily (only when a term exceeds it), by kHeadroom extra so that a
+// slowly rising sequence does not rescale at every record; terms never
+// exceed 2^0 relative to the shift, so nothing can overflow, and only terms
+// below 2^-(126 - kHeadroom) of the running maximum flush (fp32).
+constexpr float kHeadroom = 16.0f;
+
+template <class T>
+struct Acc {
+    T m, s, gx, gy, gz;
+    __device__ __forceinline__ void init() {
+        m = Math<T>::kMinusHuge;
+        s = gx = gy = gz = T(0);
+    }
+    // x: log2 exponent of the term (may be -inf for a masked term);
+    // (hx, hy, hz): gradient coefficient divided by the weight
+    __device__ __forceinline__ void add(T x, T hx, T hy, T hz) {
+        if (x > m) {  // rare after the first few records: divergent but cheap
+            const T mn = x + T(kHeadroom);
+            const T sc = Math<T>::ex2(m - mn);
+            s *= sc; gx *= sc; gy *= sc; gz *= sc;
+            m = mn;
+        }
+        const T e = Math<T>::ex2(x - m);
+        s += e;
+        gx = fma(e, hx, gx);
+        gy = fma(e, hy, gy);
+        gz = fma(e, hz, gz);
+    }
+};
+
+// ------------------------------------------------------- bulk copies
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t done;
+    do {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+    } while (!done);
+}
+// TMA bulk (non-tensor) copy global -> shared, completion counted in bytes
+// on the mbarrier. dst/src 16-byte aligned, bytes a multiple of 16.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// ------------------------------------------------------ record layouts
+// One record per primitive, in units of the compute type T, 16-B aligned.
+// Geometry is stored relative to the first corner so the closest point is
+// formed as delta = (q - a) - u ab - v ac (no absolute reconstruction; the
+// fp32 error then scales with |q - a|, not with |q|).
+//
+// point    (4):  a.xyz, pad
+// edge    (12):  a.xyz, e = b - a, 1/|e|^2, e/|e|^2, pad2
+// triangle(24):  a.xyz, ab, ac, A=|ab|^2, B=ab.ac, C=|ac|^2, 1/A, 1/C,
+//                1/|bc|^2, 1/(AC - B^2), G1, G2, pad2
+//   with G1 = n x (a - c) / |n|^2, G2 = n x (b - a) / |n|^2, n = ab x ac,
+//   the (alpha-free) barycentric shape gradients of weights.hpp:689-696.
+constexpr int kRecPoint = 4;
+constexpr int kRecEdge = 12;
+constexpr int kRecTri = 24;
+__host__ __device__ constexpr int rec_size(int kind) {
+    return kind == 0 ? kRecPoint : (kind == 1 ? kRecEdge : kRecTri);
+}
+
+// ----------------------------------------------------- decision hash
+// Same mixer as the CPU checker used by the tests (bit for bit).
+__host__ __device__ __forceinline__ uint64_t decision_mix(uint64_t node, uint64_t kind) {
+    uint64_t z = node * 4 + kind + 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+}  // namespace sdgpu

@@ -1,0 +1,127 @@
+// epilogue.cu -- K4: de-shift the per-query partial state into the
+// reference's unshifted fp64 domain and finalise exactly as
+// detail::result_from_accum does (smooth.hpp:147-159):
+//   c = sum_k s_k 2^{m_k},  grad_c = sum_k g_k 2^{m_k}
+//   c <= 0  ->  d_hat = +inf, grad = 0
+//   else        d_hat = -log(c) / alpha, grad = grad_c / (c + epsilon)
+// The -708 underflow mask of smooth.hpp:85-88 was applied per term in the
+// producing kernels, so the fp64 sums here have the reference semantics.
+#include "exact.h"
+
+#include <cmath>
+
+namespace sdgpu {
+
+template <class T>
+__global__ void finalize_kernel(const T* __restrict__ part, int splits, int64_t Q, double alpha, double eps,
+                                int64_t const_leaves, const int64_t* __restrict__ leaves_in,
+                                const int64_t* __restrict__ far_in, const uint64_t* __restrict__ hash_in,
+                                const int64_t* __restrict__ perm, FinalizeOut o) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= Q) return;
+    double M = -INFINITY;
+    for (int k = 0; k < splits; ++k) M = fmax(M, double(part[size_t(k) * 5 * Q + i]));
+    double s = 0, gx = 0, gy = 0, gz = 0;
+    for (int k = 0; k < splits; ++k) {
+        const T* p = part + size_t(k) * 5 * Q;
+        const double f = exp2(double(p[i]) - M);
+        s = fma(double(p[Q + i]), f, s);
+        gx = fma(double(p[2 * Q + i]), f, gx);
+        gy = fma(double(p[3 * Q + i]), f, gy);
+        gz = fma(double(p[4 * Q + i]), f, gz);
+    }
+    const double scale = exp2(M);
+    const double c = s * scale;
+    const double cx = gx * scale, cy = gy * scale, cz = gz * scale;
+    const int64_t j = perm ? perm[i] : i;  // tree path: undo the query sort
+    double d = INFINITY, ax = 0, ay = 0, az = 0;
+    if (c > 0.0) {
+        d = -log(c) / alpha;
+        const double den = c + eps;
+        ax = cx / den;
+        ay = cy / den;
+        az = cz / den;
+    }
+    o.d_hat[j] = d;
+    if (o.grad) {
+        o.grad[3 * j] = ax;
+        o.grad[3 * j + 1] = ay;
+        o.grad[3 * j + 2] = az;
+    }
+    if (o.c) o.c[j] = c;
+    if (o.grad_c) {
+        o.grad_c[3 * j] = cx;
+        o.grad_c[3 * j + 1] = cy;
+        o.grad_c[3 * j + 2] = cz;
+    }
+    if (o.leaves) o.leaves[j] = leaves_in ? leaves_in[i] : const_leaves;
+    if (o.far_field) o.far_field[j] = far_in ? far_in[i] : 0;
+    if (o.hash) o.hash[j] = hash_in ? hash_in[i] : 0;
+}
+
+template <class T>
+cudaError_t launch_finalize(const T* part, int splits, int64_t Q, double alpha, double epsilon,
+                            int64_t const_leaves, const int64_t* leaves_in, const int64_t* far_in,
+                            const uint64_t* hash_in, const int64_t* perm, const FinalizeOut& out, cudaStream_t st) {
+    if (Q <= 0) return cudaSuccess;
+    const int threads = 256;
+    const unsigned blocks = unsigned((Q + threads - 1) / threads);
+    finalize_kernel<T><<<blocks, threads, 0, st>>>(part, splits, Q, alpha, epsilon, const_leaves, leaves_in, far_in,
+                                                   hash_in, perm, out);
+    return cudaGetLastError();
+}
+template cudaError_t launch_finalize<float>(const float*, int, int64_t, double, double, int64_t, const int64_t*,
+                                            const int64_t*, const uint64_t*, const int64_t*, const FinalizeOut&,
+                                            cudaStream_t);
+template cudaError_t launch_finalize<double>(const double*, int, int64_t, double, double, int64_t, const int64_t*,
+                                             const int64_t*, const uint64_t*, const int64_t*, const FinalizeOut&,
+                                             cudaStream_t);
+
+__global__ void finalize_sums_kernel(const double* __restrict__ c, const double* __restrict__ gc, int64_t Q,
+                                     double alpha, double eps, double* d_hat, double* grad) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= Q) return;
+    const double ci = c[i];
+    double d = INFINITY, ax = 0, ay = 0, az = 0;
+    if (ci > 0.0) {
+        d = -log(ci) / alpha;
+        const double den = ci + eps;
+        ax = gc[3 * i] / den;
+        ay = gc[3 * i + 1] / den;
+        az = gc[3 * i + 2] / den;
+    }
+    d_hat[i] = d;
+    if (grad) {
+        grad[3 * i] = ax;
+        grad[3 * i + 1] = ay;
+        grad[3 * i + 2] = az;
+    }
+}
+
+cudaError_t launch_finalize_sums(const double* c, const double* grad_c, int64_t Q, double alpha, double epsilon,
+                                 double* d_hat, double* grad, cudaStream_t st) {
+    if (Q <= 0) return cudaSuccess;
+    const unsigned blocks = unsigned((Q + 255) / 256);
+    finalize_sums_kernel<<<blocks, 256, 0, st>>>(c, grad_c, Q, alpha, epsilon, d_hat, grad);
+    return cudaGetLastError();
+}
+
+__global__ void empty_kernel(int64_t Q, FinalizeOut o) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= Q) return;
+    o.d_hat[i] = INFINITY;
+    if (o.grad) o.grad[3 * i] = o.grad[3 * i + 1] = o.grad[3 * i + 2] = 0.0;
+    if (o.c) o.c[i] = 0.0;
+    if (o.grad_c) o.grad_c[3 * i] = o.grad_c[3 * i + 1] = o.grad_c[3 * i + 2] = 0.0;
+    if (o.leaves) o.leaves[i] = 0;
+    if (o.far_field) o.far_field[i] = 0;
+    if (o.hash) o.hash[i] = 0;
+}
+
+cudaError_t launch_empty_result(int64_t Q, const FinalizeOut& out, cudaStream_t st) {
+    if (Q <= 0) return cudaSuccess;
+    empty_kernel<<<unsigned((Q + 255) / 256), 256, 0, st>>>(Q, out);
+    return cudaGetLastError();
+}
+
+}  // namespace sdgpu

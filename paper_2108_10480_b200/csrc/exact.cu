@@ -1,0 +1,174 @@
+// exact.cu -- K1: exact all-primitive smooth distance, the GPU replacement
+// of smooth_min_dist_flat (smooth.hpp:189-198) for a whole query batch.
+//
+// Layout of work: CTAs tile the queries (kThreads threads x QPT queries per
+// thread, queries in registers) and, when there are too few query tiles to
+// fill 148 SMs, also split the primitive range ("splits"); each CTA streams
+// its primitive range through shared memory with TMA bulk copies
+// (cp.async.bulk + mbarrier, kStages-deep ring) and every thread evaluates
+// each staged primitive against its queries -- all lanes read the same
+// record, so shared-memory loads are broadcasts. Primitives are grouped by
+// (kind, weight polynomial) into segments on the host; one launch per
+// segment keeps the polynomial coefficients in kernel-parameter constant
+// memory (FFMA constant-bank operands) and the kind branch out of the loop.
+// Per-query state (Acc: shift m, sums s, g) is carried between segment
+// launches in `part`; K4 (epilogue.cu) merges splits and finalises.
+#include "exact.h"
+#include "pair.cuh"
+
+namespace sdgpu {
+
+template <class T>
+struct ExactArgs {
+    const T* rec;       // first record of this segment
+    int64_t count;      // primitives in the segment
+    int64_t chunk;      // primitives per split
+    const T* q;         // Q x 3 query points
+    int64_t Q;
+    T* part;            // [splits][5][Q] partial state (m, s, gx, gy, gz)
+    int first;          // first segment: initialise instead of loading
+    Phys<T> ph;
+    Poly<T> poly;
+};
+
+constexpr int kThreads = 256;
+constexpr int kStages = 3;
+
+template <class T, int KIND>
+constexpr int tile_prims() {
+    // ~12 KB (fp32) / 24 KB (fp64) per stage
+    return KIND == 0 ? 768 : (KIND == 1 ? 256 : 128);
+}
+
+template <class T, int KIND, bool POLY, int QPT>
+__global__ void __launch_bounds__(kThreads) exact_kernel(const __grid_constant__ ExactArgs<T> a) {
+    constexpr int R = rec_size(KIND);
+    constexpr int TILE = tile_prims<T, KIND>();
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    T* tiles = reinterpret_cast<T*>(smem_raw);
+    __shared__ uint64_t full[kStages];
+
+    const int split = blockIdx.y;
+    const int64_t p0 = int64_t(split) * a.chunk;
+    const int64_t p1 = min(a.count, p0 + a.chunk);
+    const int64_t np = max(int64_t(0), p1 - p0);
+    const int ntiles = int((np + TILE - 1) / TILE);
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    auto issue = [&](int t) {
+        const int s = t % kStages;
+        const int64_t b = p0 + int64_t(t) * TILE;
+        const int n = int(min(int64_t(TILE), p1 - b));
+        const uint32_t bytes = uint32_t(n) * R * sizeof(T);
+        mbar_arrive_expect_tx(&full[s], bytes);
+        bulk_g2s(tiles + size_t(s) * TILE * R, a.rec + b * R, bytes, &full[s]);
+    };
+    if (threadIdx.x == 0)
+        for (int t = 0; t < kStages && t < ntiles; ++t) issue(t);
+
+    // queries of this thread
+    T qx[QPT], qy[QPT], qz[QPT];
+    Acc<T> acc[QPT];
+    int64_t qi[QPT];
+    T* part = a.part + size_t(split) * 5 * a.Q;
+#pragma unroll
+    for (int k = 0; k < QPT; ++k) {
+        qi[k] = int64_t(blockIdx.x) * kThreads * QPT + k * kThreads + threadIdx.x;
+        const int64_t qc = min(qi[k], a.Q - 1);
+        qx[k] = a.q[3 * qc];
+        qy[k] = a.q[3 * qc + 1];
+        qz[k] = a.q[3 * qc + 2];
+        if (a.first) {
+            acc[k].init();
+        } else {
+            acc[k].m = part[qc];
+            acc[k].s = part[a.Q + qc];
+            acc[k].gx = part[2 * a.Q + qc];
+            acc[k].gy = part[3 * a.Q + qc];
+            acc[k].gz = part[4 * a.Q + qc];
+        }
+    }
+
+    for (int t = 0; t < ntiles; ++t) {
+        const int s = t % kStages;
+        mbar_wait(&full[s], (t / kStages) & 1);
+        const T* tile = tiles + size_t(s) * TILE * R;
+        const int n = int(min(int64_t(TILE), p1 - (p0 + int64_t(t) * TILE)));
+#pragma unroll 2
+        for (int i = 0; i < n; ++i) {
+            T rec[R];
+            using V = typename Vec4<T>::type;
+            constexpr int NV = R * sizeof(T) / sizeof(V);
+            const V* src = reinterpret_cast<const V*>(tile + size_t(i) * R);
+#pragma unroll
+            for (int j = 0; j < NV; ++j) reinterpret_cast<V*>(rec)[j] = src[j];
+#pragma unroll
+            for (int k = 0; k < QPT; ++k) {
+                if constexpr (KIND == 0) point_term(a.ph, qx[k], qy[k], qz[k], rec[0], rec[1], rec[2], acc[k]);
+                else if constexpr (KIND == 1) edge_term<T, POLY>(a.ph, a.poly, qx[k], qy[k], qz[k], rec, acc[k]);
+                else tri_term<T, POLY>(a.ph, a.poly, qx[k], qy[k], qz[k], rec, acc[k]);
+            }
+        }
+        __syncthreads();  // every thread is done with stage s
+        if (threadIdx.x == 0 && t + kStages < ntiles) issue(t + kStages);
+    }
+
+#pragma unroll
+    for (int k = 0; k < QPT; ++k) {
+        if (qi[k] >= a.Q) continue;
+        part[qi[k]] = acc[k].m;
+        part[a.Q + qi[k]] = acc[k].s;
+        part[2 * a.Q + qi[k]] = acc[k].gx;
+        part[3 * a.Q + qi[k]] = acc[k].gy;
+        part[4 * a.Q + qi[k]] = acc[k].gz;
+    }
+}
+
+template <class T, int KIND, bool POLY, int QPT>
+static cudaError_t launch_one(const ExactLaunch<T>& L, cudaStream_t st) {
+    constexpr int R = rec_size(KIND);
+    constexpr int TILE = tile_prims<T, KIND>();
+    const size_t smem = size_t(kStages) * TILE * R * sizeof(T);
+    auto kern = exact_kernel<T, KIND, POLY, QPT>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+    ExactArgs<T> a;
+    a.rec = L.rec;
+    a.count = L.count;
+    a.chunk = L.chunk;
+    a.q = L.q;
+    a.Q = L.Q;
+    a.part = L.part;
+    a.first = L.first;
+    a.ph = L.ph;
+    a.poly = L.poly;
+    const int64_t qblocks = (L.Q + int64_t(kThreads) * QPT - 1) / (int64_t(kThreads) * QPT);
+    dim3 grid(unsigned(qblocks), unsigned(L.splits));
+    kern<<<grid, kThreads, smem, st>>>(a);
+    return cudaGetLastError();
+}
+
+int64_t exact_queries_per_cta(int kind) { return int64_t(kThreads) * 2; }
+
+template <class T>
+cudaError_t launch_exact(const ExactLaunch<T>& L, cudaStream_t st) {
+    constexpr int QPT = 2;
+    switch (L.kind * 2 + (L.has_poly ? 1 : 0)) {
+        case 0:
+        case 1: return launch_one<T, 0, false, QPT>(L, st);
+        case 2: return launch_one<T, 1, false, QPT>(L, st);
+        case 3: return launch_one<T, 1, true, QPT>(L, st);
+        case 4: return launch_one<T, 2, false, QPT>(L, st);
+        case 5: return launch_one<T, 2, true, QPT>(L, st);
+    }
+    return cudaErrorInvalidValue;
+}
+
+template cudaError_t launch_exact<float>(const ExactLaunch<float>&, cudaStream_t);
+template cudaError_t launch_exact<double>(const ExactLaunch<double>&, cudaStream_t);
+
+}  // namespace sdgpu

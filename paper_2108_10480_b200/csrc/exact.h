@@ -1,0 +1,52 @@
+// exact.h -- host-side launch descriptors for the kernels (K1 exact, K3
+// tree traversal, K4 epilogue). Internal to libsdgpu.so.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "pair.cuh"
+
+namespace sdgpu {
+
+template <class T>
+struct ExactLaunch {
+    int kind = 0;          // SD_POINT / SD_EDGE / SD_TRIANGLE
+    bool has_poly = false; // false: unit weight (w = A^S)
+    const T* rec = nullptr;
+    int64_t count = 0;     // primitives in the segment
+    int64_t chunk = 0;     // primitives per split
+    int splits = 1;
+    const T* q = nullptr;
+    int64_t Q = 0;
+    T* part = nullptr;     // [splits][5][Q]
+    int first = 1;
+    Phys<T> ph{};
+    Poly<T> poly{};
+};
+
+template <class T>
+cudaError_t launch_exact(const ExactLaunch<T>& L, cudaStream_t st);
+int64_t exact_queries_per_cta(int kind);
+
+// K4: merge `splits` partial states and finalise (smooth.hpp:147-159).
+struct FinalizeOut {
+    double* d_hat = nullptr;
+    double* grad = nullptr;
+    double* c = nullptr;
+    double* grad_c = nullptr;
+    int64_t* leaves = nullptr;
+    int64_t* far_field = nullptr;
+    uint64_t* hash = nullptr;
+};
+template <class T>
+cudaError_t launch_finalize(const T* part, int splits, int64_t Q, double alpha, double epsilon,
+                            int64_t const_leaves, const int64_t* leaves_in, const int64_t* far_in,
+                            const uint64_t* hash_in, const int64_t* perm, const FinalizeOut& out, cudaStream_t st);
+cudaError_t launch_finalize_sums(const double* c, const double* grad_c, int64_t Q, double alpha, double epsilon,
+                                 double* d_hat, double* grad, cudaStream_t st);
+
+// Fills an empty-mesh result (+inf, zero gradient; smooth.hpp:151-155).
+cudaError_t launch_empty_result(int64_t Q, const FinalizeOut& out, cudaStream_t st);
+
+}  // namespace sdgpu

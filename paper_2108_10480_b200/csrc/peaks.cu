@@ -1,0 +1,85 @@
+// peaks.cu -- libsdpeaks.so: in-run microbenchmarks for the roofline
+// denominators that MEASURED_PEAKS.json does not carry (it has HBM copy and
+// bf16 GEMM only): FP32 FFMA, FP64 DFMA and MUFU (ex2) issue throughput,
+// measured on the same GPU, in the same process, right before the bench.
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace {
+
+constexpr int kChains = 8;
+constexpr int kIters = 2048;
+
+template <class T>
+__global__ void fma_kernel(T* out, T a, T b) {
+    T x[kChains];
+#pragma unroll
+    for (int c = 0; c < kChains; ++c) x[c] = T(threadIdx.x + c);
+    for (int i = 0; i < kIters; ++i) {
+#pragma unroll
+        for (int c = 0; c < kChains; ++c) x[c] = fma(x[c], a, b);
+    }
+    T s = 0;
+#pragma unroll
+    for (int c = 0; c < kChains; ++c) s += x[c];
+    if (s == T(-1234.5)) out[threadIdx.x] = s;  // defeat dead-code elimination
+}
+
+__global__ void ex2_kernel(float* out, float a) {
+    float x[kChains];
+#pragma unroll
+    for (int c = 0; c < kChains; ++c) x[c] = -1e-3f * float(threadIdx.x + c);
+    for (int i = 0; i < kIters; ++i) {
+#pragma unroll
+        for (int c = 0; c < kChains; ++c) {
+            float y;
+            asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x[c]));
+            x[c] = y * a;
+        }
+    }
+    float s = 0;
+#pragma unroll
+    for (int c = 0; c < kChains; ++c) s += x[c];
+    if (s == -1234.5f) out[threadIdx.x] = s;
+}
+
+template <class F>
+double time_ms(F&& launch, int reps) {
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    launch();  // warm-up
+    cudaEventRecord(e0);
+    for (int r = 0; r < reps; ++r) launch();
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return double(ms) / reps;
+}
+
+}  // namespace
+
+extern "C" {
+
+// Returns 0 on success. Rates in flop/s (FMA = 2 flops) and MUFU ops/s.
+int sd_measure_peaks(double* ffma_flops, double* dfma_flops, double* mufu_ops) {
+    int sms = 0;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0) != cudaSuccess) return -1;
+    void* buf = nullptr;
+    if (cudaMalloc(&buf, 4096) != cudaSuccess) return -1;
+    const int threads = 256, blocks = sms * 8;
+    const double work = double(blocks) * threads * kIters * kChains;
+    double ms = time_ms([&] { fma_kernel<float><<<blocks, threads>>>((float*)buf, 0.999f, 1e-3f); }, 10);
+    *ffma_flops = 2.0 * work / (ms * 1e-3);
+    ms = time_ms([&] { fma_kernel<double><<<blocks, threads>>>((double*)buf, 0.999, 1e-3); }, 5);
+    *dfma_flops = 2.0 * work / (ms * 1e-3);
+    ms = time_ms([&] { ex2_kernel<<<blocks, threads>>>((float*)buf, 0.999f); }, 10);
+    *mufu_ops = work / (ms * 1e-3);
+    cudaFree(buf);
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+}  // extern "C"

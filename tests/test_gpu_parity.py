@@ -1,0 +1,245 @@
+"""GPU parity: the CUDA path (through the C ABI of include/sdgpu.h) against
+the CPU oracle on the same seeded inputs and the same WeightSet table.
+
+Tolerances (BASELINE.json north_star):
+  fp32: |d - d_ref| <= 1e-5 max(1, |d_ref|),  |g - g_ref| <= 1e-4 max(1, |g_ref|)
+  fp64: |d - d_ref| <= 1e-10 max(1, |d_ref|), |g - g_ref| <= 1e-9 max(1, |g_ref|)
+  +inf must agree except in the tie band |alpha d_min - 708| < 1e-3.
+fp32 inputs (vertices, queries) are rounded to float before either side
+sees them, so parity measures arithmetic, not input rounding.
+"""
+import math
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+TOL = {0: (1e-5, 1e-4), 1: (1e-10, 1e-9)}
+
+
+def engine_for(sd, O, mesh, weights, prec, tree=None):
+    e = sd.Engine(0, prec)
+    e.set_geometry(mesh.vertices, mesh.simplices, mesh.kinds)
+    e.set_weight_table(weights.table)
+    if tree is not None:
+        e.set_bvh(tree.nodes())
+    return e
+
+
+def prep(O, mesh, q, prec):
+    if prec == 0:
+        mesh = mesh.quantized()
+        q = np.asarray(q, np.float32).astype(np.float64)
+    return mesh, np.ascontiguousarray(q, np.float64)
+
+
+def assert_close(got, ref, prec, alpha=None, what=""):
+    td, tg = TOL[prec]
+    fin = np.isfinite(ref.d_hat)
+    bad_inf = np.isfinite(got.d_hat) != fin
+    if bad_inf.any():
+        # allowed only in the -708 tie band
+        assert alpha is not None, f"{what}: inf mismatch at {np.nonzero(bad_inf)[0][:5]}"
+        band = np.abs(-np.log(np.maximum(ref.c, 1e-320)) - 708.0) < 1e-2
+        assert (band | ~bad_inf).all(), f"{what}: inf mismatch outside the tie band"
+    both = fin & np.isfinite(got.d_hat)
+    err = np.abs(got.d_hat[both] - ref.d_hat[both]) / np.maximum(1.0, np.abs(ref.d_hat[both]))
+    assert err.size == 0 or err.max() <= td, f"{what}: d_hat err {err.max():.3g} > {td}"
+    gref = ref.grad[both]
+    gerr = np.linalg.norm(got.grad[both] - gref, axis=1) / np.maximum(1.0, np.linalg.norm(gref, axis=1))
+    assert gerr.size == 0 or gerr.max() <= tg, f"{what}: grad err {gerr.max():.3g} > {tg}"
+    assert not got.grad[~np.isfinite(got.d_hat)].any(), f"{what}: nonzero gradient at +inf"
+
+
+# -------------------------------------------------------- known answers
+@pytest.mark.parametrize("prec", [0, 1])
+def test_known_answers_on_gpu(sd, oracle, prec):
+    O = oracle
+    # SinglePointClosedForm (test_smooth.cpp:40-55)
+    m = O.Mesh.from_arrays([[0, 0, 0]], [[0, -1, -1]], [0])
+    q = np.array([[0.3, -0.2, 0.6]])
+    e = engine_for(sd, O, m, O.Weights.build(m), prec)
+    r = e.smooth_min_dist_flat(q.astype(np.float32).astype(float) if prec == 0 else q,
+                               sd.SmoothParams(alpha=50.0, beta=0.0))
+    qq = q.astype(np.float32).astype(float) if prec == 0 else q
+    tol = 1e-6 if prec == 0 else 1e-12
+    assert abs(r.d_hat[0] - np.linalg.norm(qq)) < tol
+    assert np.abs(r.grad[0] - qq[0] / np.linalg.norm(qq)).max() < tol
+    assert r.leaves[0] == 1 and r.far_field[0] == 0
+    # CoincidentPointsShiftByLogCount (:57-72)
+    p = [0.1, 0.2, 0.3]
+    m = O.Mesh.from_arrays([p, p], [[0, -1, -1], [1, -1, -1]], [0, 0])
+    with pytest.raises(sd.SdError):  # coincident corners are only rejected within a simplex
+        sd.Engine(0, prec).set_geometry([[0, 0, 0], [0, 0, 0]], [[0, 1, -1]], [1])
+    e = engine_for(sd, O, m, O.Weights.build(m), prec)
+    r = e.smooth_min_dist_flat([[1.0, 0.0, 0.0]], sd.SmoothParams(alpha=80.0, beta=0.0))
+    pp = np.array(p, np.float32).astype(float) if prec == 0 else np.array(p)
+    d = np.linalg.norm(np.array([1.0, 0, 0]) - pp)
+    assert abs(r.d_hat[0] - (d - math.log(2.0) / 80.0)) < tol
+    # FarQueryUnderflowsToInfinity (:201-219)
+    m = O.point_cluster(20, 2, 0.05)
+    e = engine_for(sd, O, m, O.Weights.build(m), prec)
+    r = e.smooth_min_dist_flat([[3.0, 0.0, 0.0]], sd.SmoothParams(alpha=400.0, beta=0.0))
+    assert r.c[0] == 0.0 and math.isinf(r.d_hat[0]) and not r.grad.any()
+    r = e.smooth_min_dist_flat([[3.0, 0.0, 0.0]], sd.SmoothParams(alpha=200.0, beta=0.0))
+    assert math.isfinite(r.d_hat[0]) and abs(np.linalg.norm(r.grad[0]) - 1.0) < 1e-3
+
+
+@pytest.mark.parametrize("prec", [0, 1])
+def test_far_cluster_collapses_on_gpu(sd, oracle, prec):  # test_smooth.cpp:74-90
+    O = oracle
+    m = O.point_cluster(4, 3, 1e-3)
+    mq, q = prep(O, m, [[2.0, 0.4, -0.3]], prec)
+    t = O.Tree.build(mq)
+    e = engine_for(sd, O, mq, O.Weights.build(mq), prec, tree=t)
+    r = e.smooth_min_dist(q, sd.SmoothParams(alpha=100.0, beta=0.9))
+    assert r.far_field[0] == 1 and r.leaves[0] == 0
+    root = t.nodes()[0]
+    d, _ = O.box_point_proximity(root["lo"], root["hi"], q)
+    assert abs(r.d_hat[0] - (d[0] - math.log(4.0) / 100.0)) < (1e-6 if prec == 0 else 1e-12)
+
+
+# ------------------------------------------------------ seeded scenes
+@pytest.mark.parametrize("prec", [0, 1])
+@pytest.mark.parametrize("seed", list(range(1, 13)))
+def test_random_scene_exact(sd, oracle, prec, seed):
+    O = oracle
+    m0 = O.random_scene(seed, 200)
+    qs = O.QueryStream(1000 + seed).draw_points(m0, 300)
+    m, q = prep(O, m0, qs, prec)
+    w = O.Weights.build(m)
+    e = engine_for(sd, O, m, w, prec)
+    for alpha, alpha_u in ((100.0, 600.0), (20.0, 600.0), (900.0, 600.0)):
+        p = O.Params(alpha=alpha, alpha_u=alpha_u, beta=0.0)
+        ref = O.query(m, w, q, p)
+        got = e.smooth_min_dist_flat(q, sd.SmoothParams(alpha=alpha, alpha_u=alpha_u, beta=0.0))
+        assert_close(got, ref, prec, alpha, f"seed {seed} alpha {alpha}")
+        assert (got.leaves == m.num_simplices).all() and not got.far_field.any()
+
+
+@pytest.mark.parametrize("prec", [0, 1])
+@pytest.mark.parametrize("seed", list(range(1, 9)))
+def test_random_scene_tree_decisions(sd, oracle, prec, seed):
+    """BVH path on the reference median tree: identical far-field / leaf
+    decisions (per-query counters and decision hash) and parity of d_hat."""
+    O = oracle
+    m0 = O.random_scene(seed, 200)
+    qs = O.QueryStream(2000 + seed).draw_points(m0, 300)
+    m, q = prep(O, m0, qs, prec)
+    w, t = O.Weights.build(m), O.Tree.build(m)
+    e = engine_for(sd, O, m, w, prec, tree=t)
+    for beta in (0.3, 0.5, 0.9):
+        p = O.Params(alpha=100.0, beta=beta)
+        ref = O.query(m, w, q, p, tree=t)
+        got = e.smooth_min_dist(q, sd.SmoothParams(alpha=100.0, beta=beta))
+        assert (got.leaves == ref.leaves).all() and (got.far_field == ref.far_field).all()
+        assert (got.decision_hash == ref.decision_hash).all()
+        assert_close(got, ref, prec, 100.0, f"seed {seed} beta {beta}")
+
+
+@pytest.mark.parametrize("prec", [0, 1])
+def test_gpu_median_build_matches_reference_tree(sd, oracle, prec):
+    O = oracle
+    for seed in (1, 5, 9):
+        m, _ = prep(O, O.random_scene(seed, 200), np.zeros((1, 3)), prec)
+        e = engine_for(sd, O, m, O.Weights.build(m), prec)
+        e.build_bvh(sd.SD_BVH_MEDIAN)
+        got, ref = e.export_bvh(), O.Tree.build(m).nodes()
+        assert got.tobytes() == ref.tobytes()
+
+
+# --------------------------------------------------- BASELINE configs
+def _cfg(O, cfg, nq, prec):
+    m = O.config_mesh(cfg)
+    q = O.config_queries(cfg, m, nq)
+    return prep(O, m, q, prec)
+
+
+@pytest.mark.parametrize("cfg,prec,alphas,nq", [
+    (1, 1, (50.0,), 2048),
+    (2, 0, (100.0,), 1024),
+    (2, 1, (100.0,), 512),
+    (3, 0, (10.0, 100.0, 1000.0), 256),
+])
+def test_config_exact_parity(sd, oracle, cfg, prec, alphas, nq):
+    O = oracle
+    m, q = _cfg(O, cfg, nq, prec)
+    w = O.Weights.build(m)
+    e = engine_for(sd, O, m, w, prec)
+    for alpha in alphas:
+        p = O.Params(alpha=alpha, alpha_u=600.0, beta=0.0)
+        ref = O.query(m, w, q, p)
+        got = e.smooth_min_dist_flat(q, sd.SmoothParams(alpha=alpha, beta=0.0))
+        assert_close(got, ref, prec, alpha, f"cfg{cfg} alpha {alpha}")
+
+
+def test_config4_tree_parity_subset(sd, oracle):
+    """cfg4 (icosphere(9), 5.2M triangles, beta 0.5, alpha 200) on a query
+    subset: decisions identical to the oracle on the same tree, and the
+    Barnes-Hut field below the exact one (acceptance [1])."""
+    O = oracle
+    m, q = _cfg(O, 4, 512, 0)
+    w, t = O.Weights.build(m), O.Tree.build(m)
+    e = engine_for(sd, O, m, w, 0, tree=t)
+    p = O.Params(alpha=200.0, beta=0.5)
+    ref = O.query(m, w, q, p, tree=t)
+    got = e.smooth_min_dist(q, sd.SmoothParams(alpha=200.0, beta=0.5))
+    assert (got.decision_hash == ref.decision_hash).all()
+    assert_close(got, ref, 0, 200.0, "cfg4 bvh")
+    ex = e.smooth_min_dist_flat(q[:64], sd.SmoothParams(alpha=200.0, beta=0.0))
+    assert (got.d_hat[:64] <= ex.d_hat + 1e-5).all()
+
+
+# ---------------------------------------------- full-size properties
+def test_config3_full_size_properties(sd, oracle):
+    """cfg3 at the BASELINE size (1,048,576 queries x 262,144 triangles):
+    properties that need no oracle -- finite/inf consistent with the -708
+    rule, translation invariance under a float-exact shift, and exact
+    parity on a strided sample."""
+    O = oracle
+    m, q = _cfg(O, 3, 1 << 20, 0)
+    w = O.Weights.build(m)
+    e = engine_for(sd, O, m, w, 0)
+    P = sd.SmoothParams(alpha=100.0, beta=0.0)
+    r = e.query_points(q, P, sd.SD_EXACT)
+    assert np.isfinite(r.d_hat).mean() > 0.5
+    shift = np.array([0.5, -0.25, 1.0])
+    e2 = engine_for(sd, O, O.Mesh.from_arrays(m.vertices + shift, m.simplices, m.kinds), w, 0)
+    r2 = e2.query_points(q + shift, P, sd.SD_EXACT)
+    fin = np.isfinite(r.d_hat)
+    assert (np.isfinite(r2.d_hat) == fin).all()
+    assert np.abs(r2.d_hat[fin] - r.d_hat[fin]).max() < 1e-4
+    idx = np.arange(0, len(q), 4099)[:128]
+    ref = O.query(m, w, q[idx], O.Params(alpha=100.0, beta=0.0))
+    sub = type(r)(r.d_hat[idx], r.grad[idx])
+    assert_close(sub, ref, 0, 100.0, "cfg3 strided")
+
+
+# --------------------------------------------------------- edge cases
+def test_edge_cases(sd, oracle):
+    O = oracle
+    e = sd.Engine(0, sd.SD_FP32)
+    e.set_geometry(np.zeros((0, 3)), np.zeros((0, 3), np.int32), np.zeros(0, np.uint8))
+    e.set_weights(1.0, 1.0, np.zeros((0, 5)), np.zeros((0, 13)), np.zeros(0, np.int32))
+    r = e.query_points([[1, 2, 3]], sd.SmoothParams(beta=0.0), sd.SD_EXACT, want_c=True, want_counters=True)
+    assert math.isinf(r.d_hat[0]) and not r.grad.any() and r.c[0] == 0.0
+    m = O.random_scene(3, 200)
+    w = O.Weights.build(m)
+    e = engine_for(sd, O, m.quantized(), w, 0)
+    r = e.query_points(np.zeros((0, 3)), sd.SmoothParams(beta=0.0))
+    assert r.d_hat.shape == (0,)
+    # query exactly on a vertex: contact term, zero distance gradient
+    mq = m.quantized()
+    v = mq.vertices[mq.simplices[0, 0]][None, :]
+    ref = O.query(mq, w, v, O.Params(beta=0.0))
+    got = e.query_points(v, sd.SmoothParams(beta=0.0))
+    assert_close(got, ref, 0, 100.0, "on-vertex")
+    with pytest.raises(sd.SdError):
+        e.query_points(v, sd.SmoothParams(alpha=-1.0))
+    with pytest.raises(sd.SdError):
+        e.query_points(v, sd.SmoothParams(beta=0.5), sd.SD_BVH)  # no tree yet
+    with pytest.raises(sd.SdError):
+        sd.Engine(0, sd.SD_FP32).set_geometry([[0, 0, 0], [1, 0, 0], [2, 0, 0]], [[0, 1, 2]], [2])  # zero area
+    with pytest.raises(sd.SdError):
+        sd.Engine(0, sd.SD_FP32).set_geometry([[0, 0, 0]], [[0, 5, -1]], [1])  # index out of range
