@@ -117,7 +117,6 @@ Phys<T> make_phys(const Ctx& c, const sd_params& p) {
     ph.A = T(c.A);
     ph.lw_unit = T(S * std::log2(std::max(c.A, 1e-300)));
     ph.lw_floor = T(S * std::log2(1e-300));
-    ph.kgrad = T(S * c.A / (p.alpha * p.alpha));
     ph.w_ff = T(std::pow(std::max(c.A * c.sup_wtilde, 1e-300), S));  // weights.hpp:576-578
     ph.beta = T(p.beta);
     return ph;
@@ -125,46 +124,88 @@ Phys<T> make_phys(const Ctx& c, const sd_params& p) {
 template Phys<float> make_phys<float>(const Ctx&, const sd_params&);
 template Phys<double> make_phys<double>(const Ctx&, const sd_params&);
 
-// coefficient packing documented in pair.cuh (Poly)
-template <class T>
-Poly<T> make_poly(const Ctx& c, int kind, int poly) {
-    Poly<T> out;
-    for (int i = 0; i < kPolyCoefs; ++i) out.c[i] = T(0);
-    if (poly < 0) return out;
-    if (kind == SD_EDGE) {
-        const double* a = &c.edge_a[5 * size_t(poly)];
-        for (int i = 0; i < 5; ++i) out.c[i] = T(a[i]);
-        out.c[5] = T(a[1]);
-        out.c[6] = T(2 * a[2]);
-        out.c[7] = T(3 * a[3]);
-        out.c[8] = T(4 * a[4]);
-        return out;
-    }
-    // expand the 13 stored slots to the symmetric grid (weights.hpp:155-161)
+// Expands the 13 stored slots to the symmetric 8x8 grid (weights.hpp:155-161).
+static void tri_grid(const Ctx& c, int poly, double g[8][8]) {
     static const int kStored[13][2] = {{0, 0}, {0, 2}, {0, 3}, {0, 4}, {0, 5}, {0, 6}, {0, 7},
                                        {2, 2}, {2, 3}, {2, 4}, {2, 5}, {3, 3}, {3, 4}};
-    double g[8][8] = {};
+    for (int j = 0; j < 8; ++j)
+        for (int k = 0; k < 8; ++k) g[j][k] = 0.0;
     const double* st = &c.tri_stored[13 * size_t(poly)];
     for (int m = 0; m < 13; ++m) {
         g[kStored[m][0]][kStored[m][1]] = st[m];
         g[kStored[m][1]][kStored[m][0]] = st[m];
     }
+}
+
+static double binom(int n, int k) {
+    double r = 1.0;
+    for (int i = 0; i < k; ++i) r = r * (n - i) / (i + 1);
+    return r;
+}
+
+// True when A w~ > 0 is certified on the whole domain by the Bernstein
+// coefficients (the minimum Bernstein coefficient bounds the polynomial
+// from below), so the kernels may drop the 1e-300 floor selects.
+bool poly_certified_positive(const Ctx& c, int kind, int poly) {
+    if (poly < 0) return true;
+    double lo = INFINITY;
+    if (kind == SD_EDGE) {  // degree-4 Bernstein on [0, 1]
+        const double* a = &c.edge_a[5 * size_t(poly)];
+        for (int i = 0; i <= 4; ++i) {
+            double b = 0.0;
+            for (int j = 0; j <= i; ++j) b += binom(i, j) / binom(4, j) * a[j];
+            lo = std::min(lo, b);
+        }
+    } else {  // degree-7 Bernstein on the triangle
+        double g[8][8];
+        tri_grid(c, poly, g);
+        for (int a = 0; a <= 7; ++a)
+            for (int b = 0; a + b <= 7; ++b) {
+                double s = 0.0;
+                for (int j = 0; j <= a; ++j)
+                    for (int k = 0; k <= b; ++k)
+                        s += g[j][k] * binom(a, j) * binom(b, k) / (binom(7, j + k) * binom(j + k, j));
+                lo = std::min(lo, s);
+            }
+    }
+    return c.A * lo > 1e-6;
+}
+
+// Coefficient packing and pre-scaling documented in pair.cuh (Poly).
+template <class T>
+Poly<T> make_poly(const Ctx& c, int kind, int poly, const sd_params& p) {
+    Poly<T> out;
+    for (int i = 0; i < kPolyCoefs; ++i) out.c[i] = T(0);
+    if (poly < 0) return out;
+    const double S = p.alpha / std::max(p.alpha, p.alpha_u);
+    const double A = c.A, K = S * c.A / (p.alpha * p.alpha);
+    if (kind == SD_EDGE) {
+        const double* a = &c.edge_a[5 * size_t(poly)];
+        for (int i = 0; i < 5; ++i) out.c[i] = T(A * a[i]);
+        out.c[5] = T(K * a[1]);
+        out.c[6] = T(K * 2 * a[2]);
+        out.c[7] = T(K * 3 * a[3]);
+        out.c[8] = T(K * 4 * a[4]);
+        return out;
+    }
+    double g[8][8];
+    tri_grid(c, poly, g);
     int n = 0;
     const int rows[7] = {0, 2, 3, 4, 5, 6, 7};
     for (int j : rows)  // value rows
         for (int k = 0; j + k <= 7; ++k)
-            if (k != 1) out.c[n++] = T(g[j][k]);
+            if (k != 1) out.c[n++] = T(A * g[j][k]);
     for (int j : rows)  // d/dx rows, j >= 2
         if (j >= 2)
             for (int k = 0; j + k <= 7; ++k)
-                if (k != 1) out.c[n++] = T(j * g[j][k]);
+                if (k != 1) out.c[n++] = T(K * j * g[j][k]);
     for (int j : rows)  // d/dy rows, k >= 2
-        for (int k = 2; j + k <= 7; ++k) out.c[n++] = T(k * g[j][k]);
+        for (int k = 2; j + k <= 7; ++k) out.c[n++] = T(K * k * g[j][k]);
     if (n != kPolyCoefs) throw std::logic_error("triangle polynomial packing");
     return out;
 }
-template Poly<float> make_poly<float>(const Ctx&, int, int);
-template Poly<double> make_poly<double>(const Ctx&, int, int);
+template Poly<float> make_poly<float>(const Ctx&, int, int, const sd_params&);
+template Poly<double> make_poly<double>(const Ctx&, int, int, const sd_params&);
 
 // --------------------------------------------------------- exact layout
 template <class T>
@@ -210,10 +251,12 @@ static void exact_query(Ctx& c, const T* q, int64_t Q, const sd_params& p, const
         return;
     }
     // splits: enough CTAs for several waves over 148 SMs even for small Q
-    const int64_t qpc = exact_queries_per_cta(0);
-    const int64_t qblocks = (Q + qpc - 1) / qpc;
     int64_t maxcount = 0;
-    for (const Segment& s : c.segs) maxcount = std::max(maxcount, s.count);
+    int bigkind = 0;
+    for (const Segment& s : c.segs)
+        if (s.count > maxcount) maxcount = s.count, bigkind = s.kind;
+    const int64_t qpc = exact_queries_per_cta(bigkind);
+    const int64_t qblocks = (Q + qpc - 1) / qpc;
     const int64_t target = 148 * 8;
     int64_t splits = std::max<int64_t>(1, (target + qblocks - 1) / qblocks);
     splits = std::min<int64_t>(splits, std::max<int64_t>(1, maxcount / 512));
@@ -226,6 +269,7 @@ static void exact_query(Ctx& c, const T* q, int64_t Q, const sd_params& p, const
         ExactLaunch<T> L;
         L.kind = s.kind;
         L.has_poly = s.poly >= 0;
+        L.safe = poly_certified_positive(c, s.kind, s.poly);
         L.rec = c.rec[s.kind].as<T>() + s.offset * rec_size(s.kind);
         L.count = s.count;
         L.splits = int(splits);
@@ -235,7 +279,7 @@ static void exact_query(Ctx& c, const T* q, int64_t Q, const sd_params& p, const
         L.part = part;
         L.first = first ? 1 : 0;
         L.ph = ph;
-        L.poly = make_poly<T>(c, s.kind, s.poly);
+        L.poly = make_poly<T>(c, s.kind, s.poly, p);
         check_cuda(launch_exact<T>(L, st), "exact kernel launch");
         ++launches;
         first = false;

@@ -281,6 +281,30 @@ struct TraverseArgs {
 
 constexpr int kTravThreads = 128;
 
+// Far-field term of a whole subtree (smooth.hpp:67-75): n_B w_ff collapsed
+// onto the box's closest point; gradient (q - y_B) / d_B.
+template <class T>
+__device__ __forceinline__ void far_term(const Phys<T>& ph, int32_t count, T d, T r, T dx, T dy, T dz, Acc<T>& acc) {
+    const T lw = Math<T>::lg2(T(count) * ph.w_ff);
+    const T xm = bump(acc, masked(ph, d, fma(ph.kappa, d, lw - acc.m)), [&] { return fma(ph.kappa, d, lw); });
+    const T e = Math<T>::ex2(xm);
+    const T er = e * r;
+    acc.s += e;
+    acc.gx = fma(er, dx, acc.gx);
+    acc.gy = fma(er, dy, acc.gy);
+    acc.gz = fma(er, dz, acc.gz);
+}
+
+// Unit-weight edge / triangle leaf (poly_index < 0): w = A^S.
+template <class T, int KIND>
+__device__ __forceinline__ void unit_term(const Phys<T>& ph, const Poly<T>& pc, T qx, T qy, T qz, const T* rec,
+                                          Acc<T>& acc) {
+    acc.m -= ph.lw_unit;
+    if constexpr (KIND == 1) edge_term<T, false, false>(ph, pc, qx, qy, qz, rec, acc);
+    else tri_term<T, false, false>(ph, pc, qx, qy, qz, rec, acc);
+    acc.m += ph.lw_unit;
+}
+
 // Reference-rounded fp64 decision (bvh.hpp:105-111,185-187).
 template <class T>
 __device__ __forceinline__ bool decide64(const NodeT<T>& b, double d64, double qx, double qy, double qz,
@@ -339,17 +363,12 @@ __global__ void __launch_bounds__(kTravThreads) traverse_kernel(const __grid_con
                     far = decide64(b, a.diam64[id], double(qx), double(qy), double(qz), a.beta64);
                     ++nre;
                 }
-                if (far) {
-                    const T lw = Math<T>::lg2(T(a.count[id]) * a.ph.w_ff);
-                    acc.add(masked_exponent(a.ph, d, lw), dx * r, dy * r, dz * r);
-                }
+                if (far) far_term(a.ph, a.count[id], d, r, dx, dy, dz, acc);
             } else {
                 far = decide64(b, a.diam64[id], double(qx), double(qy), double(qz), a.beta64);
                 if (far) {
                     const T d = sqrt(s);
-                    const T r = T(1) / d;
-                    const T lw = Math<T>::lg2(T(a.count[id]) * a.ph.w_ff);
-                    acc.add(masked_exponent(a.ph, d, lw), dx * r, dy * r, dz * r);
+                    far_term(a.ph, a.count[id], d, T(1) / d, dx, dy, dz, acc);
                 }
             }
             if (far) {
@@ -369,17 +388,19 @@ __global__ void __launch_bounds__(kTravThreads) traverse_kernel(const __grid_con
             const V* src = reinterpret_cast<const V*>(a.leafrec + size_t(slot) * kRecTri);
             if (kind == 0) {
                 reinterpret_cast<V*>(rec)[0] = src[0];
+                acc.m -= a.ph.lw_unit;  // unit-weight terms take the shift relative to S log2 A
                 point_term(a.ph, qx, qy, qz, rec[0], rec[1], rec[2], acc);
+                acc.m += a.ph.lw_unit;
             } else if (kind == 1) {
 #pragma unroll
                 for (int j = 0; j < kRecEdge * int(sizeof(T)) / int(sizeof(V)); ++j) reinterpret_cast<V*>(rec)[j] = src[j];
-                if (poly >= 0) edge_term<T, true>(a.ph, polys[poly], qx, qy, qz, rec, acc);
-                else edge_term<T, false>(a.ph, polys[0], qx, qy, qz, rec, acc);
+                if (poly >= 0) edge_term<T, true, false>(a.ph, polys[poly], qx, qy, qz, rec, acc);
+                else unit_term<T, 1>(a.ph, polys[0], qx, qy, qz, rec, acc);
             } else {
 #pragma unroll
                 for (int j = 0; j < kRecTri * int(sizeof(T)) / int(sizeof(V)); ++j) reinterpret_cast<V*>(rec)[j] = src[j];
-                if (poly >= 0) tri_term<T, true>(a.ph, polys[a.ne + poly], qx, qy, qz, rec, acc);
-                else tri_term<T, false>(a.ph, polys[0], qx, qy, qz, rec, acc);
+                if (poly >= 0) tri_term<T, true, false>(a.ph, polys[a.ne + poly], qx, qy, qz, rec, acc);
+                else unit_term<T, 2>(a.ph, polys[0], qx, qy, qz, rec, acc);
             }
             ++nleaf;
             h += decision_mix(uint64_t(id), 2);
@@ -429,8 +450,8 @@ void tree_query(Ctx& c, const T* q, int64_t Q, const sd_params& p, const Finaliz
     const int ne = int(c.edge_a.size() / 5), nt = int(c.tri_stored.size() / 13);
     const int npoly = std::max(1, ne + nt);
     std::vector<Poly<T>> ptab(npoly);
-    for (int e = 0; e < ne; ++e) ptab[e] = make_poly<T>(c, SD_EDGE, e);
-    for (int k = 0; k < nt; ++k) ptab[ne + k] = make_poly<T>(c, SD_TRIANGLE, k);
+    for (int e = 0; e < ne; ++e) ptab[e] = make_poly<T>(c, SD_EDGE, e, p);
+    for (int k = 0; k < nt; ++k) ptab[ne + k] = make_poly<T>(c, SD_TRIANGLE, k, p);
     Poly<T>* dpoly = static_cast<Poly<T>*>(c.polys.ensure(ptab.size() * sizeof(Poly<T>)));
     check_cuda(cudaMemcpyAsync(dpoly, ptab.data(), ptab.size() * sizeof(Poly<T>), cudaMemcpyHostToDevice, st),
                "upload polys");

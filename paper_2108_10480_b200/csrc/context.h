@@ -112,7 +112,8 @@ struct Ctx {
 template <class T>
 Phys<T> make_phys(const Ctx& c, const sd_params& p);
 template <class T>
-Poly<T> make_poly(const Ctx& c, int kind, int poly);
+Poly<T> make_poly(const Ctx& c, int kind, int poly, const sd_params& p);
+bool poly_certified_positive(const Ctx& c, int kind, int poly);
 template <class T>
 void build_record(const Ctx& c, int64_t prim, T* out);  // rec_size(kind) values
 

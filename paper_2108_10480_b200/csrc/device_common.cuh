@@ -34,14 +34,12 @@ template <> struct Math<float> {
         asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
         return y;
     }
-    static constexpr float kMinusHuge = -1e30f;  // "no term yet" log2 shift
 };
 template <> struct Math<double> {
     static __device__ __forceinline__ double ex2(double x) { return exp2(x); }
     static __device__ __forceinline__ double lg2(double x) { return log2(x); }
     static __device__ __forceinline__ double rsqrt(double x) { return ::rsqrt(x); }
     static __device__ __forceinline__ double rcp(double x) { return 1.0 / x; }
-    static constexpr double kMinusHuge = -1e300;
 };
 
 // Vector types used to read records out of shared memory (16 B loads).
@@ -55,33 +53,19 @@ template <> struct Vec4<double> { using type = double2; };
 // (smooth.hpp:51-61, 79-93), kept as
 //   c = s * 2^m,  grad_c = g * 2^m
 // with the exponent x_i = log2(w_i exp(-alpha d_i)). The shift m is raised
-// lazily (only when a term exceeds it), by kHeadroom extra so that a
-// slowly rising sequence does not rescale at every record; terms never
-// exceed 2^0 relative to the shift, so nothing can overflow, and only terms
-// below 2^-(126 - kHeadroom) of the running maximum flush (fp32).
+// lazily (bump() in pair.cuh: only when a term exceeds it), by kHeadroom
+// extra so that a slowly rising sequence does not rescale at every record;
+// terms never exceed 2^0 relative to the shift, so nothing can overflow,
+// and only terms below 2^-(126 - kHeadroom) of the running maximum flush
+// (fp32).
 constexpr float kHeadroom = 16.0f;
 
 template <class T>
 struct Acc {
     T m, s, gx, gy, gz;
     __device__ __forceinline__ void init() {
-        m = Math<T>::kMinusHuge;
+        m = T(-INFINITY);  // no term yet
         s = gx = gy = gz = T(0);
-    }
-    // x: log2 exponent of the term (may be -inf for a masked term);
-    // (hx, hy, hz): gradient coefficient divided by the weight
-    __device__ __forceinline__ void add(T x, T hx, T hy, T hz) {
-        if (x > m) {  // rare after the first few records: divergent but cheap
-            const T mn = x + T(kHeadroom);
-            const T sc = Math<T>::ex2(m - mn);
-            s *= sc; gx *= sc; gy *= sc; gz *= sc;
-            m = mn;
-        }
-        const T e = Math<T>::ex2(x - m);
-        s += e;
-        gx = fma(e, hx, gx);
-        gy = fma(e, hy, gy);
-        gz = fma(e, hz, gz);
     }
 };
 

@@ -22,7 +22,7 @@ __global__ void finalize_kernel(const T* __restrict__ part, int splits, int64_t 
     double M = -INFINITY;
     for (int k = 0; k < splits; ++k) M = fmax(M, double(part[size_t(k) * 5 * Q + i]));
     double s = 0, gx = 0, gy = 0, gz = 0;
-    for (int k = 0; k < splits; ++k) {
+    for (int k = 0; k < splits && M > -INFINITY; ++k) {
         const T* p = part + size_t(k) * 5 * Q;
         const double f = exp2(double(p[i]) - M);
         s = fma(double(p[Q + i]), f, s);
@@ -30,7 +30,7 @@ __global__ void finalize_kernel(const T* __restrict__ part, int splits, int64_t 
         gy = fma(double(p[3 * Q + i]), f, gy);
         gz = fma(double(p[4 * Q + i]), f, gz);
     }
-    const double scale = exp2(M);
+    const double scale = M > -INFINITY ? exp2(M) : 0.0;
     const double c = s * scale;
     const double cx = gx * scale, cy = gy * scale, cz = gz * scale;
     const int64_t j = perm ? perm[i] : i;  // tree path: undo the query sort

@@ -40,7 +40,7 @@ constexpr int tile_prims() {
     return KIND == 0 ? 768 : (KIND == 1 ? 256 : 128);
 }
 
-template <class T, int KIND, bool POLY, int QPT>
+template <class T, int KIND, bool POLY, bool SAFE, int QPT>
 __global__ void __launch_bounds__(kThreads) exact_kernel(const __grid_constant__ ExactArgs<T> a) {
     constexpr int R = rec_size(KIND);
     constexpr int TILE = tile_prims<T, KIND>();
@@ -91,6 +91,8 @@ __global__ void __launch_bounds__(kThreads) exact_kernel(const __grid_constant__
             acc[k].gy = part[3 * a.Q + qc];
             acc[k].gz = part[4 * a.Q + qc];
         }
+        // unit-weight launches keep the shift relative to log2 w = S log2 A
+        if constexpr (!POLY) acc[k].m -= a.ph.lw_unit;
     }
 
     for (int t = 0; t < ntiles; ++t) {
@@ -109,8 +111,8 @@ __global__ void __launch_bounds__(kThreads) exact_kernel(const __grid_constant__
 #pragma unroll
             for (int k = 0; k < QPT; ++k) {
                 if constexpr (KIND == 0) point_term(a.ph, qx[k], qy[k], qz[k], rec[0], rec[1], rec[2], acc[k]);
-                else if constexpr (KIND == 1) edge_term<T, POLY>(a.ph, a.poly, qx[k], qy[k], qz[k], rec, acc[k]);
-                else tri_term<T, POLY>(a.ph, a.poly, qx[k], qy[k], qz[k], rec, acc[k]);
+                else if constexpr (KIND == 1) edge_term<T, POLY, SAFE>(a.ph, a.poly, qx[k], qy[k], qz[k], rec, acc[k]);
+                else tri_term<T, POLY, SAFE>(a.ph, a.poly, qx[k], qy[k], qz[k], rec, acc[k]);
             }
         }
         __syncthreads();  // every thread is done with stage s
@@ -120,6 +122,7 @@ __global__ void __launch_bounds__(kThreads) exact_kernel(const __grid_constant__
 #pragma unroll
     for (int k = 0; k < QPT; ++k) {
         if (qi[k] >= a.Q) continue;
+        if constexpr (!POLY) acc[k].m += a.ph.lw_unit;
         part[qi[k]] = acc[k].m;
         part[a.Q + qi[k]] = acc[k].s;
         part[2 * a.Q + qi[k]] = acc[k].gx;
@@ -128,12 +131,18 @@ __global__ void __launch_bounds__(kThreads) exact_kernel(const __grid_constant__
     }
 }
 
-template <class T, int KIND, bool POLY, int QPT>
+template <int KIND>
+constexpr int qpt_for() {
+    return KIND == 2 ? 2 : 4;  // queries per thread: amortise record loads
+}
+
+template <class T, int KIND, bool POLY, bool SAFE>
 static cudaError_t launch_one(const ExactLaunch<T>& L, cudaStream_t st) {
     constexpr int R = rec_size(KIND);
     constexpr int TILE = tile_prims<T, KIND>();
+    constexpr int QPT = qpt_for<KIND>();
     const size_t smem = size_t(kStages) * TILE * R * sizeof(T);
-    auto kern = exact_kernel<T, KIND, POLY, QPT>;
+    auto kern = exact_kernel<T, KIND, POLY, SAFE, QPT>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
     ExactArgs<T> a;
@@ -152,18 +161,20 @@ static cudaError_t launch_one(const ExactLaunch<T>& L, cudaStream_t st) {
     return cudaGetLastError();
 }
 
-int64_t exact_queries_per_cta(int kind) { return int64_t(kThreads) * 2; }
+int64_t exact_queries_per_cta(int kind) {
+    return int64_t(kThreads) * (kind == 2 ? qpt_for<2>() : qpt_for<1>());
+}
 
 template <class T>
 cudaError_t launch_exact(const ExactLaunch<T>& L, cudaStream_t st) {
-    constexpr int QPT = 2;
-    switch (L.kind * 2 + (L.has_poly ? 1 : 0)) {
-        case 0:
-        case 1: return launch_one<T, 0, false, QPT>(L, st);
-        case 2: return launch_one<T, 1, false, QPT>(L, st);
-        case 3: return launch_one<T, 1, true, QPT>(L, st);
-        case 4: return launch_one<T, 2, false, QPT>(L, st);
-        case 5: return launch_one<T, 2, true, QPT>(L, st);
+    if (L.kind == 0) return launch_one<T, 0, false, false>(L, st);
+    if (L.kind == 1) {
+        if (!L.has_poly) return launch_one<T, 1, false, false>(L, st);
+        return L.safe ? launch_one<T, 1, true, true>(L, st) : launch_one<T, 1, true, false>(L, st);
+    }
+    if (L.kind == 2) {
+        if (!L.has_poly) return launch_one<T, 2, false, false>(L, st);
+        return L.safe ? launch_one<T, 2, true, true>(L, st) : launch_one<T, 2, true, false>(L, st);
     }
     return cudaErrorInvalidValue;
 }

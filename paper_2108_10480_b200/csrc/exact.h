@@ -13,6 +13,7 @@ template <class T>
 struct ExactLaunch {
     int kind = 0;          // SD_POINT / SD_EDGE / SD_TRIANGLE
     bool has_poly = false; // false: unit weight (w = A^S)
+    bool safe = false;     // polynomial certified positive: no 1e-300 floor selects
     const T* rec = nullptr;
     int64_t count = 0;     // primitives in the segment
     int64_t chunk = 0;     // primitives per split

@@ -10,8 +10,16 @@
 //   term                 smooth.hpp:51-61 (arg = -alpha d, coef = w,
 //                        gcoef = w grad d - grad w / alpha)
 //   underflow mask       smooth.hpp:85-88 (terms with -alpha d < -708 are 0)
-// Each term is handed to Acc::add as x = log2(w) + log2(e) * (-alpha d) and
-// h = gcoef / w = grad d - (S A / (alpha^2 base)) * (dw~ . shape gradients).
+//
+// Every term enters the accumulator as
+//   e      = 2^(x - m),   x = log2(w) + log2(e) (-alpha d)  (masked: e = 0)
+//   s     += e
+//   g     += (e r) delta - (e k) (shape-gradient combination)
+// with r = 1/d, delta = q - closest point, and k = S A / (alpha^2 base),
+// base = A w~ (so that e k dw~ is exp(-alpha d) dw / alpha^2 scaled).
+// The host pre-scales the polynomial coefficients: the value rows by A
+// (they evaluate base = A w~ directly) and the derivative rows by
+// S A / alpha^2 (they evaluate the numerator of k).
 #pragma once
 
 #include "device_common.cuh"
@@ -26,49 +34,101 @@ struct Phys {
     T A;         // WeightSet::A
     T lw_unit;   // S log2(A): log2 weight of unit-weight primitives
     T lw_floor;  // S log2(1e-300): floored weight (weights.hpp:657-661)
-    T kgrad;     // S A / alpha^2
     T w_ff;      // (A sup w~)^S, far-field weight (weights.hpp:576-578)
     T beta;      // Barnes-Hut threshold
 };
 
-// Polynomial coefficients of one weight polynomial, in evaluation order.
-//   edge: [0..4]=a0..a4 [5]=a1 [6]=2a2 [7]=3a3 [8]=4a4  (a1 is 0 for every
-//         polynomial build_edge_weight makes, but tables may carry any a1)
+// Polynomial coefficients of one weight polynomial, in evaluation order,
+// pre-scaled as described above (value rows x A, derivative rows x S A / alpha^2).
+//   edge: [0..4] = A a0..a4; [5..8] = K (a1, 2 a2, 3 a3, 4 a4)
 //   tri : [0..22]  value rows  j=0:k{0,2..7} j=2:k{0,2..5} j=3:k{0,2..4}
-//                  j=4:k{0,2,3} j=5:k{0,2} j=6:k{0} j=7:k{0}
-//         [23..38] d/dx rows (j c_jk)  j=2..7 with the same k sets
+//                  j=4:k{0,2,3} j=5:k{0,2} j=6:k{0} j=7:k{0}      (x A)
+//         [23..38] d/dx rows (j c_jk)  j=2..7 with the same k sets (x K)
 //         [39..54] d/dy rows (k c_jk)  j=0:k{2..7} j=2:k{2..5} j=3:k{2..4}
-//                  j=4:k{2,3} j=5:k{2}
-// c_{1k} = c_{j1} = 0 exactly (weights.hpp:113-131), so rows skip k = 1.
+//                  j=4:k{2,3} j=5:k{2}                               (x K)
+// with K = S A / alpha^2; c_{1k} = c_{j1} = 0 exactly (weights.hpp:113-131).
 constexpr int kPolyCoefs = 55;
 template <class T>
 struct Poly {
     T c[kPolyCoefs];
 };
 
+// Smallest positive argument handed to rsqrt: keeps 0 * rsqrt finite at
+// contact (distance 0 -> gradient 0, exact.hpp:62) without a select.
+template <class T> struct Tiny;
+template <> struct Tiny<float> { static constexpr float v = 1e-30f; };
+template <> struct Tiny<double> { static constexpr double v = 1e-300; };
+
+// ------------------------------------------------------- accumulator
+// xm = x - m of a term (-inf when masked). When the term exceeds the shift
+// (rare after the first records), the shift is re-anchored on the term's
+// absolute exponent x, recomputed by `absx` from registers, so that the
+// stored m and every later x - m are formed from the same rounded values
+// (an uninitialised shift is -inf: its sums scale by 2^-inf = 0).
+template <class T, class F>
+__device__ __forceinline__ T bump(Acc<T>& acc, T xm, F&& absx) {
+    if (xm > T(0)) {
+        const T x = absx();
+        const T mn = x + T(kHeadroom);
+        const T sc = Math<T>::ex2(acc.m - mn);
+        acc.s *= sc; acc.gx *= sc; acc.gy *= sc; acc.gz *= sc;
+        acc.m = mn;
+        xm = x - mn;
+    }
+    return xm;
+}
+
+template <class T>
+__device__ __forceinline__ T masked(const Phys<T>& ph, T d, T xm) {
+    return d > ph.dmax ? T(-INFINITY) : xm;
+}
+
+// Exponent (x - m) and gradient factor k = dnum / base of a polynomial
+// primitive, with the reference floor (base <= 1e-300 -> w = 1e-300^S,
+// dw = 0, weights.hpp:657-661) unless the polynomial is certified positive
+// on its domain (SAFE, see api.cu), where the selects are dropped.
+template <class T, bool SAFE>
+__device__ __forceinline__ T weight_exponent(const Phys<T>& ph, T base, T dnum, T xd, T& k, T& lw) {
+    const T lg = Math<T>::lg2(base);
+    const T ib = Math<T>::rcp(base);
+    if constexpr (SAFE) {
+        k = dnum * ib;
+        lw = ph.S * lg;
+        return fma(ph.S, lg, xd);
+    } else {
+        const bool ok = base > T(sizeof(T) == 4 ? 0.0 : 1e-300);
+        k = ok ? dnum * ib : T(0);
+        lw = ok ? ph.S * lg : ph.lw_floor;
+        return lw + xd;
+    }
+}
+
 template <class T>
 __device__ __forceinline__ T clamp01(T x) {
     return fmin(fmax(x, T(0)), T(1));
 }
 
-template <class T>
-__device__ __forceinline__ T masked_exponent(const Phys<T>& ph, T d, T lw) {
-    return d > ph.dmax ? T(-INFINITY) : fma(ph.kappa, d, lw);
-}
-
 // -------------------------------------------------------------- points
+// acc.m is relative to lw_unit for the whole launch (see exact.cu), so the
+// exponent is one FFMA.
 template <class T>
 __device__ __forceinline__ void point_term(const Phys<T>& ph, T qx, T qy, T qz, T ax, T ay, T az, Acc<T>& acc) {
     const T dx = qx - ax, dy = qy - ay, dz = qz - az;
     const T s = fma(dx, dx, fma(dy, dy, dz * dz));
-    const T r = s > T(0) ? Math<T>::rsqrt(s) : T(0);
+    const T r = Math<T>::rsqrt(fmax(s, Tiny<T>::v));
     const T d = s * r;
-    acc.add(masked_exponent(ph, d, ph.lw_unit), dx * r, dy * r, dz * r);
+    const T xm = bump(acc, masked(ph, d, fma(ph.kappa, d, -acc.m)), [&] { return ph.kappa * d; });
+    const T e = Math<T>::ex2(xm);
+    const T er = e * r;
+    acc.s += e;
+    acc.gx = fma(er, dx, acc.gx);
+    acc.gy = fma(er, dy, acc.gy);
+    acc.gz = fma(er, dz, acc.gz);
 }
 
 // --------------------------------------------------------------- edges
-// rec: a.xyz e.xyz inv_e2 ge.xyz
-template <class T, bool POLY>
+// rec: a.xyz e.xyz inv_e2 ge.xyz (ge = e / |e|^2)
+template <class T, bool POLY, bool SAFE>
 __device__ __forceinline__ void edge_term(const Phys<T>& ph, const Poly<T>& pc, T qx, T qy, T qz, const T* rec,
                                           Acc<T>& acc) {
     const T apx = qx - rec[0], apy = qy - rec[1], apz = qz - rec[2];
@@ -76,22 +136,29 @@ __device__ __forceinline__ void edge_term(const Phys<T>& ph, const Poly<T>& pc, 
     const T t = clamp01(fma(ex, apx, fma(ey, apy, ez * apz)) * rec[6]);
     const T dx = fma(-t, ex, apx), dy = fma(-t, ey, apy), dz = fma(-t, ez, apz);
     const T s = fma(dx, dx, fma(dy, dy, dz * dz));
-    const T r = s > T(0) ? Math<T>::rsqrt(s) : T(0);
+    const T r = Math<T>::rsqrt(fmax(s, Tiny<T>::v));
     const T d = s * r;
-    T hx = dx * r, hy = dy * r, hz = dz * r;
-    T lw = ph.lw_unit;
     if constexpr (POLY) {
-        const T wt = fma(t, fma(t, fma(t, fma(t, pc.c[4], pc.c[3]), pc.c[2]), pc.c[1]), pc.c[0]);
-        const T wd = fma(t, fma(t, fma(t, pc.c[8], pc.c[7]), pc.c[6]), pc.c[5]);
-        const T base = ph.A * wt;
-        const bool ok = base > T(sizeof(T) == 4 ? 0.0 : 1e-300);
-        lw = ok ? ph.S * Math<T>::lg2(base) : ph.lw_floor;
-        const T k = ok ? ph.kgrad * Math<T>::rcp(base) * wd : T(0);
-        hx = fma(-k, rec[7], hx);
-        hy = fma(-k, rec[8], hy);
-        hz = fma(-k, rec[9], hz);
+        const T base = fma(t, fma(t, fma(t, fma(t, pc.c[4], pc.c[3]), pc.c[2]), pc.c[1]), pc.c[0]);
+        const T dnum = fma(t, fma(t, fma(t, pc.c[8], pc.c[7]), pc.c[6]), pc.c[5]);
+        T k, lw;
+        const T xm = bump(acc, masked(ph, d, weight_exponent<T, SAFE>(ph, base, dnum, fma(ph.kappa, d, -acc.m), k, lw)),
+                          [&] { return fma(ph.kappa, d, lw); });
+        const T e = Math<T>::ex2(xm);
+        const T er = e * r, ek = e * k;
+        acc.s += e;
+        acc.gx = fma(-ek, rec[7], fma(er, dx, acc.gx));
+        acc.gy = fma(-ek, rec[8], fma(er, dy, acc.gy));
+        acc.gz = fma(-ek, rec[9], fma(er, dz, acc.gz));
+    } else {
+        const T xm = bump(acc, masked(ph, d, fma(ph.kappa, d, -acc.m)), [&] { return ph.kappa * d; });
+        const T e = Math<T>::ex2(xm);
+        const T er = e * r;
+        acc.s += e;
+        acc.gx = fma(er, dx, acc.gx);
+        acc.gy = fma(er, dy, acc.gy);
+        acc.gz = fma(er, dz, acc.gz);
     }
-    acc.add(masked_exponent(ph, d, lw), hx, hy, hz);
 }
 
 // ----------------------------------------------------------- triangles
@@ -118,7 +185,7 @@ __device__ __forceinline__ void tri_closest(const T* rec, T d1, T d2, T& u, T& v
     if (d1 <= T(0) && d2 <= T(0)) { u = T(0); v = T(0); }                       // vertex a
 }
 
-// w~ and its barycentric gradient for the degree-7 symmetric polynomial.
+// base = A w~ and the K-scaled barycentric gradient of w~ (see Poly).
 template <class T>
 __device__ __forceinline__ void tri_poly(const Poly<T>& p, T x, T y, T& w, T& wx, T& wy) {
     const T* c = p.c;
@@ -148,7 +215,7 @@ __device__ __forceinline__ void tri_poly(const Poly<T>& p, T x, T y, T& w, T& wx
 }
 
 // rec: see device_common.cuh (kRecTri)
-template <class T, bool POLY>
+template <class T, bool POLY, bool SAFE>
 __device__ __forceinline__ void tri_term(const Phys<T>& ph, const Poly<T>& pc, T qx, T qy, T qz, const T* rec,
                                          Acc<T>& acc) {
     const T apx = qx - rec[0], apy = qy - rec[1], apz = qz - rec[2];
@@ -162,23 +229,30 @@ __device__ __forceinline__ void tri_term(const Phys<T>& ph, const Poly<T>& pc, T
     const T dy = fma(-v, acy, fma(-u, aby, apy));
     const T dz = fma(-v, acz, fma(-u, abz, apz));
     const T s = fma(dx, dx, fma(dy, dy, dz * dz));
-    const T r = s > T(0) ? Math<T>::rsqrt(s) : T(0);
+    const T r = Math<T>::rsqrt(fmax(s, Tiny<T>::v));
     const T d = s * r;
-    T hx = dx * r, hy = dy * r, hz = dz * r;
-    T lw = ph.lw_unit;
     if constexpr (POLY) {
-        T wt, wx, wy;
-        tri_poly(pc, u, v, wt, wx, wy);
-        const T base = ph.A * wt;
-        const bool ok = base > T(sizeof(T) == 4 ? 0.0 : 1e-300);
-        lw = ok ? ph.S * Math<T>::lg2(base) : ph.lw_floor;
-        const T k = ok ? ph.kgrad * Math<T>::rcp(base) : T(0);
-        const T kx = k * wx, ky = k * wy;
-        hx = fma(-kx, rec[16], fma(-ky, rec[19], hx));
-        hy = fma(-kx, rec[17], fma(-ky, rec[20], hy));
-        hz = fma(-kx, rec[18], fma(-ky, rec[21], hz));
+        T base, wx, wy;
+        tri_poly(pc, u, v, base, wx, wy);
+        T k, lw;
+        const T xm = bump(acc, masked(ph, d, weight_exponent<T, SAFE>(ph, base, T(1), fma(ph.kappa, d, -acc.m), k, lw)),
+                          [&] { return fma(ph.kappa, d, lw); });
+        const T e = Math<T>::ex2(xm);
+        const T er = e * r, ek = e * k;
+        const T kx = ek * wx, ky = ek * wy;
+        acc.s += e;
+        acc.gx = fma(-ky, rec[19], fma(-kx, rec[16], fma(er, dx, acc.gx)));
+        acc.gy = fma(-ky, rec[20], fma(-kx, rec[17], fma(er, dy, acc.gy)));
+        acc.gz = fma(-ky, rec[21], fma(-kx, rec[18], fma(er, dz, acc.gz)));
+    } else {
+        const T xm = bump(acc, masked(ph, d, fma(ph.kappa, d, -acc.m)), [&] { return ph.kappa * d; });
+        const T e = Math<T>::ex2(xm);
+        const T er = e * r;
+        acc.s += e;
+        acc.gx = fma(er, dx, acc.gx);
+        acc.gy = fma(er, dy, acc.gy);
+        acc.gz = fma(er, dz, acc.gz);
     }
-    acc.add(masked_exponent(ph, d, lw), hx, hy, hz);
 }
 
 }  // namespace sdgpu
