@@ -198,10 +198,17 @@ class Engine:
 
     # -- queries (smooth.hpp:166-198) --
     def query_points(self, q, params: SmoothParams, mode: int = SD_EXACT, *, want_grad=True, want_c=False,
-                     want_counters=False) -> SmoothResults:
-        """Host-buffer batched query: H2D, evaluate, D2H (blocking)."""
+                     want_counters=False, out: SmoothResults | None = None) -> SmoothResults:
+        """Host-buffer batched query: H2D, evaluate, D2H (blocking). `out`
+        may supply preallocated (e.g. pinned) result arrays."""
         q = np.ascontiguousarray(q, np.float64).reshape(-1, 3)
         n = len(q)
+        if out is not None:
+            r = out
+            o = _Outputs(*(None if a is None else a.ctypes.data for a in
+                           (r.d_hat, r.grad, r.c, r.grad_c, r.leaves, r.far_field, r.decision_hash)))
+            _check(lib().sd_query_points(self.h, _ptr(q), n, C.byref(params._c()), mode, C.byref(o)))
+            return r
         r = SmoothResults(np.empty(n))
         if want_grad:
             r.grad = np.empty((n, 3))

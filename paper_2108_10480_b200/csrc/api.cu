@@ -250,18 +250,30 @@ static void exact_query(Ctx& c, const T* q, int64_t Q, const sd_params& p, const
         c.last_launches = 1;
         return;
     }
-    // splits: enough CTAs for several waves over 148 SMs even for small Q
+    // splits of the primitive range: enough CTAs to fill every SM, and a
+    // CTA count close to a whole number of waves (all CTAs do equal work,
+    // so a partial last wave is pure loss)
     int64_t maxcount = 0;
-    int bigkind = 0;
+    const Segment* big = &c.segs[0];
     for (const Segment& s : c.segs)
-        if (s.count > maxcount) maxcount = s.count, bigkind = s.kind;
-    const int64_t qpc = exact_queries_per_cta(bigkind);
+        if (s.count > maxcount) maxcount = s.count, big = &s;
+    const int64_t qpc = exact_queries_per_cta(big->kind);
     const int64_t qblocks = (Q + qpc - 1) / qpc;
-    const int64_t target = 148 * 8;
-    int64_t splits = std::max<int64_t>(1, (target + qblocks - 1) / qblocks);
-    splits = std::min<int64_t>(splits, std::max<int64_t>(1, maxcount / 512));
-    splits = std::min<int64_t>(splits, 64);
-    T* part = static_cast<T*>(c.part.ensure(size_t(splits) * 5 * Q * sizeof(T)));
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device);
+    const int64_t slots = int64_t(sms) * exact_blocks_per_sm<T>(big->kind, big->poly >= 0,
+                                                                  poly_certified_positive(c, big->kind, big->poly));
+    const int64_t max_splits = std::max<int64_t>(1, std::min<int64_t>(64, maxcount / 256));
+    int64_t splits = 1;
+    double best = -1.0;
+    for (int64_t s = 1; s <= max_splits; ++s) {
+        const double waves = double(qblocks * s) / double(slots);
+        const double eff = waves / std::ceil(waves);
+        const double score = eff - (waves < 1.0 ? 1.0 : 0.0) - 0.002 * double(s);  // prefer few splits
+        if (score > best + 1e-9) best = score, splits = s;
+        if (waves >= 1.0 && eff >= 0.97) break;
+    }
+    double* part = static_cast<double*>(c.part.ensure(size_t(splits) * 5 * Q * sizeof(double)));
     const Phys<T> ph = make_phys<T>(c, p);
     int64_t launches = 0;
     bool first = true;
@@ -284,7 +296,7 @@ static void exact_query(Ctx& c, const T* q, int64_t Q, const sd_params& p, const
         ++launches;
         first = false;
     }
-    check_cuda(launch_finalize<T>(part, int(splits), Q, p.alpha, p.epsilon, c.N, nullptr, nullptr, nullptr, nullptr,
+    check_cuda(launch_finalize(part, int(splits), Q, p.alpha, p.epsilon, c.N, nullptr, nullptr, nullptr, nullptr,
                                   out, st),
                "finalize launch");
     c.last_launches = launches + 1;

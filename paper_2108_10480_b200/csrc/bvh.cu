@@ -272,7 +272,7 @@ struct TraverseArgs {
     int stack_depth;
     double beta64;
     Phys<T> ph;
-    T* part;            // [5][Q] state in sorted order
+    double* part;       // [5][Q] fp64 state in sorted order
     int64_t* leaves;    // sorted order
     int64_t* far;
     uint64_t* hash;
@@ -411,11 +411,12 @@ __global__ void __launch_bounds__(kTravThreads) traverse_kernel(const __grid_con
             id = id + 1;
         }
     }
-    a.part[i] = acc.m;
-    a.part[a.Q + i] = acc.s;
-    a.part[2 * a.Q + i] = acc.gx;
-    a.part[3 * a.Q + i] = acc.gy;
-    a.part[4 * a.Q + i] = acc.gz;
+    acc.flush();
+    a.part[i] = double(acc.m);
+    a.part[a.Q + i] = acc.ts;
+    a.part[2 * a.Q + i] = acc.tgx;
+    a.part[3 * a.Q + i] = acc.tgy;
+    a.part[4 * a.Q + i] = acc.tgz;
     a.leaves[i] = nleaf;
     a.far[i] = nfar;
     a.hash[i] = h;
@@ -456,7 +457,7 @@ void tree_query(Ctx& c, const T* q, int64_t Q, const sd_params& p, const Finaliz
     check_cuda(cudaMemcpyAsync(dpoly, ptab.data(), ptab.size() * sizeof(Poly<T>), cudaMemcpyHostToDevice, st),
                "upload polys");
 
-    T* part = static_cast<T*>(c.part.ensure(size_t(5) * Q * sizeof(T)));
+    double* part = static_cast<double*>(c.part.ensure(size_t(5) * Q * sizeof(double)));
     int64_t* cnt = static_cast<int64_t*>(c.counters.ensure(size_t(Q) * 3 * sizeof(int64_t) + 64));
     unsigned long long* re = reinterpret_cast<unsigned long long*>(cnt + 3 * Q);
     check_cuda(cudaMemsetAsync(re, 0, sizeof(unsigned long long), st), "memset");
@@ -489,7 +490,7 @@ void tree_query(Ctx& c, const T* q, int64_t Q, const sd_params& p, const Finaliz
     kern<<<unsigned((Q + kTravThreads - 1) / kTravThreads), kTravThreads, smem, st>>>(a);
     check_cuda(cudaGetLastError(), "traverse kernel");
     ++launches;
-    check_cuda(launch_finalize<T>(part, 1, Q, p.alpha, p.epsilon, 0, a.leaves, a.far, a.hash, perm, out, st),
+    check_cuda(launch_finalize(part, 1, Q, p.alpha, p.epsilon, 0, a.leaves, a.far, a.hash, perm, out, st),
                "finalize");
     ++launches;
     c.last_launches = launches;

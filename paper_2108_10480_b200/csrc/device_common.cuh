@@ -60,12 +60,30 @@ template <> struct Vec4<double> { using type = double2; };
 // (fp32).
 constexpr float kHeadroom = 16.0f;
 
+// Two-level sums: terms accumulate in T (s, g) for at most one staged tile,
+// then flush() folds them into fp64 totals (ts, tg), so the fp32 rounding
+// error grows with the tile length (<= 768 terms), not with the number of
+// primitives (up to 2^24).
 template <class T>
 struct Acc {
     T m, s, gx, gy, gz;
+    double ts, tgx, tgy, tgz;
     __device__ __forceinline__ void init() {
         m = T(-INFINITY);  // no term yet
         s = gx = gy = gz = T(0);
+        ts = tgx = tgy = tgz = 0.0;
+    }
+    __device__ __forceinline__ void flush() {
+        ts += double(s);
+        tgx += double(gx);
+        tgy += double(gy);
+        tgz += double(gz);
+        s = gx = gy = gz = T(0);
+    }
+    __device__ __forceinline__ void scale(T sc) {
+        s *= sc; gx *= sc; gy *= sc; gz *= sc;
+        const double d = double(sc);
+        ts *= d; tgx *= d; tgy *= d; tgz *= d;
     }
 };
 

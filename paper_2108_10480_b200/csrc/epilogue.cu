@@ -12,8 +12,7 @@
 
 namespace sdgpu {
 
-template <class T>
-__global__ void finalize_kernel(const T* __restrict__ part, int splits, int64_t Q, double alpha, double eps,
+__global__ void finalize_kernel(const double* __restrict__ part, int splits, int64_t Q, double alpha, double eps,
                                 int64_t const_leaves, const int64_t* __restrict__ leaves_in,
                                 const int64_t* __restrict__ far_in, const uint64_t* __restrict__ hash_in,
                                 const int64_t* __restrict__ perm, FinalizeOut o) {
@@ -23,7 +22,7 @@ __global__ void finalize_kernel(const T* __restrict__ part, int splits, int64_t 
     for (int k = 0; k < splits; ++k) M = fmax(M, double(part[size_t(k) * 5 * Q + i]));
     double s = 0, gx = 0, gy = 0, gz = 0;
     for (int k = 0; k < splits && M > -INFINITY; ++k) {
-        const T* p = part + size_t(k) * 5 * Q;
+        const double* p = part + size_t(k) * 5 * Q;
         const double f = exp2(double(p[i]) - M);
         s = fma(double(p[Q + i]), f, s);
         gx = fma(double(p[2 * Q + i]), f, gx);
@@ -59,24 +58,16 @@ __global__ void finalize_kernel(const T* __restrict__ part, int splits, int64_t 
     if (o.hash) o.hash[j] = hash_in ? hash_in[i] : 0;
 }
 
-template <class T>
-cudaError_t launch_finalize(const T* part, int splits, int64_t Q, double alpha, double epsilon,
+cudaError_t launch_finalize(const double* part, int splits, int64_t Q, double alpha, double epsilon,
                             int64_t const_leaves, const int64_t* leaves_in, const int64_t* far_in,
                             const uint64_t* hash_in, const int64_t* perm, const FinalizeOut& out, cudaStream_t st) {
     if (Q <= 0) return cudaSuccess;
     const int threads = 256;
     const unsigned blocks = unsigned((Q + threads - 1) / threads);
-    finalize_kernel<T><<<blocks, threads, 0, st>>>(part, splits, Q, alpha, epsilon, const_leaves, leaves_in, far_in,
+    finalize_kernel<<<blocks, threads, 0, st>>>(part, splits, Q, alpha, epsilon, const_leaves, leaves_in, far_in,
                                                    hash_in, perm, out);
     return cudaGetLastError();
 }
-template cudaError_t launch_finalize<float>(const float*, int, int64_t, double, double, int64_t, const int64_t*,
-                                            const int64_t*, const uint64_t*, const int64_t*, const FinalizeOut&,
-                                            cudaStream_t);
-template cudaError_t launch_finalize<double>(const double*, int, int64_t, double, double, int64_t, const int64_t*,
-                                             const int64_t*, const uint64_t*, const int64_t*, const FinalizeOut&,
-                                             cudaStream_t);
-
 __global__ void finalize_sums_kernel(const double* __restrict__ c, const double* __restrict__ gc, int64_t Q,
                                      double alpha, double eps, double* d_hat, double* grad) {
     const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;

@@ -25,7 +25,7 @@ struct ExactArgs {
     int64_t chunk;      // primitives per split
     const T* q;         // Q x 3 query points
     int64_t Q;
-    T* part;            // [splits][5][Q] partial state (m, s, gx, gy, gz)
+    double* part;       // [splits][5][Q] partial state (m, s, gx, gy, gz), fp64
     int first;          // first segment: initialise instead of loading
     Phys<T> ph;
     Poly<T> poly;
@@ -74,7 +74,7 @@ __global__ void __launch_bounds__(kThreads) exact_kernel(const __grid_constant__
     T qx[QPT], qy[QPT], qz[QPT];
     Acc<T> acc[QPT];
     int64_t qi[QPT];
-    T* part = a.part + size_t(split) * 5 * a.Q;
+    double* part = a.part + size_t(split) * 5 * a.Q;
 #pragma unroll
     for (int k = 0; k < QPT; ++k) {
         qi[k] = int64_t(blockIdx.x) * kThreads * QPT + k * kThreads + threadIdx.x;
@@ -85,11 +85,12 @@ __global__ void __launch_bounds__(kThreads) exact_kernel(const __grid_constant__
         if (a.first) {
             acc[k].init();
         } else {
-            acc[k].m = part[qc];
-            acc[k].s = part[a.Q + qc];
-            acc[k].gx = part[2 * a.Q + qc];
-            acc[k].gy = part[3 * a.Q + qc];
-            acc[k].gz = part[4 * a.Q + qc];
+            acc[k].init();
+            acc[k].m = T(part[qc]);
+            acc[k].ts = part[a.Q + qc];
+            acc[k].tgx = part[2 * a.Q + qc];
+            acc[k].tgy = part[3 * a.Q + qc];
+            acc[k].tgz = part[4 * a.Q + qc];
         }
         // unit-weight launches keep the shift relative to log2 w = S log2 A
         if constexpr (!POLY) acc[k].m -= a.ph.lw_unit;
@@ -115,6 +116,8 @@ __global__ void __launch_bounds__(kThreads) exact_kernel(const __grid_constant__
                 else tri_term<T, POLY, SAFE>(a.ph, a.poly, qx[k], qy[k], qz[k], rec, acc[k]);
             }
         }
+#pragma unroll
+        for (int k = 0; k < QPT; ++k) acc[k].flush();
         __syncthreads();  // every thread is done with stage s
         if (threadIdx.x == 0 && t + kStages < ntiles) issue(t + kStages);
     }
@@ -123,11 +126,11 @@ __global__ void __launch_bounds__(kThreads) exact_kernel(const __grid_constant__
     for (int k = 0; k < QPT; ++k) {
         if (qi[k] >= a.Q) continue;
         if constexpr (!POLY) acc[k].m += a.ph.lw_unit;
-        part[qi[k]] = acc[k].m;
-        part[a.Q + qi[k]] = acc[k].s;
-        part[2 * a.Q + qi[k]] = acc[k].gx;
-        part[3 * a.Q + qi[k]] = acc[k].gy;
-        part[4 * a.Q + qi[k]] = acc[k].gz;
+        part[qi[k]] = double(acc[k].m);
+        part[a.Q + qi[k]] = acc[k].ts;
+        part[2 * a.Q + qi[k]] = acc[k].tgx;
+        part[3 * a.Q + qi[k]] = acc[k].tgy;
+        part[4 * a.Q + qi[k]] = acc[k].tgz;
     }
 }
 
@@ -160,6 +163,29 @@ static cudaError_t launch_one(const ExactLaunch<T>& L, cudaStream_t st) {
     kern<<<grid, kThreads, smem, st>>>(a);
     return cudaGetLastError();
 }
+
+template <class T, int KIND, bool POLY, bool SAFE>
+static int occupancy_one() {
+    constexpr int R = rec_size(KIND);
+    constexpr int TILE = tile_prims<T, KIND>();
+    const size_t smem = size_t(kStages) * TILE * R * sizeof(T);
+    auto kern = exact_kernel<T, KIND, POLY, SAFE, qpt_for<KIND>()>;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess) return 1;
+    int n = 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, kThreads, smem) != cudaSuccess) return 1;
+    return n > 0 ? n : 1;
+}
+
+template <class T>
+int exact_blocks_per_sm(int kind, bool has_poly, bool safe) {
+    if (kind == 0) return occupancy_one<T, 0, false, false>();
+    if (kind == 1) return !has_poly ? occupancy_one<T, 1, false, false>()
+                                    : (safe ? occupancy_one<T, 1, true, true>() : occupancy_one<T, 1, true, false>());
+    return !has_poly ? occupancy_one<T, 2, false, false>()
+                     : (safe ? occupancy_one<T, 2, true, true>() : occupancy_one<T, 2, true, false>());
+}
+template int exact_blocks_per_sm<float>(int, bool, bool);
+template int exact_blocks_per_sm<double>(int, bool, bool);
 
 int64_t exact_queries_per_cta(int kind) {
     return int64_t(kThreads) * (kind == 2 ? qpt_for<2>() : qpt_for<1>());

@@ -20,7 +20,7 @@ struct ExactLaunch {
     int splits = 1;
     const T* q = nullptr;
     int64_t Q = 0;
-    T* part = nullptr;     // [splits][5][Q]
+    double* part = nullptr;  // [splits][5][Q] fp64 partial state
     int first = 1;
     Phys<T> ph{};
     Poly<T> poly{};
@@ -29,6 +29,8 @@ struct ExactLaunch {
 template <class T>
 cudaError_t launch_exact(const ExactLaunch<T>& L, cudaStream_t st);
 int64_t exact_queries_per_cta(int kind);
+template <class T>
+int exact_blocks_per_sm(int kind, bool has_poly, bool safe);  // resident CTAs per SM
 
 // K4: merge `splits` partial states and finalise (smooth.hpp:147-159).
 struct FinalizeOut {
@@ -40,8 +42,7 @@ struct FinalizeOut {
     int64_t* far_field = nullptr;
     uint64_t* hash = nullptr;
 };
-template <class T>
-cudaError_t launch_finalize(const T* part, int splits, int64_t Q, double alpha, double epsilon,
+cudaError_t launch_finalize(const double* part, int splits, int64_t Q, double alpha, double epsilon,
                             int64_t const_leaves, const int64_t* leaves_in, const int64_t* far_in,
                             const uint64_t* hash_in, const int64_t* perm, const FinalizeOut& out, cudaStream_t st);
 cudaError_t launch_finalize_sums(const double* c, const double* grad_c, int64_t Q, double alpha, double epsilon,

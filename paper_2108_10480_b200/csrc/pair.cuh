@@ -70,8 +70,7 @@ __device__ __forceinline__ T bump(Acc<T>& acc, T xm, F&& absx) {
     if (xm > T(0)) {
         const T x = absx();
         const T mn = x + T(kHeadroom);
-        const T sc = Math<T>::ex2(acc.m - mn);
-        acc.s *= sc; acc.gx *= sc; acc.gy *= sc; acc.gz *= sc;
+        acc.scale(Math<T>::ex2(acc.m - mn));
         acc.m = mn;
         xm = x - mn;
     }
