@@ -1,5 +1,5 @@
 // bvh.cu -- Barnes-Hut tree path: tree construction (reference median
-// split on the host; LBVH on the GPU lives in lbvh.cu), upload into the
+// split on the host; the GPU LBVH lives in lbvh.cu), upload into the
 // traversal layout, query Morton sort, and K3, the stack traversal that
 // replaces collect_contributions (smooth.hpp:101-131) for a query batch.
 //
@@ -500,8 +500,3 @@ template void tree_query<double>(Ctx&, const double*, int64_t, const sd_params&,
 
 }  // namespace sdgpu
 
-namespace sdgpu {
-void tree_build_lbvh(Ctx& c) {
-    throw std::runtime_error("LBVH builder not available in this build");
-}
-}  // namespace sdgpu

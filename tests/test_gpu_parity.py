@@ -149,6 +149,60 @@ def test_gpu_median_build_matches_reference_tree(sd, oracle, prec):
         assert got.tobytes() == ref.tobytes()
 
 
+def check_tree_structure(nodes, n):
+    """bvh.hpp invariants (T/test_bvh.cpp:27-59) + the pre-order layout."""
+    assert len(nodes) == 2 * n - 1 and nodes[0]["count"] == n
+    leaf = nodes["left"] < 0
+    assert sorted(nodes["primitive"][leaf].tolist()) == list(range(n))
+    assert (nodes["count"][leaf] == 1).all()
+    idx = np.nonzero(~leaf)[0]
+    assert (nodes["left"][idx] == idx + 1).all()
+    l, r = nodes[nodes["left"][idx]], nodes[nodes["right"][idx]]
+    assert (nodes["count"][idx] == l["count"] + r["count"]).all()
+    assert (nodes["lo"][idx] == np.minimum(l["lo"], r["lo"])).all()
+    assert (nodes["hi"][idx] == np.maximum(l["hi"], r["hi"])).all()
+    e = nodes["hi"] - nodes["lo"]
+    diag = np.sqrt((e[:, 0] * e[:, 0] + e[:, 1] * e[:, 1]) + e[:, 2] * e[:, 2])
+    assert (nodes["diameter"] == diag).all()
+
+
+@pytest.mark.parametrize("prec", [0, 1])
+@pytest.mark.parametrize("seed", [1, 2, 3, 4, 11, 12])
+def test_lbvh_structure_and_decisions(sd, oracle, prec, seed):
+    """GPU-built LBVH, exported in the reference layout: structure
+    invariants, and the oracle traversing the exported tree makes exactly
+    the GPU's far-field / leaf decisions."""
+    O = oracle
+    m0 = O.random_scene(seed, 200)
+    qs = O.QueryStream(3000 + seed).draw_points(m0, 200)
+    m, q = prep(O, m0, qs, prec)
+    w = O.Weights.build(m)
+    e = engine_for(sd, O, m, w, prec)
+    e.build_bvh(sd.SD_BVH_LBVH)
+    nodes = e.export_bvh()
+    check_tree_structure(nodes, m.num_simplices)
+    t = O.Tree.from_nodes(nodes)
+    for beta in (0.3, 0.7):
+        ref = O.query(m, w, q, O.Params(alpha=100.0, beta=beta), tree=t)
+        got = e.smooth_min_dist(q, sd.SmoothParams(alpha=100.0, beta=beta))
+        assert (got.decision_hash == ref.decision_hash).all()
+        assert (got.leaves == ref.leaves).all() and (got.far_field == ref.far_field).all()
+        assert_close(got, ref, prec, 100.0, f"lbvh seed {seed} beta {beta}")
+
+
+def test_lbvh_tiny_meshes(sd, oracle):
+    O = oracle
+    for verts, simp, kinds in (([[0, 0, 0]], [[0, -1, -1]], [0]),
+                               ([[0, 0, 0], [1, 0, 0]], [[0, -1, -1], [1, -1, -1]], [0, 0]),
+                               ([[0, 0, 0], [1, 0, 0], [0, 1, 0]], [[0, 1, 2]], [2])):
+        m = O.Mesh.from_arrays(verts, simp, kinds)
+        e = engine_for(sd, O, m, O.Weights.build(m), 1)
+        e.build_bvh(sd.SD_BVH_LBVH)
+        check_tree_structure(e.export_bvh(), m.num_simplices)
+        r = e.smooth_min_dist([[3.0, 0.5, 0.25]], sd.SmoothParams(alpha=50.0, beta=0.5))
+        assert np.isfinite(r.d_hat).all()
+
+
 # --------------------------------------------------- BASELINE configs
 def _cfg(O, cfg, nq, prec):
     m = O.config_mesh(cfg)
@@ -174,14 +228,25 @@ def test_config_exact_parity(sd, oracle, cfg, prec, alphas, nq):
         assert_close(got, ref, prec, alpha, f"cfg{cfg} alpha {alpha}")
 
 
-def test_config4_tree_parity_subset(sd, oracle):
+@pytest.mark.parametrize("builder", ["median", "lbvh"])
+def test_config4_tree_parity_subset(sd, oracle, builder):
     """cfg4 (icosphere(9), 5.2M triangles, beta 0.5, alpha 200) on a query
-    subset: decisions identical to the oracle on the same tree, and the
-    Barnes-Hut field below the exact one (acceptance [1])."""
+    subset (both halves of the query distribution): decisions identical to
+    the oracle on the same tree -- the reference median tree, or the GPU
+    LBVH exported to the oracle -- and the Barnes-Hut field below the exact
+    one (acceptance [1])."""
     O = oracle
     m, q = _cfg(O, 4, 512, 0)
-    w, t = O.Weights.build(m), O.Tree.build(m)
-    e = engine_for(sd, O, m, w, 0, tree=t)
+    w = O.Weights.build(m)
+    if builder == "median":
+        t = O.Tree.build(m)
+        e = engine_for(sd, O, m, w, 0, tree=t)
+    else:
+        e = engine_for(sd, O, m, w, 0)
+        e.build_bvh(sd.SD_BVH_LBVH)
+        nodes = e.export_bvh()
+        check_tree_structure(nodes, m.num_simplices)
+        t = O.Tree.from_nodes(nodes)
     p = O.Params(alpha=200.0, beta=0.5)
     ref = O.query(m, w, q, p, tree=t)
     got = e.smooth_min_dist(q, sd.SmoothParams(alpha=200.0, beta=0.5))
