@@ -32,6 +32,9 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 FLOPS_PER_EDGE_PAIR = 62      # SURVEY 8(d) canonical count, S != 1
+FLOPS_PER_TRI_PAIR = 192
+FLOPS_BOX_TEST, FLOPS_FAR_TERM = 10, 12
+BYTES_NODE, BYTES_LEAF = 32, 100  # fp32 traversal node record; leaf record (96 B) + meta
 MUFU_PER_EDGE_PAIR = 5
 QUERIES_PER_GPU = 262144
 ALPHA = 100.0
@@ -167,6 +170,81 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def measure_bvh(args, rank, world, local, eng_cls, dev, stream, flush, peaks):
+    """Secondary line item: BVH far-field queries/s on BASELINE configs[3]
+    (cfg4: icosphere(9), 5,242,880 triangles, 4,194,304 queries per GPU,
+    alpha 200, beta 0.5), GPU LBVH + fp32 traversal."""
+    import torch
+    import paper_2108_10480_b200 as sd
+    from paper_2108_10480_b200 import configs
+    t0 = time.perf_counter()
+    w, q = configs.cfg4(block=rank)
+    v, q = configs.quantize(w.vertices), configs.quantize(q)
+    eng = sd.Engine(local, sd.SD_FP32)
+    eng.set_geometry(v, w.simplices, w.kinds)
+    tw = time.perf_counter()
+    eng.build_weights()
+    tw = time.perf_counter() - tw
+    tb = time.perf_counter()
+    eng.build_bvh(sd.SD_BVH_LBVH)
+    tb = time.perf_counter() - tb
+    Q = len(q)
+    P = sd.SmoothParams(alpha=w.alpha, alpha_u=600.0, beta=w.beta)
+    qd = torch.tensor(q, dtype=torch.float32, device=dev)
+    d_hat = torch.empty(Q, dtype=torch.float64, device=dev)
+    grad = torch.empty(Q, 3, dtype=torch.float64, device=dev)
+    leaves = torch.empty(Q, dtype=torch.int64, device=dev)
+    far = torch.empty(Q, dtype=torch.int64, device=dev)
+
+    def step(counters=False):
+        eng.query_points_device(qd.data_ptr(), Q, P, sd.SD_BVH, d_hat.data_ptr(), grad.data_ptr(),
+                                leaves_ptr=leaves.data_ptr() if counters else None,
+                                far_ptr=far.data_ptr() if counters else None, stream=stream.cuda_stream)
+
+    step(counters=True)  # also uploads the traversal layout
+    torch.cuda.synchronize()
+    setup_s = time.perf_counter() - t0
+    L = leaves.double().sum().item()
+    F = far.double().sum().item()
+    for _ in range(max(3, args.warmup)):
+        step()
+    launches = eng.last_launch_count()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    for i in range(args.steps):
+        flush.zero_()
+        evs[i][0].record(stream)
+        step()
+        evs[i][1].record(stream)
+    torch.cuda.synchronize()
+    ms = float(np.mean([a.elapsed_time(b) for a, b in evs]))
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    ms = float(t.item())
+    pops = 2 * (L + F) - Q
+    flops = FLOPS_BOX_TEST * pops + FLOPS_FAR_TERM * F + FLOPS_PER_TRI_PAIR * L
+    nbytes = BYTES_NODE * pops + BYTES_LEAF * L
+    out = {"metric": "BVH queries/s (value+grad)", "value": world * Q / (ms * 1e-3), "unit": "queries/s",
+           "ms_per_step": ms, "queries_per_gpu": Q, "primitives": len(w.kinds),
+           "workload": "cfg4: icosphere(9) with radial displacement, 5,242,880 triangles, 4,194,304 queries "
+                       "per GPU (half uniform in [-1.5,1.5]^3, half within 0.02 of the surface), alpha=200, "
+                       "beta=0.5, fp32, GPU LBVH (BASELINE configs[3])",
+           "per_query": {"leaves": L / Q, "far_field": F / Q, "nodes_popped": pops / Q},
+           "setup_s": {"total": setup_s, "build_weights": tw, "build_lbvh": tb},
+           "gpu_launches": launches * args.steps,
+           "roofline": {"achieved_tflops": flops / (ms * 1e-3) / 1e12, "touched_gbs": nbytes / (ms * 1e-3) / 1e9,
+                        "hbm_peak_gbs": 6542.4, "algorithmic": "10 flop/popped node + 12/far term + 192/exact "
+                        "tri leaf; 32 B/popped node + 100 B/leaf (from this run's counters)"}}
+    if peaks:
+        out["roofline"]["frac_fp32"] = out["roofline"]["achieved_tflops"] / peaks["ffma_tflops"]
+    out["roofline"]["frac_hbm"] = out["roofline"]["touched_gbs"] / 6542.4
+    eng.close()
+    return out
+
+
 def run_ours(args, rank, world, local):
     import torch
     import paper_2108_10480_b200 as sd
@@ -241,6 +319,7 @@ def run_ours(args, rank, world, local):
         torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
     e2e_value = world * pairs_per_rank / float(te.item())
 
+    bvh = None if args.no_bvh else measure_bvh(args, rank, world, local, sd.Engine, dev, stream, flush, peaks)
     if rank == 0:
         achieved = pairs_per_rank * FLOPS_PER_EDGE_PAIR / (ms_max * 1e-3) / 1e12
         roof = {"bound": "fp32-fma", "achieved": achieved, "unit": "TFLOP/s", "traffic": None,
@@ -273,6 +352,7 @@ def run_ours(args, rank, world, local):
                     "d2h_bytes_per_step": Q * 4 * 8},
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clk.summary(),
+            "bvh": bvh,
             "step_ms_all": step_ms,
         }
         print(json.dumps(line), flush=True)
@@ -287,6 +367,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-bvh", action="store_true", help="skip the secondary BVH (cfg4) measurement")
     args = ap.parse_args()
     rank, world, local = dist_env()
     if args.impl == "reference":

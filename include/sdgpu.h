@@ -8,6 +8,10 @@
  *
  *   sd_set_geometry      <- SimplexMesh / Simplex / SimplexKind   (mesh.hpp:15-50)
  *   sd_set_weights       <- WeightSet (+ build_weight_set result)  (weights.hpp:565-621)
+ *   sd_build_weights     <- build_weight_set(mesh, build_adjacency(mesh))
+ *                           (weights.hpp:589-621, mesh.hpp:163-183)
+ *   sd_weights_info / sd_export_weights <- WeightSet fields / save_weight_cache
+ *                           payload (weights.hpp:565-579, 715-742)
  *   sd_set_bvh           <- Bvh / BvhNode, reference layout        (bvh.hpp:14-32)
  *   sd_build_bvh         <- build_bvh                              (bvh.hpp:34-91)
  *   sd_export_bvh        <- Bvh::nodes (save_bvh_cache record)     (bvh.hpp:193-212)
@@ -107,6 +111,15 @@ int sd_set_geometry(sd_ctx* ctx, const double* xyz, int64_t V, const int32_t* si
  * (TriWeightPoly::stored), poly_index[N] (-1: unit weight). */
 int sd_set_weights(sd_ctx* ctx, double A, double sup_wtilde, int32_t ne, const double* edge_a, int32_t nt,
                    const double* tri_stored, const int32_t* poly_index);
+
+/* Build the WeightSet of the current geometry on the host (valences,
+ * closed-form edge polynomials, triangle polynomials by the reference
+ * construction) and install it, as build_weight_set does. Then read it back
+ * with sd_weights_info (sizes, A, sup_wtilde) and sd_export_weights (arrays
+ * sized ne x 5, nt x 13 and N; NULL skips an array). */
+int sd_build_weights(sd_ctx* ctx);
+int sd_weights_info(sd_ctx* ctx, double* A, double* sup_wtilde, int32_t* ne, int32_t* nt);
+int sd_export_weights(sd_ctx* ctx, double* edge_a, double* tri_stored, int32_t* poly_index);
 
 /* Upload a reference-layout tree (e.g. from the reference build_bvh), or
  * build one on the GPU: SD_BVH_MEDIAN reproduces build_bvh exactly,

@@ -36,7 +36,7 @@ assert NODE_DTYPE.itemsize == 72
 EXPORTED_SYMBOLS = (
     "sd_last_error", "sd_abi_version", "sd_create", "sd_destroy", "sd_set_geometry", "sd_set_weights",
     "sd_set_bvh", "sd_build_bvh", "sd_bvh_size", "sd_export_bvh", "sd_query_points", "sd_query_points_device",
-    "sd_finalize_device", "sd_last_launch_count",
+    "sd_finalize_device", "sd_last_launch_count", "sd_build_weights", "sd_weights_info", "sd_export_weights",
 )
 
 
@@ -93,6 +93,9 @@ def lib():
             "sd_query_points_device": (C.c_int, [vp, vp, i64, P(_Params), C.c_int, P(_Outputs), vp]),
             "sd_finalize_device": (C.c_int, [vp, vp, vp, i64, P(_Params), vp, vp, vp]),
             "sd_last_launch_count": (C.c_int, [vp, P(i64)]),
+            "sd_build_weights": (C.c_int, [vp]),
+            "sd_weights_info": (C.c_int, [vp, P(f64), P(f64), P(i32), P(i32)]),
+            "sd_export_weights": (C.c_int, [vp, vp, vp, vp]),
         }
         for name, (res, argt) in sig.items():
             f = getattr(L, name)
@@ -125,6 +128,16 @@ class SmoothParams:
 
     def _c(self) -> _Params:
         return _Params(self.alpha, self.alpha_u, self.beta, self.epsilon)
+
+
+@dataclass
+class WeightTable:
+    """WeightSet as flat arrays (weights.hpp:565-579)."""
+    A: float
+    sup_wtilde: float
+    edge_a: np.ndarray      # (ne, 5)
+    tri_stored: np.ndarray  # (nt, 13)
+    poly_index: np.ndarray  # (N,) int32, -1 = unit weight
 
 
 @dataclass
@@ -181,6 +194,21 @@ class Engine:
     def set_weight_table(self, t):
         """Accepts any object with A, sup_wtilde, edge_a, tri_stored, poly_index."""
         self.set_weights(t.A, t.sup_wtilde, t.edge_a, t.tri_stored, t.poly_index)
+
+    def build_weights(self) -> "WeightTable":
+        """build_weight_set on the host (weights.hpp:589-621); installs and
+        returns the table."""
+        _check(lib().sd_build_weights(self.h))
+        return self.weight_table()
+
+    def weight_table(self) -> "WeightTable":
+        A, sup = C.c_double(), C.c_double()
+        ne, nt = C.c_int32(), C.c_int32()
+        _check(lib().sd_weights_info(self.h, C.byref(A), C.byref(sup), C.byref(ne), C.byref(nt)))
+        t = WeightTable(A.value, sup.value, np.zeros((ne.value, 5)), np.zeros((nt.value, 13)),
+                        np.zeros(self.num_simplices, np.int32))
+        _check(lib().sd_export_weights(self.h, _ptr(t.edge_a), _ptr(t.tri_stored), _ptr(t.poly_index)))
+        return t
 
     def set_bvh(self, nodes: np.ndarray):
         nodes = np.ascontiguousarray(nodes, dtype=NODE_DTYPE)

@@ -137,3 +137,54 @@ def torus(major=1.0, minor=0.3, nu=512, nv=256, seed=3001):
 
 def quantize(x: np.ndarray) -> np.ndarray:
     return np.asarray(x, np.float32).astype(np.float64)
+
+
+def icosphere(sub: int):
+    """shapes.hpp:25-63 (midpoint subdivision, projected to the unit sphere);
+    vertex numbering by sorted unique edges rather than first use."""
+    t = (1.0 + math.sqrt(5.0)) / 2.0
+    V = np.array([[-1, t, 0], [1, t, 0], [-1, -t, 0], [1, -t, 0], [0, -1, t], [0, 1, t], [0, -1, -t], [0, 1, -t],
+                  [t, 0, -1], [t, 0, 1], [-t, 0, -1], [-t, 0, 1]], float)
+    F = np.array([[0, 11, 5], [0, 5, 1], [0, 1, 7], [0, 7, 10], [0, 10, 11], [1, 5, 9], [5, 11, 4], [11, 10, 2],
+                  [10, 7, 6], [7, 1, 8], [3, 9, 4], [3, 4, 2], [3, 2, 6], [3, 6, 8], [3, 8, 9], [4, 9, 5],
+                  [2, 4, 11], [6, 2, 10], [8, 6, 7], [9, 8, 1]], np.int64)
+    for _ in range(sub):
+        e = np.concatenate([F[:, [0, 1]], F[:, [1, 2]], F[:, [2, 0]]])
+        e.sort(axis=1)
+        key = e[:, 0] * (len(V) + 1) + e[:, 1]
+        uk, inv = np.unique(key, return_inverse=True)
+        a, b = uk // (len(V) + 1), uk % (len(V) + 1)
+        mid = len(V) + inv.reshape(3, -1)
+        V = np.concatenate([V, 0.5 * (V[a] + V[b])])
+        ab, bc, ca = mid[0], mid[1], mid[2]
+        F = np.concatenate([np.stack([F[:, 0], ab, ca], 1), np.stack([F[:, 1], bc, ab], 1),
+                            np.stack([F[:, 2], ca, bc], 1), np.stack([ab, bc, ca], 1)])
+    V /= np.linalg.norm(V, axis=1, keepdims=True)
+    return V, F.astype(np.int32)
+
+
+def cfg4(nq: int = 4194304, seed: int = 4001, block: int = 0):
+    """icosphere(9) (5,242,880 triangles) with radial displacement
+    r <- r (1 + 0.05 sin 8 theta cos 8 phi); queries half uniform in
+    [-1.5, 1.5]^3, half on the surface + normal offset N(0, 0.01^2)
+    clamped to +-0.02. alpha = 200, beta = 0.5 (params.hpp:16)."""
+    V, F = icosphere(9)
+    r = np.linalg.norm(V, axis=1)
+    th, ph = np.arccos(V[:, 2] / r), np.arctan2(V[:, 1], V[:, 0])
+    V = V * (1.0 + 0.05 * np.sin(8 * th) * np.cos(8 * ph))[:, None]
+    rng = np.random.default_rng([seed, block])
+    h1 = nq // 2
+    q1 = rng.uniform(-1.5, 1.5, (h1, 3))
+    tri = rng.integers(0, len(F), nq - h1)
+    r1, r2 = rng.random(nq - h1), rng.random(nq - h1)
+    s = np.sqrt(r1)
+    b0, b1, b2 = 1 - s, s * (1 - r2), s * r2
+    a, b, c = V[F[tri, 0]], V[F[tri, 1]], V[F[tri, 2]]
+    p = b0[:, None] * a + b1[:, None] * b + b2[:, None] * c
+    n = np.cross(b - a, c - a)
+    n /= np.linalg.norm(n, axis=1, keepdims=True)
+    d = np.clip(rng.normal(0.0, 0.01, nq - h1), -0.02, 0.02)
+    q = np.concatenate([q1, p + d[:, None] * n])
+    w = Workload("cfg4 icosphere(9) 5,242,880 triangles, BVH far field, alpha=200, beta=0.5", V, F,
+                 np.full(len(F), 2, np.uint8), alpha=200.0, beta=0.5)
+    return w, q

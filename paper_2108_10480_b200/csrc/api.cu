@@ -7,6 +7,7 @@
 #include <stdexcept>
 
 #include "context.h"
+#include "weights_host.h"
 
 namespace sdgpu {
 
@@ -440,6 +441,45 @@ int sd_set_weights(sd_ctx* c, double A, double sup, int32_t ne, const double* ed
         c->have_weights = true;
         c->exact_ready = false;
         c->dtree_ready = false;
+    });
+}
+
+int sd_build_weights(sd_ctx* c) {
+    return guard([&] {
+        if (!c) throw ArgError{"ctx is NULL"};
+        if (!c->have_geom) throw StateError{"set the geometry before building weights"};
+        const WeightTableHost t = build_weight_table(c->sv, c->kind, c->V);
+        std::vector<double> ts;
+        for (const TriWeight& w : t.tri) ts.insert(ts.end(), w.stored, w.stored + 13);
+        c->A = t.A;
+        c->sup_wtilde = t.sup;
+        c->edge_a = t.edge_a;
+        c->tri_stored = ts;
+        c->poly_index = t.poly_index;
+        c->have_weights = true;
+        c->exact_ready = false;
+        c->dtree_ready = false;
+    });
+}
+
+int sd_weights_info(sd_ctx* c, double* A, double* sup, int32_t* ne, int32_t* nt) {
+    return guard([&] {
+        if (!c) throw ArgError{"ctx is NULL"};
+        if (!c->have_weights) throw StateError{"no weight table"};
+        if (A) *A = c->A;
+        if (sup) *sup = c->sup_wtilde;
+        if (ne) *ne = int32_t(c->edge_a.size() / 5);
+        if (nt) *nt = int32_t(c->tri_stored.size() / 13);
+    });
+}
+
+int sd_export_weights(sd_ctx* c, double* edge_a, double* tri_stored, int32_t* poly_index) {
+    return guard([&] {
+        if (!c) throw ArgError{"ctx is NULL"};
+        if (!c->have_weights) throw StateError{"no weight table"};
+        if (edge_a) std::memcpy(edge_a, c->edge_a.data(), c->edge_a.size() * sizeof(double));
+        if (tri_stored) std::memcpy(tri_stored, c->tri_stored.data(), c->tri_stored.size() * sizeof(double));
+        if (poly_index) std::memcpy(poly_index, c->poly_index.data(), c->poly_index.size() * sizeof(int32_t));
     });
 }
 
