@@ -14,7 +14,9 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <cstdlib>
 #include <numeric>
+#include <string>
 
 #include <cub/cub.cuh>
 
@@ -281,6 +283,13 @@ struct TraverseArgs {
 
 constexpr int kTravThreads = 128;
 
+// shared-memory bytes of the polynomial table, padded so the stacks after it
+// stay 16-byte aligned
+template <class T>
+__host__ __device__ constexpr size_t poly_bytes(int npoly) {
+    return (sizeof(Poly<T>) * size_t(npoly) + 15) / 16 * 16;
+}
+
 // Far-field term of a whole subtree (smooth.hpp:67-75): n_B w_ff collapsed
 // onto the box's closest point; gradient (q - y_B) / d_B.
 template <class T>
@@ -323,7 +332,7 @@ __global__ void __launch_bounds__(kTravThreads) traverse_kernel(const __grid_con
     extern __shared__ __align__(16) unsigned char smem_raw[];
     // polynomial table first, then the per-thread stacks [depth][threads]
     Poly<T>* polys = reinterpret_cast<Poly<T>*>(smem_raw);
-    int32_t* stack = reinterpret_cast<int32_t*>(smem_raw + sizeof(Poly<T>) * a.npoly);
+    int32_t* stack = reinterpret_cast<int32_t*>(smem_raw + poly_bytes<T>(a.npoly));
     for (int i = threadIdx.x; i < a.npoly * kPolyCoefs; i += blockDim.x)
         reinterpret_cast<T*>(polys)[i] = reinterpret_cast<const T*>(a.polys)[i];
     __syncthreads();
@@ -423,6 +432,139 @@ __global__ void __launch_bounds__(kTravThreads) traverse_kernel(const __grid_con
     if (nre) atomicAdd(a.rechecks, nre);
 }
 
+// K3 (default): warp-coherent packet traversal. The 32 Morton-adjacent
+// queries of a warp walk ONE node sequence; each node carries the mask of
+// lanes whose own traversal reaches it, every active lane makes exactly its
+// reference decision at that node (far field / exact leaf / descend), and
+// the warp descends into a child iff some lane descends. So each lane
+// visits precisely the nodes collect_contributions (smooth.hpp:101-131)
+// visits for its query, while node and leaf records are fetched once per
+// warp (broadcast loads) and control flow stays warp-uniform. The stack of
+// (node, lane mask) pairs lives in shared memory, one per warp.
+template <class T>
+__global__ void __launch_bounds__(kTravThreads) packet_kernel(const __grid_constant__ TraverseArgs<T> a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    Poly<T>* polys = reinterpret_cast<Poly<T>*>(smem_raw);
+    int2* stacks = reinterpret_cast<int2*>(smem_raw + poly_bytes<T>(a.npoly));
+    for (int i = threadIdx.x; i < a.npoly * kPolyCoefs; i += blockDim.x)
+        reinterpret_cast<T*>(polys)[i] = reinterpret_cast<const T*>(a.polys)[i];
+    __syncthreads();
+
+    const unsigned lane = threadIdx.x & 31u;
+    int2* st = stacks + (threadIdx.x >> 5) * a.stack_depth;
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const bool valid = i < a.Q;
+    const int64_t qi = valid ? (a.perm ? a.perm[i] : i) : 0;
+    const T qx = valid ? a.q[3 * qi] : T(0), qy = valid ? a.q[3 * qi + 1] : T(0), qz = valid ? a.q[3 * qi + 2] : T(0);
+    unsigned mask = __ballot_sync(0xffffffffu, valid);
+    if (mask == 0u) return;
+    Acc<T> acc;
+    acc.init();
+    int64_t nleaf = 0, nfar = 0;
+    uint64_t h = 0;
+    unsigned long long nre = 0;
+    int sp = 0;
+    int32_t id = 0;
+    const T beta = a.ph.beta;
+    while (true) {
+        const NodeT<T> b = a.box[id];  // warp-uniform address: one broadcast
+        int32_t link;
+        memcpy(&link, &b.v[7], sizeof(int32_t));
+        bool desc = false;
+        if ((mask >> lane) & 1u) {
+            bool far = false;
+            if (a.use_bh) {
+                const T yx = fmin(fmax(qx, b.v[0]), b.v[4]);
+                const T yy = fmin(fmax(qy, b.v[1]), b.v[5]);
+                const T yz = fmin(fmax(qz, b.v[2]), b.v[6]);
+                const T dx = qx - yx, dy = qy - yy, dz = qz - yz;
+                const T s = fma(dx, dx, fma(dy, dy, dz * dz));
+                if constexpr (sizeof(T) == 4) {
+                    const T r = s > T(0) ? Math<T>::rsqrt(s) : T(0);
+                    const T d = s * r;
+                    const T rhs = beta * d;
+                    const T band = T(1e-5) * rhs;
+                    if (s == T(0) && a.exact_boxes) far = false;
+                    else if (b.v[3] < rhs - band) far = true;
+                    else if (b.v[3] > rhs + band) far = false;
+                    else {
+                        far = decide64(b, a.diam64[id], double(qx), double(qy), double(qz), a.beta64);
+                        ++nre;
+                    }
+                    if (far) far_term(a.ph, a.count[id], d, r, dx, dy, dz, acc);
+                } else {
+                    far = decide64(b, a.diam64[id], double(qx), double(qy), double(qz), a.beta64);
+                    if (far) {
+                        const T d = sqrt(s);
+                        far_term(a.ph, a.count[id], d, T(1) / d, dx, dy, dz, acc);
+                    }
+                }
+                if (far) {
+                    ++nfar;
+                    h += decision_mix(uint64_t(id), 1);
+                }
+            }
+            if (!far) {
+                if (link < 0) {  // exact leaf: the record is the same for every lane
+                    const int slot = -link - 1;
+                    const int meta = a.leafmeta[slot];
+                    const int kind = meta & 3, poly = (meta >> 2) - 1;
+                    T rec[kRecTri];
+                    using V = typename Vec4<T>::type;
+                    const V* src = reinterpret_cast<const V*>(a.leafrec + size_t(slot) * kRecTri);
+                    if (kind == 0) {
+                        reinterpret_cast<V*>(rec)[0] = src[0];
+                        acc.m -= a.ph.lw_unit;
+                        point_term(a.ph, qx, qy, qz, rec[0], rec[1], rec[2], acc);
+                        acc.m += a.ph.lw_unit;
+                    } else if (kind == 1) {
+#pragma unroll
+                        for (int j = 0; j < kRecEdge * int(sizeof(T)) / int(sizeof(V)); ++j)
+                            reinterpret_cast<V*>(rec)[j] = src[j];
+                        if (poly >= 0) edge_term<T, true, false>(a.ph, polys[poly], qx, qy, qz, rec, acc);
+                        else unit_term<T, 1>(a.ph, polys[0], qx, qy, qz, rec, acc);
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < kRecTri * int(sizeof(T)) / int(sizeof(V)); ++j)
+                            reinterpret_cast<V*>(rec)[j] = src[j];
+                        if (poly >= 0) tri_term<T, true, false>(a.ph, polys[a.ne + poly], qx, qy, qz, rec, acc);
+                        else unit_term<T, 2>(a.ph, polys[0], qx, qy, qz, rec, acc);
+                    }
+                    ++nleaf;
+                    h += decision_mix(uint64_t(id), 2);
+                } else {
+                    desc = true;
+                }
+            }
+        }
+        const unsigned D = __ballot_sync(0xffffffffu, desc);
+        if (D) {  // descend: left child next, right child (same lanes) on the stack
+            if (lane == 0) st[sp] = make_int2(link, int(D));
+            __syncwarp();
+            ++sp;
+            id = id + 1;
+            mask = D;
+        } else {
+            if (sp == 0) break;
+            --sp;
+            const int2 e = st[sp];
+            id = e.x;
+            mask = unsigned(e.y);
+        }
+    }
+    if (!valid) return;
+    acc.flush();
+    a.part[i] = double(acc.m);
+    a.part[a.Q + i] = acc.ts;
+    a.part[2 * a.Q + i] = acc.tgx;
+    a.part[3 * a.Q + i] = acc.tgy;
+    a.part[4 * a.Q + i] = acc.tgz;
+    a.leaves[i] = nleaf;
+    a.far[i] = nfar;
+    a.hash[i] = h;
+    if (nre) atomicAdd(a.rechecks, nre);
+}
+
 template <class T>
 void tree_query(Ctx& c, const T* q, int64_t Q, const sd_params& p, const FinalizeOut& out, cudaStream_t st) {
     if (!c.dtree_ready) tree_upload(c);
@@ -484,8 +626,15 @@ void tree_query(Ctx& c, const T* q, int64_t Q, const sd_params& p, const Finaliz
     a.far = cnt + Q;
     a.hash = reinterpret_cast<uint64_t*>(cnt + 2 * Q);
     a.rechecks = re;
-    const size_t smem = sizeof(Poly<T>) * npoly + size_t(a.stack_depth) * kTravThreads * sizeof(int32_t);
-    auto kern = traverse_kernel<T>;
+    // SDGPU_TRAVERSAL=thread selects the per-thread DFS variant (A/B runs)
+    static const bool per_thread = [] {
+        const char* e = std::getenv("SDGPU_TRAVERSAL");
+        return e && std::string(e) == "thread";
+    }();
+    const size_t smem = poly_bytes<T>(npoly) +
+                        (per_thread ? size_t(a.stack_depth) * kTravThreads * sizeof(int32_t)
+                                    : size_t(a.stack_depth) * (kTravThreads / 32) * sizeof(int2));
+    auto kern = per_thread ? traverse_kernel<T> : packet_kernel<T>;
     check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)), "smem attr");
     kern<<<unsigned((Q + kTravThreads - 1) / kTravThreads), kTravThreads, smem, st>>>(a);
     check_cuda(cudaGetLastError(), "traverse kernel");
