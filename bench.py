@@ -109,7 +109,12 @@ def measure_peaks():
     L.sd_measure_peaks.argtypes = [ctypes.POINTER(ctypes.c_double)] * 3
     if L.sd_measure_peaks(ctypes.byref(f), ctypes.byref(d), ctypes.byref(m)) != 0:
         return None
-    return {"ffma_tflops": f.value / 1e12, "dfma_tflops": d.value / 1e12, "mufu_tops": m.value / 1e12}
+    out = {"ffma_tflops": f.value / 1e12, "dfma_tflops": d.value / 1e12, "mufu_tops": m.value / 1e12}
+    f2 = ctypes.c_double()
+    L.sd_measure_ffma2.argtypes = [ctypes.POINTER(ctypes.c_double)]
+    if L.sd_measure_ffma2(ctypes.byref(f2)) == 0:
+        out["ffma2_tflops"] = f2.value / 1e12
+    return out
 
 
 def workload(block: int):

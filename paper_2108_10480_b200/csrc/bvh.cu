@@ -169,6 +169,7 @@ static void upload_tree_T(Ctx& c) {
     std::vector<NodeT<T>> box(n);
     std::vector<int32_t> count(n);
     std::vector<double> d64(n);
+    std::vector<T> lgc(n);
     std::vector<T> leafrec;
     std::vector<int32_t> leafmeta;
     leafrec.reserve(size_t(N) * kRecTri);
@@ -206,6 +207,7 @@ static void upload_tree_T(Ctx& c) {
         std::memcpy(&b.v[7], &link, sizeof(int32_t));
         if (sizeof(T) == 8) std::memset(reinterpret_cast<char*>(&b.v[7]) + 4, 0, 4);
         count[id] = nd.count;
+        lgc[id] = T(std::log2(double(nd.count)));
         d64[id] = nd.diameter;
     }
     DeviceTree& t = c.dtree;
@@ -219,6 +221,7 @@ static void upload_tree_T(Ctx& c) {
     };
     up(t.box, box.data(), box.size() * sizeof(NodeT<T>));
     up(t.count, count.data(), count.size() * sizeof(int32_t));
+    up(t.lgcount, lgc.data(), lgc.size() * sizeof(T));
     up(t.diam64, d64.data(), d64.size() * sizeof(double));
     up(t.leafrec, leafrec.data(), leafrec.size() * sizeof(T));
     up(t.leafmeta, leafmeta.data(), leafmeta.size() * sizeof(int32_t));
@@ -264,6 +267,8 @@ struct TraverseArgs {
     int64_t Q;
     const NodeT<T>* box;
     const int32_t* count;
+    const T* lgcount;     // log2 n_B per node (far-field weight exponent)
+    T lw_ff;              // log2 w_ff
     const double* diam64;
     const T* leafrec;
     const int32_t* leafmeta;
@@ -293,8 +298,7 @@ __host__ __device__ constexpr size_t poly_bytes(int npoly) {
 // Far-field term of a whole subtree (smooth.hpp:67-75): n_B w_ff collapsed
 // onto the box's closest point; gradient (q - y_B) / d_B.
 template <class T>
-__device__ __forceinline__ void far_term(const Phys<T>& ph, int32_t count, T d, T r, T dx, T dy, T dz, Acc<T>& acc) {
-    const T lw = Math<T>::lg2(T(count) * ph.w_ff);
+__device__ __forceinline__ void far_term(const Phys<T>& ph, T lw, T d, T r, T dx, T dy, T dz, Acc<T>& acc) {
     const T xm = bump(acc, masked(ph, d, fma(ph.kappa, d, lw - acc.m)), [&] { return fma(ph.kappa, d, lw); });
     const T e = Math<T>::ex2(xm);
     const T er = e * r;
@@ -372,12 +376,12 @@ __global__ void __launch_bounds__(kTravThreads) traverse_kernel(const __grid_con
                     far = decide64(b, a.diam64[id], double(qx), double(qy), double(qz), a.beta64);
                     ++nre;
                 }
-                if (far) far_term(a.ph, a.count[id], d, r, dx, dy, dz, acc);
+                if (far) far_term(a.ph, a.lgcount[id] + a.lw_ff, d, r, dx, dy, dz, acc);
             } else {
                 far = decide64(b, a.diam64[id], double(qx), double(qy), double(qz), a.beta64);
                 if (far) {
                     const T d = sqrt(s);
-                    far_term(a.ph, a.count[id], d, T(1) / d, dx, dy, dz, acc);
+                    far_term(a.ph, a.lgcount[id] + a.lw_ff, d, T(1) / d, dx, dy, dz, acc);
                 }
             }
             if (far) {
@@ -441,7 +445,7 @@ __global__ void __launch_bounds__(kTravThreads) traverse_kernel(const __grid_con
 // visits for its query, while node and leaf records are fetched once per
 // warp (broadcast loads) and control flow stays warp-uniform. The stack of
 // (node, lane mask) pairs lives in shared memory, one per warp.
-template <class T>
+template <class T, bool HASH>
 __global__ void __launch_bounds__(kTravThreads) packet_kernel(const __grid_constant__ TraverseArgs<T> a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Poly<T>* polys = reinterpret_cast<Poly<T>*>(smem_raw);
@@ -491,17 +495,17 @@ __global__ void __launch_bounds__(kTravThreads) packet_kernel(const __grid_const
                         far = decide64(b, a.diam64[id], double(qx), double(qy), double(qz), a.beta64);
                         ++nre;
                     }
-                    if (far) far_term(a.ph, a.count[id], d, r, dx, dy, dz, acc);
+                    if (far) far_term(a.ph, a.lgcount[id] + a.lw_ff, d, r, dx, dy, dz, acc);
                 } else {
                     far = decide64(b, a.diam64[id], double(qx), double(qy), double(qz), a.beta64);
                     if (far) {
                         const T d = sqrt(s);
-                        far_term(a.ph, a.count[id], d, T(1) / d, dx, dy, dz, acc);
+                        far_term(a.ph, a.lgcount[id] + a.lw_ff, d, T(1) / d, dx, dy, dz, acc);
                     }
                 }
                 if (far) {
                     ++nfar;
-                    h += decision_mix(uint64_t(id), 1);
+                    if constexpr (HASH) h += decision_mix(uint64_t(id), 1);
                 }
             }
             if (!far) {
@@ -531,7 +535,7 @@ __global__ void __launch_bounds__(kTravThreads) packet_kernel(const __grid_const
                         else unit_term<T, 2>(a.ph, polys[0], qx, qy, qz, rec, acc);
                     }
                     ++nleaf;
-                    h += decision_mix(uint64_t(id), 2);
+                    if constexpr (HASH) h += decision_mix(uint64_t(id), 2);
                 } else {
                     desc = true;
                 }
@@ -561,7 +565,7 @@ __global__ void __launch_bounds__(kTravThreads) packet_kernel(const __grid_const
     a.part[4 * a.Q + i] = acc.tgz;
     a.leaves[i] = nleaf;
     a.far[i] = nfar;
-    a.hash[i] = h;
+    if (HASH) a.hash[i] = h;
     if (nre) atomicAdd(a.rechecks, nre);
 }
 
@@ -610,10 +614,13 @@ void tree_query(Ctx& c, const T* q, int64_t Q, const sd_params& p, const Finaliz
     a.Q = Q;
     a.box = t.box.as<NodeT<T>>();
     a.count = t.count.as<int32_t>();
+    a.lgcount = t.lgcount.as<T>();
     a.diam64 = t.diam64.as<double>();
     a.leafrec = t.leafrec.as<T>();
     a.leafmeta = t.leafmeta.as<int32_t>();
     a.polys = dpoly;
+    a.ph = make_phys<T>(c, p);
+    a.lw_ff = T(std::log2(std::pow(std::max(c.A * c.sup_wtilde, 1e-300), p.alpha / std::max(p.alpha, p.alpha_u))));
     a.ne = ne;
     a.npoly = npoly;
     a.use_bh = p.beta > 0.0 ? 1 : 0;
@@ -634,7 +641,8 @@ void tree_query(Ctx& c, const T* q, int64_t Q, const sd_params& p, const Finaliz
     const size_t smem = poly_bytes<T>(npoly) +
                         (per_thread ? size_t(a.stack_depth) * kTravThreads * sizeof(int32_t)
                                     : size_t(a.stack_depth) * (kTravThreads / 32) * sizeof(int2));
-    auto kern = per_thread ? traverse_kernel<T> : packet_kernel<T>;
+    // the decision hash costs ~20 integer ops per decision: only when asked for
+    auto kern = per_thread ? traverse_kernel<T> : (out.hash ? packet_kernel<T, true> : packet_kernel<T, false>);
     check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)), "smem attr");
     kern<<<unsigned((Q + kTravThreads - 1) / kTravThreads), kTravThreads, smem, st>>>(a);
     check_cuda(cudaGetLastError(), "traverse kernel");

@@ -25,6 +25,30 @@ __global__ void fma_kernel(T* out, T a, T b) {
     if (s == T(-1234.5)) out[threadIdx.x] = s;  // defeat dead-code elimination
 }
 
+// packed fp32x2 FMA (FFMA2): two FMAs per instruction
+__global__ void ffma2_kernel(float* out, float a, float b) {
+    unsigned long long x[kChains];
+    const float2 av = make_float2(a, a), bv = make_float2(b, b);
+    const unsigned long long A = *reinterpret_cast<const unsigned long long*>(&av);
+    const unsigned long long B = *reinterpret_cast<const unsigned long long*>(&bv);
+#pragma unroll
+    for (int c = 0; c < kChains; ++c) {
+        const float2 v = make_float2(float(threadIdx.x + c), float(c));
+        x[c] = *reinterpret_cast<const unsigned long long*>(&v);
+    }
+    for (int i = 0; i < kIters; ++i) {
+#pragma unroll
+        for (int c = 0; c < kChains; ++c) asm volatile("fma.rn.f32x2 %0, %0, %1, %2;" : "+l"(x[c]) : "l"(A), "l"(B));
+    }
+    float s = 0;
+#pragma unroll
+    for (int c = 0; c < kChains; ++c) {
+        const float2 v = *reinterpret_cast<const float2*>(&x[c]);
+        s += v.x + v.y;
+    }
+    if (s == -1234.5f) out[threadIdx.x] = s;
+}
+
 __global__ void ex2_kernel(float* out, float a) {
     float x[kChains];
 #pragma unroll
@@ -63,6 +87,20 @@ double time_ms(F&& launch, int reps) {
 }  // namespace
 
 extern "C" {
+
+// FFMA2 (packed fp32x2) rate in flop/s (each FFMA2 = 2 FMA = 4 flops).
+int sd_measure_ffma2(double* ffma2_flops) {
+    int sms = 0;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0) != cudaSuccess) return -1;
+    void* buf = nullptr;
+    if (cudaMalloc(&buf, 4096) != cudaSuccess) return -1;
+    const int threads = 256, blocks = sms * 8;
+    const double work = double(blocks) * threads * kIters * kChains;
+    const double ms = time_ms([&] { ffma2_kernel<<<blocks, threads>>>((float*)buf, 0.999f, 1e-3f); }, 10);
+    *ffma2_flops = 4.0 * work / (ms * 1e-3);
+    cudaFree(buf);
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
 
 // Returns 0 on success. Rates in flop/s (FMA = 2 flops) and MUFU ops/s.
 int sd_measure_peaks(double* ffma_flops, double* dfma_flops, double* mufu_ops) {

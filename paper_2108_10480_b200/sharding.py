@@ -1,0 +1,106 @@
+"""Multi-GPU plumbing for the smooth-distance path (one process per GPU).
+
+Two regimes:
+
+* query sharding (cfg1-4): geometry, weights and tree replicated; every rank
+  evaluates its own contiguous block of queries; no data-path collective.
+* primitive sharding (cfg5): the primitives are split into Morton-contiguous
+  shards (one per rank), every rank evaluates ALL queries against its shard
+  and produces the unshifted fp64 partial sums (c, grad_c) of the reference
+  (smooth.hpp:79-93 restricted to the shard, with the -708 mask applied per
+  term); ONE all_reduce(SUM) of 4 doubles per query then gives exactly the
+  whole-mesh sums, and result_from_accum (smooth.hpp:147-159) finishes.
+  The WeightSet is built on the full mesh (A and sup w~ are global,
+  weights.hpp:604,616) and sliced per shard.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+
+def query_ranges(n: int, world: int) -> list[tuple[int, int]]:
+    """Contiguous, balanced [lo, hi) query blocks, one per rank."""
+    b = np.linspace(0, n, world + 1).round().astype(np.int64)
+    return [(int(b[r]), int(b[r + 1])) for r in range(world)]
+
+
+def _morton63(p: np.ndarray) -> np.ndarray:
+    lo, hi = p.min(0), p.max(0)
+    span = np.where(hi > lo, hi - lo, 1.0)
+    c = np.clip(((p - lo) / span * 2097151.0), 0, 2097151).astype(np.uint64)
+
+    def spread(v):
+        v = v & np.uint64(0x1FFFFF)
+        v = (v | (v << np.uint64(32))) & np.uint64(0x1F00000000FFFF)
+        v = (v | (v << np.uint64(16))) & np.uint64(0x1F0000FF0000FF)
+        v = (v | (v << np.uint64(8))) & np.uint64(0x100F00F00F00F00F)
+        v = (v | (v << np.uint64(4))) & np.uint64(0x10C30C30C30C30C3)
+        v = (v | (v << np.uint64(2))) & np.uint64(0x1249249249249249)
+        return v
+
+    return (spread(c[:, 0]) << np.uint64(2)) | (spread(c[:, 1]) << np.uint64(1)) | spread(c[:, 2])
+
+
+@dataclass
+class Shard:
+    """One rank's primitive shard: a self-contained sub-mesh with its slice
+    of the global WeightSet (same polynomial tables, sliced poly_index)."""
+    prims: np.ndarray       # global primitive ids of this shard
+    vertices: np.ndarray
+    simplices: np.ndarray   # re-indexed into `vertices`
+    kinds: np.ndarray
+    poly_index: np.ndarray
+
+
+def primitive_shards(vertices, simplices, kinds, poly_index, world: int) -> list[Shard]:
+    """Morton-contiguous, equal-count primitive shards (spatially compact, so
+    each shard's own tree stays tight)."""
+    vertices = np.asarray(vertices, np.float64)
+    simplices = np.asarray(simplices, np.int32)
+    kinds = np.asarray(kinds, np.uint8)
+    n = len(kinds)
+    corner = simplices.copy()
+    for k in (1, 2):  # unused corners -> the first corner (bbox centre unchanged)
+        corner[:, k] = np.where(kinds >= k, simplices[:, k], simplices[:, 0])
+    pts = vertices[corner]                                  # (n, 3, 3)
+    centre = 0.5 * (pts.min(1) + pts.max(1))               # bbox centre, as bvh.hpp:45
+    order = np.argsort(_morton63(centre), kind="stable") if n else np.zeros(0, np.int64)
+    out = []
+    for lo, hi in query_ranges(n, world):
+        ids = np.sort(order[lo:hi])
+        s = simplices[ids]
+        k = kinds[ids]
+        used = np.unique(np.concatenate([s[:, 0], s[k >= 1, 1], s[k >= 2, 2]])) if len(ids) else np.zeros(0, np.int32)
+        remap = np.full(len(vertices), -1, np.int64)
+        remap[used] = np.arange(len(used))
+        s2 = np.where(s >= 0, remap[np.maximum(s, 0)], -1).astype(np.int32)
+        out.append(Shard(ids, vertices[used], s2, k, np.asarray(poly_index, np.int32)[ids]))
+    return out
+
+
+def finalize(c: np.ndarray, grad_c: np.ndarray, alpha: float, epsilon: float = 1e-300):
+    """result_from_accum (smooth.hpp:147-159) on summed partials (host
+    mirror of sd_finalize_device, used by CPU tests)."""
+    c = np.asarray(c, np.float64)
+    d = np.full(c.shape, np.inf)
+    g = np.zeros((len(c), 3))
+    ok = c > 0.0
+    d[ok] = -np.log(c[ok]) / alpha
+    g[ok] = grad_c[ok] / (c[ok] + epsilon)[:, None]
+    return d, g
+
+
+def allreduce_partials(c, grad_c, group=None):
+    """The single data-path collective of primitive sharding: SUM of the
+    per-query (c, grad_c) partials over ranks. Accepts torch tensors (NCCL
+    on GPU tensors, gloo on CPU tensors) and reduces them in place as one
+    fused buffer."""
+    import torch
+    import torch.distributed as dist
+    buf = torch.cat([c.reshape(-1, 1), grad_c.reshape(-1, 3)], 1).contiguous()
+    dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
+    c.copy_(buf[:, 0])
+    grad_c.copy_(buf[:, 1:].reshape(grad_c.shape))
+    return c, grad_c

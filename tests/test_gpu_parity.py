@@ -350,3 +350,56 @@ def test_build_weights_matches_oracle(sd, oracle, case):
             mg = O.tri_poly_eval(st, g)[0].min()
             mo = O.tri_poly_eval(ref.tri_stored[p], g)[0].min()
             assert mg >= mo - 1e-6, (v, ev, mg, mo)
+
+
+# ------------------------------------- primitive sharding on one device
+@pytest.mark.parametrize("prec,beta", [(1, 0.0), (0, 0.0), (0, 0.5)])
+def test_virtual_primitive_shards(sd, oracle, prec, beta):
+    """cfg5 merge path with 3 virtual shards on one GPU: each shard's engine
+    writes its unshifted fp64 partials (c, grad_c), they are summed (the
+    all_reduce of the multi-GPU run) and sd_finalize_device finishes. Must
+    equal the oracle on the whole mesh (beta = 0), or the oracle on the same
+    per-shard trees (beta > 0)."""
+    import torch
+    from paper_2108_10480_b200 import sharding
+    O = oracle
+    m0 = O.random_scene(6, 200)
+    q0 = O.QueryStream(60).draw_points(m0, 400)
+    m, q = prep(O, m0, q0, prec)
+    wt = O.Weights.build(m).table
+    shards = sharding.primitive_shards(m.vertices, m.simplices, m.kinds, wt.poly_index, 3)
+    P = sd.SmoothParams(alpha=100.0, beta=beta)
+    c_sum, g_sum = np.zeros(len(q)), np.zeros((len(q), 3))
+    ref_c, ref_g = np.zeros(len(q)), np.zeros((len(q), 3))
+    for s in shards:
+        e = sd.Engine(0, prec)
+        e.set_geometry(s.vertices, s.simplices, s.kinds)
+        e.set_weights(wt.A, wt.sup_wtilde, wt.edge_a, wt.tri_stored, s.poly_index)
+        sm = O.Mesh.from_arrays(s.vertices, s.simplices, s.kinds)
+        sw = O.Weights.from_table(O.WeightTable(wt.A, wt.sup_wtilde, wt.edge_a, wt.tri_stored, s.poly_index))
+        tree = None
+        if beta > 0:
+            e.build_bvh(sd.SD_BVH_LBVH)
+            tree = O.Tree.from_nodes(e.export_bvh())
+        r = e.query_points(q, P, sd.SD_BVH if beta > 0 else sd.SD_EXACT, want_c=True)
+        c_sum += r.c
+        g_sum += r.grad_c
+        rr = O.query(sm, sw, q, O.Params(alpha=100.0, beta=beta), tree=tree)
+        ref_c += rr.c
+        ref_g += rr.grad_c
+    dev = torch.device("cuda", 0)
+    c_d = torch.tensor(c_sum, device=dev)
+    g_d = torch.tensor(g_sum, device=dev)
+    d_d = torch.empty(len(q), dtype=torch.float64, device=dev)
+    gr_d = torch.empty(len(q), 3, dtype=torch.float64, device=dev)
+    e.finalize_device(c_d.data_ptr(), g_d.data_ptr(), len(q), P, d_d.data_ptr(), gr_d.data_ptr())
+    torch.cuda.synchronize()
+    got = sd.SmoothResults(d_d.cpu().numpy(), gr_d.cpu().numpy())
+    rd, rg = sharding.finalize(ref_c, ref_g, 100.0)
+    ref = sd.SmoothResults(rd, rg)
+    ref.c = ref_c
+    assert_close(got, ref, prec, 100.0, "virtual shards")
+    if beta == 0.0:
+        whole = O.query(m, O.Weights.from_table(wt), q, O.Params(alpha=100.0, beta=0.0))
+        fin = np.isfinite(whole.d_hat)
+        assert np.abs(rd[fin] - whole.d_hat[fin]).max() < 1e-12

@@ -1,0 +1,113 @@
+"""Multi-process (world size 2, gloo, CPU) tests of the multi-GPU host logic:
+query sharding is a pure partition; primitive sharding merges per-shard
+unshifted fp64 partials with one all_reduce(SUM) and must reproduce the
+whole-mesh reference result. Per-shard partials come from the CPU oracle
+(exactly the quantities the GPU writes through sd_query_points_device), so
+these tests cover the plumbing that the 8-GPU runs use."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from paper_2108_10480_b200 import sharding
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def test_query_ranges_partition():
+    for n in (0, 1, 7, 1000, 262144):
+        for w in (1, 2, 3, 8):
+            r = sharding.query_ranges(n, w)
+            assert r[0][0] == 0 and r[-1][1] == n
+            assert all(a[1] == b[0] for a, b in zip(r, r[1:]))
+            sizes = [hi - lo for lo, hi in r]
+            assert max(sizes) - min(sizes) <= 1
+
+
+def test_primitive_shards_cover_mesh(oracle):
+    m = oracle.random_scene(5, 200)
+    w = oracle.Weights.build(m).table
+    shards = sharding.primitive_shards(m.vertices, m.simplices, m.kinds, w.poly_index, 3)
+    ids = np.sort(np.concatenate([s.prims for s in shards]))
+    assert np.array_equal(ids, np.arange(m.num_simplices))
+    for s in shards:
+        # the sub-mesh reproduces the global corners of each primitive
+        for j, g in enumerate(s.prims):
+            for k in range(int(m.kinds[g]) + 1):
+                assert np.array_equal(s.vertices[s.simplices[j, k]], m.vertices[m.simplices[g, k]])
+        assert np.array_equal(s.poly_index, w.poly_index[s.prims])
+
+
+def _worker(rank, world, port, seed, beta, results):
+    import torch
+    import torch.distributed as dist
+
+    import oracle as O
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    m = O.random_scene(seed, 200)
+    wt = O.Weights.build(m).table  # global WeightSet (A, sup w~ are global)
+    shard = sharding.primitive_shards(m.vertices, m.simplices, m.kinds, wt.poly_index, world)[rank]
+    sm = O.Mesh.from_arrays(shard.vertices, shard.simplices, shard.kinds)
+    sw = O.Weights.from_table(O.WeightTable(wt.A, wt.sup_wtilde, wt.edge_a, wt.tri_stored, shard.poly_index))
+    q = O.QueryStream(900 + seed).draw_points(m, 120)
+    p = O.Params(alpha=100.0, beta=beta)
+    tree = O.Tree.build(sm) if beta > 0 else None   # one tree per shard
+    r = O.query(sm, sw, q, p, tree=tree)
+    c, gc = torch.tensor(r.c), torch.tensor(r.grad_c)
+    sharding.allreduce_partials(c, gc)
+    d, g = sharding.finalize(c.numpy(), gc.numpy(), p.alpha, p.epsilon)
+    if rank == 0:
+        results.put((d, g, q))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("seed", [3, 8])
+def test_primitive_sharded_merge_gloo(oracle, seed):
+    """beta = 0: the merged result equals the whole-mesh flat oracle to fp64
+    rounding (sums re-associated across shards)."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    results = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, seed, 0.0, results)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    d, g, q = results.get(timeout=300)
+    for pr in procs:
+        pr.join(timeout=300)
+        assert pr.exitcode == 0
+    m = oracle.random_scene(seed, 200)
+    w = oracle.Weights.build(m)
+    ref = oracle.query(m, w, q, oracle.Params(alpha=100.0, beta=0.0))
+    fin = np.isfinite(ref.d_hat)
+    assert (np.isfinite(d) == fin).all()
+    assert np.abs(d[fin] - ref.d_hat[fin]).max() <= 1e-12 * max(1.0, np.abs(ref.d_hat[fin]).max())
+    assert np.abs(g - ref.grad).max() <= 1e-11
+
+
+def test_primitive_sharded_bvh_is_conservative_gloo(oracle):
+    """beta > 0 with one tree per shard (the cfg5 BVH semantics): the merged
+    field stays below the exact one (acceptance [1] carried over)."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    results = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, 4, 0.5, results)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    d, g, q = results.get(timeout=300)
+    for pr in procs:
+        pr.join(timeout=300)
+        assert pr.exitcode == 0
+    m = oracle.random_scene(4, 200)
+    ref = oracle.query(m, oracle.Weights.build(m), q, oracle.Params(alpha=100.0, beta=0.0))
+    assert (d <= ref.d_hat + 1e-9).all()
