@@ -15,6 +15,7 @@
 // launches in `part`; K4 (epilogue.cu) merges splits and finalises.
 #include "exact.h"
 #include "pair.cuh"
+#include "pair2.cuh"
 
 namespace sdgpu {
 
@@ -96,6 +97,20 @@ __global__ void __launch_bounds__(kThreads) exact_kernel(const __grid_constant__
         if constexpr (!POLY) acc[k].m -= a.ph.lw_unit;
     }
 
+    // fp32 points / edges: two queries per packed fp32x2 instruction
+    constexpr bool PACKED = sizeof(T) == 4 && KIND < 2 && QPT % 2 == 0;
+    [[maybe_unused]] Acc2 acc2[PACKED ? QPT / 2 : 1];
+    [[maybe_unused]] f2 q2x[PACKED ? QPT / 2 : 1], q2y[PACKED ? QPT / 2 : 1], q2z[PACKED ? QPT / 2 : 1];
+    if constexpr (PACKED) {
+#pragma unroll
+        for (int k = 0; k < QPT / 2; ++k) {
+            acc2[k].from(acc[2 * k], acc[2 * k + 1]);
+            q2x[k] = pack(qx[2 * k], qx[2 * k + 1]);
+            q2y[k] = pack(qy[2 * k], qy[2 * k + 1]);
+            q2z[k] = pack(qz[2 * k], qz[2 * k + 1]);
+        }
+    }
+
     for (int t = 0; t < ntiles; ++t) {
         const int s = t % kStages;
         mbar_wait(&full[s], (t / kStages) & 1);
@@ -109,17 +124,34 @@ __global__ void __launch_bounds__(kThreads) exact_kernel(const __grid_constant__
             const V* src = reinterpret_cast<const V*>(tile + size_t(i) * R);
 #pragma unroll
             for (int j = 0; j < NV; ++j) reinterpret_cast<V*>(rec)[j] = src[j];
+            if constexpr (PACKED) {
 #pragma unroll
-            for (int k = 0; k < QPT; ++k) {
-                if constexpr (KIND == 0) point_term(a.ph, qx[k], qy[k], qz[k], rec[0], rec[1], rec[2], acc[k]);
-                else if constexpr (KIND == 1) edge_term<T, POLY, SAFE>(a.ph, a.poly, qx[k], qy[k], qz[k], rec, acc[k]);
-                else tri_term<T, POLY, SAFE>(a.ph, a.poly, qx[k], qy[k], qz[k], rec, acc[k]);
+                for (int k = 0; k < QPT / 2; ++k) {
+                    if constexpr (KIND == 0) point_term2(a.ph, q2x[k], q2y[k], q2z[k], (const float*)rec, acc2[k]);
+                    else edge_term2<POLY, SAFE>(a.ph, a.poly, q2x[k], q2y[k], q2z[k], (const float*)rec, acc2[k]);
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < QPT; ++k) {
+                    if constexpr (KIND == 0) point_term(a.ph, qx[k], qy[k], qz[k], rec[0], rec[1], rec[2], acc[k]);
+                    else if constexpr (KIND == 1) edge_term<T, POLY, SAFE>(a.ph, a.poly, qx[k], qy[k], qz[k], rec, acc[k]);
+                    else tri_term<T, POLY, SAFE>(a.ph, a.poly, qx[k], qy[k], qz[k], rec, acc[k]);
+                }
             }
         }
+        if constexpr (PACKED) {
 #pragma unroll
-        for (int k = 0; k < QPT; ++k) acc[k].flush();
+            for (int k = 0; k < QPT / 2; ++k) acc2[k].flush();
+        } else {
+#pragma unroll
+            for (int k = 0; k < QPT; ++k) acc[k].flush();
+        }
         __syncthreads();  // every thread is done with stage s
         if (threadIdx.x == 0 && t + kStages < ntiles) issue(t + kStages);
+    }
+    if constexpr (PACKED) {
+#pragma unroll
+        for (int k = 0; k < QPT / 2; ++k) acc2[k].to(acc[2 * k], acc[2 * k + 1]);
     }
 
 #pragma unroll

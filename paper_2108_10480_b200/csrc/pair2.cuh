@@ -1,0 +1,183 @@
+// pair2.cuh -- fp32 pair terms for TWO queries at once with Blackwell's
+// packed fp32x2 arithmetic (FFMA2 / FMUL2 / FADD2, sm_100a). The two
+// queries of a packed pair see the same staged primitive record, whose
+// scalars enter the packed instructions as broadcast operands (SASS
+// `R.F32`), so every add/mul/fma of pair.cuh costs half an issue slot;
+// selects, clamps and MUFU stay scalar per query. Semantics are those of
+// pair.cuh line for line (see there for the reference citations).
+#pragma once
+
+#include "pair.cuh"
+
+namespace sdgpu {
+
+struct f2 {
+    unsigned long long v;
+};
+__device__ __forceinline__ f2 pack(float lo, float hi) {
+    f2 r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r.v) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ f2 bcast(float s) { return pack(s, s); }
+__device__ __forceinline__ float lo(f2 a) {
+    float x, y;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(x), "=f"(y) : "l"(a.v));
+    return x;
+}
+__device__ __forceinline__ float hi(f2 a) {
+    float x, y;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(x), "=f"(y) : "l"(a.v));
+    return y;
+}
+__device__ __forceinline__ f2 add2(f2 a, f2 b) {
+    f2 d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d.v) : "l"(a.v), "l"(b.v));
+    return d;
+}
+__device__ __forceinline__ f2 sub2(f2 a, f2 b) {
+    f2 d;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d.v) : "l"(a.v), "l"(b.v));
+    return d;
+}
+__device__ __forceinline__ f2 mul2(f2 a, f2 b) {
+    f2 d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d.v) : "l"(a.v), "l"(b.v));
+    return d;
+}
+__device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c) {
+    f2 d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d.v) : "l"(a.v), "l"(b.v), "l"(c.v));
+    return d;
+}
+// scalar-broadcast forms (ptxas folds the pack into an `.F32` operand)
+__device__ __forceinline__ f2 subs(f2 a, float s) { return sub2(a, bcast(s)); }
+__device__ __forceinline__ f2 muls(f2 a, float s) { return mul2(a, bcast(s)); }
+__device__ __forceinline__ f2 fmas(f2 a, float s, f2 c) { return fma2(a, bcast(s), c); }
+__device__ __forceinline__ f2 sfma(float s, f2 b, f2 c) { return fma2(bcast(s), b, c); }
+
+// Accumulator of two queries: shifts, fp32 tile sums packed; fp64 totals
+// per query.
+struct Acc2 {
+    f2 m, s, gx, gy, gz;
+    double ts[2], tgx[2], tgy[2], tgz[2];
+    __device__ __forceinline__ void from(const Acc<float>& a, const Acc<float>& b) {
+        m = pack(a.m, b.m);
+        s = pack(a.s, b.s);
+        gx = pack(a.gx, b.gx);
+        gy = pack(a.gy, b.gy);
+        gz = pack(a.gz, b.gz);
+        ts[0] = a.ts; tgx[0] = a.tgx; tgy[0] = a.tgy; tgz[0] = a.tgz;
+        ts[1] = b.ts; tgx[1] = b.tgx; tgy[1] = b.tgy; tgz[1] = b.tgz;
+    }
+    __device__ __forceinline__ void to(Acc<float>& a, Acc<float>& b) const {
+        a.m = lo(m); a.s = lo(s); a.gx = lo(gx); a.gy = lo(gy); a.gz = lo(gz);
+        b.m = hi(m); b.s = hi(s); b.gx = hi(gx); b.gy = hi(gy); b.gz = hi(gz);
+        a.ts = ts[0]; a.tgx = tgx[0]; a.tgy = tgy[0]; a.tgz = tgz[0];
+        b.ts = ts[1]; b.tgx = tgx[1]; b.tgy = tgy[1]; b.tgz = tgz[1];
+    }
+    __device__ __forceinline__ void flush() {
+        ts[0] += double(lo(s)); tgx[0] += double(lo(gx)); tgy[0] += double(lo(gy)); tgz[0] += double(lo(gz));
+        ts[1] += double(hi(s)); tgx[1] += double(hi(gx)); tgy[1] += double(hi(gy)); tgz[1] += double(hi(gz));
+        s = gx = gy = gz = pack(0.f, 0.f);
+    }
+};
+
+// Raise the shift of one half (rare path, scalar); x = absolute exponent.
+__device__ __forceinline__ void bump_half(Acc2& a, int h, float x) {
+    float m[2] = {lo(a.m), hi(a.m)}, s[2] = {lo(a.s), hi(a.s)}, gx[2] = {lo(a.gx), hi(a.gx)},
+          gy[2] = {lo(a.gy), hi(a.gy)}, gz[2] = {lo(a.gz), hi(a.gz)};
+    const float mn = x + kHeadroom;
+    const float sc = Math<float>::ex2(m[h] - mn);
+    s[h] *= sc; gx[h] *= sc; gy[h] *= sc; gz[h] *= sc;
+    a.ts[h] *= double(sc); a.tgx[h] *= double(sc); a.tgy[h] *= double(sc); a.tgz[h] *= double(sc);
+    m[h] = mn;
+    a.m = pack(m[0], m[1]); a.s = pack(s[0], s[1]);
+    a.gx = pack(gx[0], gx[1]); a.gy = pack(gy[0], gy[1]); a.gz = pack(gz[0], gz[1]);
+}
+
+// Masks, re-anchors and exponentiates the packed x - m; `absx(h)` returns
+// the absolute exponent of half h (only evaluated on the rare path).
+template <class F>
+__device__ __forceinline__ f2 exp_terms(const Phys<float>& ph, Acc2& a, f2 d, f2 xm, F&& absx) {
+    float x0 = lo(xm), x1 = hi(xm);
+    x0 = lo(d) > ph.dmax ? -INFINITY : x0;
+    x1 = hi(d) > ph.dmax ? -INFINITY : x1;
+    if (x0 > 0.f || x1 > 0.f) {
+        if (x0 > 0.f) {
+            const float x = absx(0);
+            bump_half(a, 0, x);
+            x0 = x - lo(a.m);
+        }
+        if (x1 > 0.f) {
+            const float x = absx(1);
+            bump_half(a, 1, x);
+            x1 = x - hi(a.m);
+        }
+    }
+    return pack(Math<float>::ex2(x0), Math<float>::ex2(x1));
+}
+
+__device__ __forceinline__ f2 rsqrt2(f2 s) {
+    return pack(Math<float>::rsqrt(fmaxf(lo(s), Tiny<float>::v)), Math<float>::rsqrt(fmaxf(hi(s), Tiny<float>::v)));
+}
+
+// ------------------------------------------------------------- points
+__device__ __forceinline__ void point_term2(const Phys<float>& ph, f2 qx, f2 qy, f2 qz, const float* rec, Acc2& a) {
+    const f2 dx = subs(qx, rec[0]), dy = subs(qy, rec[1]), dz = subs(qz, rec[2]);
+    const f2 s = fma2(dx, dx, fma2(dy, dy, mul2(dz, dz)));
+    const f2 r = rsqrt2(s);
+    const f2 d = mul2(s, r);
+    const f2 xm = sub2(muls(d, ph.kappa), a.m);
+    const f2 e = exp_terms(ph, a, d, xm, [&](int h) { return ph.kappa * (h ? hi(d) : lo(d)); });
+    const f2 er = mul2(e, r);
+    a.s = add2(a.s, e);
+    a.gx = fma2(er, dx, a.gx);
+    a.gy = fma2(er, dy, a.gy);
+    a.gz = fma2(er, dz, a.gz);
+}
+
+// -------------------------------------------------------------- edges
+template <bool POLY, bool SAFE>
+__device__ __forceinline__ void edge_term2(const Phys<float>& ph, const Poly<float>& pc, f2 qx, f2 qy, f2 qz,
+                                           const float* rec, Acc2& a) {
+    const f2 apx = subs(qx, rec[0]), apy = subs(qy, rec[1]), apz = subs(qz, rec[2]);
+    const f2 dot = fmas(apx, rec[3], fmas(apy, rec[4], muls(apz, rec[5])));
+    const f2 t = pack(__saturatef(lo(dot) * rec[6]), __saturatef(hi(dot) * rec[6]));
+    const f2 dx = fmas(t, -rec[3], apx), dy = fmas(t, -rec[4], apy), dz = fmas(t, -rec[5], apz);
+    const f2 s = fma2(dx, dx, fma2(dy, dy, mul2(dz, dz)));
+    const f2 r = rsqrt2(s);
+    const f2 d = mul2(s, r);
+    const f2 xd = sub2(muls(d, ph.kappa), a.m);  // kappa d - m
+    if constexpr (POLY) {
+        const f2 base = fmas(t, pc.c[4], bcast(pc.c[3]));
+        const f2 base2 = fma2(t, fma2(t, fma2(t, base, bcast(pc.c[2])), bcast(pc.c[1])), bcast(pc.c[0]));
+        const f2 dn = fma2(t, fma2(t, fmas(t, pc.c[8], bcast(pc.c[7])), bcast(pc.c[6])), bcast(pc.c[5]));
+        const float l0 = Math<float>::lg2(lo(base2)), l1 = Math<float>::lg2(hi(base2));
+        const float i0 = Math<float>::rcp(lo(base2)), i1 = Math<float>::rcp(hi(base2));
+        f2 lw, k = mul2(dn, pack(i0, i1));
+        if constexpr (SAFE) {
+            lw = muls(pack(l0, l1), ph.S);
+        } else {
+            const bool ok0 = lo(base2) > 0.f, ok1 = hi(base2) > 0.f;
+            lw = pack(ok0 ? ph.S * l0 : ph.lw_floor, ok1 ? ph.S * l1 : ph.lw_floor);
+            k = pack(ok0 ? lo(k) : 0.f, ok1 ? hi(k) : 0.f);
+        }
+        const f2 e = exp_terms(ph, a, d, add2(lw, xd),
+                               [&](int h) { return fmaf(ph.kappa, h ? hi(d) : lo(d), h ? hi(lw) : lo(lw)); });
+        const f2 er = mul2(e, r), ek = mul2(e, k);
+        a.s = add2(a.s, e);
+        a.gx = fmas(ek, -rec[7], fma2(er, dx, a.gx));
+        a.gy = fmas(ek, -rec[8], fma2(er, dy, a.gy));
+        a.gz = fmas(ek, -rec[9], fma2(er, dz, a.gz));
+    } else {
+        const f2 e = exp_terms(ph, a, d, xd, [&](int h) { return ph.kappa * (h ? hi(d) : lo(d)); });
+        const f2 er = mul2(e, r);
+        a.s = add2(a.s, e);
+        a.gx = fma2(er, dx, a.gx);
+        a.gy = fma2(er, dy, a.gy);
+        a.gz = fma2(er, dz, a.gz);
+    }
+}
+
+}  // namespace sdgpu
