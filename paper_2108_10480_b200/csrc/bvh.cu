@@ -424,12 +424,14 @@ __global__ void __launch_bounds__(kTravThreads) traverse_kernel(const __grid_con
             id = id + 1;
         }
     }
-    acc.flush();
-    a.part[i] = double(acc.m);
-    a.part[a.Q + i] = acc.ts;
-    a.part[2 * a.Q + i] = acc.tgx;
-    a.part[3 * a.Q + i] = acc.tgy;
-    a.part[4 * a.Q + i] = acc.tgz;
+    Tot tot;
+    tot.init();
+    tot.flush(acc);
+    a.part[i] = tot.M;
+    a.part[a.Q + i] = tot.s;
+    a.part[2 * a.Q + i] = tot.gx;
+    a.part[3 * a.Q + i] = tot.gy;
+    a.part[4 * a.Q + i] = tot.gz;
     a.leaves[i] = nleaf;
     a.far[i] = nfar;
     a.hash[i] = h;
@@ -557,12 +559,14 @@ __global__ void __launch_bounds__(kTravThreads) packet_kernel(const __grid_const
         }
     }
     if (!valid) return;
-    acc.flush();
-    a.part[i] = double(acc.m);
-    a.part[a.Q + i] = acc.ts;
-    a.part[2 * a.Q + i] = acc.tgx;
-    a.part[3 * a.Q + i] = acc.tgy;
-    a.part[4 * a.Q + i] = acc.tgz;
+    Tot tot;
+    tot.init();
+    tot.flush(acc);
+    a.part[i] = tot.M;
+    a.part[a.Q + i] = tot.s;
+    a.part[2 * a.Q + i] = tot.gx;
+    a.part[3 * a.Q + i] = tot.gy;
+    a.part[4 * a.Q + i] = tot.gz;
     a.leaves[i] = nleaf;
     a.far[i] = nfar;
     if (HASH) a.hash[i] = h;

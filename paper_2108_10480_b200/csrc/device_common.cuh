@@ -60,30 +60,48 @@ template <> struct Vec4<double> { using type = double2; };
 // (fp32).
 constexpr float kHeadroom = 16.0f;
 
-// Two-level sums: terms accumulate in T (s, g) for at most one staged tile,
-// then flush() folds them into fp64 totals (ts, tg), so the fp32 rounding
-// error grows with the tile length (<= 768 terms), not with the number of
-// primitives (up to 2^24).
+// Two-level sums: terms accumulate in T (Acc: s, g relative to the shift
+// m) for at most one staged tile, then Tot::flush() folds them into fp64
+// totals kept relative to their own anchor M, so the fp32 rounding error
+// grows with the tile length (<= 768 terms), not with the number of
+// primitives (up to 2^24). The pair (M, totals) is the per-query state
+// carried between launches and merged by K4.
 template <class T>
 struct Acc {
     T m, s, gx, gy, gz;
-    double ts, tgx, tgy, tgz;
     __device__ __forceinline__ void init() {
         m = T(-INFINITY);  // no term yet
-        s = gx = gy = gz = T(0);
-        ts = tgx = tgy = tgz = 0.0;
-    }
-    __device__ __forceinline__ void flush() {
-        ts += double(s);
-        tgx += double(gx);
-        tgy += double(gy);
-        tgz += double(gz);
         s = gx = gy = gz = T(0);
     }
     __device__ __forceinline__ void scale(T sc) {
         s *= sc; gx *= sc; gy *= sc; gz *= sc;
-        const double d = double(sc);
-        ts *= d; tgx *= d; tgy *= d; tgz *= d;
+    }
+};
+
+struct Tot {
+    double M;  // anchor (log2); -inf: empty
+    double s, gx, gy, gz;
+    __device__ __forceinline__ void init() {
+        M = -INFINITY;
+        s = gx = gy = gz = 0.0;
+    }
+    // adds acc's tile sums (relative to acc.m) and clears them
+    template <class T>
+    __device__ __forceinline__ void flush(Acc<T>& a) {
+        if (a.s != T(0)) {
+            const double m = double(a.m);
+            if (m > M + 512.0 || M == -INFINITY) {  // (re-)anchor; rare
+                const double f = M == -INFINITY ? 0.0 : exp2(M - m);
+                s *= f; gx *= f; gy *= f; gz *= f;
+                M = m;
+            }
+            const double f = exp2(m - M);
+            s = fma(double(a.s), f, s);
+            gx = fma(double(a.gx), f, gx);
+            gy = fma(double(a.gy), f, gy);
+            gz = fma(double(a.gz), f, gz);
+        }
+        a.s = a.gx = a.gy = a.gz = T(0);
     }
 };
 

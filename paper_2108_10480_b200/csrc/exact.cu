@@ -37,8 +37,9 @@ constexpr int kStages = 3;
 
 template <class T, int KIND>
 constexpr int tile_prims() {
-    // ~12 KB (fp32) / 24 KB (fp64) per stage
-    return KIND == 0 ? 768 : (KIND == 1 ? 256 : 128);
+    // 6-12 KB (fp32) / 12-24 KB (fp64) per stage, so that 3 stages plus the
+    // fp64 per-query totals leave room for 3 resident CTAs per SM
+    return KIND == 0 ? 512 : 128;
 }
 
 template <class T, int KIND, bool POLY, bool SAFE, int QPT>
@@ -47,6 +48,8 @@ __global__ void __launch_bounds__(kThreads) exact_kernel(const __grid_constant__
     constexpr int TILE = tile_prims<T, KIND>();
     extern __shared__ __align__(128) unsigned char smem_raw[];
     T* tiles = reinterpret_cast<T*>(smem_raw);
+    // fp64 per-query totals live in shared memory (touched once per tile)
+    Tot* tot = reinterpret_cast<Tot*>(smem_raw + size_t(kStages) * TILE * R * sizeof(T));
     __shared__ uint64_t full[kStages];
 
     const int split = blockIdx.y;
@@ -83,15 +86,16 @@ __global__ void __launch_bounds__(kThreads) exact_kernel(const __grid_constant__
         qx[k] = a.q[3 * qc];
         qy[k] = a.q[3 * qc + 1];
         qz[k] = a.q[3 * qc + 2];
-        if (a.first) {
-            acc[k].init();
-        } else {
-            acc[k].init();
-            acc[k].m = T(part[qc]);
-            acc[k].ts = part[a.Q + qc];
-            acc[k].tgx = part[2 * a.Q + qc];
-            acc[k].tgy = part[3 * a.Q + qc];
-            acc[k].tgz = part[4 * a.Q + qc];
+        acc[k].init();
+        Tot& tk = tot[k * kThreads + threadIdx.x];
+        tk.init();
+        if (!a.first) {
+            tk.M = part[qc];
+            tk.s = part[a.Q + qc];
+            tk.gx = part[2 * a.Q + qc];
+            tk.gy = part[3 * a.Q + qc];
+            tk.gz = part[4 * a.Q + qc];
+            acc[k].m = T(tk.M);
         }
         // unit-weight launches keep the shift relative to log2 w = S log2 A
         if constexpr (!POLY) acc[k].m -= a.ph.lw_unit;
@@ -141,28 +145,31 @@ __global__ void __launch_bounds__(kThreads) exact_kernel(const __grid_constant__
         }
         if constexpr (PACKED) {
 #pragma unroll
-            for (int k = 0; k < QPT / 2; ++k) acc2[k].flush();
-        } else {
+            for (int k = 0; k < QPT / 2; ++k) acc2[k].to(acc[2 * k], acc[2 * k + 1]);
+        }
 #pragma unroll
-            for (int k = 0; k < QPT; ++k) acc[k].flush();
+        for (int k = 0; k < QPT; ++k) {
+            if constexpr (!POLY) acc[k].m += a.ph.lw_unit;  // totals are absolute
+            tot[k * kThreads + threadIdx.x].flush(acc[k]);
+            if constexpr (!POLY) acc[k].m -= a.ph.lw_unit;
+        }
+        if constexpr (PACKED) {
+#pragma unroll
+            for (int k = 0; k < QPT / 2; ++k) acc2[k].from(acc[2 * k], acc[2 * k + 1]);
         }
         __syncthreads();  // every thread is done with stage s
         if (threadIdx.x == 0 && t + kStages < ntiles) issue(t + kStages);
-    }
-    if constexpr (PACKED) {
-#pragma unroll
-        for (int k = 0; k < QPT / 2; ++k) acc2[k].to(acc[2 * k], acc[2 * k + 1]);
     }
 
 #pragma unroll
     for (int k = 0; k < QPT; ++k) {
         if (qi[k] >= a.Q) continue;
-        if constexpr (!POLY) acc[k].m += a.ph.lw_unit;
-        part[qi[k]] = double(acc[k].m);
-        part[a.Q + qi[k]] = acc[k].ts;
-        part[2 * a.Q + qi[k]] = acc[k].tgx;
-        part[3 * a.Q + qi[k]] = acc[k].tgy;
-        part[4 * a.Q + qi[k]] = acc[k].tgz;
+        const Tot& tk = tot[k * kThreads + threadIdx.x];
+        part[qi[k]] = tk.M;
+        part[a.Q + qi[k]] = tk.s;
+        part[2 * a.Q + qi[k]] = tk.gx;
+        part[3 * a.Q + qi[k]] = tk.gy;
+        part[4 * a.Q + qi[k]] = tk.gz;
     }
 }
 
@@ -176,7 +183,7 @@ static cudaError_t launch_one(const ExactLaunch<T>& L, cudaStream_t st) {
     constexpr int R = rec_size(KIND);
     constexpr int TILE = tile_prims<T, KIND>();
     constexpr int QPT = qpt_for<KIND>();
-    const size_t smem = size_t(kStages) * TILE * R * sizeof(T);
+    const size_t smem = size_t(kStages) * TILE * R * sizeof(T) + size_t(QPT) * kThreads * sizeof(Tot);
     auto kern = exact_kernel<T, KIND, POLY, SAFE, QPT>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
@@ -200,7 +207,7 @@ template <class T, int KIND, bool POLY, bool SAFE>
 static int occupancy_one() {
     constexpr int R = rec_size(KIND);
     constexpr int TILE = tile_prims<T, KIND>();
-    const size_t smem = size_t(kStages) * TILE * R * sizeof(T);
+    const size_t smem = size_t(kStages) * TILE * R * sizeof(T) + size_t(qpt_for<KIND>()) * kThreads * sizeof(Tot);
     auto kern = exact_kernel<T, KIND, POLY, SAFE, qpt_for<KIND>()>;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess) return 1;
     int n = 1;

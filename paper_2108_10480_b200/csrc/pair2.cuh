@@ -56,30 +56,19 @@ __device__ __forceinline__ f2 muls(f2 a, float s) { return mul2(a, bcast(s)); }
 __device__ __forceinline__ f2 fmas(f2 a, float s, f2 c) { return fma2(a, bcast(s), c); }
 __device__ __forceinline__ f2 sfma(float s, f2 b, f2 c) { return fma2(bcast(s), b, c); }
 
-// Accumulator of two queries: shifts, fp32 tile sums packed; fp64 totals
-// per query.
+// Accumulator of two queries: shifts and fp32 tile sums, packed.
 struct Acc2 {
     f2 m, s, gx, gy, gz;
-    double ts[2], tgx[2], tgy[2], tgz[2];
     __device__ __forceinline__ void from(const Acc<float>& a, const Acc<float>& b) {
         m = pack(a.m, b.m);
         s = pack(a.s, b.s);
         gx = pack(a.gx, b.gx);
         gy = pack(a.gy, b.gy);
         gz = pack(a.gz, b.gz);
-        ts[0] = a.ts; tgx[0] = a.tgx; tgy[0] = a.tgy; tgz[0] = a.tgz;
-        ts[1] = b.ts; tgx[1] = b.tgx; tgy[1] = b.tgy; tgz[1] = b.tgz;
     }
     __device__ __forceinline__ void to(Acc<float>& a, Acc<float>& b) const {
         a.m = lo(m); a.s = lo(s); a.gx = lo(gx); a.gy = lo(gy); a.gz = lo(gz);
         b.m = hi(m); b.s = hi(s); b.gx = hi(gx); b.gy = hi(gy); b.gz = hi(gz);
-        a.ts = ts[0]; a.tgx = tgx[0]; a.tgy = tgy[0]; a.tgz = tgz[0];
-        b.ts = ts[1]; b.tgx = tgx[1]; b.tgy = tgy[1]; b.tgz = tgz[1];
-    }
-    __device__ __forceinline__ void flush() {
-        ts[0] += double(lo(s)); tgx[0] += double(lo(gx)); tgy[0] += double(lo(gy)); tgz[0] += double(lo(gz));
-        ts[1] += double(hi(s)); tgx[1] += double(hi(gx)); tgy[1] += double(hi(gy)); tgz[1] += double(hi(gz));
-        s = gx = gy = gz = pack(0.f, 0.f);
     }
 };
 
@@ -90,7 +79,6 @@ __device__ __forceinline__ void bump_half(Acc2& a, int h, float x) {
     const float mn = x + kHeadroom;
     const float sc = Math<float>::ex2(m[h] - mn);
     s[h] *= sc; gx[h] *= sc; gy[h] *= sc; gz[h] *= sc;
-    a.ts[h] *= double(sc); a.tgx[h] *= double(sc); a.tgy[h] *= double(sc); a.tgz[h] *= double(sc);
     m[h] = mn;
     a.m = pack(m[0], m[1]); a.s = pack(s[0], s[1]);
     a.gx = pack(gx[0], gx[1]); a.gy = pack(gy[0], gy[1]); a.gz = pack(gz[0], gz[1]);
