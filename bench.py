@@ -35,7 +35,7 @@ FLOPS_PER_EDGE_PAIR = 62      # SURVEY 8(d) canonical count, S != 1
 FLOPS_PER_TRI_PAIR = 192
 FLOPS_BOX_TEST, FLOPS_FAR_TERM = 10, 12
 BYTES_NODE, BYTES_LEAF = 32, 100  # fp32 traversal node record; leaf record (96 B) + meta
-MUFU_PER_EDGE_PAIR = 5
+MUFU_PER_EDGE_PAIR = 4            # rsqrt, lg2, rcp, ex2
 QUERIES_PER_GPU = 262144
 ALPHA = 100.0
 
@@ -117,13 +117,26 @@ def measure_peaks():
     return out
 
 
-def workload(block: int):
+def workload(block: int, cfg: int = 2, alpha: float | None = None):
+    """cfg2 (headline) or cfg3 (triangles, --config 3): mesh, fp32-rounded
+    vertices and queries, and the WeightSet table."""
     from paper_2108_10480_b200 import configs
-    w, q = configs.cfg2(QUERIES_PER_GPU, block=block)
-    v = configs.quantize(w.vertices)
-    q = configs.quantize(q)
-    wt = configs.weights_without_triangles(w.simplices, w.kinds, len(v))
-    return w, v, q, wt
+    if cfg == 2:
+        w, q = configs.cfg2(QUERIES_PER_GPU, block=block)
+        wt = configs.weights_without_triangles(w.simplices, w.kinds, len(w.vertices))
+    else:
+        V, T = configs.torus()
+        rng = np.random.default_rng([3002, block])
+        lo, hi = V.min(0) - 0.5, V.max(0) + 0.5
+        q = rng.uniform(lo, hi, (1048576, 3))
+        w = configs.Workload("cfg3 torus 262,144 triangles, exact LSE", V, T, np.full(len(T), 2, np.uint8),
+                             alpha=alpha or 100.0)
+        import paper_2108_10480_b200 as sd
+        e = sd.Engine(0, sd.SD_FP32)
+        e.set_geometry(configs.quantize(V), T, w.kinds)
+        wt = e.build_weights()
+        e.close()
+    return w, configs.quantize(w.vertices), configs.quantize(q), wt
 
 
 def cpu_sample(v, s, k, wt, q, threads, target_s=12.0):
@@ -258,7 +271,11 @@ def run_ours(args, rank, world, local):
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    w, v, q, wt = workload(rank)
+    w, v, q, wt = workload(rank, args.config, args.alpha)
+    global ALPHA, FLOPS_PER_EDGE_PAIR, MUFU_PER_EDGE_PAIR
+    if args.config == 3:
+        ALPHA = w.alpha
+        FLOPS_PER_EDGE_PAIR, MUFU_PER_EDGE_PAIR = FLOPS_PER_TRI_PAIR, 4
     N, Q = len(w.kinds), len(q)
     eng = sd.Engine(local, sd.SD_FP32)
     eng.set_geometry(v, w.simplices, w.kinds)
@@ -328,8 +345,9 @@ def run_ours(args, rank, world, local):
     if rank == 0:
         achieved = pairs_per_rank * FLOPS_PER_EDGE_PAIR / (ms_max * 1e-3) / 1e12
         roof = {"bound": "fp32-fma", "achieved": achieved, "unit": "TFLOP/s", "traffic": None,
-                "kernel": "exact_kernel<float, edge, poly> x3 segment launches + finalize (step time)",
-                "algorithmic": f"{FLOPS_PER_EDGE_PAIR} flop x {pairs_per_rank} edge pairs per step"}
+                "kernel": ("exact_kernel<float, edge, poly> x3 segment launches" if args.config == 2 else
+                           "exact_kernel<float, triangle, poly>") + " + finalize (step time)",
+                "algorithmic": f"{FLOPS_PER_EDGE_PAIR} flop x {pairs_per_rank} pairs per step (SURVEY 8d)"}
         if peaks:
             roof.update({"peak": peaks["ffma_tflops"], "frac": achieved / peaks["ffma_tflops"],
                          "peak_source": "in-run FFMA microbenchmark (libsdpeaks.so); MEASURED_PEAKS.json has no FP32 entry",
@@ -342,13 +360,16 @@ def run_ours(args, rank, world, local):
             threads = O.hardware_threads()
             n, secs, _ = cpu_sample(v, w.simplices, w.kinds, wt, q, threads)
             cpu = {"value": n * N / secs, "unit": "pair-evals/s", "cores": threads, "kind": "port",
-                   "sample": f"first {n} of {Q} cfg2 queries x {N} edges ({secs:.1f} s, fp64 oracle port)"}
+                   "sample": f"first {n} of {Q} cfg{args.config} queries x {N} primitives ({secs:.1f} s, "
+                             f"fp64 oracle port)"}
         line = {
             "metric": "exact pair-evals/s (value+grad)", "value": value, "unit": "pair-evals/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": "cfg2: helix polyline 20,000 edges x 262,144 queries per GPU, exact LSE, "
-                                   "alpha=100, fp32 (BASELINE configs[1])",
+            "config": {"workload": ("cfg2: helix polyline 20,000 edges x 262,144 queries per GPU, exact LSE, "
+                                    "alpha=100, fp32 (BASELINE configs[1])") if args.config == 2 else
+                                   (f"cfg3: torus 262,144 triangles x 1,048,576 queries per GPU, exact LSE, "
+                                    f"alpha={ALPHA:g}, fp32 (BASELINE configs[2])"),
                        "queries_per_gpu": Q, "primitives": N, "l2": "flushed between timed steps (256 MiB write)",
                        "parallelism": f"query-sharded x{world}, geometry replicated"},
             "roofline": roof,
@@ -373,6 +394,9 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-bvh", action="store_true", help="skip the secondary BVH (cfg4) measurement")
+    ap.add_argument("--config", type=int, default=2, choices=[2, 3],
+                    help="exact workload: 2 = BASELINE configs[1] (headline), 3 = configs[2] torus triangles")
+    ap.add_argument("--alpha", type=float, default=None, help="alpha for --config 3 (10, 100 or 1000)")
     args = ap.parse_args()
     rank, world, local = dist_env()
     if args.impl == "reference":

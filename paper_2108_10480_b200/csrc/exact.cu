@@ -101,8 +101,8 @@ __global__ void __launch_bounds__(kThreads) exact_kernel(const __grid_constant__
         if constexpr (!POLY) acc[k].m -= a.ph.lw_unit;
     }
 
-    // fp32 points / edges: two queries per packed fp32x2 instruction
-    constexpr bool PACKED = sizeof(T) == 4 && KIND < 2 && QPT % 2 == 0;
+    // fp32: two queries per packed fp32x2 instruction
+    constexpr bool PACKED = sizeof(T) == 4 && QPT % 2 == 0;
     [[maybe_unused]] Acc2 acc2[PACKED ? QPT / 2 : 1];
     [[maybe_unused]] f2 q2x[PACKED ? QPT / 2 : 1], q2y[PACKED ? QPT / 2 : 1], q2z[PACKED ? QPT / 2 : 1];
     if constexpr (PACKED) {
@@ -132,7 +132,9 @@ __global__ void __launch_bounds__(kThreads) exact_kernel(const __grid_constant__
 #pragma unroll
                 for (int k = 0; k < QPT / 2; ++k) {
                     if constexpr (KIND == 0) point_term2(a.ph, q2x[k], q2y[k], q2z[k], (const float*)rec, acc2[k]);
-                    else edge_term2<POLY, SAFE>(a.ph, a.poly, q2x[k], q2y[k], q2z[k], (const float*)rec, acc2[k]);
+                    else if constexpr (KIND == 1)
+                        edge_term2<POLY, SAFE>(a.ph, a.poly, q2x[k], q2y[k], q2z[k], (const float*)rec, acc2[k]);
+                    else tri_term2<POLY, SAFE>(a.ph, a.poly, q2x[k], q2y[k], q2z[k], (const float*)rec, acc2[k]);
                 }
             } else {
 #pragma unroll

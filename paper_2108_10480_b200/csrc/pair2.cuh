@@ -168,4 +168,108 @@ __device__ __forceinline__ void edge_term2(const Phys<float>& ph, const Poly<flo
     }
 }
 
+// ----------------------------------------------------------- triangles
+__device__ __forceinline__ f2 hz(f2 x, f2 acc, float c) { return fma2(x, acc, bcast(c)); }  // x acc + c
+
+// packed tri_poly (pair.cuh): base = A w~ and K-scaled d/dx, d/dy
+__device__ __forceinline__ void tri_poly2(const Poly<float>& p, f2 x, f2 y, f2& w, f2& wx, f2& wy) {
+    const float* c = p.c;
+    const f2 y2 = mul2(y, y), x2 = mul2(x, x);
+    const f2 P0 = hz(y2, hz(y, hz(y, hz(y, hz(y, fmas(y, c[6], bcast(c[5])), c[4]), c[3]), c[2]), c[1]), c[0]);
+    const f2 P2 = hz(y2, hz(y, hz(y, fmas(y, c[11], bcast(c[10])), c[9]), c[8]), c[7]);
+    const f2 P3 = hz(y2, hz(y, fmas(y, c[15], bcast(c[14])), c[13]), c[12]);
+    const f2 P4 = hz(y2, fmas(y, c[18], bcast(c[17])), c[16]);
+    const f2 P5 = fmas(y2, c[20], bcast(c[19]));
+    w = fma2(x2, fma2(x, fma2(x, fma2(x, fma2(x, fmas(x, c[22], bcast(c[21])), P5), P4), P3), P2), P0);
+    const f2 Q2 = hz(y2, hz(y, hz(y, fmas(y, c[27], bcast(c[26])), c[25]), c[24]), c[23]);
+    const f2 Q3 = hz(y2, hz(y, fmas(y, c[31], bcast(c[30])), c[29]), c[28]);
+    const f2 Q4 = hz(y2, fmas(y, c[34], bcast(c[33])), c[32]);
+    const f2 Q5 = fmas(y2, c[36], bcast(c[35]));
+    wx = mul2(x, fma2(x, fma2(x, fma2(x, fma2(x, fmas(x, c[38], bcast(c[37])), Q5), Q4), Q3), Q2));
+    const f2 R0 = mul2(y, hz(y, hz(y, hz(y, hz(y, fmas(y, c[44], bcast(c[43])), c[42]), c[41]), c[40]), c[39]));
+    const f2 R2 = mul2(y, hz(y, hz(y, fmas(y, c[48], bcast(c[47])), c[46]), c[45]));
+    const f2 R3 = mul2(y, hz(y, fmas(y, c[51], bcast(c[50])), c[49]));
+    const f2 R4 = mul2(y, fmas(y, c[53], bcast(c[52])));
+    const f2 R5 = muls(y, c[54]);
+    wy = fma2(x2, fma2(x, fma2(x, fma2(x, R5, R4), R3), R2), R0);
+}
+
+// packed Ericson regions: the dot products and candidates are packed, the
+// region selects are per query (pair.cuh tri_closest)
+__device__ __forceinline__ void tri_closest2(const float* rec, f2 d1, f2 d2, f2& u, f2& v) {
+    const float A = rec[9], B = rec[10], C = rec[11];
+    const f2 d3 = subs(d1, A), d4 = subs(d2, B), d5 = subs(d1, B), d6 = subs(d2, C);
+    const f2 vc = fma2(d1, d4, mul2(pack(-lo(d3), -hi(d3)), d2));
+    const f2 vb = fma2(d5, d2, mul2(pack(-lo(d1), -hi(d1)), d6));
+    const f2 va = fma2(d3, d6, mul2(pack(-lo(d5), -hi(d5)), d4));
+    const f2 e43 = sub2(d4, d3), e56 = sub2(d5, d6);
+    const f2 ui = muls(vb, rec[15]), vi = muls(vc, rec[15]);
+    const f2 t6 = muls(e43, rec[14]);
+    const f2 vac = muls(d2, rec[13]), uab = muls(d1, rec[12]);
+    float uu[2], vv[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        auto g = [h](f2 a) { return h ? hi(a) : lo(a); };
+        float U = g(ui), V = g(vi);
+        const float D1 = g(d1), D2 = g(d2), D3 = g(d3), D4 = g(d4), D5 = g(d5), D6 = g(d6);
+        const float T6 = g(t6);
+        if (g(va) <= 0.f && g(e43) >= 0.f && g(e56) >= 0.f) { U = 1.f - T6; V = T6; }
+        if (g(vb) <= 0.f && D2 >= 0.f && D6 <= 0.f) { U = 0.f; V = g(vac); }
+        if (g(vc) <= 0.f && D1 >= 0.f && D3 <= 0.f) { U = g(uab); V = 0.f; }
+        if (D6 >= 0.f && D5 <= D6) { U = 0.f; V = 1.f; }
+        if (D3 >= 0.f && D4 <= D3) { U = 1.f; V = 0.f; }
+        if (D1 <= 0.f && D2 <= 0.f) { U = 0.f; V = 0.f; }
+        uu[h] = U;
+        vv[h] = V;
+    }
+    u = pack(uu[0], uu[1]);
+    v = pack(vv[0], vv[1]);
+}
+
+template <bool POLY, bool SAFE>
+__device__ __forceinline__ void tri_term2(const Phys<float>& ph, const Poly<float>& pc, f2 qx, f2 qy, f2 qz,
+                                          const float* rec, Acc2& a) {
+    const f2 apx = subs(qx, rec[0]), apy = subs(qy, rec[1]), apz = subs(qz, rec[2]);
+    const f2 d1 = fmas(apx, rec[3], fmas(apy, rec[4], muls(apz, rec[5])));
+    const f2 d2 = fmas(apx, rec[6], fmas(apy, rec[7], muls(apz, rec[8])));
+    f2 u, v;
+    tri_closest2(rec, d1, d2, u, v);
+    const f2 dx = fmas(v, -rec[6], fmas(u, -rec[3], apx));
+    const f2 dy = fmas(v, -rec[7], fmas(u, -rec[4], apy));
+    const f2 dz = fmas(v, -rec[8], fmas(u, -rec[5], apz));
+    const f2 s = fma2(dx, dx, fma2(dy, dy, mul2(dz, dz)));
+    const f2 r = rsqrt2(s);
+    const f2 d = mul2(s, r);
+    const f2 xd = sub2(muls(d, ph.kappa), a.m);
+    if constexpr (POLY) {
+        f2 base, wx, wy;
+        tri_poly2(pc, u, v, base, wx, wy);
+        const float l0 = Math<float>::lg2(lo(base)), l1 = Math<float>::lg2(hi(base));
+        f2 k = pack(Math<float>::rcp(lo(base)), Math<float>::rcp(hi(base)));
+        f2 lw;
+        if constexpr (SAFE) {
+            lw = muls(pack(l0, l1), ph.S);
+        } else {
+            const bool ok0 = lo(base) > 0.f, ok1 = hi(base) > 0.f;
+            lw = pack(ok0 ? ph.S * l0 : ph.lw_floor, ok1 ? ph.S * l1 : ph.lw_floor);
+            k = pack(ok0 ? lo(k) : 0.f, ok1 ? hi(k) : 0.f);
+        }
+        const f2 e = exp_terms(ph, a, d, add2(lw, xd),
+                               [&](int h) { return fmaf(ph.kappa, h ? hi(d) : lo(d), h ? hi(lw) : lo(lw)); });
+        const f2 er = mul2(e, r), ek = mul2(e, k);
+        const f2 kx = mul2(ek, wx), ky = mul2(ek, wy);
+        a.s = add2(a.s, e);
+        a.gx = fmas(ky, -rec[19], fmas(kx, -rec[16], fma2(er, dx, a.gx)));
+        a.gy = fmas(ky, -rec[20], fmas(kx, -rec[17], fma2(er, dy, a.gy)));
+        a.gz = fmas(ky, -rec[21], fmas(kx, -rec[18], fma2(er, dz, a.gz)));
+    } else {
+        const f2 e = exp_terms(ph, a, d, xd, [&](int h) { return ph.kappa * (h ? hi(d) : lo(d)); });
+        const f2 er = mul2(e, r);
+        a.s = add2(a.s, e);
+        a.gx = fma2(er, dx, a.gx);
+        a.gy = fma2(er, dy, a.gy);
+        a.gz = fma2(er, dz, a.gz);
+    }
+}
+
 }  // namespace sdgpu
