@@ -121,6 +121,11 @@ def workload(block: int, cfg: int = 2, alpha: float | None = None):
     """cfg2 (headline) or cfg3 (triangles, --config 3): mesh, fp32-rounded
     vertices and queries, and the WeightSet table."""
     from paper_2108_10480_b200 import configs
+    if cfg == 1:
+        w, q = configs.cfg1()
+        q = np.random.default_rng([1002, block]).uniform(-2, 2, q.shape)
+        wt = configs.weights_without_triangles(w.simplices, w.kinds, len(w.vertices))
+        return w, w.vertices, q, wt  # fp64 config: no rounding
     if cfg == 2:
         w, q = configs.cfg2(QUERIES_PER_GPU, block=block)
         wt = configs.weights_without_triangles(w.simplices, w.kinds, len(w.vertices))
@@ -263,6 +268,99 @@ def measure_bvh(args, rank, world, local, eng_cls, dev, stream, flush, peaks):
     return out
 
 
+def run_cfg5(args, rank, world, local):
+    """BASELINE configs[4]: mixed scene (16.8M triangles + 1M edges + 1M
+    points), 16,777,216 queries, alpha 100, beta 0.5, PRIMITIVE-sharded over
+    the ranks (Morton-contiguous shards, one GPU LBVH per shard, global
+    WeightSet), per-query fp64 partials merged with ONE NCCL all-reduce,
+    then sd_finalize_device. Strong scaling (fixed total work)."""
+    import torch
+    import paper_2108_10480_b200 as sd
+    from paper_2108_10480_b200 import configs, sharding
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    t0 = time.perf_counter()
+    w, q = configs.cfg5()
+    v, q = configs.quantize(w.vertices), configs.quantize(q)
+    tg = time.perf_counter() - t0
+    eg = sd.Engine(local, sd.SD_FP32)  # host-side: global WeightSet on the full mesh
+    eg.set_geometry(v, w.simplices, w.kinds)
+    tw = time.perf_counter()
+    wt = eg.build_weights()
+    tw = time.perf_counter() - tw
+    eg.close()
+    sh = sharding.primitive_shards(v, w.simplices, w.kinds, wt.poly_index, world)[rank]
+    eng = sd.Engine(local, sd.SD_FP32)
+    eng.set_geometry(sh.vertices, sh.simplices, sh.kinds)
+    eng.set_weights(wt.A, wt.sup_wtilde, wt.edge_a, wt.tri_stored, sh.poly_index)
+    tb = time.perf_counter()
+    eng.build_bvh(sd.SD_BVH_LBVH)
+    tb = time.perf_counter() - tb
+    Q = len(q)
+    P = sd.SmoothParams(alpha=w.alpha, alpha_u=600.0, beta=w.beta)
+    qd = torch.tensor(q, dtype=torch.float32, device=dev)
+    buf = torch.empty(4 * Q, dtype=torch.float64, device=dev)  # [c | grad_c AoS]: one all-reduce
+    d_hat = torch.empty(Q, dtype=torch.float64, device=dev)
+    grad = torch.empty(Q, 3, dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    launches = [0]
+
+    def step():
+        eng.query_points_device(qd.data_ptr(), Q, P, sd.SD_BVH, d_hat.data_ptr(), c_ptr=buf.data_ptr(),
+                                grad_c_ptr=buf.data_ptr() + 8 * Q, stream=stream.cuda_stream)
+        launches[0] = eng.last_launch_count() + 1  # + the finalize kernel below
+        if world > 1:
+            torch.distributed.all_reduce(buf, op=torch.distributed.ReduceOp.SUM)
+        eng.finalize_device(buf.data_ptr(), buf.data_ptr() + 8 * Q, Q, P, d_hat.data_ptr(), grad.data_ptr(),
+                            stream=stream.cuda_stream)
+
+    step()
+    torch.cuda.synchronize()
+    setup = time.perf_counter() - t0
+    for _ in range(max(3, args.warmup) - 1):
+        step()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.zero_()
+            evs[i][0].record(stream)
+            step()
+            evs[i][1].record(stream)
+        torch.cuda.synchronize()
+    ms = float(np.mean([a.elapsed_time(b) for a, b in evs]))
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        torch.distributed.barrier()
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    ms = float(t.item())
+    fin = float(torch.isfinite(d_hat).double().mean().item())
+    if rank == 0:
+        line = {"metric": "BVH queries/s (value+grad), primitive-sharded", "value": Q / (ms * 1e-3),
+                "unit": "queries/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+                "dtype": "f32", "data": "synthetic",
+                "config": {"workload": "cfg5: 64 rotated cfg3 tori (16,777,216 triangles) + 1M edges + 1M points, "
+                                       "16,777,216 queries uniform in the scene AABB, alpha=100, beta=0.5, fp32 "
+                                       "(BASELINE configs[4])",
+                           "parallelism": f"primitive-sharded x{world} (Morton shards, LBVH per shard), one "
+                                          f"NCCL all_reduce(SUM) of 4 fp64 per query",
+                           "primitives_per_gpu": len(sh.kinds), "l2": "flushed between timed steps"},
+                "finite_fraction": fin, "gpu_launches": launches[0] * args.steps,
+                "setup_s": {"total": setup, "generate": tg, "build_weights": tw, "build_lbvh": tb},
+                "clocks": clk.summary()}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
 def run_ours(args, rank, world, local):
     import torch
     import paper_2108_10480_b200 as sd
@@ -276,14 +374,19 @@ def run_ours(args, rank, world, local):
     if args.config == 3:
         ALPHA = w.alpha
         FLOPS_PER_EDGE_PAIR, MUFU_PER_EDGE_PAIR = FLOPS_PER_TRI_PAIR, 4
+    if args.config == 1:
+        ALPHA = w.alpha
+        FLOPS_PER_EDGE_PAIR, MUFU_PER_EDGE_PAIR = 20, 2
+    fp64 = args.config == 1 or args.fp64
+    prec = sd.SD_FP64 if fp64 else sd.SD_FP32
     N, Q = len(w.kinds), len(q)
-    eng = sd.Engine(local, sd.SD_FP32)
+    eng = sd.Engine(local, prec)
     eng.set_geometry(v, w.simplices, w.kinds)
     eng.set_weights(wt.A, wt.sup_wtilde, wt.edge_a, wt.tri_stored, wt.poly_index)
     P = sd.SmoothParams(alpha=ALPHA, alpha_u=600.0, beta=0.0)
 
     dev = torch.device("cuda", local)
-    qd = torch.tensor(q, dtype=torch.float32, device=dev)
+    qd = torch.tensor(q, dtype=torch.float64 if fp64 else torch.float32, device=dev)
     d_hat = torch.empty(Q, dtype=torch.float64, device=dev)
     grad = torch.empty(Q, 3, dtype=torch.float64, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
@@ -344,13 +447,16 @@ def run_ours(args, rank, world, local):
     bvh = None if args.no_bvh else measure_bvh(args, rank, world, local, sd.Engine, dev, stream, flush, peaks)
     if rank == 0:
         achieved = pairs_per_rank * FLOPS_PER_EDGE_PAIR / (ms_max * 1e-3) / 1e12
-        roof = {"bound": "fp32-fma", "achieved": achieved, "unit": "TFLOP/s", "traffic": None,
+        roof = {"bound": "fp64-fma" if fp64 else "fp32-fma", "achieved": achieved, "unit": "TFLOP/s",
+                "traffic": None,
                 "kernel": ("exact_kernel<float, edge, poly> x3 segment launches" if args.config == 2 else
                            "exact_kernel<float, triangle, poly>") + " + finalize (step time)",
                 "algorithmic": f"{FLOPS_PER_EDGE_PAIR} flop x {pairs_per_rank} pairs per step (SURVEY 8d)"}
         if peaks:
-            roof.update({"peak": peaks["ffma_tflops"], "frac": achieved / peaks["ffma_tflops"],
-                         "peak_source": "in-run FFMA microbenchmark (libsdpeaks.so); MEASURED_PEAKS.json has no FP32 entry",
+            pk = peaks["dfma_tflops"] if fp64 else peaks["ffma_tflops"]
+            roof.update({"peak": pk, "frac": achieved / pk,
+                         "peak_source": f"in-run {'DFMA' if fp64 else 'FFMA'} microbenchmark (libsdpeaks.so); "
+                                        "MEASURED_PEAKS.json has no FP32/FP64 entry",
                          "mufu_frac": pairs_per_rank * MUFU_PER_EDGE_PAIR / (ms_max * 1e-3) / 1e12 / peaks["mufu_tops"],
                          "peaks": peaks})
         cpu = None
@@ -365,9 +471,10 @@ def run_ours(args, rank, world, local):
         line = {
             "metric": "exact pair-evals/s (value+grad)", "value": value, "unit": "pair-evals/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": ("cfg2: helix polyline 20,000 edges x 262,144 queries per GPU, exact LSE, "
-                                    "alpha=100, fp32 (BASELINE configs[1])") if args.config == 2 else
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64" if fp64 else "f32", "data": "synthetic",
+            "config": {"workload": "cfg1: 4,096 unit-sphere points x 65,536 queries per GPU, exact LSE, alpha=50, fp64 "
+                                   "(BASELINE configs[0])" if args.config == 1 else ("cfg2: helix polyline 20,000 edges x 262,144 queries per GPU, exact LSE, "
+                                    f"alpha=100, {'fp64' if fp64 else 'fp32'} (BASELINE configs[1])") if args.config == 2 else
                                    (f"cfg3: torus 262,144 triangles x 1,048,576 queries per GPU, exact LSE, "
                                     f"alpha={ALPHA:g}, fp32 (BASELINE configs[2])"),
                        "queries_per_gpu": Q, "primitives": N, "l2": "flushed between timed steps (256 MiB write)",
@@ -394,13 +501,17 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-bvh", action="store_true", help="skip the secondary BVH (cfg4) measurement")
-    ap.add_argument("--config", type=int, default=2, choices=[2, 3],
-                    help="exact workload: 2 = BASELINE configs[1] (headline), 3 = configs[2] torus triangles")
+    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 5],
+                    help="exact workload: 2 = BASELINE configs[1] (headline), 1 = configs[0] fp64 points, "
+                         "3 = configs[2] torus triangles, 5 = configs[4] primitive-sharded BVH")
+    ap.add_argument("--fp64", action="store_true", help="fp64 arithmetic for --config 2")
     ap.add_argument("--alpha", type=float, default=None, help="alpha for --config 3 (10, 100 or 1000)")
     args = ap.parse_args()
     rank, world, local = dist_env()
     if args.impl == "reference":
         run_reference(args, rank, world)
+    elif args.config == 5:
+        run_cfg5(args, rank, world, local)
     else:
         run_ours(args, rank, world, local)
 

@@ -188,3 +188,61 @@ def cfg4(nq: int = 4194304, seed: int = 4001, block: int = 0):
     w = Workload("cfg4 icosphere(9) 5,242,880 triangles, BVH far field, alpha=200, beta=0.5", V, F,
                  np.full(len(F), 2, np.uint8), alpha=200.0, beta=0.5)
     return w, q
+
+
+def _rotation(rng):
+    """random axis-angle rotation (shapes.hpp:121-125)"""
+    ax = rng.standard_normal(3)
+    ax /= np.linalg.norm(ax)
+    a = rng.uniform(0.0, 2 * np.pi)
+    K = np.array([[0, -ax[2], ax[1]], [ax[2], 0, -ax[0]], [-ax[1], ax[0], 0]])
+    return np.eye(3) + np.sin(a) * K + (1 - np.cos(a)) * (K @ K)
+
+
+def cfg5(nq: int = 16777216, seed: int = 5001, n_extra: int = 1000000):
+    """64 randomly rotated / translated copies (centres U[-10,10]^3) of the
+    cfg3 jittered torus (16,777,216 triangles), plus 1M standalone edges
+    (a surface sample and that sample + mean edge length x a random tangent)
+    and 1M isolated points on the surfaces; queries uniform in the scene
+    AABB. alpha = 100; exact or BVH (beta = 0.5)."""
+    V0, T0 = torus()
+    e = np.concatenate([T0[:, [0, 1]], T0[:, [1, 2]], T0[:, [2, 0]]])
+    e = np.unique(np.sort(e, 1), axis=0)
+    mel = np.linalg.norm(V0[e[:, 0]] - V0[e[:, 1]], axis=1).mean()
+    rng = np.random.default_rng(seed)
+    Vs, Ts = [], []
+    for i in range(64):
+        R = _rotation(rng)
+        c = rng.uniform(-10, 10, 3)
+        Vs.append(V0 @ R.T + c)
+        Ts.append(T0 + i * len(V0))
+    V = np.concatenate(Vs)
+    T = np.concatenate(Ts).astype(np.int64)
+    r3 = np.random.default_rng(seed + 2)
+
+    def sample(n):
+        tri = r3.integers(0, len(T), n)
+        r1, r2 = r3.random(n), r3.random(n)
+        s = np.sqrt(r1)
+        a, b, c = V[T[tri, 0]], V[T[tri, 1]], V[T[tri, 2]]
+        p = (1 - s)[:, None] * a + (s * (1 - r2))[:, None] * b + (s * r2)[:, None] * c
+        nrm = np.cross(b - a, c - a)
+        nrm /= np.linalg.norm(nrm, axis=1, keepdims=True)
+        return p, nrm
+
+    p, nrm = sample(n_extra)
+    t = r3.standard_normal((n_extra, 3))
+    t -= (t * nrm).sum(1, keepdims=True) * nrm
+    t /= np.linalg.norm(t, axis=1, keepdims=True)
+    pe = p + mel * t
+    pts, _ = sample(n_extra)
+    nv = len(V)
+    V = np.concatenate([V, p, pe, pts])
+    E = np.stack([nv + np.arange(n_extra), nv + n_extra + np.arange(n_extra), -np.ones(n_extra, np.int64)], 1)
+    P = np.stack([nv + 2 * n_extra + np.arange(n_extra), -np.ones(n_extra, np.int64), -np.ones(n_extra, np.int64)], 1)
+    S = np.concatenate([T, E, P]).astype(np.int32)
+    K = np.concatenate([np.full(len(T), 2), np.full(n_extra, 1), np.zeros(n_extra)]).astype(np.uint8)
+    lo, hi = V.min(0), V.max(0)
+    q = np.random.default_rng(seed + 1).uniform(lo, hi, (nq, 3))
+    w = Workload("cfg5 64 tori (16.8M triangles) + 1M edges + 1M points", V, S, K, alpha=100.0, beta=0.5)
+    return w, q
