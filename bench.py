@@ -447,8 +447,12 @@ def run_ours(args, rank, world, local):
     bvh = None if args.no_bvh else measure_bvh(args, rank, world, local, sd.Engine, dev, stream, flush, peaks)
     if rank == 0:
         achieved = pairs_per_rank * FLOPS_PER_EDGE_PAIR / (ms_max * 1e-3) / 1e12
+        # dram read + write of the dominant launch, from the committed ncu
+        # capture of this workload (cfg2 fp32): profiles/r1_v3_exact_edge_details.csv
+        traffic = 1.166e8 if (args.config == 2 and not fp64) else None
         roof = {"bound": "fp64-fma" if fp64 else "fp32-fma", "achieved": achieved, "unit": "TFLOP/s",
-                "traffic": None,
+                "traffic": traffic, "traffic_unit": "bytes per launch (ncu dram__bytes_read+write)",
+                "algorithmic_bytes": Q * 12 + N * 48,
                 "kernel": ("exact_kernel<float, edge, poly> x3 segment launches" if args.config == 2 else
                            "exact_kernel<float, triangle, poly>") + " + finalize (step time)",
                 "algorithmic": f"{FLOPS_PER_EDGE_PAIR} flop x {pairs_per_rank} pairs per step (SURVEY 8d)"}

@@ -403,3 +403,56 @@ def test_virtual_primitive_shards(sd, oracle, prec, beta):
         whole = O.query(m, O.Weights.from_table(wt), q, O.Params(alpha=100.0, beta=0.0))
         fin = np.isfinite(whole.d_hat)
         assert np.abs(rd[fin] - whole.d_hat[fin]).max() < 1e-12
+
+
+def test_config5_primitive_sharded_parity(sd, oracle):
+    """BASELINE configs[4] (64 tori + 1M edges + 1M points, 18.8M
+    primitives) in 4 Morton primitive shards, one GPU LBVH per shard, the
+    global WeightSet: per-shard fp64 partials summed and finalised
+    (sd_finalize_device) must match the oracle run on the same per-shard
+    trees (beta = 0.5) and the oracle's flat sum over the whole mesh
+    (beta = 0, on fewer queries)."""
+    import torch
+    from paper_2108_10480_b200 import sharding
+    O = oracle
+    m, q = _cfg(O, 5, 256, 0)
+    wt = O.Weights.build(m).table
+    shards = sharding.primitive_shards(m.vertices, m.simplices, m.kinds, wt.poly_index, 4)
+    dev = torch.device("cuda", 0)
+    for beta, nq in ((0.5, 256), (0.0, 24)):
+        qq = q[:nq]
+        P = sd.SmoothParams(alpha=100.0, beta=beta)
+        cs, gs = np.zeros(nq), np.zeros((nq, 3))
+        rc, rg = np.zeros(nq), np.zeros((nq, 3))
+        for s in shards:
+            e = sd.Engine(0, sd.SD_FP32)
+            e.set_geometry(s.vertices, s.simplices, s.kinds)
+            e.set_weights(wt.A, wt.sup_wtilde, wt.edge_a, wt.tri_stored, s.poly_index)
+            sm = O.Mesh.from_arrays(s.vertices, s.simplices, s.kinds)
+            sw = O.Weights.from_table(O.WeightTable(wt.A, wt.sup_wtilde, wt.edge_a, wt.tri_stored, s.poly_index))
+            tree = None
+            if beta > 0:
+                e.build_bvh(sd.SD_BVH_LBVH)
+                tree = O.Tree.from_nodes(e.export_bvh())
+            r = e.query_points(qq, P, sd.SD_BVH if beta > 0 else sd.SD_EXACT, want_c=True, want_counters=True)
+            rr = O.query(sm, sw, qq, O.Params(alpha=100.0, beta=beta), tree=tree)
+            if beta > 0:
+                assert (r.decision_hash == rr.decision_hash).all()
+            cs += r.c
+            gs += r.grad_c
+            rc += rr.c
+            rg += rr.grad_c
+        d_d = torch.empty(nq, dtype=torch.float64, device=dev)
+        g_d = torch.empty(nq, 3, dtype=torch.float64, device=dev)
+        c_t, gc_t = torch.tensor(cs, device=dev), torch.tensor(gs, device=dev)
+        e.finalize_device(c_t.data_ptr(), gc_t.data_ptr(), nq, P, d_d.data_ptr(), g_d.data_ptr())
+        torch.cuda.synchronize()
+        got = sd.SmoothResults(d_d.cpu().numpy(), g_d.cpu().numpy())
+        rd, rgd = sharding.finalize(rc, rg, 100.0)
+        ref = sd.SmoothResults(rd, rgd)
+        ref.c = rc
+        assert_close(got, ref, 0, 100.0, f"cfg5 beta {beta}")
+        if beta == 0.0:
+            whole = O.query(m, O.Weights.from_table(wt), qq, O.Params(alpha=100.0, beta=0.0))
+            fin = np.isfinite(whole.d_hat)
+            assert np.abs(rd[fin] - whole.d_hat[fin]).max() < 1e-10
