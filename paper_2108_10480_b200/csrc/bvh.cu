@@ -125,8 +125,13 @@ void tree_build_median(Ctx& c) {
 
 // ---------------------------------------------------------------- upload
 template <class T>
-struct NodeT {  // 2 x (4 T): (lo, diam) (hi, link)
+struct alignas(16) NodeT {  // 2 x (4 T): (lo, diam) (hi, link)
     T v[8];
+};
+template <class T>
+struct alignas(16) PairT {  // both children of an internal node + their log2 n_B
+    NodeT<T> l, r;
+    T lgc[4];
 };
 
 template <class T>
@@ -220,6 +225,22 @@ static void upload_tree_T(Ctx& c) {
         if (bytes) check_cuda(cudaMemcpy(d, src, bytes, cudaMemcpyHostToDevice), "upload tree");
     };
     up(t.box, box.data(), box.size() * sizeof(NodeT<T>));
+    // child-pair records: pair[p] = (NodeT[p + 1], NodeT[right(p)],
+    // log2 n_B of both) for internal p, so one warp step fetches both
+    // children of a node and their far-field weights in one go
+    {
+        std::vector<PairT<T>> pr(static_cast<size_t>(n));
+        for (int64_t id = 0; id < n; ++id) {
+            const sd_bvh_node& nd = c.tree[id];
+            if (nd.left < 0) continue;
+            pr[id].l = box[id + 1];
+            pr[id].r = box[nd.right];
+            pr[id].lgc[0] = lgc[id + 1];
+            pr[id].lgc[1] = lgc[nd.right];
+            pr[id].lgc[2] = pr[id].lgc[3] = T(0);
+        }
+        up(t.pairs, pr.data(), pr.size() * sizeof(PairT<T>));
+    }
     up(t.count, count.data(), count.size() * sizeof(int32_t));
     up(t.lgcount, lgc.data(), lgc.size() * sizeof(T));
     up(t.diam64, d64.data(), d64.size() * sizeof(double));
@@ -266,6 +287,7 @@ struct TraverseArgs {
     const int64_t* perm;  // sorted position -> query index
     int64_t Q;
     const NodeT<T>* box;
+    const PairT<T>* pairs;  // [parent]: the two children of an internal node
     const int32_t* count;
     const T* lgcount;     // log2 n_B per node (far-field weight exponent)
     T lw_ff;              // log2 w_ff
@@ -573,6 +595,170 @@ __global__ void __launch_bounds__(kTravThreads) packet_kernel(const __grid_const
     if (nre) atomicAdd(a.rechecks, nre);
 }
 
+// One node test of the packet traversal for one lane (decision + term),
+// shared by the single-node and child-pair kernels. Returns "descend".
+template <class T, bool HASH>
+__device__ __forceinline__ bool visit(const TraverseArgs<T>& a, const Poly<T>* polys, const NodeT<T>& b,
+                                      int32_t id, T lgc, T qx, T qy, T qz, Acc<T>& acc, int64_t& nleaf,
+                                      int64_t& nfar, uint64_t& h, unsigned long long& nre) {
+    int32_t link;
+    memcpy(&link, &b.v[7], sizeof(int32_t));
+    bool far = false;
+    if (a.use_bh) {
+        const T yx = fmin(fmax(qx, b.v[0]), b.v[4]);
+        const T yy = fmin(fmax(qy, b.v[1]), b.v[5]);
+        const T yz = fmin(fmax(qz, b.v[2]), b.v[6]);
+        const T dx = qx - yx, dy = qy - yy, dz = qz - yz;
+        const T s = fma(dx, dx, fma(dy, dy, dz * dz));
+        if constexpr (sizeof(T) == 4) {
+            const T r = s > T(0) ? Math<T>::rsqrt(s) : T(0);
+            const T d = s * r;
+            const T rhs = a.ph.beta * d;
+            const T band = T(1e-5) * rhs;
+            if (s == T(0) && a.exact_boxes) far = false;
+            else if (b.v[3] < rhs - band) far = true;
+            else if (b.v[3] > rhs + band) far = false;
+            else {
+                far = decide64(b, a.diam64[id], double(qx), double(qy), double(qz), a.beta64);
+                ++nre;
+            }
+            if (far) far_term(a.ph, lgc + a.lw_ff, d, r, dx, dy, dz, acc);
+        } else {
+            far = decide64(b, a.diam64[id], double(qx), double(qy), double(qz), a.beta64);
+            if (far) {
+                const T d = sqrt(s);
+                far_term(a.ph, lgc + a.lw_ff, d, T(1) / d, dx, dy, dz, acc);
+            }
+        }
+        if (far) {
+            ++nfar;
+            if constexpr (HASH) h += decision_mix(uint64_t(id), 1);
+            return false;
+        }
+    }
+    if (link >= 0) return true;
+    const int slot = -link - 1;  // exact leaf: the record is the same for every lane
+    const int meta = a.leafmeta[slot];
+    const int kind = meta & 3, poly = (meta >> 2) - 1;
+    T rec[kRecTri];
+    using V = typename Vec4<T>::type;
+    const V* src = reinterpret_cast<const V*>(a.leafrec + size_t(slot) * kRecTri);
+    if (kind == 0) {
+        reinterpret_cast<V*>(rec)[0] = src[0];
+        acc.m -= a.ph.lw_unit;
+        point_term(a.ph, qx, qy, qz, rec[0], rec[1], rec[2], acc);
+        acc.m += a.ph.lw_unit;
+    } else if (kind == 1) {
+#pragma unroll
+        for (int j = 0; j < kRecEdge * int(sizeof(T)) / int(sizeof(V)); ++j) reinterpret_cast<V*>(rec)[j] = src[j];
+        if (poly >= 0) edge_term<T, true, false>(a.ph, polys[poly], qx, qy, qz, rec, acc);
+        else unit_term<T, 1>(a.ph, polys[0], qx, qy, qz, rec, acc);
+    } else {
+#pragma unroll
+        for (int j = 0; j < kRecTri * int(sizeof(T)) / int(sizeof(V)); ++j) reinterpret_cast<V*>(rec)[j] = src[j];
+        if (poly >= 0) tri_term<T, true, false>(a.ph, polys[a.ne + poly], qx, qy, qz, rec, acc);
+        else unit_term<T, 2>(a.ph, polys[0], qx, qy, qz, rec, acc);
+    }
+    ++nleaf;
+    if constexpr (HASH) h += decision_mix(uint64_t(id), 2);
+    return false;
+}
+
+// K3 (default): warp-coherent packet traversal over CHILD PAIRS. The root
+// is tested alone; afterwards every warp step fetches both children of
+// the current node (one 64-B pair record, broadcast) and each lane whose
+// own traversal reached the node tests both (far field / exact leaf /
+// descend) -- per-lane decisions are exactly collect_contributions'
+// (smooth.hpp:101-131). The warp continues into the left child if any
+// lane descends there (pushing the right child with its lane mask), else
+// into the right child, else pops. Stack entries (node, its link, mask)
+// live in shared memory, one stack per warp.
+template <class T, bool HASH>
+__global__ void __launch_bounds__(kTravThreads) pair_kernel(const __grid_constant__ TraverseArgs<T> a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    Poly<T>* polys = reinterpret_cast<Poly<T>*>(smem_raw);
+    int4* stacks = reinterpret_cast<int4*>(smem_raw + poly_bytes<T>(a.npoly));
+    for (int i = threadIdx.x; i < a.npoly * kPolyCoefs; i += blockDim.x)
+        reinterpret_cast<T*>(polys)[i] = reinterpret_cast<const T*>(a.polys)[i];
+    __syncthreads();
+
+    const unsigned lane = threadIdx.x & 31u;
+    int4* st = stacks + (threadIdx.x >> 5) * a.stack_depth;
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const bool valid = i < a.Q;
+    const int64_t qi = valid ? (a.perm ? a.perm[i] : i) : 0;
+    const T qx = valid ? a.q[3 * qi] : T(0), qy = valid ? a.q[3 * qi + 1] : T(0), qz = valid ? a.q[3 * qi + 2] : T(0);
+    unsigned mask = __ballot_sync(0xffffffffu, valid);
+    if (mask == 0u) return;
+    Acc<T> acc;
+    acc.init();
+    int64_t nleaf = 0, nfar = 0;
+    uint64_t h = 0;
+    unsigned long long nre = 0;
+    // root
+    const NodeT<T> root = a.box[0];
+    int32_t cur = 0, cur_link;
+    memcpy(&cur_link, &root.v[7], sizeof(int32_t));
+    {
+        const bool d = valid && visit<T, HASH>(a, polys, root, 0, a.lgcount[0], qx, qy, qz, acc, nleaf, nfar, h, nre);
+        mask = __ballot_sync(0xffffffffu, d);
+    }
+    int sp = 0;
+    while (mask) {
+        const PairT<T>& pr = a.pairs[cur];  // warp-uniform: broadcast loads
+        const NodeT<T> bl = pr.l, br = pr.r;
+        const T lgl = pr.lgc[0], lgr = pr.lgc[1];
+        const int32_t lid = cur + 1, rid = cur_link;
+        // the most likely next step descends into the left child: pull its
+        // pair record into L1 while this one is being processed
+        if (lane == 0) asm volatile("prefetch.global.L1 [%0];" ::"l"(a.pairs + lid));
+        bool dl = false, dr = false;
+        if ((mask >> lane) & 1u) {
+            dl = visit<T, HASH>(a, polys, bl, lid, lgl, qx, qy, qz, acc, nleaf, nfar, h, nre);
+            dr = visit<T, HASH>(a, polys, br, rid, lgr, qx, qy, qz, acc, nleaf, nfar, h, nre);
+        }
+        const unsigned DL = __ballot_sync(0xffffffffu, dl), DR = __ballot_sync(0xffffffffu, dr);
+        int32_t llink, rlink;
+        memcpy(&llink, &bl.v[7], sizeof(int32_t));
+        memcpy(&rlink, &br.v[7], sizeof(int32_t));
+        if (DL) {
+            if (DR) {
+                if (lane == 0) st[sp] = make_int4(rid, rlink, int(DR), 0);
+                __syncwarp();
+                ++sp;
+            }
+            cur = lid;
+            cur_link = llink;
+            mask = DL;
+        } else if (DR) {
+            cur = rid;
+            cur_link = rlink;
+            mask = DR;
+        } else if (sp > 0) {
+            --sp;
+            const int4 e = st[sp];
+            cur = e.x;
+            cur_link = e.y;
+            mask = unsigned(e.z);
+        } else {
+            mask = 0u;
+        }
+    }
+    if (!valid) return;
+    Tot tot;
+    tot.init();
+    tot.flush(acc);
+    a.part[i] = tot.M;
+    a.part[a.Q + i] = tot.s;
+    a.part[2 * a.Q + i] = tot.gx;
+    a.part[3 * a.Q + i] = tot.gy;
+    a.part[4 * a.Q + i] = tot.gz;
+    a.leaves[i] = nleaf;
+    a.far[i] = nfar;
+    if (HASH) a.hash[i] = h;
+    if (nre) atomicAdd(a.rechecks, nre);
+}
+
 template <class T>
 void tree_query(Ctx& c, const T* q, int64_t Q, const sd_params& p, const FinalizeOut& out, cudaStream_t st) {
     if (!c.dtree_ready) tree_upload(c);
@@ -617,6 +803,7 @@ void tree_query(Ctx& c, const T* q, int64_t Q, const sd_params& p, const Finaliz
     a.perm = perm;
     a.Q = Q;
     a.box = t.box.as<NodeT<T>>();
+    a.pairs = t.pairs.as<PairT<T>>();
     a.count = t.count.as<int32_t>();
     a.lgcount = t.lgcount.as<T>();
     a.diam64 = t.diam64.as<double>();
@@ -637,16 +824,19 @@ void tree_query(Ctx& c, const T* q, int64_t Q, const sd_params& p, const Finaliz
     a.far = cnt + Q;
     a.hash = reinterpret_cast<uint64_t*>(cnt + 2 * Q);
     a.rechecks = re;
-    // SDGPU_TRAVERSAL=thread selects the per-thread DFS variant (A/B runs)
-    static const bool per_thread = [] {
+    // SDGPU_TRAVERSAL = thread | packet | pair (default) selects the kernel (A/B runs)
+    static const int variant = [] {
         const char* e = std::getenv("SDGPU_TRAVERSAL");
-        return e && std::string(e) == "thread";
+        const std::string v = e ? e : "pair";
+        return v == "thread" ? 0 : (v == "packet" ? 1 : 2);
     }();
     const size_t smem = poly_bytes<T>(npoly) +
-                        (per_thread ? size_t(a.stack_depth) * kTravThreads * sizeof(int32_t)
-                                    : size_t(a.stack_depth) * (kTravThreads / 32) * sizeof(int2));
+                        (variant == 0 ? size_t(a.stack_depth) * kTravThreads * sizeof(int32_t)
+                                      : size_t(a.stack_depth) * (kTravThreads / 32) * sizeof(int4));
     // the decision hash costs ~20 integer ops per decision: only when asked for
-    auto kern = per_thread ? traverse_kernel<T> : (out.hash ? packet_kernel<T, true> : packet_kernel<T, false>);
+    auto kern = variant == 0 ? traverse_kernel<T>
+                : variant == 1 ? (out.hash ? packet_kernel<T, true> : packet_kernel<T, false>)
+                               : (out.hash ? pair_kernel<T, true> : pair_kernel<T, false>);
     check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)), "smem attr");
     kern<<<unsigned((Q + kTravThreads - 1) / kTravThreads), kTravThreads, smem, st>>>(a);
     check_cuda(cudaGetLastError(), "traverse kernel");

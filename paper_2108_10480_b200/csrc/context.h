@@ -70,7 +70,7 @@ struct DeviceTree {
     int64_t leaves = 0;
     int depth = 0;
     bool exact_boxes = true;
-    DevBuf box, count, lgcount, diam64, leafrec, leafmeta;
+    DevBuf box, pairs, count, lgcount, diam64, leafrec, leafmeta;
 };
 
 struct Ctx {
