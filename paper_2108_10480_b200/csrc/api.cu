@@ -147,8 +147,7 @@ static double binom(int n, int k) {
 // True when A w~ > 0 is certified on the whole domain by the Bernstein
 // coefficients (the minimum Bernstein coefficient bounds the polynomial
 // from below), so the kernels may drop the 1e-300 floor selects.
-bool poly_certified_positive(const Ctx& c, int kind, int poly) {
-    if (poly < 0) return true;
+static double bernstein_min(const Ctx& c, int kind, int poly) {
     double lo = INFINITY;
     if (kind == SD_EDGE) {  // degree-4 Bernstein on [0, 1]
         const double* a = &c.edge_a[5 * size_t(poly)];
@@ -169,7 +168,16 @@ bool poly_certified_positive(const Ctx& c, int kind, int poly) {
                 lo = std::min(lo, s);
             }
     }
-    return c.A * lo > 1e-6;
+    return lo;
+}
+
+bool poly_certified_positive(const Ctx& c, int kind, int poly) {
+    if (poly < 0) return true;
+    return c.A * bernstein_min(c, kind, poly) > 1e-6;
+}
+
+static double poly_lower_bound(const Ctx& c, int kind, int poly) {
+    return poly < 0 ? 1.0 : std::max(0.0, bernstein_min(c, kind, poly));
 }
 
 // Coefficient packing and pre-scaling documented in pair.cuh (Poly).
@@ -209,32 +217,116 @@ template Poly<float> make_poly<float>(const Ctx&, int, int, const sd_params&);
 template Poly<double> make_poly<double>(const Ctx&, int, int, const sd_params&);
 
 // --------------------------------------------------------- exact layout
+static uint64_t spread21h(uint64_t v) {
+    v &= 0x1fffffull;
+    v = (v | (v << 32)) & 0x1f00000000ffffull;
+    v = (v | (v << 16)) & 0x1f0000ff0000ffull;
+    v = (v | (v << 8)) & 0x100f00f00f00f00full;
+    v = (v | (v << 4)) & 0x10c30c30c30c30c3ull;
+    v = (v | (v << 2)) & 0x1249249249249249ull;
+    return v;
+}
+
+// Records per kind, grouped into (kind, polynomial) segments, Morton-ordered
+// inside each segment so that every staged tile is spatially compact; one
+// bounding box per tile (float, rounded outward) for the culling bounds of
+// exact.cu. Summation order is free: the reference's sum is re-associated
+// anyway by the parallel reduction.
 template <class T>
 static void prepare_exact(Ctx& c) {
     if (c.exact_ready) return;
     c.segs.clear();
+    double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (int64_t v = 0; v < c.V; ++v)
+        for (int a = 0; a < 3; ++a) {
+            lo[a] = std::min(lo[a], c.xyz[3 * size_t(v) + a]);
+            hi[a] = std::max(hi[a], c.xyz[3 * size_t(v) + a]);
+        }
+    for (int a = 0; a < 3; ++a) {
+        c.scene_lo[a] = c.V ? lo[a] : 0.0;
+        c.scene_hi[a] = c.V ? hi[a] : 0.0;
+    }
+    auto corners = [&](int64_t i, double blo[3], double bhi[3]) {
+        for (int a = 0; a < 3; ++a) {
+            blo[a] = INFINITY;
+            bhi[a] = -INFINITY;
+        }
+        for (int k = 0; k <= c.kind[i]; ++k)
+            for (int a = 0; a < 3; ++a) {
+                const double x = c.xyz[3 * size_t(c.sv[3 * i + k]) + a];
+                blo[a] = std::min(blo[a], x);
+                bhi[a] = std::max(bhi[a], x);
+            }
+    };
+    std::vector<uint64_t> key(size_t(c.N));
+    for (int64_t i = 0; i < c.N; ++i) {
+        double blo[3], bhi[3];
+        corners(i, blo, bhi);
+        uint64_t m = 0;
+        for (int a = 0; a < 3; ++a) {
+            const double span = c.scene_hi[a] - c.scene_lo[a];
+            const double f = span > 0 ? (0.5 * (blo[a] + bhi[a]) - c.scene_lo[a]) / span * 2097151.0 : 0.0;
+            m |= spread21h(uint64_t(std::min(std::max(f, 0.0), 2097151.0))) << (2 - a);
+        }
+        key[i] = m;
+    }
     for (int k = 0; k < 3; ++k) {
         std::vector<int64_t> ids;
         for (int64_t i = 0; i < c.N; ++i)
             if (c.kind[i] == k) ids.push_back(i);
-        std::stable_sort(ids.begin(), ids.end(),
-                         [&](int64_t a, int64_t b) { return c.poly_index[a] < c.poly_index[b]; });
+        auto pk = [&](int64_t i) { return k == SD_POINT ? -1 : c.poly_index[i]; };
+        std::stable_sort(ids.begin(), ids.end(), [&](int64_t a, int64_t b) {
+            return pk(a) != pk(b) ? pk(a) < pk(b) : key[a] < key[b];
+        });
         const int R = rec_size(k);
         std::vector<T> host(ids.size() * size_t(R));
         for (size_t j = 0; j < ids.size(); ++j) build_record<T>(c, ids[j], &host[j * R]);
         T* d = static_cast<T*>(c.rec[k].ensure(host.size() * sizeof(T)));
-        if (!host.empty()) check_cuda(cudaMemcpy(d, host.data(), host.size() * sizeof(T), cudaMemcpyHostToDevice), "upload records");
+        if (!host.empty())
+            check_cuda(cudaMemcpy(d, host.data(), host.size() * sizeof(T), cudaMemcpyHostToDevice), "upload records");
+        const int64_t TILE = exact_tile_prims(k);
+        std::vector<float4> boxes;
         size_t j = 0;
         while (j < ids.size()) {
-            const int poly = k == SD_POINT ? -1 : c.poly_index[ids[j]];
+            const int poly = pk(ids[j]);
             size_t e = j;
-            while (e < ids.size() && (k == SD_POINT ? -1 : c.poly_index[ids[e]]) == poly) ++e;
-            c.segs.push_back({k, poly, int64_t(j), int64_t(e - j)});
+            while (e < ids.size() && pk(ids[e]) == poly) ++e;
+            c.segs.push_back({k, poly, int64_t(j), int64_t(e - j), int64_t(boxes.size() / 2)});
+            for (size_t t = j; t < e; t += size_t(TILE)) {
+                double blo[3] = {INFINITY, INFINITY, INFINITY}, bhi[3] = {-INFINITY, -INFINITY, -INFINITY};
+                for (size_t u = t; u < std::min(e, t + size_t(TILE)); ++u) {
+                    double plo[3], phi[3];
+                    corners(ids[u], plo, phi);
+                    for (int a = 0; a < 3; ++a) {
+                        blo[a] = std::min(blo[a], plo[a]);
+                        bhi[a] = std::max(bhi[a], phi[a]);
+                    }
+                }
+                float fl[3], fh[3];
+                for (int a = 0; a < 3; ++a) {
+                    fl[a] = float(blo[a]);
+                    fh[a] = float(bhi[a]);
+                    if (double(fl[a]) > blo[a]) fl[a] = std::nextafter(fl[a], -INFINITY);
+                    if (double(fh[a]) < bhi[a]) fh[a] = std::nextafter(fh[a], INFINITY);
+                }
+                const double dg = std::sqrt(double(fh[0] - fl[0]) * (fh[0] - fl[0]) +
+                                            double(fh[1] - fl[1]) * (fh[1] - fl[1]) +
+                                            double(fh[2] - fl[2]) * (fh[2] - fl[2]));
+                boxes.push_back(make_float4(fl[0], fl[1], fl[2], float(dg) * (1.0f + 1e-6f)));
+                boxes.push_back(make_float4(fh[0], fh[1], fh[2], 0.0f));
+            }
             j = e;
         }
+        float4* db = static_cast<float4*>(c.tbox[k].ensure(boxes.size() * sizeof(float4)));
+        if (!boxes.empty())
+            check_cuda(cudaMemcpy(db, boxes.data(), boxes.size() * sizeof(float4), cudaMemcpyHostToDevice),
+                       "upload tile boxes");
     }
     c.exact_ready = true;
 }
+
+// smallest Bernstein coefficient (certified lower bound of w~), 0 if none
+static double poly_lower_bound(const Ctx& c, int kind, int poly);
 
 template <class T>
 __global__ void convert_queries(const double* __restrict__ in, T* __restrict__ out, int64_t n) {
@@ -277,6 +369,9 @@ static void exact_query(Ctx& c, const T* q, int64_t Q, const sd_params& p, const
     double* part = static_cast<double*>(c.part.ensure(size_t(splits) * 5 * Q * sizeof(double)));
     const Phys<T> ph = make_phys<T>(c, p);
     int64_t launches = 0;
+    // queries in Morton order so that a warp's queries share tile bounds
+    const int64_t* perm = sort_queries<T>(c, q, Q, c.scene_lo, c.scene_hi, st, launches);
+    const double S = p.alpha / std::max(p.alpha, p.alpha_u);
     bool first = true;
     for (const Segment& s : c.segs) {
         ExactLaunch<T> L;
@@ -286,7 +381,19 @@ static void exact_query(Ctx& c, const T* q, int64_t Q, const sd_params& p, const
         L.rec = c.rec[s.kind].as<T>() + s.offset * rec_size(s.kind);
         L.count = s.count;
         L.splits = int(splits);
-        L.chunk = (s.count + splits - 1) / splits;
+        const int64_t TILE = exact_tile_prims(s.kind);
+        L.chunk = ((s.count + splits - 1) / splits + TILE - 1) / TILE * TILE;  // tile-aligned splits
+        L.perm = perm;
+        L.tbox = c.tbox[s.kind].as<float4>() + 2 * s.tile0;
+        if (s.poly < 0) {  // unit weights: the shift is kept relative to S log2 A in the kernel
+            L.lwmax = T(0);
+            L.lwspan = T(0);
+        } else {
+            const double hi = S * std::log2(std::max(c.A * c.sup_wtilde, 1e-300));
+            const double lo = S * std::log2(std::max(c.A * poly_lower_bound(c, s.kind, s.poly), 1e-300));
+            L.lwmax = T(hi);
+            L.lwspan = T(hi - lo);
+        }
         L.q = q;
         L.Q = Q;
         L.part = part;
@@ -297,7 +404,7 @@ static void exact_query(Ctx& c, const T* q, int64_t Q, const sd_params& p, const
         ++launches;
         first = false;
     }
-    check_cuda(launch_finalize(part, int(splits), Q, p.alpha, p.epsilon, c.N, nullptr, nullptr, nullptr, nullptr,
+    check_cuda(launch_finalize(part, int(splits), Q, p.alpha, p.epsilon, c.N, nullptr, nullptr, nullptr, perm,
                                   out, st),
                "finalize launch");
     c.last_launches = launches + 1;

@@ -759,20 +759,19 @@ __global__ void __launch_bounds__(kTravThreads) pair_kernel(const __grid_constan
     if (nre) atomicAdd(a.rechecks, nre);
 }
 
+// Morton codes (10 bits per axis over [lo, hi]) + CUB radix sort: the
+// returned permutation lists query indices in spatial order (device
+// memory owned by the context).
 template <class T>
-void tree_query(Ctx& c, const T* q, int64_t Q, const sd_params& p, const FinalizeOut& out, cudaStream_t st) {
-    if (!c.dtree_ready) tree_upload(c);
-    const DeviceTree& t = c.dtree;
-    int64_t launches = 0;
-    // Morton order of the queries over the root box (coherent traversal)
-    const sd_bvh_node& root = c.tree[0];
-    double3 lo = make_double3(root.lo[0], root.lo[1], root.lo[2]);
+const int64_t* sort_queries(Ctx& c, const T* q, int64_t Q, const double lo[3], const double hi[3], cudaStream_t st,
+                            int64_t& launches) {
     auto inv = [](double l, double h) { return h > l ? 1024.0 / (h - l) : 0.0; };
-    double3 iv = make_double3(inv(root.lo[0], root.hi[0]), inv(root.lo[1], root.hi[1]), inv(root.lo[2], root.hi[2]));
+    const double3 dlo = make_double3(lo[0], lo[1], lo[2]);
+    const double3 iv = make_double3(inv(lo[0], hi[0]), inv(lo[1], hi[1]), inv(lo[2], hi[2]));
     uint32_t* keys = static_cast<uint32_t*>(c.keys.ensure(size_t(Q) * 2 * sizeof(uint32_t)));
     int64_t* idx = static_cast<int64_t*>(c.perm.ensure(size_t(Q) * 2 * sizeof(int64_t)));
     const unsigned blocks = unsigned((Q + 255) / 256);
-    query_morton<T><<<blocks, 256, 0, st>>>(q, Q, lo, iv, keys, idx);
+    query_morton<T><<<blocks, 256, 0, st>>>(q, Q, dlo, iv, keys, idx);
     check_cuda(cudaGetLastError(), "query morton");
     ++launches;
     size_t tmp_bytes = 0;
@@ -781,7 +780,21 @@ void tree_query(Ctx& c, const T* q, int64_t Q, const sd_params& p, const Finaliz
     check_cuda(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, keys + Q, idx, idx + Q, int(Q), 0, 30, st),
                "radix sort queries");
     launches += 4;  // onesweep histogram + passes (approximate count of CUB kernels)
-    const int64_t* perm = idx + Q;
+    return idx + Q;
+}
+template const int64_t* sort_queries<float>(Ctx&, const float*, int64_t, const double*, const double*, cudaStream_t,
+                                            int64_t&);
+template const int64_t* sort_queries<double>(Ctx&, const double*, int64_t, const double*, const double*,
+                                             cudaStream_t, int64_t&);
+
+template <class T>
+void tree_query(Ctx& c, const T* q, int64_t Q, const sd_params& p, const FinalizeOut& out, cudaStream_t st) {
+    if (!c.dtree_ready) tree_upload(c);
+    const DeviceTree& t = c.dtree;
+    int64_t launches = 0;
+    // Morton order of the queries over the root box (coherent traversal)
+    const sd_bvh_node& root = c.tree[0];
+    const int64_t* perm = sort_queries(c, q, Q, root.lo, root.hi, st, launches);
 
     // polynomial table: edge polys then triangle polys
     const int ne = int(c.edge_a.size() / 5), nt = int(c.tri_stored.size() / 13);

@@ -56,6 +56,7 @@ struct Segment {
     int poly;
     int64_t offset;  // first record in the kind's record array
     int64_t count;
+    int64_t tile0;   // first tile box of the segment in the kind's box array
 };
 
 // Tree in traversal layout (pre-order ids == reference ids).
@@ -95,6 +96,8 @@ struct Ctx {
     bool exact_ready = false;
     std::vector<Segment> segs;
     DevBuf rec[3];
+    DevBuf tbox[3];   // per kind: 2 float4 per tile (lo.xyz, diagonal) (hi.xyz, 0)
+    double scene_lo[3] = {0, 0, 0}, scene_hi[3] = {0, 0, 0};
 
     // tree (host copy in the reference layout + device traversal layout)
     bool have_tree = false;
@@ -116,6 +119,10 @@ Poly<T> make_poly(const Ctx& c, int kind, int poly, const sd_params& p);
 bool poly_certified_positive(const Ctx& c, int kind, int poly);
 template <class T>
 void build_record(const Ctx& c, int64_t prim, T* out);  // rec_size(kind) values
+
+template <class T>
+const int64_t* sort_queries(Ctx& c, const T* q, int64_t Q, const double lo[3], const double hi[3], cudaStream_t st,
+                            int64_t& launches);
 
 // Tree entry points (bvh.cu)
 void tree_upload(Ctx& c);  // host reference layout -> DeviceTree

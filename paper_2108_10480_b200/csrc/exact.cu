@@ -17,6 +17,8 @@
 #include "pair.cuh"
 #include "pair2.cuh"
 
+#include <type_traits>
+
 namespace sdgpu {
 
 template <class T>
@@ -30,7 +32,17 @@ struct ExactArgs {
     int first;          // first segment: initialise instead of loading
     Phys<T> ph;
     Poly<T> poly;
+    const int64_t* perm;  // sorted position -> query index
+    const float4* tbox;   // tile boxes of the segment (null: no tile bounds)
+    T lwmax, lwspan;      // log2 w upper bound and spread over the segment
 };
+
+// Tile bounds (per warp, per staged tile; see exact_kernel): terms of a
+// tile never exceed 2^kTileHeadroom relative to the shift after the
+// proactive raise, and tiles whose bound is too loose for the fp32 range
+// (|kappa| diag + spread of log2 w > kLooseTile) keep the per-term checks.
+constexpr float kTileHeadroom = 100.0f;
+constexpr float kLooseTile = 200.0f;
 
 constexpr int kThreads = 256;
 constexpr int kStages = 3;
@@ -79,13 +91,16 @@ __global__ void __launch_bounds__(kThreads) exact_kernel(const __grid_constant__
     Acc<T> acc[QPT];
     int64_t qi[QPT];
     double* part = a.part + size_t(split) * 5 * a.Q;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
     for (int k = 0; k < QPT; ++k) {
-        qi[k] = int64_t(blockIdx.x) * kThreads * QPT + k * kThreads + threadIdx.x;
+        // a warp owns 32 x QPT consecutive (Morton-sorted) queries
+        qi[k] = int64_t(blockIdx.x) * kThreads * QPT + int64_t(warp) * 32 * QPT + k * 32 + lane;
         const int64_t qc = min(qi[k], a.Q - 1);
-        qx[k] = a.q[3 * qc];
-        qy[k] = a.q[3 * qc + 1];
-        qz[k] = a.q[3 * qc + 2];
+        const int64_t qo = a.perm ? a.perm[qc] : qc;
+        qx[k] = a.q[3 * qo];
+        qy[k] = a.q[3 * qo + 1];
+        qz[k] = a.q[3 * qo + 2];
         acc[k].init();
         Tot& tk = tot[k * kThreads + threadIdx.x];
         tk.init();
@@ -115,11 +130,10 @@ __global__ void __launch_bounds__(kThreads) exact_kernel(const __grid_constant__
         }
     }
 
-    for (int t = 0; t < ntiles; ++t) {
-        const int s = t % kStages;
-        mbar_wait(&full[s], (t / kStages) & 1);
-        const T* tile = tiles + size_t(s) * TILE * R;
-        const int n = int(min(int64_t(TILE), p1 - (p0 + int64_t(t) * TILE)));
+    // Evaluates the staged tile against this thread's queries; MODE as in
+    // pair2.cuh exp_terms (fp64 always runs MODE 0).
+    auto compute = [&](const T* tile, int n, auto mode) {
+        constexpr int MODE = decltype(mode)::value;
 #pragma unroll 2
         for (int i = 0; i < n; ++i) {
             T rec[R];
@@ -131,10 +145,12 @@ __global__ void __launch_bounds__(kThreads) exact_kernel(const __grid_constant__
             if constexpr (PACKED) {
 #pragma unroll
                 for (int k = 0; k < QPT / 2; ++k) {
-                    if constexpr (KIND == 0) point_term2(a.ph, q2x[k], q2y[k], q2z[k], (const float*)rec, acc2[k]);
+                    if constexpr (KIND == 0)
+                        point_term2<MODE>(a.ph, q2x[k], q2y[k], q2z[k], (const float*)rec, acc2[k]);
                     else if constexpr (KIND == 1)
-                        edge_term2<POLY, SAFE>(a.ph, a.poly, q2x[k], q2y[k], q2z[k], (const float*)rec, acc2[k]);
-                    else tri_term2<POLY, SAFE>(a.ph, a.poly, q2x[k], q2y[k], q2z[k], (const float*)rec, acc2[k]);
+                        edge_term2<POLY, SAFE, MODE>(a.ph, a.poly, q2x[k], q2y[k], q2z[k], (const float*)rec, acc2[k]);
+                    else
+                        tri_term2<POLY, SAFE, MODE>(a.ph, a.poly, q2x[k], q2y[k], q2z[k], (const float*)rec, acc2[k]);
                 }
             } else {
 #pragma unroll
@@ -143,6 +159,70 @@ __global__ void __launch_bounds__(kThreads) exact_kernel(const __grid_constant__
                     else if constexpr (KIND == 1) edge_term<T, POLY, SAFE>(a.ph, a.poly, qx[k], qy[k], qz[k], rec, acc[k]);
                     else tri_term<T, POLY, SAFE>(a.ph, a.poly, qx[k], qy[k], qz[k], rec, acc[k]);
                 }
+            }
+        }
+    };
+
+    for (int t = 0; t < ntiles; ++t) {
+        const int s = t % kStages;
+        mbar_wait(&full[s], (t / kStages) & 1);
+        const T* tile = tiles + size_t(s) * TILE * R;
+        const int n = int(min(int64_t(TILE), p1 - (p0 + int64_t(t) * TILE)));
+        int mode = 0;
+        bool skip = false;
+        if (a.tbox) {
+            // Tile bounds from the tile's box: the nearest (dlo) and farthest
+            // (dhi) possible distance of each query. dlo > 708/alpha masks
+            // every term (smooth.hpp:85-88 zeroes them): the warp skips the
+            // tile. dhi < 708/alpha: nothing can be masked. kappa dlo + lwmax
+            // bounds every exponent: the shift is raised once here.
+            const int64_t g = (p0 + int64_t(t) * TILE) / TILE;
+            const float4 lo4 = __ldg(a.tbox + 2 * g), hi4 = __ldg(a.tbox + 2 * g + 1);
+            const bool loose = float(-a.ph.kappa) * lo4.w + float(a.lwspan) > kLooseTile;
+            bool all_skip = true, all_inside = true;
+#pragma unroll
+            for (int k = 0; k < QPT; ++k) {
+                const float x = float(qx[k]), y = float(qy[k]), z = float(qz[k]);
+                const float ex = fmaxf(fmaxf(lo4.x - x, x - hi4.x), 0.f), ey = fmaxf(fmaxf(lo4.y - y, y - hi4.y), 0.f),
+                            ez = fmaxf(fmaxf(lo4.z - z, z - hi4.z), 0.f);
+                const float fx = fmaxf(fabsf(x - lo4.x), fabsf(x - hi4.x)),
+                            fy = fmaxf(fabsf(y - lo4.y), fabsf(y - hi4.y)),
+                            fz = fmaxf(fabsf(z - lo4.z), fabsf(z - hi4.z));
+                const float dlo = sqrtf(fmaf(ex, ex, fmaf(ey, ey, ez * ez))) * (1.f - 1e-5f);
+                const float dhi = sqrtf(fmaf(fx, fx, fmaf(fy, fy, fz * fz))) * (1.f + 1e-5f);
+                const bool sk = qi[k] >= a.Q || dlo > float(a.ph.dmax);
+                all_skip = all_skip && sk;
+                all_inside = all_inside && (qi[k] >= a.Q || dhi < float(a.ph.dmax));
+                if (!loose && !sk) {  // raise the shift to the tile's exponent bound
+                    const T up = T(fmaf(float(a.ph.kappa), dlo, float(a.lwmax))) - T(kTileHeadroom);
+                    if constexpr (PACKED) {
+                        Acc2& a2 = acc2[k / 2];
+                        const float mk = (k & 1) ? hi(a2.m) : lo(a2.m);
+                        if (float(up) > mk) {
+                            Acc<float> u, v;
+                            a2.to(u, v);
+                            Acc<float>& w = (k & 1) ? v : u;
+                            w.scale(Math<float>::ex2(w.m - float(up)));
+                            w.m = float(up);
+                            a2.from(u, v);
+                        }
+                    } else if (up > acc[k].m) {
+                        acc[k].scale(Math<T>::ex2(acc[k].m - up));
+                        acc[k].m = up;
+                    }
+                }
+            }
+            skip = __all_sync(0xffffffffu, all_skip);
+            const bool inside = __all_sync(0xffffffffu, all_inside);
+            mode = loose ? 0 : (inside ? 2 : 1);
+        }
+        if (!skip) {
+            if constexpr (PACKED) {
+                if (mode == 2) compute(tile, n, std::integral_constant<int, 2>());
+                else if (mode == 1) compute(tile, n, std::integral_constant<int, 1>());
+                else compute(tile, n, std::integral_constant<int, 0>());
+            } else {
+                compute(tile, n, std::integral_constant<int, 0>());
             }
         }
         if constexpr (PACKED) {
@@ -199,6 +279,10 @@ static cudaError_t launch_one(const ExactLaunch<T>& L, cudaStream_t st) {
     a.first = L.first;
     a.ph = L.ph;
     a.poly = L.poly;
+    a.perm = L.perm;
+    a.tbox = L.tbox;
+    a.lwmax = L.lwmax;
+    a.lwspan = L.lwspan;
     const int64_t qblocks = (L.Q + int64_t(kThreads) * QPT - 1) / (int64_t(kThreads) * QPT);
     dim3 grid(unsigned(qblocks), unsigned(L.splits));
     kern<<<grid, kThreads, smem, st>>>(a);
@@ -227,6 +311,8 @@ int exact_blocks_per_sm(int kind, bool has_poly, bool safe) {
 }
 template int exact_blocks_per_sm<float>(int, bool, bool);
 template int exact_blocks_per_sm<double>(int, bool, bool);
+
+int exact_tile_prims(int kind) { return kind == 0 ? tile_prims<float, 0>() : tile_prims<float, 1>(); }
 
 int64_t exact_queries_per_cta(int kind) {
     return int64_t(kThreads) * (kind == 2 ? qpt_for<2>() : qpt_for<1>());

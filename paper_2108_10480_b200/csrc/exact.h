@@ -24,11 +24,16 @@ struct ExactLaunch {
     int first = 1;
     Phys<T> ph{};
     Poly<T> poly{};
+    const int64_t* perm = nullptr;  // sorted position -> query index (spatial order)
+    const float4* tbox = nullptr;   // tile boxes of this segment (2 float4 per tile), or null
+    T lwmax = T(0);                 // upper bound of log2 w over the segment (unit: 0, shift-relative)
+    T lwspan = T(0);                // lwmax - lower bound of log2 w
 };
 
 template <class T>
 cudaError_t launch_exact(const ExactLaunch<T>& L, cudaStream_t st);
 int64_t exact_queries_per_cta(int kind);
+int exact_tile_prims(int kind);  // primitives per staged tile (tile boxes use the same grid)
 template <class T>
 int exact_blocks_per_sm(int kind, bool has_poly, bool safe);  // resident CTAs per SM
 

@@ -86,12 +86,17 @@ __device__ __forceinline__ void bump_half(Acc2& a, int h, float x) {
 
 // Masks, re-anchors and exponentiates the packed x - m; `absx(h)` returns
 // the absolute exponent of half h (only evaluated on the rare path).
-template <class F>
+// MODE 0: per-term -708 mask and lazy shift check (always correct);
+// MODE 1: mask only -- the tile bound already raised the shift so that no
+//         term of this tile exceeds 2^kTileHeadroom (exact.cu);
+// MODE 2: neither -- additionally no term of this tile can be masked.
+template <int MODE = 0, class F>
 __device__ __forceinline__ f2 exp_terms(const Phys<float>& ph, Acc2& a, f2 d, f2 xm, F&& absx) {
+    if constexpr (MODE == 2) return pack(Math<float>::ex2(lo(xm)), Math<float>::ex2(hi(xm)));
     float x0 = lo(xm), x1 = hi(xm);
     x0 = lo(d) > ph.dmax ? -INFINITY : x0;
     x1 = hi(d) > ph.dmax ? -INFINITY : x1;
-    if (x0 > 0.f || x1 > 0.f) {
+    if (MODE == 0 && (x0 > 0.f || x1 > 0.f)) {
         if (x0 > 0.f) {
             const float x = absx(0);
             bump_half(a, 0, x);
@@ -111,13 +116,14 @@ __device__ __forceinline__ f2 rsqrt2(f2 s) {
 }
 
 // ------------------------------------------------------------- points
+template <int MODE = 0>
 __device__ __forceinline__ void point_term2(const Phys<float>& ph, f2 qx, f2 qy, f2 qz, const float* rec, Acc2& a) {
     const f2 dx = subs(qx, rec[0]), dy = subs(qy, rec[1]), dz = subs(qz, rec[2]);
     const f2 s = fma2(dx, dx, fma2(dy, dy, mul2(dz, dz)));
     const f2 r = rsqrt2(s);
     const f2 d = mul2(s, r);
     const f2 xm = sub2(muls(d, ph.kappa), a.m);
-    const f2 e = exp_terms(ph, a, d, xm, [&](int h) { return ph.kappa * (h ? hi(d) : lo(d)); });
+    const f2 e = exp_terms<MODE>(ph, a, d, xm, [&](int h) { return ph.kappa * (h ? hi(d) : lo(d)); });
     const f2 er = mul2(e, r);
     a.s = add2(a.s, e);
     a.gx = fma2(er, dx, a.gx);
@@ -126,7 +132,7 @@ __device__ __forceinline__ void point_term2(const Phys<float>& ph, f2 qx, f2 qy,
 }
 
 // -------------------------------------------------------------- edges
-template <bool POLY, bool SAFE>
+template <bool POLY, bool SAFE, int MODE = 0>
 __device__ __forceinline__ void edge_term2(const Phys<float>& ph, const Poly<float>& pc, f2 qx, f2 qy, f2 qz,
                                            const float* rec, Acc2& a) {
     const f2 apx = subs(qx, rec[0]), apy = subs(qy, rec[1]), apz = subs(qz, rec[2]);
@@ -151,7 +157,7 @@ __device__ __forceinline__ void edge_term2(const Phys<float>& ph, const Poly<flo
             lw = pack(ok0 ? ph.S * l0 : ph.lw_floor, ok1 ? ph.S * l1 : ph.lw_floor);
             k = pack(ok0 ? lo(k) : 0.f, ok1 ? hi(k) : 0.f);
         }
-        const f2 e = exp_terms(ph, a, d, add2(lw, xd),
+        const f2 e = exp_terms<MODE>(ph, a, d, add2(lw, xd),
                                [&](int h) { return fmaf(ph.kappa, h ? hi(d) : lo(d), h ? hi(lw) : lo(lw)); });
         const f2 er = mul2(e, r), ek = mul2(e, k);
         a.s = add2(a.s, e);
@@ -159,7 +165,7 @@ __device__ __forceinline__ void edge_term2(const Phys<float>& ph, const Poly<flo
         a.gy = fmas(ek, -rec[8], fma2(er, dy, a.gy));
         a.gz = fmas(ek, -rec[9], fma2(er, dz, a.gz));
     } else {
-        const f2 e = exp_terms(ph, a, d, xd, [&](int h) { return ph.kappa * (h ? hi(d) : lo(d)); });
+        const f2 e = exp_terms<MODE>(ph, a, d, xd, [&](int h) { return ph.kappa * (h ? hi(d) : lo(d)); });
         const f2 er = mul2(e, r);
         a.s = add2(a.s, e);
         a.gx = fma2(er, dx, a.gx);
@@ -226,7 +232,7 @@ __device__ __forceinline__ void tri_closest2(const float* rec, f2 d1, f2 d2, f2&
     v = pack(vv[0], vv[1]);
 }
 
-template <bool POLY, bool SAFE>
+template <bool POLY, bool SAFE, int MODE = 0>
 __device__ __forceinline__ void tri_term2(const Phys<float>& ph, const Poly<float>& pc, f2 qx, f2 qy, f2 qz,
                                           const float* rec, Acc2& a) {
     const f2 apx = subs(qx, rec[0]), apy = subs(qy, rec[1]), apz = subs(qz, rec[2]);
@@ -254,7 +260,7 @@ __device__ __forceinline__ void tri_term2(const Phys<float>& ph, const Poly<floa
             lw = pack(ok0 ? ph.S * l0 : ph.lw_floor, ok1 ? ph.S * l1 : ph.lw_floor);
             k = pack(ok0 ? lo(k) : 0.f, ok1 ? hi(k) : 0.f);
         }
-        const f2 e = exp_terms(ph, a, d, add2(lw, xd),
+        const f2 e = exp_terms<MODE>(ph, a, d, add2(lw, xd),
                                [&](int h) { return fmaf(ph.kappa, h ? hi(d) : lo(d), h ? hi(lw) : lo(lw)); });
         const f2 er = mul2(e, r), ek = mul2(e, k);
         const f2 kx = mul2(ek, wx), ky = mul2(ek, wy);
@@ -263,7 +269,7 @@ __device__ __forceinline__ void tri_term2(const Phys<float>& ph, const Poly<floa
         a.gy = fmas(ky, -rec[20], fmas(kx, -rec[17], fma2(er, dy, a.gy)));
         a.gz = fmas(ky, -rec[21], fmas(kx, -rec[18], fma2(er, dz, a.gz)));
     } else {
-        const f2 e = exp_terms(ph, a, d, xd, [&](int h) { return ph.kappa * (h ? hi(d) : lo(d)); });
+        const f2 e = exp_terms<MODE>(ph, a, d, xd, [&](int h) { return ph.kappa * (h ? hi(d) : lo(d)); });
         const f2 er = mul2(e, r);
         a.s = add2(a.s, e);
         a.gx = fma2(er, dx, a.gx);
