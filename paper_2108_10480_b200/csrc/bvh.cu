@@ -422,7 +422,7 @@ __global__ void __launch_bounds__(kTravThreads) traverse_kernel(const __grid_con
             using V = typename Vec4<T>::type;
             const V* src = reinterpret_cast<const V*>(a.leafrec + size_t(slot) * kRecTri);
             if (kind == 0) {
-                reinterpret_cast<V*>(rec)[0] = src[0];
+                for (int j = 0; j < kRecPoint * int(sizeof(T)) / int(sizeof(V)); ++j) reinterpret_cast<V*>(rec)[j] = src[j];
                 acc.m -= a.ph.lw_unit;  // unit-weight terms take the shift relative to S log2 A
                 point_term(a.ph, qx, qy, qz, rec[0], rec[1], rec[2], acc);
                 acc.m += a.ph.lw_unit;
@@ -541,7 +541,7 @@ __global__ void __launch_bounds__(kTravThreads) packet_kernel(const __grid_const
                     using V = typename Vec4<T>::type;
                     const V* src = reinterpret_cast<const V*>(a.leafrec + size_t(slot) * kRecTri);
                     if (kind == 0) {
-                        reinterpret_cast<V*>(rec)[0] = src[0];
+                        for (int j = 0; j < kRecPoint * int(sizeof(T)) / int(sizeof(V)); ++j) reinterpret_cast<V*>(rec)[j] = src[j];
                         acc.m -= a.ph.lw_unit;
                         point_term(a.ph, qx, qy, qz, rec[0], rec[1], rec[2], acc);
                         acc.m += a.ph.lw_unit;
@@ -644,7 +644,7 @@ __device__ __forceinline__ bool visit(const TraverseArgs<T>& a, const Poly<T>* p
     using V = typename Vec4<T>::type;
     const V* src = reinterpret_cast<const V*>(a.leafrec + size_t(slot) * kRecTri);
     if (kind == 0) {
-        reinterpret_cast<V*>(rec)[0] = src[0];
+        for (int j = 0; j < kRecPoint * int(sizeof(T)) / int(sizeof(V)); ++j) reinterpret_cast<V*>(rec)[j] = src[j];
         acc.m -= a.ph.lw_unit;
         point_term(a.ph, qx, qy, qz, rec[0], rec[1], rec[2], acc);
         acc.m += a.ph.lw_unit;

@@ -456,3 +456,57 @@ def test_config5_primitive_sharded_parity(sd, oracle):
             whole = O.query(m, O.Weights.from_table(wt), qq, O.Params(alpha=100.0, beta=0.0))
             fin = np.isfinite(whole.d_hat)
             assert np.abs(rd[fin] - whole.d_hat[fin]).max() < 1e-10
+
+
+# ------------------------------------------------------ weight regimes
+@pytest.mark.parametrize("prec", [0, 1])
+def test_unit_weight_tables(sd, oracle, prec):
+    """unit_weight_set (weights.hpp:583-587): every primitive w = 1."""
+    O = oracle
+    m0 = O.random_scene(10, 200)
+    m, q = prep(O, m0, O.QueryStream(77).draw_points(m0, 200), prec)
+    w = O.Weights.unit(m)
+    e = engine_for(sd, O, m, w, prec, tree=O.Tree.build(m))
+    for beta in (0.0, 0.5):
+        ref = O.query(m, w, q, O.Params(alpha=150.0, beta=beta), tree=O.Tree.build(m) if beta else None)
+        got = (e.smooth_min_dist if beta else e.smooth_min_dist_flat)(q, sd.SmoothParams(alpha=150.0, beta=beta))
+        assert_close(got, ref, prec, 150.0, f"unit weights beta {beta}")
+
+
+@pytest.mark.parametrize("prec", [0, 1])
+def test_floored_out_of_model_weights(sd, oracle, prec):
+    """A polynomial that is negative on the domain triggers the reference's
+    1e-300 floor (weights.hpp:657-661; test_weights.cpp:171-192): w =
+    1e-300^S, dw = 0 -- finite, on the non-certified kernel path."""
+    O = oracle
+    m = O.Mesh.from_arrays([[0, 0, 0], [1, 0, 0], [0, 1, 0], [3, 0, 0], [4, 0, 0]],
+                           [[0, 1, 2], [3, 4, -1]], [2, 1])
+    stored = np.zeros((1, 13))
+    stored[0, 0] = -2.0
+    edge = np.array([[-1.0, 0, 0, 0, 0]])
+    t = O.WeightTable(1.0, 1.0, edge, stored, np.array([0, 0], np.int32))
+    w = O.Weights.from_table(t)
+    q = np.array([[0.2, 0.3, 0.5], [3.5, 0.4, 0.0], [10.0, 10.0, 10.0]])
+    mq, q = prep(O, m, q, prec)
+    e = engine_for(sd, O, mq, w, prec)
+    for alpha in (20.0, 100.0):
+        ref = O.query(mq, w, q, O.Params(alpha=alpha, beta=0.0))
+        got = e.smooth_min_dist_flat(q, sd.SmoothParams(alpha=alpha, beta=0.0))
+        assert np.isfinite(ref.d_hat[:2]).all()
+        assert_close(got, ref, prec, alpha, f"floored alpha {alpha}")
+
+
+@pytest.mark.parametrize("prec", [0, 1])
+def test_tree_path_at_beta_zero_equals_flat(sd, oracle, prec):
+    """smooth_min_dist with beta = 0 walks the whole tree (every leaf exact,
+    test_smooth.cpp:221-241): leaves = N, no far field, same field."""
+    O = oracle
+    m0 = O.random_scene(6, 200)
+    m, q = prep(O, m0, O.QueryStream(31).draw_points(m0, 100), prec)
+    w = O.Weights.build(m)
+    e = engine_for(sd, O, m, w, prec)
+    e.build_bvh(sd.SD_BVH_LBVH)
+    got = e.query_points(q, sd.SmoothParams(alpha=100.0, beta=0.0), sd.SD_BVH, want_c=True, want_counters=True)
+    ref = O.query(m, w, q, O.Params(alpha=100.0, beta=0.0))
+    assert (got.leaves == m.num_simplices).all() and not got.far_field.any()
+    assert_close(got, ref, prec, 100.0, "tree beta 0")
