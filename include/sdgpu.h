@@ -20,6 +20,8 @@
  *                           smooth_min_dist_flat(mesh, ws, q, params)
  *                           (smooth.hpp:189-198; SD_EXACT)
  *   sd_finalize_device   <- detail::result_from_accum              (smooth.hpp:147-159)
+ *   sd_mesh_dist_points  <- smooth_mesh_dist(mesh, bvh, ws, query, params) for a
+ *                           point-cloud query mesh (smooth.hpp:212-255)
  *   sd_params            <- SmoothParams {alpha, alpha_u, beta, epsilon} (params.hpp:13-22)
  *   sd_outputs           <- SmoothResult {d_hat, grad, c, grad_c, leaves, far_field}
  *                           (smooth.hpp:20-27)
@@ -147,6 +149,18 @@ int sd_query_points_device(sd_ctx* ctx, const void* q_dev, int64_t Q, const sd_p
  * result_from_accum does (smooth.hpp:147-159). Device pointers. */
 int sd_finalize_device(sd_ctx* ctx, const double* c, const double* grad_c, int64_t Q, const sd_params* p,
                        double* d_hat, double* grad, void* stream);
+
+/* Mesh-to-mesh smooth distance d_hat(M, Mq) for a POINT-CLOUD query mesh
+ * (smooth_mesh_dist, smooth.hpp:212-255): inner smooth distances of the Nq
+ * query points (mode SD_EXACT or SD_BVH, params p), outer LogSumExp with
+ * alpha_q, per-vertex gradients = softmin mass x inner gradient / (denom +
+ * epsilon). Query vertices qxyz are Vq x 3; qpoints lists the vertex of each
+ * point simplex (NULL: every vertex is one point, Nq = Vq). Host buffers:
+ * d_hat (1 value), vertex_grads (Vq x 3, required), per_primitive (Nq, may
+ * be NULL). Blocking. */
+int sd_mesh_dist_points(sd_ctx* ctx, const double* qxyz, int64_t Vq, const int32_t* qpoints, int64_t Nq,
+                        const sd_params* p, double alpha_q, int mode, double* d_hat, double* vertex_grads,
+                        double* per_primitive);
 
 /* Number of this library's kernels launched by the last query call. */
 int sd_last_launch_count(sd_ctx* ctx, int64_t* n);

@@ -137,6 +137,30 @@ public:
     std::vector<SmoothResult> smooth_min_dist(const std::vector<Vec3>& q, const SmoothParams& p) {
         return run(q, p, p.beta > 0.0 ? SD_BVH : SD_EXACT);
     }
+    // smooth_mesh_dist (smooth.hpp:212-255) for a point-cloud query mesh
+    // (every simplex of `query` must be a point).
+    struct MeshDistResult {
+        double d_hat = std::numeric_limits<double>::infinity();
+        std::vector<Vec3> vertex_grads;
+        std::vector<double> per_primitive;
+    };
+    MeshDistResult smooth_mesh_dist(const SimplexMesh& query, const SmoothParams& p) {
+        std::vector<std::int32_t> pts;
+        for (const Simplex& s : query.simplices) {
+            if (s.kind != SimplexKind::Point) throw std::runtime_error("smooth_mesh_dist: point query meshes only");
+            pts.push_back(s.v[0]);
+        }
+        MeshDistResult r;
+        r.vertex_grads.resize(query.vertices.size());
+        r.per_primitive.resize(pts.size());
+        const sd_params sp{p.alpha, p.alpha_u, p.beta, p.epsilon};
+        check(sd_mesh_dist_points(ctx_, reinterpret_cast<const double*>(query.vertices.data()),
+                                  static_cast<std::int64_t>(query.vertices.size()), pts.data(),
+                                  static_cast<std::int64_t>(pts.size()), &sp, p.alpha_q, p.beta > 0 ? SD_BVH : SD_EXACT,
+                                  &r.d_hat, reinterpret_cast<double*>(r.vertex_grads.data()), r.per_primitive.data()));
+        return r;
+    }
+
     // smooth_min_dist_flat (smooth.hpp:189-198) for a batch.
     std::vector<SmoothResult> smooth_min_dist_flat(const std::vector<Vec3>& q, const SmoothParams& p) {
         return run(q, p, SD_EXACT);

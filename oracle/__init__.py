@@ -96,6 +96,7 @@ def _declare(L):
         "sdo_exact_min": (None, [vp, i64, vp, vp, vp, C.c_int]),
         "sdo_query": (C.c_int, [vp, vp, vp, vp, i64, vp, C.c_int] + [vp] * 8),
         "sdo_decision_mix": (u64, [u64, u64]),
+        "sdo_mesh_dist": (C.c_int, [vp, vp, vp, vp, vp, C.c_int, vp, vp, vp, vp]),
         "sdo_hardware_threads": (C.c_int, []),
     }
     for name, (res, args) in sig.items():
@@ -431,3 +432,25 @@ def query(mesh: Mesh, weights: Weights, q, params: Params, tree: Tree | None = N
                            _ptr(secs)))
     r.seconds = float(secs[0])
     return r
+
+
+@dataclass
+class MeshDistResults:
+    d_hat: float
+    vertex_grads: np.ndarray
+    per_primitive: np.ndarray
+    leaves: int
+    far_field: int
+
+
+def mesh_dist(mesh: Mesh, weights: Weights, query: Mesh, params: Params, tree: Tree | None = None,
+              threads: int = 0) -> MeshDistResults:
+    """smooth_mesh_dist (smooth.hpp:212-255) for a point-cloud query mesh."""
+    p = np.array([params.alpha, params.alpha_u, params.beta, params.epsilon, params.alpha_q], np.float64)
+    d = np.zeros(1)
+    vg = np.zeros((len(query.vertices), 3))
+    pp = np.zeros(query.num_simplices)
+    cnt = np.zeros(2, np.int64)
+    _check(lib().sdo_mesh_dist(mesh.h, weights.h, tree.h if tree is not None else None, query.h, _ptr(p),
+                               threads or hardware_threads(), _ptr(d), _ptr(vg), _ptr(pp), _ptr(cnt)))
+    return MeshDistResults(float(d[0]), vg, pp, int(cnt[0]), int(cnt[1]))

@@ -328,6 +328,28 @@ int sdo_query(void* mesh, void* ws, void* bvh, const double* q, std::int64_t Q, 
     });
 }
 
+// Mesh-to-mesh distance for a query point cloud (smooth.hpp:212-255).
+// params = {alpha, alpha_u, beta, epsilon, alpha_q}; bvh NULL = flat inner sums.
+int sdo_mesh_dist(void* mesh, void* ws, void* bvh, void* query, const double* params, int threads, double* d_hat,
+                  double* vertex_grads, double* per_primitive, std::int64_t* counters) {
+    return guard([&] {
+        Params prm = params_from(params);
+        prm.alpha_q = params[4];
+        const Mesh& q = *static_cast<Mesh*>(query);
+        const MeshDist r = smooth_mesh_dist_points(*static_cast<Mesh*>(mesh), static_cast<Bvh*>(bvh),
+                                                   *static_cast<WeightSet*>(ws), q, prm, threads);
+        *d_hat = r.d_hat;
+        for (std::size_t k = 0; k < q.nv(); ++k) {
+            vertex_grads[3 * k] = r.vertex_grads[k].x;
+            vertex_grads[3 * k + 1] = r.vertex_grads[k].y;
+            vertex_grads[3 * k + 2] = r.vertex_grads[k].z;
+        }
+        for (std::size_t j = 0; j < q.ns(); ++j) per_primitive[j] = r.per_primitive[j];
+        counters[0] = r.leaves;
+        counters[1] = r.far_field;
+    });
+}
+
 std::uint64_t sdo_decision_mix(std::uint64_t node, std::uint64_t kind) { return decision_mix(node, kind); }
 int sdo_hardware_threads() {
     const unsigned n = std::thread::hardware_concurrency();

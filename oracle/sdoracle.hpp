@@ -682,6 +682,62 @@ inline Result smooth_min_dist_flat(const Mesh& m, const WeightSet& ws, V3 q, con
 
 // parallel.hpp:25-44 -- static contiguous partition over std::threads.
 template <class Fn>
+void parallel_for(std::int64_t n, int threads, Fn&& fn);
+
+// smooth.hpp:212-255 -- mesh-to-mesh distance: outer LogSumExp (alpha_q)
+// over the inner smooth distances of the query simplices, per-vertex
+// gradients by splitting each simplex's softmin mass over its vertices.
+// Restated for query meshes of point simplices (the inner query is then the
+// point path; edge/triangle query simplices need the QP kernels, which are
+// outside this path).
+struct MeshDist {
+    double d_hat = INFINITY;
+    std::vector<V3> vertex_grads;
+    std::vector<double> per_primitive;
+    std::int64_t leaves = 0, far_field = 0;
+};
+inline MeshDist smooth_mesh_dist_points(const Mesh& m, const Bvh* bvh, const WeightSet& ws, const Mesh& query,
+                                        const Params& prm, int threads) {
+    const std::size_t nq = query.ns();
+    MeshDist out;
+    out.vertex_grads.assign(query.nv(), V3{});
+    out.per_primitive.assign(nq, INFINITY);
+    if (nq == 0) return out;
+    for (const Simplex& s : query.simplices)
+        if (s.kind != POINT) fail("smooth_mesh_dist_points: query simplices must be points");
+    std::vector<V3> inner(nq);
+    std::vector<std::int64_t> leaves(nq, 0), far(nq, 0);
+    parallel_for(std::int64_t(nq), threads, [&](std::int64_t b, std::int64_t e, int) {
+        Scratch s;
+        for (std::int64_t j = b; j < e; ++j) {
+            const V3 q = query.vertices[query.simplices[std::size_t(j)].v[0]];
+            const Result r = bvh ? smooth_min_dist(m, *bvh, ws, q, prm, s) : smooth_min_dist_flat(m, ws, q, prm, s);
+            out.per_primitive[std::size_t(j)] = r.d_hat;
+            inner[std::size_t(j)] = r.grad;
+            leaves[std::size_t(j)] = r.leaves;
+            far[std::size_t(j)] = r.far_field;
+        }
+    });
+    double denom = 0.0;  // serial, primitive order (smooth.hpp:237-245)
+    for (std::size_t j = 0; j < nq; ++j) {
+        out.leaves += leaves[j];
+        out.far_field += far[j];
+        const double mass = std::exp(-prm.alpha_q * out.per_primitive[j]);
+        denom += mass;
+        const Simplex& s = query.simplices[j];
+        const double split = mass / s.nverts();
+        for (int k = 0; k < s.nverts(); ++k) out.vertex_grads[s.v[k]] += split * inner[j];
+    }
+    if (denom <= 0.0) {
+        for (V3& g : out.vertex_grads) g = V3{};
+        return out;
+    }
+    out.d_hat = -std::log(denom) / prm.alpha_q;
+    for (V3& g : out.vertex_grads) g = g / (denom + prm.epsilon);
+    return out;
+}
+
+template <class Fn>
 void parallel_for(std::int64_t n, int threads, Fn&& fn) {
     if (n <= 0) return;
     if (threads < 1) threads = 1;

@@ -37,6 +37,7 @@ EXPORTED_SYMBOLS = (
     "sd_last_error", "sd_abi_version", "sd_create", "sd_destroy", "sd_set_geometry", "sd_set_weights",
     "sd_set_bvh", "sd_build_bvh", "sd_bvh_size", "sd_export_bvh", "sd_query_points", "sd_query_points_device",
     "sd_finalize_device", "sd_last_launch_count", "sd_build_weights", "sd_weights_info", "sd_export_weights",
+    "sd_mesh_dist_points",
 )
 
 
@@ -96,6 +97,7 @@ def lib():
             "sd_build_weights": (C.c_int, [vp]),
             "sd_weights_info": (C.c_int, [vp, P(f64), P(f64), P(i32), P(i32)]),
             "sd_export_weights": (C.c_int, [vp, vp, vp, vp]),
+            "sd_mesh_dist_points": (C.c_int, [vp, vp, i64, vp, i64, P(_Params), f64, C.c_int, vp, vp, vp]),
         }
         for name, (res, argt) in sig.items():
             f = getattr(L, name)
@@ -138,6 +140,14 @@ class WeightTable:
     edge_a: np.ndarray      # (ne, 5)
     tri_stored: np.ndarray  # (nt, 13)
     poly_index: np.ndarray  # (N,) int32, -1 = unit weight
+
+
+@dataclass
+class MeshDistResult:
+    """MeshDistResult (smooth.hpp:281-286)."""
+    d_hat: float
+    vertex_grads: np.ndarray
+    per_primitive: np.ndarray
 
 
 @dataclass
@@ -275,6 +285,23 @@ class Engine:
         """Batched smooth_min_dist (smooth.hpp:166-184): tree path when beta > 0."""
         mode = SD_BVH if params.beta > 0 else SD_EXACT
         return self.query_points(q, params, mode, want_c=True, want_counters=True)
+
+    def smooth_mesh_dist(self, query_vertices, params: SmoothParams, query_points=None,
+                         mode: int | None = None) -> "MeshDistResult":
+        """smooth_mesh_dist (smooth.hpp:212-255) for a point-cloud query mesh:
+        outer LogSumExp with params.alpha_q over the inner smooth distances;
+        tree path when beta > 0."""
+        v = np.ascontiguousarray(query_vertices, np.float64).reshape(-1, 3)
+        pts = None if query_points is None else np.ascontiguousarray(query_points, np.int32).reshape(-1)
+        n = len(v) if pts is None else len(pts)
+        d = np.zeros(1)
+        vg = np.zeros((len(v), 3))
+        pp = np.zeros(n)
+        if mode is None:
+            mode = SD_BVH if params.beta > 0 else SD_EXACT
+        _check(lib().sd_mesh_dist_points(self.h, _ptr(v), len(v), _ptr(pts), n, C.byref(params._c()),
+                                         float(params.alpha_q), mode, _ptr(d), _ptr(vg), _ptr(pp)))
+        return MeshDistResult(float(d[0]), vg, pp)
 
     def smooth_min_dist_flat(self, q, params: SmoothParams) -> SmoothResults:
         """Batched smooth_min_dist_flat (smooth.hpp:189-198)."""

@@ -246,3 +246,26 @@ def cfg5(nq: int = 16777216, seed: int = 5001, n_extra: int = 1000000):
     q = np.random.default_rng(seed + 1).uniform(lo, hi, (nq, 3))
     w = Workload("cfg5 64 tori (16.8M triangles) + 1M edges + 1M points", V, S, K, alpha=100.0, beta=0.5)
     return w, q
+
+
+def terrain_bunny(seed: int = 6001):
+    """Stand-ins for the paper's simulation row "Terrain (lidar points,
+    6,591,087, alpha 100) vs Bunny (points, 3,485, alpha_q 20)"
+    (PAPER.md:1378-1397): a lidar-like height-field point cloud over a
+    10 x 10 patch (smooth hill + ripples + N(0, 0.01^2) noise) and a
+    3,485-point bumpy closed blob resting just above the hill top."""
+    rng = np.random.default_rng(seed)
+    n = 6591087
+    xy = rng.uniform(0.0, 10.0, (n, 2))
+
+    def height(x, y):
+        return 1.5 * np.exp(-((x - 5) ** 2 + (y - 5) ** 2) / 8.0) + 0.05 * np.sin(3 * x) * np.cos(2 * y)
+
+    terrain = np.column_stack([xy, height(xy[:, 0], xy[:, 1]) + rng.normal(0, 0.01, n)])
+    m = 3485
+    d = rng.standard_normal((m, 3))
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    r = 0.5 * (1 + 0.1 * np.sin(5 * d[:, 0]) * np.cos(4 * d[:, 1]))
+    bunny = d * r[:, None] * np.array([1.0, 0.8, 0.9])
+    bunny += np.array([5.0, 5.0, height(5.0, 5.0) + 0.5 * 0.9 * 1.1 + 0.02]) - np.array([0, 0, 0])
+    return terrain, bunny

@@ -702,6 +702,66 @@ int sd_finalize_device(sd_ctx* c, const double* cs, const double* gc, int64_t Q,
     });
 }
 
+int sd_mesh_dist_points(sd_ctx* c, const double* qxyz, int64_t Vq, const int32_t* qpoints, int64_t Nq,
+                        const sd_params* p, double alpha_q, int mode, double* d_hat, double* vertex_grads,
+                        double* per_primitive) {
+    return guard([&] {
+        if (!c) throw ArgError{"ctx is NULL"};
+        check_params(p);
+        check_ready(*c, mode);
+        if (!(alpha_q > 0) || !std::isfinite(alpha_q)) throw ArgError{"alpha_q must be positive and finite"};
+        if (Vq < 0 || (Vq > 0 && !qxyz) || !d_hat || (Vq > 0 && !vertex_grads)) throw ArgError{"bad query mesh arrays"};
+        if (!qpoints) Nq = Vq;
+        if (Nq < 0) throw ArgError{"bad point count"};
+        std::vector<double> q(size_t(Nq) * 3);
+        for (int64_t j = 0; j < Nq; ++j) {
+            const int64_t v = qpoints ? qpoints[j] : j;
+            if (v < 0 || v >= Vq) throw ArgError{"query point " + std::to_string(j) + ": vertex index out of range"};
+            for (int a = 0; a < 3; ++a) q[3 * j + a] = qxyz[3 * v + a];
+        }
+        DeviceScope ds(c->device);
+        cudaStream_t st = c->stream;
+        int64_t launches = 0;
+        FinalizeOut out;
+        out.d_hat = static_cast<double*>(c->out_d.ensure(size_t(std::max<int64_t>(Nq, 1)) * sizeof(double)));
+        out.grad = static_cast<double*>(c->out_g.ensure(size_t(std::max<int64_t>(Nq, 1)) * 3 * sizeof(double)));
+        if (Nq > 0) {
+            double* qd = static_cast<double*>(c->qd.ensure(q.size() * sizeof(double)));
+            check_cuda(cudaMemcpyAsync(qd, q.data(), q.size() * sizeof(double), cudaMemcpyHostToDevice, st), "H2D");
+            if (c->precision == SD_FP32) {
+                float* qf = static_cast<float*>(c->qT.ensure(q.size() * sizeof(float)));
+                convert_queries<float><<<unsigned((3 * Nq + 255) / 256), 256, 0, st>>>(qd, qf, 3 * Nq);
+                check_cuda(cudaGetLastError(), "convert queries");
+                dispatch<float>(*c, qf, Nq, *p, mode, out, st);
+            } else {
+                dispatch<double>(*c, qd, Nq, *p, mode, out, st);
+            }
+            launches += c->last_launches;
+        }
+        int32_t* vidx = nullptr;
+        if (qpoints && Nq > 0) {
+            vidx = static_cast<int32_t*>(c->out_l.ensure(size_t(Nq) * sizeof(int32_t)));
+            check_cuda(cudaMemcpyAsync(vidx, qpoints, size_t(Nq) * sizeof(int32_t), cudaMemcpyHostToDevice, st), "H2D");
+        }
+        const size_t wb = mesh_reduce_work_bytes(Nq);
+        double* work = static_cast<double*>(c->tmp2.ensure(wb));
+        double* vg = static_cast<double*>(c->out_gc.ensure(size_t(std::max<int64_t>(Vq, 1)) * 3 * sizeof(double)));
+        double* dd = static_cast<double*>(c->out_c.ensure(sizeof(double) * 2));
+        check_cuda(launch_mesh_reduce(out.d_hat, out.grad, Nq, vidx, Vq, alpha_q, p->epsilon, work, wb, vg, dd,
+                                      launches, st),
+                   "mesh reduction");
+        check_cuda(cudaMemcpyAsync(d_hat, dd, sizeof(double), cudaMemcpyDeviceToHost, st), "D2H");
+        if (Vq > 0)
+            check_cuda(cudaMemcpyAsync(vertex_grads, vg, size_t(Vq) * 3 * sizeof(double), cudaMemcpyDeviceToHost, st),
+                       "D2H");
+        if (per_primitive && Nq > 0)
+            check_cuda(cudaMemcpyAsync(per_primitive, out.d_hat, size_t(Nq) * sizeof(double), cudaMemcpyDeviceToHost, st),
+                       "D2H");
+        check_cuda(cudaStreamSynchronize(st), "mesh dist");
+        c->last_launches = launches;
+    });
+}
+
 int sd_last_launch_count(sd_ctx* c, int64_t* n) {
     return guard([&] {
         if (!c || !n) throw ArgError{"NULL argument"};

@@ -10,6 +10,8 @@
 
 #include <cmath>
 
+#include <cub/cub.cuh>
+
 namespace sdgpu {
 
 __global__ void finalize_kernel(const double* __restrict__ part, int splits, int64_t Q, double alpha, double eps,
@@ -113,6 +115,75 @@ cudaError_t launch_empty_result(int64_t Q, const FinalizeOut& out, cudaStream_t 
     if (Q <= 0) return cudaSuccess;
     empty_kernel<<<unsigned((Q + 255) / 256), 256, 0, st>>>(Q, out);
     return cudaGetLastError();
+}
+
+// ------------------------------------------ mesh-to-mesh outer LogSumExp
+// smooth.hpp:237-254: mass_j = exp(-alpha_q d_j); denom = sum_j mass_j;
+// vertex gradient = sum over the simplices at the vertex of mass_j / n_j
+// times the inner gradient, divided by denom + epsilon; denom <= 0 ->
+// d_hat = +inf and zero gradients. Point simplices: n_j = 1.
+__global__ void mass_kernel(const double* __restrict__ d, int64_t n, double alpha_q, double* mass) {
+    const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (j < n) mass[j] = exp(-alpha_q * d[j]);
+}
+__global__ void scatter_kernel(const double* __restrict__ mass, const double* __restrict__ grad, int64_t n,
+                               const int32_t* __restrict__ vidx, double* vg) {
+    const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    const int64_t v = vidx ? vidx[j] : j;
+    const double m = mass[j];
+    atomicAdd(vg + 3 * v, m * grad[3 * j]);
+    atomicAdd(vg + 3 * v + 1, m * grad[3 * j + 1]);
+    atomicAdd(vg + 3 * v + 2, m * grad[3 * j + 2]);
+}
+__global__ void mesh_finish_kernel(double* vg, int64_t nv, const double* __restrict__ denom, double alpha_q, double eps,
+                                   double* d_out) {
+    const int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const double den = denom[0];
+    if (k == 0) d_out[0] = den > 0.0 ? -log(den) / alpha_q : INFINITY;
+    if (k >= nv) return;
+    const double f = den > 0.0 ? 1.0 / (den + eps) : 0.0;
+    vg[3 * k] = den > 0.0 ? vg[3 * k] / (den + eps) : 0.0;
+    vg[3 * k + 1] = den > 0.0 ? vg[3 * k + 1] / (den + eps) : 0.0;
+    vg[3 * k + 2] = den > 0.0 ? vg[3 * k + 2] / (den + eps) : 0.0;
+    (void)f;
+}
+
+cudaError_t launch_mesh_reduce(const double* d, const double* grad, int64_t n, const int32_t* vidx, int64_t nv,
+                               double alpha_q, double eps, double* work, size_t work_bytes, double* vg,
+                               double* d_out, int64_t& launches, cudaStream_t st) {
+    // work: [mass n][denom 1][cub temp]
+    double* mass = work;
+    double* denom = work + n;
+    void* tmp = work + n + 2;
+    size_t tb = work_bytes > (size_t(n) + 2) * sizeof(double) ? work_bytes - (size_t(n) + 2) * sizeof(double) : 0;
+    const unsigned B = 256;
+    cudaError_t e = cudaMemsetAsync(vg, 0, size_t(nv) * 3 * sizeof(double), st);
+    if (e != cudaSuccess) return e;
+    if (n > 0) {
+        mass_kernel<<<unsigned((n + B - 1) / B), B, 0, st>>>(d, n, alpha_q, mass);
+        size_t need = 0;
+        cub::DeviceReduce::Sum(nullptr, need, mass, denom, int(n), st);
+        if (need > tb) return cudaErrorMemoryAllocation;
+        e = cub::DeviceReduce::Sum(tmp, tb, mass, denom, int(n), st);
+        if (e != cudaSuccess) return e;
+        scatter_kernel<<<unsigned((n + B - 1) / B), B, 0, st>>>(mass, grad, n, vidx, vg);
+        launches += 4;
+    } else {
+        e = cudaMemsetAsync(denom, 0, sizeof(double), st);
+        if (e != cudaSuccess) return e;
+    }
+    mesh_finish_kernel<<<unsigned((std::max<int64_t>(nv, 1) + B - 1) / B), B, 0, st>>>(vg, nv, denom, alpha_q, eps,
+                                                                                        d_out);
+    ++launches;
+    return cudaGetLastError();
+}
+
+size_t mesh_reduce_work_bytes(int64_t n) {
+    size_t need = 0;
+    cub::DeviceReduce::Sum(nullptr, need, static_cast<double*>(nullptr), static_cast<double*>(nullptr),
+                           int(std::max<int64_t>(n, 1)));
+    return (size_t(n) + 2) * sizeof(double) + need + 256;
 }
 
 }  // namespace sdgpu

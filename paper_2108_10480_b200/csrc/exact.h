@@ -53,6 +53,12 @@ cudaError_t launch_finalize(const double* part, int splits, int64_t Q, double al
 cudaError_t launch_finalize_sums(const double* c, const double* grad_c, int64_t Q, double alpha, double epsilon,
                                  double* d_hat, double* grad, cudaStream_t st);
 
+// Mesh-to-mesh outer LogSumExp (smooth.hpp:237-254), point query simplices.
+cudaError_t launch_mesh_reduce(const double* d, const double* grad, int64_t n, const int32_t* vidx, int64_t nv,
+                               double alpha_q, double eps, double* work, size_t work_bytes, double* vg,
+                               double* d_out, int64_t& launches, cudaStream_t st);
+size_t mesh_reduce_work_bytes(int64_t n);
+
 // Fills an empty-mesh result (+inf, zero gradient; smooth.hpp:151-155).
 cudaError_t launch_empty_result(int64_t Q, const FinalizeOut& out, cudaStream_t st);
 

@@ -510,3 +510,58 @@ def test_tree_path_at_beta_zero_equals_flat(sd, oracle, prec):
     ref = O.query(m, w, q, O.Params(alpha=100.0, beta=0.0))
     assert (got.leaves == m.num_simplices).all() and not got.far_field.any()
     assert_close(got, ref, prec, 100.0, "tree beta 0")
+
+
+# ------------------------------------------------- mesh-to-mesh (points)
+@pytest.mark.parametrize("prec", [0, 1])
+def test_mesh_dist_single_point_matches_point_field(sd, oracle, prec):  # test_smooth.cpp:263-280
+    O = oracle
+    m = O.icosphere(1)
+    mq, q = prep(O, m, [[1.4, -0.2, 0.3]], prec)
+    w = O.Weights.build(mq)
+    e = engine_for(sd, O, mq, w, prec)
+    P = sd.SmoothParams(beta=0.0)
+    md = e.smooth_mesh_dist(q, P)
+    pt = e.smooth_min_dist_flat(q, P)
+    assert abs(md.d_hat - pt.d_hat[0]) < 1e-12 and md.per_primitive[0] == pt.d_hat[0]
+    assert np.abs(md.vertex_grads[0] - pt.grad[0]).max() < 1e-12
+
+
+@pytest.mark.parametrize("prec,beta", [(0, 0.0), (1, 0.0), (0, 0.5), (1, 0.5)])
+def test_mesh_dist_point_cloud_parity(sd, oracle, prec, beta):
+    """d_hat(M, cloud), per-point values and vertex gradients vs the oracle's
+    smooth_mesh_dist restatement; softmin identity and bounds
+    (test_smooth.cpp:282-304); shared vertices accumulate."""
+    O = oracle
+    m0 = O.random_scene(12, 200)
+    cloud0 = O.point_cluster(64, 5, 0.6)
+    m, _ = prep(O, m0, np.zeros((1, 3)), prec)
+    cv = cloud0.vertices + np.array([0.3, -0.2, 0.4])
+    if prec == 0:
+        cv = cv.astype(np.float32).astype(np.float64)
+    pts = np.concatenate([np.arange(64), [3, 3, 7]]).astype(np.int32)  # vertices 3, 7 carry extra points
+    cloud = O.Mesh.from_arrays(cv, np.stack([pts, -np.ones_like(pts), -np.ones_like(pts)], 1), np.zeros(len(pts)))
+    w = O.Weights.build(m)
+    t = O.Tree.build(m)
+    e = engine_for(sd, O, m, w, prec, tree=t)
+    P = sd.SmoothParams(alpha=100.0, beta=beta, alpha_q=40.0)
+    got = e.smooth_mesh_dist(cv, P, query_points=pts)
+    ref = O.mesh_dist(m, w, cloud, O.Params(alpha=100.0, beta=beta, alpha_q=40.0), tree=t if beta else None)
+    td, tg = TOL[prec]
+    assert abs(got.d_hat - ref.d_hat) <= td * max(1.0, abs(ref.d_hat))
+    fin = np.isfinite(ref.per_primitive)
+    assert np.abs(got.per_primitive[fin] - ref.per_primitive[fin]).max() <= td * max(1.0, np.abs(ref.per_primitive[fin]).max())
+    assert np.abs(got.vertex_grads - ref.vertex_grads).max() <= tg * max(1.0, np.abs(ref.vertex_grads).max())
+    mass = np.exp(-40.0 * (got.per_primitive - got.d_hat))
+    assert abs(mass.sum() - 1.0) < 1e-6
+    dmin = got.per_primitive.min()
+    assert got.d_hat <= dmin + 1e-9 and got.d_hat >= dmin - np.log(len(pts)) / 40.0 - 1e-9
+
+
+def test_mesh_dist_far_cloud_underflows(sd, oracle):
+    """every inner distance +inf -> denom 0 -> d_hat +inf, zero gradients."""
+    O = oracle
+    m = O.point_cluster(20, 2, 0.05)
+    e = engine_for(sd, O, m, O.Weights.build(m), 1)
+    md = e.smooth_mesh_dist([[3.0, 0, 0], [0, 4.0, 0]], sd.SmoothParams(alpha=400.0, beta=0.0, alpha_q=20.0))
+    assert np.isinf(md.d_hat) and not md.vertex_grads.any()
