@@ -217,6 +217,7 @@ static void upload_tree_T(Ctx& c) {
     }
     DeviceTree& t = c.dtree;
     t.nodes = n;
+    t.split_k = -1;
     t.leaves = slot;
     t.depth = depth;
     t.exact_boxes = exact_boxes;
@@ -247,6 +248,31 @@ static void upload_tree_T(Ctx& c) {
     up(t.leafrec, leafrec.data(), leafrec.size() * sizeof(T));
     up(t.leafmeta, leafmeta.data(), leafmeta.size() * sizeof(int32_t));
     c.dtree_ready = true;
+}
+
+// Nodes at depth exactly k (pre-order) for the split traversal, cached per k.
+void split_tables(Ctx& c, int k) {
+    DeviceTree& t = c.dtree;
+    if (t.split_k == k) return;
+    const int64_t n = int64_t(c.tree.size());
+    std::vector<int32_t> slot_of(size_t(n), -1), dep(size_t(n), 0);
+    std::vector<int32_t> nodes;
+    for (int64_t id = 0; id < n; ++id) {  // pre-order: parents precede children
+        const sd_bvh_node& nd = c.tree[id];
+        if (dep[id] == k) {
+            slot_of[id] = int32_t(nodes.size());
+            nodes.push_back(int32_t(id));
+        }
+        if (nd.left >= 0) dep[nd.left] = dep[nd.right] = dep[id] + 1;
+    }
+    t.split_count = int64_t(std::max<size_t>(nodes.size(), 1));
+    auto up = [](DevBuf& buf, const void* src, size_t bytes) {
+        void* d = buf.ensure(bytes);
+        if (bytes) check_cuda(cudaMemcpy(d, src, bytes, cudaMemcpyHostToDevice), "upload split tables");
+    };
+    up(t.slot_of, slot_of.data(), slot_of.size() * sizeof(int32_t));
+    up(t.split_nodes, nodes.data(), nodes.size() * sizeof(int32_t));
+    t.split_k = k;
 }
 
 void tree_upload(Ctx& c) {
@@ -306,6 +332,12 @@ struct TraverseArgs {
     int64_t* far;
     uint64_t* hash;
     unsigned long long* rechecks;  // fp64 re-decisions (diagnostic)
+    // split mode (few queries): see pair_kernel
+    int split_depth, nslots;
+    int64_t npackets;
+    const int32_t* slot_of;     // node -> depth-k slot, or -1
+    const int32_t* split_nodes;  // slot -> node
+    unsigned* items;            // [packet][slot] lane mask reaching the slot
 };
 
 constexpr int kTravThreads = 128;
@@ -666,14 +698,21 @@ __device__ __forceinline__ bool visit(const TraverseArgs<T>& a, const Poly<T>* p
 
 // K3 (default): warp-coherent packet traversal over CHILD PAIRS. The root
 // is tested alone; afterwards every warp step fetches both children of
-// the current node (one 64-B pair record, broadcast) and each lane whose
-// own traversal reached the node tests both (far field / exact leaf /
-// descend) -- per-lane decisions are exactly collect_contributions'
-// (smooth.hpp:101-131). The warp continues into the left child if any
-// lane descends there (pushing the right child with its lane mask), else
-// into the right child, else pops. Stack entries (node, its link, mask)
+// the current node (one pair record, broadcast) and each lane whose own
+// traversal reached the node tests both (far field / exact leaf / descend)
+// -- per-lane decisions are exactly collect_contributions'
+// (smooth.hpp:101-131). The warp continues into the left child if any lane
+// descends there (pushing the right child with its lane mask), else into
+// the right child, else pops. Stack entries (node, its link, mask, depth)
 // live in shared memory, one stack per warp.
-template <class T, bool HASH>
+//
+// SPLIT = 1 / 2 (few queries): the same walk cut at tree depth k. The top
+// pass (1) stops above depth k and records, per query packet and depth-k
+// node, the mask of lanes that reach it; the subtree pass (2) runs one warp
+// per (packet, depth-k node) from that node with that mask. Each lane still
+// visits exactly its reference node set; the partial sums land in split
+// slots merged by K4, so a batch of a few thousand queries fills the GPU.
+template <class T, bool HASH, int SPLIT>
 __global__ void __launch_bounds__(kTravThreads) pair_kernel(const __grid_constant__ TraverseArgs<T> a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Poly<T>* polys = reinterpret_cast<Poly<T>*>(smem_raw);
@@ -684,10 +723,16 @@ __global__ void __launch_bounds__(kTravThreads) pair_kernel(const __grid_constan
 
     const unsigned lane = threadIdx.x & 31u;
     int4* st = stacks + (threadIdx.x >> 5) * a.stack_depth;
-    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    // packet (32 sorted queries) and, in the subtree pass, the depth-k slot
+    const int64_t gwarp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t packet = SPLIT == 2 ? gwarp / a.nslots : gwarp;
+    const int slot = SPLIT == 2 ? int(gwarp % a.nslots) : 0;
+    if (SPLIT == 2 && packet >= a.npackets) return;
+    const int64_t i = packet * 32 + lane;
     const bool valid = i < a.Q;
     const int64_t qi = valid ? (a.perm ? a.perm[i] : i) : 0;
     const T qx = valid ? a.q[3 * qi] : T(0), qy = valid ? a.q[3 * qi + 1] : T(0), qz = valid ? a.q[3 * qi + 2] : T(0);
+    double* part = a.part + (SPLIT == 2 ? size_t(1 + slot) * 5 * a.Q : 0);
     unsigned mask = __ballot_sync(0xffffffffu, valid);
     if (mask == 0u) return;
     Acc<T> acc;
@@ -695,20 +740,48 @@ __global__ void __launch_bounds__(kTravThreads) pair_kernel(const __grid_constan
     int64_t nleaf = 0, nfar = 0;
     uint64_t h = 0;
     unsigned long long nre = 0;
-    // root
-    const NodeT<T> root = a.box[0];
-    int32_t cur = 0, cur_link;
-    memcpy(&cur_link, &root.v[7], sizeof(int32_t));
-    {
-        const bool d = valid && visit<T, HASH>(a, polys, root, 0, a.lgcount[0], qx, qy, qz, acc, nleaf, nfar, h, nre);
+    int32_t cur, cur_link;
+    int depth;
+    if constexpr (SPLIT == 2) {
+        mask &= a.items[packet * a.nslots + slot];
+        cur = a.split_nodes[slot];
+        depth = a.split_depth;
+    } else {
+        cur = 0;
+        depth = 0;
+    }
+    memcpy(&cur_link, &a.box[cur].v[7], sizeof(int32_t));
+    if (mask) {  // the start node (root, or the depth-k node) is popped alone
+        const NodeT<T> b0 = a.box[cur];
+        const bool d = ((mask >> lane) & 1u) &&
+                       visit<T, HASH>(a, polys, b0, cur, a.lgcount[cur], qx, qy, qz, acc, nleaf, nfar, h, nre);
         mask = __ballot_sync(0xffffffffu, d);
     }
     int sp = 0;
     while (mask) {
+        const int32_t lid = cur + 1, rid = cur_link;
+        if (SPLIT == 1 && depth + 1 == a.split_depth) {  // children start subtrees: hand over
+            if (lane == 0) {
+                unsigned* it = a.items + packet * a.nslots;
+                it[a.slot_of[lid]] = mask;
+                it[a.slot_of[rid]] = mask;
+            }
+            __syncwarp();
+            if (sp > 0) {
+                --sp;
+                const int4 e = st[sp];
+                cur = e.x;
+                cur_link = e.y;
+                mask = unsigned(e.z);
+                depth = e.w;
+            } else {
+                mask = 0u;
+            }
+            continue;
+        }
         const PairT<T>& pr = a.pairs[cur];  // warp-uniform: broadcast loads
         const NodeT<T> bl = pr.l, br = pr.r;
         const T lgl = pr.lgc[0], lgr = pr.lgc[1];
-        const int32_t lid = cur + 1, rid = cur_link;
         // the most likely next step descends into the left child: pull its
         // pair record into L1 while this one is being processed
         if (lane == 0) asm volatile("prefetch.global.L1 [%0];" ::"l"(a.pairs + lid));
@@ -723,23 +796,26 @@ __global__ void __launch_bounds__(kTravThreads) pair_kernel(const __grid_constan
         memcpy(&rlink, &br.v[7], sizeof(int32_t));
         if (DL) {
             if (DR) {
-                if (lane == 0) st[sp] = make_int4(rid, rlink, int(DR), 0);
+                if (lane == 0) st[sp] = make_int4(rid, rlink, int(DR), depth + 1);
                 __syncwarp();
                 ++sp;
             }
             cur = lid;
             cur_link = llink;
             mask = DL;
+            ++depth;
         } else if (DR) {
             cur = rid;
             cur_link = rlink;
             mask = DR;
+            ++depth;
         } else if (sp > 0) {
             --sp;
             const int4 e = st[sp];
             cur = e.x;
             cur_link = e.y;
             mask = unsigned(e.z);
+            depth = e.w;
         } else {
             mask = 0u;
         }
@@ -748,14 +824,20 @@ __global__ void __launch_bounds__(kTravThreads) pair_kernel(const __grid_constan
     Tot tot;
     tot.init();
     tot.flush(acc);
-    a.part[i] = tot.M;
-    a.part[a.Q + i] = tot.s;
-    a.part[2 * a.Q + i] = tot.gx;
-    a.part[3 * a.Q + i] = tot.gy;
-    a.part[4 * a.Q + i] = tot.gz;
-    a.leaves[i] = nleaf;
-    a.far[i] = nfar;
-    if (HASH) a.hash[i] = h;
+    part[i] = tot.M;
+    part[a.Q + i] = tot.s;
+    part[2 * a.Q + i] = tot.gx;
+    part[3 * a.Q + i] = tot.gy;
+    part[4 * a.Q + i] = tot.gz;
+    if constexpr (SPLIT == 2) {  // the top pass stored its counts first
+        if (nleaf) atomicAdd(reinterpret_cast<unsigned long long*>(a.leaves + i), (unsigned long long)nleaf);
+        if (nfar) atomicAdd(reinterpret_cast<unsigned long long*>(a.far + i), (unsigned long long)nfar);
+        if (HASH && h) atomicAdd(reinterpret_cast<unsigned long long*>(a.hash + i), (unsigned long long)h);
+    } else {
+        a.leaves[i] = nleaf;
+        a.far[i] = nfar;
+        if (HASH) a.hash[i] = h;
+    }
     if (nre) atomicAdd(a.rechecks, nre);
 }
 
@@ -846,15 +928,57 @@ void tree_query(Ctx& c, const T* q, int64_t Q, const sd_params& p, const Finaliz
     const size_t smem = poly_bytes<T>(npoly) +
                         (variant == 0 ? size_t(a.stack_depth) * kTravThreads * sizeof(int32_t)
                                       : size_t(a.stack_depth) * (kTravThreads / 32) * sizeof(int4));
+    // few queries: split the walk at depth k so that packets x 2^k warps fill
+    // the GPU (>= ~32 warps per SM)
+    const int64_t npackets = (Q + 31) / 32;
+    // SDGPU_SPLIT = 0 disables, = k forces depth k (A/B runs and tests)
+    const char* se = std::getenv("SDGPU_SPLIT");
+    const int forced = se && *se ? std::atoi(se) : -1;
+    int k = 0;
+    if (variant == 2 && t.depth >= 2) {
+        const int kmax = std::min(12, t.depth - 1);
+        if (forced >= 0) {
+            k = std::min(forced, kmax);
+        } else if (t.depth >= 3) {
+            while (k < std::min(10, kmax) && npackets * (int64_t(1) << k) < 148 * 32) ++k;
+        }
+        while (k > 0 && size_t(1 + (size_t(1) << k)) * 5 * size_t(Q) * sizeof(double) > (size_t(1) << 31)) --k;
+    }
+    a.split_depth = k;
+    a.npackets = npackets;
+    a.nslots = 1;
+    int nsplits = 1;
+    if (k > 0) {
+        split_tables(c, k);
+        a.nslots = int(c.dtree.split_count);
+        a.slot_of = c.dtree.slot_of.as<int32_t>();
+        a.split_nodes = c.dtree.split_nodes.as<int32_t>();
+        a.items = static_cast<unsigned*>(c.tmp2.ensure(size_t(npackets) * a.nslots * sizeof(unsigned)));
+        check_cuda(cudaMemsetAsync(a.items, 0, size_t(npackets) * a.nslots * sizeof(unsigned), st), "memset");
+        nsplits = 1 + a.nslots;
+        a.part = static_cast<double*>(c.part.ensure(size_t(nsplits) * 5 * Q * sizeof(double)));
+    }
     // the decision hash costs ~20 integer ops per decision: only when asked for
+    auto pick = [&](auto split) {
+        constexpr int S = decltype(split)::value;
+        return out.hash ? pair_kernel<T, true, S> : pair_kernel<T, false, S>;
+    };
     auto kern = variant == 0 ? traverse_kernel<T>
                 : variant == 1 ? (out.hash ? packet_kernel<T, true> : packet_kernel<T, false>)
-                               : (out.hash ? pair_kernel<T, true> : pair_kernel<T, false>);
+                : (k > 0 ? pick(std::integral_constant<int, 1>()) : pick(std::integral_constant<int, 0>()));
     check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)), "smem attr");
     kern<<<unsigned((Q + kTravThreads - 1) / kTravThreads), kTravThreads, smem, st>>>(a);
     check_cuda(cudaGetLastError(), "traverse kernel");
     ++launches;
-    check_cuda(launch_finalize(part, 1, Q, p.alpha, p.epsilon, 0, a.leaves, a.far, a.hash, perm, out, st),
+    if (k > 0) {
+        auto sub = pick(std::integral_constant<int, 2>());
+        check_cuda(cudaFuncSetAttribute(sub, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)), "smem attr");
+        const int64_t warps = npackets * a.nslots;
+        sub<<<unsigned((warps * 32 + kTravThreads - 1) / kTravThreads), kTravThreads, smem, st>>>(a);
+        check_cuda(cudaGetLastError(), "subtree kernel");
+        ++launches;
+    }
+    check_cuda(launch_finalize(a.part, nsplits, Q, p.alpha, p.epsilon, 0, a.leaves, a.far, a.hash, perm, out, st),
                "finalize");
     ++launches;
     c.last_launches = launches;

@@ -72,6 +72,9 @@ struct DeviceTree {
     int depth = 0;
     bool exact_boxes = true;
     DevBuf box, pairs, count, lgcount, diam64, leafrec, leafmeta;
+    int split_k = -1;         // depth of the cached split tables
+    int64_t split_count = 0;  // nodes at that depth
+    DevBuf slot_of, split_nodes;
 };
 
 struct Ctx {
@@ -126,6 +129,7 @@ const int64_t* sort_queries(Ctx& c, const T* q, int64_t Q, const double lo[3], c
 
 // Tree entry points (bvh.cu)
 void tree_upload(Ctx& c);  // host reference layout -> DeviceTree
+void split_tables(Ctx& c, int k);
 void tree_build_median(Ctx& c);
 void tree_build_lbvh(Ctx& c);
 template <class T>

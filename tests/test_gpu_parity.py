@@ -139,6 +139,29 @@ def test_random_scene_tree_decisions(sd, oracle, prec, seed):
 
 
 @pytest.mark.parametrize("prec", [0, 1])
+@pytest.mark.parametrize("split", ["0", "1", "3", "6", ""])
+def test_split_traversal_decisions(sd, oracle, prec, split, monkeypatch):
+    """The few-query split traversal (top pass above depth k, one warp per
+    (packet, depth-k subtree), merged in fp64) visits exactly the oracle's
+    nodes: counters and decision hash identical for every depth k, including
+    none ("0") and the automatic choice ("")."""
+    O = oracle
+    monkeypatch.setenv("SDGPU_SPLIT", split)
+    m0 = O.random_scene(7, 400)
+    qs = O.QueryStream(4242).draw_points(m0, 777)  # ragged last packet
+    m, q = prep(O, m0, qs, prec)
+    w, t = O.Weights.build(m), O.Tree.build(m)
+    e = engine_for(sd, O, m, w, prec, tree=t)
+    for beta in (0.2, 0.6):
+        p = O.Params(alpha=150.0, beta=beta)
+        ref = O.query(m, w, q, p, tree=t)
+        got = e.smooth_min_dist(q, sd.SmoothParams(alpha=150.0, beta=beta))
+        assert (got.leaves == ref.leaves).all() and (got.far_field == ref.far_field).all()
+        assert (got.decision_hash == ref.decision_hash).all()
+        assert_close(got, ref, prec, 150.0, f"split {split!r} beta {beta}")
+
+
+@pytest.mark.parametrize("prec", [0, 1])
 def test_gpu_median_build_matches_reference_tree(sd, oracle, prec):
     O = oracle
     for seed in (1, 5, 9):
