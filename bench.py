@@ -263,9 +263,39 @@ def measure_bvh(args, rank, world, local, eng_cls, dev, stream, flush, peaks):
                         "tri leaf; 32 B/popped node + 100 B/leaf (from this run's counters)"}}
     if peaks:
         out["roofline"]["frac_fp32"] = out["roofline"]["achieved_tflops"] / peaks["ffma_tflops"]
-    out["roofline"]["frac_hbm"] = out["roofline"]["touched_gbs"] / 6542.4
+    # the touched bytes are served from L1/L2 (ncu of pair_kernel: DRAM 0.9 % of
+    # peak, L2 hit 88 %, L1 hit 57 %); the kernel is issue-bound (76 % of issue
+    # slots, profiles/r1_pair_bvh_summary.md)
+    out["roofline"]["bound"] = "issue (L1/L2-resident tree)"
+    out["roofline"]["touched_frac_of_hbm_peak"] = out["roofline"]["touched_gbs"] / 6542.4
+    if rank == 0 and world == 1 and not args.no_cpu:
+        out["cpu_baseline"] = bvh_cpu_sample(eng, v, w, q, P)
     eng.close()
     return out
+
+
+def bvh_cpu_sample(eng, v, w, q, P, target_s=10.0):
+    """The oracle port (fp64, all host threads) on a bounded query subset of
+    cfg4, traversing the SAME tree (the GPU LBVH exported in the reference
+    layout) with the same WeightSet table."""
+    import oracle as O
+    O.build()
+    threads = O.hardware_threads()
+    wt = eng.weight_table()
+    m = O.Mesh.from_arrays(v, w.simplices, w.kinds)
+    ws = O.Weights.from_table(O.WeightTable(wt.A, wt.sup_wtilde, wt.edge_a, wt.tri_stored, wt.poly_index))
+    t = O.Tree.from_nodes(eng.export_bvh())
+    p = O.Params(alpha=P.alpha, alpha_u=P.alpha_u, beta=P.beta)
+    # both halves of the query distribution (uniform box / near surface)
+    half = len(q) // 2
+    pick = lambda n: np.concatenate([q[:n // 2], q[half:half + n - n // 2]])
+    pilot = max(threads * 16, 1024)
+    r = O.query(m, ws, pick(pilot), p, tree=t, threads=threads)
+    n = int(min(65536, max(pilot, pilot * target_s / max(r.seconds, 1e-3))))
+    r = O.query(m, ws, pick(n), p, tree=t, threads=threads)
+    return {"value": n / r.seconds, "unit": "queries/s", "cores": threads, "kind": "port",
+            "sample": f"{n} cfg4 queries (half from each half of the distribution) on the exported GPU LBVH, "
+                      f"fp64 oracle port, {r.seconds:.1f} s"}
 
 
 def run_cfg5(args, rank, world, local):
