@@ -70,6 +70,7 @@ def _declare(L):
         "sdo_gen_triangle_fan": (vp, [C.c_int, u64]),
         "sdo_gen_polyline": (vp, [C.c_int, u64]),
         "sdo_gen_random_queries": (None, [u64, vp, C.c_int, vp, vp]),
+        "sdo_gen_random_queries_scaled": (None, [u64, vp, C.c_int, f64, vp, vp]),
         "sdo_rng_new": (vp, [u64]),
         "sdo_rng_free": (None, [vp]),
         "sdo_rng_random_queries": (None, [vp, vp, C.c_int, vp, vp]),
@@ -98,6 +99,9 @@ def _declare(L):
         "sdo_decision_mix": (u64, [u64, u64]),
         "sdo_mesh_dist": (C.c_int, [vp, vp, vp, vp, vp, C.c_int, vp, vp, vp, vp]),
         "sdo_hardware_threads": (C.c_int, []),
+        "sdo_query_simplices": (C.c_int, [vp, vp, vp, vp, vp, i64, vp, C.c_int] + [vp] * 8),
+        "sdo_simplex_distance": (C.c_int, [vp, C.c_int, vp, C.c_int, C.c_int, vp]),
+        "sdo_box_primitive_proximity": (C.c_int, [vp, vp, vp, C.c_int, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -207,6 +211,14 @@ def random_queries(seed: int, mesh: Mesh, n: int):
     corners = np.empty((n, 3, 3), np.float64)
     dims = np.empty(n, np.int32)
     lib().sdo_gen_random_queries(seed, mesh.h, n, _ptr(corners), _ptr(dims))
+    return corners, dims
+
+
+def random_queries_scaled(seed: int, mesh: Mesh, n: int, size_scale: float):
+    """random_query(rng, bounding_box(mesh), size_scale) x n (shapes.hpp:243-265)."""
+    corners = np.empty((n, 3, 3), np.float64)
+    dims = np.empty(n, np.int32)
+    lib().sdo_gen_random_queries_scaled(seed, mesh.h, n, size_scale, _ptr(corners), _ptr(dims))
     return corners, dims
 
 
@@ -445,7 +457,7 @@ class MeshDistResults:
 
 def mesh_dist(mesh: Mesh, weights: Weights, query: Mesh, params: Params, tree: Tree | None = None,
               threads: int = 0) -> MeshDistResults:
-    """smooth_mesh_dist (smooth.hpp:212-255) for a point-cloud query mesh."""
+    """smooth_mesh_dist (smooth.hpp:212-255) for any query mesh."""
     p = np.array([params.alpha, params.alpha_u, params.beta, params.epsilon, params.alpha_q], np.float64)
     d = np.zeros(1)
     vg = np.zeros((len(query.vertices), 3))
@@ -454,3 +466,62 @@ def mesh_dist(mesh: Mesh, weights: Weights, query: Mesh, params: Params, tree: T
     _check(lib().sdo_mesh_dist(mesh.h, weights.h, tree.h if tree is not None else None, query.h, _ptr(p),
                                threads or hardware_threads(), _ptr(d), _ptr(vg), _ptr(pp), _ptr(cnt)))
     return MeshDistResults(float(d[0]), vg, pp, int(cnt[0]), int(cnt[1]))
+
+
+# ------------------------------------------------------- simplex queries
+def _corners(c, dims):
+    c = np.ascontiguousarray(c, np.float64).reshape(-1, 9)
+    d = np.ascontiguousarray(dims, np.int32).reshape(-1)
+    assert len(c) == len(d)
+    return c, d
+
+
+def query_simplices(mesh: Mesh, weights: Weights, corners, dims, params: Params, tree: Tree | None = None,
+                    threads: int = 0) -> Results:
+    """Batched query SIMPLICES (points, edges, triangles; corners (n,3,3),
+    unused corners ignored): smooth_min_dist(_flat) with a SimplexGeom g."""
+    c, d = _corners(corners, dims)
+    n = len(d)
+    r = Results(np.zeros(n), np.zeros((n, 3)), np.zeros(n), np.zeros((n, 3)), np.zeros(n, np.int64),
+                np.zeros(n, np.int64), np.zeros(n, np.uint64), 0.0)
+    secs = np.zeros(1)
+    _check(lib().sdo_query_simplices(mesh.h, weights.h, tree.h if tree is not None else None, _ptr(c), _ptr(d), n,
+                                     _ptr(_params_array(params)), threads or hardware_threads(), _ptr(r.d_hat),
+                                     _ptr(r.grad), _ptr(r.c), _ptr(r.grad_c), _ptr(r.leaves), _ptr(r.far_field),
+                                     _ptr(r.decision_hash), _ptr(secs)))
+    r.seconds = float(secs[0])
+    return r
+
+
+@dataclass
+class PairResult:
+    distance: float
+    phi: np.ndarray
+    lam: np.ndarray
+    point_f: np.ndarray
+    point_g: np.ndarray
+    grad: np.ndarray
+
+
+def simplex_distance(f, fdim: int, g, gdim: int, qp: bool = False) -> PairResult:
+    """exact.hpp:342-367 (qp=True: simplex_distance_qp, :158-313)."""
+    fc = np.zeros(9)
+    gc = np.zeros(9)
+    fa, ga = np.asarray(f, np.float64).reshape(-1), np.asarray(g, np.float64).reshape(-1)
+    fc[:len(fa)] = fa
+    gc[:len(ga)] = ga
+    out = np.zeros(14)
+    _check(lib().sdo_simplex_distance(_ptr(fc), fdim, _ptr(gc), gdim, int(qp), _ptr(out)))
+    return PairResult(float(out[0]), out[1:3].copy(), out[3:5].copy(), out[5:8].copy(), out[8:11].copy(),
+                      out[11:14].copy())
+
+
+def box_primitive_proximity(lo, hi, g, gdim: int):
+    """bvh.hpp:113-180 -> (distance, y_b, lambda, must_descend)."""
+    gc = np.zeros(9)
+    ga = np.asarray(g, np.float64).reshape(-1)
+    gc[:len(ga)] = ga
+    out = np.zeros(7)
+    _check(lib().sdo_box_primitive_proximity(_ptr(np.asarray(lo, np.float64)), _ptr(np.asarray(hi, np.float64)),
+                                             _ptr(gc), gdim, _ptr(out)))
+    return float(out[0]), out[1:4].copy(), out[4:6].copy(), bool(out[6])

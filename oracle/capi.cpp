@@ -5,6 +5,7 @@
 // baseline legs. Opaque handles own oracle meshes / weight tables / trees;
 // every entry returns 0 on success and -1 with sdo_last_error() set.
 #include "shapes.hpp"
+#include "sdoracle_simplex.hpp"
 
 #include <chrono>
 
@@ -21,6 +22,13 @@ int guard(F&& f) {
         g_err = e.what();
         return -1;
     }
+}
+Geom geom_from(const double* c, int dim) {
+    if (dim < 0 || dim > 2) fail("query simplex dim must be 0, 1 or 2");
+    Geom g;
+    g.dim = dim;
+    for (int k = 0; k <= dim; ++k) g.c[std::size_t(k)] = V3(c[3 * k], c[3 * k + 1], c[3 * k + 2]);
+    return g;
 }
 Params params_from(const double* p) {
     Params prm;
@@ -99,6 +107,21 @@ void sdo_gen_random_queries(std::uint64_t seed, void* mesh, int n, double* corne
     const Aabb box = bounding_box(*static_cast<Mesh*>(mesh));
     for (int i = 0; i < n; ++i) {
         const QuerySimplex q = random_query(rng, box);
+        for (int k = 0; k < 3; ++k) {
+            corners[9 * i + 3 * k + 0] = q.c[k].x;
+            corners[9 * i + 3 * k + 1] = q.c[k].y;
+            corners[9 * i + 3 * k + 2] = q.c[k].z;
+        }
+        dims[i] = q.dim;
+    }
+}
+
+void sdo_gen_random_queries_scaled(std::uint64_t seed, void* mesh, int n, double scale, double* corners,
+                                   std::int32_t* dims) {
+    Rng rng(seed);
+    const Aabb box = bounding_box(*static_cast<Mesh*>(mesh));
+    for (int i = 0; i < n; ++i) {
+        const QuerySimplex q = random_query(rng, box, scale);
         for (int k = 0; k < 3; ++k) {
             corners[9 * i + 3 * k + 0] = q.c[k].x;
             corners[9 * i + 3 * k + 1] = q.c[k].y;
@@ -328,7 +351,64 @@ int sdo_query(void* mesh, void* ws, void* bvh, const double* q, std::int64_t Q, 
     });
 }
 
-// Mesh-to-mesh distance for a query point cloud (smooth.hpp:212-255).
+// Query simplices (points, edges, triangles): corners n x 9, dims n
+// (smooth.hpp:166-198 with a SimplexGeom g).
+int sdo_query_simplices(void* mesh, void* ws, void* bvh, const double* corners, const std::int32_t* dims,
+                        std::int64_t Q, const double* params, int threads, double* d_hat, double* grad, double* c,
+                        double* grad_c, std::int64_t* leaves, std::int64_t* far, std::uint64_t* hash, double* secs) {
+    return guard([&] {
+        const Mesh& m = *static_cast<Mesh*>(mesh);
+        const WeightSet& w = *static_cast<WeightSet*>(ws);
+        const Bvh* b = static_cast<Bvh*>(bvh);
+        const Params prm = params_from(params);
+        if (w.poly_index.size() != m.ns()) fail("weight table does not match the mesh");
+        const auto t0 = std::chrono::steady_clock::now();
+        parallel_for(Q, threads, [&](std::int64_t lo, std::int64_t hi, int) {
+            Scratch s;
+            for (std::int64_t i = lo; i < hi; ++i) {
+                const Geom g = geom_from(corners + 9 * i, dims[i]);
+                const Result r = b ? smooth_min_dist(m, *b, w, g, prm, s) : smooth_min_dist_flat(m, w, g, prm, s);
+                d_hat[i] = r.d_hat;
+                if (grad) { grad[3 * i] = r.grad.x; grad[3 * i + 1] = r.grad.y; grad[3 * i + 2] = r.grad.z; }
+                if (c) c[i] = r.c;
+                if (grad_c) { grad_c[3 * i] = r.grad_c.x; grad_c[3 * i + 1] = r.grad_c.y; grad_c[3 * i + 2] = r.grad_c.z; }
+                if (leaves) leaves[i] = r.leaves;
+                if (far) far[i] = r.far_field;
+                if (hash) hash[i] = r.decision_hash;
+            }
+        });
+        if (secs) secs[0] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    });
+}
+
+// exact.hpp:342-367 / 158-313: out = distance, phi[2], lambda[2],
+// point_f[3], point_g[3], grad[3]
+static void put_pair(const GPair& r, double* out) {
+    const double v[14] = {r.distance, r.phi.c[0], r.phi.c[1], r.lambda.c[0], r.lambda.c[1],
+                          r.point_f.x, r.point_f.y, r.point_f.z, r.point_g.x, r.point_g.y, r.point_g.z,
+                          r.grad.x, r.grad.y, r.grad.z};
+    std::memcpy(out, v, sizeof(v));
+}
+int sdo_simplex_distance(const double* f, int fdim, const double* g, int gdim, int qp, double* out) {
+    return guard([&] {
+        const Geom F = geom_from(f, fdim), G = geom_from(g, gdim);
+        put_pair(qp ? simplex_distance_qp(F, G) : simplex_distance(F, G), out);
+    });
+}
+// bvh.hpp:113-180: out = distance, y_b[3], lambda[2], must_descend
+int sdo_box_primitive_proximity(const double* lo, const double* hi, const double* g, int gdim, double* out) {
+    return guard([&] {
+        Aabb box;
+        box.lo = V3(lo[0], lo[1], lo[2]);
+        box.hi = V3(hi[0], hi[1], hi[2]);
+        const GBoxProx p = box_primitive_proximity(box, geom_from(g, gdim));
+        const double v[7] = {p.distance, p.y_b.x, p.y_b.y, p.y_b.z, p.lambda.c[0], p.lambda.c[1],
+                             p.must_descend ? 1.0 : 0.0};
+        std::memcpy(out, v, sizeof(v));
+    });
+}
+
+// Mesh-to-mesh distance for any query mesh (smooth.hpp:212-255).
 // params = {alpha, alpha_u, beta, epsilon, alpha_q}; bvh NULL = flat inner sums.
 int sdo_mesh_dist(void* mesh, void* ws, void* bvh, void* query, const double* params, int threads, double* d_hat,
                   double* vertex_grads, double* per_primitive, std::int64_t* counters) {
@@ -336,8 +416,8 @@ int sdo_mesh_dist(void* mesh, void* ws, void* bvh, void* query, const double* pa
         Params prm = params_from(params);
         prm.alpha_q = params[4];
         const Mesh& q = *static_cast<Mesh*>(query);
-        const MeshDist r = smooth_mesh_dist_points(*static_cast<Mesh*>(mesh), static_cast<Bvh*>(bvh),
-                                                   *static_cast<WeightSet*>(ws), q, prm, threads);
+        const MeshDist r = smooth_mesh_dist(*static_cast<Mesh*>(mesh), static_cast<Bvh*>(bvh),
+                                            *static_cast<WeightSet*>(ws), q, prm, threads);
         *d_hat = r.d_hat;
         for (std::size_t k = 0; k < q.nv(); ++k) {
             vertex_grads[3 * k] = r.vertex_grads[k].x;
