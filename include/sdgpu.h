@@ -20,8 +20,13 @@
  *                           smooth_min_dist_flat(mesh, ws, q, params)
  *                           (smooth.hpp:189-198; SD_EXACT)
  *   sd_finalize_device   <- detail::result_from_accum              (smooth.hpp:147-159)
- *   sd_mesh_dist_points  <- smooth_mesh_dist(mesh, bvh, ws, query, params) for a
- *                           point-cloud query mesh (smooth.hpp:212-255)
+ *   sd_query_simplices   <- smooth_min_dist(mesh, bvh, ws, SimplexGeom g, params) /
+ *                           smooth_min_dist_flat(mesh, ws, g, params) for query
+ *                           points, edges and triangles (smooth.hpp:166-198,
+ *                           exact.hpp:110-367, bvh.hpp:113-180)
+ *   sd_mesh_dist         <- smooth_mesh_dist(mesh, bvh, ws, query, params) for
+ *                           any query mesh (smooth.hpp:212-255)
+ *   sd_mesh_dist_points  <- the same for a point-cloud query mesh
  *   sd_params            <- SmoothParams {alpha, alpha_u, beta, epsilon} (params.hpp:13-22)
  *   sd_outputs           <- SmoothResult {d_hat, grad, c, grad_c, leaves, far_field}
  *                           (smooth.hpp:20-27)
@@ -161,6 +166,26 @@ int sd_finalize_device(sd_ctx* ctx, const double* c, const double* grad_c, int64
 int sd_mesh_dist_points(sd_ctx* ctx, const double* qxyz, int64_t Vq, const int32_t* qpoints, int64_t Nq,
                         const sd_params* p, double alpha_q, int mode, double* d_hat, double* vertex_grads,
                         double* per_primitive);
+
+/* Query SIMPLICES g (points, edges, triangles): smooth_min_dist(mesh, bvh,
+ * ws, g, params) (mode SD_BVH, smooth.hpp:166-184; Barnes-Hut decisions use
+ * the separating-halfspace box proximity of bvh.hpp:113-180) or
+ * smooth_min_dist_flat(mesh, ws, g, params) (SD_EXACT, :189-198). corners:
+ * Q x 9 host doubles (c0, c1, c2 of each query; unused corners ignored),
+ * dims: Q values in {0, 1, 2}. The gradient is d d_hat / d (rigid
+ * translation of g), as the reference's. Computed in fp64 whatever the
+ * context precision. Outputs as sd_query_points. Blocking. */
+int sd_query_simplices(sd_ctx* ctx, const double* corners, const int32_t* dims, int64_t Q, const sd_params* p,
+                       int mode, const sd_outputs* out);
+
+/* smooth_mesh_dist (smooth.hpp:212-255) for ANY query mesh: Vq vertices
+ * (qxyz, Vq x 3), Nq simplices (qsimplices Nq x 3 vertex indices, -1 past
+ * the simplex's corners; qkinds SD_POINT / SD_EDGE / SD_TRIANGLE). Each
+ * simplex's softmin mass is split evenly over its corners. Outputs as
+ * sd_mesh_dist_points. A point-only query mesh takes the point path. */
+int sd_mesh_dist(sd_ctx* ctx, const double* qxyz, int64_t Vq, const int32_t* qsimplices, const uint8_t* qkinds,
+                 int64_t Nq, const sd_params* p, double alpha_q, int mode, double* d_hat, double* vertex_grads,
+                 double* per_primitive);
 
 /* Number of this library's kernels launched by the last query call. */
 int sd_last_launch_count(sd_ctx* ctx, int64_t* n);

@@ -38,6 +38,8 @@ EXPORTED_SYMBOLS = (
     "sd_set_bvh", "sd_build_bvh", "sd_bvh_size", "sd_export_bvh", "sd_query_points", "sd_query_points_device",
     "sd_finalize_device", "sd_last_launch_count", "sd_build_weights", "sd_weights_info", "sd_export_weights",
     "sd_mesh_dist_points",
+    "sd_query_simplices",
+    "sd_mesh_dist",
 )
 
 
@@ -98,6 +100,8 @@ def lib():
             "sd_weights_info": (C.c_int, [vp, P(f64), P(f64), P(i32), P(i32)]),
             "sd_export_weights": (C.c_int, [vp, vp, vp, vp]),
             "sd_mesh_dist_points": (C.c_int, [vp, vp, i64, vp, i64, P(_Params), f64, C.c_int, vp, vp, vp]),
+            "sd_query_simplices": (C.c_int, [vp, vp, vp, i64, P(_Params), C.c_int, P(_Outputs)]),
+            "sd_mesh_dist": (C.c_int, [vp, vp, i64, vp, vp, i64, P(_Params), f64, C.c_int, vp, vp, vp]),
         }
         for name, (res, argt) in sig.items():
             f = getattr(L, name)
@@ -301,6 +305,41 @@ class Engine:
             mode = SD_BVH if params.beta > 0 else SD_EXACT
         _check(lib().sd_mesh_dist_points(self.h, _ptr(v), len(v), _ptr(pts), n, C.byref(params._c()),
                                          float(params.alpha_q), mode, _ptr(d), _ptr(vg), _ptr(pp)))
+        return MeshDistResult(float(d[0]), vg, pp)
+
+    def query_simplices(self, corners, dims, params: SmoothParams, mode: int | None = None) -> SmoothResults:
+        """Batched query SIMPLICES (smooth_min_dist / _flat with a SimplexGeom
+        g, smooth.hpp:166-198): corners (n, 3, 3) (unused corners ignored),
+        dims (n,) in {0, 1, 2}; tree path when beta > 0 unless `mode` says."""
+        c = np.ascontiguousarray(corners, np.float64).reshape(-1, 9)
+        d = np.ascontiguousarray(dims, np.int32).reshape(-1)
+        if len(c) != len(d):
+            raise ValueError("corners and dims differ in length")
+        n = len(d)
+        if mode is None:
+            mode = SD_BVH if params.beta > 0 else SD_EXACT
+        r = SmoothResults(np.empty(n), np.empty((n, 3)), np.empty(n), np.empty((n, 3)), np.empty(n, np.int64),
+                          np.empty(n, np.int64), np.empty(n, np.uint64))
+        o = _Outputs(*(a.ctypes.data for a in (r.d_hat, r.grad, r.c, r.grad_c, r.leaves, r.far_field,
+                                               r.decision_hash)))
+        _check(lib().sd_query_simplices(self.h, _ptr(c), _ptr(d), n, C.byref(params._c()), mode, C.byref(o)))
+        return r
+
+    def smooth_mesh_dist_general(self, query_vertices, query_simplices, query_kinds, params: SmoothParams,
+                                 mode: int | None = None) -> "MeshDistResult":
+        """smooth_mesh_dist (smooth.hpp:212-255) for any query mesh: simplices
+        (n, 3) vertex indices (-1 past the corners), kinds (n,)."""
+        v = np.ascontiguousarray(query_vertices, np.float64).reshape(-1, 3)
+        sv = np.ascontiguousarray(query_simplices, np.int32).reshape(-1, 3)
+        k = np.ascontiguousarray(query_kinds, np.uint8).reshape(-1)
+        n = len(k)
+        d = np.zeros(1)
+        vg = np.zeros((len(v), 3))
+        pp = np.zeros(n)
+        if mode is None:
+            mode = SD_BVH if params.beta > 0 else SD_EXACT
+        _check(lib().sd_mesh_dist(self.h, _ptr(v), len(v), _ptr(sv), _ptr(k), n, C.byref(params._c()),
+                                  float(params.alpha_q), mode, _ptr(d), _ptr(vg), _ptr(pp)))
         return MeshDistResult(float(d[0]), vg, pp)
 
     def smooth_min_dist_flat(self, q, params: SmoothParams) -> SmoothResults:

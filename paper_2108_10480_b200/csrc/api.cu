@@ -522,6 +522,7 @@ int sd_set_geometry(sd_ctx* c, const double* xyz, int64_t V, const int32_t* sv, 
         c->exact_ready = false;
         c->have_tree = false;
         c->dtree_ready = false;
+        c->sx_tree_ready = c->sx_prim_ready = false;
         c->tree.clear();
     });
 }
@@ -548,6 +549,7 @@ int sd_set_weights(sd_ctx* c, double A, double sup, int32_t ne, const double* ed
         c->have_weights = true;
         c->exact_ready = false;
         c->dtree_ready = false;
+        c->sx_tree_ready = c->sx_prim_ready = false;
     });
 }
 
@@ -566,6 +568,7 @@ int sd_build_weights(sd_ctx* c) {
         c->have_weights = true;
         c->exact_ready = false;
         c->dtree_ready = false;
+        c->sx_tree_ready = c->sx_prim_ready = false;
     });
 }
 
@@ -599,6 +602,7 @@ int sd_set_bvh(sd_ctx* c, const sd_bvh_node* nodes, int64_t n) {
         c->tree.assign(nodes, nodes + n);
         c->have_tree = true;
         c->dtree_ready = false;
+        c->sx_tree_ready = c->sx_prim_ready = false;
     });
 }
 
@@ -747,7 +751,7 @@ int sd_mesh_dist_points(sd_ctx* c, const double* qxyz, int64_t Vq, const int32_t
         double* work = static_cast<double*>(c->tmp2.ensure(wb));
         double* vg = static_cast<double*>(c->out_gc.ensure(size_t(std::max<int64_t>(Vq, 1)) * 3 * sizeof(double)));
         double* dd = static_cast<double*>(c->out_c.ensure(sizeof(double) * 2));
-        check_cuda(launch_mesh_reduce(out.d_hat, out.grad, Nq, vidx, Vq, alpha_q, p->epsilon, work, wb, vg, dd,
+        check_cuda(launch_mesh_reduce(out.d_hat, out.grad, Nq, vidx, 1, Vq, alpha_q, p->epsilon, work, wb, vg, dd,
                                       launches, st),
                    "mesh reduction");
         check_cuda(cudaMemcpyAsync(d_hat, dd, sizeof(double), cudaMemcpyDeviceToHost, st), "D2H");
@@ -755,6 +759,119 @@ int sd_mesh_dist_points(sd_ctx* c, const double* qxyz, int64_t Vq, const int32_t
             check_cuda(cudaMemcpyAsync(vertex_grads, vg, size_t(Vq) * 3 * sizeof(double), cudaMemcpyDeviceToHost, st),
                        "D2H");
         if (per_primitive && Nq > 0)
+            check_cuda(cudaMemcpyAsync(per_primitive, out.d_hat, size_t(Nq) * sizeof(double), cudaMemcpyDeviceToHost, st),
+                       "D2H");
+        check_cuda(cudaStreamSynchronize(st), "mesh dist");
+        c->last_launches = launches;
+    });
+}
+
+static void query_outputs(Ctx& c, int64_t Q, const sd_outputs* o, FinalizeOut& out) {
+    out.d_hat = static_cast<double*>(c.out_d.ensure(size_t(Q) * sizeof(double)));
+    if (o->grad) out.grad = static_cast<double*>(c.out_g.ensure(size_t(Q) * 3 * sizeof(double)));
+    if (o->c) out.c = static_cast<double*>(c.out_c.ensure(size_t(Q) * sizeof(double)));
+    if (o->grad_c) out.grad_c = static_cast<double*>(c.out_gc.ensure(size_t(Q) * 3 * sizeof(double)));
+    if (o->leaves) out.leaves = static_cast<int64_t*>(c.out_l.ensure(size_t(Q) * sizeof(int64_t)));
+    if (o->far_field) out.far_field = static_cast<int64_t*>(c.out_f.ensure(size_t(Q) * sizeof(int64_t)));
+    if (o->decision_hash) out.hash = static_cast<uint64_t*>(c.out_h.ensure(size_t(Q) * sizeof(uint64_t)));
+}
+
+// corners / dims -> device (c.qgeom, c.qdim), validated
+static void upload_simplices(Ctx& c, const double* corners, const int32_t* dims, int64_t Q, cudaStream_t st) {
+    for (int64_t i = 0; i < Q; ++i)
+        if (dims[i] < 0 || dims[i] > 2) throw ArgError{"query " + std::to_string(i) + ": dim must be 0, 1 or 2"};
+    double* qg = static_cast<double*>(c.qgeom.ensure(size_t(Q) * 9 * sizeof(double)));
+    int32_t* qd = static_cast<int32_t*>(c.qdim.ensure(size_t(Q) * sizeof(int32_t)));
+    check_cuda(cudaMemcpyAsync(qg, corners, size_t(Q) * 9 * sizeof(double), cudaMemcpyHostToDevice, st), "H2D corners");
+    check_cuda(cudaMemcpyAsync(qd, dims, size_t(Q) * sizeof(int32_t), cudaMemcpyHostToDevice, st), "H2D dims");
+}
+
+int sd_query_simplices(sd_ctx* c, const double* corners, const int32_t* dims, int64_t Q, const sd_params* p, int mode,
+                       const sd_outputs* o) {
+    return guard([&] {
+        if (!c) throw ArgError{"ctx is NULL"};
+        check_params(p);
+        check_ready(*c, mode);
+        if (Q < 0 || (Q > 0 && (!corners || !dims || !o || !o->d_hat))) throw ArgError{"bad query / output pointers"};
+        if (Q == 0) return;
+        DeviceScope ds(c->device);
+        cudaStream_t st = c->stream;
+        upload_simplices(*c, corners, dims, Q, st);
+        FinalizeOut out;
+        query_outputs(*c, Q, o, out);
+        simplex_query(*c, c->qgeom.as<double>(), c->qdim.as<int32_t>(), Q, *p, mode, out, st);
+        auto d2h = [&](void* dst, const void* src, size_t bytes) {
+            if (dst) check_cuda(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st), "D2H results");
+        };
+        d2h(o->d_hat, out.d_hat, size_t(Q) * sizeof(double));
+        d2h(o->grad, out.grad, size_t(Q) * 3 * sizeof(double));
+        d2h(o->c, out.c, size_t(Q) * sizeof(double));
+        d2h(o->grad_c, out.grad_c, size_t(Q) * 3 * sizeof(double));
+        d2h(o->leaves, out.leaves, size_t(Q) * sizeof(int64_t));
+        d2h(o->far_field, out.far_field, size_t(Q) * sizeof(int64_t));
+        d2h(o->decision_hash, out.hash, size_t(Q) * sizeof(uint64_t));
+        check_cuda(cudaStreamSynchronize(st), "query simplices");
+    });
+}
+
+int sd_mesh_dist(sd_ctx* c, const double* qxyz, int64_t Vq, const int32_t* qsimplices, const uint8_t* qkinds,
+                 int64_t Nq, const sd_params* p, double alpha_q, int mode, double* d_hat, double* vertex_grads,
+                 double* per_primitive) {
+    return guard([&] {
+        if (!c) throw ArgError{"ctx is NULL"};
+        check_params(p);
+        check_ready(*c, mode);
+        if (!(alpha_q > 0) || !std::isfinite(alpha_q)) throw ArgError{"alpha_q must be positive and finite"};
+        if (Vq < 0 || Nq < 0 || (Vq > 0 && !qxyz) || (Nq > 0 && (!qsimplices || !qkinds)) || !d_hat ||
+            (Vq > 0 && !vertex_grads))
+            throw ArgError{"bad query mesh arrays"};
+        bool points_only = true;
+        std::vector<int32_t> sv(size_t(Nq) * 3, -1), pts(static_cast<size_t>(Nq));
+        std::vector<double> corners(size_t(Nq) * 9, 0.0);
+        std::vector<int32_t> dims(static_cast<size_t>(Nq));
+        for (int64_t j = 0; j < Nq; ++j) {
+            const int kind = qkinds[j];
+            if (kind > SD_TRIANGLE) throw ArgError{"query simplex " + std::to_string(j) + ": bad kind"};
+            points_only = points_only && kind == SD_POINT;
+            dims[j] = kind;
+            for (int k = 0; k <= kind; ++k) {
+                const int32_t v = qsimplices[3 * j + k];
+                if (v < 0 || v >= Vq)
+                    throw ArgError{"query simplex " + std::to_string(j) + ": vertex index out of range"};
+                sv[3 * j + k] = v;
+                for (int a = 0; a < 3; ++a) corners[9 * j + 3 * k + a] = qxyz[3 * size_t(v) + a];
+            }
+            pts[j] = sv[3 * j];
+        }
+        if (points_only) {
+            const int rc = sd_mesh_dist_points(c, qxyz, Vq, pts.data(), Nq, p, alpha_q, mode, d_hat, vertex_grads,
+                                               per_primitive);
+            if (rc != SD_OK) throw ArgError{sd_last_error()};
+            return;
+        }
+        DeviceScope ds(c->device);
+        cudaStream_t st = c->stream;
+        int64_t launches = 0;
+        upload_simplices(*c, corners.data(), dims.data(), Nq, st);
+        FinalizeOut out;
+        out.d_hat = static_cast<double*>(c->out_d.ensure(size_t(Nq) * sizeof(double)));
+        out.grad = static_cast<double*>(c->out_g.ensure(size_t(Nq) * 3 * sizeof(double)));
+        simplex_query(*c, c->qgeom.as<double>(), c->qdim.as<int32_t>(), Nq, *p, mode, out, st);
+        launches += c->last_launches;
+        int32_t* vidx = static_cast<int32_t*>(c->out_l.ensure(sv.size() * sizeof(int32_t)));
+        check_cuda(cudaMemcpyAsync(vidx, sv.data(), sv.size() * sizeof(int32_t), cudaMemcpyHostToDevice, st), "H2D");
+        const size_t wb = mesh_reduce_work_bytes(Nq);
+        double* work = static_cast<double*>(c->tmp2.ensure(wb));
+        double* vg = static_cast<double*>(c->out_gc.ensure(size_t(std::max<int64_t>(Vq, 1)) * 3 * sizeof(double)));
+        double* dd = static_cast<double*>(c->out_c.ensure(sizeof(double) * 2));
+        check_cuda(launch_mesh_reduce(out.d_hat, out.grad, Nq, vidx, 3, Vq, alpha_q, p->epsilon, work, wb, vg, dd,
+                                      launches, st),
+                   "mesh reduction");
+        check_cuda(cudaMemcpyAsync(d_hat, dd, sizeof(double), cudaMemcpyDeviceToHost, st), "D2H");
+        if (Vq > 0)
+            check_cuda(cudaMemcpyAsync(vertex_grads, vg, size_t(Vq) * 3 * sizeof(double), cudaMemcpyDeviceToHost, st),
+                       "D2H");
+        if (per_primitive)
             check_cuda(cudaMemcpyAsync(per_primitive, out.d_hat, size_t(Nq) * sizeof(double), cudaMemcpyDeviceToHost, st),
                        "D2H");
         check_cuda(cudaStreamSynchronize(st), "mesh dist");

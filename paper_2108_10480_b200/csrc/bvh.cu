@@ -20,7 +20,7 @@
 
 #include <cub/cub.cuh>
 
-#include "context.h"
+#include "traverse.cuh"
 
 namespace sdgpu {
 
@@ -121,21 +121,12 @@ static void median_build_host(const Ctx& c, std::vector<sd_bvh_node>& out) {
 void tree_build_median(Ctx& c) {
     median_build_host(c, c.tree);
     c.dtree_ready = false;
+    c.sx_tree_ready = c.sx_prim_ready = false;
 }
 
 // ---------------------------------------------------------------- upload
 template <class T>
-struct alignas(16) NodeT {  // 2 x (4 T): (lo, diam) (hi, link)
-    T v[8];
-};
-template <class T>
-struct alignas(16) PairT {  // both children of an internal node + their log2 n_B
-    NodeT<T> l, r;
-    T lgc[4];
-};
-
-template <class T>
-static void upload_tree_T(Ctx& c) {
+static void upload_tree_T(Ctx& c, DeviceTree& t) {
     const int64_t n = int64_t(c.tree.size());
     const int64_t N = c.N;
     if (n != 2 * N - 1) throw std::runtime_error("tree must have 2N - 1 nodes");
@@ -215,7 +206,6 @@ static void upload_tree_T(Ctx& c) {
         lgc[id] = T(std::log2(double(nd.count)));
         d64[id] = nd.diameter;
     }
-    DeviceTree& t = c.dtree;
     t.nodes = n;
     t.split_k = -1;
     t.leaves = slot;
@@ -247,12 +237,10 @@ static void upload_tree_T(Ctx& c) {
     up(t.diam64, d64.data(), d64.size() * sizeof(double));
     up(t.leafrec, leafrec.data(), leafrec.size() * sizeof(T));
     up(t.leafmeta, leafmeta.data(), leafmeta.size() * sizeof(int32_t));
-    c.dtree_ready = true;
 }
 
 // Nodes at depth exactly k (pre-order) for the split traversal, cached per k.
-void split_tables(Ctx& c, int k) {
-    DeviceTree& t = c.dtree;
+void split_tables(Ctx& c, DeviceTree& t, int k) {
     if (t.split_k == k) return;
     const int64_t n = int64_t(c.tree.size());
     std::vector<int32_t> slot_of(size_t(n), -1), dep(size_t(n), 0);
@@ -276,9 +264,12 @@ void split_tables(Ctx& c, int k) {
 }
 
 void tree_upload(Ctx& c) {
-    if (c.precision == SD_FP32) upload_tree_T<float>(c);
-    else upload_tree_T<double>(c);
+    if (c.precision == SD_FP32) upload_tree_T<float>(c, c.dtree);
+    else upload_tree_T<double>(c, c.dtree);
+    c.dtree_ready = true;
 }
+
+void tree_upload64(Ctx& c, DeviceTree& t) { upload_tree_T<double>(c, t); }
 
 // ---------------------------------------------------------- query order
 __device__ __forceinline__ uint32_t spread10(uint32_t v) {
@@ -307,61 +298,6 @@ __global__ void query_morton(const T* __restrict__ q, int64_t Q, double3 lo, dou
 }
 
 // ------------------------------------------------------------ traversal
-template <class T>
-struct TraverseArgs {
-    const T* q;
-    const int64_t* perm;  // sorted position -> query index
-    int64_t Q;
-    const NodeT<T>* box;
-    const PairT<T>* pairs;  // [parent]: the two children of an internal node
-    const int32_t* count;
-    const T* lgcount;     // log2 n_B per node (far-field weight exponent)
-    T lw_ff;              // log2 w_ff
-    const double* diam64;
-    const T* leafrec;
-    const int32_t* leafmeta;
-    const Poly<T>* polys;  // [0, ne): edge polys, [ne, ne + nt): tri polys
-    int ne, npoly;
-    int use_bh;
-    int exact_boxes;  // every fp32 box equals its fp64 box (quantized geometry)
-    int stack_depth;
-    double beta64;
-    Phys<T> ph;
-    double* part;       // [5][Q] fp64 state in sorted order
-    int64_t* leaves;    // sorted order
-    int64_t* far;
-    uint64_t* hash;
-    unsigned long long* rechecks;  // fp64 re-decisions (diagnostic)
-    // split mode (few queries): see pair_kernel
-    int split_depth, nslots;
-    int64_t npackets;
-    const int32_t* slot_of;     // node -> depth-k slot, or -1
-    const int32_t* split_nodes;  // slot -> node
-    unsigned* items;            // [packet][slot] lane mask reaching the slot
-};
-
-constexpr int kTravThreads = 128;
-
-// shared-memory bytes of the polynomial table, padded so the stacks after it
-// stay 16-byte aligned
-template <class T>
-__host__ __device__ constexpr size_t poly_bytes(int npoly) {
-    return (sizeof(Poly<T>) * size_t(npoly) + 15) / 16 * 16;
-}
-
-// Far-field term of a whole subtree (smooth.hpp:67-75): n_B w_ff collapsed
-// onto the box's closest point; gradient (q - y_B) / d_B.
-template <class T>
-__device__ __forceinline__ void far_term(const Phys<T>& ph, T lw, T d, T r, T dx, T dy, T dz, Acc<T>& acc) {
-    const T xm = bump(acc, masked(ph, d, fma(ph.kappa, d, lw - acc.m)), [&] { return fma(ph.kappa, d, lw); });
-    const T e = Math<T>::ex2(xm);
-    const T er = e * r;
-    acc.s += e;
-    acc.gx = fma(er, dx, acc.gx);
-    acc.gy = fma(er, dy, acc.gy);
-    acc.gz = fma(er, dz, acc.gz);
-}
-
 // Unit-weight edge / triangle leaf (poly_index < 0): w = A^S.
 template <class T, int KIND>
 __device__ __forceinline__ void unit_term(const Phys<T>& ph, const Poly<T>& pc, T qx, T qy, T qz, const T* rec,
@@ -696,150 +632,22 @@ __device__ __forceinline__ bool visit(const TraverseArgs<T>& a, const Poly<T>* p
     return false;
 }
 
-// K3 (default): warp-coherent packet traversal over CHILD PAIRS. The root
-// is tested alone; afterwards every warp step fetches both children of
-// the current node (one pair record, broadcast) and each lane whose own
-// traversal reached the node tests both (far field / exact leaf / descend)
-// -- per-lane decisions are exactly collect_contributions'
-// (smooth.hpp:101-131). The warp continues into the left child if any lane
-// descends there (pushing the right child with its lane mask), else into
-// the right child, else pops. Stack entries (node, its link, mask, depth)
-// live in shared memory, one stack per warp.
-//
-// SPLIT = 1 / 2 (few queries): the same walk cut at tree depth k. The top
-// pass (1) stops above depth k and records, per query packet and depth-k
-// node, the mask of lanes that reach it; the subtree pass (2) runs one warp
-// per (packet, depth-k node) from that node with that mask. Each lane still
-// visits exactly its reference node set; the partial sums land in split
-// slots merged by K4, so a batch of a few thousand queries fills the GPU.
-template <class T, bool HASH, int SPLIT>
-__global__ void __launch_bounds__(kTravThreads) pair_kernel(const __grid_constant__ TraverseArgs<T> a) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    Poly<T>* polys = reinterpret_cast<Poly<T>*>(smem_raw);
-    int4* stacks = reinterpret_cast<int4*>(smem_raw + poly_bytes<T>(a.npoly));
-    for (int i = threadIdx.x; i < a.npoly * kPolyCoefs; i += blockDim.x)
-        reinterpret_cast<T*>(polys)[i] = reinterpret_cast<const T*>(a.polys)[i];
-    __syncthreads();
-
-    const unsigned lane = threadIdx.x & 31u;
-    int4* st = stacks + (threadIdx.x >> 5) * a.stack_depth;
-    // packet (32 sorted queries) and, in the subtree pass, the depth-k slot
-    const int64_t gwarp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    const int64_t packet = SPLIT == 2 ? gwarp / a.nslots : gwarp;
-    const int slot = SPLIT == 2 ? int(gwarp % a.nslots) : 0;
-    if (SPLIT == 2 && packet >= a.npackets) return;
-    const int64_t i = packet * 32 + lane;
-    const bool valid = i < a.Q;
-    const int64_t qi = valid ? (a.perm ? a.perm[i] : i) : 0;
-    const T qx = valid ? a.q[3 * qi] : T(0), qy = valid ? a.q[3 * qi + 1] : T(0), qz = valid ? a.q[3 * qi + 2] : T(0);
-    double* part = a.part + (SPLIT == 2 ? size_t(1 + slot) * 5 * a.Q : 0);
-    unsigned mask = __ballot_sync(0xffffffffu, valid);
-    if (mask == 0u) return;
-    Acc<T> acc;
-    acc.init();
-    int64_t nleaf = 0, nfar = 0;
-    uint64_t h = 0;
-    unsigned long long nre = 0;
-    int32_t cur, cur_link;
-    int depth;
-    if constexpr (SPLIT == 2) {
-        mask &= a.items[packet * a.nslots + slot];
-        cur = a.split_nodes[slot];
-        depth = a.split_depth;
-    } else {
-        cur = 0;
-        depth = 0;
+// The point query of one lane (K3's VIS for bvh.cu).
+template <class T>
+struct PointVisit {
+    T qx, qy, qz;
+    __device__ __forceinline__ void load(const TraverseArgs<T>& a, int64_t qi, bool valid) {
+        qx = valid ? a.q[3 * qi] : T(0);
+        qy = valid ? a.q[3 * qi + 1] : T(0);
+        qz = valid ? a.q[3 * qi + 2] : T(0);
     }
-    memcpy(&cur_link, &a.box[cur].v[7], sizeof(int32_t));
-    if (mask) {  // the start node (root, or the depth-k node) is popped alone
-        const NodeT<T> b0 = a.box[cur];
-        const bool d = ((mask >> lane) & 1u) &&
-                       visit<T, HASH>(a, polys, b0, cur, a.lgcount[cur], qx, qy, qz, acc, nleaf, nfar, h, nre);
-        mask = __ballot_sync(0xffffffffu, d);
+    template <bool HASH>
+    __device__ __forceinline__ bool visit(const TraverseArgs<T>& a, const Poly<T>* polys, const NodeT<T>& b,
+                                          int32_t id, T lgc, Acc<T>& acc, int64_t& nleaf, int64_t& nfar, uint64_t& h,
+                                          unsigned long long& nre) const {
+        return sdgpu::visit<T, HASH>(a, polys, b, id, lgc, qx, qy, qz, acc, nleaf, nfar, h, nre);
     }
-    int sp = 0;
-    while (mask) {
-        const int32_t lid = cur + 1, rid = cur_link;
-        if (SPLIT == 1 && depth + 1 == a.split_depth) {  // children start subtrees: hand over
-            if (lane == 0) {
-                unsigned* it = a.items + packet * a.nslots;
-                it[a.slot_of[lid]] = mask;
-                it[a.slot_of[rid]] = mask;
-            }
-            __syncwarp();
-            if (sp > 0) {
-                --sp;
-                const int4 e = st[sp];
-                cur = e.x;
-                cur_link = e.y;
-                mask = unsigned(e.z);
-                depth = e.w;
-            } else {
-                mask = 0u;
-            }
-            continue;
-        }
-        const PairT<T>& pr = a.pairs[cur];  // warp-uniform: broadcast loads
-        const NodeT<T> bl = pr.l, br = pr.r;
-        const T lgl = pr.lgc[0], lgr = pr.lgc[1];
-        // the most likely next step descends into the left child: pull its
-        // pair record into L1 while this one is being processed
-        if (lane == 0) asm volatile("prefetch.global.L1 [%0];" ::"l"(a.pairs + lid));
-        bool dl = false, dr = false;
-        if ((mask >> lane) & 1u) {
-            dl = visit<T, HASH>(a, polys, bl, lid, lgl, qx, qy, qz, acc, nleaf, nfar, h, nre);
-            dr = visit<T, HASH>(a, polys, br, rid, lgr, qx, qy, qz, acc, nleaf, nfar, h, nre);
-        }
-        const unsigned DL = __ballot_sync(0xffffffffu, dl), DR = __ballot_sync(0xffffffffu, dr);
-        int32_t llink, rlink;
-        memcpy(&llink, &bl.v[7], sizeof(int32_t));
-        memcpy(&rlink, &br.v[7], sizeof(int32_t));
-        if (DL) {
-            if (DR) {
-                if (lane == 0) st[sp] = make_int4(rid, rlink, int(DR), depth + 1);
-                __syncwarp();
-                ++sp;
-            }
-            cur = lid;
-            cur_link = llink;
-            mask = DL;
-            ++depth;
-        } else if (DR) {
-            cur = rid;
-            cur_link = rlink;
-            mask = DR;
-            ++depth;
-        } else if (sp > 0) {
-            --sp;
-            const int4 e = st[sp];
-            cur = e.x;
-            cur_link = e.y;
-            mask = unsigned(e.z);
-            depth = e.w;
-        } else {
-            mask = 0u;
-        }
-    }
-    if (!valid) return;
-    Tot tot;
-    tot.init();
-    tot.flush(acc);
-    part[i] = tot.M;
-    part[a.Q + i] = tot.s;
-    part[2 * a.Q + i] = tot.gx;
-    part[3 * a.Q + i] = tot.gy;
-    part[4 * a.Q + i] = tot.gz;
-    if constexpr (SPLIT == 2) {  // the top pass stored its counts first
-        if (nleaf) atomicAdd(reinterpret_cast<unsigned long long*>(a.leaves + i), (unsigned long long)nleaf);
-        if (nfar) atomicAdd(reinterpret_cast<unsigned long long*>(a.far + i), (unsigned long long)nfar);
-        if (HASH && h) atomicAdd(reinterpret_cast<unsigned long long*>(a.hash + i), (unsigned long long)h);
-    } else {
-        a.leaves[i] = nleaf;
-        a.far[i] = nfar;
-        if (HASH) a.hash[i] = h;
-    }
-    if (nre) atomicAdd(a.rechecks, nre);
-}
+};
 
 // Morton codes (10 bits per axis over [lo, hi]) + CUB radix sort: the
 // returned permutation lists query indices in spatial order (device
@@ -919,63 +727,26 @@ void tree_query(Ctx& c, const T* q, int64_t Q, const sd_params& p, const Finaliz
     a.far = cnt + Q;
     a.hash = reinterpret_cast<uint64_t*>(cnt + 2 * Q);
     a.rechecks = re;
+    a.qgeom = nullptr;
+    a.qdim = nullptr;
+    a.leafgeom = nullptr;
     // SDGPU_TRAVERSAL = thread | packet | pair (default) selects the kernel (A/B runs)
     static const int variant = [] {
         const char* e = std::getenv("SDGPU_TRAVERSAL");
         const std::string v = e ? e : "pair";
         return v == "thread" ? 0 : (v == "packet" ? 1 : 2);
     }();
-    const size_t smem = poly_bytes<T>(npoly) +
-                        (variant == 0 ? size_t(a.stack_depth) * kTravThreads * sizeof(int32_t)
-                                      : size_t(a.stack_depth) * (kTravThreads / 32) * sizeof(int4));
-    // few queries: split the walk at depth k so that packets x 2^k warps fill
-    // the GPU (>= ~32 warps per SM)
-    const int64_t npackets = (Q + 31) / 32;
-    // SDGPU_SPLIT = 0 disables, = k forces depth k (A/B runs and tests)
-    const char* se = std::getenv("SDGPU_SPLIT");
-    const int forced = se && *se ? std::atoi(se) : -1;
-    int k = 0;
-    if (variant == 2 && t.depth >= 2) {
-        const int kmax = std::min(12, t.depth - 1);
-        if (forced >= 0) {
-            k = std::min(forced, kmax);
-        } else if (t.depth >= 3) {
-            while (k < std::min(10, kmax) && npackets * (int64_t(1) << k) < 148 * 32) ++k;
-        }
-        while (k > 0 && size_t(1 + (size_t(1) << k)) * 5 * size_t(Q) * sizeof(double) > (size_t(1) << 31)) --k;
-    }
-    a.split_depth = k;
-    a.npackets = npackets;
-    a.nslots = 1;
     int nsplits = 1;
-    if (k > 0) {
-        split_tables(c, k);
-        a.nslots = int(c.dtree.split_count);
-        a.slot_of = c.dtree.slot_of.as<int32_t>();
-        a.split_nodes = c.dtree.split_nodes.as<int32_t>();
-        a.items = static_cast<unsigned*>(c.tmp2.ensure(size_t(npackets) * a.nslots * sizeof(unsigned)));
-        check_cuda(cudaMemsetAsync(a.items, 0, size_t(npackets) * a.nslots * sizeof(unsigned), st), "memset");
-        nsplits = 1 + a.nslots;
-        a.part = static_cast<double*>(c.part.ensure(size_t(nsplits) * 5 * Q * sizeof(double)));
-    }
-    // the decision hash costs ~20 integer ops per decision: only when asked for
-    auto pick = [&](auto split) {
-        constexpr int S = decltype(split)::value;
-        return out.hash ? pair_kernel<T, true, S> : pair_kernel<T, false, S>;
-    };
-    auto kern = variant == 0 ? traverse_kernel<T>
-                : variant == 1 ? (out.hash ? packet_kernel<T, true> : packet_kernel<T, false>)
-                : (k > 0 ? pick(std::integral_constant<int, 1>()) : pick(std::integral_constant<int, 0>()));
-    check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)), "smem attr");
-    kern<<<unsigned((Q + kTravThreads - 1) / kTravThreads), kTravThreads, smem, st>>>(a);
-    check_cuda(cudaGetLastError(), "traverse kernel");
-    ++launches;
-    if (k > 0) {
-        auto sub = pick(std::integral_constant<int, 2>());
-        check_cuda(cudaFuncSetAttribute(sub, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)), "smem attr");
-        const int64_t warps = npackets * a.nslots;
-        sub<<<unsigned((warps * 32 + kTravThreads - 1) / kTravThreads), kTravThreads, smem, st>>>(a);
-        check_cuda(cudaGetLastError(), "subtree kernel");
+    if (variant == 2) {
+        nsplits = launch_pair_traversal<T, PointVisit<T>>(c, c.dtree, a, out.hash != nullptr, st, launches);
+    } else {
+        const size_t smem = poly_bytes<T>(npoly) +
+                            (variant == 0 ? size_t(a.stack_depth) * kTravThreads * sizeof(int32_t)
+                                          : size_t(a.stack_depth) * (kTravThreads / 32) * sizeof(int4));
+        auto kern = variant == 0 ? traverse_kernel<T> : (out.hash ? packet_kernel<T, true> : packet_kernel<T, false>);
+        check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)), "smem attr");
+        kern<<<unsigned((Q + kTravThreads - 1) / kTravThreads), kTravThreads, smem, st>>>(a);
+        check_cuda(cudaGetLastError(), "traverse kernel");
         ++launches;
     }
     check_cuda(launch_finalize(a.part, nsplits, Q, p.alpha, p.epsilon, 0, a.leaves, a.far, a.hash, perm, out, st),

@@ -108,6 +108,14 @@ struct Ctx {
     DeviceTree dtree;
     bool dtree_ready = false;
 
+    // simplex queries (simplex.cu): fp64 traversal layout of the same tree
+    // (when the context is SD_FP32), fp64 leaf geometry in tree order and
+    // per-primitive geometry in index order; rebuilt after any geometry,
+    // weight or tree change
+    DeviceTree dtree64;
+    DevBuf leafgeom, primgeom, primmeta, qgeom, qdim;
+    bool sx_tree_ready = false, sx_prim_ready = false;
+
     // scratch
     DevBuf qd, qT, part, out_d, out_g, out_c, out_gc, out_l, out_f, out_h;
     DevBuf perm, keys, tmp, tmp2, counters, polys;
@@ -129,7 +137,10 @@ const int64_t* sort_queries(Ctx& c, const T* q, int64_t Q, const double lo[3], c
 
 // Tree entry points (bvh.cu)
 void tree_upload(Ctx& c);  // host reference layout -> DeviceTree
-void split_tables(Ctx& c, int k);
+void tree_upload64(Ctx& c, DeviceTree& t);  // same, fp64 records
+void simplex_query(Ctx& c, const double* corners, const int32_t* dims, int64_t Q, const sd_params& p, int mode,
+                   const FinalizeOut& out, cudaStream_t st);
+void split_tables(Ctx& c, DeviceTree& t, int k);  // nodes at depth k of c.tree
 void tree_build_median(Ctx& c);
 void tree_build_lbvh(Ctx& c);
 template <class T>

@@ -126,15 +126,30 @@ __global__ void mass_kernel(const double* __restrict__ d, int64_t n, double alph
     const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (j < n) mass[j] = exp(-alpha_q * d[j]);
 }
+// vidx: vertex of each point simplex (stride 1; NULL = identity), or the
+// corners of each simplex (stride 3, -1 past the last corner): the mass is
+// split evenly over the corners (smooth.hpp:243-245).
 __global__ void scatter_kernel(const double* __restrict__ mass, const double* __restrict__ grad, int64_t n,
-                               const int32_t* __restrict__ vidx, double* vg) {
+                               const int32_t* __restrict__ vidx, int stride, double* vg) {
     const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (j >= n) return;
-    const int64_t v = vidx ? vidx[j] : j;
-    const double m = mass[j];
-    atomicAdd(vg + 3 * v, m * grad[3 * j]);
-    atomicAdd(vg + 3 * v + 1, m * grad[3 * j + 1]);
-    atomicAdd(vg + 3 * v + 2, m * grad[3 * j + 2]);
+    if (stride == 1) {
+        const int64_t v = vidx ? vidx[j] : j;
+        const double m = mass[j];
+        atomicAdd(vg + 3 * v, m * grad[3 * j]);
+        atomicAdd(vg + 3 * v + 1, m * grad[3 * j + 1]);
+        atomicAdd(vg + 3 * v + 2, m * grad[3 * j + 2]);
+        return;
+    }
+    const int32_t* s = vidx + size_t(stride) * j;
+    const int nv = 1 + (s[1] >= 0) + (s[1] >= 0 && s[2] >= 0);
+    const double split = mass[j] / nv;
+    for (int k = 0; k < nv; ++k) {
+        const int64_t v = s[k];
+        atomicAdd(vg + 3 * v, split * grad[3 * j]);
+        atomicAdd(vg + 3 * v + 1, split * grad[3 * j + 1]);
+        atomicAdd(vg + 3 * v + 2, split * grad[3 * j + 2]);
+    }
 }
 __global__ void mesh_finish_kernel(double* vg, int64_t nv, const double* __restrict__ denom, double alpha_q, double eps,
                                    double* d_out) {
@@ -149,8 +164,8 @@ __global__ void mesh_finish_kernel(double* vg, int64_t nv, const double* __restr
     (void)f;
 }
 
-cudaError_t launch_mesh_reduce(const double* d, const double* grad, int64_t n, const int32_t* vidx, int64_t nv,
-                               double alpha_q, double eps, double* work, size_t work_bytes, double* vg,
+cudaError_t launch_mesh_reduce(const double* d, const double* grad, int64_t n, const int32_t* vidx, int stride,
+                               int64_t nv, double alpha_q, double eps, double* work, size_t work_bytes, double* vg,
                                double* d_out, int64_t& launches, cudaStream_t st) {
     // work: [mass n][denom 1][cub temp]
     double* mass = work;
@@ -167,7 +182,7 @@ cudaError_t launch_mesh_reduce(const double* d, const double* grad, int64_t n, c
         if (need > tb) return cudaErrorMemoryAllocation;
         e = cub::DeviceReduce::Sum(tmp, tb, mass, denom, int(n), st);
         if (e != cudaSuccess) return e;
-        scatter_kernel<<<unsigned((n + B - 1) / B), B, 0, st>>>(mass, grad, n, vidx, vg);
+        scatter_kernel<<<unsigned((n + B - 1) / B), B, 0, st>>>(mass, grad, n, vidx, stride, vg);
         launches += 4;
     } else {
         e = cudaMemsetAsync(denom, 0, sizeof(double), st);

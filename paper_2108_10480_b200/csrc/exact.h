@@ -53,8 +53,10 @@ cudaError_t launch_finalize(const double* part, int splits, int64_t Q, double al
 cudaError_t launch_finalize_sums(const double* c, const double* grad_c, int64_t Q, double alpha, double epsilon,
                                  double* d_hat, double* grad, cudaStream_t st);
 
-// Mesh-to-mesh outer LogSumExp (smooth.hpp:237-254), point query simplices.
-cudaError_t launch_mesh_reduce(const double* d, const double* grad, int64_t n, const int32_t* vidx, int64_t nv,
+// Mesh-to-mesh outer LogSumExp (smooth.hpp:237-254); vidx stride 1: point
+// simplices, stride 3: corner lists (-1 padded).
+cudaError_t launch_mesh_reduce(const double* d, const double* grad, int64_t n, const int32_t* vidx, int stride,
+                               int64_t nv,
                                double alpha_q, double eps, double* work, size_t work_bytes, double* vg,
                                double* d_out, int64_t& launches, cudaStream_t st);
 size_t mesh_reduce_work_bytes(int64_t n);

@@ -189,6 +189,7 @@ void tree_build_lbvh(Ctx& c) {
     const int64_t n = c.N;
     c.tree.clear();
     c.dtree_ready = false;
+    c.sx_tree_ready = c.sx_prim_ready = false;
     if (n == 0) return;
     cudaStream_t st = c.stream;
     // scene box of the primitive corners (host: O(V), exact)
