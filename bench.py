@@ -393,59 +393,79 @@ def run_cfg5(args, rank, world, local):
 
 def run_m2m(args, rank, world, local):
     """Mesh-to-mesh smooth distance d_hat(M, Mq) (smooth_mesh_dist,
-    smooth.hpp:212-255) on stand-ins for the paper's timed simulation row
-    Terrain (6,591,087 lidar points, alpha 100) vs Bunny (3,485 points,
-    alpha_q 20): 250.0 ms average per evaluation on 28 CPU threads
-    (PAPER.md:1378-1397). One step = one evaluation through the public host
-    API (query cloud H2D, inner BVH queries, outer LogSumExp, vertex
-    gradients D2H); the terrain's weights and tree are built once."""
+    smooth.hpp:212-255) on seeded stand-ins for every row of the paper's
+    timing table (average evaluation time on 28 CPU
+    threads; sim_rows.py has the shapes, with each row's primitive types,
+    counts, alpha and alpha_q). One step = one evaluation through the public
+    host API (query mesh H2D, inner BVH queries -- points on the fp32 point
+    path, edges / triangles on the fp64 simplex path -- outer LogSumExp,
+    vertex gradients D2H); the data mesh's weights and GPU LBVH are built
+    once per row. The oracle port evaluates the same row once on the host
+    threads (cpu_ms) and its d_hat checks ours."""
     import torch
     import paper_2108_10480_b200 as sd
-    from paper_2108_10480_b200 import configs
+    from paper_2108_10480_b200 import configs, sim_rows
     torch.cuda.set_device(local)
-    terrain, bunny = configs.terrain_bunny()
-    terrain, bunny = configs.quantize(terrain), configs.quantize(bunny)
-    n = len(terrain)
-    S = np.stack([np.arange(n), -np.ones(n, np.int64), -np.ones(n, np.int64)], 1).astype(np.int32)
-    K = np.zeros(n, np.uint8)
-    eng = sd.Engine(local, sd.SD_FP32)
-    eng.set_geometry(terrain, S, K)
-    eng.build_weights()
-    eng.build_bvh(sd.SD_BVH_LBVH)
-    P = sd.SmoothParams(alpha=100.0, alpha_u=600.0, beta=0.5, alpha_q=20.0)
-    for _ in range(max(3, args.warmup)):
-        md = eng.smooth_mesh_dist(bunny, P)
-    times = []
+    names = args.rows.split(",") if args.rows else list(sim_rows.ROWS)
+    rows = []
     with ClockSampler(local) as clk:
-        for _ in range(args.steps):
-            torch.cuda.synchronize()
+        for name in names:
+            r = sim_rows.ROWS[name]()
+            dv = configs.quantize(r.data.vertices)
+            qv = configs.quantize(r.query.vertices)
+            eng = sd.Engine(local, sd.SD_FP32)
             t0 = time.perf_counter()
-            md = eng.smooth_mesh_dist(bunny, P)
-            times.append(time.perf_counter() - t0)
-    ms = 1e3 * float(np.mean(times))
+            eng.set_geometry(dv, r.data.simplices, r.data.kinds)
+            eng.build_weights()
+            eng.build_bvh(sd.SD_BVH_LBVH)
+            setup = time.perf_counter() - t0
+            P = sd.SmoothParams(alpha=r.alpha, alpha_u=600.0, beta=0.5, alpha_q=r.alpha_q)
+            run = lambda: eng.smooth_mesh_dist_general(qv, r.query.simplices, r.query.kinds, P)
+            for _ in range(max(3, args.warmup)):
+                md = run()
+            launches = eng.last_launch_count()
+            times = []
+            for _ in range(args.steps):
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                md = run()
+                times.append(time.perf_counter() - t0)
+            ms = 1e3 * float(np.mean(times))
+            row = {"row": r.name, "types": r.types, "alpha": r.alpha, "alpha_q": r.alpha_q, "gpu_ms": ms,
+                   "gpu_ms_min": 1e3 * float(np.min(times)), "paper_ms": r.paper_ms, "speedup_vs_paper": r.paper_ms / ms,
+                   "d_hat": md.d_hat, "setup_s": setup, "gpu_launches": launches}
+            if not args.no_cpu:
+                import oracle as O
+                O.build()
+                threads = O.hardware_threads()
+                om = O.Mesh.from_arrays(dv, r.data.simplices, r.data.kinds)
+                # same table and tree as the GPU run
+                wt = eng.weight_table()
+                ow = O.Weights.from_table(O.WeightTable(wt.A, wt.sup_wtilde, wt.edge_a, wt.tri_stored, wt.poly_index))
+                ot = O.Tree.from_nodes(eng.export_bvh())
+                oq = O.Mesh.from_arrays(qv, r.query.simplices, r.query.kinds)
+                t0 = time.perf_counter()
+                ref = O.mesh_dist(om, ow, oq, O.Params(alpha=r.alpha, beta=0.5, alpha_q=r.alpha_q), tree=ot,
+                                  threads=threads)
+                row.update({"cpu_ms": 1e3 * (time.perf_counter() - t0), "cpu_threads": threads,
+                            "cpu_d_hat": ref.d_hat, "d_hat_abs_err": abs(ref.d_hat - md.d_hat),
+                            "leaves_per_query": ref.leaves / r.query.n, "far_per_query": ref.far_field / r.query.n})
+            eng.close()
+            rows.append(row)
+            print(json.dumps(row), file=sys.stderr, flush=True)
+    tot = sum(x["gpu_ms"] for x in rows)
+    paper = sum(x["paper_ms"] for x in rows)
     cpu = None
     if not args.no_cpu:
-        import oracle as O
-        O.build()
-        threads = O.hardware_threads()
-        om = O.Mesh.from_arrays(terrain, S, K)
-        ow = O.Weights.build(om)
-        ot = O.Tree.build(om)
-        oq = O.Mesh.from_arrays(bunny, np.stack([np.arange(len(bunny)), -np.ones(len(bunny)), -np.ones(len(bunny))], 1),
-                                np.zeros(len(bunny)))
-        t0 = time.perf_counter()
-        ref = O.mesh_dist(om, ow, oq, O.Params(alpha=100.0, beta=0.5, alpha_q=20.0), tree=ot, threads=threads)
-        cpu_ms = 1e3 * (time.perf_counter() - t0)
-        cpu = {"value": cpu_ms, "unit": "ms", "cores": threads, "kind": "port",
-               "sample": "one full evaluation (all 3,485 query points), fp64 oracle port, median-split tree",
-               "d_hat": ref.d_hat}
-    line = {"metric": "mesh-to-mesh d_hat(M, Mq) + vertex gradients, avg evaluation time", "value": ms, "unit": "ms",
-            "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
-            "scaling": "none", "vs_baseline": ms / 250.0031, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": "Terrain stand-in (6,591,087 points, alpha=100) vs Bunny stand-in (3,485 points, "
-                                   "alpha_q=20), beta=0.5, GPU LBVH; paper row PAPER.md:1378-1397 (250.0 ms, 28 CPU "
-                                   "threads, real lidar / bunny data)"},
-            "d_hat": md.d_hat, "cpu_baseline": cpu, "clocks": clk.summary()}
+        cpu = {"value": sum(x["cpu_ms"] for x in rows), "unit": "ms", "cores": rows[0]["cpu_threads"], "kind": "port",
+               "sample": "one evaluation of every row, fp64 oracle port on the host threads, same weights and tree"}
+    line = {"metric": "mesh-to-mesh d_hat(M, Mq) + vertex gradients, sum of avg evaluation times over the paper's "
+                      "timing table", "value": tot, "unit": "ms", "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": tot, "higher_is_better": False, "scaling": "none",
+            "vs_baseline": tot / paper, "dtype": "f32 points / f64 simplices", "data": "synthetic stand-ins",
+            "config": {"workload": f"{len(rows)} rows of PAPER.md:1378-1397 (sim_rows.py stand-ins), beta=0.5, "
+                                   "GPU LBVH, e2e through sd_mesh_dist", "paper_total_ms": paper},
+            "rows": rows, "cpu_baseline": cpu, "clocks": clk.summary()}
     print(json.dumps(line), flush=True)
 
 
@@ -597,7 +617,8 @@ def main():
                     help="exact workload: 2 = BASELINE configs[1] (headline), 1 = configs[0] fp64 points, "
                          "3 = configs[2] torus triangles, 5 = configs[4] primitive-sharded BVH")
     ap.add_argument("--fp64", action="store_true", help="fp64 arithmetic for --config 2")
-    ap.add_argument("--m2m", action="store_true", help="mesh-to-mesh Terrain-vs-Bunny evaluation (paper timing row)")
+    ap.add_argument("--m2m", action="store_true", help="mesh-to-mesh evaluations of the paper's timing table rows")
+    ap.add_argument("--rows", default="", help="comma-separated sim_rows names for --m2m (default: all)")
     ap.add_argument("--alpha", type=float, default=None, help="alpha for --config 3 (10, 100 or 1000)")
     args = ap.parse_args()
     rank, world, local = dist_env()

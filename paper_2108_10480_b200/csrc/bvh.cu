@@ -239,27 +239,46 @@ static void upload_tree_T(Ctx& c, DeviceTree& t) {
     up(t.leafmeta, leafmeta.data(), leafmeta.size() * sizeof(int32_t));
 }
 
-// Nodes at depth exactly k (pre-order) for the split traversal, cached per k.
+// Split slots at depth k (see pair_kernel): nodes at depth k and leaves
+// above it, in pre-order; per slot its ancestors (root first) and the bits
+// of those ancestors whose first slot (in pre-order) it is. Cached per k.
 void split_tables(Ctx& c, DeviceTree& t, int k) {
     if (t.split_k == k) return;
     const int64_t n = int64_t(c.tree.size());
-    std::vector<int32_t> slot_of(size_t(n), -1), dep(size_t(n), 0);
-    std::vector<int32_t> nodes;
+    std::vector<int32_t> parent(size_t(n), -1), dep(size_t(n), 0);
     for (int64_t id = 0; id < n; ++id) {  // pre-order: parents precede children
         const sd_bvh_node& nd = c.tree[id];
-        if (dep[id] == k) {
-            slot_of[id] = int32_t(nodes.size());
-            nodes.push_back(int32_t(id));
+        if (nd.left >= 0) {
+            dep[nd.left] = dep[nd.right] = dep[id] + 1;
+            parent[nd.left] = parent[nd.right] = int32_t(id);
         }
-        if (nd.left >= 0) dep[nd.left] = dep[nd.right] = dep[id] + 1;
     }
-    t.split_count = int64_t(std::max<size_t>(nodes.size(), 1));
+    std::vector<char> has_first(size_t(n), 0);
+    std::vector<int2> meta;
+    std::vector<int32_t> path;
+    std::vector<int32_t> anc;
+    for (int64_t id = 0; id < n; ++id) {
+        const bool leaf = c.tree[id].left < 0;
+        if (!(dep[id] == k || (leaf && dep[id] < k))) continue;
+        anc.clear();
+        for (int32_t p = parent[id]; p >= 0; p = parent[p]) anc.push_back(p);
+        std::reverse(anc.begin(), anc.end());  // root first
+        unsigned first = 0;
+        for (size_t j = 0; j < anc.size(); ++j)
+            if (!has_first[anc[j]]) {
+                has_first[anc[j]] = 1;
+                first |= 1u << j;
+            }
+        meta.push_back(make_int2(int(id), int(anc.size()) | int(first << 8)));
+        for (int j = 0; j < k; ++j) path.push_back(j < int(anc.size()) ? anc[j] : 0);
+    }
+    t.split_count = int64_t(meta.size());
     auto up = [](DevBuf& buf, const void* src, size_t bytes) {
         void* d = buf.ensure(bytes);
         if (bytes) check_cuda(cudaMemcpy(d, src, bytes, cudaMemcpyHostToDevice), "upload split tables");
     };
-    up(t.slot_of, slot_of.data(), slot_of.size() * sizeof(int32_t));
-    up(t.split_nodes, nodes.data(), nodes.size() * sizeof(int32_t));
+    up(t.split_meta, meta.data(), meta.size() * sizeof(int2));
+    up(t.split_path, path.data(), path.size() * sizeof(int32_t));
     t.split_k = k;
 }
 
@@ -563,6 +582,43 @@ __global__ void __launch_bounds__(kTravThreads) packet_kernel(const __grid_const
     if (nre) atomicAdd(a.rechecks, nre);
 }
 
+// Barnes-Hut admissibility of box b for query point q (bvh.hpp:105-111,
+// 185-187): fp32 decides outside a 1e-5 relative band, fp64 re-decides in
+// the reference rounding inside it. On "far" also returns d_B, 1/d_B and
+// q - y_B for the far-field term.
+template <class T>
+__device__ __forceinline__ bool point_far(const TraverseArgs<T>& a, const NodeT<T>& b, int32_t id, T qx, T qy, T qz,
+                                          T& d, T& r, T& dx, T& dy, T& dz, unsigned long long& nre) {
+    const T yx = fmin(fmax(qx, b.v[0]), b.v[4]);
+    const T yy = fmin(fmax(qy, b.v[1]), b.v[5]);
+    const T yz = fmin(fmax(qz, b.v[2]), b.v[6]);
+    dx = qx - yx;
+    dy = qy - yy;
+    dz = qz - yz;
+    const T s = fma(dx, dx, fma(dy, dy, dz * dz));
+    bool far;
+    if constexpr (sizeof(T) == 4) {
+        r = s > T(0) ? Math<T>::rsqrt(s) : T(0);
+        d = s * r;
+        const T rhs = a.ph.beta * d;
+        const T band = T(1e-5) * rhs;
+        if (s == T(0) && a.exact_boxes) far = false;
+        else if (b.v[3] < rhs - band) far = true;
+        else if (b.v[3] > rhs + band) far = false;
+        else {
+            far = decide64(b, a.diam64[id], double(qx), double(qy), double(qz), a.beta64);
+            ++nre;
+        }
+    } else {
+        far = decide64(b, a.diam64[id], double(qx), double(qy), double(qz), a.beta64);
+        if (far) {
+            d = sqrt(s);
+            r = T(1) / d;
+        }
+    }
+    return far;
+}
+
 // One node test of the packet traversal for one lane (decision + term),
 // shared by the single-node and child-pair kernels. Returns "descend".
 template <class T, bool HASH>
@@ -571,34 +627,10 @@ __device__ __forceinline__ bool visit(const TraverseArgs<T>& a, const Poly<T>* p
                                       int64_t& nfar, uint64_t& h, unsigned long long& nre) {
     int32_t link;
     memcpy(&link, &b.v[7], sizeof(int32_t));
-    bool far = false;
     if (a.use_bh) {
-        const T yx = fmin(fmax(qx, b.v[0]), b.v[4]);
-        const T yy = fmin(fmax(qy, b.v[1]), b.v[5]);
-        const T yz = fmin(fmax(qz, b.v[2]), b.v[6]);
-        const T dx = qx - yx, dy = qy - yy, dz = qz - yz;
-        const T s = fma(dx, dx, fma(dy, dy, dz * dz));
-        if constexpr (sizeof(T) == 4) {
-            const T r = s > T(0) ? Math<T>::rsqrt(s) : T(0);
-            const T d = s * r;
-            const T rhs = a.ph.beta * d;
-            const T band = T(1e-5) * rhs;
-            if (s == T(0) && a.exact_boxes) far = false;
-            else if (b.v[3] < rhs - band) far = true;
-            else if (b.v[3] > rhs + band) far = false;
-            else {
-                far = decide64(b, a.diam64[id], double(qx), double(qy), double(qz), a.beta64);
-                ++nre;
-            }
-            if (far) far_term(a.ph, lgc + a.lw_ff, d, r, dx, dy, dz, acc);
-        } else {
-            far = decide64(b, a.diam64[id], double(qx), double(qy), double(qz), a.beta64);
-            if (far) {
-                const T d = sqrt(s);
-                far_term(a.ph, lgc + a.lw_ff, d, T(1) / d, dx, dy, dz, acc);
-            }
-        }
-        if (far) {
+        T d, r, dx, dy, dz;
+        if (point_far(a, b, id, qx, qy, qz, d, r, dx, dy, dz, nre)) {
+            far_term(a.ph, lgc + a.lw_ff, d, r, dx, dy, dz, acc);
             ++nfar;
             if constexpr (HASH) h += decision_mix(uint64_t(id), 1);
             return false;
@@ -646,6 +678,19 @@ struct PointVisit {
                                           int32_t id, T lgc, Acc<T>& acc, int64_t& nleaf, int64_t& nfar, uint64_t& h,
                                           unsigned long long& nre) const {
         return sdgpu::visit<T, HASH>(a, polys, b, id, lgc, qx, qy, qz, acc, nleaf, nfar, h, nre);
+    }
+    template <bool HASH>
+    __device__ __forceinline__ bool far_test(const TraverseArgs<T>& a, const NodeT<T>& b, int32_t id, T lgc, bool emit,
+                                             Acc<T>& acc, int64_t& nfar, uint64_t& h, unsigned long long& nre) const {
+        if (!a.use_bh) return false;
+        T d, r, dx, dy, dz;
+        if (!point_far(a, b, id, qx, qy, qz, d, r, dx, dy, dz, nre)) return false;
+        if (emit) {
+            far_term(a.ph, lgc + a.lw_ff, d, r, dx, dy, dz, acc);
+            ++nfar;
+            if constexpr (HASH) h += decision_mix(uint64_t(id), 1);
+        }
+        return true;
     }
 };
 
@@ -738,7 +783,9 @@ void tree_query(Ctx& c, const T* q, int64_t Q, const sd_params& p, const Finaliz
     }();
     int nsplits = 1;
     if (variant == 2) {
-        nsplits = launch_pair_traversal<T, PointVisit<T>>(c, c.dtree, a, out.hash != nullptr, st, launches);
+        if (!(use_frontier(Q, 16384) &&
+              launch_frontier<T, PointVisit<T>>(c, c.dtree, a, out.hash != nullptr, st, launches)))
+            nsplits = launch_pair_traversal<T, PointVisit<T>>(c, c.dtree, a, out.hash != nullptr, st, launches);
     } else {
         const size_t smem = poly_bytes<T>(npoly) +
                             (variant == 0 ? size_t(a.stack_depth) * kTravThreads * sizeof(int32_t)

@@ -73,8 +73,8 @@ struct DeviceTree {
     bool exact_boxes = true;
     DevBuf box, pairs, count, lgcount, diam64, leafrec, leafmeta;
     int split_k = -1;         // depth of the cached split tables
-    int64_t split_count = 0;  // nodes at that depth
-    DevBuf slot_of, split_nodes;
+    int64_t split_count = 0;  // slots at that depth
+    DevBuf split_meta, split_path;  // see split_tables (bvh.cu)
 };
 
 struct Ctx {
@@ -118,7 +118,7 @@ struct Ctx {
 
     // scratch
     DevBuf qd, qT, part, out_d, out_g, out_c, out_gc, out_l, out_f, out_h;
-    DevBuf perm, keys, tmp, tmp2, counters, polys;
+    DevBuf perm, keys, tmp, tmp2, counters, polys, flag;
     int64_t last_launches = 0;
 };
 

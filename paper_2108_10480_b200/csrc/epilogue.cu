@@ -14,23 +14,11 @@
 
 namespace sdgpu {
 
-__global__ void finalize_kernel(const double* __restrict__ part, int splits, int64_t Q, double alpha, double eps,
-                                int64_t const_leaves, const int64_t* __restrict__ leaves_in,
-                                const int64_t* __restrict__ far_in, const uint64_t* __restrict__ hash_in,
-                                const int64_t* __restrict__ perm, FinalizeOut o) {
-    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i >= Q) return;
-    double M = -INFINITY;
-    for (int k = 0; k < splits; ++k) M = fmax(M, double(part[size_t(k) * 5 * Q + i]));
-    double s = 0, gx = 0, gy = 0, gz = 0;
-    for (int k = 0; k < splits && M > -INFINITY; ++k) {
-        const double* p = part + size_t(k) * 5 * Q;
-        const double f = exp2(double(p[i]) - M);
-        s = fma(double(p[Q + i]), f, s);
-        gx = fma(double(p[2 * Q + i]), f, gx);
-        gy = fma(double(p[3 * Q + i]), f, gy);
-        gz = fma(double(p[4 * Q + i]), f, gz);
-    }
+__device__ __forceinline__ void finalize_write(double M, double s, double gx, double gy, double gz, int64_t i,
+                                               double alpha, double eps, int64_t const_leaves,
+                                               const int64_t* __restrict__ leaves_in, const int64_t* __restrict__ far_in,
+                                               const uint64_t* __restrict__ hash_in, const int64_t* __restrict__ perm,
+                                               const FinalizeOut& o) {
     const double scale = M > -INFINITY ? exp2(M) : 0.0;
     const double c = s * scale;
     const double cx = gx * scale, cy = gy * scale, cz = gz * scale;
@@ -60,11 +48,68 @@ __global__ void finalize_kernel(const double* __restrict__ part, int splits, int
     if (o.hash) o.hash[j] = hash_in ? hash_in[i] : 0;
 }
 
+__global__ void finalize_kernel(const double* __restrict__ part, int splits, int64_t Q, double alpha, double eps,
+                                int64_t const_leaves, const int64_t* __restrict__ leaves_in,
+                                const int64_t* __restrict__ far_in, const uint64_t* __restrict__ hash_in,
+                                const int64_t* __restrict__ perm, FinalizeOut o) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= Q) return;
+    double M = -INFINITY;
+    for (int k = 0; k < splits; ++k) M = fmax(M, double(part[size_t(k) * 5 * Q + i]));
+    double s = 0, gx = 0, gy = 0, gz = 0;
+    for (int k = 0; k < splits && M > -INFINITY; ++k) {
+        const double* p = part + size_t(k) * 5 * Q;
+        const double f = exp2(double(p[i]) - M);
+        s = fma(double(p[Q + i]), f, s);
+        gx = fma(double(p[2 * Q + i]), f, gx);
+        gy = fma(double(p[3 * Q + i]), f, gy);
+        gz = fma(double(p[4 * Q + i]), f, gz);
+    }
+    finalize_write(M, s, gx, gy, gz, i, alpha, eps, const_leaves, leaves_in, far_in, hash_in, perm, o);
+}
+
+// Many splits (the few-query split traversal): one warp per query, lanes
+// over the splits, shuffle merge.
+__global__ void finalize_warp_kernel(const double* __restrict__ part, int splits, int64_t Q, double alpha, double eps,
+                                     int64_t const_leaves, const int64_t* __restrict__ leaves_in,
+                                     const int64_t* __restrict__ far_in, const uint64_t* __restrict__ hash_in,
+                                     const int64_t* __restrict__ perm, FinalizeOut o) {
+    const int64_t i = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (i >= Q) return;
+    double M = -INFINITY;
+    for (int k = lane; k < splits; k += 32) M = fmax(M, part[size_t(k) * 5 * Q + i]);
+    for (int off = 16; off; off >>= 1) M = fmax(M, __shfl_xor_sync(0xffffffffu, M, off));
+    double s = 0, gx = 0, gy = 0, gz = 0;
+    if (M > -INFINITY) {
+        for (int k = lane; k < splits; k += 32) {
+            const double* p = part + size_t(k) * 5 * Q;
+            const double f = exp2(p[i] - M);
+            s = fma(p[Q + i], f, s);
+            gx = fma(p[2 * Q + i], f, gx);
+            gy = fma(p[3 * Q + i], f, gy);
+            gz = fma(p[4 * Q + i], f, gz);
+        }
+        for (int off = 16; off; off >>= 1) {
+            s += __shfl_xor_sync(0xffffffffu, s, off);
+            gx += __shfl_xor_sync(0xffffffffu, gx, off);
+            gy += __shfl_xor_sync(0xffffffffu, gy, off);
+            gz += __shfl_xor_sync(0xffffffffu, gz, off);
+        }
+    }
+    if (lane == 0) finalize_write(M, s, gx, gy, gz, i, alpha, eps, const_leaves, leaves_in, far_in, hash_in, perm, o);
+}
+
 cudaError_t launch_finalize(const double* part, int splits, int64_t Q, double alpha, double epsilon,
                             int64_t const_leaves, const int64_t* leaves_in, const int64_t* far_in,
                             const uint64_t* hash_in, const int64_t* perm, const FinalizeOut& out, cudaStream_t st) {
     if (Q <= 0) return cudaSuccess;
     const int threads = 256;
+    if (splits >= 32) {
+        finalize_warp_kernel<<<unsigned((Q * 32 + threads - 1) / threads), threads, 0, st>>>(
+            part, splits, Q, alpha, epsilon, const_leaves, leaves_in, far_in, hash_in, perm, out);
+        return cudaGetLastError();
+    }
     const unsigned blocks = unsigned((Q + threads - 1) / threads);
     finalize_kernel<<<blocks, threads, 0, st>>>(part, splits, Q, alpha, epsilon, const_leaves, leaves_in, far_in,
                                                    hash_in, perm, out);

@@ -513,23 +513,30 @@ struct SimplexVisit {
     __device__ __forceinline__ void load(const TraverseArgs<double>& a, int64_t qi, bool valid) {
         g = sx::load_query(a.qgeom, a.qdim, qi, valid);
     }
+    // collect_contributions (smooth.hpp:114-121), bh_condition (bvh.hpp:185-187)
+    template <bool HASH>
+    __device__ __forceinline__ bool far_test(const TraverseArgs<double>& a, const NodeT<double>& b, int32_t id,
+                                             double lgc, bool emit, Acc<double>& acc, int64_t& nfar, uint64_t& h,
+                                             unsigned long long&) const {
+        if (!a.use_bh) return false;
+        const sx::BoxProx pr =
+            sx::box_primitive_proximity(sx::mk(b.v[0], b.v[1], b.v[2]), sx::mk(b.v[4], b.v[5], b.v[6]), g);
+        if (!(!pr.must_descend && pr.distance > 0.0 && a.diam64[id] < a.beta64 * pr.distance)) return false;
+        if (emit) {
+            const sx::D3 diff = g.at(pr.lam) - pr.yb;
+            far_term(a.ph, lgc + a.lw_ff, pr.distance, 1.0 / pr.distance, diff.x, diff.y, diff.z, acc);
+            ++nfar;
+            if constexpr (HASH) h += decision_mix(uint64_t(id), 1);
+        }
+        return true;
+    }
     template <bool HASH>
     __device__ __forceinline__ bool visit(const TraverseArgs<double>& a, const Poly<double>* polys,
                                           const NodeT<double>& b, int32_t id, double lgc, Acc<double>& acc,
-                                          int64_t& nleaf, int64_t& nfar, uint64_t& h, unsigned long long&) const {
+                                          int64_t& nleaf, int64_t& nfar, uint64_t& h, unsigned long long& nre) const {
         int32_t link;
         memcpy(&link, &b.v[7], sizeof(int32_t));
-        if (a.use_bh) {  // collect_contributions (smooth.hpp:114-121), bh_condition (bvh.hpp:185-187)
-            const sx::BoxProx pr =
-                sx::box_primitive_proximity(sx::mk(b.v[0], b.v[1], b.v[2]), sx::mk(b.v[4], b.v[5], b.v[6]), g);
-            if (!pr.must_descend && pr.distance > 0.0 && a.diam64[id] < a.beta64 * pr.distance) {
-                const sx::D3 diff = g.at(pr.lam) - pr.yb;
-                far_term(a.ph, lgc + a.lw_ff, pr.distance, 1.0 / pr.distance, diff.x, diff.y, diff.z, acc);
-                ++nfar;
-                if constexpr (HASH) h += decision_mix(uint64_t(id), 1);
-                return false;
-            }
-        }
+        if (far_test<HASH>(a, b, id, lgc, true, acc, nfar, h, nre)) return false;
         if (link >= 0) return true;
         const int slot = -link - 1;
         sx::leaf_term(a.ph, polys, a.ne, a.leafmeta[slot], a.leafgeom + size_t(slot) * 16, g, acc);
@@ -757,7 +764,10 @@ void simplex_query(Ctx& c, const double* corners, const int32_t* dims, int64_t Q
     a.qgeom = corners;
     a.qdim = dims;
     a.leafgeom = c.leafgeom.as<double>();
-    const int nsplits = launch_pair_traversal<double, SimplexVisit>(c, t, a, out.hash != nullptr, st, launches);
+    // node tests cost a QP: few-query batches go node-parallel
+    int nsplits = 1;
+    if (!(use_frontier(Q, 16384) && launch_frontier<double, SimplexVisit>(c, t, a, out.hash != nullptr, st, launches)))
+        nsplits = launch_pair_traversal<double, SimplexVisit>(c, t, a, out.hash != nullptr, st, launches, 4);
     check_cuda(launch_finalize(a.part, nsplits, Q, p.alpha, p.epsilon, 0, a.leaves, a.far, a.hash, perm, out, st),
                "finalize");
     ++launches;

@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <stdexcept>
 
 #include "context.h"
 
@@ -51,9 +52,8 @@ struct TraverseArgs {
     // split mode (few queries): see pair_kernel
     int split_depth, nslots;
     int64_t npackets;
-    const int32_t* slot_of;     // node -> depth-k slot, or -1
-    const int32_t* split_nodes;  // slot -> node
-    unsigned* items;            // [packet][slot] lane mask reaching the slot
+    const int2* split_meta;     // slot -> (node, path length | first-slot bits << 8)
+    const int32_t* split_path;  // [slot][split_depth] ancestors, root first
     // simplex queries (simplex.cu): fp64 corners and dims per query, and
     // the fp64 leaf geometry (16 doubles per leaf slot)
     const double* qgeom;
@@ -93,16 +93,21 @@ __device__ __forceinline__ void far_term(const Phys<T>& ph, T lw, T d, T r, T dx
 // the right child, else pops. Stack entries (node, its link, mask, depth)
 // live in shared memory, one stack per warp.
 //
-// SPLIT = 1 / 2 (few queries): the same walk cut at tree depth k. The top
-// pass (1) stops above depth k and records, per query packet and depth-k
-// node, the mask of lanes that reach it; the subtree pass (2) runs one warp
-// per (packet, depth-k node) from that node with that mask. Each lane still
-// visits exactly its reference node set; the partial sums land in split
-// slots merged by K4, so a batch of a few thousand queries fills the GPU.
+// SPLIT = 1 (few queries): one warp per (query packet, slot), the slots
+// being the nodes at tree depth k plus the leaves above that depth, so that
+// every root-to-leaf path crosses exactly one slot. The warp first re-tests
+// the slot's ancestors (root first) for its lanes: a lane for which an
+// ancestor is admissible does not reach the slot, and that ancestor's
+// far-field term is emitted only by the warp of the first slot below it.
+// The lanes that reach the slot then walk its subtree as above. Per lane the
+// decisions and terms are exactly the unsplit walk's; the partial sums land
+// in one fp64 state per slot, merged by K4, so a batch of a few hundred
+// queries still spreads over thousands of warps.
 //
 // VIS is the per-lane query: load(a, qi, valid) reads it, visit<HASH>(...)
 // tests one node for it (point queries: bvh.cu; simplex queries:
-// simplex.cu) and returns "descend".
+// simplex.cu) and returns "descend"; far_test<HASH>(...) is the
+// admissibility test alone (emitting the far-field term only when asked).
 template <class T, class VIS, bool HASH, int SPLIT>
 __global__ void __launch_bounds__(kTravThreads) pair_kernel(const __grid_constant__ TraverseArgs<T> a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -114,17 +119,17 @@ __global__ void __launch_bounds__(kTravThreads) pair_kernel(const __grid_constan
 
     const unsigned lane = threadIdx.x & 31u;
     int4* st = stacks + (threadIdx.x >> 5) * a.stack_depth;
-    // packet (32 sorted queries) and, in the subtree pass, the depth-k slot
+    // packet (32 sorted queries) and, when split, the slot
     const int64_t gwarp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    const int64_t packet = SPLIT == 2 ? gwarp / a.nslots : gwarp;
-    const int slot = SPLIT == 2 ? int(gwarp % a.nslots) : 0;
-    if (SPLIT == 2 && packet >= a.npackets) return;
+    const int64_t packet = SPLIT ? gwarp / a.nslots : gwarp;
+    const int slot = SPLIT ? int(gwarp % a.nslots) : 0;
+    if (SPLIT && packet >= a.npackets) return;
     const int64_t i = packet * 32 + lane;
     const bool valid = i < a.Q;
     const int64_t qi = valid ? (a.perm ? a.perm[i] : i) : 0;
     VIS qv;
     qv.load(a, qi, valid);
-    double* part = a.part + (SPLIT == 2 ? size_t(1 + slot) * 5 * a.Q : 0);
+    double* part = a.part + (SPLIT ? size_t(slot) * 5 * a.Q : 0);
     unsigned mask = __ballot_sync(0xffffffffu, valid);
     if (mask == 0u) return;
     Acc<T> acc;
@@ -132,18 +137,27 @@ __global__ void __launch_bounds__(kTravThreads) pair_kernel(const __grid_constan
     int64_t nleaf = 0, nfar = 0;
     uint64_t h = 0;
     unsigned long long nre = 0;
-    int32_t cur, cur_link;
-    int depth;
-    if constexpr (SPLIT == 2) {
-        mask &= a.items[packet * a.nslots + slot];
-        cur = a.split_nodes[slot];
-        depth = a.split_depth;
-    } else {
-        cur = 0;
-        depth = 0;
+    int32_t cur = 0, cur_link;
+    int depth = 0;
+    if constexpr (SPLIT) {
+        const int2 sm = a.split_meta[slot];  // (node, path length | first-slot bits << 8)
+        cur = sm.x;
+        const int len = sm.y & 0xff;
+        const unsigned first = unsigned(sm.y) >> 8;
+        const int32_t* path = a.split_path + size_t(slot) * a.split_depth;
+        for (int j = 0; j < len && mask; ++j) {
+            const int32_t anc = path[j];
+            const NodeT<T> b = a.box[anc];
+            bool far = false;
+            if ((mask >> lane) & 1u)
+                far = qv.template far_test<HASH>(a, b, anc, a.lgcount[anc], ((first >> j) & 1u) != 0u, acc, nfar, h,
+                                                 nre);
+            mask &= ~__ballot_sync(0xffffffffu, far);
+        }
+        depth = len;
     }
     memcpy(&cur_link, &a.box[cur].v[7], sizeof(int32_t));
-    if (mask) {  // the start node (root, or the depth-k node) is popped alone
+    if (mask) {  // the start node (root, or the slot) is popped alone
         const NodeT<T> b0 = a.box[cur];
         const bool d = ((mask >> lane) & 1u) &&
                        qv.template visit<HASH>(a, polys, b0, cur, a.lgcount[cur], acc, nleaf, nfar, h, nre);
@@ -152,25 +166,6 @@ __global__ void __launch_bounds__(kTravThreads) pair_kernel(const __grid_constan
     int sp = 0;
     while (mask) {
         const int32_t lid = cur + 1, rid = cur_link;
-        if (SPLIT == 1 && depth + 1 == a.split_depth) {  // children start subtrees: hand over
-            if (lane == 0) {
-                unsigned* it = a.items + packet * a.nslots;
-                it[a.slot_of[lid]] = mask;
-                it[a.slot_of[rid]] = mask;
-            }
-            __syncwarp();
-            if (sp > 0) {
-                --sp;
-                const int4 e = st[sp];
-                cur = e.x;
-                cur_link = e.y;
-                mask = unsigned(e.z);
-                depth = e.w;
-            } else {
-                mask = 0u;
-            }
-            continue;
-        }
         const PairT<T>& pr = a.pairs[cur];  // warp-uniform: broadcast loads
         const NodeT<T> bl = pr.l, br = pr.r;
         const T lgl = pr.lgc[0], lgr = pr.lgc[1];
@@ -221,7 +216,7 @@ __global__ void __launch_bounds__(kTravThreads) pair_kernel(const __grid_constan
     part[2 * a.Q + i] = tot.gx;
     part[3 * a.Q + i] = tot.gy;
     part[4 * a.Q + i] = tot.gz;
-    if constexpr (SPLIT == 2) {  // the top pass stored its counts first
+    if constexpr (SPLIT != 0) {  // counters were zeroed; the slots add
         if (nleaf) atomicAdd(reinterpret_cast<unsigned long long*>(a.leaves + i), (unsigned long long)nleaf);
         if (nfar) atomicAdd(reinterpret_cast<unsigned long long*>(a.far + i), (unsigned long long)nfar);
         if (HASH && h) atomicAdd(reinterpret_cast<unsigned long long*>(a.hash + i), (unsigned long long)h);
@@ -233,28 +228,148 @@ __global__ void __launch_bounds__(kTravThreads) pair_kernel(const __grid_constan
     if (nre) atomicAdd(a.rechecks, nre);
 }
 
-// Launches K3 (SPLIT 0, or the split pair 1 + 2) for VIS over the tree t
-// and returns the number of fp64 partial slots written to a.part (merged by
-// K4). a.part must hold 5 Q doubles; it is re-pointed when splitting.
+// K3F (few queries, node-parallel): one warp per query; the lanes test up
+// to 32 nodes of that query's walk at once. The warp pops the top 32 (or
+// fewer) entries of its shared-memory stack, every lane tests its node
+// exactly like the serial walk would (far field / exact leaf / descend),
+// and the children of descending nodes are pushed (ballot + prefix count).
+// A node is tested iff all its ancestors descended -- the reference's
+// visited set -- only the order of the terms differs. Each lane keeps its
+// own accumulator; the 32 states are merged in fp64 at the end.
+// Stack bound: the entries stay sorted by depth (children of the popped top
+// entries are deeper than everything left below them), and entries of depth
+// d are only created while the depth-(d-1) entries on top are popped -- in
+// the same batch as every depth-d entry above them -- so each level holds at
+// most 2 x 32 entries and 64 (depth + 1) always suffice. The guard below
+// can therefore not fire; it records a flag instead of writing past the
+// stack.
+template <class T, class VIS, bool HASH>
+__global__ void __launch_bounds__(kTravThreads) frontier_kernel(const __grid_constant__ TraverseArgs<T> a, int cap,
+                                                                int* overflow) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    Poly<T>* polys = reinterpret_cast<Poly<T>*>(smem_raw);
+    int32_t* stacks = reinterpret_cast<int32_t*>(smem_raw + poly_bytes<T>(a.npoly));
+    for (int i = threadIdx.x; i < a.npoly * kPolyCoefs; i += blockDim.x)
+        reinterpret_cast<T*>(polys)[i] = reinterpret_cast<const T*>(a.polys)[i];
+    __syncthreads();
+    const unsigned lane = threadIdx.x & 31u;
+    const int64_t i = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;  // sorted query position
+    if (i >= a.Q) return;
+    int32_t* stk = stacks + size_t(threadIdx.x >> 5) * cap;
+    const int64_t qi = a.perm ? a.perm[i] : i;
+    VIS qv;
+    qv.load(a, qi, true);
+    Acc<T> acc;
+    acc.init();
+    int64_t nleaf = 0, nfar = 0;
+    uint64_t h = 0;
+    unsigned long long nre = 0;
+    if (lane == 0) stk[0] = 0;
+    __syncwarp();
+    int n = 1;
+    while (n > 0) {
+        const int take = n < 32 ? n : 32;
+        const int base = n - take;
+        const int32_t id = int(lane) < take ? stk[base + lane] : -1;
+        __syncwarp();
+        bool d = false;
+        if (id >= 0) {
+            const NodeT<T> b = a.box[id];
+            d = qv.template visit<HASH>(a, polys, b, id, a.lgcount[id], acc, nleaf, nfar, h, nre);
+        }
+        const unsigned D = __ballot_sync(0xffffffffu, d);
+        const int pushed = 2 * __popc(D);
+        if (base + pushed > cap) {  // unreachable (see above)
+            if (lane == 0) atomicExch(overflow, 1);
+            break;
+        }
+        if (d) {
+            const int pos = base + 2 * __popc(D & ((1u << lane) - 1u));
+            int32_t link;
+            memcpy(&link, &a.box[id].v[7], sizeof(int32_t));
+            stk[pos] = link;    // right child below ...
+            stk[pos + 1] = id + 1;  // ... left child on top
+        }
+        __syncwarp();
+        n = base + pushed;
+    }
+    // merge the lanes' states (fp64, anchored at the warp maximum)
+    Tot tot;
+    tot.init();
+    tot.flush(acc);
+    double M = tot.M;
+    for (int off = 16; off; off >>= 1) M = fmax(M, __shfl_xor_sync(0xffffffffu, M, off));
+    const double f = (M == -INFINITY || tot.M == -INFINITY) ? 0.0 : exp2(tot.M - M);
+    double s = tot.s * f, gx = tot.gx * f, gy = tot.gy * f, gz = tot.gz * f;
+    unsigned long long L = (unsigned long long)nleaf, F = (unsigned long long)nfar, H = h;
+    for (int off = 16; off; off >>= 1) {
+        s += __shfl_xor_sync(0xffffffffu, s, off);
+        gx += __shfl_xor_sync(0xffffffffu, gx, off);
+        gy += __shfl_xor_sync(0xffffffffu, gy, off);
+        gz += __shfl_xor_sync(0xffffffffu, gz, off);
+        L += __shfl_xor_sync(0xffffffffu, L, off);
+        F += __shfl_xor_sync(0xffffffffu, F, off);
+        H += __shfl_xor_sync(0xffffffffu, H, off);
+    }
+    if (lane == 0) {
+        a.part[i] = M;
+        a.part[a.Q + i] = s;
+        a.part[2 * a.Q + i] = gx;
+        a.part[3 * a.Q + i] = gy;
+        a.part[4 * a.Q + i] = gz;
+        a.leaves[i] = int64_t(L);
+        a.far[i] = int64_t(F);
+        if (HASH) a.hash[i] = H;
+    }
+    if (nre) atomicAdd(a.rechecks, nre);
+}
+
+// K3F launcher: returns false (nothing launched) when the stacks would not
+// fit in shared memory.
 template <class T, class VIS>
-int launch_pair_traversal(Ctx& c, DeviceTree& t, TraverseArgs<T>& a, bool hash, cudaStream_t st, int64_t& launches) {
+bool launch_frontier(Ctx& c, DeviceTree& t, TraverseArgs<T>& a, bool hash, cudaStream_t st, int64_t& launches) {
+    const int cap = 64 * (t.depth + 1);
+    const size_t smem = poly_bytes<T>(a.npoly) + size_t(cap) * (kTravThreads / 32) * sizeof(int32_t);
+    if (smem > 200 * 1024) return false;
+    int* flag = static_cast<int*>(c.flag.ensure(sizeof(int)));
+    auto kern = hash ? frontier_kernel<T, VIS, true> : frontier_kernel<T, VIS, false>;
+    check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)), "smem attr");
+    kern<<<unsigned((a.Q * 32 + kTravThreads - 1) / kTravThreads), kTravThreads, smem, st>>>(a, cap, flag);
+    check_cuda(cudaGetLastError(), "frontier kernel");
+    ++launches;
+    return true;
+}
+
+// Few-query mode choice: SDGPU_FRONTIER = 1 / 0 forces it on / off;
+// default: node-parallel when the batch has at most `limit` queries.
+inline bool use_frontier(int64_t Q, int64_t limit) {
+    const char* e = std::getenv("SDGPU_FRONTIER");
+    if (e && *e) return std::atoi(e) != 0;
+    return Q <= limit;
+}
+
+// Launches K3 (unsplit, or split at depth k for few queries) for VIS over
+// the tree t and returns the number of fp64 partial slots written to a.part
+// (merged by K4). a.part must hold 5 Q doubles; it is re-pointed when
+// splitting. `weight` raises the warp target for expensive node tests.
+template <class T, class VIS>
+int launch_pair_traversal(Ctx& c, DeviceTree& t, TraverseArgs<T>& a, bool hash, cudaStream_t st, int64_t& launches,
+                          int weight = 1) {
     const int64_t Q = a.Q;
     const size_t smem = poly_bytes<T>(a.npoly) + size_t(a.stack_depth) * (kTravThreads / 32) * sizeof(int4);
-    // few queries: split the walk at depth k so that packets x 2^k warps fill
-    // the GPU (>= ~32 warps per SM)
     const int64_t npackets = (Q + 31) / 32;
     // SDGPU_SPLIT = 0 disables, = k forces depth k (A/B runs and tests)
     const char* se = std::getenv("SDGPU_SPLIT");
     const int forced = se && *se ? std::atoi(se) : -1;
     int k = 0;
     if (t.depth >= 2) {
-        const int kmax = std::min(12, t.depth - 1);
+        const int kmax = std::min(14, t.depth);
         if (forced >= 0) {
             k = std::min(forced, kmax);
-        } else if (t.depth >= 3) {
-            while (k < std::min(10, kmax) && npackets * (int64_t(1) << k) < 148 * 32) ++k;
+        } else {  // >= ~32 (x weight) warps per SM
+            while (k < kmax && npackets * (int64_t(1) << k) < int64_t(148) * 32 * weight) ++k;
         }
-        while (k > 0 && size_t(1 + (size_t(1) << k)) * 5 * size_t(Q) * sizeof(double) > (size_t(1) << 31)) --k;
+        while (k > 0 && (size_t(1) << k) * 5 * size_t(Q) * sizeof(double) > (size_t(1) << 31)) --k;
     }
     a.split_depth = k;
     a.npackets = npackets;
@@ -263,31 +378,21 @@ int launch_pair_traversal(Ctx& c, DeviceTree& t, TraverseArgs<T>& a, bool hash, 
     if (k > 0) {
         split_tables(c, t, k);
         a.nslots = int(t.split_count);
-        a.slot_of = t.slot_of.as<int32_t>();
-        a.split_nodes = t.split_nodes.as<int32_t>();
-        a.items = static_cast<unsigned*>(c.tmp2.ensure(size_t(npackets) * a.nslots * sizeof(unsigned)));
-        check_cuda(cudaMemsetAsync(a.items, 0, size_t(npackets) * a.nslots * sizeof(unsigned), st), "memset");
-        nsplits = 1 + a.nslots;
+        a.split_meta = t.split_meta.as<int2>();
+        a.split_path = t.split_path.as<int32_t>();
+        check_cuda(cudaMemsetAsync(a.leaves, 0, size_t(Q) * sizeof(int64_t), st), "memset");
+        check_cuda(cudaMemsetAsync(a.far, 0, size_t(Q) * sizeof(int64_t), st), "memset");
+        if (hash) check_cuda(cudaMemsetAsync(a.hash, 0, size_t(Q) * sizeof(uint64_t), st), "memset");
+        nsplits = a.nslots;
         a.part = static_cast<double*>(c.part.ensure(size_t(nsplits) * 5 * Q * sizeof(double)));
     }
-    // the decision hash costs ~20 integer ops per decision: only when asked for
-    auto pick = [&](auto split) {
-        constexpr int S = decltype(split)::value;
-        return hash ? pair_kernel<T, VIS, true, S> : pair_kernel<T, VIS, false, S>;
-    };
-    auto kern = k > 0 ? pick(std::integral_constant<int, 1>()) : pick(std::integral_constant<int, 0>());
+    auto kern = k > 0 ? (hash ? pair_kernel<T, VIS, true, 1> : pair_kernel<T, VIS, false, 1>)
+                      : (hash ? pair_kernel<T, VIS, true, 0> : pair_kernel<T, VIS, false, 0>);
     check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)), "smem attr");
-    kern<<<unsigned((Q + kTravThreads - 1) / kTravThreads), kTravThreads, smem, st>>>(a);
+    const int64_t warps = npackets * a.nslots;
+    kern<<<unsigned((warps * 32 + kTravThreads - 1) / kTravThreads), kTravThreads, smem, st>>>(a);
     check_cuda(cudaGetLastError(), "traverse kernel");
     ++launches;
-    if (k > 0) {
-        auto sub = pick(std::integral_constant<int, 2>());
-        check_cuda(cudaFuncSetAttribute(sub, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)), "smem attr");
-        const int64_t warps = npackets * a.nslots;
-        sub<<<unsigned((warps * 32 + kTravThreads - 1) / kTravThreads), kTravThreads, smem, st>>>(a);
-        check_cuda(cudaGetLastError(), "subtree kernel");
-        ++launches;
-    }
     return nsplits;
 }
 

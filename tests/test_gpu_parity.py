@@ -139,14 +139,19 @@ def test_random_scene_tree_decisions(sd, oracle, prec, seed):
 
 
 @pytest.mark.parametrize("prec", [0, 1])
-@pytest.mark.parametrize("split", ["0", "1", "3", "6", ""])
+@pytest.mark.parametrize("split", ["0", "1", "3", "6", "", "frontier"])
 def test_split_traversal_decisions(sd, oracle, prec, split, monkeypatch):
-    """The few-query split traversal (top pass above depth k, one warp per
-    (packet, depth-k subtree), merged in fp64) visits exactly the oracle's
-    nodes: counters and decision hash identical for every depth k, including
-    none ("0") and the automatic choice ("")."""
+    """The few-query traversal modes visit exactly the oracle's nodes:
+    the slot split (one warp per (packet, depth-k slot) after re-testing the
+    slot's ancestors, merged in fp64) at every depth k, none ("0"), the
+    automatic choice (""), and the node-parallel frontier kernel: counters
+    and decision hash identical."""
     O = oracle
-    monkeypatch.setenv("SDGPU_SPLIT", split)
+    if split == "frontier":
+        monkeypatch.setenv("SDGPU_FRONTIER", "1")
+    else:
+        monkeypatch.setenv("SDGPU_FRONTIER", "0")
+        monkeypatch.setenv("SDGPU_SPLIT", split)
     m0 = O.random_scene(7, 400)
     qs = O.QueryStream(4242).draw_points(m0, 777)  # ragged last packet
     m, q = prep(O, m0, qs, prec)

@@ -106,9 +106,13 @@ def test_simplex_lbvh_decisions(sd, oracle):
     _close(got, ref, "lbvh")
 
 
-@pytest.mark.parametrize("split", ["0", "3", ""])
+@pytest.mark.parametrize("split", ["0", "3", "", "frontier"])
 def test_simplex_split_traversal(sd, oracle, split, monkeypatch):
-    monkeypatch.setenv("SDGPU_SPLIT", split)
+    if split == "frontier":
+        monkeypatch.setenv("SDGPU_FRONTIER", "1")
+    else:
+        monkeypatch.setenv("SDGPU_FRONTIER", "0")
+        monkeypatch.setenv("SDGPU_SPLIT", split)
     O = oracle
     m, c, d = _scene(O, 3, 300, 100, 1, 333)
     w, t = O.Weights.build(m), O.Tree.build(m)
