@@ -43,6 +43,21 @@ int main() {
         // conservativeness (acceptance [1]): tree field below the exact one
         for (size_t i = 0; i < q.size(); ++i)
             if (!(tree[i].d_hat <= exact[i].d_hat + 1e-9)) return 2;
+
+        // query edges / triangles and a mesh-to-mesh distance
+        const std::vector<SimplexGeom> g = {SimplexGeom::edge({0.5, 0.5, 2.0}, {0.5, 0.5, 3.0}),
+                                            SimplexGeom::triangle({4, 0, 0}, {4, 1, 0}, {4, 0, 1})};
+        const auto gs = eng.smooth_min_dist(g, p);
+        for (size_t i = 0; i < g.size(); ++i)
+            std::printf("g%zu (dim %d): d_hat %.9f grad (%.6f %.6f %.6f)\n", i, g[i].dim, gs[i].d_hat, gs[i].grad.x,
+                        gs[i].grad.y, gs[i].grad.z);
+        SimplexMesh qm;
+        qm.vertices = {{4, 0, 0}, {4, 1, 0}, {4, 0, 1}, {0.5, 0.5, 2.0}};
+        qm.simplices = {Simplex::triangle(0, 1, 2), Simplex::edge(2, 3)};
+        p.alpha_q = 20.0;
+        const auto md = eng.smooth_mesh_dist(qm, p);
+        std::printf("mesh-to-mesh d_hat %.9f, vertex 0 grad (%.6f %.6f %.6f)\n", md.d_hat, md.vertex_grads[0].x,
+                    md.vertex_grads[0].y, md.vertex_grads[0].z);
         return std::isfinite(exact[0].d_hat) ? 0 : 3;
     } catch (const std::exception& e) {
         std::fprintf(stderr, "error: %s\n", e.what());

@@ -10,6 +10,8 @@
 //   eng.build_bvh(SD_BVH_LBVH);         // or set_bvh(reference_tree)
 //   auto r = eng.smooth_min_dist(queries, params);      // one call per batch
 //   auto e = eng.smooth_min_dist_flat(queries, params); // exact (beta ignored)
+//   auto g = eng.smooth_min_dist(simplex_geoms, params); // query edges / triangles
+//   auto m = eng.smooth_mesh_dist(query_mesh, params);   // mesh-to-mesh
 //
 // Failures throw std::runtime_error, as the reference's fail() does
 // (common.hpp:50); the evaluator semantics are the reference's (+inf and a
@@ -46,6 +48,16 @@ struct Simplex {
 struct SimplexMesh {
     std::vector<Vec3> vertices;
     std::vector<Simplex> simplices;
+};
+
+// A query simplex by its corners (exact.hpp:24-41): dim 0 point, 1 edge,
+// 2 triangle; corners past dim are ignored.
+struct SimplexGeom {
+    Vec3 c[3];
+    int dim = 0;
+    static SimplexGeom point(Vec3 a) { return {{a, {}, {}}, 0}; }
+    static SimplexGeom edge(Vec3 a, Vec3 b) { return {{a, b, {}}, 1}; }
+    static SimplexGeom triangle(Vec3 a, Vec3 b, Vec3 c) { return {{a, b, c}, 2}; }
 };
 
 struct SmoothParams {
@@ -137,27 +149,36 @@ public:
     std::vector<SmoothResult> smooth_min_dist(const std::vector<Vec3>& q, const SmoothParams& p) {
         return run(q, p, p.beta > 0.0 ? SD_BVH : SD_EXACT);
     }
-    // smooth_mesh_dist (smooth.hpp:212-255) for a point-cloud query mesh
-    // (every simplex of `query` must be a point).
+    // smooth_min_dist (smooth.hpp:166-184) / _flat (:189-198) for a batch of
+    // query SIMPLICES (points, edges, triangles); fp64 on the device.
+    std::vector<SmoothResult> smooth_min_dist(const std::vector<SimplexGeom>& g, const SmoothParams& p) {
+        return run_simplices(g, p, p.beta > 0.0 ? SD_BVH : SD_EXACT);
+    }
+    std::vector<SmoothResult> smooth_min_dist_flat(const std::vector<SimplexGeom>& g, const SmoothParams& p) {
+        return run_simplices(g, p, SD_EXACT);
+    }
+
+    // smooth_mesh_dist (smooth.hpp:212-255) for any query mesh.
     struct MeshDistResult {
         double d_hat = std::numeric_limits<double>::infinity();
         std::vector<Vec3> vertex_grads;
         std::vector<double> per_primitive;
     };
     MeshDistResult smooth_mesh_dist(const SimplexMesh& query, const SmoothParams& p) {
-        std::vector<std::int32_t> pts;
-        for (const Simplex& s : query.simplices) {
-            if (s.kind != SimplexKind::Point) throw std::runtime_error("smooth_mesh_dist: point query meshes only");
-            pts.push_back(s.v[0]);
+        std::vector<std::int32_t> sv(3 * query.simplices.size());
+        std::vector<std::uint8_t> kind(query.simplices.size());
+        for (size_t j = 0; j < query.simplices.size(); ++j) {
+            for (int k = 0; k < 3; ++k) sv[3 * j + k] = query.simplices[j].v[k];
+            kind[j] = static_cast<std::uint8_t>(query.simplices[j].kind);
         }
         MeshDistResult r;
         r.vertex_grads.resize(query.vertices.size());
-        r.per_primitive.resize(pts.size());
+        r.per_primitive.resize(kind.size());
         const sd_params sp{p.alpha, p.alpha_u, p.beta, p.epsilon};
-        check(sd_mesh_dist_points(ctx_, reinterpret_cast<const double*>(query.vertices.data()),
-                                  static_cast<std::int64_t>(query.vertices.size()), pts.data(),
-                                  static_cast<std::int64_t>(pts.size()), &sp, p.alpha_q, p.beta > 0 ? SD_BVH : SD_EXACT,
-                                  &r.d_hat, reinterpret_cast<double*>(r.vertex_grads.data()), r.per_primitive.data()));
+        check(sd_mesh_dist(ctx_, reinterpret_cast<const double*>(query.vertices.data()),
+                           static_cast<std::int64_t>(query.vertices.size()), sv.data(), kind.data(),
+                           static_cast<std::int64_t>(kind.size()), &sp, p.alpha_q, p.beta > 0 ? SD_BVH : SD_EXACT,
+                           &r.d_hat, reinterpret_cast<double*>(r.vertex_grads.data()), r.per_primitive.data()));
         return r;
     }
 
@@ -180,6 +201,36 @@ private:
         for (size_t i = 0; i < n; ++i) {
             out[i].d_hat = d[i];
             out[i].grad = {g[3 * i], g[3 * i + 1], g[3 * i + 2]};
+            out[i].c = c[i];
+            out[i].grad_c = {gc[3 * i], gc[3 * i + 1], gc[3 * i + 2]};
+            out[i].leaves = leaves[i];
+            out[i].far_field = far[i];
+            out[i].decision_hash = hash[i];
+        }
+        return out;
+    }
+
+    std::vector<SmoothResult> run_simplices(const std::vector<SimplexGeom>& g, const SmoothParams& p, int mode) {
+        const size_t n = g.size();
+        std::vector<double> corners(9 * n, 0.0), d(n), c(n), gr(3 * n), gc(3 * n);
+        std::vector<std::int32_t> dims(n);
+        std::vector<std::int64_t> leaves(n), far(n);
+        std::vector<std::uint64_t> hash(n);
+        for (size_t i = 0; i < n; ++i) {
+            dims[i] = g[i].dim;
+            for (int k = 0; k < 3; ++k) {
+                corners[9 * i + 3 * k] = g[i].c[k].x;
+                corners[9 * i + 3 * k + 1] = g[i].c[k].y;
+                corners[9 * i + 3 * k + 2] = g[i].c[k].z;
+            }
+        }
+        sd_outputs o{d.data(), gr.data(), c.data(), gc.data(), leaves.data(), far.data(), hash.data()};
+        const sd_params sp{p.alpha, p.alpha_u, p.beta, p.epsilon};
+        check(sd_query_simplices(ctx_, corners.data(), dims.data(), static_cast<std::int64_t>(n), &sp, mode, &o));
+        std::vector<SmoothResult> out(n);
+        for (size_t i = 0; i < n; ++i) {
+            out[i].d_hat = d[i];
+            out[i].grad = {gr[3 * i], gr[3 * i + 1], gr[3 * i + 2]};
             out[i].c = c[i];
             out[i].grad_c = {gc[3 * i], gc[3 * i + 1], gc[3 * i + 2]};
             out[i].leaves = leaves[i];
