@@ -228,22 +228,24 @@ __global__ void __launch_bounds__(kTravThreads) pair_kernel(const __grid_constan
     if (nre) atomicAdd(a.rechecks, nre);
 }
 
-// K3F (few queries, node-parallel): one warp per query; the lanes test up
-// to 32 nodes of that query's walk at once. The warp pops the top 32 (or
-// fewer) entries of its shared-memory stack, every lane tests its node
-// exactly like the serial walk would (far field / exact leaf / descend),
-// and the children of descending nodes are pushed (ballot + prefix count).
-// A node is tested iff all its ancestors descended -- the reference's
-// visited set -- only the order of the terms differs. Each lane keeps its
-// own accumulator; the 32 states are merged in fp64 at the end.
+// K3F (few queries, node-parallel): a group of G lanes per query (32 / G
+// queries per warp); the lanes of a group test up to G nodes of their
+// query's walk at once. A group pops the top G (or fewer) entries of its
+// shared-memory stack, every lane tests its node exactly like the serial
+// walk would (far field / exact leaf / descend), and the children of
+// descending nodes are pushed (ballot + prefix count within the group). A
+// node is tested iff all its ancestors descended -- the reference's visited
+// set -- only the order of the terms differs. Each lane keeps its own
+// accumulator; the G states of a query are merged in fp64 at the end. (The
+// walk of one query is a narrow frontier -- ~4 live nodes near a surface --
+// so G = 4..8 keeps most lanes busy; G = 32 is one query per warp.)
 // Stack bound: the entries stay sorted by depth (children of the popped top
 // entries are deeper than everything left below them), and entries of depth
-// d are only created while the depth-(d-1) entries on top are popped -- in
-// the same batch as every depth-d entry above them -- so each level holds at
-// most 2 x 32 entries and 64 (depth + 1) always suffice. The guard below
-// can therefore not fire; it records a flag instead of writing past the
-// stack.
-template <class T, class VIS, bool HASH>
+// d are only created while depth-(d-1) entries on top are popped -- in the
+// same batch as every depth-d entry above them -- so each level holds at
+// most 2 G entries and 2 G (depth + 1) always suffice. The guard below can
+// therefore not fire; it records a flag instead of writing past the stack.
+template <class T, class VIS, bool HASH, int G>
 __global__ void __launch_bounds__(kTravThreads) frontier_kernel(const __grid_constant__ TraverseArgs<T> a, int cap,
                                                                 int* overflow) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -253,56 +255,62 @@ __global__ void __launch_bounds__(kTravThreads) frontier_kernel(const __grid_con
         reinterpret_cast<T*>(polys)[i] = reinterpret_cast<const T*>(a.polys)[i];
     __syncthreads();
     const unsigned lane = threadIdx.x & 31u;
-    const int64_t i = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;  // sorted query position
-    if (i >= a.Q) return;
-    int32_t* stk = stacks + size_t(threadIdx.x >> 5) * cap;
-    const int64_t qi = a.perm ? a.perm[i] : i;
+    const unsigned grp = lane / G, r = lane % G;
+    const unsigned gshift = grp * G;
+    constexpr unsigned gmask = G == 32 ? 0xffffffffu : ((1u << G) - 1u);
+    const int64_t i = ((int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5) * (32 / G) + grp;  // sorted position
+    const bool valid = i < a.Q;
+    int32_t* stk = stacks + size_t(threadIdx.x / G) * cap;
+    const int64_t qi = valid ? (a.perm ? a.perm[i] : i) : 0;
     VIS qv;
-    qv.load(a, qi, true);
+    qv.load(a, qi, valid);
     Acc<T> acc;
     acc.init();
     int64_t nleaf = 0, nfar = 0;
     uint64_t h = 0;
     unsigned long long nre = 0;
-    if (lane == 0) stk[0] = 0;
+    if (r == 0) stk[0] = 0;
     __syncwarp();
-    int n = 1;
-    while (n > 0) {
-        const int take = n < 32 ? n : 32;
+    int n = valid ? 1 : 0;
+    while (__any_sync(0xffffffffu, n > 0)) {
+        const int take = n < G ? n : G;
         const int base = n - take;
-        const int32_t id = int(lane) < take ? stk[base + lane] : -1;
+        const int32_t id = int(r) < take ? stk[base + r] : -1;
         __syncwarp();
         bool d = false;
         if (id >= 0) {
             const NodeT<T> b = a.box[id];
             d = qv.template visit<HASH>(a, polys, b, id, a.lgcount[id], acc, nleaf, nfar, h, nre);
         }
-        const unsigned D = __ballot_sync(0xffffffffu, d);
+        const unsigned D = (__ballot_sync(0xffffffffu, d) >> gshift) & gmask;
         const int pushed = 2 * __popc(D);
         if (base + pushed > cap) {  // unreachable (see above)
-            if (lane == 0) atomicExch(overflow, 1);
-            break;
+            if (r == 0) atomicExch(overflow, 1);
+            n = 0;
+            continue;
         }
         if (d) {
-            const int pos = base + 2 * __popc(D & ((1u << lane) - 1u));
+            const int pos = base + 2 * __popc(D & ((1u << r) - 1u));
             int32_t link;
             memcpy(&link, &a.box[id].v[7], sizeof(int32_t));
-            stk[pos] = link;    // right child below ...
+            stk[pos] = link;        // right child below ...
             stk[pos + 1] = id + 1;  // ... left child on top
         }
         __syncwarp();
         n = base + pushed;
     }
-    // merge the lanes' states (fp64, anchored at the warp maximum)
+    // merge the group's states (fp64, anchored at the group maximum)
     Tot tot;
     tot.init();
     tot.flush(acc);
     double M = tot.M;
-    for (int off = 16; off; off >>= 1) M = fmax(M, __shfl_xor_sync(0xffffffffu, M, off));
+#pragma unroll
+    for (int off = G / 2; off; off >>= 1) M = fmax(M, __shfl_xor_sync(0xffffffffu, M, off));
     const double f = (M == -INFINITY || tot.M == -INFINITY) ? 0.0 : exp2(tot.M - M);
     double s = tot.s * f, gx = tot.gx * f, gy = tot.gy * f, gz = tot.gz * f;
     unsigned long long L = (unsigned long long)nleaf, F = (unsigned long long)nfar, H = h;
-    for (int off = 16; off; off >>= 1) {
+#pragma unroll
+    for (int off = G / 2; off; off >>= 1) {
         s += __shfl_xor_sync(0xffffffffu, s, off);
         gx += __shfl_xor_sync(0xffffffffu, gx, off);
         gy += __shfl_xor_sync(0xffffffffu, gy, off);
@@ -311,7 +319,7 @@ __global__ void __launch_bounds__(kTravThreads) frontier_kernel(const __grid_con
         F += __shfl_xor_sync(0xffffffffu, F, off);
         H += __shfl_xor_sync(0xffffffffu, H, off);
     }
-    if (lane == 0) {
+    if (r == 0 && valid) {
         a.part[i] = M;
         a.part[a.Q + i] = s;
         a.part[2 * a.Q + i] = gx;
@@ -324,17 +332,29 @@ __global__ void __launch_bounds__(kTravThreads) frontier_kernel(const __grid_con
     if (nre) atomicAdd(a.rechecks, nre);
 }
 
-// K3F launcher: returns false (nothing launched) when the stacks would not
-// fit in shared memory.
+// K3F launcher with group width G (SDGPU_FRONTIER_G overrides): returns
+// false (nothing launched) when the stacks would not fit in shared memory.
 template <class T, class VIS>
-bool launch_frontier(Ctx& c, DeviceTree& t, TraverseArgs<T>& a, bool hash, cudaStream_t st, int64_t& launches) {
-    const int cap = 64 * (t.depth + 1);
-    const size_t smem = poly_bytes<T>(a.npoly) + size_t(cap) * (kTravThreads / 32) * sizeof(int32_t);
+bool launch_frontier(Ctx& c, DeviceTree& t, TraverseArgs<T>& a, bool hash, cudaStream_t st, int64_t& launches,
+                     int G = 4) {
+    const char* e = std::getenv("SDGPU_FRONTIER_G");
+    if (e && *e) G = std::atoi(e);
+    if (G != 4 && G != 8 && G != 16 && G != 32) G = 4;
+    const int cap = 2 * G * (t.depth + 1);
+    const size_t smem = poly_bytes<T>(a.npoly) + size_t(cap) * (kTravThreads / G) * sizeof(int32_t);
     if (smem > 200 * 1024) return false;
     int* flag = static_cast<int*>(c.flag.ensure(sizeof(int)));
-    auto kern = hash ? frontier_kernel<T, VIS, true> : frontier_kernel<T, VIS, false>;
+    using K = void (*)(TraverseArgs<T>, int, int*);
+    K kern;
+    switch (G) {
+        case 8: kern = hash ? frontier_kernel<T, VIS, true, 8> : frontier_kernel<T, VIS, false, 8>; break;
+        case 16: kern = hash ? frontier_kernel<T, VIS, true, 16> : frontier_kernel<T, VIS, false, 16>; break;
+        case 32: kern = hash ? frontier_kernel<T, VIS, true, 32> : frontier_kernel<T, VIS, false, 32>; break;
+        default: kern = hash ? frontier_kernel<T, VIS, true, 4> : frontier_kernel<T, VIS, false, 4>; break;
+    }
     check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)), "smem attr");
-    kern<<<unsigned((a.Q * 32 + kTravThreads - 1) / kTravThreads), kTravThreads, smem, st>>>(a, cap, flag);
+    const int64_t threads = (a.Q + 32 / G - 1) / (32 / G) * 32;
+    kern<<<unsigned((threads + kTravThreads - 1) / kTravThreads), kTravThreads, smem, st>>>(a, cap, flag);
     check_cuda(cudaGetLastError(), "frontier kernel");
     ++launches;
     return true;

@@ -139,7 +139,7 @@ def test_random_scene_tree_decisions(sd, oracle, prec, seed):
 
 
 @pytest.mark.parametrize("prec", [0, 1])
-@pytest.mark.parametrize("split", ["0", "1", "3", "6", "", "frontier"])
+@pytest.mark.parametrize("split", ["0", "1", "3", "6", "", "frontier", "frontier32"])
 def test_split_traversal_decisions(sd, oracle, prec, split, monkeypatch):
     """The few-query traversal modes visit exactly the oracle's nodes:
     the slot split (one warp per (packet, depth-k slot) after re-testing the
@@ -147,8 +147,9 @@ def test_split_traversal_decisions(sd, oracle, prec, split, monkeypatch):
     automatic choice (""), and the node-parallel frontier kernel: counters
     and decision hash identical."""
     O = oracle
-    if split == "frontier":
+    if split.startswith("frontier"):
         monkeypatch.setenv("SDGPU_FRONTIER", "1")
+        monkeypatch.setenv("SDGPU_FRONTIER_G", split[8:] or "4")
     else:
         monkeypatch.setenv("SDGPU_FRONTIER", "0")
         monkeypatch.setenv("SDGPU_SPLIT", split)

@@ -106,10 +106,11 @@ def test_simplex_lbvh_decisions(sd, oracle):
     _close(got, ref, "lbvh")
 
 
-@pytest.mark.parametrize("split", ["0", "3", "", "frontier"])
+@pytest.mark.parametrize("split", ["0", "3", "", "frontier", "frontier32"])
 def test_simplex_split_traversal(sd, oracle, split, monkeypatch):
-    if split == "frontier":
+    if split.startswith("frontier"):
         monkeypatch.setenv("SDGPU_FRONTIER", "1")
+        monkeypatch.setenv("SDGPU_FRONTIER_G", split[8:] or "4")
     else:
         monkeypatch.setenv("SDGPU_FRONTIER", "0")
         monkeypatch.setenv("SDGPU_SPLIT", split)
