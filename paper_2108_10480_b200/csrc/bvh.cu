@@ -783,8 +783,12 @@ void tree_query(Ctx& c, const T* q, int64_t Q, const sd_params& p, const Finaliz
     }();
     int nsplits = 1;
     if (variant == 2) {
-        if (!(use_frontier(Q, 16384) &&
-              launch_frontier<T, PointVisit<T>>(c, c.dtree, a, out.hash != nullptr, st, launches)))
+        // few / sparse queries: node-parallel K3F (one warp per query); dense
+        // batches: K3 packets (tools/frontier_crossover.py: cfg4, 1k..262k
+        // queries: K3F 0.10 / 0.32 / 0.73 / 2.06 / 6.8 ms vs K3 2.8 / 7.0 / 7.7 /
+        // 6.3 / 7.3 ms; the full dense 4.19M batch: K3 29.7 ms)
+        if (!(use_frontier(Q, 65536) &&
+              launch_frontier<T, PointVisit<T>>(c, c.dtree, a, out.hash != nullptr, st, launches, 32)))
             nsplits = launch_pair_traversal<T, PointVisit<T>>(c, c.dtree, a, out.hash != nullptr, st, launches);
     } else {
         const size_t smem = poly_bytes<T>(npoly) +

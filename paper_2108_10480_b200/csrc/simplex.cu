@@ -766,7 +766,8 @@ void simplex_query(Ctx& c, const double* corners, const int32_t* dims, int64_t Q
     a.leafgeom = c.leafgeom.as<double>();
     // node tests cost a QP: few-query batches go node-parallel
     int nsplits = 1;
-    if (!(use_frontier(Q, 16384) && launch_frontier<double, SimplexVisit>(c, t, a, out.hash != nullptr, st, launches)))
+    if (!(use_frontier(Q, int64_t(1) << 22) &&
+          launch_frontier<double, SimplexVisit>(c, t, a, out.hash != nullptr, st, launches, 32)))
         nsplits = launch_pair_traversal<double, SimplexVisit>(c, t, a, out.hash != nullptr, st, launches, 4);
     check_cuda(launch_finalize(a.part, nsplits, Q, p.alpha, p.epsilon, 0, a.leaves, a.far, a.hash, perm, out, st),
                "finalize");

@@ -257,14 +257,16 @@ def test_config_exact_parity(sd, oracle, cfg, prec, alphas, nq):
         assert_close(got, ref, prec, alpha, f"cfg{cfg} alpha {alpha}")
 
 
-@pytest.mark.parametrize("builder", ["median", "lbvh"])
-def test_config4_tree_parity_subset(sd, oracle, builder):
+@pytest.mark.parametrize("builder,kernel", [("median", "K3F"), ("lbvh", "K3F"), ("lbvh", "K3")])
+def test_config4_tree_parity_subset(sd, oracle, builder, kernel, monkeypatch):
     """cfg4 (icosphere(9), 5.2M triangles, beta 0.5, alpha 200) on a query
     subset (both halves of the query distribution): decisions identical to
     the oracle on the same tree -- the reference median tree, or the GPU
     LBVH exported to the oracle -- and the Barnes-Hut field below the exact
-    one (acceptance [1])."""
+    one (acceptance [1]); both traversal kernels (K3F is the default for
+    this batch size, K3 the one the full-size bench runs)."""
     O = oracle
+    monkeypatch.setenv("SDGPU_FRONTIER", "1" if kernel == "K3F" else "0")
     m, q = _cfg(O, 4, 512, 0)
     w = O.Weights.build(m)
     if builder == "median":
