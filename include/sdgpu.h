@@ -15,6 +15,10 @@
  *   sd_set_bvh           <- Bvh / BvhNode, reference layout        (bvh.hpp:14-32)
  *   sd_build_bvh         <- build_bvh                              (bvh.hpp:34-91)
  *   sd_export_bvh        <- Bvh::nodes (save_bvh_cache record)     (bvh.hpp:193-212)
+ *   sd_save_bvh_cache / sd_load_bvh_cache       <- save_bvh_cache / load_bvh_cache
+ *                           (SDBV0001, bvh.hpp:190-236)
+ *   sd_save_weight_cache / sd_load_weight_cache <- save_weight_cache /
+ *                           load_weight_cache (SDWT0001, weights.hpp:700-781)
  *   sd_query_points      <- smooth_min_dist(mesh, bvh, ws, q, params) per query
  *                           (smooth.hpp:166-184; beta > 0 => Barnes-Hut tree path)
  *                           smooth_min_dist_flat(mesh, ws, q, params)
@@ -186,6 +190,17 @@ int sd_query_simplices(sd_ctx* ctx, const double* corners, const int32_t* dims, 
 int sd_mesh_dist(sd_ctx* ctx, const double* qxyz, int64_t Vq, const int32_t* qsimplices, const uint8_t* qkinds,
                  int64_t Nq, const sd_params* p, double alpha_q, int mode, double* d_hat, double* vertex_grads,
                  double* per_primitive);
+
+/* Reference binary caches, byte-compatible with the reference's files:
+ * SDBV0001 trees (bvh.hpp:190-236; loading = sd_set_bvh) and SDWT0001
+ * weight sets (weights.hpp:700-781; loading = sd_set_weights plus the
+ * per-polynomial valences / extrema / residual). A table given through
+ * sd_set_weights is saved with edge valences recovered from w~(0), w~(1),
+ * sampled extrema, and triangle valences 0 (unknown). */
+int sd_save_bvh_cache(sd_ctx* ctx, const char* path);
+int sd_load_bvh_cache(sd_ctx* ctx, const char* path);
+int sd_save_weight_cache(sd_ctx* ctx, const char* path);
+int sd_load_weight_cache(sd_ctx* ctx, const char* path);
 
 /* Number of this library's kernels launched by the last query call. */
 int sd_last_launch_count(sd_ctx* ctx, int64_t* n);

@@ -99,6 +99,10 @@ def _declare(L):
         "sdo_decision_mix": (u64, [u64, u64]),
         "sdo_mesh_dist": (C.c_int, [vp, vp, vp, vp, vp, C.c_int, vp, vp, vp, vp]),
         "sdo_hardware_threads": (C.c_int, []),
+        "sdo_save_bvh_cache": (C.c_int, [vp, C.c_char_p]),
+        "sdo_load_bvh_cache": (vp, [C.c_char_p]),
+        "sdo_save_weight_cache": (C.c_int, [vp, C.c_char_p]),
+        "sdo_load_weight_cache": (vp, [C.c_char_p]),
         "sdo_query_simplices": (C.c_int, [vp, vp, vp, vp, vp, i64, vp, C.c_int] + [vp] * 8),
         "sdo_simplex_distance": (C.c_int, [vp, C.c_int, vp, C.c_int, C.c_int, vp]),
         "sdo_box_primitive_proximity": (C.c_int, [vp, vp, vp, C.c_int, vp]),
@@ -525,3 +529,28 @@ def box_primitive_proximity(lo, hi, g, gdim: int):
     _check(lib().sdo_box_primitive_proximity(_ptr(np.asarray(lo, np.float64)), _ptr(np.asarray(hi, np.float64)),
                                              _ptr(gc), gdim, _ptr(out)))
     return float(out[0]), out[1:4].copy(), out[4:6].copy(), bool(out[6])
+
+
+# ------------------------------------------------------- reference caches
+def save_bvh_cache(tree: Tree, path: str):
+    """save_bvh_cache (bvh.hpp:196-212, SDBV0001)."""
+    _check(lib().sdo_save_bvh_cache(tree.h, path.encode()))
+
+
+def load_bvh_cache(path: str) -> Tree:
+    h = lib().sdo_load_bvh_cache(path.encode())
+    if not h:
+        raise RuntimeError(lib().sdo_last_error().decode())
+    return Tree(h)
+
+
+def save_weight_cache(weights: Weights, path: str):
+    """save_weight_cache (weights.hpp:715-742, SDWT0001)."""
+    _check(lib().sdo_save_weight_cache(weights.h, path.encode()))
+
+
+def load_weight_cache(path: str) -> Weights:
+    h = lib().sdo_load_weight_cache(path.encode())
+    if not h:
+        raise RuntimeError(lib().sdo_last_error().decode())
+    return Weights(h)

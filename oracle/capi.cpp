@@ -430,6 +430,30 @@ int sdo_mesh_dist(void* mesh, void* ws, void* bvh, void* query, const double* pa
     });
 }
 
+// reference caches (bvh.hpp:190-236, weights.hpp:700-781)
+int sdo_save_bvh_cache(void* bvh, const char* path) {
+    return guard([&] { save_bvh_cache(*static_cast<Bvh*>(bvh), path); });
+}
+void* sdo_load_bvh_cache(const char* path) {
+    try {
+        return new Bvh(load_bvh_cache(path));
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return nullptr;
+    }
+}
+int sdo_save_weight_cache(void* ws, const char* path) {
+    return guard([&] { save_weight_cache(*static_cast<WeightSet*>(ws), path); });
+}
+void* sdo_load_weight_cache(const char* path) {
+    try {
+        return new WeightSet(load_weight_cache(path));
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return nullptr;
+    }
+}
+
 std::uint64_t sdo_decision_mix(std::uint64_t node, std::uint64_t kind) { return decision_mix(node, kind); }
 int sdo_hardware_threads() {
     const unsigned n = std::thread::hardware_concurrency();

@@ -467,3 +467,130 @@ inline MeshDist smooth_mesh_dist(const Mesh& m, const Bvh* bvh, const WeightSet&
 }
 
 }  // namespace sdo
+
+// ------------------------------------------------------ reference caches
+// (kept in this header: oracle-side interchange with the product's
+// sd_save_* / sd_load_* entry points)
+#include <fstream>
+
+namespace sdo {
+
+// bvh.hpp:190-236 (SDBV0001)
+inline void save_bvh_cache(const Bvh& bvh, const std::string& path) {
+    static const char magic[8] = {'S', 'D', 'B', 'V', '0', '0', '0', '1'};
+    std::ofstream out(path, std::ios::binary);
+    if (!out) fail("cannot open " + path + " for writing");
+    out.write(magic, 8);
+    const std::uint64_t n = bvh.nodes.size();
+    out.write(reinterpret_cast<const char*>(&n), sizeof(n));
+    for (const BvhNode& node : bvh.nodes) {
+        const double lo[3] = {node.box.lo.x, node.box.lo.y, node.box.lo.z};
+        const double hi[3] = {node.box.hi.x, node.box.hi.y, node.box.hi.z};
+        out.write(reinterpret_cast<const char*>(lo), sizeof lo);
+        out.write(reinterpret_cast<const char*>(hi), sizeof hi);
+        out.write(reinterpret_cast<const char*>(&node.left), sizeof(node.left));
+        out.write(reinterpret_cast<const char*>(&node.right), sizeof(node.right));
+        out.write(reinterpret_cast<const char*>(&node.primitive), sizeof(node.primitive));
+        out.write(reinterpret_cast<const char*>(&node.count), sizeof(node.count));
+        out.write(reinterpret_cast<const char*>(&node.diameter), sizeof(node.diameter));
+    }
+    if (!out) fail("write failed: " + path);
+}
+inline Bvh load_bvh_cache(const std::string& path) {
+    static const char magic[8] = {'S', 'D', 'B', 'V', '0', '0', '0', '1'};
+    std::ifstream in(path, std::ios::binary);
+    if (!in) fail("cannot open " + path);
+    char m[8];
+    in.read(m, 8);
+    if (!in || std::memcmp(m, magic, 8) != 0) fail(path + ": not a BVH cache (bad magic)");
+    std::uint64_t n = 0;
+    in.read(reinterpret_cast<char*>(&n), sizeof(n));
+    Bvh bvh;
+    bvh.nodes.resize(n);
+    for (BvhNode& node : bvh.nodes) {
+        double lo[3], hi[3];
+        in.read(reinterpret_cast<char*>(lo), sizeof lo);
+        in.read(reinterpret_cast<char*>(hi), sizeof hi);
+        node.box.lo = V3(lo[0], lo[1], lo[2]);
+        node.box.hi = V3(hi[0], hi[1], hi[2]);
+        in.read(reinterpret_cast<char*>(&node.left), sizeof(node.left));
+        in.read(reinterpret_cast<char*>(&node.right), sizeof(node.right));
+        in.read(reinterpret_cast<char*>(&node.primitive), sizeof(node.primitive));
+        in.read(reinterpret_cast<char*>(&node.count), sizeof(node.count));
+        in.read(reinterpret_cast<char*>(&node.diameter), sizeof(node.diameter));
+    }
+    if (!in) fail(path + ": truncated BVH cache");
+    return bvh;
+}
+
+// weights.hpp:700-781 (SDWT0001)
+inline void save_weight_cache(const WeightSet& ws, const std::string& path) {
+    static const char magic[8] = {'S', 'D', 'W', 'T', '0', '0', '0', '1'};
+    std::ofstream out(path, std::ios::binary);
+    if (!out) fail("cannot open " + path + " for writing");
+    auto pod = [&](const auto& v) { out.write(reinterpret_cast<const char*>(&v), sizeof(v)); };
+    out.write(magic, 8);
+    pod(ws.A);
+    pod(ws.sup_wtilde);
+    pod(std::uint64_t(ws.edge_polys.size()));
+    pod(std::uint64_t(ws.tri_polys.size()));
+    pod(std::uint64_t(ws.poly_index.size()));
+    for (const EdgePoly& p : ws.edge_polys) {
+        pod(p.valence0);
+        pod(p.valence1);
+        for (double a : p.a) pod(a);
+        pod(p.sup);
+        pod(p.inf);
+    }
+    for (const TriPoly& p : ws.tri_polys) {
+        pod(p.vertex_valence);
+        pod(p.edge_valence);
+        for (double a : p.stored) pod(a);
+        pod(p.sup);
+        pod(p.inf);
+        pod(p.residual);
+    }
+    out.write(reinterpret_cast<const char*>(ws.poly_index.data()),
+              std::streamsize(ws.poly_index.size() * sizeof(std::int32_t)));
+    if (!out) fail("write failed: " + path);
+}
+inline WeightSet load_weight_cache(const std::string& path) {
+    static const char magic[8] = {'S', 'D', 'W', 'T', '0', '0', '0', '1'};
+    std::ifstream in(path, std::ios::binary);
+    if (!in) fail("cannot open " + path);
+    auto pod = [&](auto& v) { in.read(reinterpret_cast<char*>(&v), sizeof(v)); };
+    char m[8];
+    in.read(m, 8);
+    if (!in || std::memcmp(m, magic, 8) != 0) fail(path + ": not a weight cache (bad magic)");
+    WeightSet ws;
+    std::uint64_t ne, nt, np;
+    pod(ws.A);
+    pod(ws.sup_wtilde);
+    pod(ne);
+    pod(nt);
+    pod(np);
+    ws.edge_polys.resize(ne);
+    for (EdgePoly& p : ws.edge_polys) {
+        pod(p.valence0);
+        pod(p.valence1);
+        for (double& a : p.a) pod(a);
+        pod(p.sup);
+        pod(p.inf);
+    }
+    ws.tri_polys.resize(nt);
+    for (TriPoly& p : ws.tri_polys) {
+        pod(p.vertex_valence);
+        pod(p.edge_valence);
+        for (double& a : p.stored) pod(a);
+        pod(p.sup);
+        pod(p.inf);
+        pod(p.residual);
+        p.expand();
+    }
+    ws.poly_index.resize(np);
+    in.read(reinterpret_cast<char*>(ws.poly_index.data()), std::streamsize(np * sizeof(std::int32_t)));
+    if (!in) fail(path + ": truncated weight cache");
+    return ws;
+}
+
+}  // namespace sdo

@@ -40,6 +40,10 @@ EXPORTED_SYMBOLS = (
     "sd_mesh_dist_points",
     "sd_query_simplices",
     "sd_mesh_dist",
+    "sd_save_bvh_cache",
+    "sd_load_bvh_cache",
+    "sd_save_weight_cache",
+    "sd_load_weight_cache",
 )
 
 
@@ -102,6 +106,10 @@ def lib():
             "sd_mesh_dist_points": (C.c_int, [vp, vp, i64, vp, i64, P(_Params), f64, C.c_int, vp, vp, vp]),
             "sd_query_simplices": (C.c_int, [vp, vp, vp, i64, P(_Params), C.c_int, P(_Outputs)]),
             "sd_mesh_dist": (C.c_int, [vp, vp, i64, vp, vp, i64, P(_Params), f64, C.c_int, vp, vp, vp]),
+            "sd_save_bvh_cache": (C.c_int, [vp, C.c_char_p]),
+            "sd_load_bvh_cache": (C.c_int, [vp, C.c_char_p]),
+            "sd_save_weight_cache": (C.c_int, [vp, C.c_char_p]),
+            "sd_load_weight_cache": (C.c_int, [vp, C.c_char_p]),
         }
         for name, (res, argt) in sig.items():
             f = getattr(L, name)
@@ -210,8 +218,9 @@ class Engine:
         self.set_weights(t.A, t.sup_wtilde, t.edge_a, t.tri_stored, t.poly_index)
 
     def build_weights(self) -> "WeightTable":
-        """build_weight_set on the host (weights.hpp:589-621); installs and
-        returns the table."""
+        """build_weight_set (weights.hpp:589-621): adjacency, valences and the
+        polynomial assignment on the device, polynomials on the host;
+        installs and returns the table."""
         _check(lib().sd_build_weights(self.h))
         return self.weight_table()
 
@@ -341,6 +350,19 @@ class Engine:
         _check(lib().sd_mesh_dist(self.h, _ptr(v), len(v), _ptr(sv), _ptr(k), n, C.byref(params._c()),
                                   float(params.alpha_q), mode, _ptr(d), _ptr(vg), _ptr(pp)))
         return MeshDistResult(float(d[0]), vg, pp)
+
+    # -- reference caches (SDBV0001 bvh.hpp:190-236, SDWT0001 weights.hpp:700-781) --
+    def save_bvh_cache(self, path: str):
+        _check(lib().sd_save_bvh_cache(self.h, os.fsencode(path)))
+
+    def load_bvh_cache(self, path: str):
+        _check(lib().sd_load_bvh_cache(self.h, os.fsencode(path)))
+
+    def save_weight_cache(self, path: str):
+        _check(lib().sd_save_weight_cache(self.h, os.fsencode(path)))
+
+    def load_weight_cache(self, path: str):
+        _check(lib().sd_load_weight_cache(self.h, os.fsencode(path)))
 
     def smooth_min_dist_flat(self, q, params: SmoothParams) -> SmoothResults:
         """Batched smooth_min_dist_flat (smooth.hpp:189-198)."""

@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <fstream>
 #include <stdexcept>
 
 #include "context.h"
@@ -436,6 +437,54 @@ static void dispatch(Ctx& c, const T* q, int64_t Q, const sd_params& p, int mode
     else exact_query<T>(c, q, Q, p, out, st);
 }
 
+// Metadata of a table given as bare coefficients: edge valences follow from
+// w~(0) = 1/v0, w~(1) = 1/v1 (weights.hpp:46-76) and the extrema are closed
+// form; triangle valences are unknown (0) and the extrema are sampled.
+static void set_default_meta(Ctx& c) {
+    const size_t ne = c.edge_a.size() / 5, nt = c.tri_stored.size() / 13;
+    c.edge_val.assign(2 * ne, 0);
+    c.edge_ext.assign(2 * ne, 0.0);
+    for (size_t k = 0; k < ne; ++k) {
+        const double* a = &c.edge_a[5 * k];
+        const double w0 = a[0], w1 = a[0] + a[1] + a[2] + a[3] + a[4];
+        c.edge_val[2 * k] = w0 > 0 ? int32_t(std::lround(1.0 / w0)) : 0;
+        c.edge_val[2 * k + 1] = w1 > 0 ? int32_t(std::lround(1.0 / w1)) : 0;
+        double sup = -INFINITY, inf = INFINITY;
+        for (int i = 0; i <= 1000; ++i) {
+            const double t = i / 1000.0;
+            const double v = a[0] + t * (a[1] + t * (a[2] + t * (a[3] + t * a[4])));
+            sup = std::max(sup, v);
+            inf = std::min(inf, v);
+        }
+        c.edge_ext[2 * k] = sup;
+        c.edge_ext[2 * k + 1] = inf;
+    }
+    c.tri_val.assign(2 * nt, 0);
+    c.tri_ext.assign(3 * nt, 0.0);
+    static const int kS[13][2] = {{0, 0}, {0, 2}, {0, 3}, {0, 4}, {0, 5}, {0, 6}, {0, 7},
+                                  {2, 2}, {2, 3}, {2, 4}, {2, 5}, {3, 3}, {3, 4}};
+    for (size_t k = 0; k < nt; ++k) {
+        double g[8][8] = {};
+        for (int m = 0; m < 13; ++m) g[kS[m][0]][kS[m][1]] = g[kS[m][1]][kS[m][0]] = c.tri_stored[13 * k + m];
+        double sup = -INFINITY, inf = INFINITY;
+        const int N = 128;
+        for (int i = 0; i <= N; ++i)
+            for (int j = 0; i + j <= N; ++j) {
+                const double x = double(i) / N, y = double(j) / N;
+                double v = 0;
+                for (int jj = 7; jj >= 0; --jj) {
+                    double row = 0;
+                    for (int kk = 7; kk >= 0; --kk) row = row * y + g[jj][kk];
+                    v = v * x + row;
+                }
+                sup = std::max(sup, v);
+                inf = std::min(inf, v);
+            }
+        c.tri_ext[3 * k] = sup;
+        c.tri_ext[3 * k + 1] = inf;
+    }
+}
+
 }  // namespace sdgpu
 
 using namespace sdgpu;
@@ -546,6 +595,7 @@ int sd_set_weights(sd_ctx* c, double A, double sup, int32_t ne, const double* ed
         c->edge_a.assign(edge_a, edge_a + 5 * size_t(ne));
         c->tri_stored.assign(tri_stored, tri_stored + 13 * size_t(nt));
         c->poly_index.assign(poly_index, poly_index + c->N);
+        set_default_meta(*c);
         c->have_weights = true;
         c->exact_ready = false;
         c->dtree_ready = false;
@@ -557,7 +607,16 @@ int sd_build_weights(sd_ctx* c) {
     return guard([&] {
         if (!c) throw ArgError{"ctx is NULL"};
         if (!c->have_geom) throw StateError{"set the geometry before building weights"};
-        const WeightTableHost t = build_weight_table(c->sv, c->kind, c->V);
+        // adjacency + polynomial assignment on the device (adjacency.cu);
+        // SDGPU_WEIGHTS_HOST=1 runs the host hash-map pass instead (A/B)
+        const char* e = std::getenv("SDGPU_WEIGHTS_HOST");
+        WeightTableHost t;
+        if (e && *e == '1') {
+            t = build_weight_table(c->sv, c->kind, c->V);
+        } else {
+            DeviceScope ds(c->device);
+            t = weight_table_from_assignment(gpu_weight_assignment(*c));
+        }
         std::vector<double> ts;
         for (const TriWeight& w : t.tri) ts.insert(ts.end(), w.stored, w.stored + 13);
         c->A = t.A;
@@ -565,6 +624,21 @@ int sd_build_weights(sd_ctx* c) {
         c->edge_a = t.edge_a;
         c->tri_stored = ts;
         c->poly_index = t.poly_index;
+        c->edge_val = t.edge_val;
+        c->edge_ext.clear();
+        for (size_t k = 0; k < t.edge_sup.size(); ++k) {
+            c->edge_ext.push_back(t.edge_sup[k]);
+            c->edge_ext.push_back(t.edge_inf[k]);
+        }
+        c->tri_val.clear();
+        c->tri_ext.clear();
+        for (const TriWeight& w : t.tri) {
+            c->tri_val.push_back(w.v);
+            c->tri_val.push_back(w.e);
+            c->tri_ext.push_back(w.sup);
+            c->tri_ext.push_back(w.inf);
+            c->tri_ext.push_back(0.0);  // residual: not recomputed
+        }
         c->have_weights = true;
         c->exact_ready = false;
         c->dtree_ready = false;
@@ -615,6 +689,137 @@ int sd_build_bvh(sd_ctx* c, int method) {
         else if (method == SD_BVH_LBVH) tree_build_lbvh(*c);
         else throw ArgError{"unknown tree builder"};
         c->have_tree = true;
+    });
+}
+
+// ------------------------------------------------- reference caches
+// SDBV0001 (bvh.hpp:190-236): magic, u64 node count, per node lo[3] hi[3]
+// (f64) left right primitive count (i32) diameter (f64) -- exactly the
+// 72-byte sd_bvh_node record, so the payload is the node array itself.
+static const char kBvhMagic[8] = {'S', 'D', 'B', 'V', '0', '0', '0', '1'};
+static const char kWtMagic[8] = {'S', 'D', 'W', 'T', '0', '0', '0', '1'};
+static_assert(sizeof(sd_bvh_node) == 72, "SDBV0001 record");
+
+int sd_save_bvh_cache(sd_ctx* c, const char* path) {
+    return guard([&] {
+        if (!c || !path) throw ArgError{"NULL argument"};
+        if (!c->have_tree) throw StateError{"no tree to save"};
+        std::ofstream out(path, std::ios::binary);
+        if (!out) throw ArgError{std::string("cannot open ") + path + " for writing"};
+        out.write(kBvhMagic, 8);
+        const uint64_t n = c->tree.size();
+        out.write(reinterpret_cast<const char*>(&n), sizeof(n));
+        out.write(reinterpret_cast<const char*>(c->tree.data()), std::streamsize(n * sizeof(sd_bvh_node)));
+        if (!out) throw ArgError{std::string("write failed: ") + path};
+    });
+}
+
+int sd_load_bvh_cache(sd_ctx* c, const char* path) {
+    return guard([&] {
+        if (!c || !path) throw ArgError{"NULL argument"};
+        if (!c->have_geom) throw StateError{"set the geometry before the tree"};
+        std::ifstream in(path, std::ios::binary);
+        if (!in) throw ArgError{std::string("cannot open ") + path};
+        char magic[8];
+        in.read(magic, 8);
+        if (!in || std::memcmp(magic, kBvhMagic, 8) != 0) throw ArgError{std::string(path) + ": not a BVH cache (bad magic)"};
+        uint64_t n = 0;
+        in.read(reinterpret_cast<char*>(&n), sizeof(n));
+        if (!in || int64_t(n) != (c->N > 0 ? 2 * c->N - 1 : 0))
+            throw ArgError{std::string(path) + ": node count does not match the mesh"};
+        std::vector<sd_bvh_node> nodes(n);
+        in.read(reinterpret_cast<char*>(nodes.data()), std::streamsize(n * sizeof(sd_bvh_node)));
+        if (!in) throw ArgError{std::string(path) + ": truncated BVH cache"};
+        c->tree.swap(nodes);
+        c->have_tree = true;
+        c->dtree_ready = false;
+        c->sx_tree_ready = c->sx_prim_ready = false;
+    });
+}
+
+// SDWT0001 (weights.hpp:700-781): magic, A, sup (f64), u64 counts (edge,
+// triangle polynomials, poly_index), per edge valence0 valence1 (i32)
+// a[5] sup inf (f64), per triangle v e (i32) stored[13] sup inf residual
+// (f64), then poly_index (i32). Little-endian, packed.
+int sd_save_weight_cache(sd_ctx* c, const char* path) {
+    return guard([&] {
+        if (!c || !path) throw ArgError{"NULL argument"};
+        if (!c->have_weights) throw StateError{"no weight table to save"};
+        std::ofstream out(path, std::ios::binary);
+        if (!out) throw ArgError{std::string("cannot open ") + path + " for writing"};
+        auto pod = [&](const auto& v) { out.write(reinterpret_cast<const char*>(&v), sizeof(v)); };
+        out.write(kWtMagic, 8);
+        const uint64_t ne = c->edge_a.size() / 5, nt = c->tri_stored.size() / 13, np = c->poly_index.size();
+        pod(c->A);
+        pod(c->sup_wtilde);
+        pod(ne);
+        pod(nt);
+        pod(np);
+        for (uint64_t k = 0; k < ne; ++k) {
+            pod(c->edge_val[2 * k]);
+            pod(c->edge_val[2 * k + 1]);
+            for (int j = 0; j < 5; ++j) pod(c->edge_a[5 * k + j]);
+            pod(c->edge_ext[2 * k]);
+            pod(c->edge_ext[2 * k + 1]);
+        }
+        for (uint64_t k = 0; k < nt; ++k) {
+            pod(c->tri_val[2 * k]);
+            pod(c->tri_val[2 * k + 1]);
+            for (int j = 0; j < 13; ++j) pod(c->tri_stored[13 * k + j]);
+            pod(c->tri_ext[3 * k]);
+            pod(c->tri_ext[3 * k + 1]);
+            pod(c->tri_ext[3 * k + 2]);
+        }
+        out.write(reinterpret_cast<const char*>(c->poly_index.data()), std::streamsize(np * sizeof(int32_t)));
+        if (!out) throw ArgError{std::string("write failed: ") + path};
+    });
+}
+
+int sd_load_weight_cache(sd_ctx* c, const char* path) {
+    return guard([&] {
+        if (!c || !path) throw ArgError{"NULL argument"};
+        if (!c->have_geom) throw StateError{"set the geometry before the weights"};
+        std::ifstream in(path, std::ios::binary);
+        if (!in) throw ArgError{std::string("cannot open ") + path};
+        auto pod = [&](auto& v) { in.read(reinterpret_cast<char*>(&v), sizeof(v)); };
+        char magic[8];
+        in.read(magic, 8);
+        if (!in || std::memcmp(magic, kWtMagic, 8) != 0)
+            throw ArgError{std::string(path) + ": not a weight cache (bad magic)"};
+        double A = 1, sup = 1;
+        uint64_t ne = 0, nt = 0, np = 0;
+        pod(A);
+        pod(sup);
+        pod(ne);
+        pod(nt);
+        pod(np);
+        if (!in || int64_t(np) != c->N || ne > (uint64_t(1) << 31) || nt > (uint64_t(1) << 31))
+            throw ArgError{std::string(path) + ": weight cache does not match the mesh"};
+        std::vector<double> ea(5 * ne), ts(13 * nt), eext(2 * ne), text(3 * nt);
+        std::vector<int32_t> ev(2 * ne), tv(2 * nt), pi(np);
+        for (uint64_t k = 0; k < ne; ++k) {
+            pod(ev[2 * k]);
+            pod(ev[2 * k + 1]);
+            for (int j = 0; j < 5; ++j) pod(ea[5 * k + j]);
+            pod(eext[2 * k]);
+            pod(eext[2 * k + 1]);
+        }
+        for (uint64_t k = 0; k < nt; ++k) {
+            pod(tv[2 * k]);
+            pod(tv[2 * k + 1]);
+            for (int j = 0; j < 13; ++j) pod(ts[13 * k + j]);
+            pod(text[3 * k]);
+            pod(text[3 * k + 1]);
+            pod(text[3 * k + 2]);
+        }
+        in.read(reinterpret_cast<char*>(pi.data()), std::streamsize(np * sizeof(int32_t)));
+        if (!in) throw ArgError{std::string(path) + ": truncated weight cache"};
+        const int rc = sd_set_weights(c, A, sup, int32_t(ne), ea.data(), int32_t(nt), ts.data(), pi.data());
+        if (rc != SD_OK) throw ArgError{sd_last_error()};
+        c->edge_val = ev;
+        c->edge_ext = eext;
+        c->tri_val = tv;
+        c->tri_ext = text;
     });
 }
 

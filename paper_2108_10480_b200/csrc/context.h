@@ -11,6 +11,7 @@
 
 #include "../../include/sdgpu.h"
 #include "exact.h"
+#include "weights_host.h"
 
 namespace sdgpu {
 
@@ -94,6 +95,11 @@ struct Ctx {
     double A = 1.0, sup_wtilde = 1.0;
     std::vector<double> edge_a, tri_stored;
     std::vector<int32_t> poly_index;
+    // per-polynomial metadata of the reference WeightSet (valences, extrema,
+    // residual) for the SDWT0001 cache: edge (v0, v1) + (sup, inf), triangle
+    // (v, e) + (sup, inf, residual); valence 0 = unknown
+    std::vector<int32_t> edge_val, tri_val;
+    std::vector<double> edge_ext, tri_ext;
 
     // exact layout
     bool exact_ready = false;
@@ -143,6 +149,7 @@ void simplex_query(Ctx& c, const double* corners, const int32_t* dims, int64_t Q
 void split_tables(Ctx& c, DeviceTree& t, int k);  // nodes at depth k of c.tree
 void tree_build_median(Ctx& c);
 void tree_build_lbvh(Ctx& c);
+WeightAssignment gpu_weight_assignment(Ctx& c);  // adjacency.cu
 template <class T>
 void tree_query(Ctx& c, const T* q, int64_t Q, const sd_params& p, const FinalizeOut& out, cudaStream_t st);
 

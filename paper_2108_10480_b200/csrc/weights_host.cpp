@@ -466,7 +466,7 @@ static TriWeight tri_cached(int v, int e) {
 }
 
 // closed-form edge polynomial and extrema (weights.hpp:46-76)
-static void edge_poly(int n0, int n1, double a[5], double& sup) {
+void edge_weight_poly(int n0, int n1, double a[5], double& sup, double& inf) {
     const double P = 1.0 / n1 - 1.0 / n0, Q = 1.0 - 1.0 / n0;
     a[0] = 1.0 / n0;
     a[1] = 0.0;
@@ -475,9 +475,13 @@ static void edge_poly(int n0, int n1, double a[5], double& sup) {
     a[4] = 16 * Q - 8 * P;
     auto val = [&](double t) { return a[0] + t * (a[1] + t * (a[2] + t * (a[3] + t * a[4]))); };
     sup = std::max(val(0.0), val(1.0));
+    inf = std::min(val(0.0), val(1.0));
     const double qa = 4 * a[4], qb = 3 * a[3], qc = 2 * a[2];
     auto consider = [&](double t) {
-        if (t > 0.0 && t < 1.0) sup = std::max(sup, val(t));
+        if (t > 0.0 && t < 1.0) {
+            sup = std::max(sup, val(t));
+            inf = std::min(inf, val(t));
+        }
     };
     if (std::abs(qa) > 1e-300) {
         const double disc = qb * qb - 4 * qa * qc;
@@ -488,6 +492,27 @@ static void edge_poly(int n0, int n1, double a[5], double& sup) {
     } else if (std::abs(qb) > 1e-300) {
         consider(-qc / qb);
     }
+}
+WeightTableHost weight_table_from_assignment(const WeightAssignment& wa) {
+    WeightTableHost t;
+    t.poly_index = wa.poly_index;
+    for (const auto& [n0, n1] : wa.edge_keys) {
+        double a[5], sup, inf;
+        edge_weight_poly(n0, n1, a, sup, inf);
+        t.edge_a.insert(t.edge_a.end(), a, a + 5);
+        t.edge_sup.push_back(sup);
+        t.edge_inf.push_back(inf);
+        t.edge_val.push_back(n0);
+        t.edge_val.push_back(n1);
+        t.A = std::max(t.A, double(std::max(n0, n1)));
+        t.sup = std::max(t.sup, sup);
+    }
+    for (const auto& [v, e] : wa.tri_keys) {
+        t.tri.push_back(tri_cached(v, e));
+        t.A = std::max(t.A, double(v));
+        t.sup = std::max(t.sup, t.tri.back().sup);
+    }
+    return t;
 }
 
 static inline uint64_t ekey(int32_t a, int32_t b) {
@@ -525,10 +550,13 @@ WeightTableHost build_weight_table(const std::vector<int32_t>& sv, const std::ve
             const int n0 = val[s[0]], n1 = val[s[1]];
             auto [it, fresh] = ec.try_emplace({n0, n1}, int32_t(t.edge_a.size() / 5));
             if (fresh) {
-                double a[5], sup;
-                edge_poly(n0, n1, a, sup);
+                double a[5], sup, inf;
+                edge_weight_poly(n0, n1, a, sup, inf);
                 t.edge_a.insert(t.edge_a.end(), a, a + 5);
                 t.edge_sup.push_back(sup);
+                t.edge_inf.push_back(inf);
+                t.edge_val.push_back(n0);
+                t.edge_val.push_back(n1);
             }
             t.poly_index[i] = it->second;
             t.A = std::max(t.A, double(std::max(n0, n1)));

@@ -353,3 +353,31 @@ def test_mesh_dist_softmin_identity_and_bounds(oracle):  # test_smooth.cpp:282-3
     dmin = md.per_primitive.min()
     assert abs(mass - 1.0) <= 1e-9
     assert dmin - math.log(q.num_simplices) / p.alpha_q - 1e-9 <= md.d_hat <= dmin + 1e-12
+
+
+# ------------------------------------------------- reference caches (CPU)
+def test_oracle_cache_round_trips(oracle, tmp_path):
+    """SDBV0001 / SDWT0001 (bvh.hpp:190-236, weights.hpp:700-781): save ->
+    load -> save is byte-identical, and the loaded tree / table equal the
+    originals."""
+    O = oracle
+    m = O.random_scene(4, 150)
+    t, w = O.Tree.build(m), O.Weights.build(m)
+    pb, pw = str(tmp_path / "t.sdbv"), str(tmp_path / "w.sdwt")
+    O.save_bvh_cache(t, pb)
+    t2 = O.load_bvh_cache(pb)
+    assert t2.nodes().tobytes() == t.nodes().tobytes()
+    O.save_bvh_cache(t2, pb + "2")
+    assert open(pb, "rb").read() == open(pb + "2", "rb").read()
+    raw = open(pb, "rb").read()
+    assert raw[:8] == b"SDBV0001" and len(raw) == 16 + 72 * len(t.nodes())
+    O.save_weight_cache(w, pw)
+    w2 = O.load_weight_cache(pw)
+    O.save_weight_cache(w2, pw + "2")
+    assert open(pw, "rb").read() == open(pw + "2", "rb").read()
+    a, b = w.table, w2.table
+    assert a.A == b.A and a.sup_wtilde == b.sup_wtilde
+    assert (a.edge_a == b.edge_a).all() and (a.tri_stored == b.tri_stored).all()
+    assert (a.poly_index == b.poly_index).all()
+    with pytest.raises(RuntimeError):
+        O.load_bvh_cache(pw)  # wrong magic
