@@ -31,6 +31,8 @@
  *   sd_mesh_dist         <- smooth_mesh_dist(mesh, bvh, ws, query, params) for
  *                           any query mesh (smooth.hpp:212-255)
  *   sd_mesh_dist_points  <- the same for a point-cloud query mesh
+ *   sd_render            <- render (render.hpp:77-134), sd_write_ppm / sd_write_png
+ *   sd_grid_benchmark    <- grid_benchmark (bench.hpp:29-70), sd_write_grid_csv
  *   sd_params            <- SmoothParams {alpha, alpha_u, beta, epsilon} (params.hpp:13-22)
  *   sd_outputs           <- SmoothResult {d_hat, grad, c, grad_c, leaves, far_field}
  *                           (smooth.hpp:20-27)
@@ -190,6 +192,37 @@ int sd_query_simplices(sd_ctx* ctx, const double* corners, const int32_t* dims, 
 int sd_mesh_dist(sd_ctx* ctx, const double* qxyz, int64_t Vq, const int32_t* qsimplices, const uint8_t* qkinds,
                  int64_t Nq, const sd_params* p, double alpha_q, int mode, double* d_hat, double* vertex_grads,
                  double* per_primitive);
+
+/* RenderConfig (render.hpp:17-25). threshold 0 = 1e-3 x bbox diagonal. */
+typedef struct sd_render_config {
+    double origin[3], target[3], up[3];
+    double fov_deg;
+    int32_t width, height;
+    double threshold;
+    int32_t max_steps;
+} sd_render_config;
+
+/* render (render.hpp:77-134): sphere-traces d_hat = 0 for width x height
+ * rays (one device wavefront step per marching step; per ray exactly the
+ * reference's iteration). rgb: W*H*3 bytes, rows top to bottom (black =
+ * miss); hit_t: W*H ray parameters (-1 = miss); stats (optional): leaves,
+ * far_field, rays, hits; seconds (optional): device time. mode SD_BVH as
+ * the reference (tree path; beta from p). Blocking. */
+int sd_render(sd_ctx* ctx, const sd_params* p, int mode, const sd_render_config* cfg, uint8_t* rgb, double* hit_t,
+              int64_t* stats, double* seconds);
+
+/* grid_benchmark (bench.hpp:29-70): d_hat (+ leaves / far-field counts,
+ * optional) at the n^3 voxel centres of [0,1]^3, x fastest. seconds:
+ * device time of the whole batch. Blocking. */
+int sd_grid_benchmark(sd_ctx* ctx, const sd_params* p, int mode, int32_t n, double* d_hat, int64_t* leaves,
+                      int64_t* far_field, double* seconds);
+
+/* Output writers of the callers: write_ppm (render.hpp:139-146, P6),
+ * write_png (:172-203, zlib level 6), write_grid_csv (bench.hpp:75-88). */
+int sd_write_ppm(const uint8_t* rgb, int32_t width, int32_t height, const char* path);
+int sd_write_png(const uint8_t* rgb, int32_t width, int32_t height, const char* path);
+int sd_write_grid_csv(const double* d_hat, const int64_t* leaves, const int64_t* far_field, int32_t n,
+                      const double* slab_seconds, const char* path);
 
 /* Reference binary caches, byte-compatible with the reference's files:
  * SDBV0001 trees (bvh.hpp:190-236; loading = sd_set_bvh) and SDWT0001

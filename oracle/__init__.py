@@ -99,6 +99,10 @@ def _declare(L):
         "sdo_decision_mix": (u64, [u64, u64]),
         "sdo_mesh_dist": (C.c_int, [vp, vp, vp, vp, vp, C.c_int, vp, vp, vp, vp]),
         "sdo_hardware_threads": (C.c_int, []),
+        "sdo_render": (C.c_int, [vp, vp, vp, vp, vp, C.c_int, vp, vp, vp, vp]),
+        "sdo_write_ppm": (C.c_int, [vp, C.c_int, C.c_int, C.c_char_p]),
+        "sdo_grid_benchmark": (C.c_int, [vp, vp, vp, vp, C.c_int, C.c_int, vp, vp, vp]),
+        "sdo_write_grid_csv": (C.c_int, [vp, vp, vp, C.c_int, vp, C.c_char_p]),
         "sdo_save_bvh_cache": (C.c_int, [vp, C.c_char_p]),
         "sdo_load_bvh_cache": (vp, [C.c_char_p]),
         "sdo_save_weight_cache": (C.c_int, [vp, C.c_char_p]),
@@ -554,3 +558,56 @@ def load_weight_cache(path: str) -> Weights:
     if not h:
         raise RuntimeError(lib().sdo_last_error().decode())
     return Weights(h)
+
+
+# ------------------------------------------------------------- callers
+@dataclass
+class RenderResult:
+    rgb: np.ndarray    # (H, W, 3) uint8
+    hit_t: np.ndarray  # (H, W), -1 on miss
+    leaves: int
+    far_field: int
+    rays: int
+    hits: int
+    seconds: float
+
+
+def render_config(origin=(1.5, 1.5, 1.5), target=(0.5, 0.5, 0.5), up=(0, 1, 0), fov_deg=45.0, width=256,
+                  height=256, threshold=0.0, max_steps=128) -> np.ndarray:
+    """RenderConfig (render.hpp:17-25) as the 14 doubles the C entry takes."""
+    return np.array([*origin, *target, *up, fov_deg, width, height, threshold, max_steps], np.float64)
+
+
+def render(mesh: Mesh, weights: Weights, tree: Tree, params: Params, cfg=None, threads: int = 0) -> RenderResult:
+    """render (render.hpp:77-134): per-pixel sphere tracing of d_hat = 0."""
+    cfg = render_config() if cfg is None else np.asarray(cfg, np.float64)
+    w, h = int(cfg[10]), int(cfg[11])
+    rgb = np.zeros((h, w, 3), np.uint8)
+    hit = np.zeros((h, w))
+    st = np.zeros(4, np.int64)
+    secs = np.zeros(1)
+    _check(lib().sdo_render(mesh.h, weights.h, tree.h, _ptr(_params_array(params)), _ptr(cfg),
+                            threads or hardware_threads(), _ptr(rgb), _ptr(hit), _ptr(st), _ptr(secs)))
+    return RenderResult(rgb, hit, int(st[0]), int(st[1]), int(st[2]), int(st[3]), float(secs[0]))
+
+
+def write_ppm(rgb: np.ndarray, path: str):
+    rgb = np.ascontiguousarray(rgb, np.uint8)
+    _check(lib().sdo_write_ppm(_ptr(rgb), rgb.shape[1], rgb.shape[0], path.encode()))
+
+
+def grid_benchmark(mesh: Mesh, weights: Weights, tree: Tree, params: Params, n: int, threads: int = 0):
+    """grid_benchmark (bench.hpp:29-70): (d_hat, leaves, far_field), x fastest."""
+    n3 = n ** 3
+    d, lv, fr = np.zeros(n3), np.zeros(n3, np.int64), np.zeros(n3, np.int64)
+    _check(lib().sdo_grid_benchmark(mesh.h, weights.h, tree.h, _ptr(_params_array(params)), n,
+                                    threads or hardware_threads(), _ptr(d), _ptr(lv), _ptr(fr)))
+    return d, lv, fr
+
+
+def write_grid_csv(d, leaves, far, n: int, slab_seconds, path: str):
+    d = np.ascontiguousarray(d, np.float64)
+    lv = np.ascontiguousarray(leaves, np.int64)
+    fr = np.ascontiguousarray(far, np.int64)
+    ss = np.ascontiguousarray(slab_seconds, np.float64)
+    _check(lib().sdo_write_grid_csv(_ptr(d), _ptr(lv), _ptr(fr), n, _ptr(ss), path.encode()))

@@ -6,6 +6,7 @@
 // every entry returns 0 on success and -1 with sdo_last_error() set.
 #include "shapes.hpp"
 #include "sdoracle_simplex.hpp"
+#include "sdoracle_callers.hpp"
 
 #include <chrono>
 
@@ -452,6 +453,57 @@ void* sdo_load_weight_cache(const char* path) {
         g_err = e.what();
         return nullptr;
     }
+}
+
+// render (render.hpp:77-134): cfg = origin[3] target[3] up[3] fov width height
+// threshold max_steps (12 doubles); stats = leaves, far_field, rays, hits
+int sdo_render(void* mesh, void* ws, void* bvh, const double* params, const double* cfg, int threads,
+               std::uint8_t* rgb, double* hit_t, std::int64_t* stats, double* seconds) {
+    return guard([&] {
+        RenderConfig rc;
+        rc.origin = V3(cfg[0], cfg[1], cfg[2]);
+        rc.target = V3(cfg[3], cfg[4], cfg[5]);
+        rc.up = V3(cfg[6], cfg[7], cfg[8]);
+        rc.fov_deg = cfg[9];
+        rc.width = int(cfg[10]);
+        rc.height = int(cfg[11]);
+        rc.threshold = cfg[12];
+        rc.max_steps = int(cfg[13]);
+        const RenderOut r = render(*static_cast<Mesh*>(mesh), *static_cast<Bvh*>(bvh), *static_cast<WeightSet*>(ws),
+                                   params_from(params), rc, threads);
+        std::memcpy(rgb, r.rgb.data(), r.rgb.size());
+        std::memcpy(hit_t, r.hit_t.data(), r.hit_t.size() * sizeof(double));
+        stats[0] = r.leaves;
+        stats[1] = r.far_field;
+        stats[2] = r.rays;
+        stats[3] = r.hits;
+        *seconds = r.seconds;
+    });
+}
+int sdo_write_ppm(const std::uint8_t* rgb, int w, int h, const char* path) {
+    return guard([&] { write_ppm(std::vector<std::uint8_t>(rgb, rgb + 3 * std::size_t(w) * h), w, h, path); });
+}
+// grid_benchmark (bench.hpp:29-70) and write_grid_csv (:75-88)
+int sdo_grid_benchmark(void* mesh, void* ws, void* bvh, const double* params, int n, int threads, double* d,
+                       std::int64_t* leaves, std::int64_t* far) {
+    return guard([&] {
+        const GridOut r = grid_benchmark(*static_cast<Mesh*>(mesh), *static_cast<Bvh*>(bvh),
+                                         *static_cast<WeightSet*>(ws), params_from(params), n, threads);
+        std::memcpy(d, r.d_hat.data(), r.d_hat.size() * sizeof(double));
+        std::memcpy(leaves, r.leaves.data(), r.leaves.size() * sizeof(std::int64_t));
+        std::memcpy(far, r.far_field.data(), r.far_field.size() * sizeof(std::int64_t));
+    });
+}
+int sdo_write_grid_csv(const double* d, const std::int64_t* leaves, const std::int64_t* far, int n,
+                       const double* slab_seconds, const char* path) {
+    return guard([&] {
+        const std::size_t n3 = std::size_t(n) * n * n;
+        GridOut r;
+        r.d_hat.assign(d, d + n3);
+        r.leaves.assign(leaves, leaves + n3);
+        r.far_field.assign(far, far + n3);
+        write_grid_csv(r, n, std::vector<double>(slab_seconds, slab_seconds + n), path);
+    });
 }
 
 std::uint64_t sdo_decision_mix(std::uint64_t node, std::uint64_t kind) { return decision_mix(node, kind); }

@@ -40,6 +40,11 @@ EXPORTED_SYMBOLS = (
     "sd_mesh_dist_points",
     "sd_query_simplices",
     "sd_mesh_dist",
+    "sd_render",
+    "sd_grid_benchmark",
+    "sd_write_ppm",
+    "sd_write_png",
+    "sd_write_grid_csv",
     "sd_save_bvh_cache",
     "sd_load_bvh_cache",
     "sd_save_weight_cache",
@@ -57,6 +62,12 @@ class SdError(RuntimeError):
 
 class _Params(C.Structure):
     _fields_ = [("alpha", C.c_double), ("alpha_u", C.c_double), ("beta", C.c_double), ("epsilon", C.c_double)]
+
+
+class _RenderConfig(C.Structure):
+    _fields_ = [("origin", C.c_double * 3), ("target", C.c_double * 3), ("up", C.c_double * 3),
+                ("fov_deg", C.c_double), ("width", C.c_int32), ("height", C.c_int32), ("threshold", C.c_double),
+                ("max_steps", C.c_int32)]
 
 
 class _Outputs(C.Structure):
@@ -106,6 +117,11 @@ def lib():
             "sd_mesh_dist_points": (C.c_int, [vp, vp, i64, vp, i64, P(_Params), f64, C.c_int, vp, vp, vp]),
             "sd_query_simplices": (C.c_int, [vp, vp, vp, i64, P(_Params), C.c_int, P(_Outputs)]),
             "sd_mesh_dist": (C.c_int, [vp, vp, i64, vp, vp, i64, P(_Params), f64, C.c_int, vp, vp, vp]),
+            "sd_render": (C.c_int, [vp, P(_Params), C.c_int, P(_RenderConfig), vp, vp, vp, vp]),
+            "sd_grid_benchmark": (C.c_int, [vp, P(_Params), C.c_int, i32, vp, vp, vp, vp]),
+            "sd_write_ppm": (C.c_int, [vp, i32, i32, C.c_char_p]),
+            "sd_write_png": (C.c_int, [vp, i32, i32, C.c_char_p]),
+            "sd_write_grid_csv": (C.c_int, [vp, vp, vp, i32, vp, C.c_char_p]),
             "sd_save_bvh_cache": (C.c_int, [vp, C.c_char_p]),
             "sd_load_bvh_cache": (C.c_int, [vp, C.c_char_p]),
             "sd_save_weight_cache": (C.c_int, [vp, C.c_char_p]),
@@ -351,6 +367,30 @@ class Engine:
                                   float(params.alpha_q), mode, _ptr(d), _ptr(vg), _ptr(pp)))
         return MeshDistResult(float(d[0]), vg, pp)
 
+    # -- batched callers (render.hpp:77-134, bench.hpp:29-70) --
+    def render(self, params: SmoothParams, origin=(1.5, 1.5, 1.5), target=(0.5, 0.5, 0.5), up=(0.0, 1.0, 0.0),
+               fov_deg=45.0, width=256, height=256, threshold=0.0, max_steps=128,
+               mode: int = SD_BVH) -> "RenderResult":
+        """Sphere-traced image of d_hat = 0 (render.hpp:77-134)."""
+        cfg = _RenderConfig((C.c_double * 3)(*origin), (C.c_double * 3)(*target), (C.c_double * 3)(*up),
+                            float(fov_deg), int(width), int(height), float(threshold), int(max_steps))
+        rgb = np.zeros((height, width, 3), np.uint8)
+        hit = np.zeros((height, width))
+        st = np.zeros(4, np.int64)
+        secs = np.zeros(1)
+        _check(lib().sd_render(self.h, C.byref(params._c()), mode, C.byref(cfg), _ptr(rgb), _ptr(hit), _ptr(st),
+                               _ptr(secs)))
+        return RenderResult(rgb, hit, int(st[0]), int(st[1]), int(st[2]), int(st[3]), float(secs[0]))
+
+    def grid_benchmark(self, params: SmoothParams, n: int, mode: int = SD_BVH):
+        """d_hat, leaves, far-field counts at the n^3 voxel centres of [0,1]^3
+        (x fastest) and the device seconds (bench.hpp:29-70)."""
+        n3 = n ** 3
+        d, lv, fr, secs = np.zeros(n3), np.zeros(n3, np.int64), np.zeros(n3, np.int64), np.zeros(1)
+        _check(lib().sd_grid_benchmark(self.h, C.byref(params._c()), mode, n, _ptr(d), _ptr(lv), _ptr(fr),
+                                       _ptr(secs)))
+        return d, lv, fr, float(secs[0])
+
     # -- reference caches (SDBV0001 bvh.hpp:190-236, SDWT0001 weights.hpp:700-781) --
     def save_bvh_cache(self, path: str):
         _check(lib().sd_save_bvh_cache(self.h, os.fsencode(path)))
@@ -367,3 +407,40 @@ class Engine:
     def smooth_min_dist_flat(self, q, params: SmoothParams) -> SmoothResults:
         """Batched smooth_min_dist_flat (smooth.hpp:189-198)."""
         return self.query_points(q, params, SD_EXACT, want_c=True, want_counters=True)
+
+
+@dataclass
+class RenderResult:
+    """RenderResult (render.hpp:37-45)."""
+    rgb: np.ndarray    # (H, W, 3) uint8, rows top to bottom
+    hit_t: np.ndarray  # (H, W), -1 on miss
+    leaves: int
+    far_field: int
+    rays: int
+    hits: int
+    seconds: float
+
+    @property
+    def mean_leaves_per_ray(self) -> float:
+        return self.leaves / self.rays if self.rays else 0.0
+
+
+def write_ppm(rgb: np.ndarray, path: str):
+    """write_ppm (render.hpp:139-146)."""
+    rgb = np.ascontiguousarray(rgb, np.uint8)
+    _check(lib().sd_write_ppm(_ptr(rgb), rgb.shape[1], rgb.shape[0], os.fsencode(path)))
+
+
+def write_png(rgb: np.ndarray, path: str):
+    """write_png (render.hpp:172-203)."""
+    rgb = np.ascontiguousarray(rgb, np.uint8)
+    _check(lib().sd_write_png(_ptr(rgb), rgb.shape[1], rgb.shape[0], os.fsencode(path)))
+
+
+def write_grid_csv(d_hat, leaves, far_field, n: int, slab_seconds, path: str):
+    """write_grid_csv (bench.hpp:75-88)."""
+    d = np.ascontiguousarray(d_hat, np.float64)
+    lv = np.ascontiguousarray(leaves, np.int64)
+    fr = np.ascontiguousarray(far_field, np.int64)
+    ss = np.ascontiguousarray(slab_seconds, np.float64)
+    _check(lib().sd_write_grid_csv(_ptr(d), _ptr(lv), _ptr(fr), n, _ptr(ss), os.fsencode(path)))

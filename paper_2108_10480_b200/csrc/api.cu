@@ -3,9 +3,12 @@
 // (kind, polynomial) segments), and query dispatch to K1/K3/K4.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <fstream>
 #include <stdexcept>
+
+#include <zlib.h>
 
 #include "context.h"
 #include "weights_host.h"
@@ -435,6 +438,22 @@ static void dispatch(Ctx& c, const T* q, int64_t Q, const sd_params& p, int mode
     }
     if (mode == SD_BVH && c.N > 0) tree_query<T>(c, q, Q, p, out, st);
     else exact_query<T>(c, q, Q, p, out, st);
+}
+
+// fp64 query points already on the device, converted to the context
+// precision and evaluated (batched callers, callers.cu). Uses c.qT.
+void query_batch_f64(Ctx& c, const double* q, int64_t Q, const sd_params& p, int mode, const FinalizeOut& out,
+                     cudaStream_t st) {
+    if (c.precision == SD_FP32) {
+        float* qf = static_cast<float*>(c.qT.ensure(size_t(std::max<int64_t>(Q, 1)) * 3 * sizeof(float)));
+        if (Q > 0) {
+            convert_queries<float><<<unsigned((3 * Q + 255) / 256), 256, 0, st>>>(q, qf, 3 * Q);
+            check_cuda(cudaGetLastError(), "convert queries");
+        }
+        dispatch<float>(c, qf, Q, p, mode, out, st);
+    } else {
+        dispatch<double>(c, q, Q, p, mode, out, st);
+    }
 }
 
 // Metadata of a table given as bare coefficients: edge valences follow from
@@ -1081,6 +1100,102 @@ int sd_mesh_dist(sd_ctx* c, const double* qxyz, int64_t Vq, const int32_t* qsimp
                        "D2H");
         check_cuda(cudaStreamSynchronize(st), "mesh dist");
         c->last_launches = launches;
+    });
+}
+
+int sd_render(sd_ctx* c, const sd_params* p, int mode, const sd_render_config* cfg, uint8_t* rgb, double* hit_t,
+              int64_t* stats, double* seconds) {
+    return guard([&] {
+        if (!c || !cfg || !rgb || !hit_t) throw ArgError{"NULL argument"};
+        check_params(p);
+        check_ready(*c, mode);
+        if (cfg->width <= 0 || cfg->height <= 0 || int64_t(cfg->width) * cfg->height > (int64_t(1) << 28))
+            throw ArgError{"bad image size"};
+        if (cfg->max_steps < 0 || !(cfg->fov_deg > 0 && cfg->fov_deg < 180)) throw ArgError{"bad render config"};
+        DeviceScope ds(c->device);
+        render_impl(*c, *p, mode, *cfg, rgb, hit_t, stats, seconds);
+    });
+}
+
+int sd_grid_benchmark(sd_ctx* c, const sd_params* p, int mode, int32_t n, double* d_hat, int64_t* leaves,
+                      int64_t* far_field, double* seconds) {
+    return guard([&] {
+        if (!c || !d_hat) throw ArgError{"NULL argument"};
+        check_params(p);
+        check_ready(*c, mode);
+        if (n <= 0 || n > 512) throw ArgError{"resolution must be in 1..512"};
+        DeviceScope ds(c->device);
+        grid_impl(*c, *p, mode, n, d_hat, leaves, far_field, seconds);
+    });
+}
+
+int sd_write_ppm(const uint8_t* rgb, int32_t w, int32_t h, const char* path) {
+    return guard([&] {
+        if (!rgb || !path || w < 0 || h < 0) throw ArgError{"bad arguments"};
+        std::ofstream out(path, std::ios::binary);
+        if (!out) throw ArgError{std::string("cannot open ") + path + " for writing"};
+        out << "P6\n" << w << " " << h << "\n255\n";
+        out.write(reinterpret_cast<const char*>(rgb), std::streamsize(size_t(w) * h * 3));
+        if (!out) throw ArgError{std::string("write failed: ") + path};
+    });
+}
+
+int sd_write_png(const uint8_t* rgb, int32_t w, int32_t h, const char* path) {
+    return guard([&] {
+        if (!rgb || !path || w < 0 || h < 0) throw ArgError{"bad arguments"};
+        std::ofstream out(path, std::ios::binary);
+        if (!out) throw ArgError{std::string("cannot open ") + path + " for writing"};
+        auto chunk = [&](const char type[4], const uint8_t* data, uint32_t len) {
+            auto be32 = [&](uint32_t v) {
+                const uint8_t b[4] = {uint8_t(v >> 24), uint8_t(v >> 16), uint8_t(v >> 8), uint8_t(v)};
+                out.write(reinterpret_cast<const char*>(b), 4);
+            };
+            be32(len);
+            out.write(type, 4);
+            if (len) out.write(reinterpret_cast<const char*>(data), len);
+            uLong crc = crc32(0L, Z_NULL, 0);
+            crc = crc32(crc, reinterpret_cast<const Bytef*>(type), 4);
+            if (len) crc = crc32(crc, data, len);
+            be32(uint32_t(crc));
+        };
+        static const uint8_t sig[8] = {137, 80, 78, 71, 13, 10, 26, 10};
+        out.write(reinterpret_cast<const char*>(sig), 8);
+        uint8_t ihdr[13] = {uint8_t(uint32_t(w) >> 24), uint8_t(uint32_t(w) >> 16), uint8_t(uint32_t(w) >> 8),
+                            uint8_t(w), uint8_t(uint32_t(h) >> 24), uint8_t(uint32_t(h) >> 16),
+                            uint8_t(uint32_t(h) >> 8), uint8_t(h), 8, 2, 0, 0, 0};
+        chunk("IHDR", ihdr, 13);
+        std::vector<uint8_t> raw;
+        raw.reserve(size_t(h) * (1 + 3 * size_t(w)));
+        for (int y = 0; y < h; ++y) {
+            raw.push_back(0);
+            raw.insert(raw.end(), rgb + 3 * size_t(y) * w, rgb + 3 * size_t(y + 1) * w);
+        }
+        uLongf comp_len = compressBound(uLong(raw.size()));
+        std::vector<uint8_t> comp(comp_len);
+        if (compress2(comp.data(), &comp_len, raw.data(), uLong(raw.size()), 6) != Z_OK)
+            throw ArgError{std::string("zlib compression failed for ") + path};
+        chunk("IDAT", comp.data(), uint32_t(comp_len));
+        chunk("IEND", nullptr, 0);
+        if (!out) throw ArgError{std::string("write failed: ") + path};
+    });
+}
+
+int sd_write_grid_csv(const double* d, const int64_t* leaves, const int64_t* far, int32_t n, const double* slab,
+                      const char* path) {
+    return guard([&] {
+        if (!d || !leaves || !far || !slab || !path || n <= 0) throw ArgError{"bad arguments"};
+        std::ofstream out(path);
+        if (!out) throw ArgError{std::string("cannot open ") + path + " for writing"};
+        out << "voxel_index,d_hat,leaves_visited,far_field,slab_time_s\n";
+        char buf[160];
+        const size_t n3 = size_t(n) * n * n;
+        for (size_t idx = 0; idx < n3; ++idx) {
+            const int k = int(idx / (size_t(n) * n));
+            std::snprintf(buf, sizeof buf, "%zu,%.17g,%lld,%lld,%.6g\n", idx, d[idx], static_cast<long long>(leaves[idx]),
+                          static_cast<long long>(far[idx]), slab[k]);
+            out << buf;
+        }
+        if (!out) throw ArgError{std::string("write failed: ") + path};
     });
 }
 

@@ -144,6 +144,12 @@ const int64_t* sort_queries(Ctx& c, const T* q, int64_t Q, const double lo[3], c
 // Tree entry points (bvh.cu)
 void tree_upload(Ctx& c);  // host reference layout -> DeviceTree
 void tree_upload64(Ctx& c, DeviceTree& t);  // same, fp64 records
+void query_batch_f64(Ctx& c, const double* q, int64_t Q, const sd_params& p, int mode, const FinalizeOut& out,
+                     cudaStream_t st);  // api.cu
+void render_impl(Ctx& c, const sd_params& p, int mode, const sd_render_config& cfg, uint8_t* rgb, double* hit_t,
+                 int64_t* stats, double* seconds);  // callers.cu
+void grid_impl(Ctx& c, const sd_params& p, int mode, int n, double* d_hat, int64_t* leaves, int64_t* far,
+               double* seconds);  // callers.cu
 void simplex_query(Ctx& c, const double* corners, const int32_t* dims, int64_t Q, const sd_params& p, int mode,
                    const FinalizeOut& out, cudaStream_t st);
 void split_tables(Ctx& c, DeviceTree& t, int k);  // nodes at depth k of c.tree
