@@ -498,6 +498,72 @@ def run_m2m(args, rank, world, local):
     print(json.dumps(line), flush=True)
 
 
+def run_render(args, rank, world, local):
+    """The reference's batched callers on their acceptance workloads:
+    beta_ablation (bench.hpp:94-145) of the sphere tracer (render.hpp:77-134)
+    on uv_torus (7,200 triangles) in the benchmark frame, 256 x 256, alpha
+    200, alpha_u 1200, beta in {0, 0.2, 0.5} (acceptance [6],
+    T/acceptance.cpp:367-390), and grid_benchmark (bench.hpp:29-70) at 64^3
+    on the same mesh. GPU: sd_render / sd_grid_benchmark (device time of
+    the whole call); CPU: the oracle port's render on the host threads."""
+    import torch
+    import paper_2108_10480_b200 as sd
+    from paper_2108_10480_b200 import callers, configs
+    torch.cuda.set_device(local)
+    V, T = configs.torus(0.35, 0.15, 60, 60, jitter=False)
+    V = configs.benchmark_frame(V)
+    K = np.full(len(T), 2, np.uint8)
+    e = V.max(0) - V.min(0)
+    diag = float(np.sqrt((e[0] * e[0] + e[1] * e[1]) + e[2] * e[2]))
+    eng = sd.Engine(local, sd.SD_FP64 if args.fp64 else sd.SD_FP32)
+    eng.set_geometry(V, T, K)
+    eng.build_weights()
+    eng.build_bvh(sd.SD_BVH_LBVH)
+    P = sd.SmoothParams(alpha=200.0, alpha_u=1200.0)
+    for _ in range(max(1, args.warmup)):
+        eng.render(sd.SmoothParams(alpha=200.0, alpha_u=1200.0, beta=0.2))
+    with ClockSampler(local) as clk:
+        rows = [callers.beta_ablation(eng, P, [0.0, 0.2, 0.5], diag) for _ in range(max(1, args.steps))]
+        grids = [eng.grid_benchmark(sd.SmoothParams(alpha=100.0, beta=0.3), 64) for _ in range(max(1, args.steps))]
+    # per-beta median over the repetitions
+    med = []
+    for k, beta in enumerate((0.0, 0.2, 0.5)):
+        rs = [r[k] for r in rows]
+        secs = float(np.median([r.seconds for r in rs]))
+        med.append({"beta": beta, "seconds": secs, "mean_disp_rel": rs[0].mean_disp_rel,
+                    "max_disp_rel": rs[0].max_disp_rel, "mismatched_hits": rs[0].mismatched_hits,
+                    "leaves": rs[0].leaves})
+    for m in med:
+        m["speedup_vs_beta0"] = med[0]["seconds"] / m["seconds"]
+    grid_s = float(np.median([g[3] for g in grids]))
+    cpu = None
+    if not args.no_cpu:
+        import oracle as O
+        O.build()
+        threads = O.hardware_threads()
+        wt = eng.weight_table()
+        om = O.Mesh.from_arrays(V, T, K)
+        ow = O.Weights.from_table(O.WeightTable(wt.A, wt.sup_wtilde, wt.edge_a, wt.tri_stored, wt.poly_index))
+        ot = O.Tree.from_nodes(eng.export_bvh())
+        r = O.render(om, ow, ot, O.Params(alpha=200.0, alpha_u=1200.0, beta=0.2), O.render_config(), threads)
+        g = eng.render(sd.SmoothParams(alpha=200.0, alpha_u=1200.0, beta=0.2))
+        cpu = {"value": r.seconds, "unit": "s", "cores": threads, "kind": "port",
+               "sample": "the beta = 0.2 render (256 x 256) on the same tree and weights, fp64 oracle port",
+               "hits": r.hits, "gpu_hits": g.hits,
+               "hit_mismatch": int(((r.hit_t >= 0) != (g.hit_t >= 0)).sum())}
+    line = {"metric": "sphere-traced render time (256x256, beta 0.2) -- acceptance [6] workload", "value": med[1]["seconds"],
+            "unit": "s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * med[1]["seconds"],
+            "higher_is_better": False, "scaling": "none", "vs_baseline": None,
+            "dtype": "f64" if args.fp64 else "f32", "data": "synthetic (uv_torus 60x60, benchmark frame)",
+            "config": {"workload": "render.hpp:77-134 via sd_render, beta_ablation {0, 0.2, 0.5}, alpha 200, "
+                                   "alpha_u 1200, GPU LBVH; grid_benchmark 64^3 alpha 100 beta 0.3"},
+            "ablation": med, "acceptance_6": {"speedup_beta02": med[1]["speedup_vs_beta0"],
+                                              "pass": med[1]["speedup_vs_beta0"] >= 5.0
+                                              and med[1]["mean_disp_rel"] < 0.04 and med[2]["mean_disp_rel"] < 0.04},
+            "grid_64_seconds": grid_s, "cpu_baseline": cpu, "clocks": clk.summary()}
+    print(json.dumps(line), flush=True)
+
+
 def run_ours(args, rank, world, local):
     import torch
     import paper_2108_10480_b200 as sd
@@ -648,6 +714,7 @@ def main():
     ap.add_argument("--fp64", action="store_true", help="fp64 arithmetic for --config 2")
     ap.add_argument("--m2m", action="store_true", help="mesh-to-mesh evaluations of the paper's timing table rows")
     ap.add_argument("--rows", default="", help="comma-separated sim_rows names for --m2m (default: all)")
+    ap.add_argument("--render", action="store_true", help="sphere tracer beta ablation + grid benchmark (callers)")
     ap.add_argument("--alpha", type=float, default=None, help="alpha for --config 3 (10, 100 or 1000)")
     args = ap.parse_args()
     rank, world, local = dist_env()
@@ -658,6 +725,9 @@ def main():
     elif args.m2m:
         if rank == 0:
             run_m2m(args, rank, world, local)
+    elif args.render:
+        if rank == 0:
+            run_render(args, rank, world, local)
     else:
         run_ours(args, rank, world, local)
 

@@ -118,7 +118,7 @@ def cfg2(nq: int = 262144, seed: int = 2001, block: int = 0):
     return w, q
 
 
-def torus(major=1.0, minor=0.3, nu=512, nv=256, seed=3001):
+def torus(major=1.0, minor=0.3, nu=512, nv=256, seed=3001, jitter=True):
     """uv_torus (shapes.hpp:67-89) + N(0, (0.1 mean edge)^2) jitter."""
     i, j = np.meshgrid(np.arange(nu), np.arange(nv), indexing="ij")
     u, vv = 2 * np.pi * i / nu, 2 * np.pi * j / nv
@@ -131,8 +131,19 @@ def torus(major=1.0, minor=0.3, nu=512, nv=256, seed=3001):
     e = np.concatenate([T[:, [0, 1]], T[:, [1, 2]], T[:, [2, 0]]])
     e = np.unique(np.sort(e, 1), axis=0)
     mel = np.linalg.norm(V[e[:, 0]] - V[e[:, 1]], axis=1).mean()
-    V = V + np.random.default_rng(seed).normal(0.0, 0.1 * mel, V.shape)
+    if jitter:
+        V = V + np.random.default_rng(seed).normal(0.0, 0.1 * mel, V.shape)
     return V, T
+
+
+def benchmark_frame(V: np.ndarray) -> np.ndarray:
+    """normalize_to_benchmark_frame (mesh.hpp:126-135): scale 0.5 / bbox
+    diagonal, bbox centre to (0.5, 0.5, 0.5)."""
+    lo, hi = V.min(0), V.max(0)
+    e = hi - lo
+    diag = math.sqrt((e[0] * e[0] + e[1] * e[1]) + e[2] * e[2])
+    scale = 0.5 / diag if diag > 0 else 1.0
+    return scale * V + (0.5 - scale * (0.5 * (lo + hi)))
 
 
 def quantize(x: np.ndarray) -> np.ndarray:

@@ -101,7 +101,7 @@ def test_render_single_point_matches_oracle(sd, oracle, prec):  # test_render.cp
     assert r.hits > 0 and 2.4 <= r.hit_t[32, 32] <= 3.01 and r.hit_t[0, 0] == -1.0 and r.rgb[0, 0, 0] == 0
     assert (r.hit_t >= 0).sum() == r.hits == ref.hits
     assert np.array_equal(r.hit_t >= 0, ref.hit_t >= 0)
-    assert np.abs(r.hit_t - ref.hit_t).max() <= 1e-9
+    assert np.abs(r.hit_t - ref.hit_t).max() <= (1e-9 if prec == 1 else 1e-5)  # fp32 d_hat: 1e-5 relative
     assert np.abs(r.rgb.astype(int) - ref.rgb.astype(int)).max() <= (0 if prec == 1 else 1)
 
 
