@@ -541,7 +541,8 @@ int sd_destroy(sd_ctx* c) {
         {
             DeviceScope ds(c->device);
             if (c->stream) cudaStreamDestroy(c->stream);
-            c->stream = nullptr;
+            if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+            c->stream = c->copy_stream = nullptr;
         }
         delete c;
     });
@@ -882,8 +883,7 @@ int sd_query_points(sd_ctx* c, const double* q, int64_t Q, const sd_params* p, i
         if (Q == 0) return;
         DeviceScope ds(c->device);
         cudaStream_t st = c->stream;
-        double* qd = c->qd.ensure(size_t(Q) * 3 * sizeof(double)) ? c->qd.as<double>() : nullptr;
-        check_cuda(cudaMemcpyAsync(qd, q, size_t(Q) * 3 * sizeof(double), cudaMemcpyHostToDevice, st), "H2D queries");
+        double* qd = static_cast<double*>(c->qd.ensure(size_t(Q) * 3 * sizeof(double)));
         FinalizeOut out;
         out.d_hat = static_cast<double*>(c->out_d.ensure(size_t(Q) * sizeof(double)));
         if (o->grad) out.grad = static_cast<double*>(c->out_g.ensure(size_t(Q) * 3 * sizeof(double)));
@@ -892,28 +892,70 @@ int sd_query_points(sd_ctx* c, const double* q, int64_t Q, const sd_params* p, i
         if (o->leaves) out.leaves = static_cast<int64_t*>(c->out_l.ensure(size_t(Q) * sizeof(int64_t)));
         if (o->far_field) out.far_field = static_cast<int64_t*>(c->out_f.ensure(size_t(Q) * sizeof(int64_t)));
         if (o->decision_hash) out.hash = static_cast<uint64_t*>(c->out_h.ensure(size_t(Q) * sizeof(uint64_t)));
-        int64_t conv = 0;
-        if (c->precision == SD_FP32) {
-            float* qf = static_cast<float*>(c->qT.ensure(size_t(Q) * 3 * sizeof(float)));
-            convert_queries<float><<<unsigned((3 * Q + 255) / 256), 256, 0, st>>>(qd, qf, 3 * Q);
-            check_cuda(cudaGetLastError(), "convert queries");
-            conv = 1;
-            dispatch<float>(*c, qf, Q, *p, mode, out, st);
-        } else {
-            dispatch<double>(*c, qd, Q, *p, mode, out, st);
+        float* qf = c->precision == SD_FP32 ? static_cast<float*>(c->qT.ensure(size_t(Q) * 3 * sizeof(float))) : nullptr;
+        // Optional chunk pipeline (SDGPU_PIPELINE=1, batches >= 2^17): every
+        // chunk's H2D is queued on the copy stream up front, chunk k computes
+        // on the context stream once its queries landed, and its results go
+        // back on the copy stream while chunk k+1 computes. Off by default:
+        // on cfg2 the transfers are ~4 % of the step and four quarter-size
+        // exact launches lose more than the overlap gains (e2e 6.6e11 vs
+        // 7.05e11 pair-evals/s unpipelined).
+        const char* pe = std::getenv("SDGPU_PIPELINE");
+        const int chunks = (Q >= (int64_t(1) << 17) && pe && *pe == '1') ? 4 : 1;
+        cudaStream_t cs = st;
+        if (chunks > 1) {
+            if (!c->copy_stream) check_cuda(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking), "stream");
+            cs = c->copy_stream;
         }
-        c->last_launches += conv;
-        auto d2h = [&](void* dst, const void* src, size_t bytes) {
-            if (dst) check_cuda(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st), "D2H results");
-        };
-        d2h(o->d_hat, out.d_hat, size_t(Q) * sizeof(double));
-        d2h(o->grad, out.grad, size_t(Q) * 3 * sizeof(double));
-        d2h(o->c, out.c, size_t(Q) * sizeof(double));
-        d2h(o->grad_c, out.grad_c, size_t(Q) * 3 * sizeof(double));
-        d2h(o->leaves, out.leaves, size_t(Q) * sizeof(int64_t));
-        d2h(o->far_field, out.far_field, size_t(Q) * sizeof(int64_t));
-        d2h(o->decision_hash, out.hash, size_t(Q) * sizeof(uint64_t));
+        std::vector<cudaEvent_t> ev(size_t(2 * chunks));
+        for (auto& e : ev) check_cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+        const int64_t per = (Q + chunks - 1) / chunks;
+        for (int k = 0; k < chunks; ++k) {
+            const int64_t off = k * per, n = std::min(Q, off + per) - off;
+            check_cuda(cudaMemcpyAsync(qd + 3 * off, q + 3 * off, size_t(n) * 3 * sizeof(double), cudaMemcpyHostToDevice,
+                                       cs),
+                       "H2D queries");
+            check_cuda(cudaEventRecord(ev[2 * k], cs), "event");
+        }
+        int64_t launches = 0;
+        auto shift = [](auto* ptr, int64_t by) { return ptr ? ptr + by : ptr; };
+        for (int k = 0; k < chunks; ++k) {
+            const int64_t off = k * per, n = std::min(Q, off + per) - off;
+            check_cuda(cudaStreamWaitEvent(st, ev[2 * k], 0), "wait");
+            FinalizeOut oc = out;
+            oc.d_hat = shift(out.d_hat, off);
+            oc.grad = shift(out.grad, 3 * off);
+            oc.c = shift(out.c, off);
+            oc.grad_c = shift(out.grad_c, 3 * off);
+            oc.leaves = shift(out.leaves, off);
+            oc.far_field = shift(out.far_field, off);
+            oc.hash = shift(out.hash, off);
+            if (qf) {
+                convert_queries<float><<<unsigned((3 * n + 255) / 256), 256, 0, st>>>(qd + 3 * off, qf + 3 * off, 3 * n);
+                check_cuda(cudaGetLastError(), "convert queries");
+                dispatch<float>(*c, qf + 3 * off, n, *p, mode, oc, st);
+                ++launches;
+            } else {
+                dispatch<double>(*c, qd + 3 * off, n, *p, mode, oc, st);
+            }
+            launches += c->last_launches;
+            check_cuda(cudaEventRecord(ev[2 * k + 1], st), "event");
+            check_cuda(cudaStreamWaitEvent(cs, ev[2 * k + 1], 0), "wait");
+            auto d2h = [&](void* dst, const void* src, size_t bytes) {
+                if (dst) check_cuda(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, cs), "D2H results");
+            };
+            d2h(o->d_hat ? o->d_hat + off : nullptr, oc.d_hat, size_t(n) * sizeof(double));
+            d2h(o->grad ? o->grad + 3 * off : nullptr, oc.grad, size_t(n) * 3 * sizeof(double));
+            d2h(o->c ? o->c + off : nullptr, oc.c, size_t(n) * sizeof(double));
+            d2h(o->grad_c ? o->grad_c + 3 * off : nullptr, oc.grad_c, size_t(n) * 3 * sizeof(double));
+            d2h(o->leaves ? o->leaves + off : nullptr, oc.leaves, size_t(n) * sizeof(int64_t));
+            d2h(o->far_field ? o->far_field + off : nullptr, oc.far_field, size_t(n) * sizeof(int64_t));
+            d2h(o->decision_hash ? o->decision_hash + off : nullptr, oc.hash, size_t(n) * sizeof(uint64_t));
+        }
+        check_cuda(cudaStreamSynchronize(cs), "query");
         check_cuda(cudaStreamSynchronize(st), "query");
+        for (auto& e : ev) cudaEventDestroy(e);
+        c->last_launches = launches;
     });
 }
 

@@ -81,7 +81,8 @@ struct DeviceTree {
 struct Ctx {
     int device = 0;
     int precision = SD_FP32;
-    cudaStream_t stream = nullptr;  // library-owned stream for host-buffer calls
+    cudaStream_t stream = nullptr;       // library-owned stream for host-buffer calls
+    cudaStream_t copy_stream = nullptr;  // H2D / D2H of pipelined host-buffer batches
 
     // geometry (vertices already rounded to float in SD_FP32)
     std::vector<double> xyz;
