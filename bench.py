@@ -651,8 +651,10 @@ def run_ours(args, rank, world, local):
     if rank == 0:
         achieved = pairs_per_rank * FLOPS_PER_EDGE_PAIR / (ms_max * 1e-3) / 1e12
         # dram read + write of the dominant launch, from the committed ncu
-        # capture of this workload (cfg2 fp32): profiles/r1_v3_exact_edge_details.csv
-        traffic = 1.166e8 if (args.config == 2 and not fp64) else None
+        # capture of this workload (cfg2 fp32, tile-bound kernel):
+        # profiles/r1_v5_exact_edge_details.csv (133.5 MB read + 68.9 MB written,
+        # the fp64 per-query partial state of 12 primitive splits)
+        traffic = 2.024e8 if (args.config == 2 and not fp64) else None
         roof = {"bound": "fp64-fma" if fp64 else "fp32-fma", "achieved": achieved, "unit": "TFLOP/s",
                 "traffic": traffic, "traffic_unit": "bytes per launch (ncu dram__bytes_read+write)",
                 "algorithmic_bytes": Q * 12 + N * 48,
