@@ -582,6 +582,38 @@ __global__ void __launch_bounds__(kTravThreads) packet_kernel(const __grid_const
     if (nre) atomicAdd(a.rechecks, nre);
 }
 
+// Exact leaf term of one lane (smooth.hpp:51-61); the record is the same
+// for every lane of the warp.
+template <class T, bool HASH>
+__device__ __forceinline__ void leaf_visit(const TraverseArgs<T>& a, const Poly<T>* polys, int32_t id, int32_t link,
+                                           T qx, T qy, T qz, Acc<T>& acc, int64_t& nleaf, uint64_t& h) {
+    const int slot = -link - 1;  // exact leaf: the record is the same for every lane
+    const int meta = a.leafmeta[slot];
+    const int kind = meta & 3, poly = (meta >> 2) - 1;
+    T rec[kRecTri];
+    using V = typename Vec4<T>::type;
+    const V* src = reinterpret_cast<const V*>(a.leafrec + size_t(slot) * kRecTri);
+    if (kind == 0) {
+        for (int j = 0; j < kRecPoint * int(sizeof(T)) / int(sizeof(V)); ++j) reinterpret_cast<V*>(rec)[j] = src[j];
+        acc.m -= a.ph.lw_unit;
+        point_term(a.ph, qx, qy, qz, rec[0], rec[1], rec[2], acc);
+        acc.m += a.ph.lw_unit;
+    } else if (kind == 1) {
+#pragma unroll
+        for (int j = 0; j < kRecEdge * int(sizeof(T)) / int(sizeof(V)); ++j) reinterpret_cast<V*>(rec)[j] = src[j];
+        if (poly >= 0) edge_term<T, true, false>(a.ph, polys[poly], qx, qy, qz, rec, acc);
+        else unit_term<T, 1>(a.ph, polys[0], qx, qy, qz, rec, acc);
+    } else {
+#pragma unroll
+        for (int j = 0; j < kRecTri * int(sizeof(T)) / int(sizeof(V)); ++j) reinterpret_cast<V*>(rec)[j] = src[j];
+        if (poly >= 0) tri_term<T, true, false>(a.ph, polys[a.ne + poly], qx, qy, qz, rec, acc);
+        else unit_term<T, 2>(a.ph, polys[0], qx, qy, qz, rec, acc);
+    }
+    ++nleaf;
+    if constexpr (HASH) h += decision_mix(uint64_t(id), 2);
+}
+
+
 // Barnes-Hut admissibility of box b for query point q (bvh.hpp:105-111,
 // 185-187): fp32 decides outside a 1e-5 relative band, fp64 re-decides in
 // the reference rounding inside it. On "far" also returns d_B, 1/d_B and
@@ -637,30 +669,7 @@ __device__ __forceinline__ bool visit(const TraverseArgs<T>& a, const Poly<T>* p
         }
     }
     if (link >= 0) return true;
-    const int slot = -link - 1;  // exact leaf: the record is the same for every lane
-    const int meta = a.leafmeta[slot];
-    const int kind = meta & 3, poly = (meta >> 2) - 1;
-    T rec[kRecTri];
-    using V = typename Vec4<T>::type;
-    const V* src = reinterpret_cast<const V*>(a.leafrec + size_t(slot) * kRecTri);
-    if (kind == 0) {
-        for (int j = 0; j < kRecPoint * int(sizeof(T)) / int(sizeof(V)); ++j) reinterpret_cast<V*>(rec)[j] = src[j];
-        acc.m -= a.ph.lw_unit;
-        point_term(a.ph, qx, qy, qz, rec[0], rec[1], rec[2], acc);
-        acc.m += a.ph.lw_unit;
-    } else if (kind == 1) {
-#pragma unroll
-        for (int j = 0; j < kRecEdge * int(sizeof(T)) / int(sizeof(V)); ++j) reinterpret_cast<V*>(rec)[j] = src[j];
-        if (poly >= 0) edge_term<T, true, false>(a.ph, polys[poly], qx, qy, qz, rec, acc);
-        else unit_term<T, 1>(a.ph, polys[0], qx, qy, qz, rec, acc);
-    } else {
-#pragma unroll
-        for (int j = 0; j < kRecTri * int(sizeof(T)) / int(sizeof(V)); ++j) reinterpret_cast<V*>(rec)[j] = src[j];
-        if (poly >= 0) tri_term<T, true, false>(a.ph, polys[a.ne + poly], qx, qy, qz, rec, acc);
-        else unit_term<T, 2>(a.ph, polys[0], qx, qy, qz, rec, acc);
-    }
-    ++nleaf;
-    if constexpr (HASH) h += decision_mix(uint64_t(id), 2);
+    leaf_visit<T, HASH>(a, polys, id, link, qx, qy, qz, acc, nleaf, h);
     return false;
 }
 
@@ -691,6 +700,19 @@ struct PointVisit {
             if constexpr (HASH) h += decision_mix(uint64_t(id), 1);
         }
         return true;
+    }
+
+    // Both children of a node (K3's child-pair step): two scalar tests. (A
+    // packed fp32x2 variant with a branch-free far-field path measured
+    // slower on cfg4 -- 33.0 ms vs 29.7 ms: 80 registers and an exponential
+    // for every child -- and was dropped.)
+    template <bool HASH>
+    __device__ __forceinline__ void visit_pair(const TraverseArgs<T>& a, const Poly<T>* polys, const NodeT<T>& bl,
+                                               const NodeT<T>& br, int32_t lid, int32_t rid, T lgl, T lgr,
+                                               Acc<T>& acc, int64_t& nleaf, int64_t& nfar, uint64_t& h,
+                                               unsigned long long& nre, bool& dl, bool& dr) const {
+        dl = visit<HASH>(a, polys, bl, lid, lgl, acc, nleaf, nfar, h, nre);
+        dr = visit<HASH>(a, polys, br, rid, lgr, acc, nleaf, nfar, h, nre);
     }
 };
 

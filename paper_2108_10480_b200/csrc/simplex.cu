@@ -544,6 +544,15 @@ struct SimplexVisit {
         if constexpr (HASH) h += decision_mix(uint64_t(id), 2);
         return false;
     }
+    template <bool HASH>
+    __device__ __forceinline__ void visit_pair(const TraverseArgs<double>& a, const Poly<double>* polys,
+                                               const NodeT<double>& bl, const NodeT<double>& br, int32_t lid,
+                                               int32_t rid, double lgl, double lgr, Acc<double>& acc, int64_t& nleaf,
+                                               int64_t& nfar, uint64_t& h, unsigned long long& nre, bool& dl,
+                                               bool& dr) const {
+        dl = visit<HASH>(a, polys, bl, lid, lgl, acc, nleaf, nfar, h, nre);
+        dr = visit<HASH>(a, polys, br, rid, lgr, acc, nleaf, nfar, h, nre);
+    }
 };
 
 // Exact path: thread = query, blockIdx.y = primitive range (index order);

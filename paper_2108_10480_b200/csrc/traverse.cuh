@@ -173,10 +173,8 @@ __global__ void __launch_bounds__(kTravThreads) pair_kernel(const __grid_constan
         // pair record into L1 while this one is being processed
         if (lane == 0) asm volatile("prefetch.global.L1 [%0];" ::"l"(a.pairs + lid));
         bool dl = false, dr = false;
-        if ((mask >> lane) & 1u) {
-            dl = qv.template visit<HASH>(a, polys, bl, lid, lgl, acc, nleaf, nfar, h, nre);
-            dr = qv.template visit<HASH>(a, polys, br, rid, lgr, acc, nleaf, nfar, h, nre);
-        }
+        if ((mask >> lane) & 1u)
+            qv.template visit_pair<HASH>(a, polys, bl, br, lid, rid, lgl, lgr, acc, nleaf, nfar, h, nre, dl, dr);
         const unsigned DL = __ballot_sync(0xffffffffu, dl), DR = __ballot_sync(0xffffffffu, dr);
         int32_t llink, rlink;
         memcpy(&llink, &bl.v[7], sizeof(int32_t));
