@@ -26,6 +26,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <string>
 #include <vector>
 
 #include "traverse.cuh"
@@ -220,11 +221,86 @@ __device__ __forceinline__ void clamp_domain(Bary& b, int dim) {
     }
 }
 
-__device__ __noinline__ GPair simplex_distance_qp(const Geom& f, const Geom& g) {
-    const int nf = f.dim == 0 ? 1 : (f.dim == 1 ? 3 : 7);
-    const int ng = g.dim == 0 ? 1 : (g.dim == 1 ? 3 : 7);
+// One candidate of the face enumeration: face i of f against face j of g
+// (the loop body of exact.hpp:196-311). Returns false when the pair is
+// skipped (k > 3, singular restriction, infeasible); otherwise the clamped
+// barycentrics, points and squared distance.
+__device__ __forceinline__ bool qp_candidate(const Geom& f, const Geom& g, int i, int j, Bary& fb, Bary& gb, D3& pf,
+                                             D3& pg, double& d2) {
     const D3 fe1 = f.c1 - f.c0, fe2 = f.c2 - f.c0;
     const D3 ge1 = g.c1 - g.c0, ge2 = g.c2 - g.c0;
+    const Face Ff = face_of(f.dim, i);
+    const Face Fg = face_of(g.dim, j);
+    const int k = Ff.k + Fg.k;
+    if (k > 3) return false;
+    D3 fd0 = D3{0, 0, 0}, fd1 = D3{0, 0, 0};
+    if (Ff.k >= 1) fd0 = Ff.d00 * fe1 + Ff.d01 * fe2;
+    if (Ff.k >= 2) fd1 = Ff.d10 * fe1 + Ff.d11 * fe2;
+    const D3 f0 = f.at(bary_at(Ff, 0.0, 0.0));
+    D3 gd0 = D3{0, 0, 0}, gd1 = D3{0, 0, 0};
+    if (Fg.k >= 1) gd0 = -(Fg.d00 * ge1 + Fg.d01 * ge2);
+    if (Fg.k >= 2) gd1 = -(Fg.d10 * ge1 + Fg.d11 * ge2);
+    // cols = [f directions..., g directions...]
+    const D3 c0 = Ff.k >= 1 ? fd0 : gd0;
+    const D3 c1 = Ff.k >= 2 ? fd1 : (Ff.k == 1 ? gd0 : gd1);
+    const D3 c2 = Ff.k == 2 ? gd0 : gd1;
+    const D3 d0 = f0 - g.at(bary_at(Fg, 0.0, 0.0));
+    double z0 = 0.0, z1 = 0.0, z2 = 0.0;
+    if (k == 1) {
+        const double m = sqnorm(c0);
+        if (m <= 0.0) return false;
+        z0 = -dot(c0, d0) / m;
+    } else if (k == 2) {
+        const double a11 = sqnorm(c0), a22 = sqnorm(c1);
+        const double a12 = dot(c0, c1);
+        const double det = a11 * a22 - a12 * a12;
+        if (det <= 1e-12 * a11 * a22) return false;
+        const double r1 = -dot(c0, d0), r2 = -dot(c1, d0);
+        z0 = (a22 * r1 - a12 * r2) / det;
+        z1 = (a11 * r2 - a12 * r1) / det;
+    } else if (k == 3) {
+        const double m00 = dot(c0, c0), m01 = dot(c0, c1), m02 = dot(c0, c2);
+        const double m10 = dot(c1, c0), m11 = dot(c1, c1), m12 = dot(c1, c2);
+        const double m20 = dot(c2, c0), m21 = dot(c2, c1), m22 = dot(c2, c2);
+        // Eigen determinant: first-row cofactor expansion
+        const double det = m00 * (m11 * m22 - m12 * m21) - m01 * (m10 * m22 - m12 * m20) +
+                           m02 * (m10 * m21 - m11 * m20);
+        const double scale = m00 * m11 * m22;
+        if (fabs(det) <= 1e-12 * scale) return false;
+        // Eigen inverse: cofactor_3x3(i, j) = m(i1,j1) m(i2,j2) - m(i1,j2) m(i2,j1)
+        const double k00 = m11 * m22 - m12 * m21, k10 = m21 * m02 - m22 * m01, k20 = m01 * m12 - m02 * m11;
+        const double idet = 1.0 / (k00 * m00 + k10 * m10 + k20 * m20);
+        const double r00 = k00 * idet, r01 = k10 * idet, r02 = k20 * idet;
+        const double r10 = (m12 * m20 - m10 * m22) * idet;  // cofactor (0,1)
+        const double r11 = (m22 * m00 - m20 * m02) * idet;  // cofactor (1,1)
+        const double r12 = (m02 * m10 - m00 * m12) * idet;  // cofactor (2,1)
+        const double r20 = (m10 * m21 - m11 * m20) * idet;  // cofactor (0,2)
+        const double r21 = (m20 * m01 - m21 * m00) * idet;  // cofactor (1,2)
+        const double r22 = (m00 * m11 - m01 * m10) * idet;  // cofactor (2,2)
+        const double h0 = -dot(c0, d0), h1 = -dot(c1, d0), h2 = -dot(c2, d0);
+        z0 = r00 * h0 + r01 * h1 + r02 * h2;
+        z1 = r10 * h0 + r11 * h1 + r12 * h2;
+        z2 = r20 * h0 + r21 * h1 + r22 * h2;
+    }
+    fb = bary_at(Ff, z0, z1);
+    const double gz0 = Ff.k == 0 ? z0 : (Ff.k == 1 ? z1 : z2);
+    const double gz1 = Ff.k == 0 ? z1 : z2;
+    gb = bary_at(Fg, gz0, gz1);
+    if (!feasible(fb, f.dim) || !feasible(gb, g.dim)) return false;
+    clamp_domain(fb, f.dim);
+    clamp_domain(gb, g.dim);
+    pf = f.at(fb);
+    pg = g.at(gb);
+    d2 = sqnorm(pg - pf);
+    return true;
+}
+
+__device__ __forceinline__ int num_faces(int dim) { return dim == 0 ? 1 : (dim == 1 ? 3 : 7); }
+
+// exact.hpp:158-313, serial: the first strictly best candidate in
+// enumeration order (f faces outer, g faces inner).
+__device__ __noinline__ GPair simplex_distance_qp(const Geom& f, const Geom& g) {
+    const int nf = num_faces(f.dim), ng = num_faces(g.dim);
     GPair best;
     best.phi = best.lam = Bary{0.0, 0.0};
     best.pf = best.pg = D3{0.0, 0.0, 0.0};
@@ -232,79 +308,12 @@ __device__ __noinline__ GPair simplex_distance_qp(const Geom& f, const Geom& g) 
     bool have = false;
 #pragma unroll 1
     for (int i = 0; i < nf; ++i) {
-        const Face Ff = face_of(f.dim, i);
-        D3 fd0 = D3{0, 0, 0}, fd1 = D3{0, 0, 0};
-        if (Ff.k >= 1) fd0 = Ff.d00 * fe1 + Ff.d01 * fe2;
-        if (Ff.k >= 2) fd1 = Ff.d10 * fe1 + Ff.d11 * fe2;
-        const D3 f0 = f.at(bary_at(Ff, 0.0, 0.0));
 #pragma unroll 1
         for (int j = 0; j < ng; ++j) {
-            const Face Fg = face_of(g.dim, j);
-            const int k = Ff.k + Fg.k;
-            if (k > 3) continue;
-            D3 gd0 = D3{0, 0, 0}, gd1 = D3{0, 0, 0};
-            if (Fg.k >= 1) gd0 = -(Fg.d00 * ge1 + Fg.d01 * ge2);
-            if (Fg.k >= 2) gd1 = -(Fg.d10 * ge1 + Fg.d11 * ge2);
-            // cols = [f directions..., g directions...]
-            const D3 c0 = Ff.k >= 1 ? fd0 : gd0;
-            const D3 c1 = Ff.k >= 2 ? fd1 : (Ff.k == 1 ? gd0 : gd1);
-            const D3 c2 = Ff.k == 2 ? gd0 : gd1;
-            const D3 d0 = f0 - g.at(bary_at(Fg, 0.0, 0.0));
-            double z0 = 0.0, z1 = 0.0, z2 = 0.0;
-            bool solved = true;
-            if (k == 1) {
-                const double m = sqnorm(c0);
-                if (m <= 0.0) solved = false;
-                else z0 = -dot(c0, d0) / m;
-            } else if (k == 2) {
-                const double a11 = sqnorm(c0), a22 = sqnorm(c1);
-                const double a12 = dot(c0, c1);
-                const double det = a11 * a22 - a12 * a12;
-                if (det <= 1e-12 * a11 * a22) {
-                    solved = false;
-                } else {
-                    const double r1 = -dot(c0, d0), r2 = -dot(c1, d0);
-                    z0 = (a22 * r1 - a12 * r2) / det;
-                    z1 = (a11 * r2 - a12 * r1) / det;
-                }
-            } else if (k == 3) {
-                const double m00 = dot(c0, c0), m01 = dot(c0, c1), m02 = dot(c0, c2);
-                const double m10 = dot(c1, c0), m11 = dot(c1, c1), m12 = dot(c1, c2);
-                const double m20 = dot(c2, c0), m21 = dot(c2, c1), m22 = dot(c2, c2);
-                // Eigen determinant: first-row cofactor expansion
-                const double det = m00 * (m11 * m22 - m12 * m21) - m01 * (m10 * m22 - m12 * m20) +
-                                   m02 * (m10 * m21 - m11 * m20);
-                const double scale = m00 * m11 * m22;
-                if (fabs(det) <= 1e-12 * scale) {
-                    solved = false;
-                } else {
-                    // Eigen inverse: cofactor_3x3(i, j) = m(i1,j1) m(i2,j2) - m(i1,j2) m(i2,j1)
-                    const double k00 = m11 * m22 - m12 * m21, k10 = m21 * m02 - m22 * m01,
-                                 k20 = m01 * m12 - m02 * m11;
-                    const double idet = 1.0 / (k00 * m00 + k10 * m10 + k20 * m20);
-                    const double r00 = k00 * idet, r01 = k10 * idet, r02 = k20 * idet;
-                    const double r10 = (m12 * m20 - m10 * m22) * idet;  // cofactor (0,1)
-                    const double r11 = (m22 * m00 - m20 * m02) * idet;  // cofactor (1,1)
-                    const double r12 = (m02 * m10 - m00 * m12) * idet;  // cofactor (2,1)
-                    const double r20 = (m10 * m21 - m11 * m20) * idet;  // cofactor (0,2)
-                    const double r21 = (m20 * m01 - m21 * m00) * idet;  // cofactor (1,2)
-                    const double r22 = (m00 * m11 - m01 * m10) * idet;  // cofactor (2,2)
-                    const double h0 = -dot(c0, d0), h1 = -dot(c1, d0), h2 = -dot(c2, d0);
-                    z0 = r00 * h0 + r01 * h1 + r02 * h2;
-                    z1 = r10 * h0 + r11 * h1 + r12 * h2;
-                    z2 = r20 * h0 + r21 * h1 + r22 * h2;
-                }
-            }
-            if (!solved && k > 0) continue;
-            Bary fb = bary_at(Ff, z0, z1);
-            const double gz0 = Ff.k == 0 ? z0 : (Ff.k == 1 ? z1 : z2);
-            const double gz1 = Ff.k == 0 ? z1 : z2;
-            Bary gb = bary_at(Fg, gz0, gz1);
-            if (!feasible(fb, f.dim) || !feasible(gb, g.dim)) continue;
-            clamp_domain(fb, f.dim);
-            clamp_domain(gb, g.dim);
-            const D3 pf = f.at(fb), pg = g.at(gb);
-            const double d2 = sqnorm(pg - pf);
+            Bary fb, gb;
+            D3 pf, pg;
+            double d2;
+            if (!qp_candidate(f, g, i, j, fb, gb, pf, pg, d2)) continue;
             if (!have || d2 < best_d2) {
                 have = true;
                 best_d2 = d2;
@@ -319,8 +328,68 @@ __device__ __noinline__ GPair simplex_distance_qp(const Geom& f, const Geom& g) 
     return best;
 }
 
-// exact.hpp:342-367
-__device__ GPair simplex_distance(const Geom& f, const Geom& g) {
+// The same QP with the candidates spread over a group of GW lanes (8, 16
+// or 32; all lanes of the group hold the same f, g): the minimum over (d2,
+// enumeration index) is exactly the serial scan's first strictly best
+// candidate. Shuffles use the group's mask, so groups of a warp may run
+// different QPs at the same time.
+template <int GW>
+__device__ __forceinline__ unsigned group_mask() {
+    const unsigned lane = threadIdx.x & 31u;
+    return GW == 32 ? 0xffffffffu : (((1u << GW) - 1u) << (lane & ~unsigned(GW - 1)));
+}
+template <int GW>
+__device__ __noinline__ GPair simplex_distance_qp_warp(const Geom& f, const Geom& g) {
+    const unsigned mask = group_mask<GW>();
+    const int lane = threadIdx.x & 31, r = lane & (GW - 1), base = lane - r;
+    const int nf = num_faces(f.dim), ng = num_faces(g.dim), total = nf * ng;
+    double bd2 = INFINITY;
+    int bidx = 0x7fffffff;
+    Bary bfb{0, 0}, bgb{0, 0};
+    D3 bpf{0, 0, 0}, bpg{0, 0, 0};
+    for (int c = r; c < total; c += GW) {
+        Bary fb, gb;
+        D3 pf, pg;
+        double d2;
+        if (qp_candidate(f, g, c / ng, c % ng, fb, gb, pf, pg, d2) && d2 < bd2) {  // c increases per lane
+            bd2 = d2;
+            bidx = c;
+            bfb = fb;
+            bgb = gb;
+            bpf = pf;
+            bpg = pg;
+        }
+    }
+    double md2 = bd2;
+    int midx = bidx;
+#pragma unroll
+    for (int off = GW / 2; off; off >>= 1) {
+        const double o = __shfl_xor_sync(mask, md2, off);
+        const int oi = __shfl_xor_sync(mask, midx, off);
+        if (o < md2 || (o == md2 && oi < midx)) {
+            md2 = o;
+            midx = oi;
+        }
+    }
+    GPair best;
+    if (midx == 0x7fffffff) {  // no candidate (not reachable: vertex pairs always qualify)
+        best.phi = best.lam = Bary{0.0, 0.0};
+        best.pf = best.pg = D3{0.0, 0.0, 0.0};
+    } else {
+        const int src = base + (midx % GW);
+        auto sh = [&](double v) { return __shfl_sync(mask, v, src); };
+        best.phi = Bary{sh(bfb.c0), sh(bfb.c1)};
+        best.lam = Bary{sh(bgb.c0), sh(bgb.c1)};
+        best.pf = D3{sh(bpf.x), sh(bpf.y), sh(bpf.z)};
+        best.pg = D3{sh(bpg.x), sh(bpg.y), sh(bpg.z)};
+    }
+    finish_pair(best);
+    return best;
+}
+
+// exact.hpp:342-367 (GW > 0: the QP spread over a group of GW lanes)
+template <int GW>
+__device__ GPair simplex_distance_t(const Geom& f, const Geom& g) {
     if (g.dim == 0) return point_geom_distance(f, g.c0);
     if (f.dim == 0) {
         const GPair r = point_geom_distance(g, f.c0);
@@ -343,8 +412,10 @@ __device__ GPair simplex_distance(const Geom& f, const Geom& g) {
         finish_pair(r);
         return r;
     }
-    return simplex_distance_qp(f, g);
+    if constexpr (GW > 0) return simplex_distance_qp_warp<GW>(f, g);
+    else return simplex_distance_qp(f, g);
 }
+__device__ __forceinline__ GPair simplex_distance(const Geom& f, const Geom& g) { return simplex_distance_t<0>(f, g); }
 
 // bvh.hpp:105-111 and 113-180
 struct BoxProx {
@@ -353,7 +424,8 @@ struct BoxProx {
     Bary lam;
     bool must_descend;
 };
-__device__ __noinline__ BoxProx box_primitive_proximity(D3 lo, D3 hi, const Geom& g) {
+template <int GW>
+__device__ BoxProx box_primitive_proximity_t(D3 lo, D3 hi, const Geom& g) {
     BoxProx r;
     r.lam = Bary{0.0, 0.0};
     r.must_descend = false;
@@ -389,7 +461,7 @@ __device__ __noinline__ BoxProx box_primitive_proximity(D3 lo, D3 hi, const Geom
         feat.dim = 0;
         feat.c0 = mk(side(0), side(1), side(2));
         feat.c1 = feat.c2 = D3{0, 0, 0};
-        const GPair p = simplex_distance(feat, g);
+        const GPair p = simplex_distance_t<GW>(feat, g);
         r.distance = p.distance;
         r.yb = p.pf;
         r.lam = p.lam;
@@ -408,7 +480,7 @@ __device__ __noinline__ BoxProx box_primitive_proximity(D3 lo, D3 hi, const Geom
         feat.c0 = a;
         feat.c1 = b;
         feat.c2 = D3{0, 0, 0};
-        const GPair p = simplex_distance(feat, g);
+        const GPair p = simplex_distance_t<GW>(feat, g);
         r.distance = p.distance;
         r.yb = p.pf;
         r.lam = p.lam;
@@ -426,10 +498,10 @@ __device__ __noinline__ BoxProx box_primitive_proximity(D3 lo, D3 hi, const Geom
         feat.c0 = r00;
         feat.c1 = r10;
         feat.c2 = r11;
-        const GPair p1 = simplex_distance(feat, g);
+        const GPair p1 = simplex_distance_t<GW>(feat, g);
         feat.c1 = r11;
         feat.c2 = r01;
-        const GPair p2 = simplex_distance(feat, g);
+        const GPair p2 = simplex_distance_t<GW>(feat, g);
         const bool first = p1.distance <= p2.distance;
         r.distance = first ? p1.distance : p2.distance;
         r.yb = first ? p1.pf : p2.pf;
@@ -437,19 +509,25 @@ __device__ __noinline__ BoxProx box_primitive_proximity(D3 lo, D3 hi, const Geom
     }
     return r;
 }
+__device__ __noinline__ BoxProx box_primitive_proximity(D3 lo, D3 hi, const Geom& g) {
+    return box_primitive_proximity_t<0>(lo, hi, g);
+}
 
-// One exact leaf term for query g (smooth.hpp:51-61): w and the alpha-scaled
-// shape gradient at the closest point phi on f, in the log2 accumulator.
-// geo: corners (9), shape gradients (edge: e/|e|^2; tri: G1, G2), pad.
-__device__ __noinline__ void leaf_term(const Phys<double>& ph, const Poly<double>* polys, int ne, int meta,
-                                          const double* geo, const Geom& g, Acc<double>& acc) {
-    const int kind = meta & 3, poly = (meta >> 2) - 1;
+// Leaf geometry record: corners (9), shape gradients (edge: e/|e|^2; tri:
+// G1, G2), pad.
+__device__ __forceinline__ Geom leaf_geom(int meta, const double* geo) {
     Geom f;
-    f.dim = kind;
+    f.dim = meta & 3;
     f.c0 = mk(geo[0], geo[1], geo[2]);
     f.c1 = mk(geo[3], geo[4], geo[5]);
     f.c2 = mk(geo[6], geo[7], geo[8]);
-    const GPair p = simplex_distance(f, g);
+    return f;
+}
+
+// The weight and accumulation half of a leaf term, given the closest pair.
+__device__ __forceinline__ void leaf_accumulate(const Phys<double>& ph, const Poly<double>* polys, int ne, int meta,
+                                                const double* geo, const GPair& p, Acc<double>& acc) {
+    const int kind = meta & 3, poly = (meta >> 2) - 1;
     const double d = p.distance;
     double lw = ph.lw_unit, kx = 0.0, ky = 0.0;
     if (kind == 1 && poly >= 0) {
@@ -493,6 +571,13 @@ __device__ __noinline__ void leaf_term(const Phys<double>& ph, const Poly<double
     acc.gx += gx;
     acc.gy += gy;
     acc.gz += gz;
+}
+
+// One exact leaf term for query g (smooth.hpp:51-61): w and the alpha-scaled
+// shape gradient at the closest point phi on f, in the log2 accumulator.
+__device__ __noinline__ void leaf_term(const Phys<double>& ph, const Poly<double>* polys, int ne, int meta,
+                                       const double* geo, const Geom& g, Acc<double>& acc) {
+    leaf_accumulate(ph, polys, ne, meta, geo, simplex_distance(leaf_geom(meta, geo), g), acc);
 }
 
 __device__ __forceinline__ Geom load_query(const double* qg, const int32_t* qd, int64_t qi, bool valid) {
@@ -554,6 +639,119 @@ struct SimplexVisit {
         dr = visit<HASH>(a, polys, br, rid, lgr, acc, nleaf, nfar, h, nre);
     }
 };
+
+// K3W (default for simplex queries): one warp per query simplex; its walk
+// is processed 32 / GW nodes at a time (a shared-memory stack as in K3F),
+// and every node test is cooperative over a group of GW lanes -- the
+// face-enumeration QP of a box feature or a leaf has up to 49 independent
+// candidates, which the group evaluates in parallel before a (d2, index)
+// arg-min. A node is tested iff all its ancestors descended (the
+// reference's visited set); each group accumulates the terms of its nodes
+// and the groups' states merge in fp64 at the end. The per-lane QP of
+// K3 / K3F serialises the 49 candidates and diverges between feature types
+// (3.5 active lanes per instruction in the frontier kernel's profile).
+// Stack bound as K3F: 2 (32 / GW) entries per level.
+constexpr int kWarpThreads = 128;
+template <int GW, bool HASH>
+__global__ void __launch_bounds__(kWarpThreads) simplex_warp_kernel(const __grid_constant__ TraverseArgs<double> a,
+                                                                    int cap) {
+    constexpr int NG = 32 / GW;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    Poly<double>* polys = reinterpret_cast<Poly<double>*>(smem_raw);
+    int32_t* stacks = reinterpret_cast<int32_t*>(smem_raw + poly_bytes<double>(a.npoly));
+    for (int t = threadIdx.x; t < a.npoly * kPolyCoefs; t += blockDim.x)
+        reinterpret_cast<double*>(polys)[t] = reinterpret_cast<const double*>(a.polys)[t];
+    __syncthreads();
+    const int lane = threadIdx.x & 31, grp = lane / GW, r = lane % GW;
+    const int64_t i = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;  // sorted position
+    if (i >= a.Q) return;
+    int32_t* stk = stacks + size_t(threadIdx.x >> 5) * cap;
+    const int64_t qi = a.perm ? a.perm[i] : i;
+    const sx::Geom g = sx::load_query(a.qgeom, a.qdim, qi, true);
+    Acc<double> acc;
+    acc.init();
+    int64_t nleaf = 0, nfar = 0;
+    uint64_t h = 0;
+    if (lane == 0) stk[0] = 0;
+    __syncwarp();
+    int n = 1;
+    while (n > 0) {
+        const int take = n < NG ? n : NG;
+        const int base = n - take;
+        const int32_t id = grp < take ? stk[base + grp] : -1;
+        __syncwarp();
+        bool d = false;
+        int32_t link = 0;
+        if (id >= 0) {  // uniform within the group
+            const NodeT<double> b = a.box[id];
+            memcpy(&link, &b.v[7], sizeof(int32_t));
+            bool far = false;
+            if (a.use_bh) {  // collect_contributions (smooth.hpp:114-121), bh_condition (bvh.hpp:185-187)
+                const sx::BoxProx pr = sx::box_primitive_proximity_t<GW>(sx::mk(b.v[0], b.v[1], b.v[2]),
+                                                                          sx::mk(b.v[4], b.v[5], b.v[6]), g);
+                if (!pr.must_descend && pr.distance > 0.0 && a.diam64[id] < a.beta64 * pr.distance) {
+                    const sx::D3 diff = g.at(pr.lam) - pr.yb;
+                    far_term(a.ph, a.lgcount[id] + a.lw_ff, pr.distance, 1.0 / pr.distance, diff.x, diff.y, diff.z,
+                             acc);
+                    ++nfar;
+                    if constexpr (HASH) h += decision_mix(uint64_t(id), 1);
+                    far = true;
+                }
+            }
+            if (!far) {
+                if (link < 0) {
+                    const int slot = -link - 1;
+                    const int meta = a.leafmeta[slot];
+                    const double* geo = a.leafgeom + size_t(slot) * 16;
+                    const sx::GPair p = sx::simplex_distance_t<GW>(sx::leaf_geom(meta, geo), g);
+                    sx::leaf_accumulate(a.ph, polys, a.ne, meta, geo, p, acc);
+                    ++nleaf;
+                    if constexpr (HASH) h += decision_mix(uint64_t(id), 2);
+                } else {
+                    d = true;
+                }
+            }
+        }
+        const unsigned D = __ballot_sync(0xffffffffu, d && r == 0);  // one bit per descending group
+        if (d && r == 0) {
+            const int pos = base + 2 * __popc(D & ((1u << lane) - 1u));
+            stk[pos] = link;        // right child below ...
+            stk[pos + 1] = id + 1;  // ... left child on top
+        }
+        __syncwarp();
+        n = base + 2 * __popc(D);
+    }
+    // merge the groups' states (fp64, anchored at the warp maximum); within a
+    // group every lane holds the same state, lane r = 0 contributes it
+    Tot tot;
+    tot.init();
+    tot.flush(acc);
+    double M = r == 0 ? tot.M : -INFINITY;
+    for (int off = 16; off; off >>= 1) M = fmax(M, __shfl_xor_sync(0xffffffffu, M, off));
+    const double f = (r != 0 || M == -INFINITY || tot.M == -INFINITY) ? 0.0 : exp2(tot.M - M);
+    double s = tot.s * f, gx = tot.gx * f, gy = tot.gy * f, gz = tot.gz * f;
+    unsigned long long L = r == 0 ? (unsigned long long)nleaf : 0ull, F = r == 0 ? (unsigned long long)nfar : 0ull,
+                       H = r == 0 ? h : 0ull;
+    for (int off = 16; off; off >>= 1) {
+        s += __shfl_xor_sync(0xffffffffu, s, off);
+        gx += __shfl_xor_sync(0xffffffffu, gx, off);
+        gy += __shfl_xor_sync(0xffffffffu, gy, off);
+        gz += __shfl_xor_sync(0xffffffffu, gz, off);
+        L += __shfl_xor_sync(0xffffffffu, L, off);
+        F += __shfl_xor_sync(0xffffffffu, F, off);
+        H += __shfl_xor_sync(0xffffffffu, H, off);
+    }
+    if (lane == 0) {
+        a.part[i] = M;
+        a.part[a.Q + i] = s;
+        a.part[2 * a.Q + i] = gx;
+        a.part[3 * a.Q + i] = gy;
+        a.part[4 * a.Q + i] = gz;
+        a.leaves[i] = int64_t(L);
+        a.far[i] = int64_t(F);
+        if (HASH) a.hash[i] = H;
+    }
+}
 
 // Exact path: thread = query, blockIdx.y = primitive range (index order);
 // partial states [split][5][Q] merged by K4.
@@ -773,11 +971,30 @@ void simplex_query(Ctx& c, const double* corners, const int32_t* dims, int64_t Q
     a.qgeom = corners;
     a.qdim = dims;
     a.leafgeom = c.leafgeom.as<double>();
-    // node tests cost a QP: few-query batches go node-parallel
+    // SDGPU_SIMPLEX_KERNEL = warp (default: K3W) | frontier (K3F) | pair (K3)
+    const char* ke = std::getenv("SDGPU_SIMPLEX_KERNEL");
+    const std::string kern = ke && *ke ? ke : "warp";
     int nsplits = 1;
-    if (!(use_frontier(Q, int64_t(1) << 22) &&
-          launch_frontier<double, SimplexVisit>(c, t, a, out.hash != nullptr, st, launches, 32)))
+    if (kern == "warp") {
+        // group width: lanes per node test (SDGPU_SIMPLEX_GW = 8 | 16 | 32)
+        const char* ge = std::getenv("SDGPU_SIMPLEX_GW");
+        // (tools/simplex_sweep.sh over the paper-table rows: 8 ~ 16 < 32)
+        int gw = ge && *ge ? std::atoi(ge) : 8;
+        if (gw != 16 && gw != 32) gw = 8;
+        const int cap = 2 * (32 / gw) * (t.depth + 1);
+        const size_t smem = poly_bytes<double>(npoly) + size_t(cap) * (kWarpThreads / 32) * sizeof(int32_t);
+        using K = void (*)(TraverseArgs<double>, int);
+        K kw = gw == 8 ? (out.hash ? simplex_warp_kernel<8, true> : simplex_warp_kernel<8, false>)
+             : gw == 32 ? (out.hash ? simplex_warp_kernel<32, true> : simplex_warp_kernel<32, false>)
+                        : (out.hash ? simplex_warp_kernel<16, true> : simplex_warp_kernel<16, false>);
+        check_cuda(cudaFuncSetAttribute(kw, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)), "smem attr");
+        kw<<<unsigned((Q * 32 + kWarpThreads - 1) / kWarpThreads), kWarpThreads, smem, st>>>(a, cap);
+        check_cuda(cudaGetLastError(), "simplex warp kernel");
+        ++launches;
+    } else if (!(kern == "frontier" &&
+                 launch_frontier<double, SimplexVisit>(c, t, a, out.hash != nullptr, st, launches, 32))) {
         nsplits = launch_pair_traversal<double, SimplexVisit>(c, t, a, out.hash != nullptr, st, launches, 4);
+    }
     check_cuda(launch_finalize(a.part, nsplits, Q, p.alpha, p.epsilon, 0, a.leaves, a.far, a.hash, perm, out, st),
                "finalize");
     ++launches;

@@ -106,13 +106,19 @@ def test_simplex_lbvh_decisions(sd, oracle):
     _close(got, ref, "lbvh")
 
 
-@pytest.mark.parametrize("split", ["0", "3", "", "frontier", "frontier32"])
+@pytest.mark.parametrize("split", ["0", "3", "", "frontier", "frontier32", "warp8", "warp16", "warp32"])
 def test_simplex_split_traversal(sd, oracle, split, monkeypatch):
-    if split.startswith("frontier"):
-        monkeypatch.setenv("SDGPU_FRONTIER", "1")
+    """Every simplex traversal kernel -- K3W (group-cooperative QP, 8/16/32
+    lanes per node), K3F (node-parallel), K3 (packets, slot split at depth
+    0/3/auto) -- makes the oracle's decisions."""
+    if split.startswith("warp"):
+        monkeypatch.setenv("SDGPU_SIMPLEX_KERNEL", "warp")
+        monkeypatch.setenv("SDGPU_SIMPLEX_GW", split[4:])
+    elif split.startswith("frontier"):
+        monkeypatch.setenv("SDGPU_SIMPLEX_KERNEL", "frontier")
         monkeypatch.setenv("SDGPU_FRONTIER_G", split[8:] or "4")
     else:
-        monkeypatch.setenv("SDGPU_FRONTIER", "0")
+        monkeypatch.setenv("SDGPU_SIMPLEX_KERNEL", "pair")
         monkeypatch.setenv("SDGPU_SPLIT", split)
     O = oracle
     m, c, d = _scene(O, 3, 300, 100, 1, 333)
