@@ -401,6 +401,23 @@ def run_cfg5(args, rank, world, local):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
     ms = float(t.item())
     fin = float(torch.isfinite(d_hat).double().mean().item())
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        # the oracle port on 4,096 of the queries, same tree and table
+        import oracle as O
+        O.build()
+        threads = O.hardware_threads()
+        om = O.Mesh.from_arrays(v, w.simplices, w.kinds)
+        ow = O.Weights.from_table(O.WeightTable(wt.A, wt.sup_wtilde, wt.edge_a, wt.tri_stored, wt.poly_index))
+        ot = O.Tree.from_nodes(eng.export_bvh())
+        sample = np.linspace(0, Q - 1, 4096).astype(np.int64)
+        r = O.query(om, ow, q[sample], O.Params(alpha=w.alpha, alpha_u=600.0, beta=w.beta), tree=ot, threads=threads)
+        got = d_hat[torch.as_tensor(sample, device=dev)].cpu().numpy()
+        ok = np.isfinite(r.d_hat)
+        cpu = {"value": 4096 / r.seconds, "unit": "queries/s", "cores": threads, "kind": "port",
+               "sample": f"4,096 evenly spaced cfg5 queries on the exported LBVH, fp64 oracle port, {r.seconds:.2f} s",
+               "max_abs_d_hat_diff": float(np.abs(got[ok] - r.d_hat[ok]).max()) if ok.any() else 0.0}
+        del om, ow, ot
     if rank == 0:
         line = {"metric": "BVH queries/s (value+grad), primitive-sharded", "value": Q / (ms * 1e-3),
                 "unit": "queries/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -412,7 +429,7 @@ def run_cfg5(args, rank, world, local):
                            "parallelism": f"primitive-sharded x{world} (Morton shards, LBVH per shard), one "
                                           f"NCCL all_reduce(SUM) of 4 fp64 per query",
                            "primitives_per_gpu": len(sh.kinds), "l2": "flushed between timed steps"},
-                "finite_fraction": fin, "gpu_launches": launches[0] * args.steps,
+                "finite_fraction": fin, "gpu_launches": launches[0] * args.steps, "cpu_baseline": cpu,
                 "setup_s": {"total": setup, "generate": tg, "build_weights": tw, "build_lbvh": tb},
                 "clocks": clk.summary()}
         print(json.dumps(line), flush=True)
