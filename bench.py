@@ -47,6 +47,16 @@ def dist_env():
     return rank, world, local
 
 
+def tree_method(sd):
+    """The reference's median-split tree (build_bvh, bvh.hpp:34-91), built on
+    the device by median.cu; BENCH_TREE=lbvh selects the GPU LBVH (A/B)."""
+    return sd.SD_BVH_LBVH if os.environ.get("BENCH_TREE") == "lbvh" else sd.SD_BVH_MEDIAN
+
+
+def tree_name():
+    return "GPU LBVH" if os.environ.get("BENCH_TREE") == "lbvh" else "reference median-split tree built on the GPU"
+
+
 class ClockSampler:
     """SM clocks and clock-event (throttle) reasons sampled DURING the timed
     region: NVML polled every 2 ms from a thread (nvidia-smi -lms 200 as the
@@ -225,7 +235,8 @@ def run_reference(args, rank, world):
 def measure_bvh(args, rank, world, local, eng_cls, dev, stream, flush, peaks):
     """Secondary line item: BVH far-field queries/s on BASELINE configs[3]
     (cfg4: icosphere(9), 5,242,880 triangles, 4,194,304 queries per GPU,
-    alpha 200, beta 0.5), GPU LBVH + fp32 traversal."""
+    alpha 200, beta 0.5), the reference's median tree built on the GPU + fp32
+    traversal."""
     import torch
     import paper_2108_10480_b200 as sd
     from paper_2108_10480_b200 import configs
@@ -238,7 +249,8 @@ def measure_bvh(args, rank, world, local, eng_cls, dev, stream, flush, peaks):
     eng.build_weights()
     tw = time.perf_counter() - tw
     tb = time.perf_counter()
-    eng.build_bvh(sd.SD_BVH_LBVH)
+    # BENCH_TREE=median builds the reference's median-split tree instead (A/B)
+    eng.build_bvh(tree_method(sd))
     tb = time.perf_counter() - tb
     Q = len(q)
     P = sd.SmoothParams(alpha=w.alpha, alpha_u=600.0, beta=w.beta)
@@ -283,9 +295,9 @@ def measure_bvh(args, rank, world, local, eng_cls, dev, stream, flush, peaks):
            "ms_per_step": ms, "queries_per_gpu": Q, "primitives": len(w.kinds),
            "workload": "cfg4: icosphere(9) with radial displacement, 5,242,880 triangles, 4,194,304 queries "
                        "per GPU (half uniform in [-1.5,1.5]^3, half within 0.02 of the surface), alpha=200, "
-                       "beta=0.5, fp32, GPU LBVH (BASELINE configs[3])",
+                       f"beta=0.5, fp32, {tree_name()} (BASELINE configs[3])",
            "per_query": {"leaves": L / Q, "far_field": F / Q, "nodes_popped": pops / Q},
-           "setup_s": {"total": setup_s, "build_weights": tw, "build_lbvh": tb},
+           "setup_s": {"total": setup_s, "build_weights": tw, "build_tree": tb},
            "gpu_launches": launches * args.steps,
            "roofline": {"achieved_tflops": flops / (ms * 1e-3) / 1e12, "touched_gbs": nbytes / (ms * 1e-3) / 1e9,
                         "hbm_peak_gbs": 6542.4, "algorithmic": "10 flop/popped node + 12/far term + 192/exact "
@@ -305,7 +317,7 @@ def measure_bvh(args, rank, world, local, eng_cls, dev, stream, flush, peaks):
 
 def bvh_cpu_sample(eng, v, w, q, P, target_s=10.0):
     """The oracle port (fp64, all host threads) on a bounded query subset of
-    cfg4, traversing the SAME tree (the GPU LBVH exported in the reference
+    cfg4, traversing the SAME tree (the GPU-built tree exported in the reference
     layout) with the same WeightSet table."""
     import oracle as O
     O.build()
@@ -323,14 +335,14 @@ def bvh_cpu_sample(eng, v, w, q, P, target_s=10.0):
     n = int(min(65536, max(pilot, pilot * target_s / max(r.seconds, 1e-3))))
     r = O.query(m, ws, pick(n), p, tree=t, threads=threads)
     return {"value": n / r.seconds, "unit": "queries/s", "cores": threads, "kind": "port",
-            "sample": f"{n} cfg4 queries (half from each half of the distribution) on the exported GPU LBVH, "
+            "sample": f"{n} cfg4 queries (half from each half of the distribution) on the exported GPU-built tree, "
                       f"fp64 oracle port, {r.seconds:.1f} s"}
 
 
 def run_cfg5(args, rank, world, local):
     """BASELINE configs[4]: mixed scene (16.8M triangles + 1M edges + 1M
     points), 16,777,216 queries, alpha 100, beta 0.5, PRIMITIVE-sharded over
-    the ranks (Morton-contiguous shards, one GPU LBVH per shard, global
+    the ranks (Morton-contiguous shards, one GPU-built tree per shard, global
     WeightSet), per-query fp64 partials merged with ONE NCCL all-reduce,
     then sd_finalize_device. Strong scaling (fixed total work)."""
     import torch
@@ -356,7 +368,8 @@ def run_cfg5(args, rank, world, local):
     eng.set_geometry(sh.vertices, sh.simplices, sh.kinds)
     eng.set_weights(wt.A, wt.sup_wtilde, wt.edge_a, wt.tri_stored, sh.poly_index)
     tb = time.perf_counter()
-    eng.build_bvh(sd.SD_BVH_LBVH)
+    # BENCH_TREE=median builds the reference's median-split tree instead (A/B)
+    eng.build_bvh(tree_method(sd))
     tb = time.perf_counter() - tb
     Q = len(q)
     P = sd.SmoothParams(alpha=w.alpha, alpha_u=600.0, beta=w.beta)
@@ -415,7 +428,7 @@ def run_cfg5(args, rank, world, local):
         got = d_hat[torch.as_tensor(sample, device=dev)].cpu().numpy()
         ok = np.isfinite(r.d_hat)
         cpu = {"value": 4096 / r.seconds, "unit": "queries/s", "cores": threads, "kind": "port",
-               "sample": f"4,096 evenly spaced cfg5 queries on the exported LBVH, fp64 oracle port, {r.seconds:.2f} s",
+               "sample": f"4,096 evenly spaced cfg5 queries on the exported GPU-built tree, fp64 oracle port, {r.seconds:.2f} s",
                "max_abs_d_hat_diff": float(np.abs(got[ok] - r.d_hat[ok]).max()) if ok.any() else 0.0}
         del om, ow, ot
     if rank == 0:
@@ -426,11 +439,11 @@ def run_cfg5(args, rank, world, local):
                 "config": {"workload": "cfg5: 64 rotated cfg3 tori (16,777,216 triangles) + 1M edges + 1M points, "
                                        "16,777,216 queries uniform in the scene AABB, alpha=100, beta=0.5, fp32 "
                                        "(BASELINE configs[4])",
-                           "parallelism": f"primitive-sharded x{world} (Morton shards, LBVH per shard), one "
+                           "parallelism": f"primitive-sharded x{world} (Morton shards, {tree_name()} per shard), one "
                                           f"NCCL all_reduce(SUM) of 4 fp64 per query",
                            "primitives_per_gpu": len(sh.kinds), "l2": "flushed between timed steps"},
                 "finite_fraction": fin, "gpu_launches": launches[0] * args.steps, "cpu_baseline": cpu,
-                "setup_s": {"total": setup, "generate": tg, "build_weights": tw, "build_lbvh": tb},
+                "setup_s": {"total": setup, "generate": tg, "build_weights": tw, "build_tree": tb},
                 "clocks": clk.summary()}
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -445,7 +458,7 @@ def run_m2m(args, rank, world, local):
     counts, alpha and alpha_q). One step = one evaluation through the public
     host API (query mesh H2D, inner BVH queries -- points on the fp32 point
     path, edges / triangles on the fp64 simplex path -- outer LogSumExp,
-    vertex gradients D2H); the data mesh's weights and GPU LBVH are built
+    vertex gradients D2H); the data mesh's weights and tree are built
     once per row. The oracle port evaluates the same row once on the host
     threads (cpu_ms) and its d_hat checks ours."""
     import torch
@@ -463,7 +476,7 @@ def run_m2m(args, rank, world, local):
             t0 = time.perf_counter()
             eng.set_geometry(dv, r.data.simplices, r.data.kinds)
             eng.build_weights()
-            eng.build_bvh(sd.SD_BVH_LBVH)
+            eng.build_bvh(tree_method(sd))
             setup = time.perf_counter() - t0
             P = sd.SmoothParams(alpha=r.alpha, alpha_u=600.0, beta=0.5, alpha_q=r.alpha_q)
             run = lambda: eng.smooth_mesh_dist_general(qv, r.query.simplices, r.query.kinds, P)
@@ -510,7 +523,7 @@ def run_m2m(args, rank, world, local):
             "warmup": args.warmup, "ms_per_step": tot, "higher_is_better": False, "scaling": "none",
             "vs_baseline": tot / paper, "dtype": "f32 points / f64 simplices", "data": "synthetic stand-ins",
             "config": {"workload": f"{len(rows)} rows of PAPER.md:1378-1397 (sim_rows.py stand-ins), beta=0.5, "
-                                   "GPU LBVH, e2e through sd_mesh_dist", "paper_total_ms": paper},
+                                   f"{tree_name()}, e2e through sd_mesh_dist", "paper_total_ms": paper},
             "rows": rows, "cpu_baseline": cpu, "clocks": clk.summary()}
     print(json.dumps(line), flush=True)
 
@@ -535,7 +548,7 @@ def run_render(args, rank, world, local):
     eng = sd.Engine(local, sd.SD_FP64 if args.fp64 else sd.SD_FP32)
     eng.set_geometry(V, T, K)
     eng.build_weights()
-    eng.build_bvh(sd.SD_BVH_LBVH)
+    eng.build_bvh(tree_method(sd))
     P = sd.SmoothParams(alpha=200.0, alpha_u=1200.0)
     for _ in range(max(1, args.warmup)):
         eng.render(sd.SmoothParams(alpha=200.0, alpha_u=1200.0, beta=0.2))
@@ -573,7 +586,7 @@ def run_render(args, rank, world, local):
             "higher_is_better": False, "scaling": "none", "vs_baseline": None,
             "dtype": "f64" if args.fp64 else "f32", "data": "synthetic (uv_torus 60x60, benchmark frame)",
             "config": {"workload": "render.hpp:77-134 via sd_render, beta_ablation {0, 0.2, 0.5}, alpha 200, "
-                                   "alpha_u 1200, GPU LBVH; grid_benchmark 64^3 alpha 100 beta 0.3"},
+                                   f"alpha_u 1200, {tree_name()}; grid_benchmark 64^3 alpha 100 beta 0.3"},
             "ablation": med, "acceptance_6": {"speedup_beta02": med[1]["speedup_vs_beta0"],
                                               "pass": med[1]["speedup_vs_beta0"] >= 5.0
                                               and med[1]["mean_disp_rel"] < 0.04 and med[2]["mean_disp_rel"] < 0.04},

@@ -705,7 +705,9 @@ int sd_build_bvh(sd_ctx* c, int method) {
         if (!c) throw ArgError{"ctx is NULL"};
         if (!c->have_geom) throw StateError{"set the geometry before building a tree"};
         DeviceScope ds(c->device);
-        if (method == SD_BVH_MEDIAN) tree_build_median(*c);
+        const char* mh = std::getenv("SDGPU_MEDIAN_HOST");
+        if (method == SD_BVH_MEDIAN && mh && *mh == '1') tree_build_median_host(*c);
+        else if (method == SD_BVH_MEDIAN) tree_build_median_gpu(*c);
         else if (method == SD_BVH_LBVH) tree_build_lbvh(*c);
         else throw ArgError{"unknown tree builder"};
         c->have_tree = true;

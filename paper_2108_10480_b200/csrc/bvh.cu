@@ -118,7 +118,7 @@ static void median_build_host(const Ctx& c, std::vector<sd_bvh_node>& out) {
     }
 }
 
-void tree_build_median(Ctx& c) {
+void tree_build_median_host(Ctx& c) {
     median_build_host(c, c.tree);
     c.dtree_ready = false;
     c.sx_tree_ready = c.sx_prim_ready = false;

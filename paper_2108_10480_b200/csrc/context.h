@@ -154,7 +154,8 @@ void grid_impl(Ctx& c, const sd_params& p, int mode, int n, double* d_hat, int64
 void simplex_query(Ctx& c, const double* corners, const int32_t* dims, int64_t Q, const sd_params& p, int mode,
                    const FinalizeOut& out, cudaStream_t st);
 void split_tables(Ctx& c, DeviceTree& t, int k);  // nodes at depth k of c.tree
-void tree_build_median(Ctx& c);
+void tree_build_median_host(Ctx& c);  // bvh.cu, single-threaded restatement
+void tree_build_median_gpu(Ctx& c);   // median.cu, same tree on the device
 void tree_build_lbvh(Ctx& c);
 WeightAssignment gpu_weight_assignment(Ctx& c);  // adjacency.cu
 template <class T>

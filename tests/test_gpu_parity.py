@@ -596,3 +596,29 @@ def test_mesh_dist_far_cloud_underflows(sd, oracle):
     e = engine_for(sd, O, m, O.Weights.build(m), 1)
     md = e.smooth_mesh_dist([[3.0, 0, 0], [0, 4.0, 0]], sd.SmoothParams(alpha=400.0, beta=0.0, alpha_q=20.0))
     assert np.isinf(md.d_hat) and not md.vertex_grads.any()
+
+
+@pytest.mark.parametrize("case", ["cfg3", "cfg5_mixed_subset", "ties"])
+def test_gpu_median_build_equals_host_build(sd, oracle, case, monkeypatch):
+    """The device median build (median.cu: segmented reductions + stable
+    segmented sorts per level) emits the host restatement's tree byte for
+    byte -- at 262k triangles, on a mixed point/edge/triangle scene, and on
+    a grid with exactly tied centroids (index tie-break)."""
+    O = oracle
+    if case == "cfg3":
+        m = O.config_mesh(3)
+    elif case == "cfg5_mixed_subset":
+        m = O.random_scene(17, 5000)
+    else:
+        g = np.stack(np.meshgrid(np.arange(12.0), np.arange(9.0), np.arange(7.0), indexing="ij"), -1).reshape(-1, 3)
+        g = np.concatenate([g, g])  # duplicated points: equal centroids everywhere
+        m = O.Mesh.from_arrays(g, np.stack([np.arange(len(g)), -np.ones(len(g)), -np.ones(len(g))], 1), np.zeros(len(g)))
+    e = sd.Engine(0, sd.SD_FP64)
+    e.set_geometry(m.vertices, m.simplices, m.kinds)
+    e.build_bvh(sd.SD_BVH_MEDIAN)
+    gpu = e.export_bvh()
+    monkeypatch.setenv("SDGPU_MEDIAN_HOST", "1")
+    e.build_bvh(sd.SD_BVH_MEDIAN)
+    assert gpu.tobytes() == e.export_bvh().tobytes()
+    if case != "cfg3":
+        assert gpu.tobytes() == O.Tree.build(m).nodes().tobytes()
