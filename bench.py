@@ -47,20 +47,22 @@ def dist_env():
     return rank, world, local
 
 
-# Tree per workload (BENCH_TREE=median|lbvh overrides): the reference's
-# median-split tree (build_bvh, bvh.hpp:34-91, built on the device by
-# median.cu) on the single-surface cfg4 (28.4 ms vs 29.7 ms with the LBVH:
-# 1152 vs 1335 popped nodes per query); the GPU LBVH on the clustered scenes,
-# whose Morton splits follow the gaps between objects (cfg5 35 ms vs 62 ms,
-# City Street 22 ms vs 38 ms with the median tree).
-def tree_method(sd, default="lbvh"):
-    t = os.environ.get("BENCH_TREE") or default
-    return sd.SD_BVH_MEDIAN if t == "median" else sd.SD_BVH_LBVH
+# Tree builder (BENCH_TREE=median|lbvh|auto, default auto): SD_BVH_AUTO
+# builds the reference's median-split tree (build_bvh, bvh.hpp:34-91, on the
+# device by median.cu) and the GPU LBVH and keeps the smaller surface-area
+# cost -- the median tree on single surfaces (cfg4 28.4 ms vs 29.7 ms:
+# 1152 vs 1335 popped nodes per query; Terrain 8.2 vs 15.6 ms), the LBVH on
+# clustered scenes whose Morton splits follow the gaps between objects (cfg5
+# 35 vs 62 ms, City Street 22 vs 38 ms).
+def tree_method(sd):
+    t = os.environ.get("BENCH_TREE") or "auto"
+    return {"median": sd.SD_BVH_MEDIAN, "lbvh": sd.SD_BVH_LBVH}.get(t, sd.SD_BVH_AUTO)
 
 
-def tree_name(default="lbvh"):
-    t = os.environ.get("BENCH_TREE") or default
-    return "reference median-split tree built on the GPU" if t == "median" else "GPU LBVH"
+def tree_name():
+    t = os.environ.get("BENCH_TREE") or "auto"
+    return {"median": "reference median-split tree built on the GPU", "lbvh": "GPU LBVH"}.get(
+        t, "GPU tree (median split or LBVH, smaller surface-area cost)")
 
 
 class ClockSampler:
@@ -256,7 +258,7 @@ def measure_bvh(args, rank, world, local, eng_cls, dev, stream, flush, peaks):
     tw = time.perf_counter() - tw
     tb = time.perf_counter()
     # BENCH_TREE=median builds the reference's median-split tree instead (A/B)
-    eng.build_bvh(tree_method(sd, "median"))
+    eng.build_bvh(tree_method(sd))
     tb = time.perf_counter() - tb
     Q = len(q)
     P = sd.SmoothParams(alpha=w.alpha, alpha_u=600.0, beta=w.beta)
@@ -301,7 +303,7 @@ def measure_bvh(args, rank, world, local, eng_cls, dev, stream, flush, peaks):
            "ms_per_step": ms, "queries_per_gpu": Q, "primitives": len(w.kinds),
            "workload": "cfg4: icosphere(9) with radial displacement, 5,242,880 triangles, 4,194,304 queries "
                        "per GPU (half uniform in [-1.5,1.5]^3, half within 0.02 of the surface), alpha=200, "
-                       f"beta=0.5, fp32, {tree_name("median")} (BASELINE configs[3])",
+                       f"beta=0.5, fp32, {tree_name()} (BASELINE configs[3])",
            "per_query": {"leaves": L / Q, "far_field": F / Q, "nodes_popped": pops / Q},
            "setup_s": {"total": setup_s, "build_weights": tw, "build_tree": tb},
            "gpu_launches": launches * args.steps,

@@ -93,7 +93,7 @@ typedef struct sd_outputs {
 
 enum { SD_FP32 = 0, SD_FP64 = 1 };                  /* arithmetic precision */
 enum { SD_EXACT = 0, SD_BVH = 1 };                  /* query mode */
-enum { SD_BVH_MEDIAN = 0, SD_BVH_LBVH = 1 };        /* tree builders */
+enum { SD_BVH_MEDIAN = 0, SD_BVH_LBVH = 1, SD_BVH_AUTO = 2 };  /* tree builders */
 enum { SD_POINT = 0, SD_EDGE = 1, SD_TRIANGLE = 2 }; /* SimplexKind (mesh.hpp:15) */
 
 enum {
@@ -136,8 +136,9 @@ int sd_export_weights(sd_ctx* ctx, double* edge_a, double* tri_stored, int32_t* 
 
 /* Upload a reference-layout tree (e.g. from the reference build_bvh), or
  * build one on the GPU: SD_BVH_MEDIAN reproduces build_bvh exactly,
- * SD_BVH_LBVH is the Morton-code linear BVH. Either way the tree can be
- * exported in the reference layout so a CPU evaluator can run on it. */
+ * SD_BVH_LBVH is the Morton-code linear BVH, SD_BVH_AUTO builds both and
+ * keeps the one with the smaller surface-area cost. Either way the tree can
+ * be exported in the reference layout so a CPU evaluator can run on it. */
 int sd_set_bvh(sd_ctx* ctx, const sd_bvh_node* nodes, int64_t n);
 int sd_build_bvh(sd_ctx* ctx, int method);
 int sd_bvh_size(sd_ctx* ctx, int64_t* n);

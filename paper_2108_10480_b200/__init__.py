@@ -24,7 +24,7 @@ LIB_PATH = os.path.join(_HERE, "libsdgpu.so")
 
 SD_FP32, SD_FP64 = 0, 1
 SD_EXACT, SD_BVH = 0, 1
-SD_BVH_MEDIAN, SD_BVH_LBVH = 0, 1
+SD_BVH_MEDIAN, SD_BVH_LBVH, SD_BVH_AUTO = 0, 1, 2
 SD_POINT, SD_EDGE, SD_TRIANGLE = 0, 1, 2
 
 NODE_DTYPE = np.dtype(

@@ -456,6 +456,22 @@ void query_batch_f64(Ctx& c, const double* q, int64_t Q, const sd_params& p, int
     }
 }
 
+// Surface-area cost of a tree: sum over internal nodes of the box area,
+// relative to the root's.
+static double sah_cost(const std::vector<sd_bvh_node>& t) {
+    if (t.empty()) return 0.0;
+    auto area = [](const sd_bvh_node& n) {
+        const double x = std::max(0.0, n.hi[0] - n.lo[0]), y = std::max(0.0, n.hi[1] - n.lo[1]),
+                     z = std::max(0.0, n.hi[2] - n.lo[2]);
+        return 2.0 * (x * y + y * z + x * z);
+    };
+    double sum = 0.0;
+    for (const sd_bvh_node& n : t)
+        if (n.left >= 0) sum += area(n);
+    const double root = area(t[0]);
+    return root > 0.0 ? sum / root : sum;
+}
+
 // Metadata of a table given as bare coefficients: edge valences follow from
 // w~(0) = 1/v0, w~(1) = 1/v1 (weights.hpp:46-76) and the extrema are closed
 // form; triangle valences are unknown (0) and the extrema are sampled.
@@ -709,7 +725,20 @@ int sd_build_bvh(sd_ctx* c, int method) {
         if (method == SD_BVH_MEDIAN && mh && *mh == '1') tree_build_median_host(*c);
         else if (method == SD_BVH_MEDIAN) tree_build_median_gpu(*c);
         else if (method == SD_BVH_LBVH) tree_build_lbvh(*c);
-        else throw ArgError{"unknown tree builder"};
+        else if (method == SD_BVH_AUTO) {
+            // both device builders; keep the tree with the smaller surface-area
+            // cost sum_internal area / area(root) -- it predicted the faster
+            // traversal on every measured workload (tools/tree_cost.py)
+            tree_build_median_gpu(*c);
+            std::vector<sd_bvh_node> median;
+            median.swap(c->tree);
+            tree_build_lbvh(*c);
+            if (sah_cost(median) < sah_cost(c->tree)) c->tree.swap(median);
+            c->dtree_ready = false;
+            c->sx_tree_ready = c->sx_prim_ready = false;
+        } else {
+            throw ArgError{"unknown tree builder"};
+        }
         c->have_tree = true;
     });
 }

@@ -622,3 +622,30 @@ def test_gpu_median_build_equals_host_build(sd, oracle, case, monkeypatch):
     assert gpu.tobytes() == e.export_bvh().tobytes()
     if case != "cfg3":
         assert gpu.tobytes() == O.Tree.build(m).nodes().tobytes()
+
+
+def test_auto_tree_picks_the_smaller_surface_area_cost(sd, oracle):
+    """SD_BVH_AUTO keeps whichever device tree (median split or LBVH) has
+    the smaller sum of internal box areas; the result is one of the two
+    exactly and traverses to the oracle's decisions."""
+    O = oracle
+    m = O.random_scene(19, 3000)
+    e = sd.Engine(0, sd.SD_FP64)
+    e.set_geometry(m.vertices, m.simplices, m.kinds)
+    e.set_weight_table(O.Weights.build(m).table)
+    trees = {}
+    for k in (sd.SD_BVH_MEDIAN, sd.SD_BVH_LBVH, sd.SD_BVH_AUTO):
+        e.build_bvh(k)
+        trees[k] = e.export_bvh()
+
+    def cost(t):
+        ext = np.maximum(t["hi"] - t["lo"], 0)
+        a = 2 * (ext[:, 0] * ext[:, 1] + ext[:, 1] * ext[:, 2] + ext[:, 0] * ext[:, 2])
+        return a[t["left"] >= 0].sum() / a[0]
+    best = sd.SD_BVH_MEDIAN if cost(trees[sd.SD_BVH_MEDIAN]) < cost(trees[sd.SD_BVH_LBVH]) else sd.SD_BVH_LBVH
+    assert trees[sd.SD_BVH_AUTO].tobytes() == trees[best].tobytes()
+    q = O.random_point_queries(5, m, 300)
+    t = O.Tree.from_nodes(trees[sd.SD_BVH_AUTO])
+    ref = O.query(m, O.Weights.build(m), q, O.Params(beta=0.5), tree=t)
+    got = e.smooth_min_dist(q, sd.SmoothParams(beta=0.5))
+    assert (got.decision_hash == ref.decision_hash).all()
