@@ -164,7 +164,7 @@ def measure_peaks():
     return out
 
 
-def workload(block: int, cfg: int = 2, alpha: float | None = None):
+def workload(block: int, cfg: int = 2, alpha: float | None = None, device: int = 0):
     """cfg2 (headline) or cfg3 (triangles, --config 3): mesh, fp32-rounded
     vertices and queries, and the WeightSet table."""
     from paper_2108_10480_b200 import configs
@@ -184,7 +184,7 @@ def workload(block: int, cfg: int = 2, alpha: float | None = None):
         w = configs.Workload("cfg3 torus 262,144 triangles, exact LSE", V, T, np.full(len(T), 2, np.uint8),
                              alpha=alpha or 100.0)
         import paper_2108_10480_b200 as sd
-        e = sd.Engine(0, sd.SD_FP32)
+        e = sd.Engine(device, sd.SD_FP32)
         e.set_geometry(configs.quantize(V), T, w.kinds)
         wt = e.build_weights()
         e.close()
@@ -610,7 +610,7 @@ def run_ours(args, rank, world, local):
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    w, v, q, wt = workload(rank, args.config, args.alpha)
+    w, v, q, wt = workload(rank, args.config, args.alpha, local)
     global ALPHA, FLOPS_PER_EDGE_PAIR, MUFU_PER_EDGE_PAIR
     if args.config == 3:
         ALPHA = w.alpha
