@@ -150,8 +150,11 @@ class ClockSampler:
                 "samples": len(sm), "source": "nvml" if self.nvml is not None else "nvidia-smi"}
 
 
-def measure_peaks():
+def measure_peaks(device: int = 0):
     L = ctypes.CDLL(os.path.join(ROOT, "paper_2108_10480_b200", "libsdpeaks.so"))
+    L.sd_peaks_set_device.argtypes = [ctypes.c_int]
+    if L.sd_peaks_set_device(device) != 0:
+        return None
     f, d, m = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
     L.sd_measure_peaks.argtypes = [ctypes.POINTER(ctypes.c_double)] * 3
     if L.sd_measure_peaks(ctypes.byref(f), ctypes.byref(d), ctypes.byref(m)) != 0:
@@ -637,7 +640,7 @@ def run_ours(args, rank, world, local):
         eng.query_points_device(qd.data_ptr(), Q, P, sd.SD_EXACT, d_hat.data_ptr(), grad.data_ptr(),
                                 stream=stream.cuda_stream)
 
-    peaks = measure_peaks() if rank == 0 or True else None
+    peaks = measure_peaks(local) if rank == 0 else None  # only rank 0 reports the roofline
     for _ in range(max(3, args.warmup)):
         step()
     torch.cuda.synchronize()

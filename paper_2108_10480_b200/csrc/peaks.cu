@@ -91,7 +91,9 @@ extern "C" {
 // FFMA2 (packed fp32x2) rate in flop/s (each FFMA2 = 2 FMA = 4 flops).
 int sd_measure_ffma2(double* ffma2_flops) {
     int sms = 0;
-    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0) != cudaSuccess) return -1;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return -1;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return -1;
     void* buf = nullptr;
     if (cudaMalloc(&buf, 4096) != cudaSuccess) return -1;
     const int threads = 256, blocks = sms * 8;
@@ -102,10 +104,16 @@ int sd_measure_ffma2(double* ffma2_flops) {
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 
+// Selects the device the measurements run on (this library has its own
+// CUDA runtime state: it does not see the caller's current device).
+int sd_peaks_set_device(int device) { return cudaSetDevice(device) == cudaSuccess ? 0 : -1; }
+
 // Returns 0 on success. Rates in flop/s (FMA = 2 flops) and MUFU ops/s.
 int sd_measure_peaks(double* ffma_flops, double* dfma_flops, double* mufu_ops) {
     int sms = 0;
-    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0) != cudaSuccess) return -1;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return -1;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return -1;
     void* buf = nullptr;
     if (cudaMalloc(&buf, 4096) != cudaSuccess) return -1;
     const int threads = 256, blocks = sms * 8;
