@@ -162,6 +162,21 @@ int sd_query_points_device(sd_ctx* ctx, const void* q_dev, int64_t Q, const sd_p
 int sd_finalize_device(sd_ctx* ctx, const double* c, const double* grad_c, int64_t Q, const sd_params* p,
                        double* d_hat, double* grad, void* stream);
 
+/* Primitive-sharded merge through peer memory (the alternative to one
+ * all-reduce of the partial sums). Queries are owned in blocks of
+ * q_per_owner: query i belongs to rank i / q_per_owner. Every rank calls
+ * sd_scatter_partials with its unshifted partials (c, grad_c as written by
+ * sd_query_points_device) and a DEVICE array of the world ranks' symmetric
+ * buffers (each world x 4 x q_per_owner doubles, e.g. torch symmetric
+ * memory): its contribution to query i is stored into the owner's buffer.
+ * After a cross-rank barrier each rank calls sd_reduce_owned on its own
+ * buffer: the world contributions of its n_owned queries are summed in rank
+ * order and finalised (result_from_accum) into d_hat / grad. */
+int sd_scatter_partials(sd_ctx* ctx, const double* c, const double* grad_c, int64_t Q, double* const* peer_bufs,
+                        int32_t world, int32_t rank, int64_t q_per_owner, void* stream);
+int sd_reduce_owned(sd_ctx* ctx, const double* sbuf, int64_t q_per_owner, int64_t n_owned, int32_t world,
+                    const sd_params* p, double* d_hat, double* grad, void* stream);
+
 /* Mesh-to-mesh smooth distance d_hat(M, Mq) for a POINT-CLOUD query mesh
  * (smooth_mesh_dist, smooth.hpp:212-255): inner smooth distances of the Nq
  * query points (mode SD_EXACT or SD_BVH, params p), outer LogSumExp with

@@ -40,6 +40,8 @@ EXPORTED_SYMBOLS = (
     "sd_mesh_dist_points",
     "sd_query_simplices",
     "sd_mesh_dist",
+    "sd_scatter_partials",
+    "sd_reduce_owned",
     "sd_render",
     "sd_grid_benchmark",
     "sd_write_ppm",
@@ -118,6 +120,8 @@ def lib():
             "sd_query_simplices": (C.c_int, [vp, vp, vp, i64, P(_Params), C.c_int, P(_Outputs)]),
             "sd_mesh_dist": (C.c_int, [vp, vp, i64, vp, vp, i64, P(_Params), f64, C.c_int, vp, vp, vp]),
             "sd_render": (C.c_int, [vp, P(_Params), C.c_int, P(_RenderConfig), vp, vp, vp, vp]),
+            "sd_scatter_partials": (C.c_int, [vp, vp, vp, i64, vp, i32, i32, i64, vp]),
+            "sd_reduce_owned": (C.c_int, [vp, vp, i64, i64, i32, P(_Params), vp, vp, vp]),
             "sd_grid_benchmark": (C.c_int, [vp, P(_Params), C.c_int, i32, vp, vp, vp, vp]),
             "sd_write_ppm": (C.c_int, [vp, i32, i32, C.c_char_p]),
             "sd_write_png": (C.c_int, [vp, i32, i32, C.c_char_p]),
@@ -304,6 +308,21 @@ class Engine:
         _check(lib().sd_finalize_device(self.h, C.c_void_p(c_ptr), C.c_void_p(grad_c_ptr), n, C.byref(params._c()),
                                         C.c_void_p(d_hat_ptr), C.c_void_p(grad_ptr) if grad_ptr else None,
                                         C.c_void_p(stream) if stream else None))
+
+    def scatter_partials(self, c_ptr: int, grad_c_ptr: int, n: int, peer_table_ptr: int, world: int, rank: int,
+                         q_per_owner: int, stream: int | None = None):
+        """Store this rank's partial sums into the owners' symmetric buffers
+        (peer_table_ptr: device array of the world buffer pointers)."""
+        _check(lib().sd_scatter_partials(self.h, C.c_void_p(c_ptr), C.c_void_p(grad_c_ptr), n,
+                                         C.c_void_p(peer_table_ptr), world, rank, q_per_owner,
+                                         C.c_void_p(stream) if stream else None))
+
+    def reduce_owned(self, sbuf_ptr: int, q_per_owner: int, n_owned: int, world: int, params: SmoothParams,
+                     d_hat_ptr: int, grad_ptr: int | None, stream: int | None = None):
+        """Sum the world contributions of this rank's owned queries and finalise."""
+        _check(lib().sd_reduce_owned(self.h, C.c_void_p(sbuf_ptr), q_per_owner, n_owned, world, C.byref(params._c()),
+                                     C.c_void_p(d_hat_ptr), C.c_void_p(grad_ptr) if grad_ptr else None,
+                                     C.c_void_p(stream) if stream else None))
 
     def last_launch_count(self) -> int:
         n = C.c_int64()

@@ -1003,6 +1003,35 @@ int sd_finalize_device(sd_ctx* c, const double* cs, const double* gc, int64_t Q,
     });
 }
 
+int sd_scatter_partials(sd_ctx* c, const double* cs, const double* gc, int64_t Q, double* const* peer_bufs,
+                        int32_t world, int32_t rank, int64_t q_per_owner, void* stream) {
+    return guard([&] {
+        if (!c) throw ArgError{"ctx is NULL"};
+        if (Q < 0 || world < 1 || rank < 0 || rank >= world || q_per_owner <= 0 || q_per_owner * world < Q ||
+            (Q > 0 && (!cs || !gc || !peer_bufs)))
+            throw ArgError{"bad exchange arguments"};
+        DeviceScope ds(c->device);
+        check_cuda(launch_scatter_partials(cs, gc, Q, peer_bufs, rank, q_per_owner, static_cast<cudaStream_t>(stream)),
+                   "scatter partials");
+        c->last_launches = Q > 0 ? 1 : 0;
+    });
+}
+
+int sd_reduce_owned(sd_ctx* c, const double* sbuf, int64_t q_per_owner, int64_t n_owned, int32_t world,
+                    const sd_params* p, double* d_hat, double* grad, void* stream) {
+    return guard([&] {
+        if (!c) throw ArgError{"ctx is NULL"};
+        check_params(p);
+        if (q_per_owner <= 0 || n_owned < 0 || n_owned > q_per_owner || world < 1 || (n_owned > 0 && (!sbuf || !d_hat)))
+            throw ArgError{"bad exchange arguments"};
+        DeviceScope ds(c->device);
+        check_cuda(launch_reduce_owned(sbuf, q_per_owner, n_owned, world, p->alpha, p->epsilon, d_hat, grad,
+                                       static_cast<cudaStream_t>(stream)),
+                   "reduce owned");
+        c->last_launches = n_owned > 0 ? 1 : 0;
+    });
+}
+
 int sd_mesh_dist_points(sd_ctx* c, const double* qxyz, int64_t Vq, const int32_t* qpoints, int64_t Nq,
                         const sd_params* p, double alpha_q, int mode, double* d_hat, double* vertex_grads,
                         double* per_primitive) {

@@ -162,6 +162,68 @@ cudaError_t launch_empty_result(int64_t Q, const FinalizeOut& out, cudaStream_t 
     return cudaGetLastError();
 }
 
+// --------------------------------- primitive-sharded exchange
+// Instead of an all-reduce of the per-query partial sums, rank r stores its
+// unshifted partials (c, grad_c) of query i straight into the symmetric
+// buffer of the query's owner o = i / qown (NVLink stores through the
+// peer pointer table; layout [world][4][qown] SoA), and each owner then sums
+// the world contributions of its queries in rank order and finalises them
+// (result_from_accum, smooth.hpp:147-159): a reduce-scatter done by the
+// producing ranks' own stores, half the traffic of an all-reduce.
+__global__ void scatter_partials_kernel(const double* __restrict__ c, const double* __restrict__ gc, int64_t Q,
+                                        double* const* __restrict__ peers, int rank, int64_t qown) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= Q) return;
+    const int64_t o = i / qown, j = i - o * qown;
+    double* dst = peers[o] + size_t(rank) * 4 * qown + j;
+    dst[0] = c[i];
+    dst[qown] = gc[3 * i];
+    dst[2 * qown] = gc[3 * i + 1];
+    dst[3 * qown] = gc[3 * i + 2];
+}
+
+__global__ void reduce_owned_kernel(const double* __restrict__ sbuf, int64_t qown, int64_t n, int world, double alpha,
+                                    double eps, double* d_hat, double* grad) {
+    const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    double c = 0.0, gx = 0.0, gy = 0.0, gz = 0.0;
+    for (int r = 0; r < world; ++r) {
+        const double* p = sbuf + size_t(r) * 4 * qown + j;
+        c += p[0];
+        gx += p[qown];
+        gy += p[2 * qown];
+        gz += p[3 * qown];
+    }
+    double d = INFINITY, ax = 0, ay = 0, az = 0;
+    if (c > 0.0) {
+        d = -log(c) / alpha;
+        const double den = c + eps;
+        ax = gx / den;
+        ay = gy / den;
+        az = gz / den;
+    }
+    d_hat[j] = d;
+    if (grad) {
+        grad[3 * j] = ax;
+        grad[3 * j + 1] = ay;
+        grad[3 * j + 2] = az;
+    }
+}
+
+cudaError_t launch_scatter_partials(const double* c, const double* grad_c, int64_t Q, double* const* peers, int rank,
+                                    int64_t qown, cudaStream_t st) {
+    if (Q <= 0) return cudaSuccess;
+    scatter_partials_kernel<<<unsigned((Q + 255) / 256), 256, 0, st>>>(c, grad_c, Q, peers, rank, qown);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_reduce_owned(const double* sbuf, int64_t qown, int64_t n, int world, double alpha, double epsilon,
+                                double* d_hat, double* grad, cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    reduce_owned_kernel<<<unsigned((n + 255) / 256), 256, 0, st>>>(sbuf, qown, n, world, alpha, epsilon, d_hat, grad);
+    return cudaGetLastError();
+}
+
 // ------------------------------------------ mesh-to-mesh outer LogSumExp
 // smooth.hpp:237-254: mass_j = exp(-alpha_q d_j); denom = sum_j mass_j;
 // vertex gradient = sum over the simplices at the vertex of mass_j / n_j

@@ -53,6 +53,12 @@ cudaError_t launch_finalize(const double* part, int splits, int64_t Q, double al
 cudaError_t launch_finalize_sums(const double* c, const double* grad_c, int64_t Q, double alpha, double epsilon,
                                  double* d_hat, double* grad, cudaStream_t st);
 
+// Primitive-sharded exchange through peer memory (epilogue.cu).
+cudaError_t launch_scatter_partials(const double* c, const double* grad_c, int64_t Q, double* const* peers, int rank,
+                                    int64_t qown, cudaStream_t st);
+cudaError_t launch_reduce_owned(const double* sbuf, int64_t qown, int64_t n, int world, double alpha, double epsilon,
+                                double* d_hat, double* grad, cudaStream_t st);
+
 // Mesh-to-mesh outer LogSumExp (smooth.hpp:237-254); vidx stride 1: point
 // simplices, stride 3: corner lists (-1 padded).
 cudaError_t launch_mesh_reduce(const double* d, const double* grad, int64_t n, const int32_t* vidx, int stride,

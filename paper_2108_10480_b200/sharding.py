@@ -11,7 +11,10 @@ Two regimes:
   term); ONE all_reduce(SUM) of 4 doubles per query then gives exactly the
   whole-mesh sums, and result_from_accum (smooth.hpp:147-159) finishes.
   The WeightSet is built on the full mesh (A and sup w~ are global,
-  weights.hpp:604,616) and sliced per shard.
+  weights.hpp:604,616) and sliced per shard. Instead of the all-reduce the
+  ranks can also store their partials straight into the owner's symmetric
+  buffer (sd_scatter_partials over peer memory) and each owner finalises
+  its block of queries (sd_reduce_owned): owner_blocks gives the blocks.
 """
 from __future__ import annotations
 
@@ -104,3 +107,28 @@ def allreduce_partials(c, grad_c, group=None):
     c.copy_(buf[:, 0])
     grad_c.copy_(buf[:, 1:].reshape(grad_c.shape))
     return c, grad_c
+
+
+def owner_blocks(n: int, world: int) -> tuple[int, list[int]]:
+    """Peer-memory exchange ownership: query i belongs to rank i // per, per
+    = ceil(n / world); returns per and the number of queries each rank owns."""
+    per = max(1, -(-n // world))
+    return per, [max(0, min(per, n - r * per)) for r in range(world)]
+
+
+def exchange_reference(partials, per: int):
+    """What the owners hold after every rank scattered its partials: for
+    owner o, the sum over ranks (in rank order) of (c, grad_c) of its block.
+    partials: list over ranks of (c (n,), grad_c (n, 3))."""
+    n = len(partials[0][0])
+    world = len(partials)
+    out = []
+    for o in range(world):
+        lo, hi = o * per, min(n, (o + 1) * per)
+        c = np.zeros(max(0, hi - lo))
+        g = np.zeros((max(0, hi - lo), 3))
+        for r in range(world):
+            c = c + partials[r][0][lo:hi]
+            g = g + partials[r][1][lo:hi]
+        out.append((c, g))
+    return out

@@ -649,3 +649,62 @@ def test_auto_tree_picks_the_smaller_surface_area_cost(sd, oracle):
     ref = O.query(m, O.Weights.build(m), q, O.Params(beta=0.5), tree=t)
     got = e.smooth_min_dist(q, sd.SmoothParams(beta=0.5))
     assert (got.decision_hash == ref.decision_hash).all()
+
+
+
+def test_peer_exchange_with_virtual_ranks(sd, oracle):
+    """The peer-memory merge of the primitive-sharded path (sd_scatter_partials
+    + sd_reduce_owned) with 4 virtual ranks on one GPU: each rank's engine
+    stores its partials into the four owners' buffers through a device
+    pointer table, exactly as over NVLink, then every owner finalises its
+    block. Equal to summing the partials and finalising (the all-reduce
+    path), and to the oracle on the whole mesh."""
+    import torch
+    from paper_2108_10480_b200 import sharding
+    O = oracle
+    m = O.random_scene(11, 400)
+    q = O.QueryStream(61).draw_points(m, 700)
+    wt = O.Weights.build(m).table
+    world = 4
+    shards = sharding.primitive_shards(m.vertices, m.simplices, m.kinds, wt.poly_index, world)
+    P = sd.SmoothParams(alpha=100.0, beta=0.0)
+    dev = torch.device("cuda", 0)
+    n = len(q)
+    per, counts = sharding.owner_blocks(n, world)
+    sbufs = [torch.zeros(world * 4 * per, dtype=torch.float64, device=dev) for _ in range(world)]
+    table = torch.tensor([b.data_ptr() for b in sbufs], dtype=torch.int64, device=dev)
+    qd = torch.tensor(q, dtype=torch.float64, device=dev)
+    partials = []
+    for r, s in enumerate(shards):
+        e = sd.Engine(0, sd.SD_FP64)
+        e.set_geometry(s.vertices, s.simplices, s.kinds)
+        e.set_weights(wt.A, wt.sup_wtilde, wt.edge_a, wt.tri_stored, s.poly_index)
+        c = torch.empty(n, dtype=torch.float64, device=dev)
+        g = torch.empty(n, 3, dtype=torch.float64, device=dev)
+        d = torch.empty(n, dtype=torch.float64, device=dev)
+        e.query_points_device(qd.data_ptr(), n, P, sd.SD_EXACT, d.data_ptr(), c_ptr=c.data_ptr(),
+                              grad_c_ptr=g.data_ptr())
+        e.scatter_partials(c.data_ptr(), g.data_ptr(), n, table.data_ptr(), world, r, per)
+        torch.cuda.synchronize()
+        partials.append((c.cpu().numpy(), g.cpu().numpy()))
+    expect = sharding.exchange_reference(partials, per)
+    d_all = np.zeros(n)
+    for o in range(world):
+        sb = sbufs[o].cpu().numpy().reshape(world, 4, per)
+        lo = o * per
+        for r in range(world):  # rank r's contribution landed in owner o's slot r
+            assert np.array_equal(sb[r, 0, :counts[o]], partials[r][0][lo:lo + counts[o]])
+            assert np.array_equal(sb[r, 1:, :counts[o]].T, partials[r][1][lo:lo + counts[o]])
+        dd = torch.empty(max(1, counts[o]), dtype=torch.float64, device=dev)
+        gg = torch.empty(max(1, counts[o]), 3, dtype=torch.float64, device=dev)
+        e.reduce_owned(sbufs[o].data_ptr(), per, counts[o], world, P, dd.data_ptr(), gg.data_ptr())
+        torch.cuda.synchronize()
+        rd, rg = sharding.finalize(expect[o][0], expect[o][1], 100.0)
+        got = dd.cpu().numpy()[:counts[o]]
+        fin = np.isfinite(rd)
+        assert (np.isfinite(got) == fin).all()
+        assert np.abs(got[fin] - rd[fin]).max(initial=0.0) <= 1e-14 * max(1.0, np.abs(rd[fin]).max(initial=0.0))
+        d_all[lo:lo + counts[o]] = got
+    whole = O.query(m, O.Weights.from_table(wt), q, O.Params(alpha=100.0, beta=0.0))
+    fin = np.isfinite(whole.d_hat)
+    assert np.abs(d_all[fin] - whole.d_hat[fin]).max() < 1e-10

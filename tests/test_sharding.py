@@ -111,3 +111,15 @@ def test_primitive_sharded_bvh_is_conservative_gloo(oracle):
     m = oracle.random_scene(4, 200)
     ref = oracle.query(m, oracle.Weights.build(m), q, oracle.Params(alpha=100.0, beta=0.0))
     assert (d <= ref.d_hat + 1e-9).all()
+
+
+
+def test_owner_blocks_cover_every_query_once():
+    from paper_2108_10480_b200 import sharding
+    for n, world in ((0, 1), (1, 8), (7, 8), (1000, 3), (16777216, 8), (5, 2)):
+        per, counts = sharding.owner_blocks(n, world)
+        assert sum(counts) == n and len(counts) == world
+        assert all(0 <= c <= per for c in counts)
+        assert per * world >= n
+        owners = [i // per for i in range(min(n, 50))]
+        assert all(0 <= o < world for o in owners)
