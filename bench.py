@@ -392,10 +392,42 @@ def run_cfg5(args, rank, world, local):
 
     launches = [0]
 
+    # merge: one NCCL all_reduce of the partials (default), or the peer-memory
+    # exchange (--exchange peer): every rank stores its partials into the
+    # owners' symmetric buffers (torch symmetric memory), a device barrier,
+    # and each owner finalises its block of queries
+    exchange = args.exchange
+    per, counts = sharding.owner_blocks(Q, world)
+    hdl = None
+    if exchange == "peer":
+        try:
+            if world > 1:
+                import torch.distributed._symmetric_memory as symm_mem
+                sbuf = symm_mem.empty(world * 4 * per, dtype=torch.float64, device=dev)
+                hdl = symm_mem.rendezvous(sbuf, torch.distributed.group.WORLD.group_name)
+                ptrs = list(hdl.buffer_ptrs)
+            else:
+                sbuf = torch.zeros(world * 4 * per, dtype=torch.float64, device=dev)
+                ptrs = [sbuf.data_ptr()]
+            table = torch.tensor(ptrs, dtype=torch.int64, device=dev)
+        except Exception as ex:  # noqa: BLE001 -- fall back to the all-reduce
+            exchange = f"nccl (peer exchange unavailable: {type(ex).__name__}: {ex})"
+
     def step():
         eng.query_points_device(qd.data_ptr(), Q, P, sd.SD_BVH, d_hat.data_ptr(), c_ptr=buf.data_ptr(),
                                 grad_c_ptr=buf.data_ptr() + 8 * Q, stream=stream.cuda_stream)
-        launches[0] = eng.last_launch_count() + 1  # + the finalize kernel below
+        launches[0] = eng.last_launch_count() + 1  # + the finalize / reduce kernel below
+        if exchange == "peer":
+            eng.scatter_partials(buf.data_ptr(), buf.data_ptr() + 8 * Q, Q, table.data_ptr(), world, rank, per,
+                                 stream=stream.cuda_stream)
+            if hdl is not None:
+                hdl.barrier(channel=0)
+            eng.reduce_owned(sbuf.data_ptr(), per, counts[rank], world, P, d_hat.data_ptr(), grad.data_ptr(),
+                             stream=stream.cuda_stream)
+            if hdl is not None:  # owners done reading before the next step's stores
+                hdl.barrier(channel=1)
+            launches[0] += 1
+            return
         if world > 1:
             torch.distributed.all_reduce(buf, op=torch.distributed.ReduceOp.SUM)
         eng.finalize_device(buf.data_ptr(), buf.data_ptr() + 8 * Q, Q, P, d_hat.data_ptr(), grad.data_ptr(),
@@ -424,7 +456,8 @@ def run_cfg5(args, rank, world, local):
         torch.distributed.barrier()
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
     ms = float(t.item())
-    fin = float(torch.isfinite(d_hat).double().mean().item())
+    nres = counts[rank] if exchange == "peer" else Q  # peer exchange: this rank's block of results
+    fin = float(torch.isfinite(d_hat[:nres]).double().mean().item())
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         # the oracle port on 4,096 of the queries, same tree and table
@@ -450,8 +483,10 @@ def run_cfg5(args, rank, world, local):
                 "config": {"workload": "cfg5: 64 rotated cfg3 tori (16,777,216 triangles) + 1M edges + 1M points, "
                                        "16,777,216 queries uniform in the scene AABB, alpha=100, beta=0.5, fp32 "
                                        "(BASELINE configs[4])",
-                           "parallelism": f"primitive-sharded x{world} (Morton shards, {tree_name()} per shard), one "
-                                          f"NCCL all_reduce(SUM) of 4 fp64 per query",
+                           "parallelism": f"primitive-sharded x{world} (Morton shards, {tree_name()} per shard), "
+                                          + ("partials stored into the owners' symmetric buffers over peer memory, "
+                                             "owner-side reduce + finalize" if exchange == "peer" else
+                                             f"one NCCL all_reduce(SUM) of 4 fp64 per query; exchange={exchange}"),
                            "primitives_per_gpu": len(sh.kinds), "l2": "flushed between timed steps"},
                 "finite_fraction": fin, "gpu_launches": launches[0] * args.steps, "cpu_baseline": cpu,
                 "setup_s": {"total": setup, "generate": tg, "build_weights": tw, "build_tree": tb},
@@ -758,6 +793,8 @@ def main():
     ap.add_argument("--m2m", action="store_true", help="mesh-to-mesh evaluations of the paper's timing table rows")
     ap.add_argument("--rows", default="", help="comma-separated sim_rows names for --m2m (default: all)")
     ap.add_argument("--render", action="store_true", help="sphere tracer beta ablation + grid benchmark (callers)")
+    ap.add_argument("--exchange", choices=["nccl", "peer"], default="nccl",
+                    help="--config 5 merge: NCCL all-reduce or stores into the owners' buffers over peer memory")
     ap.add_argument("--alpha", type=float, default=None, help="alpha for --config 3 (10, 100 or 1000)")
     args = ap.parse_args()
     rank, world, local = dist_env()
