@@ -734,8 +734,9 @@ def run_ours(args, rank, world, local):
         roof = {"bound": "fp64-fma" if fp64 else "fp32-fma", "achieved": achieved, "unit": "TFLOP/s",
                 "traffic": traffic, "traffic_unit": "bytes per launch (ncu dram__bytes_read+write)",
                 "algorithmic_bytes": Q * 12 + N * 48,
-                "kernel": ("exact_kernel<float, edge, poly> x3 segment launches" if args.config == 2 else
-                           "exact_kernel<float, triangle, poly>") + " + finalize (step time)",
+                "kernel": (f"exact_kernel<{'double' if fp64 else 'float'}, "
+                           + {1: "point>", 2: "edge, poly> x3 segment launches", 3: "triangle, poly>"}[args.config]
+                           + " + finalize (step time)"),
                 "algorithmic": f"{FLOPS_PER_EDGE_PAIR} flop x {pairs_per_rank} pairs per step (SURVEY 8d)"}
         if peaks:
             pk = peaks["dfma_tflops"] if fp64 else peaks["ffma_tflops"]

@@ -354,7 +354,7 @@ static void exact_query(Ctx& c, const T* q, int64_t Q, const sd_params& p, const
     const Segment* big = &c.segs[0];
     for (const Segment& s : c.segs)
         if (s.count > maxcount) maxcount = s.count, big = &s;
-    const int64_t qpc = exact_queries_per_cta(big->kind);
+    const int64_t qpc = exact_queries_per_cta<T>(big->kind);
     const int64_t qblocks = (Q + qpc - 1) / qpc;
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device);

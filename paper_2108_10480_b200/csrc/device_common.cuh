@@ -35,11 +35,77 @@ template <> struct Math<float> {
         return y;
     }
 };
+// fp64: branch-free kernels on the DFMA pipe for the argument ranges the
+// accumulator produces (the library routines carry special-case branches
+// and slow-path calls that dominated the fp64 exact kernel). Accuracy
+// ~1-2 ulp; coefficients from tools/fp64_poly_fit.py.
 template <> struct Math<double> {
-    static __device__ __forceinline__ double ex2(double x) { return exp2(x); }
-    static __device__ __forceinline__ double lg2(double x) { return log2(x); }
-    static __device__ __forceinline__ double rsqrt(double x) { return ::rsqrt(x); }
-    static __device__ __forceinline__ double rcp(double x) { return 1.0 / x; }
+    // 2^x for x <= 1023; x < -1020 (incl. -inf, a masked term) gives 0 --
+    // the sums only ever see x = exponent - running shift <= 0, where a
+    // term below 2^-1020 of the largest one is below fp64 resolution.
+    static __device__ __forceinline__ double ex2(double x) {
+        const double big = 6755399441055744.0;  // 1.5 * 2^52: x + big rounds x to an integer
+        const double t = x + big;
+        const double f = x - (t - big);  // [-1/2, 1/2]
+        double p = 4.4558179083360645e-10;
+        p = fma(p, f, 7.074194297288521e-09);
+        p = fma(p, f, 1.0178057087733941e-07);
+        p = fma(p, f, 1.3215432535912375e-06);
+        p = fma(p, f, 1.5252733841556773e-05);
+        p = fma(p, f, 0.00015403530463724353);
+        p = fma(p, f, 0.001333355814640647);
+        p = fma(p, f, 0.009618129107587256);
+        p = fma(p, f, 0.055504108664821625);
+        p = fma(p, f, 0.24022650695910158);
+        p = fma(p, f, 0.6931471805599453);
+        p = fma(p, f, 1.0);
+        const int n = __double2loint(t);  // the integer, two's complement in the low word
+        const double r = __hiloint2double(__double2hiint(p) + (n << 20), __double2loint(p));
+        return x < -1020.0 ? 0.0 : r;
+    }
+    // log2 x for positive normal x (callers select away other inputs):
+    // x = 2^e m, m in [sqrt(1/2), sqrt2), log2 m = z g(z^2), z = (m-1)/(m+1).
+    static __device__ __forceinline__ double lg2(double x) {
+        int hi = __double2hiint(x);
+        int e = (hi >> 20) - 1023;
+        hi = (hi & 0x000fffff) | 0x3ff00000;
+        const bool up = hi > 0x3ff6a09e;
+        hi = up ? hi - 0x00100000 : hi;
+        e = up ? e + 1 : e;
+        const double m = __hiloint2double(hi, __double2loint(x));
+        const double num = m - 1.0, den = m + 1.0;
+        const double r = rcp(den);
+        double z = num * r;
+        z = fma(r, fma(-z, den, num), z);
+        const double w = z * z;
+        double g = 0.21365920165930558;
+        g = fma(g, w, 0.22091306083083528);
+        g = fma(g, w, 0.2623343533779628);
+        g = fma(g, w, 0.3205985348978951);
+        g = fma(g, w, 0.4121985858410509);
+        g = fma(g, w, 0.5770780163455196);
+        g = fma(g, w, 0.9617966939259898);
+        g = fma(g, w, 2.8853900817779268);
+        return fma(z, g, double(e));
+    }
+    // 1/sqrt(x) for positive normal x: MUFU seed + two Newton steps
+    static __device__ __forceinline__ double rsqrt(double x) {
+        double y;
+        asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+        double e = fma(-(x * y), y, 1.0);
+        y = fma(0.5 * y, e, y);
+        e = fma(-(x * y), y, 1.0);
+        return fma(0.5 * y, e, y);
+    }
+    // 1/x for finite nonzero normal x: MUFU seed + two Newton steps
+    static __device__ __forceinline__ double rcp(double x) {
+        double r;
+        asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+        double e = fma(-x, r, 1.0);
+        r = fma(r, e, r);
+        e = fma(-x, r, 1.0);
+        return fma(r, e, r);
+    }
 };
 
 // Vector types used to read records out of shared memory (16 B loads).

@@ -54,8 +54,8 @@ constexpr int tile_prims() {
     return KIND == 0 ? 512 : 128;
 }
 
-template <class T, int KIND, bool POLY, bool SAFE, int QPT>
-__global__ void __launch_bounds__(kThreads) exact_kernel(const __grid_constant__ ExactArgs<T> a) {
+template <class T, int KIND, bool POLY, bool SAFE, int QPT, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) exact_kernel(const __grid_constant__ ExactArgs<T> a) {
     constexpr int R = rec_size(KIND);
     constexpr int TILE = tile_prims<T, KIND>();
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -255,50 +255,67 @@ __global__ void __launch_bounds__(kThreads) exact_kernel(const __grid_constant__
     }
 }
 
-template <int KIND>
+// Queries per thread (amortise record loads) and the launch-bounds CTA
+// floor per (type, kind). fp64 values from tools/fp64_sweep.sh on a B200
+// (ms per evaluation, QPT 1/2/4 x floor 1/2): points QPT 2 (cfg1 0.886 ms vs
+// 0.906 / 1.001-1.183), edges QPT 2 with 2 CTAs/SM (cfg2 32.2 ms vs
+// 33.5-37.2), triangles QPT 1 with 2 CTAs/SM (cfg3 torus, 32k queries:
+// 109.5 ms vs 114.7-125.6).
+template <class T, int KIND>
 constexpr int qpt_for() {
-    return KIND == 2 ? 2 : 4;  // queries per thread: amortise record loads
+    if constexpr (sizeof(T) == 4) return KIND == 2 ? 2 : 4;
+    else return KIND == 2 ? 1 : 2;
+}
+template <class T, int KIND>
+constexpr int minb_for() {
+    return sizeof(T) == 8 && KIND != 0 ? 2 : 1;
+}
+
+template <class T, int KIND, int QPT>
+static size_t smem_bytes() {
+    return size_t(kStages) * tile_prims<T, KIND>() * rec_size(KIND) * sizeof(T) + size_t(QPT) * kThreads * sizeof(Tot);
+}
+
+template <class T, int KIND, bool POLY, bool SAFE, class F>
+static auto with_kernel(F&& f) {
+    constexpr int QPT = qpt_for<T, KIND>();
+    return f(exact_kernel<T, KIND, POLY, SAFE, QPT, minb_for<T, KIND>()>, smem_bytes<T, KIND, QPT>(), QPT);
 }
 
 template <class T, int KIND, bool POLY, bool SAFE>
 static cudaError_t launch_one(const ExactLaunch<T>& L, cudaStream_t st) {
-    constexpr int R = rec_size(KIND);
-    constexpr int TILE = tile_prims<T, KIND>();
-    constexpr int QPT = qpt_for<KIND>();
-    const size_t smem = size_t(kStages) * TILE * R * sizeof(T) + size_t(QPT) * kThreads * sizeof(Tot);
-    auto kern = exact_kernel<T, KIND, POLY, SAFE, QPT>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    if (e != cudaSuccess) return e;
-    ExactArgs<T> a;
-    a.rec = L.rec;
-    a.count = L.count;
-    a.chunk = L.chunk;
-    a.q = L.q;
-    a.Q = L.Q;
-    a.part = L.part;
-    a.first = L.first;
-    a.ph = L.ph;
-    a.poly = L.poly;
-    a.perm = L.perm;
-    a.tbox = L.tbox;
-    a.lwmax = L.lwmax;
-    a.lwspan = L.lwspan;
-    const int64_t qblocks = (L.Q + int64_t(kThreads) * QPT - 1) / (int64_t(kThreads) * QPT);
-    dim3 grid(unsigned(qblocks), unsigned(L.splits));
-    kern<<<grid, kThreads, smem, st>>>(a);
-    return cudaGetLastError();
+    return with_kernel<T, KIND, POLY, SAFE>([&](auto kern, size_t smem, int QPT) -> cudaError_t {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        if (e != cudaSuccess) return e;
+        ExactArgs<T> a;
+        a.rec = L.rec;
+        a.count = L.count;
+        a.chunk = L.chunk;
+        a.q = L.q;
+        a.Q = L.Q;
+        a.part = L.part;
+        a.first = L.first;
+        a.ph = L.ph;
+        a.poly = L.poly;
+        a.perm = L.perm;
+        a.tbox = L.tbox;
+        a.lwmax = L.lwmax;
+        a.lwspan = L.lwspan;
+        const int64_t qblocks = (L.Q + int64_t(kThreads) * QPT - 1) / (int64_t(kThreads) * QPT);
+        dim3 grid(unsigned(qblocks), unsigned(L.splits));
+        kern<<<grid, kThreads, smem, st>>>(a);
+        return cudaGetLastError();
+    });
 }
 
 template <class T, int KIND, bool POLY, bool SAFE>
 static int occupancy_one() {
-    constexpr int R = rec_size(KIND);
-    constexpr int TILE = tile_prims<T, KIND>();
-    const size_t smem = size_t(kStages) * TILE * R * sizeof(T) + size_t(qpt_for<KIND>()) * kThreads * sizeof(Tot);
-    auto kern = exact_kernel<T, KIND, POLY, SAFE, qpt_for<KIND>()>;
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess) return 1;
-    int n = 1;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, kThreads, smem) != cudaSuccess) return 1;
-    return n > 0 ? n : 1;
+    return with_kernel<T, KIND, POLY, SAFE>([&](auto kern, size_t smem, int) -> int {
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess) return 1;
+        int n = 1;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, kThreads, smem) != cudaSuccess) return 1;
+        return n > 0 ? n : 1;
+    });
 }
 
 template <class T>
@@ -314,9 +331,13 @@ template int exact_blocks_per_sm<double>(int, bool, bool);
 
 int exact_tile_prims(int kind) { return kind == 0 ? tile_prims<float, 0>() : tile_prims<float, 1>(); }
 
+template <class T>
 int64_t exact_queries_per_cta(int kind) {
-    return int64_t(kThreads) * (kind == 2 ? qpt_for<2>() : qpt_for<1>());
+    const int q = kind == 0 ? qpt_for<T, 0>() : (kind == 1 ? qpt_for<T, 1>() : qpt_for<T, 2>());
+    return int64_t(kThreads) * q;
 }
+template int64_t exact_queries_per_cta<float>(int);
+template int64_t exact_queries_per_cta<double>(int);
 
 template <class T>
 cudaError_t launch_exact(const ExactLaunch<T>& L, cudaStream_t st) {

@@ -32,6 +32,7 @@ struct ExactLaunch {
 
 template <class T>
 cudaError_t launch_exact(const ExactLaunch<T>& L, cudaStream_t st);
+template <class T>
 int64_t exact_queries_per_cta(int kind);
 int exact_tile_prims(int kind);  // primitives per staged tile (tile boxes use the same grid)
 template <class T>
