@@ -252,8 +252,12 @@ def measure_bvh(args, rank, world, local, eng_cls, dev, stream, flush, peaks):
     import paper_2108_10480_b200 as sd
     from paper_2108_10480_b200 import configs
     t0 = time.perf_counter()
-    w, q = configs.cfg4(block=rank)
+    strong = args.bvh_strong
+    # weak (default): every rank its own cfg4 batch; strong: ONE batch split
+    # into Morton-contiguous blocks of equal estimated cost
+    w, q = configs.cfg4(block=0 if strong else rank)
     v, q = configs.quantize(w.vertices), configs.quantize(q)
+    Q_total = len(q) * (1 if strong else world)
     eng = sd.Engine(local, sd.SD_FP32)
     eng.set_geometry(v, w.simplices, w.kinds)
     tw = time.perf_counter()
@@ -263,8 +267,23 @@ def measure_bvh(args, rank, world, local, eng_cls, dev, stream, flush, peaks):
     # BENCH_TREE=median builds the reference's median-split tree instead (A/B)
     eng.build_bvh(tree_method(sd))
     tb = time.perf_counter() - tb
-    Q = len(q)
     P = sd.SmoothParams(alpha=w.alpha, alpha_u=600.0, beta=w.beta)
+    balance = None
+    if strong:
+        from paper_2108_10480_b200 import sharding
+
+        def counters(sub):
+            r = eng.smooth_min_dist(sub, P)
+            return r.leaves, r.far_field
+
+        order = sharding.morton_order(q)
+        est = sharding.estimate_query_costs(counters, q[order], stride=64)
+        ranges = sharding.balanced_ranges(est, world)
+        lo, hi = ranges[rank]
+        q = np.ascontiguousarray(q[order[lo:hi]])
+        balance = {"ranges": ranges, "estimated_cost_share": [float(est[a:b].sum() / est.sum()) for a, b in ranges],
+                   "estimate": "strided sample (1/64) of the Morton-sorted batch, popped nodes 2(L+F)-1"}
+    Q = len(q)
     qd = torch.tensor(q, dtype=torch.float32, device=dev)
     d_hat = torch.empty(Q, dtype=torch.float64, device=dev)
     grad = torch.empty(Q, 3, dtype=torch.float64, device=dev)
@@ -299,20 +318,31 @@ def measure_bvh(args, rank, world, local, eng_cls, dev, stream, flush, peaks):
     if world > 1:
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
     ms = float(t.item())
-    pops = 2 * (L + F) - Q
-    flops = FLOPS_BOX_TEST * pops + FLOPS_FAR_TERM * F + FLOPS_PER_TRI_PAIR * L
-    nbytes = BYTES_NODE * pops + BYTES_LEAF * L
-    out = {"metric": "BVH queries/s (value+grad)", "value": world * Q / (ms * 1e-3), "unit": "queries/s",
+    if world > 1:  # counters summed over ranks (per-query means below are whole-job)
+        lf = torch.tensor([L, F, float(Q)], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(lf)
+        L, F, Qsum = (float(x) for x in lf.tolist())
+    else:
+        Qsum = float(Q)
+    pops = 2 * (L + F) - Qsum
+    # algorithmic work per GPU per step (whole-job / ranks), over the
+    # max-over-ranks step time: the roofline is a per-GPU figure
+    flops = (FLOPS_BOX_TEST * pops + FLOPS_FAR_TERM * F + FLOPS_PER_TRI_PAIR * L) / world
+    nbytes = (BYTES_NODE * pops + BYTES_LEAF * L) / world
+    out = {"metric": "BVH queries/s (value+grad)", "value": Q_total / (ms * 1e-3), "unit": "queries/s",
+           "scaling": "strong" if strong else "weak",
            "ms_per_step": ms, "queries_per_gpu": Q, "primitives": len(w.kinds),
            "workload": "cfg4: icosphere(9) with radial displacement, 5,242,880 triangles, 4,194,304 queries "
                        "per GPU (half uniform in [-1.5,1.5]^3, half within 0.02 of the surface), alpha=200, "
                        f"beta=0.5, fp32, {tree_name()} (BASELINE configs[3])",
-           "per_query": {"leaves": L / Q, "far_field": F / Q, "nodes_popped": pops / Q},
+           "per_query": {"leaves": L / Qsum, "far_field": F / Qsum, "nodes_popped": pops / Qsum},
            "setup_s": {"total": setup_s, "build_weights": tw, "build_tree": tb},
            "gpu_launches": launches * args.steps,
            "roofline": {"achieved_tflops": flops / (ms * 1e-3) / 1e12, "touched_gbs": nbytes / (ms * 1e-3) / 1e9,
                         "hbm_peak_gbs": 6542.4, "algorithmic": "10 flop/popped node + 12/far term + 192/exact "
                         "tri leaf; 32 B/popped node + 100 B/leaf (from this run's counters)"}}
+    if balance:
+        out["balance"] = balance
     if peaks:
         out["roofline"]["frac_fp32"] = out["roofline"]["achieved_tflops"] / peaks["ffma_tflops"]
     # the touched bytes are served from L1/L2 (ncu of pair_kernel: DRAM 0.9 % of
@@ -787,6 +817,8 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-bvh", action="store_true", help="skip the secondary BVH (cfg4) measurement")
+    ap.add_argument("--bvh-strong", action="store_true",
+                    help="BVH leg: split ONE cfg4 batch across the ranks by estimated cost (strong scaling)")
     ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 5],
                     help="exact workload: 2 = BASELINE configs[1] (headline), 1 = configs[0] fp64 points, "
                          "3 = configs[2] torus triangles, 5 = configs[4] primitive-sharded BVH")

@@ -4,6 +4,10 @@ Two regimes:
 
 * query sharding (cfg1-4): geometry, weights and tree replicated; every rank
   evaluates its own contiguous block of queries; no data-path collective.
+  A fixed batch is split after a Morton sort into contiguous blocks of equal
+  estimated BVH cost: shard_queries / balanced_ranges, with
+  the per-query cost (popped nodes 2 (leaves + far) - 1) taken from a
+  previous evaluation or a strided sample (estimate_query_costs).
 * primitive sharding (cfg5): the primitives are split into Morton-contiguous
   shards (one per rank), every rank evaluates ALL queries against its shard
   and produces the unshifted fp64 partial sums (c, grad_c) of the reference
@@ -27,6 +31,66 @@ def query_ranges(n: int, world: int) -> list[tuple[int, int]]:
     """Contiguous, balanced [lo, hi) query blocks, one per rank."""
     b = np.linspace(0, n, world + 1).round().astype(np.int64)
     return [(int(b[r]), int(b[r + 1])) for r in range(world)]
+
+
+def balanced_ranges(cost, world: int) -> list[tuple[int, int]]:
+    """Contiguous [lo, hi) blocks of a cost sequence, one per rank, each
+    holding about 1/world of the total cost: rank r starts at the first
+    position whose cost prefix reaches r/world of the total (each block's
+    cost is within one element's cost of the even share). Zero total cost
+    falls back to equal counts."""
+    c = np.asarray(cost, np.float64)
+    n = len(c)
+    if world <= 1 or n == 0:
+        return query_ranges(n, max(1, world))
+    if (c < 0).any():
+        raise ValueError("costs must be non-negative")
+    tot = float(c.sum())
+    if tot <= 0.0:
+        return query_ranges(n, world)
+    pre = np.concatenate([[0.0], np.cumsum(c)])  # pre[i] = cost of [0, i)
+    b = [0]
+    for r in range(1, world):
+        # boundary i minimising |pre[i] - r tot / world|, kept monotone
+        t = r * tot / world
+        i = int(np.searchsorted(pre, t))
+        if i > 0 and (i > n or t - pre[i - 1] <= pre[i] - t):
+            i -= 1
+        b.append(min(max(i, b[-1]), n))
+    b.append(n)
+    return [(b[r], b[r + 1]) for r in range(world)]
+
+
+def morton_order(points) -> np.ndarray:
+    """Query order along a 63-bit Morton curve over the batch's box (stable)."""
+    p = np.asarray(points, np.float64).reshape(-1, 3)
+    return np.argsort(_morton63(p), kind="stable") if len(p) else np.zeros(0, np.int64)
+
+
+def estimate_query_costs(evaluate, points_sorted, stride: int = 64) -> np.ndarray:
+    """Per-query BVH cost estimate for a Morton-sorted batch: `evaluate(sub)`
+    returns (leaves, far_field) for a query subset (e.g. Engine.smooth_min_dist
+    counters); every stride-th query is evaluated and its popped-node count
+    2 (L + F) - 1 is given to the stride-long run of neighbours it starts
+    (the runs are spatially compact, so the walks are alike)."""
+    p = np.asarray(points_sorted, np.float64).reshape(-1, 3)
+    n = len(p)
+    if n == 0:
+        return np.zeros(0)
+    idx = np.arange(0, n, max(1, int(stride)))
+    leaves, far = evaluate(p[idx])
+    pops = np.maximum(2.0 * (np.asarray(leaves, np.float64) + np.asarray(far, np.float64)) - 1.0, 1.0)
+    return np.repeat(pops, np.diff(np.append(idx, n)))
+
+
+def shard_queries(points, world: int, cost=None):
+    """Morton order + contiguous blocks of equal estimated cost (equal counts
+    without a cost). cost is per query in the ORIGINAL order. Returns (order,
+    ranges): rank r evaluates points[order[lo:hi]]."""
+    order = morton_order(points)
+    if cost is None:
+        return order, query_ranges(len(order), world)
+    return order, balanced_ranges(np.asarray(cost, np.float64)[order], world)
 
 
 def _morton63(p: np.ndarray) -> np.ndarray:

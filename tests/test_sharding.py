@@ -31,6 +31,64 @@ def test_query_ranges_partition():
             assert max(sizes) - min(sizes) <= 1
 
 
+def test_balanced_ranges_split_cost_evenly():
+    rng = np.random.default_rng(3)
+    for n in (1, 5, 100, 10000):
+        for w in (1, 2, 3, 8):
+            for cost in (np.ones(n), rng.exponential(1.0, n), rng.integers(0, 3, n).astype(float),
+                         np.where(np.arange(n) < n // 3, 50.0, 1.0)):
+                r = sharding.balanced_ranges(cost, w)
+                assert len(r) == w and r[0][0] == 0 and r[-1][1] == n
+                assert all(a[1] == b[0] and a[0] <= a[1] for a, b in zip(r, r[1:]))
+                if cost.sum() > 0:
+                    share = cost.sum() / w
+                    for lo, hi in r:  # within one element of the even share
+                        assert abs(cost[lo:hi].sum() - share) <= cost.max() * (1 + 1e-12) * 2
+    # uniform costs reproduce the equal-count split up to rounding
+    r = sharding.balanced_ranges(np.ones(1000), 8)
+    assert [hi - lo for lo, hi in r] == [125] * 8
+    assert sharding.balanced_ranges(np.zeros(10), 3) == sharding.query_ranges(10, 3)
+    with pytest.raises(ValueError):
+        sharding.balanced_ranges(np.array([1.0, -1.0]), 2)
+
+
+def test_cost_estimate_and_shard_queries(oracle):
+    """The strided estimate from the oracle's counters (the GPU returns the
+    same counters) balances the measured popped nodes across ranks much
+    better than equal counts on a half-near / half-far batch."""
+    O = oracle
+    m = O.random_scene(11, 300)
+    rng = np.random.default_rng(7)
+    near = O.QueryStream(77).draw_points(m, 600)
+    lo, hi = m.vertices.min(0), m.vertices.max(0)
+    span = hi - lo
+    # a far cloud off to one side: Morton-contiguous cheap queries
+    far = rng.uniform(lo + span * np.array([4.0, 0.0, 0.0]), hi + span * np.array([5.0, 0.0, 0.0]), size=(600, 3))
+    q = np.concatenate([near, far])
+    w, t = O.Weights.build(m), O.Tree.build(m)
+    p = O.Params(alpha=100.0, beta=0.5)
+    ref = O.query(m, w, q, p, tree=t)
+    true_cost = 2.0 * (ref.leaves + ref.far_field) - 1.0
+    order = sharding.morton_order(q)
+
+    def evaluate(sub):
+        r = O.query(m, w, sub, p, tree=t)
+        return r.leaves, r.far_field
+
+    est_sorted = sharding.estimate_query_costs(evaluate, q[order], stride=8)
+    assert est_sorted.shape == (len(q),)
+    est = np.empty(len(q))
+    est[order] = est_sorted
+    o2, ranges = sharding.shard_queries(q, 4, cost=est)
+    assert np.array_equal(o2, order)
+    assert np.array_equal(np.sort(np.concatenate([order[a:b] for a, b in ranges])), np.arange(len(q)))
+    bal = [true_cost[order[a:b]].sum() for a, b in ranges]
+    _, eq = sharding.shard_queries(q, 4)
+    flat = [true_cost[order[a:b]].sum() for a, b in eq]
+    assert max(bal) / np.mean(bal) < max(flat) / np.mean(flat)
+    assert max(bal) / np.mean(bal) < 1.25
+
+
 def test_primitive_shards_cover_mesh(oracle):
     m = oracle.random_scene(5, 200)
     w = oracle.Weights.build(m).table
