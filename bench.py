@@ -318,6 +318,23 @@ def measure_bvh(args, rank, world, local, eng_cls, dev, stream, flush, peaks):
     if world > 1:
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
     ms = float(t.item())
+    # end to end through the public host API: pinned fp64 host queries in,
+    # d_hat + gradient out (H2D, Morton sort, traversal, finalize, D2H)
+    qh = torch.tensor(q, dtype=torch.float64).pin_memory().numpy()
+    res = sd.SmoothResults(torch.empty(Q, dtype=torch.float64).pin_memory().numpy(),
+                           torch.empty(Q, 3, dtype=torch.float64).pin_memory().numpy())
+    eng.query_points(qh, P, sd.SD_BVH, out=res)
+    e2e_times = []
+    for _ in range(max(3, args.steps)):
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        eng.query_points(qh, P, sd.SD_BVH, out=res)
+        e2e_times.append(time.perf_counter() - t1)
+    te = torch.tensor([float(np.mean(e2e_times))], dtype=torch.float64, device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
+    e2e = {"value": Q_total / float(te.item()), "unit": "queries/s", "h2d_bytes_per_step": Q * 24,
+           "d2h_bytes_per_step": Q * 32}
     if world > 1:  # counters summed over ranks (per-query means below are whole-job)
         lf = torch.tensor([L, F, float(Q)], dtype=torch.float64, device=dev)
         torch.distributed.all_reduce(lf)
@@ -330,7 +347,7 @@ def measure_bvh(args, rank, world, local, eng_cls, dev, stream, flush, peaks):
     flops = (FLOPS_BOX_TEST * pops + FLOPS_FAR_TERM * F + FLOPS_PER_TRI_PAIR * L) / world
     nbytes = (BYTES_NODE * pops + BYTES_LEAF * L) / world
     out = {"metric": "BVH queries/s (value+grad)", "value": Q_total / (ms * 1e-3), "unit": "queries/s",
-           "scaling": "strong" if strong else "weak",
+           "scaling": "strong" if strong else "weak", "e2e": e2e,
            "ms_per_step": ms, "queries_per_gpu": Q, "primitives": len(w.kinds),
            "workload": "cfg4: icosphere(9) with radial displacement, 5,242,880 triangles, 4,194,304 queries "
                        "per GPU (half uniform in [-1.5,1.5]^3, half within 0.02 of the surface), alpha=200, "
