@@ -5,6 +5,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <memory>
 #include <fstream>
 #include <stdexcept>
 
@@ -938,8 +939,12 @@ int sd_query_points(sd_ctx* c, const double* q, int64_t Q, const sd_params* p, i
             if (!c->copy_stream) check_cuda(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking), "stream");
             cs = c->copy_stream;
         }
-        std::vector<cudaEvent_t> ev(size_t(2 * chunks));
-        for (auto& e : ev) check_cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+        std::vector<std::unique_ptr<ScopedEvent>> evs;
+        std::vector<cudaEvent_t> ev;
+        for (int k = 0; k < 2 * chunks; ++k) {
+            evs.push_back(std::make_unique<ScopedEvent>(cudaEventDisableTiming));
+            ev.push_back(*evs.back());
+        }
         const int64_t per = (Q + chunks - 1) / chunks;
         for (int k = 0; k < chunks; ++k) {
             const int64_t off = k * per, n = std::min(Q, off + per) - off;
@@ -985,7 +990,6 @@ int sd_query_points(sd_ctx* c, const double* q, int64_t Q, const sd_params* p, i
         }
         check_cuda(cudaStreamSynchronize(cs), "query");
         check_cuda(cudaStreamSynchronize(st), "query");
-        for (auto& e : ev) cudaEventDestroy(e);
         c->last_launches = launches;
     });
 }

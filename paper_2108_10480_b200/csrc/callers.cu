@@ -196,9 +196,7 @@ void render_impl(Ctx& c, const sd_params& p, int mode, const sd_render_config& c
     out.far_field = static_cast<int64_t*>(b_qf.ensure(size_t(N) * sizeof(int64_t)));
     int* nsel = static_cast<int*>(b_n.ensure(sizeof(int)));
 
-    cudaEvent_t e0, e1;
-    check_cuda(cudaEventCreate(&e0), "event");
-    check_cuda(cudaEventCreate(&e1), "event");
+    ScopedEvent e0, e1;
     check_cuda(cudaEventRecord(e0, st), "event");
     const unsigned B = 256;
     ray_dirs<<<unsigned((N + B - 1) / B), B, 0, st>>>(cam, W, H, dirs);
@@ -241,8 +239,6 @@ void render_impl(Ctx& c, const sd_params& p, int mode, const sd_render_config& c
     check_cuda(cudaStreamSynchronize(st), "render");
     float ms = 0;
     check_cuda(cudaEventElapsedTime(&ms, e0, e1), "event");
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
     int64_t L = 0, F = 0, hits = 0;
     for (int64_t i = 0; i < N; ++i) {
         L += hl[i];
@@ -269,9 +265,7 @@ void grid_impl(Ctx& c, const sd_params& p, int mode, int n, double* d_out, int64
     out.d_hat = static_cast<double*>(b_d.ensure(size_t(n3) * sizeof(double)));
     if (leaves_out) out.leaves = static_cast<int64_t*>(b_l.ensure(size_t(n3) * sizeof(int64_t)));
     if (far_out) out.far_field = static_cast<int64_t*>(b_f.ensure(size_t(n3) * sizeof(int64_t)));
-    cudaEvent_t e0, e1;
-    check_cuda(cudaEventCreate(&e0), "event");
-    check_cuda(cudaEventCreate(&e1), "event");
+    ScopedEvent e0, e1;
     check_cuda(cudaEventRecord(e0, st), "event");
     grid_points<<<unsigned((n3 + 255) / 256), 256, 0, st>>>(n, q);
     query_batch_f64(c, q, n3, p, mode, out, st);
@@ -286,8 +280,6 @@ void grid_impl(Ctx& c, const sd_params& p, int mode, int n, double* d_out, int64
     check_cuda(cudaStreamSynchronize(st), "grid benchmark");
     float ms = 0;
     check_cuda(cudaEventElapsedTime(&ms, e0, e1), "event");
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
     if (seconds) *seconds = ms * 1e-3;
     c.last_launches += 2;
 }

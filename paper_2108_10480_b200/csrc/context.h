@@ -23,6 +23,20 @@ struct CudaError {
 };
 void check_cuda(cudaError_t e, const char* where);  // throws CudaError
 
+// A CUDA event released on every exit path (check_cuda throws).
+struct ScopedEvent {
+    cudaEvent_t e = nullptr;
+    explicit ScopedEvent(unsigned flags = cudaEventDefault) {
+        check_cuda(cudaEventCreateWithFlags(&e, flags), "cudaEventCreate");
+    }
+    ~ScopedEvent() {
+        if (e) cudaEventDestroy(e);
+    }
+    ScopedEvent(const ScopedEvent&) = delete;
+    ScopedEvent& operator=(const ScopedEvent&) = delete;
+    operator cudaEvent_t() const { return e; }
+};
+
 // Grow-only device buffer.
 struct DevBuf {
     void* p = nullptr;

@@ -742,3 +742,30 @@ def test_fp64_kernel_math_is_near_ulp(sd, oracle, seed):
                                       np.maximum(1.0, np.linalg.norm(ref.grad[gm], axis=1))).max(initial=0.0)))
     print(f"fp64 worst relative error: d_hat {worst_d:.3g}, grad {worst_g:.3g}")
     assert worst_d <= 1e-14 and worst_g <= 1e-13, (worst_d, worst_g)
+
+
+@pytest.mark.parametrize("prec", [0, 1])
+def test_host_chunk_pipeline_matches_unpipelined(sd, oracle, prec, monkeypatch):
+    """sd_query_points' optional chunk pipeline (SDGPU_PIPELINE=1: four
+    chunks, H2D / compute / D2H overlapped on two streams) returns exactly
+    the unpipelined results for a ragged batch above its 2^17-query
+    threshold, exact and BVH: decisions (counters, hash) identical, values
+    within the parity tolerance (a chunk is a smaller batch, so the kernel
+    choice and with it the summation order may differ)."""
+    O = oracle
+    m0 = O.random_scene(4, 300)
+    rng = np.random.default_rng(17)
+    lo, hi = m0.vertices.min(0), m0.vertices.max(0)
+    q0 = rng.uniform(lo - 0.2, hi + 0.2, size=((1 << 17) + 4097, 3))
+    m, q = prep(O, m0, q0, prec)
+    w, t = O.Weights.build(m), O.Tree.build(m)
+    e = engine_for(sd, O, m, w, prec, tree=t)
+    for mode, beta in ((sd.SD_EXACT, 0.0), (sd.SD_BVH, 0.5)):
+        p = sd.SmoothParams(alpha=120.0, beta=beta)
+        monkeypatch.delenv("SDGPU_PIPELINE", raising=False)
+        a = e.query_points(q, p, mode, want_c=True, want_counters=True)
+        monkeypatch.setenv("SDGPU_PIPELINE", "1")
+        b = e.query_points(q, p, mode, want_c=True, want_counters=True)
+        for f in ("leaves", "far_field", "decision_hash"):
+            assert np.array_equal(getattr(a, f), getattr(b, f)), (mode, f)
+        assert_close(b, a, prec, 120.0, f"pipeline mode {mode}")
