@@ -711,6 +711,7 @@ int sd_set_bvh(sd_ctx* c, const sd_bvh_node* nodes, int64_t n) {
         if (n != (c->N > 0 ? 2 * c->N - 1 : 0) || (n > 0 && !nodes))
             throw ArgError{"tree must have 2N - 1 nodes (one primitive per leaf)"};
         c->tree.assign(nodes, nodes + n);
+        c->tree_trusted = false;
         c->have_tree = true;
         c->dtree_ready = false;
         c->sx_tree_ready = c->sx_prim_ready = false;
@@ -783,6 +784,7 @@ int sd_load_bvh_cache(sd_ctx* c, const char* path) {
         in.read(reinterpret_cast<char*>(nodes.data()), std::streamsize(n * sizeof(sd_bvh_node)));
         if (!in) throw ArgError{std::string(path) + ": truncated BVH cache"};
         c->tree.swap(nodes);
+        c->tree_trusted = false;
         c->have_tree = true;
         c->dtree_ready = false;
         c->sx_tree_ready = c->sx_prim_ready = false;

@@ -120,30 +120,41 @@ static void median_build_host(const Ctx& c, std::vector<sd_bvh_node>& out) {
 
 void tree_build_median_host(Ctx& c) {
     median_build_host(c, c.tree);
+    c.tree_trusted = true;
     c.dtree_ready = false;
     c.sx_tree_ready = c.sx_prim_ready = false;
 }
 
 // ---------------------------------------------------------------- upload
 template <class T>
-static void upload_tree_T(Ctx& c, DeviceTree& t) {
+void upload_tree_device(Ctx& c, DeviceTree& t, int depth);  // layout.cu
+
+// Checks an externally supplied tree (sd_set_bvh, SDBV0001 cache) and returns
+// its depth; trees from this library's builders skip the check.
+static int validate_tree(const Ctx& c) {
     const int64_t n = int64_t(c.tree.size());
     const int64_t N = c.N;
     if (n != 2 * N - 1) throw std::runtime_error("tree must have 2N - 1 nodes");
+    std::vector<int32_t> dep(size_t(n), 0);
+    int depth = 0;
+    if (c.tree_trusted) {  // pre-order: parents precede children
+        for (int64_t id = 0; id < n; ++id) {
+            const sd_bvh_node& nd = c.tree[id];
+            depth = std::max(depth, dep[id]);
+            if (nd.left >= 0) dep[nd.left] = dep[nd.right] = dep[id] + 1;
+        }
+        return depth;
+    }
     // validate and compute the pre-order numbering of the given tree
     std::vector<int32_t> pre(n, -1), stack;
-    std::vector<int32_t> order;
-    order.reserve(n);
+    int64_t visited = 0;
     stack.push_back(0);
     std::vector<char> seen_prim(N, 0);
-    int depth = 0;
-    std::vector<int> dep(n, 0);
     while (!stack.empty()) {
         const int32_t id = stack.back();
         stack.pop_back();
         if (id < 0 || id >= n || pre[id] >= 0) throw std::runtime_error("tree: bad or repeated child index");
-        pre[id] = int32_t(order.size());
-        order.push_back(id);
+        pre[id] = int32_t(visited++);
         const sd_bvh_node& nd = c.tree[id];
         depth = std::max(depth, dep[id]);
         if (nd.left < 0) {
@@ -157,86 +168,15 @@ static void upload_tree_T(Ctx& c, DeviceTree& t) {
             stack.push_back(nd.left);
         }
     }
-    if (int64_t(order.size()) != n) throw std::runtime_error("tree: unreachable nodes");
-    bool identity = true;
-    for (int64_t i = 0; i < n && identity; ++i) identity = pre[i] == i;
-    if (!identity) throw std::runtime_error("tree must be in pre-order layout (left child = parent + 1, root 0)");
+    if (visited != n) throw std::runtime_error("tree: unreachable nodes");
+    for (int64_t i = 0; i < n; ++i)
+        if (pre[i] != i) throw std::runtime_error("tree must be in pre-order layout (left child = parent + 1, root 0)");
+    return depth;
+}
 
-    std::vector<NodeT<T>> box(n);
-    std::vector<int32_t> count(n);
-    std::vector<double> d64(n);
-    std::vector<T> lgc(n);
-    std::vector<T> leafrec;
-    std::vector<int32_t> leafmeta;
-    leafrec.reserve(size_t(N) * kRecTri);
-    int64_t slot = 0;
-    bool exact_boxes = true;
-    for (int64_t id = 0; id < n; ++id) {
-        const sd_bvh_node& nd = c.tree[id];
-        NodeT<T>& b = box[id];
-        for (int a = 0; a < 3; ++a) {
-            // outward rounding keeps the fp32 box a superset (exact when the
-            // geometry was quantized to float, as SD_FP32 does)
-            T l = T(nd.lo[a]), h = T(nd.hi[a]);
-            if (double(l) > nd.lo[a]) l = std::nextafter(l, T(-INFINITY));
-            if (double(h) < nd.hi[a]) h = std::nextafter(h, T(INFINITY));
-            exact_boxes = exact_boxes && double(l) == nd.lo[a] && double(h) == nd.hi[a];
-            b.v[a] = l;
-            b.v[4 + a] = h;
-        }
-        b.v[3] = T(nd.diameter);
-        int32_t link;
-        if (nd.left < 0) {
-            link = int32_t(-(slot + 1));
-            const int32_t p = nd.primitive;
-            T rec[kRecTri];
-            build_record<T>(c, p, rec);
-            leafrec.insert(leafrec.end(), rec, rec + kRecTri);
-            const int k = c.kind[p];
-            const int poly = k == SD_POINT ? -1 : c.poly_index[p];
-            leafmeta.push_back(k | ((poly + 1) << 2));
-            ++slot;
-        } else {
-            if (nd.left != id + 1) throw std::runtime_error("tree: left child must follow its parent");
-            link = nd.right;
-        }
-        std::memcpy(&b.v[7], &link, sizeof(int32_t));
-        if (sizeof(T) == 8) std::memset(reinterpret_cast<char*>(&b.v[7]) + 4, 0, 4);
-        count[id] = nd.count;
-        lgc[id] = T(std::log2(double(nd.count)));
-        d64[id] = nd.diameter;
-    }
-    t.nodes = n;
-    t.split_k = -1;
-    t.leaves = slot;
-    t.depth = depth;
-    t.exact_boxes = exact_boxes;
-    auto up = [](DevBuf& buf, const void* src, size_t bytes) {
-        void* d = buf.ensure(bytes);
-        if (bytes) check_cuda(cudaMemcpy(d, src, bytes, cudaMemcpyHostToDevice), "upload tree");
-    };
-    up(t.box, box.data(), box.size() * sizeof(NodeT<T>));
-    // child-pair records: pair[p] = (NodeT[p + 1], NodeT[right(p)],
-    // log2 n_B of both) for internal p, so one warp step fetches both
-    // children of a node and their far-field weights in one go
-    {
-        std::vector<PairT<T>> pr(static_cast<size_t>(n));
-        for (int64_t id = 0; id < n; ++id) {
-            const sd_bvh_node& nd = c.tree[id];
-            if (nd.left < 0) continue;
-            pr[id].l = box[id + 1];
-            pr[id].r = box[nd.right];
-            pr[id].lgc[0] = lgc[id + 1];
-            pr[id].lgc[1] = lgc[nd.right];
-            pr[id].lgc[2] = pr[id].lgc[3] = T(0);
-        }
-        up(t.pairs, pr.data(), pr.size() * sizeof(PairT<T>));
-    }
-    up(t.count, count.data(), count.size() * sizeof(int32_t));
-    up(t.lgcount, lgc.data(), lgc.size() * sizeof(T));
-    up(t.diam64, d64.data(), d64.size() * sizeof(double));
-    up(t.leafrec, leafrec.data(), leafrec.size() * sizeof(T));
-    up(t.leafmeta, leafmeta.data(), leafmeta.size() * sizeof(int32_t));
+template <class T>
+static void upload_tree_T(Ctx& c, DeviceTree& t) {
+    upload_tree_device<T>(c, t, validate_tree(c));
 }
 
 // Split slots at depth k (see pair_kernel): nodes at depth k and leaves

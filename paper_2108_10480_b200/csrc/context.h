@@ -125,6 +125,7 @@ struct Ctx {
 
     // tree (host copy in the reference layout + device traversal layout)
     bool have_tree = false;
+    bool tree_trusted = false;  // built here (pre-order, complete): no validation pass
     std::vector<sd_bvh_node> tree;
     DeviceTree dtree;
     bool dtree_ready = false;

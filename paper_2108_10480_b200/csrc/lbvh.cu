@@ -272,6 +272,7 @@ void tree_build_lbvh(Ctx& c) {
     emit<<<unsigned((nn + B - 1) / B), B, 0, st>>>(n, sids, d_nbox, d_left, d_right, d_count, d_pre, d_out);
     check_cuda(cudaGetLastError(), "lbvh emit");
     c.tree.resize(size_t(nn));
+    c.tree_trusted = true;
     check_cuda(cudaMemcpyAsync(c.tree.data(), d_out, size_t(nn) * sizeof(sd_bvh_node), cudaMemcpyDeviceToHost, st),
                "lbvh download");
     check_cuda(cudaStreamSynchronize(st), "lbvh build");

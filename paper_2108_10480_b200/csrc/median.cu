@@ -6,11 +6,14 @@
 //   extent (ties -> x, then y), left = the first n/2 primitives in
 //   (centroid[axis], index) order (nth_element's unique partition sets),
 //   pre-order ids: left = id + 1, right = id + 2 (n/2)
-// Every level works on all nodes at once: a segmented reduction gives the
-// node boxes, two stable segmented sorts (by index, then by the centroid
-// coordinate on the node's axis) order each node's primitives, and each node
-// splits its sorted segment in the middle. Node records are emitted in the
-// reference layout as they are decided.
+// Every level works on all nodes at once, with device-wide primitives whose
+// parallelism does not depend on the segment sizes (the top levels have one
+// huge segment): a reduce-by-key over the positions gives the node boxes, and
+// ONE radix sort of 2 ceil(log2 n)-bit keys (segment start, rank of the
+// primitive on the node's axis) orders every node's primitives, where the
+// per-axis ranks -- positions in (centroid coordinate, index) order -- are
+// computed once up front. Each node splits its sorted segment in the middle. Node
+// records are emitted in the reference layout as they are decided.
 #include <algorithm>
 #include <cmath>
 #include <vector>
@@ -47,15 +50,6 @@ struct BoxOf {
 struct Seg {
     int32_t begin, end, id, pad;
 };
-struct BeginOf {
-    const int32_t* p;
-    __host__ __device__ int operator()(int s) const { return p[4 * s]; }
-};
-struct EndOf {
-    const int32_t* p;
-    __host__ __device__ int operator()(int s) const { return p[4 * s + 1]; }
-};
-
 __global__ void prim_boxes(const double* __restrict__ xyz, const int32_t* __restrict__ sv,
                            const uint8_t* __restrict__ kind, int64_t n, MBox* boxes, double* ce, int32_t* order) {
     const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -114,22 +108,61 @@ __global__ void split_nodes(const Seg* __restrict__ segs, int S, const MBox* __r
     put_node(out, g.id, b, g.id + 1, g.id + 2 * half, -1, n);
 }
 
-// centroid coordinate on the node's axis, for every element of an active
-// segment (segments sorted by begin; elements outside keep a dummy key)
-__global__ void axis_keys(const int32_t* __restrict__ order, int64_t n, const Seg* __restrict__ segs, int S,
-                          const int8_t* __restrict__ axis, const double* __restrict__ ce, double* key) {
-    const int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (k >= n) return;
-    int lo = 0, hi = S;  // first segment with begin > k
+// segment of position k: the first segment with begin > k, minus one
+__device__ __forceinline__ int seg_of(const Seg* __restrict__ segs, int S, int64_t k) {
+    int lo = 0, hi = S;
     while (lo < hi) {
         const int mid = (lo + hi) >> 1;
         if (segs[mid].begin <= k) lo = mid + 1;
         else hi = mid;
     }
     const int s = lo - 1;
-    // + 0.0 folds -0.0 into +0.0: the radix order of the keys is then the
-    // comparator's (equal coordinates tie on the index, pass 1)
-    key[k] = (s >= 0 && k < segs[s].end) ? __dadd_rn(ce[3 * int64_t(order[k]) + axis[s]], 0.0) : 0.0;
+    return (s >= 0 && k < segs[s].end) ? s : -1;
+}
+
+// reduce-by-key keys: the segment of an active position, a value >= S that
+// differs from both neighbours' for a finished one (its own run)
+__global__ void seg_keys(int64_t n, const Seg* __restrict__ segs, int S, int32_t* key) {
+    const int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const int s = seg_of(segs, S, k);
+    key[k] = s >= 0 ? s : int32_t(S + k);
+}
+
+__global__ void scatter_boxes(const int32_t* __restrict__ ukey, const MBox* __restrict__ agg,
+                              const int* __restrict__ nruns, int S, MBox* sbox) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= *nruns) return;
+    const int32_t s = ukey[r];
+    if (s < S) sbox[s] = agg[r];
+}
+
+// sort keys of a level: (segment start << rb) | rank on the segment's axis
+// for an active position, (k << rb) for a finished one (it stays in place);
+// rb = ceil(log2 n) bits hold any position or rank
+__global__ void sort_keys(const int32_t* __restrict__ order, int64_t n, const Seg* __restrict__ segs, int S,
+                          const int8_t* __restrict__ axis, const int32_t* __restrict__ rank, int rb, uint64_t* key) {
+    const int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const int s = seg_of(segs, S, k);
+    key[k] = s >= 0 ? (uint64_t(segs[s].begin) << rb) | uint64_t(rank[int64_t(axis[s]) * n + order[k]])
+                    : uint64_t(k) << rb;
+}
+
+// order-preserving bits of a centroid coordinate (+ 0.0 folds -0.0 into
+// +0.0: equal coordinates then tie on the index, as in the comparator)
+__global__ void coord_keys(const double* __restrict__ ce, int64_t n, int a, uint64_t* key, int32_t* ids) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double x = __dadd_rn(ce[3 * i + a], 0.0);
+    const uint64_t b = uint64_t(__double_as_longlong(x));
+    key[i] = (b >> 63) ? ~b : (b | (uint64_t(1) << 63));
+    ids[i] = int32_t(i);
+}
+
+__global__ void scatter_rank(const int32_t* __restrict__ sorted_ids, int64_t n, int32_t* rank) {
+    const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (j < n) rank[sorted_ids[j]] = int32_t(j);
 }
 
 // children: leaves are emitted, larger children go to the next level
@@ -163,7 +196,7 @@ void tree_build_median_gpu(Ctx& c) {
     cudaStream_t st = c.stream;
     const unsigned B = 256;
     DevBuf b_xyz, b_sv, b_kind, b_pbox, b_ce, b_ord, b_ord2, b_key, b_key2, b_segs, b_next, b_flag, b_sbox, b_axis,
-        b_out, b_tmp, b_ns;
+        b_out, b_tmp, b_ns, b_rank, b_skey, b_ukey, b_agg, b_nruns;
     double* xyz = static_cast<double*>(b_xyz.ensure(c.xyz.size() * sizeof(double)));
     int32_t* sv = static_cast<int32_t*>(b_sv.ensure(c.sv.size() * sizeof(int32_t)));
     uint8_t* kind = static_cast<uint8_t*>(b_kind.ensure(c.kind.size()));
@@ -174,11 +207,32 @@ void tree_build_median_gpu(Ctx& c) {
     double* ce = static_cast<double*>(b_ce.ensure(size_t(n) * 3 * sizeof(double)));
     int32_t* order = static_cast<int32_t*>(b_ord.ensure(size_t(n) * sizeof(int32_t)));
     int32_t* order2 = static_cast<int32_t*>(b_ord2.ensure(size_t(n) * sizeof(int32_t)));
-    double* key = static_cast<double*>(b_key.ensure(size_t(n) * sizeof(double)));
-    double* key2 = static_cast<double*>(b_key2.ensure(size_t(n) * sizeof(double)));
+    uint64_t* key = static_cast<uint64_t*>(b_key.ensure(size_t(n) * sizeof(uint64_t)));
+    uint64_t* key2 = static_cast<uint64_t*>(b_key2.ensure(size_t(n) * sizeof(uint64_t)));
+    int32_t* rank = static_cast<int32_t*>(b_rank.ensure(size_t(3 * n) * sizeof(int32_t)));
+    int32_t* skey = static_cast<int32_t*>(b_skey.ensure(size_t(n) * sizeof(int32_t)));
+    int32_t* ukey = static_cast<int32_t*>(b_ukey.ensure(size_t(n) * sizeof(int32_t)));
+    MBox* agg = static_cast<MBox*>(b_agg.ensure(size_t(n) * sizeof(MBox)));
+    int* nruns = static_cast<int*>(b_nruns.ensure(sizeof(int)));
     sd_bvh_node* out = static_cast<sd_bvh_node*>(b_out.ensure(size_t(2 * n - 1) * sizeof(sd_bvh_node)));
     prim_boxes<<<unsigned((n + B - 1) / B), B, 0, st>>>(xyz, sv, kind, n, pbox, ce, order);
     check_cuda(cudaGetLastError(), "median prim boxes");
+    const unsigned G = unsigned((n + B - 1) / B);
+    // per-axis ranks: positions in (centroid coordinate, index) order (the
+    // radix sort is stable and its input is in index order)
+    for (int a = 0; a < 3; ++a) {
+        coord_keys<<<G, B, 0, st>>>(ce, n, a, key, order2);
+        check_cuda(cudaGetLastError(), "median coord keys");
+        size_t tb = 0;
+        cub::DeviceRadixSort::SortPairs(nullptr, tb, key, key2, order2, skey, int(n), 0, 64, st);
+        check_cuda(cub::DeviceRadixSort::SortPairs(b_tmp.ensure(tb), tb, key, key2, order2, skey, int(n), 0, 64, st),
+                   "median axis ranks");
+        scatter_rank<<<G, B, 0, st>>>(skey, n, rank + size_t(a) * n);
+        check_cuda(cudaGetLastError(), "median ranks");
+    }
+    int rb = 1;  // ceil(log2 n): bits of a position or a rank
+    while ((int64_t(1) << rb) < n) ++rb;
+    const int key_bits = 2 * rb;
 
     Seg* segs = static_cast<Seg*>(b_segs.ensure(size_t(std::max<int64_t>(n, 2)) * sizeof(Seg)));
     Seg* next = static_cast<Seg*>(b_next.ensure(size_t(std::max<int64_t>(n, 2)) * sizeof(Seg)));
@@ -203,6 +257,7 @@ void tree_build_median_gpu(Ctx& c) {
                          ? std::sqrt(dx * dx + dy * dy + dz * dz)
                          : 0.0;
         c.tree.assign(1, r);
+        c.tree_trusted = true;
         return;
     }
     const Seg root{0, int32_t(n), 0, 0};
@@ -210,40 +265,29 @@ void tree_build_median_gpu(Ctx& c) {
     int S = 1;
     while (S > 0) {
         // node boxes: union of the primitive boxes of each segment
-        const int32_t* seg_i32 = reinterpret_cast<const int32_t*>(segs);
+        // (reduce-by-key over the positions; finished positions are own runs)
         cub::CountingInputIterator<int64_t> cnt(0);
         cub::TransformInputIterator<MBox, BoxOf, cub::CountingInputIterator<int64_t>> boxes_in(cnt, BoxOf{pbox, order});
-        MBox empty;
-        for (int a = 0; a < 3; ++a) {
-            empty.lo[a] = INFINITY;
-            empty.hi[a] = -INFINITY;
-        }
-        // begin / end offsets with stride 4 (Seg layout)
-        cub::CountingInputIterator<int> sidx(0);
-        cub::TransformInputIterator<int, BeginOf, cub::CountingInputIterator<int>> bo(sidx, BeginOf{seg_i32});
-        cub::TransformInputIterator<int, EndOf, cub::CountingInputIterator<int>> eo(sidx, EndOf{seg_i32});
+        seg_keys<<<G, B, 0, st>>>(n, segs, S, skey);
+        check_cuda(cudaGetLastError(), "median segment keys");
         size_t tb = 0;
-        cub::DeviceSegmentedReduce::Reduce(nullptr, tb, boxes_in, sbox, S, bo, eo, BoxUnion{}, empty, st);
-        check_cuda(cub::DeviceSegmentedReduce::Reduce(b_tmp.ensure(tb), tb, boxes_in, sbox, S, bo, eo, BoxUnion{}, empty,
-                                                      st),
+        cub::DeviceReduce::ReduceByKey(nullptr, tb, skey, ukey, boxes_in, agg, nruns, BoxUnion{}, n, st);
+        check_cuda(cub::DeviceReduce::ReduceByKey(b_tmp.ensure(tb), tb, skey, ukey, boxes_in, agg, nruns, BoxUnion{}, n,
+                                                  st),
                    "median node boxes");
+        scatter_boxes<<<G, B, 0, st>>>(ukey, agg, nruns, S, sbox);
+        check_cuda(cudaGetLastError(), "median node boxes scatter");
         split_nodes<<<unsigned((S + B - 1) / B), B, 0, st>>>(segs, S, sbox, axis, out);
         check_cuda(cudaGetLastError(), "median split");
-        // pass 1: primitives of each segment by index (stable sort of the ids)
-        check_cuda(cudaMemcpyAsync(order2, order, size_t(n) * sizeof(int32_t), cudaMemcpyDeviceToDevice, st), "copy");
+        // every segment's primitives in (centroid[axis], index) order, in place
+        sort_keys<<<G, B, 0, st>>>(order, n, segs, S, axis, rank, rb, key);
+        check_cuda(cudaGetLastError(), "median sort keys");
         tb = 0;
-        cub::DeviceSegmentedSort::StableSortKeys(nullptr, tb, order, order2, int(n), S, bo, eo, st);
-        check_cuda(cub::DeviceSegmentedSort::StableSortKeys(b_tmp.ensure(tb), tb, order, order2, int(n), S, bo, eo, st),
-                   "median sort ids");
-        // pass 2: stable by the centroid coordinate on the node's axis
-        axis_keys<<<unsigned((n + B - 1) / B), B, 0, st>>>(order2, n, segs, S, axis, ce, key);
-        check_cuda(cudaGetLastError(), "median keys");
-        check_cuda(cudaMemcpyAsync(order, order2, size_t(n) * sizeof(int32_t), cudaMemcpyDeviceToDevice, st), "copy");
-        tb = 0;
-        cub::DeviceSegmentedSort::StableSortPairs(nullptr, tb, key, key2, order2, order, int(n), S, bo, eo, st);
-        check_cuda(cub::DeviceSegmentedSort::StableSortPairs(b_tmp.ensure(tb), tb, key, key2, order2, order, int(n), S,
-                                                              bo, eo, st),
-                   "median sort centroids");
+        cub::DeviceRadixSort::SortPairs(nullptr, tb, key, key2, order, order2, int(n), 0, key_bits, st);
+        check_cuda(cub::DeviceRadixSort::SortPairs(b_tmp.ensure(tb), tb, key, key2, order, order2, int(n), 0, key_bits,
+                                                   st),
+                   "median sort");
+        std::swap(order, order2);
         // split in the middle; leaves out, the rest to the next level
         children<<<unsigned((S + B - 1) / B), B, 0, st>>>(segs, S, order, pbox, out, next, flag);
         check_cuda(cudaGetLastError(), "median children");
@@ -255,6 +299,7 @@ void tree_build_median_gpu(Ctx& c) {
         check_cuda(cudaStreamSynchronize(st), "median level");
     }
     c.tree.resize(size_t(2 * n - 1));
+    c.tree_trusted = true;
     check_cuda(cudaMemcpyAsync(c.tree.data(), out, size_t(2 * n - 1) * sizeof(sd_bvh_node), cudaMemcpyDeviceToHost, st),
                "D2H tree");
     check_cuda(cudaStreamSynchronize(st), "median build");
