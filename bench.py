@@ -240,7 +240,39 @@ def run_reference(args, rank, world):
                          "sample": f"{n} of {QUERIES_PER_GPU} cfg2 queries x {N} edges per step"},
         "e2e": {"value": value, "unit": "pair-evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    if not args.no_bvh:
+        line["bvh"] = reference_bvh(threads)
     print(json.dumps(line), flush=True)
+
+
+def reference_bvh(threads, target_s=10.0):
+    """The reference's own CPU path for the BVH metric: the oracle port builds
+    the WeightSet and the median-split tree of cfg4 on the host
+    (build_weight_set / build_bvh restated) and evaluates a bounded query
+    sample (both halves of the distribution) on all host threads."""
+    import oracle as O
+    from paper_2108_10480_b200 import configs
+    t0 = time.perf_counter()
+    w, q = configs.cfg4()
+    v, q = configs.quantize(w.vertices), configs.quantize(q)
+    m = O.Mesh.from_arrays(v, w.simplices, w.kinds)
+    ws = O.Weights.build(m)
+    tree = O.Tree.build(m)
+    setup = time.perf_counter() - t0
+    p = O.Params(alpha=w.alpha, alpha_u=600.0, beta=w.beta)
+    half = len(q) // 2
+    pick = lambda n: np.concatenate([q[:n // 2], q[half:half + n - n // 2]])
+    pilot = max(threads * 16, 1024)
+    r = O.query(m, ws, pick(pilot), p, tree=tree, threads=threads)  # also warms the tree pages
+    n = int(min(262144, max(pilot, pilot * target_s / max(r.seconds, 1e-3))))
+    r = O.query(m, ws, pick(n), p, tree=tree, threads=threads)
+    return {"metric": "BVH queries/s (value+grad)", "value": n / r.seconds, "unit": "queries/s",
+            "workload": "cfg4 (BASELINE configs[3]): icosphere(9), 5,242,880 triangles, alpha=200, beta=0.5, "
+                        "host-built median tree and WeightSet",
+            "cpu_baseline": {"value": n / r.seconds, "unit": "queries/s", "cores": threads, "kind": "port",
+                             "sample": f"{n} cfg4 queries (half from each half of the distribution), "
+                                       f"{r.seconds:.1f} s"},
+            "setup_s": setup}
 
 
 def measure_bvh(args, rank, world, local, eng_cls, dev, stream, flush, peaks):
