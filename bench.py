@@ -290,7 +290,8 @@ def measure_bvh(args, rank, world, local, eng_cls, dev, stream, flush, peaks):
     w, q = configs.cfg4(block=0 if strong else rank)
     v, q = configs.quantize(w.vertices), configs.quantize(q)
     Q_total = len(q) * (1 if strong else world)
-    eng = sd.Engine(local, sd.SD_FP32)
+    bvh64 = args.fp64 and args.config == 2  # --fp64: the BVH leg in fp64 too
+    eng = sd.Engine(local, sd.SD_FP64 if bvh64 else sd.SD_FP32)
     eng.set_geometry(v, w.simplices, w.kinds)
     tw = time.perf_counter()
     eng.build_weights()
@@ -316,7 +317,7 @@ def measure_bvh(args, rank, world, local, eng_cls, dev, stream, flush, peaks):
         balance = {"ranges": ranges, "estimated_cost_share": [float(est[a:b].sum() / est.sum()) for a, b in ranges],
                    "estimate": "strided sample (1/64) of the Morton-sorted batch, popped nodes 2(L+F)-1"}
     Q = len(q)
-    qd = torch.tensor(q, dtype=torch.float32, device=dev)
+    qd = torch.tensor(q, dtype=torch.float64 if bvh64 else torch.float32, device=dev)
     d_hat = torch.empty(Q, dtype=torch.float64, device=dev)
     grad = torch.empty(Q, 3, dtype=torch.float64, device=dev)
     leaves = torch.empty(Q, dtype=torch.int64, device=dev)
@@ -383,7 +384,8 @@ def measure_bvh(args, rank, world, local, eng_cls, dev, stream, flush, peaks):
            "ms_per_step": ms, "queries_per_gpu": Q, "primitives": len(w.kinds),
            "workload": "cfg4: icosphere(9) with radial displacement, 5,242,880 triangles, 4,194,304 queries "
                        "per GPU (half uniform in [-1.5,1.5]^3, half within 0.02 of the surface), alpha=200, "
-                       f"beta=0.5, fp32, {tree_name()} (BASELINE configs[3])",
+                       f"beta=0.5, {'fp64' if bvh64 else 'fp32'}, {tree_name()} (BASELINE configs[3])",
+           "dtype": "f64" if bvh64 else "f32",
            "per_query": {"leaves": L / Qsum, "far_field": F / Qsum, "nodes_popped": pops / Qsum},
            "setup_s": {"total": setup_s, "build_weights": tw, "build_tree": tb},
            "gpu_launches": launches * args.steps,

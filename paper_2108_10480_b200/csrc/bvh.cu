@@ -582,10 +582,20 @@ __device__ __forceinline__ bool point_far(const TraverseArgs<T>& a, const NodeT<
             ++nre;
         }
     } else {
-        far = decide64(b, a.diam64[id], double(qx), double(qy), double(qz), a.beta64);
+        // squared test with FMA-contracted s and a 1e-12 relative band; the
+        // reference-rounded decision (sqrt and all) only inside the band
+        const double diam = b.v[3];  // the fp64 diameter itself (T = double)
+        const double dd = diam * diam, rhs2 = a.beta64 * a.beta64 * s;
+        if (s == 0.0) far = false;  // d_B = 0 exactly: fp64 boxes are the reference's
+        else if (dd < rhs2 * (1.0 - 1e-12)) far = true;
+        else if (dd > rhs2 * (1.0 + 1e-12)) far = false;
+        else {
+            far = decide64(b, a.diam64[id], double(qx), double(qy), double(qz), a.beta64);
+            ++nre;
+        }
         if (far) {
-            d = sqrt(s);
-            r = T(1) / d;
+            r = Math<double>::rsqrt(s);
+            d = s * r;
         }
     }
     return far;
