@@ -570,16 +570,19 @@ __device__ __forceinline__ bool point_far(const TraverseArgs<T>& a, const NodeT<
     const T s = fma(dx, dx, fma(dy, dy, dz * dz));
     bool far;
     if constexpr (sizeof(T) == 4) {
-        r = s > T(0) ? Math<T>::rsqrt(s) : T(0);
-        d = s * r;
-        const T rhs = a.ph.beta * d;
-        const T band = T(1e-5) * rhs;
+        // squared: diam^2 against beta^2 s with a 2e-5 relative band (the
+        // reciprocal square root only for far-field nodes)
+        const T dd = b.v[3] * b.v[3], rhs2 = (a.ph.beta * a.ph.beta) * s;
         if (s == T(0) && a.exact_boxes) far = false;
-        else if (b.v[3] < rhs - band) far = true;
-        else if (b.v[3] > rhs + band) far = false;
+        else if (dd < rhs2 - T(2e-5) * rhs2) far = true;
+        else if (dd > rhs2 + T(2e-5) * rhs2) far = false;
         else {
             far = decide64(b, a.diam64[id], double(qx), double(qy), double(qz), a.beta64);
             ++nre;
+        }
+        if (far) {
+            r = s > T(0) ? Math<T>::rsqrt(s) : T(0);
+            d = s * r;
         }
     } else {
         // squared test with FMA-contracted s and a 1e-12 relative band; the
