@@ -296,7 +296,7 @@ __global__ void __launch_bounds__(kTravThreads) traverse_kernel(const __grid_con
     const T qx = a.q[3 * qi], qy = a.q[3 * qi + 1], qz = a.q[3 * qi + 2];
     Acc<T> acc;
     acc.init();
-    int64_t nleaf = 0, nfar = 0;
+    int32_t nleaf = 0, nfar = 0;  // per query: < 2^31 nodes
     uint64_t h = 0;
     unsigned long long nre = 0;
     int sp = 0;
@@ -415,7 +415,7 @@ __global__ void __launch_bounds__(kTravThreads) packet_kernel(const __grid_const
     if (mask == 0u) return;
     Acc<T> acc;
     acc.init();
-    int64_t nleaf = 0, nfar = 0;
+    int32_t nleaf = 0, nfar = 0;  // per query: < 2^31 nodes
     uint64_t h = 0;
     unsigned long long nre = 0;
     int sp = 0;
@@ -526,7 +526,7 @@ __global__ void __launch_bounds__(kTravThreads) packet_kernel(const __grid_const
 // for every lane of the warp.
 template <class T, bool HASH>
 __device__ __forceinline__ void leaf_visit(const TraverseArgs<T>& a, const Poly<T>* polys, int32_t id, int32_t link,
-                                           T qx, T qy, T qz, Acc<T>& acc, int64_t& nleaf, uint64_t& h) {
+                                           T qx, T qy, T qz, Acc<T>& acc, int32_t& nleaf, uint64_t& h) {
     const int slot = -link - 1;  // exact leaf: the record is the same for every lane
     const int meta = a.leafmeta[slot];
     const int kind = meta & 3, poly = (meta >> 2) - 1;
@@ -608,8 +608,8 @@ __device__ __forceinline__ bool point_far(const TraverseArgs<T>& a, const NodeT<
 // shared by the single-node and child-pair kernels. Returns "descend".
 template <class T, bool HASH>
 __device__ __forceinline__ bool visit(const TraverseArgs<T>& a, const Poly<T>* polys, const NodeT<T>& b,
-                                      int32_t id, T lgc, T qx, T qy, T qz, Acc<T>& acc, int64_t& nleaf,
-                                      int64_t& nfar, uint64_t& h, unsigned long long& nre) {
+                                      int32_t id, T lgc, T qx, T qy, T qz, Acc<T>& acc, int32_t& nleaf,
+                                      int32_t& nfar, uint64_t& h, unsigned long long& nre) {
     int32_t link;
     memcpy(&link, &b.v[7], sizeof(int32_t));
     if (a.use_bh) {
@@ -637,13 +637,13 @@ struct PointVisit {
     }
     template <bool HASH>
     __device__ __forceinline__ bool visit(const TraverseArgs<T>& a, const Poly<T>* polys, const NodeT<T>& b,
-                                          int32_t id, T lgc, Acc<T>& acc, int64_t& nleaf, int64_t& nfar, uint64_t& h,
+                                          int32_t id, T lgc, Acc<T>& acc, int32_t& nleaf, int32_t& nfar, uint64_t& h,
                                           unsigned long long& nre) const {
         return sdgpu::visit<T, HASH>(a, polys, b, id, lgc, qx, qy, qz, acc, nleaf, nfar, h, nre);
     }
     template <bool HASH>
     __device__ __forceinline__ bool far_test(const TraverseArgs<T>& a, const NodeT<T>& b, int32_t id, T lgc, bool emit,
-                                             Acc<T>& acc, int64_t& nfar, uint64_t& h, unsigned long long& nre) const {
+                                             Acc<T>& acc, int32_t& nfar, uint64_t& h, unsigned long long& nre) const {
         if (!a.use_bh) return false;
         T d, r, dx, dy, dz;
         if (!point_far(a, b, id, qx, qy, qz, d, r, dx, dy, dz, nre)) return false;
@@ -662,7 +662,7 @@ struct PointVisit {
     template <bool HASH>
     __device__ __forceinline__ void visit_pair(const TraverseArgs<T>& a, const Poly<T>* polys, const NodeT<T>& bl,
                                                const NodeT<T>& br, int32_t lid, int32_t rid, T lgl, T lgr,
-                                               Acc<T>& acc, int64_t& nleaf, int64_t& nfar, uint64_t& h,
+                                               Acc<T>& acc, int32_t& nleaf, int32_t& nfar, uint64_t& h,
                                                unsigned long long& nre, bool& dl, bool& dr) const {
         dl = visit<HASH>(a, polys, bl, lid, lgl, acc, nleaf, nfar, h, nre);
         dr = visit<HASH>(a, polys, br, rid, lgr, acc, nleaf, nfar, h, nre);

@@ -601,7 +601,7 @@ struct SimplexVisit {
     // collect_contributions (smooth.hpp:114-121), bh_condition (bvh.hpp:185-187)
     template <bool HASH>
     __device__ __forceinline__ bool far_test(const TraverseArgs<double>& a, const NodeT<double>& b, int32_t id,
-                                             double lgc, bool emit, Acc<double>& acc, int64_t& nfar, uint64_t& h,
+                                             double lgc, bool emit, Acc<double>& acc, int32_t& nfar, uint64_t& h,
                                              unsigned long long&) const {
         if (!a.use_bh) return false;
         const sx::BoxProx pr =
@@ -618,7 +618,7 @@ struct SimplexVisit {
     template <bool HASH>
     __device__ __forceinline__ bool visit(const TraverseArgs<double>& a, const Poly<double>* polys,
                                           const NodeT<double>& b, int32_t id, double lgc, Acc<double>& acc,
-                                          int64_t& nleaf, int64_t& nfar, uint64_t& h, unsigned long long& nre) const {
+                                          int32_t& nleaf, int32_t& nfar, uint64_t& h, unsigned long long& nre) const {
         int32_t link;
         memcpy(&link, &b.v[7], sizeof(int32_t));
         if (far_test<HASH>(a, b, id, lgc, true, acc, nfar, h, nre)) return false;
@@ -632,8 +632,8 @@ struct SimplexVisit {
     template <bool HASH>
     __device__ __forceinline__ void visit_pair(const TraverseArgs<double>& a, const Poly<double>* polys,
                                                const NodeT<double>& bl, const NodeT<double>& br, int32_t lid,
-                                               int32_t rid, double lgl, double lgr, Acc<double>& acc, int64_t& nleaf,
-                                               int64_t& nfar, uint64_t& h, unsigned long long& nre, bool& dl,
+                                               int32_t rid, double lgl, double lgr, Acc<double>& acc, int32_t& nleaf,
+                                               int32_t& nfar, uint64_t& h, unsigned long long& nre, bool& dl,
                                                bool& dr) const {
         dl = visit<HASH>(a, polys, bl, lid, lgl, acc, nleaf, nfar, h, nre);
         dr = visit<HASH>(a, polys, br, rid, lgr, acc, nleaf, nfar, h, nre);
@@ -670,7 +670,7 @@ __global__ void __launch_bounds__(kWarpThreads) simplex_warp_kernel(const __grid
     const sx::Geom g = sx::load_query(a.qgeom, a.qdim, qi, true);
     Acc<double> acc;
     acc.init();
-    int64_t nleaf = 0, nfar = 0;
+    int32_t nleaf = 0, nfar = 0;  // per query: < 2^31 nodes
     uint64_t h = 0;
     if (lane == 0) stk[0] = 0;
     __syncwarp();

@@ -134,7 +134,7 @@ __global__ void __launch_bounds__(kTravThreads) pair_kernel(const __grid_constan
     if (mask == 0u) return;
     Acc<T> acc;
     acc.init();
-    int64_t nleaf = 0, nfar = 0;
+    int32_t nleaf = 0, nfar = 0;  // per query: < 2^31 nodes
     uint64_t h = 0;
     unsigned long long nre = 0;
     int32_t cur = 0, cur_link;
@@ -264,7 +264,7 @@ __global__ void __launch_bounds__(kTravThreads) frontier_kernel(const __grid_con
     qv.load(a, qi, valid);
     Acc<T> acc;
     acc.init();
-    int64_t nleaf = 0, nfar = 0;
+    int32_t nleaf = 0, nfar = 0;  // per query: < 2^31 nodes
     uint64_t h = 0;
     unsigned long long nre = 0;
     if (r == 0) stk[0] = 0;
