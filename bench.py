@@ -495,12 +495,12 @@ def run_cfg5(args, rank, world, local):
             exchange = f"nccl (peer exchange unavailable: {type(ex).__name__}: {ex})"
 
     def step():
-        eng.query_points_device(qd.data_ptr(), Q, P, sd.SD_BVH, d_hat.data_ptr(), c_ptr=buf.data_ptr(),
-                                grad_c_ptr=buf.data_ptr() + 8 * Q, stream=stream.cuda_stream)
-        launches[0] = eng.last_launch_count() + 1  # + the finalize / reduce kernel below
         if exchange == "peer":
-            eng.scatter_partials(buf.data_ptr(), buf.data_ptr() + 8 * Q, Q, table.data_ptr(), world, rank, per,
-                                 stream=stream.cuda_stream)
+            # evaluation with the stores into the owners' buffers fused into
+            # its finalize epilogue (sd_query_points_scatter)
+            eng.query_points_scatter(qd.data_ptr(), Q, P, sd.SD_BVH, table.data_ptr(), world, rank, per,
+                                     stream=stream.cuda_stream)
+            launches[0] = eng.last_launch_count()
             if hdl is not None:
                 hdl.barrier(channel=0)
             eng.reduce_owned(sbuf.data_ptr(), per, counts[rank], world, P, d_hat.data_ptr(), grad.data_ptr(),
@@ -509,6 +509,9 @@ def run_cfg5(args, rank, world, local):
                 hdl.barrier(channel=1)
             launches[0] += 1
             return
+        eng.query_points_device(qd.data_ptr(), Q, P, sd.SD_BVH, d_hat.data_ptr(), c_ptr=buf.data_ptr(),
+                                grad_c_ptr=buf.data_ptr() + 8 * Q, stream=stream.cuda_stream)
+        launches[0] = eng.last_launch_count() + 1  # + the finalize kernel below
         if world > 1:
             torch.distributed.all_reduce(buf, op=torch.distributed.ReduceOp.SUM)
         eng.finalize_device(buf.data_ptr(), buf.data_ptr() + 8 * Q, Q, P, d_hat.data_ptr(), grad.data_ptr(),
@@ -565,7 +568,8 @@ def run_cfg5(args, rank, world, local):
                                        "16,777,216 queries uniform in the scene AABB, alpha=100, beta=0.5, fp32 "
                                        "(BASELINE configs[4])",
                            "parallelism": f"primitive-sharded x{world} (Morton shards, {tree_name()} per shard), "
-                                          + ("partials stored into the owners' symmetric buffers over peer memory, "
+                                          + ("partials stored into the owners' symmetric buffers over peer memory "
+                                             "by the evaluation's own finalize epilogue (sd_query_points_scatter), "
                                              "owner-side reduce + finalize" if exchange == "peer" else
                                              f"one NCCL all_reduce(SUM) of 4 fp64 per query; exchange={exchange}"),
                            "primitives_per_gpu": len(sh.kinds), "l2": "flushed between timed steps"},

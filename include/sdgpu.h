@@ -174,6 +174,16 @@ int sd_finalize_device(sd_ctx* ctx, const double* c, const double* grad_c, int64
  * order and finalised (result_from_accum) into d_hat / grad. */
 int sd_scatter_partials(sd_ctx* ctx, const double* c, const double* grad_c, int64_t Q, double* const* peer_bufs,
                         int32_t world, int32_t rank, int64_t q_per_owner, void* stream);
+/* The same exchange fused into the evaluation: sd_query_points_device's
+ * work for this rank's shard, whose finalize epilogue stores the unshifted
+ * partials (c, grad_c) of query i straight into rank i / q_per_owner's
+ * symmetric buffer (slot `rank`) instead of writing them locally -- no
+ * separate scatter pass. q (device, fp32 or fp64 as the context); per-query
+ * leaf / far-field counters optional (device, NULL to skip). Follow with a
+ * barrier and sd_reduce_owned. */
+int sd_query_points_scatter(sd_ctx* ctx, const void* q, int64_t Q, const sd_params* p, int mode,
+                            double* const* peer_bufs, int32_t world, int32_t rank, int64_t q_per_owner,
+                            int64_t* leaves, int64_t* far_field, void* stream);
 int sd_reduce_owned(sd_ctx* ctx, const double* sbuf, int64_t q_per_owner, int64_t n_owned, int32_t world,
                     const sd_params* p, double* d_hat, double* grad, void* stream);
 

@@ -41,6 +41,7 @@ EXPORTED_SYMBOLS = (
     "sd_query_simplices",
     "sd_mesh_dist",
     "sd_scatter_partials",
+    "sd_query_points_scatter",
     "sd_reduce_owned",
     "sd_render",
     "sd_grid_benchmark",
@@ -121,6 +122,7 @@ def lib():
             "sd_mesh_dist": (C.c_int, [vp, vp, i64, vp, vp, i64, P(_Params), f64, C.c_int, vp, vp, vp]),
             "sd_render": (C.c_int, [vp, P(_Params), C.c_int, P(_RenderConfig), vp, vp, vp, vp]),
             "sd_scatter_partials": (C.c_int, [vp, vp, vp, i64, vp, i32, i32, i64, vp]),
+            "sd_query_points_scatter": (C.c_int, [vp, vp, i64, P(_Params), C.c_int, vp, i32, i32, i64, vp, vp, vp]),
             "sd_reduce_owned": (C.c_int, [vp, vp, i64, i64, i32, P(_Params), vp, vp, vp]),
             "sd_grid_benchmark": (C.c_int, [vp, P(_Params), C.c_int, i32, vp, vp, vp, vp]),
             "sd_write_ppm": (C.c_int, [vp, i32, i32, C.c_char_p]),
@@ -316,6 +318,19 @@ class Engine:
         _check(lib().sd_scatter_partials(self.h, C.c_void_p(c_ptr), C.c_void_p(grad_c_ptr), n,
                                          C.c_void_p(peer_table_ptr), world, rank, q_per_owner,
                                          C.c_void_p(stream) if stream else None))
+
+    def query_points_scatter(self, q_ptr: int, n: int, params: SmoothParams, mode: int, peer_table_ptr: int,
+                             world: int, rank: int, q_per_owner: int, leaves_ptr: int | None = None,
+                             far_ptr: int | None = None, stream: int | None = None):
+        """Evaluate this rank's shard for device queries q_ptr and store the
+        partial sums straight into the owners' symmetric buffers from the
+        finalize epilogue (the fused form of query_points_device +
+        scatter_partials)."""
+        _check(lib().sd_query_points_scatter(self.h, C.c_void_p(q_ptr), n, C.byref(params._c()), mode,
+                                             C.c_void_p(peer_table_ptr), world, rank, q_per_owner,
+                                             C.c_void_p(leaves_ptr) if leaves_ptr else None,
+                                             C.c_void_p(far_ptr) if far_ptr else None,
+                                             C.c_void_p(stream) if stream else None))
 
     def reduce_owned(self, sbuf_ptr: int, q_per_owner: int, n_owned: int, world: int, params: SmoothParams,
                      d_hat_ptr: int, grad_ptr: int | None, stream: int | None = None):

@@ -1023,6 +1023,30 @@ int sd_scatter_partials(sd_ctx* c, const double* cs, const double* gc, int64_t Q
     });
 }
 
+int sd_query_points_scatter(sd_ctx* c, const void* q, int64_t Q, const sd_params* p, int mode,
+                            double* const* peer_bufs, int32_t world, int32_t rank, int64_t q_per_owner,
+                            int64_t* leaves, int64_t* far_field, void* stream) {
+    return guard([&] {
+        if (!c) throw ArgError{"ctx is NULL"};
+        check_params(p);
+        check_ready(*c, mode);
+        if (Q < 0 || world < 1 || rank < 0 || rank >= world || q_per_owner <= 0 || q_per_owner * world < Q ||
+            (Q > 0 && (!q || !peer_bufs)))
+            throw ArgError{"bad exchange arguments"};
+        if (Q == 0) return;
+        DeviceScope ds(c->device);
+        FinalizeOut out;
+        out.peers = peer_bufs;
+        out.peer_rank = rank;
+        out.peer_qown = q_per_owner;
+        out.leaves = leaves;
+        out.far_field = far_field;
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        if (c->precision == SD_FP32) dispatch<float>(*c, static_cast<const float*>(q), Q, *p, mode, out, st);
+        else dispatch<double>(*c, static_cast<const double*>(q), Q, *p, mode, out, st);
+    });
+}
+
 int sd_reduce_owned(sd_ctx* c, const double* sbuf, int64_t q_per_owner, int64_t n_owned, int32_t world,
                     const sd_params* p, double* d_hat, double* grad, void* stream) {
     return guard([&] {

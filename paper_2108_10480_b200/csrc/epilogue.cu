@@ -23,6 +23,18 @@ __device__ __forceinline__ void finalize_write(double M, double s, double gx, do
     const double c = s * scale;
     const double cx = gx * scale, cy = gy * scale, cz = gz * scale;
     const int64_t j = perm ? perm[i] : i;  // tree path: undo the query sort
+    if (o.peers) {  // fused exchange: NVLink stores into the owner's buffer
+        const int64_t ow = j / o.peer_qown, k = j - ow * o.peer_qown;
+        double* dst = o.peers[ow] + size_t(o.peer_rank) * 4 * o.peer_qown + k;
+        dst[0] = c;
+        dst[o.peer_qown] = cx;
+        dst[2 * o.peer_qown] = cy;
+        dst[3 * o.peer_qown] = cz;
+        if (o.leaves) o.leaves[j] = leaves_in ? leaves_in[i] : const_leaves;
+        if (o.far_field) o.far_field[j] = far_in ? far_in[i] : 0;
+        if (o.hash) o.hash[j] = hash_in ? hash_in[i] : 0;
+        return;
+    }
     double d = INFINITY, ax = 0, ay = 0, az = 0;
     if (c > 0.0) {
         d = -log(c) / alpha;
@@ -147,6 +159,14 @@ cudaError_t launch_finalize_sums(const double* c, const double* grad_c, int64_t 
 __global__ void empty_kernel(int64_t Q, FinalizeOut o) {
     const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= Q) return;
+    if (o.peers) {  // an empty shard contributes zero partials
+        const int64_t ow = i / o.peer_qown, k = i - ow * o.peer_qown;
+        double* dst = o.peers[ow] + size_t(o.peer_rank) * 4 * o.peer_qown + k;
+        dst[0] = dst[o.peer_qown] = dst[2 * o.peer_qown] = dst[3 * o.peer_qown] = 0.0;
+        if (o.leaves) o.leaves[i] = 0;
+        if (o.far_field) o.far_field[i] = 0;
+        return;
+    }
     o.d_hat[i] = INFINITY;
     if (o.grad) o.grad[3 * i] = o.grad[3 * i + 1] = o.grad[3 * i + 2] = 0.0;
     if (o.c) o.c[i] = 0.0;
@@ -170,6 +190,9 @@ cudaError_t launch_empty_result(int64_t Q, const FinalizeOut& out, cudaStream_t 
 // the world contributions of its queries in rank order and finalises them
 // (result_from_accum, smooth.hpp:147-159): a reduce-scatter done by the
 // producing ranks' own stores, half the traffic of an all-reduce.
+// sd_query_points_scatter fuses the stores into K4 (finalize_write above:
+// FinalizeOut::peers), so the partials never round-trip through local
+// memory; this standalone kernel serves partials computed elsewhere.
 __global__ void scatter_partials_kernel(const double* __restrict__ c, const double* __restrict__ gc, int64_t Q,
                                         double* const* __restrict__ peers, int rank, int64_t qown) {
     const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;

@@ -47,7 +47,15 @@ struct FinalizeOut {
     int64_t* leaves = nullptr;
     int64_t* far_field = nullptr;
     uint64_t* hash = nullptr;
+    // primitive-sharded exchange fused into the epilogue: when set, the
+    // unshifted partials (c, grad_c) of query j go straight into the owner's
+    // symmetric buffer peers[j / peer_qown] (slot peer_rank, SoA [4][qown])
+    // instead of d_hat / grad / c / grad_c
+    double* const* peers = nullptr;
+    int peer_rank = 0;
+    int64_t peer_qown = 0;
 };
+
 cudaError_t launch_finalize(const double* part, int splits, int64_t Q, double alpha, double epsilon,
                             int64_t const_leaves, const int64_t* leaves_in, const int64_t* far_in,
                             const uint64_t* hash_in, const int64_t* perm, const FinalizeOut& out, cudaStream_t st);

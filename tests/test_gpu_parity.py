@@ -769,3 +769,75 @@ def test_host_chunk_pipeline_matches_unpipelined(sd, oracle, prec, monkeypatch):
         for f in ("leaves", "far_field", "decision_hash"):
             assert np.array_equal(getattr(a, f), getattr(b, f)), (mode, f)
         assert_close(b, a, prec, 120.0, f"pipeline mode {mode}")
+
+
+@pytest.mark.parametrize("prec,beta", [(1, 0.0), (0, 0.0), (1, 0.5), (0, 0.5)])
+def test_fused_evaluate_and_scatter_with_virtual_ranks(sd, oracle, prec, beta):
+    """sd_query_points_scatter: the finalize epilogue stores every query's
+    unshifted partials straight into its owner's buffer (4 virtual ranks, one
+    GPU, a device pointer table as over NVLink). Bit-equal to the unfused
+    query_points_device (c, grad_c) + scatter_partials, including an empty
+    shard, exact and BVH; the owners' reduce matches the oracle."""
+    import torch
+    from paper_2108_10480_b200 import sharding
+    O = oracle
+    m0 = O.random_scene(12, 400)
+    qs = O.QueryStream(62).draw_points(m0, 700)
+    m, q = prep(O, m0, qs, prec)
+    wt = O.Weights.build(m).table
+    world = 4
+    shards = sharding.primitive_shards(m.vertices, m.simplices, m.kinds, wt.poly_index, world - 1)
+    shards.append(None)  # rank 3 holds no primitives
+    P = sd.SmoothParams(alpha=100.0, beta=beta)
+    mode = sd.SD_BVH if beta > 0 else sd.SD_EXACT
+    dev = torch.device("cuda", 0)
+    n = len(q)
+    per, counts = sharding.owner_blocks(n, world)
+    fused = [torch.full((world * 4 * per,), np.nan, dtype=torch.float64, device=dev) for _ in range(world)]
+    plain = [torch.full((world * 4 * per,), np.nan, dtype=torch.float64, device=dev) for _ in range(world)]
+    tf = torch.tensor([b.data_ptr() for b in fused], dtype=torch.int64, device=dev)
+    tp = torch.tensor([b.data_ptr() for b in plain], dtype=torch.int64, device=dev)
+    qd = torch.tensor(q, dtype=torch.float64 if prec else torch.float32, device=dev)
+    for r, s in enumerate(shards):
+        e = sd.Engine(0, prec)
+        if s is None:
+            e.set_geometry(np.zeros((0, 3)), np.zeros((0, 3), np.int32), np.zeros(0, np.uint8))
+            e.set_weights(wt.A, wt.sup_wtilde, wt.edge_a, wt.tri_stored, np.zeros(0, np.int32))
+        else:
+            e.set_geometry(s.vertices, s.simplices, s.kinds)
+            e.set_weights(wt.A, wt.sup_wtilde, wt.edge_a, wt.tri_stored, s.poly_index)
+            if beta > 0:
+                e.build_bvh(sd.SD_BVH_MEDIAN)
+        lf = torch.empty(n, dtype=torch.int64, device=dev)
+        ff = torch.empty(n, dtype=torch.int64, device=dev)
+        e.query_points_scatter(qd.data_ptr(), n, P, mode, tf.data_ptr(), world, r, per, lf.data_ptr(), ff.data_ptr())
+        c = torch.empty(n, dtype=torch.float64, device=dev)
+        g = torch.empty(n, 3, dtype=torch.float64, device=dev)
+        d = torch.empty(n, dtype=torch.float64, device=dev)
+        lp = torch.empty(n, dtype=torch.int64, device=dev)
+        fp = torch.empty(n, dtype=torch.int64, device=dev)
+        e.query_points_device(qd.data_ptr(), n, P, mode, d.data_ptr(), c_ptr=c.data_ptr(), grad_c_ptr=g.data_ptr(),
+                              leaves_ptr=lp.data_ptr(), far_ptr=fp.data_ptr())
+        e.scatter_partials(c.data_ptr(), g.data_ptr(), n, tp.data_ptr(), world, r, per)
+        torch.cuda.synchronize()
+        assert torch.equal(lf, lp) and torch.equal(ff, fp)
+    for o in range(world):
+        a = fused[o].view(world, 4, per)[:, :, :counts[o]]
+        b = plain[o].view(world, 4, per)[:, :, :counts[o]]
+        assert torch.equal(a, b), f"owner {o}"
+    # owners finalise; the whole matches the oracle on the full mesh
+    ref = O.query(m, O.Weights.from_table(wt), q, O.Params(alpha=100.0, beta=0.0))
+    d_all = np.zeros(n)
+    for o in range(world):
+        dd = torch.empty(max(1, counts[o]), dtype=torch.float64, device=dev)
+        e.reduce_owned(fused[o].data_ptr(), per, counts[o], world, P, dd.data_ptr(), None)
+        torch.cuda.synchronize()
+        d_all[o * per:o * per + counts[o]] = dd.cpu().numpy()[:counts[o]]
+    if beta == 0.0:
+        td = TOL[prec][0]
+        fin = np.isfinite(ref.d_hat)
+        assert (np.isfinite(d_all) == fin).all()
+        assert (np.abs(d_all[fin] - ref.d_hat[fin]) <= td * np.maximum(1.0, np.abs(ref.d_hat[fin]))).all()
+    else:  # Barnes-Hut per shard: conservative w.r.t. the exact whole-mesh field
+        fin = np.isfinite(ref.d_hat)
+        assert (d_all[fin] <= ref.d_hat[fin] + 1e-5 * np.maximum(1.0, np.abs(ref.d_hat[fin]))).all()
