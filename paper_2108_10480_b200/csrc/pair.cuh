@@ -77,9 +77,12 @@ __device__ __forceinline__ T bump(Acc<T>& acc, T xm, F&& absx) {
     return xm;
 }
 
+// (unordered compare: a distance that overflowed the compute type -- s = inf,
+// d = inf * 0 = NaN, queries beyond ~1e19 in fp32 -- is masked like the
+// huge distance it stands for)
 template <class T>
 __device__ __forceinline__ T masked(const Phys<T>& ph, T d, T xm) {
-    return d > ph.dmax ? T(-INFINITY) : xm;
+    return !(d <= ph.dmax) ? T(-INFINITY) : xm;
 }
 
 // Exponent (x - m) and gradient factor k = dnum / base of a polynomial

@@ -94,8 +94,8 @@ template <int MODE = 0, class F>
 __device__ __forceinline__ f2 exp_terms(const Phys<float>& ph, Acc2& a, f2 d, f2 xm, F&& absx) {
     if constexpr (MODE == 2) return pack(Math<float>::ex2(lo(xm)), Math<float>::ex2(hi(xm)));
     float x0 = lo(xm), x1 = hi(xm);
-    x0 = lo(d) > ph.dmax ? -INFINITY : x0;
-    x1 = hi(d) > ph.dmax ? -INFINITY : x1;
+    x0 = !(lo(d) <= ph.dmax) ? -INFINITY : x0;  // NaN (overflowed) distances too
+    x1 = !(hi(d) <= ph.dmax) ? -INFINITY : x1;
     if (MODE == 0 && (x0 > 0.f || x1 > 0.f)) {
         if (x0 > 0.f) {
             const float x = absx(0);

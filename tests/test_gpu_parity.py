@@ -841,3 +841,27 @@ def test_fused_evaluate_and_scatter_with_virtual_ranks(sd, oracle, prec, beta):
     else:  # Barnes-Hut per shard: conservative w.r.t. the exact whole-mesh field
         fin = np.isfinite(ref.d_hat)
         assert (d_all[fin] <= ref.d_hat[fin] + 1e-5 * np.maximum(1.0, np.abs(ref.d_hat[fin]))).all()
+
+
+@pytest.mark.parametrize("prec", [0, 1])
+def test_huge_query_coordinates_underflow_like_the_reference(sd, oracle, prec):
+    """Queries so far away that |q - p|^2 overflows the compute type (fp32:
+    beyond ~1.8e19) give c = 0, d_hat = +inf and a zero gradient, as the
+    reference's -708 mask does for the huge distance; exact and BVH, with
+    identical decisions; ordinary queries in the same batch are unaffected."""
+    O = oracle
+    m0 = O.random_scene(5, 200)
+    qs = np.concatenate([O.QueryStream(55).draw_points(m0, 40),
+                         [[1e20, 0.0, 0.0], [0.0, -1e30, 0.0], [3e19, 3e19, 3e19], [1e15, 2.0, -1e15]]])
+    m, q = prep(O, m0, qs, prec)
+    w, t = O.Weights.build(m), O.Tree.build(m)
+    e = engine_for(sd, O, m, w, prec, tree=t)
+    for beta in (0.0, 0.5):
+        p = O.Params(alpha=100.0, beta=beta)
+        ref = O.query(m, w, q, p, tree=t if beta > 0 else None)
+        got = e.smooth_min_dist(q, sd.SmoothParams(alpha=100.0, beta=beta)) if beta > 0 else \
+            e.smooth_min_dist_flat(q, sd.SmoothParams(alpha=100.0, beta=0.0))
+        assert np.isinf(ref.d_hat[-4:]).all() and np.isinf(got.d_hat[-4:]).all()
+        assert not got.grad[-4:].any() and not np.isnan(got.grad).any()
+        assert (got.leaves == ref.leaves).all() and (got.far_field == ref.far_field).all()
+        assert_close(got, ref, prec, 100.0, f"huge coords beta {beta}")
