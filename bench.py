@@ -830,6 +830,8 @@ def run_ours(args, rank, world, local):
                                         "MEASURED_PEAKS.json has no FP32/FP64 entry",
                          "mufu_frac": pairs_per_rank * MUFU_PER_EDGE_PAIR / (ms_max * 1e-3) / 1e12 / peaks["mufu_tops"],
                          "peaks": peaks})
+            # bound-aware roofline = max(flops / P_fma, mufu / P_mufu)
+            roof["bound_aware_frac"] = max(roof["frac"], roof["mufu_frac"])
         cpu = None
         if world == 1 and not args.no_cpu:
             import oracle as O
