@@ -669,21 +669,85 @@ struct PointVisit {
     }
 };
 
-// Morton codes (10 bits per axis over [lo, hi]) + CUB radix sort: the
-// returned permutation lists query indices in spatial order (device
-// memory owned by the context).
+struct QBox {
+    float lo[3], hi[3];
+};
+struct QBoxUnion {
+    __device__ __forceinline__ QBox operator()(const QBox& a, const QBox& b) const {
+        QBox r;
+        for (int k = 0; k < 3; ++k) {
+            r.lo[k] = fminf(a.lo[k], b.lo[k]);
+            r.hi[k] = fmaxf(a.hi[k], b.hi[k]);
+        }
+        return r;
+    }
+};
+template <class T>
+struct QBoxOf {
+    const T* q;
+    __device__ __forceinline__ QBox operator()(int64_t i) const {
+        QBox r;
+        for (int k = 0; k < 3; ++k) r.lo[k] = r.hi[k] = float(q[3 * i + k]);
+        return r;
+    }
+};
+
+// Morton keys over the union of [lo, hi] (the root box) and the queries' own
+// box, read from device memory (no host round trip): queries outside the
+// scene keep distinct cells instead of piling up on its faces
+template <class T>
+__global__ void query_morton_union(const T* __restrict__ q, int64_t Q, double3 lo, double3 hi,
+                                   const QBox* __restrict__ qb, uint32_t* keys, int64_t* idx) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= Q) return;
+    const double l[3] = {fmin(lo.x, double(qb->lo[0])), fmin(lo.y, double(qb->lo[1])), fmin(lo.z, double(qb->lo[2]))};
+    const double h[3] = {fmax(hi.x, double(qb->hi[0])), fmax(hi.y, double(qb->hi[1])), fmax(hi.z, double(qb->hi[2]))};
+    uint32_t key = 0;
+    for (int a = 0; a < 3; ++a) {
+        const double s = h[a] > l[a] ? 1024.0 / (h[a] - l[a]) : 0.0;
+        const uint32_t cell = uint32_t(fmin(fmax((double(q[3 * i + a]) - l[a]) * s, 0.0), 1023.0));
+        key |= spread10(cell) << (2 - a);
+    }
+    keys[i] = key;
+    idx[i] = i;
+}
+
+// Morton codes (10 bits per axis over [lo, hi] joined with the queries'
+// box) + CUB radix sort: the returned permutation lists query indices in
+// spatial order (device memory owned by the context).
 template <class T>
 const int64_t* sort_queries(Ctx& c, const T* q, int64_t Q, const double lo[3], const double hi[3], cudaStream_t st,
                             int64_t& launches) {
-    auto inv = [](double l, double h) { return h > l ? 1024.0 / (h - l) : 0.0; };
-    const double3 dlo = make_double3(lo[0], lo[1], lo[2]);
-    const double3 iv = make_double3(inv(lo[0], hi[0]), inv(lo[1], hi[1]), inv(lo[2], hi[2]));
     uint32_t* keys = static_cast<uint32_t*>(c.keys.ensure(size_t(Q) * 2 * sizeof(uint32_t)));
     int64_t* idx = static_cast<int64_t*>(c.perm.ensure(size_t(Q) * 2 * sizeof(int64_t)));
     const unsigned blocks = unsigned((Q + 255) / 256);
-    query_morton<T><<<blocks, 256, 0, st>>>(q, Q, dlo, iv, keys, idx);
+    static const bool union_box = [] {
+        const char* e = std::getenv("SDGPU_QBOX");
+        return !(e && *e == '0');
+    }();
+    if (union_box) {
+        QBox* qb = static_cast<QBox*>(c.qbox.ensure(sizeof(QBox)));
+        QBox init;
+        for (int k = 0; k < 3; ++k) {
+            init.lo[k] = INFINITY;
+            init.hi[k] = -INFINITY;
+        }
+        cub::CountingInputIterator<int64_t> cnt(0);
+        cub::TransformInputIterator<QBox, QBoxOf<T>, cub::CountingInputIterator<int64_t>> in(cnt, QBoxOf<T>{q});
+        size_t tb = 0;
+        cub::DeviceReduce::Reduce(nullptr, tb, in, qb, Q, QBoxUnion{}, init, st);
+        check_cuda(cub::DeviceReduce::Reduce(c.tmp.ensure(tb), tb, in, qb, Q, QBoxUnion{}, init, st), "query box");
+        query_morton_union<T><<<blocks, 256, 0, st>>>(q, Q, make_double3(lo[0], lo[1], lo[2]),
+                                                      make_double3(hi[0], hi[1], hi[2]), qb, keys, idx);
+        launches += 2;
+    } else {
+        auto inv = [](double l, double h) { return h > l ? 1024.0 / (h - l) : 0.0; };
+        const double3 dlo = make_double3(lo[0], lo[1], lo[2]);
+        const double3 iv = make_double3(inv(lo[0], hi[0]), inv(lo[1], hi[1]), inv(lo[2], hi[2]));
+        query_morton<T><<<blocks, 256, 0, st>>>(q, Q, dlo, iv, keys, idx);
+        ++launches;
+    }
     check_cuda(cudaGetLastError(), "query morton");
-    ++launches;
     size_t tmp_bytes = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys, keys + Q, idx, idx + Q, int(Q), 0, 30, st);
     void* tmp = c.tmp.ensure(tmp_bytes);

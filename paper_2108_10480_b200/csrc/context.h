@@ -140,7 +140,7 @@ struct Ctx {
 
     // scratch
     DevBuf qd, qT, part, out_d, out_g, out_c, out_gc, out_l, out_f, out_h;
-    DevBuf perm, keys, tmp, tmp2, counters, polys, flag;
+    DevBuf perm, keys, tmp, tmp2, counters, polys, flag, qbox;
     int64_t last_launches = 0;
 };
 
