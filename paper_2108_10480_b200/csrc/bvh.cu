@@ -524,9 +524,9 @@ __global__ void __launch_bounds__(kTravThreads) packet_kernel(const __grid_const
 
 // Exact leaf term of one lane (smooth.hpp:51-61); the record is the same
 // for every lane of the warp.
-template <class T, bool HASH>
+template <class T, bool HASH, class CNT>
 __device__ __forceinline__ void leaf_visit(const TraverseArgs<T>& a, const Poly<T>* polys, int32_t id, int32_t link,
-                                           T qx, T qy, T qz, Acc<T>& acc, int32_t& nleaf, uint64_t& h) {
+                                           T qx, T qy, T qz, Acc<T>& acc, CNT& nleaf, uint64_t& h) {
     const int slot = -link - 1;  // exact leaf: the record is the same for every lane
     const int meta = a.leafmeta[slot];
     const int kind = meta & 3, poly = (meta >> 2) - 1;
@@ -606,10 +606,10 @@ __device__ __forceinline__ bool point_far(const TraverseArgs<T>& a, const NodeT<
 
 // One node test of the packet traversal for one lane (decision + term),
 // shared by the single-node and child-pair kernels. Returns "descend".
-template <class T, bool HASH>
+template <class T, bool HASH, class CNT>
 __device__ __forceinline__ bool visit(const TraverseArgs<T>& a, const Poly<T>* polys, const NodeT<T>& b,
-                                      int32_t id, T lgc, T qx, T qy, T qz, Acc<T>& acc, int32_t& nleaf,
-                                      int32_t& nfar, uint64_t& h, unsigned long long& nre) {
+                                      int32_t id, T lgc, T qx, T qy, T qz, Acc<T>& acc, CNT& nleaf,
+                                      CNT& nfar, uint64_t& h, unsigned long long& nre) {
     int32_t link;
     memcpy(&link, &b.v[7], sizeof(int32_t));
     if (a.use_bh) {
@@ -622,7 +622,7 @@ __device__ __forceinline__ bool visit(const TraverseArgs<T>& a, const Poly<T>* p
         }
     }
     if (link >= 0) return true;
-    leaf_visit<T, HASH>(a, polys, id, link, qx, qy, qz, acc, nleaf, h);
+    leaf_visit<T, HASH, CNT>(a, polys, id, link, qx, qy, qz, acc, nleaf, h);
     return false;
 }
 
@@ -635,15 +635,15 @@ struct PointVisit {
         qy = valid ? a.q[3 * qi + 1] : T(0);
         qz = valid ? a.q[3 * qi + 2] : T(0);
     }
-    template <bool HASH>
+    template <bool HASH, class CNT>
     __device__ __forceinline__ bool visit(const TraverseArgs<T>& a, const Poly<T>* polys, const NodeT<T>& b,
-                                          int32_t id, T lgc, Acc<T>& acc, int32_t& nleaf, int32_t& nfar, uint64_t& h,
+                                          int32_t id, T lgc, Acc<T>& acc, CNT& nleaf, CNT& nfar, uint64_t& h,
                                           unsigned long long& nre) const {
-        return sdgpu::visit<T, HASH>(a, polys, b, id, lgc, qx, qy, qz, acc, nleaf, nfar, h, nre);
+        return sdgpu::visit<T, HASH, CNT>(a, polys, b, id, lgc, qx, qy, qz, acc, nleaf, nfar, h, nre);
     }
-    template <bool HASH>
+    template <bool HASH, class CNT>
     __device__ __forceinline__ bool far_test(const TraverseArgs<T>& a, const NodeT<T>& b, int32_t id, T lgc, bool emit,
-                                             Acc<T>& acc, int32_t& nfar, uint64_t& h, unsigned long long& nre) const {
+                                             Acc<T>& acc, CNT& nfar, uint64_t& h, unsigned long long& nre) const {
         if (!a.use_bh) return false;
         T d, r, dx, dy, dz;
         if (!point_far(a, b, id, qx, qy, qz, d, r, dx, dy, dz, nre)) return false;
@@ -659,10 +659,10 @@ struct PointVisit {
     // packed fp32x2 variant with a branch-free far-field path measured
     // slower on cfg4 -- 33.0 ms vs 29.7 ms: 80 registers and an exponential
     // for every child -- and was dropped.)
-    template <bool HASH>
+    template <bool HASH, class CNT>
     __device__ __forceinline__ void visit_pair(const TraverseArgs<T>& a, const Poly<T>* polys, const NodeT<T>& bl,
                                                const NodeT<T>& br, int32_t lid, int32_t rid, T lgl, T lgr,
-                                               Acc<T>& acc, int32_t& nleaf, int32_t& nfar, uint64_t& h,
+                                               Acc<T>& acc, CNT& nleaf, CNT& nfar, uint64_t& h,
                                                unsigned long long& nre, bool& dl, bool& dr) const {
         dl = visit<HASH>(a, polys, bl, lid, lgl, acc, nleaf, nfar, h, nre);
         dr = visit<HASH>(a, polys, br, rid, lgr, acc, nleaf, nfar, h, nre);
@@ -750,7 +750,9 @@ const int64_t* sort_queries(Ctx& c, const T* q, int64_t Q, const double lo[3], c
         const char* e = std::getenv("SDGPU_QBOX");
         return !(e && *e == '0');
     }();
-    if (union_box) {
+    // small batches (the few-query kernels walk one query per warp, and the
+    // extra reduction launch shows in re-query loops): root-box Morton order
+    if (union_box && Q > 65536) {
         QBox* qb = static_cast<QBox*>(c.qbox.ensure(sizeof(QBox)));
         QBox init;
         for (int k = 0; k < 3; ++k) {

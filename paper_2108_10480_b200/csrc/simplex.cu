@@ -599,9 +599,9 @@ struct SimplexVisit {
         g = sx::load_query(a.qgeom, a.qdim, qi, valid);
     }
     // collect_contributions (smooth.hpp:114-121), bh_condition (bvh.hpp:185-187)
-    template <bool HASH>
+    template <bool HASH, class CNT>
     __device__ __forceinline__ bool far_test(const TraverseArgs<double>& a, const NodeT<double>& b, int32_t id,
-                                             double lgc, bool emit, Acc<double>& acc, int32_t& nfar, uint64_t& h,
+                                             double lgc, bool emit, Acc<double>& acc, CNT& nfar, uint64_t& h,
                                              unsigned long long&) const {
         if (!a.use_bh) return false;
         const sx::BoxProx pr =
@@ -615,10 +615,10 @@ struct SimplexVisit {
         }
         return true;
     }
-    template <bool HASH>
+    template <bool HASH, class CNT>
     __device__ __forceinline__ bool visit(const TraverseArgs<double>& a, const Poly<double>* polys,
                                           const NodeT<double>& b, int32_t id, double lgc, Acc<double>& acc,
-                                          int32_t& nleaf, int32_t& nfar, uint64_t& h, unsigned long long& nre) const {
+                                          CNT& nleaf, CNT& nfar, uint64_t& h, unsigned long long& nre) const {
         int32_t link;
         memcpy(&link, &b.v[7], sizeof(int32_t));
         if (far_test<HASH>(a, b, id, lgc, true, acc, nfar, h, nre)) return false;
@@ -629,11 +629,11 @@ struct SimplexVisit {
         if constexpr (HASH) h += decision_mix(uint64_t(id), 2);
         return false;
     }
-    template <bool HASH>
+    template <bool HASH, class CNT>
     __device__ __forceinline__ void visit_pair(const TraverseArgs<double>& a, const Poly<double>* polys,
                                                const NodeT<double>& bl, const NodeT<double>& br, int32_t lid,
-                                               int32_t rid, double lgl, double lgr, Acc<double>& acc, int32_t& nleaf,
-                                               int32_t& nfar, uint64_t& h, unsigned long long& nre, bool& dl,
+                                               int32_t rid, double lgl, double lgr, Acc<double>& acc, CNT& nleaf,
+                                               CNT& nfar, uint64_t& h, unsigned long long& nre, bool& dl,
                                                bool& dr) const {
         dl = visit<HASH>(a, polys, bl, lid, lgl, acc, nleaf, nfar, h, nre);
         dr = visit<HASH>(a, polys, br, rid, lgr, acc, nleaf, nfar, h, nre);
