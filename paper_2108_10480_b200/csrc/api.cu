@@ -927,15 +927,18 @@ int sd_query_points(sd_ctx* c, const double* q, int64_t Q, const sd_params* p, i
         if (o->far_field) out.far_field = static_cast<int64_t*>(c->out_f.ensure(size_t(Q) * sizeof(int64_t)));
         if (o->decision_hash) out.hash = static_cast<uint64_t*>(c->out_h.ensure(size_t(Q) * sizeof(uint64_t)));
         float* qf = c->precision == SD_FP32 ? static_cast<float*>(c->qT.ensure(size_t(Q) * 3 * sizeof(float))) : nullptr;
-        // Optional chunk pipeline (SDGPU_PIPELINE=1, batches >= 2^17): every
+        // Optional chunk pipeline (SDGPU_PIPELINE=1: 4 chunks, =k: k chunks;
+        // batches >= 2^17): every
         // chunk's H2D is queued on the copy stream up front, chunk k computes
         // on the context stream once its queries landed, and its results go
         // back on the copy stream while chunk k+1 computes. Off by default:
         // on cfg2 the transfers are ~4 % of the step and four quarter-size
         // exact launches lose more than the overlap gains (e2e 6.6e11 vs
-        // 7.05e11 pair-evals/s unpipelined).
+        // 7.05e11 pair-evals/s unpipelined; tools/e2e_chunks.py medians: 1 chunk
+        // 7.18 ms, 2 chunks 7.25 ms, 4 chunks 7.88 ms).
         const char* pe = std::getenv("SDGPU_PIPELINE");
-        const int chunks = (Q >= (int64_t(1) << 17) && pe && *pe == '1') ? 4 : 1;
+        const int want = pe && *pe ? std::atoi(pe) : 0;  // 1: four chunks, k >= 2: k chunks
+        const int chunks = (Q >= (int64_t(1) << 17) && want > 0) ? (want == 1 ? 4 : std::min(want, 16)) : 1;
         cudaStream_t cs = st;
         if (chunks > 1) {
             if (!c->copy_stream) check_cuda(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking), "stream");
