@@ -35,7 +35,7 @@ FLOPS_PER_EDGE_PAIR = 62      # SURVEY 8(d) canonical count, S != 1
 FLOPS_PER_TRI_PAIR = 192
 FLOPS_BOX_TEST, FLOPS_FAR_TERM = 10, 12
 BYTES_NODE, BYTES_LEAF = 32, 100  # fp32 traversal node record; leaf record (96 B) + meta
-MUFU_PER_EDGE_PAIR = 4            # rsqrt, lg2, rcp, ex2
+MUFU_PER_EDGE_PAIR = 3            # rsqrt, lg2, ex2 (no reciprocal on certified-positive weights)
 QUERIES_PER_GPU = 262144
 ALPHA = 100.0
 
@@ -737,7 +737,7 @@ def run_ours(args, rank, world, local):
     global ALPHA, FLOPS_PER_EDGE_PAIR, MUFU_PER_EDGE_PAIR
     if args.config == 3:
         ALPHA = w.alpha
-        FLOPS_PER_EDGE_PAIR, MUFU_PER_EDGE_PAIR = FLOPS_PER_TRI_PAIR, 4
+        FLOPS_PER_EDGE_PAIR, MUFU_PER_EDGE_PAIR = FLOPS_PER_TRI_PAIR, 3
     if args.config == 1:
         ALPHA = w.alpha
         FLOPS_PER_EDGE_PAIR, MUFU_PER_EDGE_PAIR = 20, 2
@@ -813,9 +813,9 @@ def run_ours(args, rank, world, local):
         achieved = pairs_per_rank * FLOPS_PER_EDGE_PAIR / (ms_max * 1e-3) / 1e12
         # dram read + write of the dominant launch, from the committed ncu
         # capture of this workload (cfg2 fp32, tile-bound kernel):
-        # profiles/r1_v5_exact_edge_details.csv (133.5 MB read + 68.9 MB written,
-        # the fp64 per-query partial state of 12 primitive splits)
-        traffic = 2.024e8 if (args.config == 2 and not fp64) else None
+        # profiles/r1_v6_exact_edge_details.csv (132.6 MB read + 68.2 MB written,
+        # the fp64 per-query partial state of the 8 primitive splits)
+        traffic = 2.008e8 if (args.config == 2 and not fp64) else None
         roof = {"bound": "fp64-fma" if fp64 else "fp32-fma", "achieved": achieved, "unit": "TFLOP/s",
                 "traffic": traffic, "traffic_unit": "bytes per launch (ncu dram__bytes_read+write)",
                 "algorithmic_bytes": Q * 12 + N * 48,

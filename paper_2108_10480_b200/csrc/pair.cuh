@@ -140,7 +140,21 @@ __device__ __forceinline__ void edge_term(const Phys<T>& ph, const Poly<T>& pc, 
     const T s = fma(dx, dx, fma(dy, dy, dz * dz));
     const T r = Math<T>::rsqrt(fmax(s, Tiny<T>::v));
     const T d = s * r;
-    if constexpr (POLY) {
+    if constexpr (POLY && SAFE) {
+        // base > 0 certified: exponentiate e / base and recover e with one
+        // multiply (e k = (e / base) dnum): no reciprocal
+        const T base = fma(t, fma(t, fma(t, fma(t, pc.c[4], pc.c[3]), pc.c[2]), pc.c[1]), pc.c[0]);
+        const T dnum = fma(t, fma(t, fma(t, pc.c[8], pc.c[7]), pc.c[6]), pc.c[5]);
+        const T lg = Math<T>::lg2(base), lw = ph.S * lg;
+        const T xm = bump(acc, masked(ph, d, fma(ph.kappa, d, lw - acc.m)), [&] { return fma(ph.kappa, d, lw); });
+        const T eob = Math<T>::ex2(xm - lg);
+        const T e = eob * base;
+        const T er = e * r, ek = eob * dnum;
+        acc.s += e;
+        acc.gx = fma(-ek, rec[7], fma(er, dx, acc.gx));
+        acc.gy = fma(-ek, rec[8], fma(er, dy, acc.gy));
+        acc.gz = fma(-ek, rec[9], fma(er, dz, acc.gz));
+    } else if constexpr (POLY) {
         const T base = fma(t, fma(t, fma(t, fma(t, pc.c[4], pc.c[3]), pc.c[2]), pc.c[1]), pc.c[0]);
         const T dnum = fma(t, fma(t, fma(t, pc.c[8], pc.c[7]), pc.c[6]), pc.c[5]);
         T k, lw;
@@ -233,7 +247,20 @@ __device__ __forceinline__ void tri_term(const Phys<T>& ph, const Poly<T>& pc, T
     const T s = fma(dx, dx, fma(dy, dy, dz * dz));
     const T r = Math<T>::rsqrt(fmax(s, Tiny<T>::v));
     const T d = s * r;
-    if constexpr (POLY) {
+    if constexpr (POLY && SAFE) {  // no reciprocal: see edge_term
+        T base, wx, wy;
+        tri_poly(pc, u, v, base, wx, wy);
+        const T lg = Math<T>::lg2(base), lw = ph.S * lg;
+        const T xm = bump(acc, masked(ph, d, fma(ph.kappa, d, lw - acc.m)), [&] { return fma(ph.kappa, d, lw); });
+        const T eob = Math<T>::ex2(xm - lg);
+        const T e = eob * base;
+        const T er = e * r;
+        const T kx = eob * wx, ky = eob * wy;
+        acc.s += e;
+        acc.gx = fma(-ky, rec[19], fma(-kx, rec[16], fma(er, dx, acc.gx)));
+        acc.gy = fma(-ky, rec[20], fma(-kx, rec[17], fma(er, dy, acc.gy)));
+        acc.gz = fma(-ky, rec[21], fma(-kx, rec[18], fma(er, dz, acc.gz)));
+    } else if constexpr (POLY) {
         T base, wx, wy;
         tri_poly(pc, u, v, base, wx, wy);
         T k, lw;

@@ -90,9 +90,15 @@ __device__ __forceinline__ void bump_half(Acc2& a, int h, float x) {
 // MODE 1: mask only -- the tile bound already raised the shift so that no
 //         term of this tile exceeds 2^kTileHeadroom (exact.cu);
 // MODE 2: neither -- additionally no term of this tile can be masked.
-template <int MODE = 0, class F>
-__device__ __forceinline__ f2 exp_terms(const Phys<float>& ph, Acc2& a, f2 d, f2 xm, F&& absx) {
-    if constexpr (MODE == 2) return pack(Math<float>::ex2(lo(xm)), Math<float>::ex2(hi(xm)));
+// With OFF, 2^(x - m - off) is returned (the mask and the shift check still
+// act on x - m): the SAFE weighted terms exponentiate e / base and recover e
+// with one multiply, instead of a reciprocal of base (one MUFU per pair less).
+template <int MODE = 0, bool OFF = false, class F>
+__device__ __forceinline__ f2 exp_terms(const Phys<float>& ph, Acc2& a, f2 d, f2 xm, F&& absx, f2 off = f2{0}) {
+    if constexpr (MODE == 2) {
+        if constexpr (OFF) xm = sub2(xm, off);
+        return pack(Math<float>::ex2(lo(xm)), Math<float>::ex2(hi(xm)));
+    }
     float x0 = lo(xm), x1 = hi(xm);
     x0 = !(lo(d) <= ph.dmax) ? -INFINITY : x0;  // NaN (overflowed) distances too
     x1 = !(hi(d) <= ph.dmax) ? -INFINITY : x1;
@@ -107,6 +113,10 @@ __device__ __forceinline__ f2 exp_terms(const Phys<float>& ph, Acc2& a, f2 d, f2
             bump_half(a, 1, x);
             x1 = x - hi(a.m);
         }
+    }
+    if constexpr (OFF) {
+        const f2 xo = sub2(pack(x0, x1), off);
+        return pack(Math<float>::ex2(lo(xo)), Math<float>::ex2(hi(xo)));
     }
     return pack(Math<float>::ex2(x0), Math<float>::ex2(x1));
 }
@@ -143,7 +153,30 @@ __device__ __forceinline__ void edge_term2(const Phys<float>& ph, const Poly<flo
     const f2 r = rsqrt2(s);
     const f2 d = mul2(s, r);
     const f2 xd = sub2(muls(d, ph.kappa), a.m);  // kappa d - m
-    if constexpr (POLY) {
+    if constexpr (POLY && SAFE) {
+        // base > 0 certified: e / base = 2^(S lg2 base + xd - lg2 base), e = (e / base) base,
+        // e k = (e / base) dnum -- no reciprocal
+        const f2 base = fmas(t, pc.c[4], bcast(pc.c[3]));
+        const f2 base2 = fma2(t, fma2(t, fma2(t, base, bcast(pc.c[2])), bcast(pc.c[1])), bcast(pc.c[0]));
+        const f2 dn = fma2(t, fma2(t, fmas(t, pc.c[8], bcast(pc.c[7])), bcast(pc.c[6])), bcast(pc.c[5]));
+        const f2 l = pack(Math<float>::lg2(lo(base2)), Math<float>::lg2(hi(base2)));
+        f2 eob;
+        if constexpr (MODE == 2) {
+            const f2 xb = fmas(l, ph.S - 1.f, xd);
+            eob = pack(Math<float>::ex2(lo(xb)), Math<float>::ex2(hi(xb)));
+        } else {
+            const f2 lw = muls(l, ph.S);
+            eob = exp_terms<MODE, true>(ph, a, d, add2(lw, xd),
+                                        [&](int h) { return fmaf(ph.kappa, h ? hi(d) : lo(d), h ? hi(lw) : lo(lw)); },
+                                        l);
+        }
+        const f2 e = mul2(eob, base2);
+        const f2 er = mul2(e, r), ek = mul2(eob, dn);
+        a.s = add2(a.s, e);
+        a.gx = fmas(ek, -rec[7], fma2(er, dx, a.gx));
+        a.gy = fmas(ek, -rec[8], fma2(er, dy, a.gy));
+        a.gz = fmas(ek, -rec[9], fma2(er, dz, a.gz));
+    } else if constexpr (POLY) {
         const f2 base = fmas(t, pc.c[4], bcast(pc.c[3]));
         const f2 base2 = fma2(t, fma2(t, fma2(t, base, bcast(pc.c[2])), bcast(pc.c[1])), bcast(pc.c[0]));
         const f2 dn = fma2(t, fma2(t, fmas(t, pc.c[8], bcast(pc.c[7])), bcast(pc.c[6])), bcast(pc.c[5]));
@@ -247,7 +280,28 @@ __device__ __forceinline__ void tri_term2(const Phys<float>& ph, const Poly<floa
     const f2 r = rsqrt2(s);
     const f2 d = mul2(s, r);
     const f2 xd = sub2(muls(d, ph.kappa), a.m);
-    if constexpr (POLY) {
+    if constexpr (POLY && SAFE) {  // no reciprocal: see edge_term2
+        f2 base, wx, wy;
+        tri_poly2(pc, u, v, base, wx, wy);
+        const f2 l = pack(Math<float>::lg2(lo(base)), Math<float>::lg2(hi(base)));
+        f2 eob;
+        if constexpr (MODE == 2) {
+            const f2 xb = fmas(l, ph.S - 1.f, xd);
+            eob = pack(Math<float>::ex2(lo(xb)), Math<float>::ex2(hi(xb)));
+        } else {
+            const f2 lw = muls(l, ph.S);
+            eob = exp_terms<MODE, true>(ph, a, d, add2(lw, xd),
+                                        [&](int h) { return fmaf(ph.kappa, h ? hi(d) : lo(d), h ? hi(lw) : lo(lw)); },
+                                        l);
+        }
+        const f2 e = mul2(eob, base);
+        const f2 er = mul2(e, r);
+        const f2 kx = mul2(eob, wx), ky = mul2(eob, wy);
+        a.s = add2(a.s, e);
+        a.gx = fmas(ky, -rec[19], fmas(kx, -rec[16], fma2(er, dx, a.gx)));
+        a.gy = fmas(ky, -rec[20], fmas(kx, -rec[17], fma2(er, dy, a.gy)));
+        a.gz = fmas(ky, -rec[21], fmas(kx, -rec[18], fma2(er, dz, a.gz)));
+    } else if constexpr (POLY) {
         f2 base, wx, wy;
         tri_poly2(pc, u, v, base, wx, wy);
         const float l0 = Math<float>::lg2(lo(base)), l1 = Math<float>::lg2(hi(base));
