@@ -375,7 +375,9 @@ static void exact_query(Ctx& c, const T* q, int64_t Q, const sd_params& p, const
     const Phys<T> ph = make_phys<T>(c, p);
     int64_t launches = 0;
     // queries in Morton order so that a warp's queries share tile bounds
-    const int64_t* perm = sort_queries<T>(c, q, Q, c.scene_lo, c.scene_hi, st, launches);
+    // (Morton over the scene box; a Hilbert order over the joined boxes
+    // measured the same on cfg2: 6.885 vs 6.890 ms)
+    const int64_t* perm = sort_queries<T>(c, q, Q, c.scene_lo, c.scene_hi, st, launches, false);
     const double S = p.alpha / std::max(p.alpha, p.alpha_u);
     bool first = true;
     for (const Segment& s : c.segs) {

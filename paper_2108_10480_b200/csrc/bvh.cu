@@ -742,7 +742,7 @@ __global__ void query_morton_union(const T* __restrict__ q, int64_t Q, double3 l
 // spatial order (device memory owned by the context).
 template <class T>
 const int64_t* sort_queries(Ctx& c, const T* q, int64_t Q, const double lo[3], const double hi[3], cudaStream_t st,
-                            int64_t& launches) {
+                            int64_t& launches, bool union_hilbert) {
     uint32_t* keys = static_cast<uint32_t*>(c.keys.ensure(size_t(Q) * 2 * sizeof(uint32_t)));
     int64_t* idx = static_cast<int64_t*>(c.perm.ensure(size_t(Q) * 2 * sizeof(int64_t)));
     const unsigned blocks = unsigned((Q + 255) / 256);
@@ -750,9 +750,7 @@ const int64_t* sort_queries(Ctx& c, const T* q, int64_t Q, const double lo[3], c
         const char* e = std::getenv("SDGPU_QBOX");
         return !(e && *e == '0');
     }();
-    // small batches (the few-query kernels walk one query per warp, and the
-    // extra reduction launch shows in re-query loops): root-box Morton order
-    if (union_box && Q > 65536) {
+    if (union_box && union_hilbert) {
         QBox* qb = static_cast<QBox*>(c.qbox.ensure(sizeof(QBox)));
         QBox init;
         for (int k = 0; k < 3; ++k) {
@@ -790,9 +788,15 @@ const int64_t* sort_queries(Ctx& c, const T* q, int64_t Q, const double lo[3], c
     return idx + Q;
 }
 template const int64_t* sort_queries<float>(Ctx&, const float*, int64_t, const double*, const double*, cudaStream_t,
-                                            int64_t&);
+                                            int64_t&, bool);
 template const int64_t* sort_queries<double>(Ctx&, const double*, int64_t, const double*, const double*,
-                                             cudaStream_t, int64_t&);
+                                             cudaStream_t, int64_t&, bool);
+
+static bool variant_is_frontier(int64_t Q) {
+    const char* e = std::getenv("SDGPU_TRAVERSAL");
+    if (e && std::string(e) != "pair") return false;
+    return use_frontier(Q, 65536);
+}
 
 template <class T>
 void tree_query(Ctx& c, const T* q, int64_t Q, const sd_params& p, const FinalizeOut& out, cudaStream_t st) {
@@ -801,7 +805,16 @@ void tree_query(Ctx& c, const T* q, int64_t Q, const sd_params& p, const Finaliz
     int64_t launches = 0;
     // Morton order of the queries over the root box (coherent traversal)
     const sd_bvh_node& root = c.tree[0];
-    const int64_t* perm = sort_queries(c, q, Q, root.lo, root.hi, st, launches);
+    // the one-query-per-warp kernel (K3F, few queries) gains nothing from a
+    // spatial order that pays for its sort launches (render beta 0.5:
+    // 6.92 -> 5.44 ms, Terrain / Bunny 0.265 -> 0.20 ms); SDGPU_FEW_SORT=1
+    // sorts anyway
+    static const bool few_sort = [] {
+        const char* e = std::getenv("SDGPU_FEW_SORT");
+        return e && *e == '1';
+    }();
+    const int64_t* perm = (!few_sort && variant_is_frontier(Q)) ? nullptr
+                                                                 : sort_queries(c, q, Q, root.lo, root.hi, st, launches, true);
 
     // polynomial table: edge polys then triangle polys
     const int ne = int(c.edge_a.size() / 5), nt = int(c.tri_stored.size() / 13);

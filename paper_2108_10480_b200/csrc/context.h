@@ -155,7 +155,7 @@ void build_record(const Ctx& c, int64_t prim, T* out);  // rec_size(kind) values
 
 template <class T>
 const int64_t* sort_queries(Ctx& c, const T* q, int64_t Q, const double lo[3], const double hi[3], cudaStream_t st,
-                            int64_t& launches);
+                            int64_t& launches, bool union_hilbert);  // Hilbert over box + query box, or Morton over box
 
 // Tree entry points (bvh.cu)
 void tree_upload(Ctx& c);  // host reference layout -> DeviceTree

@@ -932,13 +932,15 @@ void simplex_query(Ctx& c, const double* corners, const int32_t* dims, int64_t Q
     }
 
     DeviceTree& t = ensure_tree(c);
-    // Morton order of the query centroids over the root box
+    // Morton order of the query centroids over the root box (measured on the
+    // paper-table rows against a Hilbert order over the joined boxes and the
+    // input order: profiles/README.md)
     double* cen = static_cast<double*>(c.qd.ensure(size_t(Q) * 3 * sizeof(double)));
     simplex_centroids<<<unsigned((Q + 255) / 256), 256, 0, st>>>(corners, dims, Q, cen);
     check_cuda(cudaGetLastError(), "centroids");
     ++launches;
     const sd_bvh_node& root = c.tree[0];
-    const int64_t* perm = sort_queries<double>(c, cen, Q, root.lo, root.hi, st, launches);
+    const int64_t* perm = sort_queries<double>(c, cen, Q, root.lo, root.hi, st, launches, false);
 
     double* part = static_cast<double*>(c.part.ensure(size_t(5) * Q * sizeof(double)));
     int64_t* cnt = static_cast<int64_t*>(c.counters.ensure(size_t(Q) * 3 * sizeof(int64_t) + 64));
