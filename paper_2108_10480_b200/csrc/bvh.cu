@@ -874,7 +874,8 @@ void tree_query(Ctx& c, const T* q, int64_t Q, const sd_params& p, const Finaliz
         // 6.3 / 7.3 ms; the full dense 4.19M batch: K3 29.7 ms)
         if (!(use_frontier(Q, 65536) &&
               launch_frontier<T, PointVisit<T>>(c, c.dtree, a, out.hash != nullptr, st, launches, 32)))
-            nsplits = launch_pair_traversal<T, PointVisit<T>>(c, c.dtree, a, out.hash != nullptr, st, launches);
+            nsplits = launch_pair_traversal<T, PointVisit<T>>(c, c.dtree, a, out.hash != nullptr, st, launches, 1,
+                                                                 true);
     } else {
         const size_t smem = poly_bytes<T>(npoly) +
                             (variant == 0 ? size_t(a.stack_depth) * kTravThreads * sizeof(int32_t)

@@ -59,9 +59,15 @@ struct TraverseArgs {
     const double* qgeom;
     const int32_t* qdim;
     const double* leafgeom;
+    // deferred sparse entries (pair_kernel DEFER): the end of each node's
+    // pre-order subtree, the popcount threshold and the per-warp capacity
+    const int32_t* esc = nullptr;
+    int defer_t = 0, defer_cap = 0;
 };
 
 constexpr int kTravThreads = 128;
+constexpr int kDeferDefault = 0;  // pair_kernel DEFER threshold (SDGPU_DEFER); off: see profiles/README.md
+constexpr int kDeferCap = 64;     // deferred entries per warp (SDGPU_DEFER_CAP)
 
 // shared-memory bytes of the polynomial table, padded so the stacks after it
 // stay 16-byte aligned
@@ -108,8 +114,18 @@ __device__ __forceinline__ void far_term(const Phys<T>& ph, T lw, T d, T r, T dx
 // tests one node for it (point queries: bvh.cu; simplex queries:
 // simplex.cu) and returns "descend"; far_test<HASH>(...) is the
 // admissibility test alone (emitting the far-field term only when asked).
-template <class T, class VIS, bool HASH, int SPLIT>
-__global__ void __launch_bounds__(kTravThreads) pair_kernel(const __grid_constant__ TraverseArgs<T> a) {
+//
+// DEFER (unsplit point queries): an entry whose lane mask has at most
+// a.defer_t lanes -- the deep, query-specific tails of the walk, where a
+// packet step would run with most lanes idle -- is not walked by the packet
+// but appended to a per-warp list (while it has room). Once the packet walk
+// is over, every lane walks the subtrees of the listed entries that carry
+// its bit on its own, stackless in pre-order (descend: id + 1; far field or
+// leaf: a.esc[id], the end of id's subtree), all lanes at once. Per lane
+// the visited node set is still exactly collect_contributions'; only the
+// order of the terms changes.
+template <class T, class VIS, bool HASH, int SPLIT, bool DEFER>
+__device__ __forceinline__ void pair_walk(const TraverseArgs<T>& a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Poly<T>* polys = reinterpret_cast<Poly<T>*>(smem_raw);
     int4* stacks = reinterpret_cast<int4*>(smem_raw + poly_bytes<T>(a.npoly));
@@ -119,6 +135,8 @@ __global__ void __launch_bounds__(kTravThreads) pair_kernel(const __grid_constan
 
     const unsigned lane = threadIdx.x & 31u;
     int4* st = stacks + (threadIdx.x >> 5) * a.stack_depth;
+    int2* dlist = reinterpret_cast<int2*>(stacks + (kTravThreads / 32) * a.stack_depth) + (threadIdx.x >> 5) * a.defer_cap;
+    int nd = 0;  // deferred entries (warp-uniform)
     // packet (32 sorted queries) and, when split, the slot
     const int64_t gwarp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int64_t packet = SPLIT ? gwarp / a.nslots : gwarp;
@@ -180,7 +198,10 @@ __global__ void __launch_bounds__(kTravThreads) pair_kernel(const __grid_constan
         memcpy(&llink, &bl.v[7], sizeof(int32_t));
         memcpy(&rlink, &br.v[7], sizeof(int32_t));
         if (DL) {
-            if (DR) {
+            if (DEFER && DR && __popc(DR) <= a.defer_t && nd < a.defer_cap) {
+                if (lane == 0) dlist[nd] = make_int2(rid, int(DR));
+                ++nd;
+            } else if (DR) {
                 if (lane == 0) st[sp] = make_int4(rid, rlink, int(DR), depth + 1);
                 __syncwarp();
                 ++sp;
@@ -204,6 +225,47 @@ __global__ void __launch_bounds__(kTravThreads) pair_kernel(const __grid_constan
         } else {
             mask = 0u;
         }
+        if constexpr (DEFER) {
+            while (mask && __popc(mask) <= a.defer_t && nd < a.defer_cap) {
+                if (lane == 0) dlist[nd] = make_int2(cur, int(mask));
+                ++nd;
+                if (sp > 0) {
+                    --sp;
+                    const int4 e = st[sp];
+                    cur = e.x;
+                    cur_link = e.y;
+                    mask = unsigned(e.z);
+                    depth = e.w;
+                } else {
+                    mask = 0u;
+                }
+            }
+        }
+    }
+    if constexpr (DEFER) {
+        if (nd > 0) {  // per-lane stackless walks of the deferred subtrees
+            __syncwarp();
+            int j = 0;
+            int32_t n = 0, end = 0;
+            auto next = [&]() {
+                while (j < nd) {
+                    const int2 e = dlist[j++];
+                    if ((unsigned(e.y) >> lane) & 1u) {
+                        n = e.x + 1;
+                        end = a.esc[e.x];
+                        return true;
+                    }
+                }
+                return false;
+            };
+            bool act = valid && next();
+            while (act) {
+                const NodeT<T> b = a.box[n];
+                const bool d = qv.template visit<HASH>(a, polys, b, n, a.lgcount[n], acc, nleaf, nfar, h, nre);
+                n = d ? n + 1 : a.esc[n];
+                if (n == end) act = next();
+            }
+        }
     }
     if (!valid) return;
     Tot tot;
@@ -224,6 +286,18 @@ __global__ void __launch_bounds__(kTravThreads) pair_kernel(const __grid_constan
         if (HASH) a.hash[i] = h;
     }
     if (nre) atomicAdd(a.rechecks, nre);
+}
+
+template <class T, class VIS, bool HASH, int SPLIT>
+__global__ void __launch_bounds__(kTravThreads) pair_kernel(const __grid_constant__ TraverseArgs<T> a) {
+    pair_walk<T, VIS, HASH, SPLIT, false>(a);
+}
+// the deferring walk holds the packet state and the per-lane walk state:
+// pinned to the packet kernel's register budget (fp32 64, fp64 124)
+template <class T, class VIS, bool HASH>
+__global__ void __launch_bounds__(kTravThreads, sizeof(T) == 4 ? 8 : 4)
+    pair_kernel_defer(const __grid_constant__ TraverseArgs<T> a) {
+    pair_walk<T, VIS, HASH, 0, true>(a);
 }
 
 // K3F (few queries, node-parallel): a group of G lanes per query (32 / G
@@ -372,9 +446,9 @@ inline bool use_frontier(int64_t Q, int64_t limit) {
 // splitting. `weight` raises the warp target for expensive node tests.
 template <class T, class VIS>
 int launch_pair_traversal(Ctx& c, DeviceTree& t, TraverseArgs<T>& a, bool hash, cudaStream_t st, int64_t& launches,
-                          int weight = 1) {
+                          int weight = 1, bool allow_defer = false) {
     const int64_t Q = a.Q;
-    const size_t smem = poly_bytes<T>(a.npoly) + size_t(a.stack_depth) * (kTravThreads / 32) * sizeof(int4);
+    size_t smem = poly_bytes<T>(a.npoly) + size_t(a.stack_depth) * (kTravThreads / 32) * sizeof(int4);
     const int64_t npackets = (Q + 31) / 32;
     // SDGPU_SPLIT = 0 disables, = k forces depth k (A/B runs and tests)
     const char* se = std::getenv("SDGPU_SPLIT");
@@ -404,8 +478,20 @@ int launch_pair_traversal(Ctx& c, DeviceTree& t, TraverseArgs<T>& a, bool hash, 
         nsplits = a.nslots;
         a.part = static_cast<double*>(c.part.ensure(size_t(nsplits) * 5 * Q * sizeof(double)));
     }
+    // deferred sparse entries (unsplit point walks): SDGPU_DEFER = popcount
+    // threshold (0 = off), SDGPU_DEFER_CAP = entries per warp
+    const char* de = std::getenv("SDGPU_DEFER");
+    const char* dc = std::getenv("SDGPU_DEFER_CAP");
+    const int defer_t = de && *de ? std::max(0, std::min(32, std::atoi(de))) : kDeferDefault;
+    const int defer_cap = dc && *dc ? std::max(1, std::min(1024, std::atoi(dc))) : kDeferCap;
+    const bool defer = allow_defer && k == 0 && defer_t > 0 && t.has_esc;
+    a.esc = defer ? t.esc.as<int32_t>() : nullptr;
+    a.defer_t = defer ? defer_t : 0;
+    a.defer_cap = defer ? defer_cap : 0;
+    if (defer) smem += size_t(defer_cap) * (kTravThreads / 32) * sizeof(int2);
     auto kern = k > 0 ? (hash ? pair_kernel<T, VIS, true, 1> : pair_kernel<T, VIS, false, 1>)
-                      : (hash ? pair_kernel<T, VIS, true, 0> : pair_kernel<T, VIS, false, 0>);
+                      : defer ? (hash ? pair_kernel_defer<T, VIS, true> : pair_kernel_defer<T, VIS, false>)
+                              : (hash ? pair_kernel<T, VIS, true, 0> : pair_kernel<T, VIS, false, 0>);
     check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)), "smem attr");
     const int64_t warps = npackets * a.nslots;
     kern<<<unsigned((warps * 32 + kTravThreads - 1) / kTravThreads), kTravThreads, smem, st>>>(a);

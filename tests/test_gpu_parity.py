@@ -139,17 +139,26 @@ def test_random_scene_tree_decisions(sd, oracle, prec, seed):
 
 
 @pytest.mark.parametrize("prec", [0, 1])
-@pytest.mark.parametrize("split", ["0", "1", "3", "6", "", "frontier", "frontier32"])
+@pytest.mark.parametrize("split", ["0", "1", "3", "6", "", "frontier", "frontier32",
+                                   "defer0", "defer1", "defer32", "defer32cap1", "defer12cap3"])
 def test_split_traversal_decisions(sd, oracle, prec, split, monkeypatch):
     """The few-query traversal modes visit exactly the oracle's nodes:
     the slot split (one warp per (packet, depth-k slot) after re-testing the
     slot's ancestors, merged in fp64) at every depth k, none ("0"), the
     automatic choice (""), and the node-parallel frontier kernel: counters
-    and decision hash identical."""
+    and decision hash identical. "deferT[capC]": the unsplit packet walk
+    handing entries of at most T lanes to per-lane stackless walks (a list
+    of C entries per warp; a full list keeps the rest in the packet)."""
     O = oracle
     if split.startswith("frontier"):
         monkeypatch.setenv("SDGPU_FRONTIER", "1")
         monkeypatch.setenv("SDGPU_FRONTIER_G", split[8:] or "4")
+    elif split.startswith("defer"):
+        t, _, cap = split[5:].partition("cap")
+        monkeypatch.setenv("SDGPU_FRONTIER", "0")
+        monkeypatch.setenv("SDGPU_SPLIT", "0")
+        monkeypatch.setenv("SDGPU_DEFER", t)
+        monkeypatch.setenv("SDGPU_DEFER_CAP", cap or "64")
     else:
         monkeypatch.setenv("SDGPU_FRONTIER", "0")
         monkeypatch.setenv("SDGPU_SPLIT", split)
@@ -257,7 +266,7 @@ def test_config_exact_parity(sd, oracle, cfg, prec, alphas, nq):
         assert_close(got, ref, prec, alpha, f"cfg{cfg} alpha {alpha}")
 
 
-@pytest.mark.parametrize("builder,kernel", [("median", "K3F"), ("lbvh", "K3F"), ("lbvh", "K3")])
+@pytest.mark.parametrize("builder,kernel", [("median", "K3F"), ("lbvh", "K3F"), ("lbvh", "K3"), ("median", "K3D")])
 def test_config4_tree_parity_subset(sd, oracle, builder, kernel, monkeypatch):
     """cfg4 (icosphere(9), 5.2M triangles, beta 0.5, alpha 200) on a query
     subset (both halves of the query distribution): decisions identical to
@@ -267,6 +276,8 @@ def test_config4_tree_parity_subset(sd, oracle, builder, kernel, monkeypatch):
     this batch size, K3 the one the full-size bench runs)."""
     O = oracle
     monkeypatch.setenv("SDGPU_FRONTIER", "1" if kernel == "K3F" else "0")
+    if kernel == "K3D":  # the unsplit packet walk with deferred per-lane tails (the full-size default)
+        monkeypatch.setenv("SDGPU_SPLIT", "0")
     m, q = _cfg(O, 4, 512, 0)
     w = O.Weights.build(m)
     if builder == "median":
