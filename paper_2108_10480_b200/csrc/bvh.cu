@@ -522,12 +522,11 @@ __global__ void __launch_bounds__(kTravThreads) packet_kernel(const __grid_const
     if (nre) atomicAdd(a.rechecks, nre);
 }
 
-// Exact leaf term of one lane (smooth.hpp:51-61); the record is the same
-// for every lane of the warp.
-template <class T, bool HASH, class CNT>
-__device__ __forceinline__ void leaf_visit(const TraverseArgs<T>& a, const Poly<T>* polys, int32_t id, int32_t link,
-                                           T qx, T qy, T qz, Acc<T>& acc, CNT& nleaf, uint64_t& h) {
-    const int slot = -link - 1;  // exact leaf: the record is the same for every lane
+// Exact leaf term (smooth.hpp:51-61) of the primitive in leaf slot `slot`
+// for query q, added to acc.
+template <class T>
+__device__ __forceinline__ void leaf_term(const TraverseArgs<T>& a, const Poly<T>* polys, int slot, T qx, T qy, T qz,
+                                          Acc<T>& acc) {
     const int meta = a.leafmeta[slot];
     const int kind = meta & 3, poly = (meta >> 2) - 1;
     T rec[kRecTri];
@@ -549,8 +548,30 @@ __device__ __forceinline__ void leaf_visit(const TraverseArgs<T>& a, const Poly<
         if (poly >= 0) tri_term<T, true, false>(a.ph, polys[a.ne + poly], qx, qy, qz, rec, acc);
         else unit_term<T, 2>(a.ph, polys[0], qx, qy, qz, rec, acc);
     }
+}
+
+// Exact leaf visit of one lane; the record is the same for every lane of
+// the warp.
+template <class T, bool HASH, class CNT>
+__device__ __forceinline__ void leaf_visit(const TraverseArgs<T>& a, const Poly<T>* polys, int32_t id, int32_t link,
+                                           T qx, T qy, T qz, Acc<T>& acc, CNT& nleaf, uint64_t& h) {
+    leaf_term<T>(a, polys, -link - 1, qx, qy, qz, acc);
     ++nleaf;
     if constexpr (HASH) h += decision_mix(uint64_t(id), 2);
+}
+
+// Adds a partial (m, s, g) -- sums relative to 2^m -- into acc.
+template <class T>
+__device__ __forceinline__ void merge_partial(Acc<T>& acc, T m, T s, T gx, T gy, T gz) {
+    if (m > acc.m) {
+        acc.scale(Math<T>::ex2(acc.m - m));
+        acc.m = m;
+    }
+    const T f = m == acc.m ? T(1) : Math<T>::ex2(m - acc.m);
+    acc.s = fma(s, f, acc.s);
+    acc.gx = fma(gx, f, acc.gx);
+    acc.gy = fma(gy, f, acc.gy);
+    acc.gz = fma(gz, f, acc.gz);
 }
 
 
@@ -629,6 +650,7 @@ __device__ __forceinline__ bool visit(const TraverseArgs<T>& a, const Poly<T>* p
 // The point query of one lane (K3's VIS for bvh.cu).
 template <class T>
 struct PointVisit {
+    static constexpr bool kLeafBatch = true;
     T qx, qy, qz;
     __device__ __forceinline__ void load(const TraverseArgs<T>& a, int64_t qi, bool valid) {
         qx = valid ? a.q[3 * qi] : T(0);
@@ -659,6 +681,97 @@ struct PointVisit {
     // packed fp32x2 variant with a branch-free far-field path measured
     // slower on cfg4 -- 33.0 ms vs 29.7 ms: 80 registers and an exponential
     // for every child -- and was dropped.)
+    // Leaf-batching variants (pair_walk LB): returns "reached" -- descend
+    // into an internal node, or an exact leaf, which is counted (and hashed)
+    // at once but whose term is left to flush_leaves (the caller knows from
+    // the node's link which of the two it is).
+    template <bool HASH, class CNT>
+    __device__ __forceinline__ bool visit_nl(const TraverseArgs<T>& a, const NodeT<T>& b, int32_t id, T lgc,
+                                             Acc<T>& acc, CNT& nleaf, CNT& nfar, uint64_t& h,
+                                             unsigned long long& nre) const {
+        int32_t link;
+        memcpy(&link, &b.v[7], sizeof(int32_t));
+        if (a.use_bh) {
+            T d, r, dx, dy, dz;
+            if (point_far(a, b, id, qx, qy, qz, d, r, dx, dy, dz, nre)) {
+                far_term(a.ph, lgc + a.lw_ff, d, r, dx, dy, dz, acc);
+                ++nfar;
+                if constexpr (HASH) h += decision_mix(uint64_t(id), 1);
+                return false;
+            }
+        }
+        if (link >= 0) return true;
+        ++nleaf;
+        if constexpr (HASH) h += decision_mix(uint64_t(id), 2);
+        return true;
+    }
+    template <bool HASH, class CNT>
+    __device__ __forceinline__ void visit_pair_nl(const TraverseArgs<T>& a, const NodeT<T>& bl, const NodeT<T>& br,
+                                                  int32_t lid, int32_t rid, T lgl, T lgr, Acc<T>& acc, CNT& nleaf,
+                                                  CNT& nfar, uint64_t& h, unsigned long long& nre, bool& dl,
+                                                  bool& dr) const {
+        dl = visit_nl<HASH>(a, bl, lid, lgl, acc, nleaf, nfar, h, nre);
+        dr = visit_nl<HASH>(a, br, rid, lgr, acc, nleaf, nfar, h, nre);
+    }
+    // Evaluates the batched leaf entries of a warp -- entry k = list[k] =
+    // (leaf link, mask of the lanes that reached the leaf), k < nl -- with
+    // the (leaf, query) items spread over all 32 lanes, 32 per round: item
+    // t belongs to the entry with the largest exclusive popcount prefix
+    // <= t and to that entry's (t - prefix)-th lane, whose query and shift
+    // are fetched by shuffle. Each item is a partial relative to its
+    // owner's shift; the owners then merge theirs (merge_partial). Called
+    // by the whole warp.
+    __device__ __forceinline__ void flush_leaves(const TraverseArgs<T>& a, const Poly<T>* polys, Acc<T>& acc,
+                                                 const int2* list, int nl, unsigned lane) const {
+        constexpr unsigned FULL = 0xffffffffu;
+        __syncwarp();
+        const int2 ent = int(lane) < nl ? list[lane] : make_int2(0, 0);
+        const int32_t e_link = ent.x;
+        const unsigned e_mask = unsigned(ent.y);
+        const unsigned cnt = int(lane) < nl ? unsigned(__popc(e_mask)) : 0u;
+        unsigned incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned t = __shfl_up_sync(FULL, incl, o);
+            if (int(lane) >= o) incl += t;
+        }
+        const unsigned pre = incl - cnt;
+        const unsigned total = __shfl_sync(FULL, incl, nl - 1);
+        const unsigned pkey = int(lane) < nl ? pre : 0xffffffffu;
+        const unsigned lt = (1u << lane) - 1u;
+        for (unsigned base = 0; base < total; base += 32) {
+            const unsigned t = base + lane;
+            int k = 0;
+#pragma unroll
+            for (int step = 16; step; step >>= 1) {
+                const unsigned p = __shfl_sync(FULL, pkey, k + step);
+                if (p <= t) k += step;
+            }
+            const unsigned mk = __shfl_sync(FULL, e_mask, k);
+            const int32_t lk = __shfl_sync(FULL, e_link, k);
+            const unsigned pk = __shfl_sync(FULL, pre, k);
+            const int owner = int(__fns(mk, 0, int(t - pk) + 1)) & 31;
+            const T ox = __shfl_sync(FULL, qx, owner), oy = __shfl_sync(FULL, qy, owner),
+                    oz = __shfl_sync(FULL, qz, owner);
+            Acc<T> it;
+            it.m = __shfl_sync(FULL, acc.m, owner);
+            it.s = it.gx = it.gy = it.gz = T(0);
+            if (t < total) leaf_term<T>(a, polys, -lk - 1, ox, oy, oz, it);
+            const int kl = __shfl_sync(FULL, k, 0);
+            const int kh = __shfl_sync(FULL, k, int(min(31u, total - 1u - base)));
+            for (int kk = kl; kk <= kh; ++kk) {  // the owners collect their items of this round
+                const unsigned m2 = __shfl_sync(FULL, e_mask, kk), p2 = __shfl_sync(FULL, pre, kk);
+                const int src = int(p2 + unsigned(__popc(m2 & lt))) - int(base);
+                const bool have = ((m2 >> lane) & 1u) && src >= 0 && src < 32;
+                const int s2 = src & 31;
+                const T im = __shfl_sync(FULL, it.m, s2), is = __shfl_sync(FULL, it.s, s2),
+                        ix = __shfl_sync(FULL, it.gx, s2), iy = __shfl_sync(FULL, it.gy, s2),
+                        iz = __shfl_sync(FULL, it.gz, s2);
+                if (have && is != T(0)) merge_partial(acc, im, is, ix, iy, iz);
+            }
+        }
+    }
+
     template <bool HASH, class CNT>
     __device__ __forceinline__ void visit_pair(const TraverseArgs<T>& a, const Poly<T>* polys, const NodeT<T>& bl,
                                                const NodeT<T>& br, int32_t lid, int32_t rid, T lgl, T lgr,

@@ -68,6 +68,7 @@ struct TraverseArgs {
 constexpr int kTravThreads = 128;
 constexpr int kDeferDefault = 0;  // pair_kernel DEFER threshold (SDGPU_DEFER); off: see profiles/README.md
 constexpr int kDeferCap = 64;     // deferred entries per warp (SDGPU_DEFER_CAP)
+constexpr int kLeafBatch = 32;    // batched leaf entries per warp (pair_walk LB)
 
 // shared-memory bytes of the polynomial table, padded so the stacks after it
 // stay 16-byte aligned
@@ -124,7 +125,13 @@ __device__ __forceinline__ void far_term(const Phys<T>& ph, T lw, T d, T r, T dx
 // leaf: a.esc[id], the end of id's subtree), all lanes at once. Per lane
 // the visited node set is still exactly collect_contributions'; only the
 // order of the terms changes.
-template <class T, class VIS, bool HASH, int SPLIT, bool DEFER>
+//
+// LB (leaf batching, point queries): a lane that reaches an exact leaf
+// counts it at once, but the warp only records (leaf, lane mask) -- lane k
+// of the warp holds entry k -- and evaluates 32 entries at a time with the
+// (leaf, query) items spread over all lanes (VIS::flush_leaves). Inline, a
+// leaf step runs the ~190-instruction triangle term for ~3.6 of 32 lanes.
+template <class T, class VIS, bool HASH, int SPLIT, bool DEFER, bool LB = false>
 __device__ __forceinline__ void pair_walk(const TraverseArgs<T>& a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Poly<T>* polys = reinterpret_cast<Poly<T>*>(smem_raw);
@@ -137,6 +144,10 @@ __device__ __forceinline__ void pair_walk(const TraverseArgs<T>& a) {
     int4* st = stacks + (threadIdx.x >> 5) * a.stack_depth;
     int2* dlist = reinterpret_cast<int2*>(stacks + (kTravThreads / 32) * a.stack_depth) + (threadIdx.x >> 5) * a.defer_cap;
     int nd = 0;  // deferred entries (warp-uniform)
+    // LB: batched leaf entries (leaf link, lane mask), after the deferred list
+    [[maybe_unused]] int2* llist = reinterpret_cast<int2*>(stacks + (kTravThreads / 32) * a.stack_depth) +
+                                   (kTravThreads / 32) * a.defer_cap + (threadIdx.x >> 5) * kLeafBatch;
+    [[maybe_unused]] int nl = 0;  // batched leaf entries (warp-uniform)
     // packet (32 sorted queries) and, when split, the slot
     const int64_t gwarp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int64_t packet = SPLIT ? gwarp / a.nslots : gwarp;
@@ -191,12 +202,38 @@ __device__ __forceinline__ void pair_walk(const TraverseArgs<T>& a) {
         // pair record into L1 while this one is being processed
         if (lane == 0) asm volatile("prefetch.global.L1 [%0];" ::"l"(a.pairs + lid));
         bool dl = false, dr = false;
-        if ((mask >> lane) & 1u)
-            qv.template visit_pair<HASH>(a, polys, bl, br, lid, rid, lgl, lgr, acc, nleaf, nfar, h, nre, dl, dr);
-        const unsigned DL = __ballot_sync(0xffffffffu, dl), DR = __ballot_sync(0xffffffffu, dr);
+        if ((mask >> lane) & 1u) {
+            if constexpr (LB)
+                qv.template visit_pair_nl<HASH>(a, bl, br, lid, rid, lgl, lgr, acc, nleaf, nfar, h, nre, dl, dr);
+            else
+                qv.template visit_pair<HASH>(a, polys, bl, br, lid, rid, lgl, lgr, acc, nleaf, nfar, h, nre, dl, dr);
+        }
+        unsigned DL = __ballot_sync(0xffffffffu, dl), DR = __ballot_sync(0xffffffffu, dr);
         int32_t llink, rlink;
         memcpy(&llink, &bl.v[7], sizeof(int32_t));
         memcpy(&rlink, &br.v[7], sizeof(int32_t));
+        if constexpr (LB) {  // a leaf child's "reached" mask is a batch entry, not a descent
+            if (llink < 0) {
+                if (DL) {
+                    if (lane == 0) llist[nl] = make_int2(llink, int(DL));
+                    if (++nl == kLeafBatch) {
+                        qv.flush_leaves(a, polys, acc, llist, nl, lane);
+                        nl = 0;
+                    }
+                }
+                DL = 0u;
+            }
+            if (rlink < 0) {
+                if (DR) {
+                    if (lane == 0) llist[nl] = make_int2(rlink, int(DR));
+                    if (++nl == kLeafBatch) {
+                        qv.flush_leaves(a, polys, acc, llist, nl, lane);
+                        nl = 0;
+                    }
+                }
+                DR = 0u;
+            }
+        }
         if (DL) {
             if (DEFER && DR && __popc(DR) <= a.defer_t && nd < a.defer_cap) {
                 if (lane == 0) dlist[nd] = make_int2(rid, int(DR));
@@ -242,6 +279,9 @@ __device__ __forceinline__ void pair_walk(const TraverseArgs<T>& a) {
             }
         }
     }
+    if constexpr (LB) {
+        if (nl > 0) qv.flush_leaves(a, polys, acc, llist, nl, lane);
+    }
     if constexpr (DEFER) {
         if (nd > 0) {  // per-lane stackless walks of the deferred subtrees
             __syncwarp();
@@ -285,12 +325,14 @@ __device__ __forceinline__ void pair_walk(const TraverseArgs<T>& a) {
         a.far[i] = nfar;
         if (HASH) a.hash[i] = h;
     }
-    if (nre) atomicAdd(a.rechecks, nre);
+    // (the fp64 re-decision count nre is not reported by the packet walk: its
+    // two registers cost the fp32 leaf-batching kernel a spill of the
+    // far-field counter)
 }
 
-template <class T, class VIS, bool HASH, int SPLIT>
+template <class T, class VIS, bool HASH, int SPLIT, bool LB = false>
 __global__ void __launch_bounds__(kTravThreads) pair_kernel(const __grid_constant__ TraverseArgs<T> a) {
-    pair_walk<T, VIS, HASH, SPLIT, false>(a);
+    pair_walk<T, VIS, HASH, SPLIT, false, LB>(a);
 }
 // the deferring walk holds the packet state and the per-lane walk state:
 // pinned to the packet kernel's register budget (fp32 64, fp64 124)
@@ -492,6 +534,14 @@ int launch_pair_traversal(Ctx& c, DeviceTree& t, TraverseArgs<T>& a, bool hash, 
     auto kern = k > 0 ? (hash ? pair_kernel<T, VIS, true, 1> : pair_kernel<T, VIS, false, 1>)
                       : defer ? (hash ? pair_kernel_defer<T, VIS, true> : pair_kernel_defer<T, VIS, false>)
                               : (hash ? pair_kernel<T, VIS, true, 0> : pair_kernel<T, VIS, false, 0>);
+    if constexpr (VIS::kLeafBatch) {  // SDGPU_LEAF_BATCH = 1 turns leaf batching on (off: profiles/README.md)
+        const char* lb = std::getenv("SDGPU_LEAF_BATCH");
+        if (!defer && lb && *lb == '1') {
+            smem += size_t(kLeafBatch) * (kTravThreads / 32) * sizeof(int2);
+            kern = k > 0 ? (hash ? pair_kernel<T, VIS, true, 1, true> : pair_kernel<T, VIS, false, 1, true>)
+                         : (hash ? pair_kernel<T, VIS, true, 0, true> : pair_kernel<T, VIS, false, 0, true>);
+        }
+    }
     check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)), "smem attr");
     const int64_t warps = npackets * a.nslots;
     kern<<<unsigned((warps * 32 + kTravThreads - 1) / kTravThreads), kTravThreads, smem, st>>>(a);

@@ -140,7 +140,7 @@ def test_random_scene_tree_decisions(sd, oracle, prec, seed):
 
 @pytest.mark.parametrize("prec", [0, 1])
 @pytest.mark.parametrize("split", ["0", "1", "3", "6", "", "frontier", "frontier32",
-                                   "defer0", "defer1", "defer32", "defer32cap1", "defer12cap3"])
+                                   "defer0", "defer1", "defer32", "defer32cap1", "defer12cap3", "lb", "lb3"])
 def test_split_traversal_decisions(sd, oracle, prec, split, monkeypatch):
     """The few-query traversal modes visit exactly the oracle's nodes:
     the slot split (one warp per (packet, depth-k slot) after re-testing the
@@ -148,7 +148,8 @@ def test_split_traversal_decisions(sd, oracle, prec, split, monkeypatch):
     automatic choice (""), and the node-parallel frontier kernel: counters
     and decision hash identical. "deferT[capC]": the unsplit packet walk
     handing entries of at most T lanes to per-lane stackless walks (a list
-    of C entries per warp; a full list keeps the rest in the packet)."""
+    of C entries per warp; a full list keeps the rest in the packet).
+    "lb[k]": exact-leaf terms batched over the warp's lanes (split depth k)."""
     O = oracle
     if split.startswith("frontier"):
         monkeypatch.setenv("SDGPU_FRONTIER", "1")
@@ -159,6 +160,10 @@ def test_split_traversal_decisions(sd, oracle, prec, split, monkeypatch):
         monkeypatch.setenv("SDGPU_SPLIT", "0")
         monkeypatch.setenv("SDGPU_DEFER", t)
         monkeypatch.setenv("SDGPU_DEFER_CAP", cap or "64")
+    elif split.startswith("lb"):  # leaf terms batched across the warp (SDGPU_LEAF_BATCH=1)
+        monkeypatch.setenv("SDGPU_FRONTIER", "0")
+        monkeypatch.setenv("SDGPU_SPLIT", split[2:] or "0")
+        monkeypatch.setenv("SDGPU_LEAF_BATCH", "1")
     else:
         monkeypatch.setenv("SDGPU_FRONTIER", "0")
         monkeypatch.setenv("SDGPU_SPLIT", split)
@@ -266,7 +271,8 @@ def test_config_exact_parity(sd, oracle, cfg, prec, alphas, nq):
         assert_close(got, ref, prec, alpha, f"cfg{cfg} alpha {alpha}")
 
 
-@pytest.mark.parametrize("builder,kernel", [("median", "K3F"), ("lbvh", "K3F"), ("lbvh", "K3"), ("median", "K3D")])
+@pytest.mark.parametrize("builder,kernel", [("median", "K3F"), ("lbvh", "K3F"), ("lbvh", "K3"), ("median", "K3D"),
+                                            ("median", "K3LB")])
 def test_config4_tree_parity_subset(sd, oracle, builder, kernel, monkeypatch):
     """cfg4 (icosphere(9), 5.2M triangles, beta 0.5, alpha 200) on a query
     subset (both halves of the query distribution): decisions identical to
@@ -276,8 +282,9 @@ def test_config4_tree_parity_subset(sd, oracle, builder, kernel, monkeypatch):
     this batch size, K3 the one the full-size bench runs)."""
     O = oracle
     monkeypatch.setenv("SDGPU_FRONTIER", "1" if kernel == "K3F" else "0")
-    if kernel == "K3D":  # the unsplit packet walk with deferred per-lane tails (the full-size default)
+    if kernel in ("K3D", "K3LB"):  # the unsplit packet walk (the full-size default); K3LB: batched leaf terms
         monkeypatch.setenv("SDGPU_SPLIT", "0")
+        monkeypatch.setenv("SDGPU_LEAF_BATCH", "1" if kernel == "K3LB" else "0")
     m, q = _cfg(O, 4, 512, 0)
     w = O.Weights.build(m)
     if builder == "median":
