@@ -594,9 +594,9 @@ __device__ __forceinline__ bool point_far(const TraverseArgs<T>& a, const NodeT<
         // squared: diam^2 against beta^2 s with a 2e-5 relative band (the
         // reciprocal square root only for far-field nodes)
         const T dd = b.v[3] * b.v[3], rhs2 = (a.ph.beta * a.ph.beta) * s;
-        if (s == T(0) && a.exact_boxes) far = false;
-        else if (dd < rhs2 - T(2e-5) * rhs2) far = true;
-        else if (dd > rhs2 + T(2e-5) * rhs2) far = false;
+        const T gap = dd - rhs2;  // exact sign outside the band (|gap| >> its rounding)
+        if (fabs(gap) > T(2e-5) * rhs2) far = gap < T(0);
+        else if (s == T(0) && a.exact_boxes) far = false;
         else {
             far = decide64(b, a.diam64[id], double(qx), double(qy), double(qz), a.beta64);
             ++nre;

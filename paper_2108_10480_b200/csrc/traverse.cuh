@@ -141,6 +141,7 @@ __device__ __forceinline__ void pair_walk(const TraverseArgs<T>& a) {
     __syncthreads();
 
     const unsigned lane = threadIdx.x & 31u;
+    const unsigned lanebit = 1u << lane;
     int4* st = stacks + (threadIdx.x >> 5) * a.stack_depth;
     int2* dlist = reinterpret_cast<int2*>(stacks + (kTravThreads / 32) * a.stack_depth) + (threadIdx.x >> 5) * a.defer_cap;
     int nd = 0;  // deferred entries (warp-uniform)
@@ -200,9 +201,9 @@ __device__ __forceinline__ void pair_walk(const TraverseArgs<T>& a) {
         const T lgl = pr.lgc[0], lgr = pr.lgc[1];
         // the most likely next step descends into the left child: pull its
         // pair record into L1 while this one is being processed
-        if (lane == 0) asm volatile("prefetch.global.L1 [%0];" ::"l"(a.pairs + lid));
+        if (lane == 0) asm volatile("prefetch.global.L1 [%0];" ::"l"(&pr + 1));  // = a.pairs + lid
         bool dl = false, dr = false;
-        if ((mask >> lane) & 1u) {
+        if (mask & lanebit) {
             if constexpr (LB)
                 qv.template visit_pair_nl<HASH>(a, bl, br, lid, rid, lgl, lgr, acc, nleaf, nfar, h, nre, dl, dr);
             else
