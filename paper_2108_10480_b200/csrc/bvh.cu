@@ -633,7 +633,7 @@ __device__ __forceinline__ bool visit(const TraverseArgs<T>& a, const Poly<T>* p
                                       CNT& nfar, uint64_t& h, unsigned long long& nre) {
     int32_t link;
     memcpy(&link, &b.v[7], sizeof(int32_t));
-    if (a.use_bh) {
+    {  // no Barnes-Hut (beta <= 0): tree_query passes beta = 0, which is never admissible
         T d, r, dx, dy, dz;
         if (point_far(a, b, id, qx, qy, qz, d, r, dx, dy, dz, nre)) {
             far_term(a.ph, lgc + a.lw_ff, d, r, dx, dy, dz, acc);
@@ -691,7 +691,7 @@ struct PointVisit {
                                              unsigned long long& nre) const {
         int32_t link;
         memcpy(&link, &b.v[7], sizeof(int32_t));
-        if (a.use_bh) {
+        {  // beta = 0 when there is no Barnes-Hut (see visit)
             T d, r, dx, dy, dz;
             if (point_far(a, b, id, qx, qy, qz, d, r, dx, dy, dz, nre)) {
                 far_term(a.ph, lgc + a.lw_ff, d, r, dx, dy, dz, acc);
@@ -965,6 +965,10 @@ void tree_query(Ctx& c, const T* q, int64_t Q, const sd_params& p, const Finaliz
     a.stack_depth = t.depth + 1;
     a.beta64 = p.beta;
     a.ph = make_phys<T>(c, p);
+    if (!a.use_bh) {  // smooth.hpp:106: no far field; beta = 0 makes every box test fail
+        a.beta64 = 0.0;
+        a.ph.beta = T(0);
+    }
     a.part = part;
     a.leaves = cnt;
     a.far = cnt + Q;
