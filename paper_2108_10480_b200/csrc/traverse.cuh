@@ -97,7 +97,7 @@ __device__ __forceinline__ void far_term(const Phys<T>& ph, T lw, T d, T r, T dx
 // -- per-lane decisions are exactly collect_contributions'
 // (smooth.hpp:101-131). The warp continues into the left child if any lane
 // descends there (pushing the right child with its lane mask), else into
-// the right child, else pops. Stack entries (node, its link, mask, depth)
+// the right child, else pops. Stack entries (node, its link, mask)
 // live in shared memory, one stack per warp.
 //
 // SPLIT = 1 (few queries): one warp per (query packet, slot), the slots
@@ -168,7 +168,6 @@ __device__ __forceinline__ void pair_walk(const TraverseArgs<T>& a) {
     uint64_t h = 0;
     unsigned long long nre = 0;
     int32_t cur = 0, cur_link;
-    int depth = 0;
     if constexpr (SPLIT) {
         const int2 sm = a.split_meta[slot];  // (node, path length | first-slot bits << 8)
         cur = sm.x;
@@ -184,7 +183,6 @@ __device__ __forceinline__ void pair_walk(const TraverseArgs<T>& a) {
                                                  nre);
             mask &= ~__ballot_sync(0xffffffffu, far);
         }
-        depth = len;
     }
     memcpy(&cur_link, &a.box[cur].v[7], sizeof(int32_t));
     if (mask) {  // the start node (root, or the slot) is popped alone
@@ -196,12 +194,12 @@ __device__ __forceinline__ void pair_walk(const TraverseArgs<T>& a) {
     int sp = 0;
     while (mask) {
         const int32_t lid = cur + 1, rid = cur_link;
-        const PairT<T>& pr = a.pairs[cur];  // warp-uniform: broadcast loads
+        const PairT<T>& pr = a.pairs[uint32_t(cur)];  // warp-uniform: broadcast loads
         const NodeT<T> bl = pr.l, br = pr.r;
         const T lgl = pr.lgc[0], lgr = pr.lgc[1];
         // the most likely next step descends into the left child: pull its
         // pair record into L1 while this one is being processed
-        if (lane == 0) asm volatile("prefetch.global.L1 [%0];" ::"l"(&pr + 1));  // = a.pairs + lid
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(&pr + 1));  // = a.pairs + lid (one request per warp)
         bool dl = false, dr = false;
         if (mask & lanebit) {
             if constexpr (LB)
@@ -240,26 +238,23 @@ __device__ __forceinline__ void pair_walk(const TraverseArgs<T>& a) {
                 if (lane == 0) dlist[nd] = make_int2(rid, int(DR));
                 ++nd;
             } else if (DR) {
-                if (lane == 0) st[sp] = make_int4(rid, rlink, int(DR), depth + 1);
+                if (lane == 0) st[sp] = make_int4(rid, rlink, int(DR), 0);
                 __syncwarp();
                 ++sp;
             }
             cur = lid;
             cur_link = llink;
             mask = DL;
-            ++depth;
         } else if (DR) {
             cur = rid;
             cur_link = rlink;
             mask = DR;
-            ++depth;
         } else if (sp > 0) {
             --sp;
             const int4 e = st[sp];
             cur = e.x;
             cur_link = e.y;
             mask = unsigned(e.z);
-            depth = e.w;
         } else {
             mask = 0u;
         }
@@ -273,8 +268,7 @@ __device__ __forceinline__ void pair_walk(const TraverseArgs<T>& a) {
                     cur = e.x;
                     cur_link = e.y;
                     mask = unsigned(e.z);
-                    depth = e.w;
-                } else {
+                        } else {
                     mask = 0u;
                 }
             }
