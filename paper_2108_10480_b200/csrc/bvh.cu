@@ -601,8 +601,8 @@ __device__ __forceinline__ bool point_far(const TraverseArgs<T>& a, const NodeT<
             far = decide64(b, a.diam64[id], double(qx), double(qy), double(qz), a.beta64);
             ++nre;
         }
-        if (far) {
-            r = s > T(0) ? Math<T>::rsqrt(s) : T(0);
+        if (far) {  // s = 0 only for an fp64-confirmed box that the fp32 box contains; then dx = dy = dz = 0
+            r = Math<T>::rsqrt(fmax(s, T(1e-30)));
             d = s * r;
         }
     } else {
