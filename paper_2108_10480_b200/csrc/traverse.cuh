@@ -131,6 +131,15 @@ __device__ __forceinline__ void far_term(const Phys<T>& ph, T lw, T d, T r, T dx
 // of the warp holds entry k -- and evaluates 32 entries at a time with the
 // (leaf, query) items spread over all lanes (VIS::flush_leaves). Inline, a
 // leaf step runs the ~190-instruction triangle term for ~3.6 of 32 lanes.
+__device__ __forceinline__ void st_shared_int4(uint32_t addr, int x, int y, int z) {
+    asm volatile("st.shared.v4.s32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(x), "r"(y), "r"(z), "r"(0) : "memory");
+}
+__device__ __forceinline__ int4 ld_shared_int4(uint32_t addr) {
+    int4 v;
+    asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr) : "memory");
+    return v;
+}
+
 template <class T, class VIS, bool HASH, int SPLIT, bool DEFER, bool LB = false>
 __device__ __forceinline__ void pair_walk(const TraverseArgs<T>& a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -191,7 +200,9 @@ __device__ __forceinline__ void pair_walk(const TraverseArgs<T>& a) {
                        qv.template visit<HASH>(a, polys, b0, cur, a.lgcount[cur], acc, nleaf, nfar, h, nre);
         mask = __ballot_sync(0xffffffffu, d);
     }
-    int sp = 0;
+    // stack top as a shared-window byte address (one add per push / pop)
+    const uint32_t st0 = smem_u32(st);
+    uint32_t top = st0;
     while (mask) {
         const int32_t lid = cur + 1, rid = cur_link;
         const PairT<T>& pr = a.pairs[uint32_t(cur)];  // warp-uniform: broadcast loads
@@ -238,9 +249,9 @@ __device__ __forceinline__ void pair_walk(const TraverseArgs<T>& a) {
                 if (lane == 0) dlist[nd] = make_int2(rid, int(DR));
                 ++nd;
             } else if (DR) {
-                if (lane == 0) st[sp] = make_int4(rid, rlink, int(DR), 0);
+                if (lane == 0) st_shared_int4(top, rid, rlink, int(DR));
                 __syncwarp();
-                ++sp;
+                top += 16;
             }
             cur = lid;
             cur_link = llink;
@@ -249,9 +260,9 @@ __device__ __forceinline__ void pair_walk(const TraverseArgs<T>& a) {
             cur = rid;
             cur_link = rlink;
             mask = DR;
-        } else if (sp > 0) {
-            --sp;
-            const int4 e = st[sp];
+        } else if (top != st0) {
+            top -= 16;
+            const int4 e = ld_shared_int4(top);
             cur = e.x;
             cur_link = e.y;
             mask = unsigned(e.z);
@@ -262,9 +273,9 @@ __device__ __forceinline__ void pair_walk(const TraverseArgs<T>& a) {
             while (mask && __popc(mask) <= a.defer_t && nd < a.defer_cap) {
                 if (lane == 0) dlist[nd] = make_int2(cur, int(mask));
                 ++nd;
-                if (sp > 0) {
-                    --sp;
-                    const int4 e = st[sp];
+                if (top != st0) {
+                    top -= 16;
+                    const int4 e = ld_shared_int4(top);
                     cur = e.x;
                     cur_link = e.y;
                     mask = unsigned(e.z);
