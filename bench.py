@@ -403,8 +403,8 @@ def measure_bvh(args, rank, world, local, eng_cls, dev, stream, flush, peaks):
     out["roofline"]["touched_frac_of_hbm_peak"] = out["roofline"]["touched_gbs"] / 6542.4
     # the issue-slot bound, from the committed ncu capture of this kernel (not
     # measured in this run): warp instructions per launch and issue-slot use
-    out["roofline"]["ncu_issue"] = {"issue_slots_busy": 0.761, "ipc": 3.03, "warp_instructions": 2.027e10,
-                                    "avg_active_lanes": 17.1, "source": "profiles/r1_pair_bvh_details.csv, "
+    out["roofline"]["ncu_issue"] = {"issue_slots_busy": 0.768, "ipc": 3.05, "warp_instructions": 2.009e10,
+                                    "avg_active_lanes": 17.0, "source": "profiles/r1_pair_bvh_details.csv, "
                                     "profiles/r1_k3_source_breakdown.md (fp32, median tree)"}
     if rank == 0 and world == 1 and not args.no_cpu:
         out["cpu_baseline"] = bvh_cpu_sample(eng, v, w, q, P)
