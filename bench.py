@@ -1,26 +1,43 @@
 #!/usr/bin/env python
-"""Benchmark of the B200 smooth-distance engine (exact path, BASELINE cfg2).
+"""Benchmark of the B200 smooth-distance engine.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-A step is one exact pass of d_hat + grad over the workload's queries
-(smooth_min_dist_flat for every query, smooth.hpp:189-198): BASELINE.json
-configs[1], the helix polyline (20,000 edges) against 262,144 queries per
-GPU, alpha = 100, fp32. Multi-GPU runs shard queries (each rank its own
-block of the same query distribution) with the geometry replicated: no
-collective on the data path, "scaling": "weak". One JSON line on rank 0.
+Headline (`metric` "exact pair-evals/s (value+grad)"): BASELINE.json
+configs[2], the jittered torus (262,144 triangles) against its 1,048,576
+queries, alpha = 100, fp32: a step is one exact pass of d_hat + grad over the
+batch (smooth_min_dist_flat for every query, smooth.hpp:189-198). The same
+JSON line carries, as extra keys, cfg3 at alpha 10 and 1000, cfg2 (helix,
+20,000 edges x 262,144 queries) in fp32 and fp64, and the BVH far-field
+metric on configs[3] (cfg4: icosphere(9), 5,242,880 triangles, 4,194,304
+queries, alpha 200, beta 0.5), plus a `parity` object: the timed outputs of
+every leg checked against the CPU oracle on config-scale samples, and cfg4
+Barnes-Hut against exact on 65,536 queries.
+
+Multi-GPU: one process per GPU. Without torchrun, --gpus N > 1 re-launches
+this script under torch.distributed.run with N ranks; the world size must
+equal --gpus. The BASELINE batch is fixed and split across the ranks
+("scaling": "strong"): exact legs by equal contiguous query blocks (uniform
+queries, uniform per-pair work), the BVH leg by Hilbert-contiguous blocks of
+equal estimated traversal cost (sharding.balanced_ranges). No collective on
+the data path (geometry replicated, queries sharded); the BVH leg also
+reports the weak-scaling variant (every rank a full cfg4 batch) at N > 1.
 
 --impl reference times the reference CPU evaluator of the same path on this
-host's cores: the reference cannot be built here (Eigen3/GTest/CLI11 are
-absent), so its line-faithful fp64 restatement in oracle/ stands in
-("kind": "port"). Only that leg and the cpu_baseline leg execute oracle/.
+host's cores: the reference cannot be installed as a package here (a CMake
+header library, no Eigen), so its line-faithful fp64 restatement in oracle/
+stands in ("kind": "port"). Only that leg, the cpu_baseline legs and the
+parity checker execute oracle/.
 """
 from __future__ import annotations
 
 import argparse
 import ctypes
+import glob
+import hashlib
 import json
 import os
+import socket
 import subprocess
 import sys
 import threading
@@ -31,15 +48,16 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-FLOPS_PER_EDGE_PAIR = 62      # SURVEY 8(d) canonical count, S != 1
-FLOPS_PER_TRI_PAIR = 192
+# SURVEY 8(d) canonical algorithmic flops per pair evaluation (S != 1)
+FLOPS_PER_PAIR = {0: 20, 1: 62, 2: 192}
 FLOPS_BOX_TEST, FLOPS_FAR_TERM = 10, 12
 BYTES_NODE, BYTES_LEAF = 32, 100  # fp32 traversal node record; leaf record (96 B) + meta
-MUFU_PER_EDGE_PAIR = 3            # rsqrt, lg2, ex2 (no reciprocal on certified-positive weights)
-QUERIES_PER_GPU = 262144
-ALPHA = 100.0
+MUFU_PER_PAIR = {0: 2, 1: 3, 2: 3}  # rsqrt, lg2, ex2 (no reciprocal on certified-positive weights)
+SMS = 148
+TOL = {"f32": (1e-5, 1e-4), "f64": (1e-10, 1e-9)}  # north_star: relative d_hat / gradient
 
 
+# ------------------------------------------------------------- processes
 def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -47,24 +65,74 @@ def dist_env():
     return rank, world, local
 
 
-# Tree builder (BENCH_TREE=median|lbvh|auto, default auto): SD_BVH_AUTO
-# builds the reference's median-split tree (build_bvh, bvh.hpp:34-91, on the
-# device by median.cu) and the GPU LBVH and keeps the smaller surface-area
-# cost -- the median tree on single surfaces (cfg4 28.4 ms vs 29.7 ms:
-# 1152 vs 1335 popped nodes per query; Terrain 8.2 vs 15.6 ms), the LBVH on
-# clustered scenes whose Morton splits follow the gaps between objects (cfg5
-# 35 vs 62 ms, City Street 22 vs 38 ms).
-def tree_method(sd):
-    t = os.environ.get("BENCH_TREE") or "auto"
-    return {"median": sd.SD_BVH_MEDIAN, "lbvh": sd.SD_BVH_LBVH}.get(t, sd.SD_BVH_AUTO)
+def free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
 
 
-def tree_name():
-    t = os.environ.get("BENCH_TREE") or "auto"
-    return {"median": "reference median-split tree built on the GPU", "lbvh": "GPU LBVH"}.get(
-        t, "GPU tree (median split or LBVH, smaller surface-area cost)")
+def maybe_spawn(args) -> bool:
+    """--gpus N > 1 outside torchrun: run this script under
+    torch.distributed.run with N ranks (127.0.0.1 rendezvous) and return
+    True (the caller exits with its status)."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return False
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+    rc = subprocess.call(cmd)
+    sys.exit(rc)
 
 
+class Run:
+    """Process group plumbing: barrier, max / sum over ranks, all-gather of
+    small objects (NCCL on GPUs, gloo in --stub runs)."""
+
+    def __init__(self, rank, world, local, backend):
+        self.rank, self.world, self.local = rank, world, local
+        self.backend = backend
+        import torch
+        self.torch = torch
+        if world > 1:
+            import torch.distributed as dist
+            if backend == "nccl":
+                dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+            else:
+                dist.init_process_group("gloo")
+            self.dist = dist
+        self.dev = torch.device("cuda", local) if backend == "nccl" else torch.device("cpu")
+
+    def barrier(self):
+        if self.world > 1:
+            self.dist.barrier()
+
+    def reduce(self, xs, op="max"):
+        xs = [float(x) for x in (xs if isinstance(xs, (list, tuple)) else [xs])]
+        if self.world > 1:
+            t = self.torch.tensor(xs, dtype=self.torch.float64, device=self.dev)
+            self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX if op == "max" else self.dist.ReduceOp.SUM)
+            xs = [float(v) for v in t.cpu().tolist()]
+        return xs
+
+    def gather(self, obj):
+        if self.world == 1:
+            return [obj]
+        out = [None] * self.world
+        self.dist.all_gather_object(out, obj)
+        return out
+
+    def close(self):
+        if self.world > 1:
+            self.dist.barrier()
+            self.dist.destroy_process_group()
+
+
+def strong_blocks(n: int, world: int):
+    """Equal contiguous [lo, hi) blocks of a fixed batch (exact legs)."""
+    from paper_2108_10480_b200 import sharding
+    return sharding.query_ranges(n, world)
+
+
+# ------------------------------------------------------------ clocks
 class ClockSampler:
     """SM clocks and clock-event (throttle) reasons sampled DURING the timed
     region: NVML polled every 2 ms from a thread (nvidia-smi -lms 200 as the
@@ -75,6 +143,7 @@ class ClockSampler:
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
     # nvmlClocksEventReason* bits
     BITS = {"sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40}
+    ALL = []  # every sample of the run (the top-level "clocks")
 
     def __init__(self, gpu: int):
         self.gpu = gpu
@@ -139,17 +208,21 @@ class ClockSampler:
                 self.proc.wait(timeout=5)
             except subprocess.TimeoutExpired:
                 self.proc.kill()
+        ClockSampler.ALL.extend(self.lines)
 
-    def summary(self):
-        sm = [x[0] for x in self.lines]
-        smax = [x[1] for x in self.lines]
-        reasons = set(n for x in self.lines for n in x[2])
+    @staticmethod
+    def summarize(lines, source="nvml"):
+        sm = [x[0] for x in lines]
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
-        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(smax), "reasons": sorted(reasons),
-                "samples": len(sm), "source": "nvml" if self.nvml is not None else "nvidia-smi"}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(x[1] for x in lines),
+                "reasons": sorted(set(n for x in lines for n in x[2])), "samples": len(sm), "source": source}
+
+    def summary(self):
+        return self.summarize(self.lines, "nvml" if self.nvml is not None else "nvidia-smi")
 
 
+# ---------------------------------------------------------------- peaks
 def measure_peaks(device: int = 0):
     L = ctypes.CDLL(os.path.join(ROOT, "paper_2108_10480_b200", "libsdpeaks.so"))
     L.sd_peaks_set_device.argtypes = [ctypes.c_int]
@@ -167,77 +240,564 @@ def measure_peaks(device: int = 0):
     return out
 
 
-def workload(block: int, cfg: int = 2, alpha: float | None = None, device: int = 0):
-    """cfg2 (headline) or cfg3 (triangles, --config 3): mesh, fp32-rounded
-    vertices and queries, and the WeightSet table."""
+def compute_peak(peaks, sm_mhz, fp64: bool):
+    """Roofline denominator: the largest of the in-run probes and the
+    nominal pipe rate at the sampled SM clock (148 SMs x 128 FP32 / 64 FP64
+    lanes x 2 flop per FMA)."""
+    clk = (sm_mhz or 1965.0) * 1e6
+    nominal = SMS * (64 if fp64 else 128) * 2 * clk / 1e12
+    cands = {"nominal_at_sampled_clock": nominal}
+    if peaks:
+        if fp64:
+            cands["dfma_probe"] = peaks["dfma_tflops"]
+        else:
+            cands["ffma_probe"] = peaks["ffma_tflops"]
+            if "ffma2_tflops" in peaks:
+                cands["ffma2_probe"] = peaks["ffma2_tflops"]
+    src = max(cands, key=cands.get)
+    return cands[src], src, cands
+
+
+def source_hash() -> str:
+    """Hash of the CUDA sources: ncu figures stamped with another hash are
+    stale and not reported."""
+    h = hashlib.sha256()
+    for p in sorted(glob.glob(os.path.join(ROOT, "paper_2108_10480_b200", "csrc", "*"))):
+        if p.endswith((".cu", ".cuh", ".h", ".cpp")):
+            with open(p, "rb") as f:
+                h.update(os.path.basename(p).encode() + f.read())
+    return h.hexdigest()[:16]
+
+
+def ncu_stamp(kernel_key: str):
+    """Per-launch ncu figures of `kernel_key` (profiles/ncu_stamps.json,
+    written by tools/ncu_stamp.py from a capture of the same sources), or
+    None when the capture is of different sources."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_stamps.json")) as f:
+            st = json.load(f)
+    except (OSError, ValueError):
+        return None
+    e = st.get(kernel_key)
+    if not e or e.get("src_sha") != source_hash():
+        return None
+    return e
+
+
+# ------------------------------------------------------------- timing
+def time_device(run, step, stream, flush, steps, warmup, eng=None):
+    """W >= 3 untimed steps, then exactly K steps between CUDA events on the
+    launching stream with an L2 flush (256 MiB write) before each; barrier
+    + synchronize on both sides; max over ranks. With `eng`, the engine's
+    own event pairs around its dominant launches are read as well."""
+    torch = run.torch
+    for _ in range(max(3, warmup)):
+        step()
+    torch.cuda.synchronize()
+    if eng is not None:
+        eng.kernel_times()
+        eng.set_kernel_timing(True)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    run.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(run.local) as clk:
+        for i in range(steps):
+            flush.zero_()
+            evs[i][0].record(stream)
+            step()
+            evs[i][1].record(stream)
+        torch.cuda.synchronize()
+    run.barrier()
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    kern = None
+    if eng is not None:
+        kern = eng.kernel_times()
+        eng.set_kernel_timing(False)
+    ms, kms = run.reduce([float(np.mean(step_ms)), float(np.mean(kern)) if kern is not None and len(kern) else 0.0])
+    return {"ms": ms, "step_ms": step_ms, "kernel_ms": kms if kern is not None else None,
+            "kernel_launch_groups": int(len(kern)) if kern is not None else 0, "clocks": clk.summary()}
+
+
+def time_e2e(run, call, steps):
+    """End to end through the public host API, wall clock per call (the call
+    is blocking: H2D + evaluation + D2H), max over ranks."""
+    torch = run.torch
+    call()
+    times = []
+    run.barrier()
+    for _ in range(steps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        call()
+        times.append(time.perf_counter() - t0)
+    return run.reduce(float(np.mean(times)))[0]
+
+
+# ------------------------------------------------------------- workloads
+def cfg3_workload():
+    """BASELINE configs[2]: torus 512 x 256 (262,144 triangles) with vertex
+    jitter, 1,048,576 queries uniform in the AABB expanded by 0.5; fp32
+    inputs (rounded before the GPU and the oracle see them)."""
     from paper_2108_10480_b200 import configs
-    if cfg == 1:
-        w, q = configs.cfg1()
-        q = np.random.default_rng([1002, block]).uniform(-2, 2, q.shape)
-        wt = configs.weights_without_triangles(w.simplices, w.kinds, len(w.vertices))
-        return w, w.vertices, q, wt  # fp64 config: no rounding
-    if cfg == 2:
-        w, q = configs.cfg2(QUERIES_PER_GPU, block=block)
-        wt = configs.weights_without_triangles(w.simplices, w.kinds, len(w.vertices))
-    else:
-        V, T = configs.torus()
-        rng = np.random.default_rng([3002, block])
-        lo, hi = V.min(0) - 0.5, V.max(0) + 0.5
-        q = rng.uniform(lo, hi, (1048576, 3))
-        w = configs.Workload("cfg3 torus 262,144 triangles, exact LSE", V, T, np.full(len(T), 2, np.uint8),
-                             alpha=alpha or 100.0)
-        import paper_2108_10480_b200 as sd
-        e = sd.Engine(device, sd.SD_FP32)
-        e.set_geometry(configs.quantize(V), T, w.kinds)
-        wt = e.build_weights()
-        e.close()
-    return w, configs.quantize(w.vertices), configs.quantize(q), wt
+    V, T = configs.torus()
+    rng = np.random.default_rng([3002, 0])
+    lo, hi = V.min(0) - 0.5, V.max(0) + 0.5
+    q = rng.uniform(lo, hi, (1048576, 3))
+    return configs.quantize(V), T, np.full(len(T), 2, np.uint8), configs.quantize(q)
 
 
-def cpu_sample(v, s, k, wt, q, threads, target_s=12.0):
-    """Times the oracle port on a bounded prefix of the queries, sized from a
-    pilot so that the sample takes about target_s seconds."""
+def cfg2_workload():
+    from paper_2108_10480_b200 import configs
+    w, q = configs.cfg2(262144, block=0)
+    wt = configs.weights_without_triangles(w.simplices, w.kinds, len(w.vertices))
+    return w, wt, q
+
+
+def oracle_objects(v, s, k, wt, nodes=None):
     import oracle as O
+    O.build()
     m = O.Mesh.from_arrays(v, s, k)
-    w = O.Weights.from_table(O.WeightTable(wt.A, wt.sup_wtilde, wt.edge_a, wt.tri_stored, wt.poly_index))
-    p = O.Params(alpha=ALPHA, alpha_u=600.0, beta=0.0)
-    pilot = max(threads * 2, 64)
+    ws = O.Weights.from_table(O.WeightTable(wt.A, wt.sup_wtilde, wt.edge_a, wt.tri_stored, wt.poly_index))
+    t = O.Tree.from_nodes(nodes) if nodes is not None else None
+    return O, m, ws, t
+
+
+# ------------------------------------------------------------- parity
+def parity_stats(got_d, got_g, ref_d, ref_g, alpha, dtype):
+    """Both tolerance forms of north_star's relative bound on the same pairs:
+    the survey's (error / max(1, |ref|)) and the strict relative one with a
+    1/alpha floor for d_hat (|d_hat| < 1/alpha is below the LSE's own
+    resolution) and a 1e-3 floor for the gradient norm. +inf must agree."""
+    td, tg = TOL[dtype]
+    got_d, ref_d = np.asarray(got_d, np.float64), np.asarray(ref_d, np.float64)
+    fr, fg = np.isfinite(ref_d), np.isfinite(got_d)
+    both = fr & fg
+    dd = np.abs(got_d - ref_d)[both]
+    rd = np.abs(ref_d[both])
+    out = {"n": int(len(ref_d)), "finite": int(both.sum()), "inf_mismatch": int((fr != fg).sum()),
+           "tol_d_hat": td, "tol_grad": tg}
+    if dd.size:
+        e1 = dd / np.maximum(1.0, rd)
+        e2 = dd / np.maximum(rd, 1.0 / alpha)
+        out.update({"d_hat_max_err_survey": float(e1.max()), "d_hat_max_err_strict": float(e2.max()),
+                    "d_hat_over_tol_strict": int((e2 > td).sum()), "d_hat_max_abs": float(dd.max())})
+    if got_g is not None and ref_g is not None and dd.size:
+        gd = np.linalg.norm(np.asarray(got_g)[both] - np.asarray(ref_g)[both], axis=1)
+        gn = np.linalg.norm(np.asarray(ref_g)[both], axis=1)
+        g1 = gd / np.maximum(1.0, gn)
+        g2 = gd / np.maximum(gn, 1e-3)
+        out.update({"grad_max_err_survey": float(g1.max()), "grad_max_err_strict": float(g2.max()),
+                    "grad_over_tol_strict": int((g2 > tg).sum())})
+    out["pass_survey"] = bool(out["inf_mismatch"] == 0 and out.get("d_hat_max_err_survey", 0.0) <= td
+                              and out.get("grad_max_err_survey", 0.0) <= tg)
+    out["pass_strict"] = bool(out["inf_mismatch"] == 0 and out.get("d_hat_over_tol_strict", 0) == 0
+                              and out.get("grad_over_tol_strict", 0) == 0)
+    return out
+
+
+# ------------------------------------------------------------ exact legs
+def exact_leg(run, eng, q, prec, N, kind, P, steps, warmup, flush, stream, peaks, e2e_steps=0, q_total=None,
+              label=""):
+    """Times one exact configuration on this rank's query block q (fp32 /
+    fp64 device buffer, inputs resident), optionally end to end through
+    sd_query_points with pinned host buffers. Returns the result dict and
+    this rank's (d_hat, grad) of the timed steps (host copies)."""
+    import paper_2108_10480_b200 as sd
+    torch = run.torch
+    fp64 = prec == sd.SD_FP64
+    Q = len(q)
+    q_total = q_total or Q * run.world
+    dev = run.dev
+    qd = torch.tensor(q, dtype=torch.float64 if fp64 else torch.float32, device=dev)
+    d_hat = torch.empty(Q, dtype=torch.float64, device=dev)
+    grad = torch.empty(Q, 3, dtype=torch.float64, device=dev)
+
+    def step():
+        eng.query_points_device(qd.data_ptr(), Q, P, sd.SD_EXACT, d_hat.data_ptr(), grad.data_ptr(),
+                                stream=stream.cuda_stream)
+
+    t = time_device(run, step, stream, flush, steps, warmup, eng)
+    launches = eng.last_launch_count()
+    pairs_rank = Q * N
+    out = {"value": q_total * N / (t["ms"] * 1e-3), "unit": "pair-evals/s", "ms_per_step": t["ms"],
+           "queries": q_total, "queries_per_gpu": Q, "primitives": N, "dtype": "f64" if fp64 else "f32",
+           "alpha": P.alpha, "gpu_launches": launches * steps, "clocks": t["clocks"]}
+    kms = t["kernel_ms"]
+    if kms:
+        achieved = FLOPS_PER_PAIR[kind] * pairs_rank / (kms * 1e-3) / 1e12
+        peak, src, cands = compute_peak(peaks, t["clocks"].get("sm_mhz"), fp64)
+        out["roofline"] = {
+            "bound": "fp64-fma" if fp64 else "fp32-fma", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+            "frac": achieved / peak, "peak_source": src, "peak_candidates": cands,
+            "kernel_ms": kms, "step_ms": t["ms"], "kernel_share_of_step": kms / t["ms"],
+            "algorithmic": f"{FLOPS_PER_PAIR[kind]} flop/pair x {pairs_rank} pairs per launch group (SURVEY 8d); "
+                           "kernel time = CUDA events on the launching stream around the exact segment launches "
+                           "(sd_set_kernel_timing), query sort and finalize excluded",
+            "kernel": f"exact_kernel<{'double' if fp64 else 'float'}, {['point', 'edge', 'triangle'][kind]}>"}
+        if peaks and not fp64:
+            out["roofline"]["mufu_frac"] = MUFU_PER_PAIR[kind] * pairs_rank / (kms * 1e-3) / 1e12 / peaks["mufu_tops"]
+    if e2e_steps:
+        qh = torch.tensor(q, dtype=torch.float64).pin_memory().numpy()
+        res = sd.SmoothResults(torch.empty(Q, dtype=torch.float64).pin_memory().numpy(),
+                               torch.empty(Q, 3, dtype=torch.float64).pin_memory().numpy())
+        te = time_e2e(run, lambda: eng.query_points(qh, P, sd.SD_EXACT, out=res), e2e_steps)
+        out["e2e"] = {"value": q_total * N / te, "unit": "pair-evals/s", "h2d_bytes_per_step": Q * 3 * 8,
+                      "d2h_bytes_per_step": Q * 4 * 8, "steps": e2e_steps,
+                      "api": "sd_query_points (pinned host fp64 queries in, d_hat + grad out)"}
+    return out, d_hat.cpu().numpy(), grad.cpu().numpy()
+
+
+def cpu_exact_sample(v, s, k, wt, q, alpha, threads, target_s):
+    """The oracle port on a bounded prefix of the queries, sized by a pilot
+    so the sample takes about target_s seconds."""
+    O, m, w, _ = oracle_objects(v, s, k, wt)
+    p = O.Params(alpha=alpha, alpha_u=600.0, beta=0.0)
+    pilot = max(threads * 2, 32)
     r = O.query(m, w, q[:pilot], p, threads=threads)
     n = int(min(len(q), max(pilot, pilot * target_s / max(r.seconds, 1e-3))))
     r = O.query(m, w, q[:n], p, threads=threads)
-    return n, r.seconds, r
+    return n, r
 
 
+def run_exact_headline(args, run, peaks, stream, flush, line):
+    """cfg3 (BASELINE configs[2]) alpha 100 = the headline; alpha 10 / 1000,
+    cfg2 fp32 / fp64 as extra keys; parity of every leg's timed outputs."""
+    import paper_2108_10480_b200 as sd
+    rank, world = run.rank, run.world
+    par = line.setdefault("parity", {})
+    # ---- cfg3 torus
+    v3, t3, k3, q3 = cfg3_workload()
+    eng = sd.Engine(run.local, sd.SD_FP32)
+    eng.set_geometry(v3, t3, k3)
+    wt3 = eng.build_weights()
+    lo, hi = strong_blocks(len(q3), world)[rank]
+    qb = q3[lo:hi]
+    N3 = len(k3)
+    P = sd.SmoothParams(alpha=100.0, alpha_u=600.0, beta=0.0)
+    head, d100, g100 = exact_leg(run, eng, qb, sd.SD_FP32, N3, 2, P, args.steps, args.warmup, flush, stream, peaks,
+                                 e2e_steps=max(3, min(args.steps, 10)), q_total=len(q3))
+    extra = {}
+    outs = {100.0: (d100, g100)}
+    for alpha in (10.0, 1000.0):
+        Pa = sd.SmoothParams(alpha=alpha, alpha_u=600.0, beta=0.0)
+        r, d, g = exact_leg(run, eng, qb, sd.SD_FP32, N3, 2, Pa, max(1, min(args.steps, 3)), 3, flush, stream, peaks,
+                            q_total=len(q3))
+        extra[f"exact_cfg3_alpha{alpha:g}"] = r
+        outs[alpha] = (d, g)
+    eng.close()
+    threads = None
+    if rank == 0 and not args.no_cpu:
+        import oracle as O
+        O.build()
+        threads = O.hardware_threads()
+        # parity: strided samples of the timed outputs (this rank's block)
+        _, m, w, _ = oracle_objects(v3, t3, k3, wt3)
+        for alpha, nq in ((100.0, 512), (10.0, 256), (1000.0, 256)):
+            idx = np.linspace(0, len(qb) - 1, nq).astype(np.int64)
+            ref = O.query(m, w, qb[idx], O.Params(alpha=alpha, alpha_u=600.0, beta=0.0), threads=threads)
+            d, g = outs[alpha]
+            par[f"cfg3_alpha{alpha:g}"] = parity_stats(d[idx], g[idx], ref.d_hat, ref.grad, alpha, "f32")
+            par[f"cfg3_alpha{alpha:g}"]["sample"] = f"{nq} evenly spaced timed queries of rank 0's block"
+        if world == 1:
+            n, r = cpu_exact_sample(v3, t3, k3, wt3, qb, 100.0, threads, 10.0)
+            line["cpu_baseline"] = {"value": n * N3 / r.seconds, "unit": "pair-evals/s", "cores": threads,
+                                    "kind": "port", "sample": f"first {n} of {len(qb)} cfg3 queries x {N3} "
+                                    f"triangles, alpha 100 ({r.seconds:.1f} s, fp64 oracle port)"}
+    line.update({"metric": "exact pair-evals/s (value+grad)", "value": head["value"], "unit": "pair-evals/s",
+                 "ms_per_step": head["ms_per_step"], "dtype": "f32",
+                 "config": {"workload": "cfg3: torus R=1 r=0.3, 512x256 grid (262,144 triangles), vertex jitter, "
+                                        "1,048,576 queries uniform in the AABB expanded by 0.5, exact LSE, alpha=100, "
+                                        "fp32 (BASELINE configs[2])",
+                            "queries": len(q3), "queries_per_gpu": len(qb), "primitives": N3,
+                            "l2": "flushed between timed steps (256 MiB write)",
+                            "parallelism": f"query-sharded x{world} (equal contiguous blocks of the fixed batch), "
+                                           "geometry replicated"},
+                 "roofline": head.get("roofline"), "e2e": head.get("e2e"), "gpu_launches": head["gpu_launches"],
+                 "clocks": head["clocks"]})
+    line.update(extra)
+    # ---- cfg2 helix (BASELINE configs[1]), fp32 and fp64
+    w2, wt2, q2 = cfg2_workload()
+    from paper_2108_10480_b200 import configs
+    v2, q2 = configs.quantize(w2.vertices), configs.quantize(q2)
+    lo, hi = strong_blocks(len(q2), world)[rank]
+    qb2 = q2[lo:hi]
+    N2 = len(w2.kinds)
+    P2 = sd.SmoothParams(alpha=100.0, alpha_u=600.0, beta=0.0)
+    res2 = {}
+    for prec, key in ((sd.SD_FP32, "exact_cfg2"), (sd.SD_FP64, "exact_cfg2_fp64")):
+        e = sd.Engine(run.local, prec)
+        e.set_geometry(v2, w2.simplices, w2.kinds)
+        e.set_weights(wt2.A, wt2.sup_wtilde, wt2.edge_a, wt2.tri_stored, wt2.poly_index)
+        r, d, g = exact_leg(run, e, qb2, prec, N2, 1, P2, args.steps, args.warmup, flush, stream, peaks,
+                            e2e_steps=3, q_total=len(q2))
+        r["workload"] = ("cfg2: helix polyline 20,000 edges x 262,144 queries, exact LSE, alpha=100 "
+                         "(BASELINE configs[1])")
+        line[key] = r
+        res2[prec] = (d, g)
+        e.close()
+    if rank == 0 and not args.no_cpu:
+        # the oracle port on a ~7 s prefix of the timed cfg2 queries: the cfg2
+        # cpu baseline at the reference's precision and the parity reference
+        n, r = cpu_exact_sample(v2, w2.simplices, w2.kinds, wt2, qb2, 100.0, threads, 7.0)
+        cpu2 = {"value": n * N2 / r.seconds, "unit": "pair-evals/s", "cores": threads, "kind": "port",
+                "sample": f"first {n} of {len(qb2)} cfg2 queries x {N2} edges ({r.seconds:.1f} s, fp64 oracle port)"}
+        for prec, key, dt in ((sd.SD_FP32, "exact_cfg2", "f32"), (sd.SD_FP64, "exact_cfg2_fp64", "f64")):
+            d, g = res2[prec]
+            par[key] = parity_stats(d[:n], g[:n], r.d_hat, r.grad, 100.0, dt)
+            par[key]["sample"] = f"first {n} timed queries of rank 0's block"
+            line[key]["cpu_baseline"] = cpu2
+            line[key]["vs_cpu_port"] = line[key]["value"] / cpu2["value"] if world == 1 else None
+            if "e2e" in line[key] and world == 1:
+                line[key]["e2e_vs_cpu_port"] = line[key]["e2e"]["value"] / cpu2["value"]
+
+
+# ------------------------------------------------------------- BVH leg
+def tree_method(sd):
+    """BENCH_TREE=median|lbvh|auto (default auto): SD_BVH_AUTO builds the
+    reference's median-split tree (build_bvh, bvh.hpp:34-91, on the device)
+    and the GPU LBVH and keeps the smaller surface-area cost."""
+    t = os.environ.get("BENCH_TREE") or "auto"
+    return {"median": sd.SD_BVH_MEDIAN, "lbvh": sd.SD_BVH_LBVH}.get(t, sd.SD_BVH_AUTO)
+
+
+def tree_name():
+    t = os.environ.get("BENCH_TREE") or "auto"
+    return {"median": "reference median-split tree built on the GPU", "lbvh": "GPU LBVH"}.get(
+        t, "GPU tree (median split or LBVH, smaller surface-area cost)")
+
+
+def measure_bvh(args, run, stream, flush, peaks, fp64=False):
+    """BASELINE configs[3] (cfg4): BVH far-field queries/s. The fixed
+    4,194,304-query batch is split across the ranks (strong scaling; at N=1
+    the whole batch in input order); the timed outputs are then checked
+    against the oracle on 65,536 queries (decision hash, counters, d_hat,
+    grad) and Barnes-Hut against exact on the same queries."""
+    import paper_2108_10480_b200 as sd
+    from paper_2108_10480_b200 import configs, sharding
+    torch = run.torch
+    rank, world = run.rank, run.world
+    t0 = time.perf_counter()
+    w, q = configs.cfg4()
+    v, q = configs.quantize(w.vertices), configs.quantize(q)
+    Q_total = len(q)
+    eng = sd.Engine(run.local, sd.SD_FP64 if fp64 else sd.SD_FP32)
+    eng.set_geometry(v, w.simplices, w.kinds)
+    tw = time.perf_counter()
+    wt = eng.build_weights()
+    tw = time.perf_counter() - tw
+    tb = time.perf_counter()
+    eng.build_bvh(tree_method(sd))
+    tb = time.perf_counter() - tb
+    P = sd.SmoothParams(alpha=w.alpha, alpha_u=600.0, beta=w.beta)
+    balance = None
+    sel = np.arange(Q_total)
+    if world > 1:
+        def counters(sub):
+            r = eng.smooth_min_dist(sub, P)
+            return r.leaves, r.far_field
+
+        order = sharding.morton_order(q)
+        est = sharding.estimate_query_costs(counters, q[order], stride=64)
+        ranges = sharding.balanced_ranges(est, world)
+        lo, hi = ranges[rank]
+        sel = order[lo:hi]
+        balance = {"ranges": ranges, "estimated_cost_share": [float(est[a:b].sum() / est.sum()) for a, b in ranges],
+                   "estimate": "strided sample (1/64) of the Morton-sorted batch, popped nodes 2(L+F)-1"}
+    qb = np.ascontiguousarray(q[sel])
+    Q = len(qb)
+    qd = torch.tensor(qb, dtype=torch.float64 if fp64 else torch.float32, device=run.dev)
+    d_hat = torch.empty(Q, dtype=torch.float64, device=run.dev)
+    grad = torch.empty(Q, 3, dtype=torch.float64, device=run.dev)
+    leaves = torch.empty(Q, dtype=torch.int64, device=run.dev)
+    far = torch.empty(Q, dtype=torch.int64, device=run.dev)
+    hsh = torch.empty(Q, dtype=torch.int64, device=run.dev)
+
+    def step(counters=False):
+        eng.query_points_device(qd.data_ptr(), Q, P, sd.SD_BVH, d_hat.data_ptr(), grad.data_ptr(),
+                                leaves_ptr=leaves.data_ptr() if counters else None,
+                                far_ptr=far.data_ptr() if counters else None,
+                                hash_ptr=hsh.data_ptr() if counters else None, stream=stream.cuda_stream)
+
+    step(counters=True)  # also uploads the traversal layout; counters + decision hash of the batch
+    torch.cuda.synchronize()
+    counted = (d_hat.cpu().numpy(), leaves.cpu().numpy(), far.cpu().numpy(), hsh.cpu().numpy().view(np.uint64))
+    setup_s = time.perf_counter() - t0
+    L, F = float(counted[1].sum()), float(counted[2].sum())
+    t = time_device(run, step, stream, flush, args.steps, args.warmup, eng)
+    launches = eng.last_launch_count()
+    ms, kms = t["ms"], t["kernel_ms"]
+    got_d, got_g = d_hat.cpu().numpy(), grad.cpu().numpy()
+    qh = torch.tensor(qb, dtype=torch.float64).pin_memory().numpy()
+    res = sd.SmoothResults(torch.empty(Q, dtype=torch.float64).pin_memory().numpy(),
+                           torch.empty(Q, 3, dtype=torch.float64).pin_memory().numpy())
+    te = time_e2e(run, lambda: eng.query_points(qh, P, sd.SD_BVH, out=res), max(3, min(args.steps, 10)))
+    e2e = {"value": Q_total / te, "unit": "queries/s", "h2d_bytes_per_step": Q * 24, "d2h_bytes_per_step": Q * 32,
+           "api": "sd_query_points (pinned host fp64 queries in, d_hat + grad out)"}
+    L, F, Qs = run.reduce([L, F, float(Q)], "sum")
+    pops = 2 * (L + F) - Qs
+    flops = (FLOPS_BOX_TEST * pops + FLOPS_FAR_TERM * F + FLOPS_PER_PAIR[2] * L) / world
+    nbytes = (BYTES_NODE * pops + BYTES_LEAF * L) / world
+    out = {"metric": "BVH queries/s (value+grad)", "value": Q_total / (ms * 1e-3), "unit": "queries/s",
+           "scaling": "strong", "e2e": e2e, "ms_per_step": ms, "queries": Q_total, "queries_per_gpu": Q,
+           "primitives": len(w.kinds),
+           "workload": "cfg4: icosphere(9) with radial displacement, 5,242,880 triangles, 4,194,304 queries "
+                       "(half uniform in [-1.5,1.5]^3, half within 0.02 of the surface), alpha=200, "
+                       f"beta=0.5, {'fp64' if fp64 else 'fp32'}, {tree_name()} (BASELINE configs[3])",
+           "dtype": "f64" if fp64 else "f32", "clocks": t["clocks"],
+           "per_query": {"leaves": L / Qs, "far_field": F / Qs, "nodes_popped": pops / Qs},
+           "setup_s": {"total": setup_s, "build_weights": tw, "build_tree": tb},
+           "gpu_launches": launches * args.steps}
+    if kms:
+        peak, src, cands = compute_peak(peaks, t["clocks"].get("sm_mhz"), fp64)
+        achieved = flops / (kms * 1e-3) / 1e12
+        roof = {"bound": "issue (L1/L2-resident tree; see ncu)", "achieved": achieved, "unit": "TFLOP/s",
+                "peak": peak, "peak_source": src, "frac": achieved / peak, "kernel_ms": kms,
+                "kernel_share_of_step": kms / ms,
+                "algorithmic": "10 flop/popped node + 12/far term + 192/exact tri leaf (this run's counters); "
+                               "kernel time = CUDA events around the traversal launch (sort and finalize excluded)",
+                "modelled_l1l2_bytes_per_launch": nbytes,
+                "modelled_l1l2_gbs": nbytes / (kms * 1e-3) / 1e9,
+                "modelled_bytes": "32 B per popped node + 100 B per exact leaf, served from L1/L2, not DRAM",
+                "traffic": None}
+        st = ncu_stamp("bvh_cfg4_f64" if fp64 else "bvh_cfg4_f32")
+        if st:
+            roof["traffic"] = st.get("dram_bytes")
+            roof["ncu"] = st
+        out["roofline"] = roof
+    if balance:
+        out["balance"] = balance
+    par = None
+    if rank == 0 and not args.no_cpu:
+        par = bvh_parity(eng, v, w, wt, qb, counted, got_d, got_g, P, world == 1)
+        if world == 1:
+            out["cpu_baseline"] = par.pop("cpu_baseline")
+    if world > 1 and not args.no_weak:
+        # weak scaling variant: every rank a full cfg4 batch of its own
+        _, qw = configs.cfg4(block=rank)
+        qw = configs.quantize(qw)
+        qwd = torch.tensor(qw, dtype=torch.float64 if fp64 else torch.float32, device=run.dev)
+        dw = torch.empty(len(qw), dtype=torch.float64, device=run.dev)
+        gw = torch.empty(len(qw), 3, dtype=torch.float64, device=run.dev)
+        tw2 = time_device(run, lambda: eng.query_points_device(qwd.data_ptr(), len(qw), P, sd.SD_BVH, dw.data_ptr(),
+                                                                gw.data_ptr(), stream=stream.cuda_stream),
+                          stream, flush, args.steps, args.warmup)
+        out["weak"] = {"value": world * len(qw) / (tw2["ms"] * 1e-3), "unit": "queries/s", "scaling": "weak",
+                       "ms_per_step": tw2["ms"], "queries_per_gpu": len(qw)}
+    eng.close()
+    return out, par
+
+
+def bvh_parity(eng, v, w, wt, qb, counted, got_d, got_g, P, full_batch, n_sample=65536):
+    """cfg4 at config scale: the oracle port on the SAME tree (exported in
+    the reference layout) and table, on n_sample queries (half from each
+    half of the distribution at N=1): decision hash and counters of every
+    query, d_hat / grad of the timed outputs, plus Barnes-Hut against the
+    GPU exact path on the same queries (acceptance [1]: d_hat_BH <= d_hat
+    + tol) and GPU exact against the oracle's exact on a 32-query subset."""
+    import paper_2108_10480_b200 as sd
+    O, m, ws, t = oracle_objects(v, w.simplices, w.kinds, wt, eng.export_bvh())
+    threads = O.hardware_threads()
+    Q = len(qb)
+    if full_batch:
+        half = Q // 2
+        idx = np.concatenate([np.linspace(0, half - 1, n_sample // 2), np.linspace(half, Q - 1, n_sample // 2)])
+    else:
+        idx = np.linspace(0, Q - 1, min(n_sample, Q))
+    idx = idx.astype(np.int64)
+    p = O.Params(alpha=P.alpha, alpha_u=P.alpha_u, beta=P.beta)
+    ref = O.query(m, ws, qb[idx], p, tree=t, threads=threads)
+    cd, cl, cf, ch = counted
+    out = {"n": int(len(idx)), "sample": "32,768 evenly spaced queries from each half of the distribution"
+           if full_batch else f"{len(idx)} evenly spaced queries of rank 0's block",
+           "hash_mismatch": int((ch[idx] != ref.decision_hash).sum()),
+           "leaves_mismatch": int((cl[idx] != ref.leaves).sum()),
+           "far_field_mismatch": int((cf[idx] != ref.far_field).sum()),
+           "timed_equals_counted_run": bool(np.array_equal(cd[idx], got_d[idx], equal_nan=True))}
+    out.update(parity_stats(got_d[idx], got_g[idx], ref.d_hat, ref.grad, P.alpha, "f32"))
+    out["cpu_baseline"] = {"value": len(idx) / ref.seconds, "unit": "queries/s", "cores": threads, "kind": "port",
+                           "sample": f"{len(idx)} cfg4 queries (both halves) on the exported GPU-built tree, "
+                                     f"fp64 oracle port, {ref.seconds:.2f} s"}
+    # Barnes-Hut vs exact on the same queries (GPU exact, checked below)
+    ex = eng.query_points(qb[idx], sd.SmoothParams(alpha=P.alpha, alpha_u=P.alpha_u, beta=0.0), sd.SD_EXACT)
+    fin = np.isfinite(ex.d_hat) & np.isfinite(got_d[idx])
+    diff = got_d[idx][fin] - ex.d_hat[fin]
+    out["bvh_minus_exact"] = {"n": int(fin.sum()), "max": float(diff.max()), "mean": float(diff.mean()),
+                              "min": float(diff.min()), "violations_bh_le_exact_plus_1e-5": int((diff > 1e-5).sum()),
+                              "criterion": "acceptance [1] (T/acceptance.cpp:76-115): d_hat_BH <= d_hat_exact + tol"}
+    sub = idx[np.linspace(0, len(idx) - 1, 32).astype(np.int64)]
+    rex = O.query(m, ws, qb[sub], O.Params(alpha=P.alpha, alpha_u=P.alpha_u, beta=0.0), threads=threads)
+    pos = np.searchsorted(idx, sub)
+    out["gpu_exact_vs_oracle_exact"] = parity_stats(ex.d_hat[pos], ex.grad[pos], rex.d_hat, rex.grad, P.alpha, "f32")
+    out["gpu_exact_vs_oracle_exact"]["sample"] = "32 of the sample queries x 5,242,880 triangles"
+    return out
+
+
+# ----------------------------------------------------------- our arm
+def run_ours(args, rank, world, local):
+    import torch
+    torch.cuda.set_device(local)
+    run = Run(rank, world, local, "nccl")
+    dev = run.dev
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+    stream = torch.cuda.current_stream(dev)
+    peaks = measure_peaks(local)
+    line = {"metric": "exact pair-evals/s (value+grad)", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "data": "synthetic (seeded generators of BASELINE configs[1..3])"}
+    t0 = time.perf_counter()
+    run_exact_headline(args, run, peaks, stream, flush, line)
+    if not args.no_bvh:
+        bvh, par = measure_bvh(args, run, stream, flush, peaks)
+        line["bvh"] = bvh
+        if par is not None:
+            line.setdefault("parity", {})["cfg4_bvh"] = par
+    if peaks:
+        line["peaks_probe"] = peaks
+    line["clocks_all"] = ClockSampler.summarize(ClockSampler.ALL)
+    line["bench_seconds"] = time.perf_counter() - t0
+    if rank == 0:
+        line["gpu_launches_note"] = "libsdgpu.so kernels launched inside the headline's timed region"
+        print(json.dumps(line), flush=True)
+    run.close()
+
+
+# ------------------------------------------------------ reference arm
 def run_reference(args, rank, world):
+    """The reference's own CPU path, on our headline's config, metric and
+    unit: the oracle port (fp64, all host threads) builds the cfg3 WeightSet
+    the reference way and evaluates a bounded query sample per step; the
+    `bvh` object does the same for cfg4 on the host-built median tree."""
     if rank != 0:
         return
     import oracle as O
     O.build()
-    w, v, q, wt = workload(0)
     threads = O.hardware_threads()
-    N = len(w.kinds)
-    n, secs, _ = cpu_sample(v, w.simplices, w.kinds, wt, q, threads, target_s=3.0)
-    import oracle as O2  # noqa: F401  (same module; warm-up steps below)
-    m = O.Mesh.from_arrays(v, w.simplices, w.kinds)
-    ws = O.Weights.from_table(O.WeightTable(wt.A, wt.sup_wtilde, wt.edge_a, wt.tri_stored, wt.poly_index))
-    p = O.Params(alpha=ALPHA, alpha_u=600.0, beta=0.0)
+    v3, t3, k3, q3 = cfg3_workload()
+    m = O.Mesh.from_arrays(v3, t3, k3)
+    ws = O.Weights.build(m)
+    p = O.Params(alpha=100.0, alpha_u=600.0, beta=0.0)
+    N = len(k3)
+    pilot = max(threads * 2, 32)
+    r = O.query(m, ws, q3[:pilot], p, threads=threads)
+    n = int(min(len(q3), max(pilot, pilot * 2.0 / max(r.seconds, 1e-3))))  # ~2 s per step
     for i in range(args.warmup):
-        O.query(m, ws, q[:n], p, threads=threads)
+        O.query(m, ws, q3[:n], p, threads=threads)
     times = []
     for i in range(args.steps):
-        lo = (i * n) % max(1, len(q) - n)
-        r = O.query(m, ws, q[lo:lo + n], p, threads=threads)
-        times.append(r.seconds)
+        lo = (i * n) % max(1, len(q3) - n)
+        times.append(O.query(m, ws, q3[lo:lo + n], p, threads=threads).seconds)
     t = float(np.mean(times))
     value = n * N / t
     line = {
         "impl": "reference", "metric": "exact pair-evals/s (value+grad)", "value": value, "unit": "pair-evals/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "cfg2: helix polyline 20,000 edges, exact LSE, alpha=100 (BASELINE configs[1])",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded generators of BASELINE configs[1..3])",
+        "config": {"workload": "cfg3: torus 262,144 triangles, 1,048,576 queries, exact LSE, alpha=100 "
+                               "(BASELINE configs[2]); a bounded sample of the batch per step",
                    "queries_per_step": n, "primitives": N, "parallelism": f"{threads} host threads"},
         "cpu_baseline": {"value": value, "unit": "pair-evals/s", "cores": threads, "kind": "port",
-                         "sample": f"{n} of {QUERIES_PER_GPU} cfg2 queries x {N} edges per step"},
+                         "sample": f"{n} of {len(q3)} cfg3 queries x {N} triangles per step"},
         "e2e": {"value": value, "unit": "pair-evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     if not args.no_bvh:
@@ -275,184 +835,65 @@ def reference_bvh(threads, target_s=10.0):
             "setup_s": setup}
 
 
-def measure_bvh(args, rank, world, local, eng_cls, dev, stream, flush, peaks):
-    """Secondary line item: BVH far-field queries/s on BASELINE configs[3]
-    (cfg4: icosphere(9), 5,242,880 triangles, 4,194,304 queries per GPU,
-    alpha 200, beta 0.5), the reference's median tree built on the GPU + fp32
-    traversal."""
-    import torch
-    import paper_2108_10480_b200 as sd
-    from paper_2108_10480_b200 import configs
-    t0 = time.perf_counter()
-    strong = args.bvh_strong
-    # weak (default): every rank its own cfg4 batch; strong: ONE batch split
-    # into Morton-contiguous blocks of equal estimated cost (SURVEY 8(e))
-    w, q = configs.cfg4(block=0 if strong else rank)
-    v, q = configs.quantize(w.vertices), configs.quantize(q)
-    Q_total = len(q) * (1 if strong else world)
-    bvh64 = args.fp64 and args.config == 2  # --fp64: the BVH leg in fp64 too
-    eng = sd.Engine(local, sd.SD_FP64 if bvh64 else sd.SD_FP32)
-    eng.set_geometry(v, w.simplices, w.kinds)
-    tw = time.perf_counter()
-    eng.build_weights()
-    tw = time.perf_counter() - tw
-    tb = time.perf_counter()
-    # BENCH_TREE=median builds the reference's median-split tree instead (A/B)
-    eng.build_bvh(tree_method(sd))
-    tb = time.perf_counter() - tb
-    P = sd.SmoothParams(alpha=w.alpha, alpha_u=600.0, beta=w.beta)
-    balance = None
-    if strong:
-        from paper_2108_10480_b200 import sharding
+# ------------------------------------------------------------ stub arm
+def run_stub(args, rank, world, local):
+    """CPU stand-in for the multi-GPU plumbing (tests/test_bench_spawn.py):
+    the same spawn path, process group (gloo), strong split of a fixed
+    batch, max-over-ranks timing and all-gathered result checksum, with a
+    numpy exact LSE over a tiny point cloud as the evaluator."""
+    run = Run(rank, world, local, "gloo")
+    rng = np.random.default_rng(7)
+    pts = rng.standard_normal((64, 3))
+    q = rng.uniform(-2, 2, (4096, 3))
+    lo, hi = strong_blocks(len(q), world)[rank]
 
-        def counters(sub):
-            r = eng.smooth_min_dist(sub, P)
-            return r.leaves, r.far_field
+    def evaluate(qs, alpha=50.0):
+        d = np.linalg.norm(qs[:, None, :] - pts[None], axis=2)
+        m = d.min(1)
+        return m - np.log(np.exp(-alpha * (d - m[:, None])).sum(1)) / alpha
 
-        order = sharding.morton_order(q)
-        est = sharding.estimate_query_costs(counters, q[order], stride=64)
-        ranges = sharding.balanced_ranges(est, world)
-        lo, hi = ranges[rank]
-        q = np.ascontiguousarray(q[order[lo:hi]])
-        balance = {"ranges": ranges, "estimated_cost_share": [float(est[a:b].sum() / est.sum()) for a, b in ranges],
-                   "estimate": "strided sample (1/64) of the Morton-sorted batch, popped nodes 2(L+F)-1"}
-    Q = len(q)
-    qd = torch.tensor(q, dtype=torch.float64 if bvh64 else torch.float32, device=dev)
-    d_hat = torch.empty(Q, dtype=torch.float64, device=dev)
-    grad = torch.empty(Q, 3, dtype=torch.float64, device=dev)
-    leaves = torch.empty(Q, dtype=torch.int64, device=dev)
-    far = torch.empty(Q, dtype=torch.int64, device=dev)
-
-    def step(counters=False):
-        eng.query_points_device(qd.data_ptr(), Q, P, sd.SD_BVH, d_hat.data_ptr(), grad.data_ptr(),
-                                leaves_ptr=leaves.data_ptr() if counters else None,
-                                far_ptr=far.data_ptr() if counters else None, stream=stream.cuda_stream)
-
-    step(counters=True)  # also uploads the traversal layout
-    torch.cuda.synchronize()
-    setup_s = time.perf_counter() - t0
-    L = leaves.double().sum().item()
-    F = far.double().sum().item()
     for _ in range(max(3, args.warmup)):
-        step()
-    launches = eng.last_launch_count()
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    if world > 1:
-        torch.distributed.barrier()
-    torch.cuda.synchronize()
-    for i in range(args.steps):
-        flush.zero_()
-        evs[i][0].record(stream)
-        step()
-        evs[i][1].record(stream)
-    torch.cuda.synchronize()
-    ms = float(np.mean([a.elapsed_time(b) for a, b in evs]))
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-    ms = float(t.item())
-    # end to end through the public host API: pinned fp64 host queries in,
-    # d_hat + gradient out (H2D, Morton sort, traversal, finalize, D2H)
-    qh = torch.tensor(q, dtype=torch.float64).pin_memory().numpy()
-    res = sd.SmoothResults(torch.empty(Q, dtype=torch.float64).pin_memory().numpy(),
-                           torch.empty(Q, 3, dtype=torch.float64).pin_memory().numpy())
-    eng.query_points(qh, P, sd.SD_BVH, out=res)
-    e2e_times = []
-    for _ in range(max(3, args.steps)):
-        torch.cuda.synchronize()
-        t1 = time.perf_counter()
-        eng.query_points(qh, P, sd.SD_BVH, out=res)
-        e2e_times.append(time.perf_counter() - t1)
-    te = torch.tensor([float(np.mean(e2e_times))], dtype=torch.float64, device=dev)
-    if world > 1:
-        torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
-    e2e = {"value": Q_total / float(te.item()), "unit": "queries/s", "h2d_bytes_per_step": Q * 24,
-           "d2h_bytes_per_step": Q * 32}
-    if world > 1:  # counters summed over ranks (per-query means below are whole-job)
-        lf = torch.tensor([L, F, float(Q)], dtype=torch.float64, device=dev)
-        torch.distributed.all_reduce(lf)
-        L, F, Qsum = (float(x) for x in lf.tolist())
-    else:
-        Qsum = float(Q)
-    pops = 2 * (L + F) - Qsum
-    # algorithmic work per GPU per step (whole-job / ranks), over the
-    # max-over-ranks step time: the roofline is a per-GPU figure
-    flops = (FLOPS_BOX_TEST * pops + FLOPS_FAR_TERM * F + FLOPS_PER_TRI_PAIR * L) / world
-    nbytes = (BYTES_NODE * pops + BYTES_LEAF * L) / world
-    out = {"metric": "BVH queries/s (value+grad)", "value": Q_total / (ms * 1e-3), "unit": "queries/s",
-           "scaling": "strong" if strong else "weak", "e2e": e2e,
-           "ms_per_step": ms, "queries_per_gpu": Q, "primitives": len(w.kinds),
-           "workload": "cfg4: icosphere(9) with radial displacement, 5,242,880 triangles, 4,194,304 queries "
-                       "per GPU (half uniform in [-1.5,1.5]^3, half within 0.02 of the surface), alpha=200, "
-                       f"beta=0.5, {'fp64' if bvh64 else 'fp32'}, {tree_name()} (BASELINE configs[3])",
-           "dtype": "f64" if bvh64 else "f32",
-           "per_query": {"leaves": L / Qsum, "far_field": F / Qsum, "nodes_popped": pops / Qsum},
-           "setup_s": {"total": setup_s, "build_weights": tw, "build_tree": tb},
-           "gpu_launches": launches * args.steps,
-           "roofline": {"achieved_tflops": flops / (ms * 1e-3) / 1e12, "touched_gbs": nbytes / (ms * 1e-3) / 1e9,
-                        "hbm_peak_gbs": 6542.4, "algorithmic": "10 flop/popped node + 12/far term + 192/exact "
-                        "tri leaf; 32 B/popped node + 100 B/leaf (from this run's counters)"}}
-    if balance:
-        out["balance"] = balance
-    if peaks:
-        out["roofline"]["frac_fp32"] = out["roofline"]["achieved_tflops"] / peaks["ffma_tflops"]
-    # the touched bytes are served from L1/L2 (ncu of pair_kernel: DRAM 0.9 % of
-    # peak, L2 hit 88 %, L1 hit 57 %); the kernel is issue-bound (76 % of issue
-    # slots, profiles/r1_pair_bvh_summary.md)
-    out["roofline"]["bound"] = "issue (L1/L2-resident tree)"
-    out["roofline"]["touched_frac_of_hbm_peak"] = out["roofline"]["touched_gbs"] / 6542.4
-    # the issue-slot bound, from the committed ncu capture of this kernel (not
-    # measured in this run): warp instructions per launch and issue-slot use
-    out["roofline"]["ncu_issue"] = {"issue_slots_busy": 0.768, "ipc": 3.05, "warp_instructions": 2.009e10,
-                                    "avg_active_lanes": 17.0, "source": "profiles/r1_pair_bvh_details.csv, "
-                                    "profiles/r1_k3_source_breakdown.md (fp32, median tree)"}
-    if rank == 0 and world == 1 and not args.no_cpu:
-        out["cpu_baseline"] = bvh_cpu_sample(eng, v, w, q, P)
-    eng.close()
-    return out
+        evaluate(q[lo:hi])
+    run.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        out = evaluate(q[lo:hi])
+    ms = run.reduce(1e3 * (time.perf_counter() - t0) / max(1, args.steps))[0]
+    parts = run.gather({"rank": rank, "lo": lo, "hi": hi, "sum": float(out.sum())})
+    if rank == 0:
+        full = float(evaluate(q).sum())
+        print(json.dumps({"metric": "stub exact pair-evals/s", "value": len(q) * len(pts) / (ms * 1e-3),
+                          "unit": "pair-evals/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                          "ms_per_step": ms, "scaling": "strong", "blocks": [(p["lo"], p["hi"]) for p in parts],
+                          "checksum": sum(p["sum"] for p in parts), "checksum_single": full,
+                          "backend": run.backend}), flush=True)
+    run.close()
 
 
-def bvh_cpu_sample(eng, v, w, q, P, target_s=10.0):
-    """The oracle port (fp64, all host threads) on a bounded query subset of
-    cfg4, traversing the SAME tree (the GPU-built tree exported in the reference
-    layout) with the same WeightSet table."""
-    import oracle as O
-    O.build()
-    threads = O.hardware_threads()
-    wt = eng.weight_table()
-    m = O.Mesh.from_arrays(v, w.simplices, w.kinds)
-    ws = O.Weights.from_table(O.WeightTable(wt.A, wt.sup_wtilde, wt.edge_a, wt.tri_stored, wt.poly_index))
-    t = O.Tree.from_nodes(eng.export_bvh())
-    p = O.Params(alpha=P.alpha, alpha_u=P.alpha_u, beta=P.beta)
-    # both halves of the query distribution (uniform box / near surface)
-    half = len(q) // 2
-    pick = lambda n: np.concatenate([q[:n // 2], q[half:half + n - n // 2]])
-    pilot = max(threads * 16, 1024)
-    r = O.query(m, ws, pick(pilot), p, tree=t, threads=threads)
-    n = int(min(65536, max(pilot, pilot * target_s / max(r.seconds, 1e-3))))
-    r = O.query(m, ws, pick(n), p, tree=t, threads=threads)
-    return {"value": n / r.seconds, "unit": "queries/s", "cores": threads, "kind": "port",
-            "sample": f"{n} cfg4 queries (half from each half of the distribution) on the exported GPU-built tree, "
-                      f"fp64 oracle port, {r.seconds:.1f} s"}
-
-
+# ------------------------------------------------------ other configs
 def run_cfg5(args, rank, world, local):
     """BASELINE configs[4]: mixed scene (16.8M triangles + 1M edges + 1M
     points), 16,777,216 queries, alpha 100, beta 0.5, PRIMITIVE-sharded over
     the ranks (Morton-contiguous shards, one GPU-built tree per shard, global
     WeightSet), per-query fp64 partials merged with ONE NCCL all-reduce,
-    then sd_finalize_device. Strong scaling (fixed total work)."""
+    then sd_finalize_device. Strong scaling (fixed total work). --exact: the
+    exact path (smooth_min_dist_flat, smooth.hpp:189-198) over the same
+    primitive shards and merge, on an evenly spaced subset of the queries
+    (--exact-queries, default 65,536: the whole batch would be 3.2e14 pair
+    evaluations per step)."""
     import torch
     import paper_2108_10480_b200 as sd
     from paper_2108_10480_b200 import configs, sharding
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+    run = Run(rank, world, local, "nccl")
     t0 = time.perf_counter()
     w, q = configs.cfg5()
     v, q = configs.quantize(w.vertices), configs.quantize(q)
+    exact = args.exact
+    mode = sd.SD_EXACT if exact else sd.SD_BVH
+    if exact:
+        q = np.ascontiguousarray(q[np.linspace(0, len(q) - 1, args.exact_queries).astype(np.int64)])
     tg = time.perf_counter() - t0
     eg = sd.Engine(local, sd.SD_FP32)  # host-side: global WeightSet on the full mesh
     eg.set_geometry(v, w.simplices, w.kinds)
@@ -466,7 +907,8 @@ def run_cfg5(args, rank, world, local):
     eng.set_weights(wt.A, wt.sup_wtilde, wt.edge_a, wt.tri_stored, sh.poly_index)
     tb = time.perf_counter()
     # BENCH_TREE=median builds the reference's median-split tree instead (A/B)
-    eng.build_bvh(tree_method(sd))
+    if not exact:
+        eng.build_bvh(tree_method(sd))
     tb = time.perf_counter() - tb
     Q = len(q)
     P = sd.SmoothParams(alpha=w.alpha, alpha_u=600.0, beta=w.beta)
@@ -503,7 +945,7 @@ def run_cfg5(args, rank, world, local):
         if exchange == "peer":
             # evaluation with the stores into the owners' buffers fused into
             # its finalize epilogue (sd_query_points_scatter)
-            eng.query_points_scatter(qd.data_ptr(), Q, P, sd.SD_BVH, table.data_ptr(), world, rank, per,
+            eng.query_points_scatter(qd.data_ptr(), Q, P, mode, table.data_ptr(), world, rank, per,
                                      stream=stream.cuda_stream)
             launches[0] = eng.last_launch_count()
             if hdl is not None:
@@ -514,7 +956,7 @@ def run_cfg5(args, rank, world, local):
                 hdl.barrier(channel=1)
             launches[0] += 1
             return
-        eng.query_points_device(qd.data_ptr(), Q, P, sd.SD_BVH, d_hat.data_ptr(), c_ptr=buf.data_ptr(),
+        eng.query_points_device(qd.data_ptr(), Q, P, mode, d_hat.data_ptr(), c_ptr=buf.data_ptr(),
                                 grad_c_ptr=buf.data_ptr() + 8 * Q, stream=stream.cuda_stream)
         launches[0] = eng.last_launch_count() + 1  # + the finalize kernel below
         if world > 1:
@@ -555,23 +997,34 @@ def run_cfg5(args, rank, world, local):
         threads = O.hardware_threads()
         om = O.Mesh.from_arrays(v, w.simplices, w.kinds)
         ow = O.Weights.from_table(O.WeightTable(wt.A, wt.sup_wtilde, wt.edge_a, wt.tri_stored, wt.poly_index))
-        ot = O.Tree.from_nodes(eng.export_bvh())
-        sample = np.linspace(0, Q - 1, 4096).astype(np.int64)
-        r = O.query(om, ow, q[sample], O.Params(alpha=w.alpha, alpha_u=600.0, beta=w.beta), tree=ot, threads=threads)
+        ot = None if exact else O.Tree.from_nodes(eng.export_bvh())
+        nsamp = 16 if exact else 4096
+        sample = np.linspace(0, Q - 1, nsamp).astype(np.int64)
+        r = O.query(om, ow, q[sample], O.Params(alpha=w.alpha, alpha_u=600.0, beta=0.0 if exact else w.beta),
+                    tree=None if exact else ot, threads=threads)
         got = d_hat[torch.as_tensor(sample, device=dev)].cpu().numpy()
         ok = np.isfinite(r.d_hat)
-        cpu = {"value": 4096 / r.seconds, "unit": "queries/s", "cores": threads, "kind": "port",
-               "sample": f"4,096 evenly spaced cfg5 queries on the exported GPU-built tree, fp64 oracle port, {r.seconds:.2f} s",
-               "max_abs_d_hat_diff": float(np.abs(got[ok] - r.d_hat[ok]).max()) if ok.any() else 0.0}
+        NP = len(w.kinds)
+        cpu = {"value": (nsamp * NP if exact else nsamp) / r.seconds, "unit": "pair-evals/s" if exact else "queries/s",
+               "cores": threads, "kind": "port",
+               "sample": f"{nsamp} evenly spaced cfg5 queries "
+                         + ("x all primitives (exact)" if exact else "on the exported GPU-built tree")
+                         + f", fp64 oracle port, {r.seconds:.2f} s",
+               "max_abs_d_hat_diff": float(np.abs(got[ok] - r.d_hat[ok]).max()) if ok.any() else 0.0,
+               "parity": parity_stats(got, None, r.d_hat, None, w.alpha, "f32")}
         del om, ow, ot
     if rank == 0:
-        line = {"metric": "BVH queries/s (value+grad), primitive-sharded", "value": Q / (ms * 1e-3),
-                "unit": "queries/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        NP = len(w.kinds)
+        line = {"metric": ("exact pair-evals/s (value+grad), primitive-sharded" if exact else
+                           "BVH queries/s (value+grad), primitive-sharded"),
+                "value": (Q * NP if exact else Q) / (ms * 1e-3),
+                "unit": "pair-evals/s" if exact else "queries/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
                 "dtype": "f32", "data": "synthetic",
                 "config": {"workload": "cfg5: 64 rotated cfg3 tori (16,777,216 triangles) + 1M edges + 1M points, "
-                                       "16,777,216 queries uniform in the scene AABB, alpha=100, beta=0.5, fp32 "
-                                       "(BASELINE configs[4])",
+                                       + (f"{Q:,} evenly spaced of the 16,777,216 queries, exact LSE" if exact else
+                                          "16,777,216 queries uniform in the scene AABB, beta=0.5")
+                                       + ", alpha=100, fp32 (BASELINE configs[4])",
                            "parallelism": f"primitive-sharded x{world} (Morton shards, {tree_name()} per shard), "
                                           + ("partials stored into the owners' symmetric buffers over peer memory "
                                              "by the evaluation's own finalize epilogue (sd_query_points_scatter), "
@@ -582,8 +1035,8 @@ def run_cfg5(args, rank, world, local):
                 "setup_s": {"total": setup, "generate": tg, "build_weights": tw, "build_tree": tb},
                 "clocks": clk.summary()}
         print(json.dumps(line), flush=True)
-    if world > 1:
-        torch.distributed.destroy_process_group()
+    run.close()
+
 
 
 def run_m2m(args, rank, world, local):
@@ -730,146 +1183,6 @@ def run_render(args, rank, world, local):
     print(json.dumps(line), flush=True)
 
 
-def run_ours(args, rank, world, local):
-    import torch
-    import paper_2108_10480_b200 as sd
-
-    torch.cuda.set_device(local)
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    w, v, q, wt = workload(rank, args.config, args.alpha, local)
-    global ALPHA, FLOPS_PER_EDGE_PAIR, MUFU_PER_EDGE_PAIR
-    if args.config == 3:
-        ALPHA = w.alpha
-        FLOPS_PER_EDGE_PAIR, MUFU_PER_EDGE_PAIR = FLOPS_PER_TRI_PAIR, 3
-    if args.config == 1:
-        ALPHA = w.alpha
-        FLOPS_PER_EDGE_PAIR, MUFU_PER_EDGE_PAIR = 20, 2
-    fp64 = args.config == 1 or args.fp64
-    prec = sd.SD_FP64 if fp64 else sd.SD_FP32
-    N, Q = len(w.kinds), len(q)
-    eng = sd.Engine(local, prec)
-    eng.set_geometry(v, w.simplices, w.kinds)
-    eng.set_weights(wt.A, wt.sup_wtilde, wt.edge_a, wt.tri_stored, wt.poly_index)
-    P = sd.SmoothParams(alpha=ALPHA, alpha_u=600.0, beta=0.0)
-
-    dev = torch.device("cuda", local)
-    qd = torch.tensor(q, dtype=torch.float64 if fp64 else torch.float32, device=dev)
-    d_hat = torch.empty(Q, dtype=torch.float64, device=dev)
-    grad = torch.empty(Q, 3, dtype=torch.float64, device=dev)
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
-    stream = torch.cuda.current_stream(dev)
-
-    def step():
-        eng.query_points_device(qd.data_ptr(), Q, P, sd.SD_EXACT, d_hat.data_ptr(), grad.data_ptr(),
-                                stream=stream.cuda_stream)
-
-    peaks = measure_peaks(local) if rank == 0 else None  # only rank 0 reports the roofline
-    for _ in range(max(3, args.warmup)):
-        step()
-    torch.cuda.synchronize()
-    launches_per_step = eng.last_launch_count()
-
-    def barrier():
-        if world > 1:
-            torch.distributed.barrier()
-
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    barrier()
-    torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
-        for i in range(args.steps):
-            flush.zero_()  # L2 flush between timed iterations (outside the events)
-            evs[i][0].record(stream)
-            step()
-            evs[i][1].record(stream)
-        torch.cuda.synchronize()
-    barrier()
-    step_ms = [a.elapsed_time(b) for a, b in evs]
-    ms = float(np.mean(step_ms))
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-    ms_max = float(t.item())
-    pairs_per_rank = Q * N
-    value = world * pairs_per_rank / (ms_max * 1e-3)
-
-    # end to end through the public host API: pinned host q in, d_hat+grad out
-    qh = torch.tensor(q, dtype=torch.float64).pin_memory().numpy()
-    res = sd.SmoothResults(torch.empty(Q, dtype=torch.float64).pin_memory().numpy(),
-                           torch.empty(Q, 3, dtype=torch.float64).pin_memory().numpy())
-    e2e_times = []
-    barrier()
-    eng.query_points(qh, P, sd.SD_EXACT, out=res)  # warm the host-path buffers
-    for i in range(max(3, args.steps)):
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        eng.query_points(qh, P, sd.SD_EXACT, out=res)
-        e2e_times.append(time.perf_counter() - t0)
-    e2e_s = float(np.mean(e2e_times))
-    te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
-    if world > 1:
-        torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
-    e2e_value = world * pairs_per_rank / float(te.item())
-
-    bvh = None if args.no_bvh else measure_bvh(args, rank, world, local, sd.Engine, dev, stream, flush, peaks)
-    if rank == 0:
-        achieved = pairs_per_rank * FLOPS_PER_EDGE_PAIR / (ms_max * 1e-3) / 1e12
-        # dram read + write of the dominant launch, from the committed ncu
-        # capture of this workload (cfg2 fp32, tile-bound kernel):
-        # profiles/r1_v6_exact_edge_details.csv (132.6 MB read + 68.2 MB written,
-        # the fp64 per-query partial state of the 8 primitive splits)
-        traffic = 2.008e8 if (args.config == 2 and not fp64) else None
-        roof = {"bound": "fp64-fma" if fp64 else "fp32-fma", "achieved": achieved, "unit": "TFLOP/s",
-                "traffic": traffic, "traffic_unit": "bytes per launch (ncu dram__bytes_read+write)",
-                "algorithmic_bytes": Q * 12 + N * 48,
-                "kernel": (f"exact_kernel<{'double' if fp64 else 'float'}, "
-                           + {1: "point>", 2: "edge, poly> x3 segment launches", 3: "triangle, poly>"}[args.config]
-                           + " + finalize (step time)"),
-                "algorithmic": f"{FLOPS_PER_EDGE_PAIR} flop x {pairs_per_rank} pairs per step (SURVEY 8d)"}
-        if peaks:
-            pk = peaks["dfma_tflops"] if fp64 else peaks["ffma_tflops"]
-            roof.update({"peak": pk, "frac": achieved / pk,
-                         "peak_source": f"in-run {'DFMA' if fp64 else 'FFMA'} microbenchmark (libsdpeaks.so); "
-                                        "MEASURED_PEAKS.json has no FP32/FP64 entry",
-                         "mufu_frac": pairs_per_rank * MUFU_PER_EDGE_PAIR / (ms_max * 1e-3) / 1e12 / peaks["mufu_tops"],
-                         "peaks": peaks})
-            # bound-aware roofline = max(flops / P_fma, mufu / P_mufu)
-            roof["bound_aware_frac"] = max(roof["frac"], roof["mufu_frac"])
-        cpu = None
-        if world == 1 and not args.no_cpu:
-            import oracle as O
-            O.build()
-            threads = O.hardware_threads()
-            n, secs, _ = cpu_sample(v, w.simplices, w.kinds, wt, q, threads)
-            cpu = {"value": n * N / secs, "unit": "pair-evals/s", "cores": threads, "kind": "port",
-                   "sample": f"first {n} of {Q} cfg{args.config} queries x {N} primitives ({secs:.1f} s, "
-                             f"fp64 oracle port)"}
-        line = {
-            "metric": "exact pair-evals/s (value+grad)", "value": value, "unit": "pair-evals/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64" if fp64 else "f32", "data": "synthetic",
-            "config": {"workload": "cfg1: 4,096 unit-sphere points x 65,536 queries per GPU, exact LSE, alpha=50, fp64 "
-                                   "(BASELINE configs[0])" if args.config == 1 else ("cfg2: helix polyline 20,000 edges x 262,144 queries per GPU, exact LSE, "
-                                    f"alpha=100, {'fp64' if fp64 else 'fp32'} (BASELINE configs[1])") if args.config == 2 else
-                                   (f"cfg3: torus 262,144 triangles x 1,048,576 queries per GPU, exact LSE, "
-                                    f"alpha={ALPHA:g}, fp32 (BASELINE configs[2])"),
-                       "queries_per_gpu": Q, "primitives": N, "l2": "flushed between timed steps (256 MiB write)",
-                       "parallelism": f"query-sharded x{world}, geometry replicated"},
-            "roofline": roof,
-            "cpu_baseline": cpu,
-            "e2e": {"value": e2e_value, "unit": "pair-evals/s", "h2d_bytes_per_step": Q * 3 * 8,
-                    "d2h_bytes_per_step": Q * 4 * 8},
-            "gpu_launches": launches_per_step * args.steps,
-            "clocks": clk.summary(),
-            "bvh": bvh,
-            "step_ms_all": step_ms,
-        }
-        print(json.dumps(line), flush=True)
-    if world > 1:
-        torch.distributed.destroy_process_group()
-
 
 def main():
     ap = argparse.ArgumentParser()
@@ -877,23 +1190,29 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
-    ap.add_argument("--no-bvh", action="store_true", help="skip the secondary BVH (cfg4) measurement")
-    ap.add_argument("--bvh-strong", action="store_true",
-                    help="BVH leg: split ONE cfg4 batch across the ranks by estimated cost (strong scaling)")
-    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 5],
-                    help="exact workload: 2 = BASELINE configs[1] (headline), 1 = configs[0] fp64 points, "
-                         "3 = configs[2] torus triangles, 5 = configs[4] primitive-sharded BVH")
-    ap.add_argument("--fp64", action="store_true", help="fp64 arithmetic for --config 2")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline and oracle parity legs")
+    ap.add_argument("--no-bvh", action="store_true", help="skip the BVH (cfg4) leg")
+    ap.add_argument("--no-weak", action="store_true", help="N > 1: skip the weak-scaling BVH variant")
+    ap.add_argument("--config", type=int, default=0, choices=[0, 5],
+                    help="0 = the default line (cfg3 headline + cfg2 + cfg4), 5 = configs[4] primitive-sharded")
+    ap.add_argument("--exact", action="store_true", help="--config 5: the exact path instead of the BVH path")
+    ap.add_argument("--exact-queries", type=int, default=65536, help="--config 5 --exact: evenly spaced queries")
+    ap.add_argument("--bvh-fp64", action="store_true", help="run only the BVH leg, in fp64")
+    ap.add_argument("--fp64", action="store_true", help="--render in fp64")
     ap.add_argument("--m2m", action="store_true", help="mesh-to-mesh evaluations of the paper's timing table rows")
     ap.add_argument("--rows", default="", help="comma-separated sim_rows names for --m2m (default: all)")
     ap.add_argument("--render", action="store_true", help="sphere tracer beta ablation + grid benchmark (callers)")
     ap.add_argument("--exchange", choices=["nccl", "peer"], default="nccl",
                     help="--config 5 merge: NCCL all-reduce or stores into the owners' buffers over peer memory")
-    ap.add_argument("--alpha", type=float, default=None, help="alpha for --config 3 (10, 100 or 1000)")
+    ap.add_argument("--stub", action="store_true", help="CPU stand-in evaluator over gloo (plumbing tests)")
     args = ap.parse_args()
+    maybe_spawn(args)
     rank, world, local = dist_env()
-    if args.impl == "reference":
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}")
+    if args.stub:
+        run_stub(args, rank, world, local)
+    elif args.impl == "reference":
         run_reference(args, rank, world)
     elif args.config == 5:
         run_cfg5(args, rank, world, local)
@@ -903,6 +1222,17 @@ def main():
     elif args.render:
         if rank == 0:
             run_render(args, rank, world, local)
+    elif args.bvh_fp64:
+        import torch
+        torch.cuda.set_device(local)
+        run = Run(rank, world, local, "nccl")
+        flush = torch.empty(256 << 20, dtype=torch.uint8, device=run.dev)
+        out, par = measure_bvh(args, run, torch.cuda.current_stream(run.dev), flush, measure_peaks(local), fp64=True)
+        if rank == 0:
+            out.update({"n_gpus": world, "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
+                        "vs_baseline": None, "data": "synthetic", "parity": par})
+            print(json.dumps(out), flush=True)
+        run.close()
     else:
         run_ours(args, rank, world, local)
 

@@ -261,6 +261,16 @@ int sd_load_bvh_cache(sd_ctx* ctx, const char* path);
 int sd_save_weight_cache(sd_ctx* ctx, const char* path);
 int sd_load_weight_cache(sd_ctx* ctx, const char* path);
 
+/* Kernel timing (measurement support, not in the reference): with timing
+ * on, every query call records a CUDA event pair on its launching stream
+ * around its dominant compute launches (the exact segment launches, or the
+ * tree traversal), excluding the query sort and the finalize epilogue.
+ * sd_kernel_times synchronises on the recorded events, writes up to cap
+ * elapsed times in milliseconds (call order), sets *n to the number
+ * recorded, and clears the list; with ms == NULL it only sets *n. */
+int sd_set_kernel_timing(sd_ctx* ctx, int on);
+int sd_kernel_times(sd_ctx* ctx, double* ms, int64_t cap, int64_t* n);
+
 /* Number of this library's kernels launched by the last query call. */
 int sd_last_launch_count(sd_ctx* ctx, int64_t* n);
 

@@ -36,7 +36,7 @@ assert NODE_DTYPE.itemsize == 72
 EXPORTED_SYMBOLS = (
     "sd_last_error", "sd_abi_version", "sd_create", "sd_destroy", "sd_set_geometry", "sd_set_weights",
     "sd_set_bvh", "sd_build_bvh", "sd_bvh_size", "sd_export_bvh", "sd_query_points", "sd_query_points_device",
-    "sd_finalize_device", "sd_last_launch_count", "sd_build_weights", "sd_weights_info", "sd_export_weights",
+    "sd_finalize_device", "sd_last_launch_count", "sd_set_kernel_timing", "sd_kernel_times", "sd_build_weights", "sd_weights_info", "sd_export_weights",
     "sd_mesh_dist_points",
     "sd_query_simplices",
     "sd_mesh_dist",
@@ -114,6 +114,8 @@ def lib():
             "sd_query_points_device": (C.c_int, [vp, vp, i64, P(_Params), C.c_int, P(_Outputs), vp]),
             "sd_finalize_device": (C.c_int, [vp, vp, vp, i64, P(_Params), vp, vp, vp]),
             "sd_last_launch_count": (C.c_int, [vp, P(i64)]),
+            "sd_set_kernel_timing": (C.c_int, [vp, C.c_int]),
+            "sd_kernel_times": (C.c_int, [vp, vp, i64, P(i64)]),
             "sd_build_weights": (C.c_int, [vp]),
             "sd_weights_info": (C.c_int, [vp, P(f64), P(f64), P(i32), P(i32)]),
             "sd_export_weights": (C.c_int, [vp, vp, vp, vp]),
@@ -338,6 +340,19 @@ class Engine:
         _check(lib().sd_reduce_owned(self.h, C.c_void_p(sbuf_ptr), q_per_owner, n_owned, world, C.byref(params._c()),
                                      C.c_void_p(d_hat_ptr), C.c_void_p(grad_ptr) if grad_ptr else None,
                                      C.c_void_p(stream) if stream else None))
+
+    def set_kernel_timing(self, on: bool = True):
+        """Record a CUDA event pair around the dominant compute launches of
+        every following query call (see sd_set_kernel_timing)."""
+        _check(lib().sd_set_kernel_timing(self.h, 1 if on else 0))
+
+    def kernel_times(self) -> np.ndarray:
+        """Milliseconds of the timed launch groups since the last read (synchronises)."""
+        n = C.c_int64()
+        _check(lib().sd_kernel_times(self.h, None, 0, C.byref(n)))
+        out = np.zeros(n.value, np.float64)
+        _check(lib().sd_kernel_times(self.h, _ptr(out), n.value, C.byref(n)))
+        return out
 
     def last_launch_count(self) -> int:
         n = C.c_int64()

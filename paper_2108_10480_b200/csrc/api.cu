@@ -380,6 +380,7 @@ static void exact_query(Ctx& c, const T* q, int64_t Q, const sd_params& p, const
     const int64_t* perm = sort_queries<T>(c, q, Q, c.scene_lo, c.scene_hi, st, launches, false);
     const double S = p.alpha / std::max(p.alpha, p.alpha_u);
     bool first = true;
+    KernelTimer timer(c, st);
     for (const Segment& s : c.segs) {
         ExactLaunch<T> L;
         L.kind = s.kind;
@@ -411,6 +412,7 @@ static void exact_query(Ctx& c, const T* q, int64_t Q, const sd_params& p, const
         ++launches;
         first = false;
     }
+    timer.stop();
     check_cuda(launch_finalize(part, int(splits), Q, p.alpha, p.epsilon, c.N, nullptr, nullptr, nullptr, perm,
                                   out, st),
                "finalize launch");
@@ -439,8 +441,11 @@ static void dispatch(Ctx& c, const T* q, int64_t Q, const sd_params& p, int mode
         c.last_launches = 0;
         return;
     }
-    if (mode == SD_BVH && c.N > 0) tree_query<T>(c, q, Q, p, out, st);
-    else exact_query<T>(c, q, Q, p, out, st);
+    FinalizeOut o = out;
+    if constexpr (sizeof(T) == 4) o.qf = q;
+    else o.qd = q;
+    if (mode == SD_BVH && c.N > 0) tree_query<T>(c, q, Q, p, o, st);
+    else exact_query<T>(c, q, Q, p, o, st);
 }
 
 // fp64 query points already on the device, converted to the context
@@ -562,6 +567,8 @@ int sd_destroy(sd_ctx* c) {
             if (c->stream) cudaStreamDestroy(c->stream);
             if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
             c->stream = c->copy_stream = nullptr;
+            for (auto& pr : c->ev_pairs) c->ev_pool.insert(c->ev_pool.end(), {pr.first, pr.second});
+            for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
         }
         delete c;
     });
@@ -1333,6 +1340,33 @@ int sd_write_grid_csv(const double* d, const int64_t* leaves, const int64_t* far
             out << buf;
         }
         if (!out) throw ArgError{std::string("write failed: ") + path};
+    });
+}
+
+int sd_set_kernel_timing(sd_ctx* c, int on) {
+    return guard([&] {
+        if (!c) throw ArgError{"ctx is NULL"};
+        c->timing = on != 0;
+    });
+}
+
+int sd_kernel_times(sd_ctx* c, double* ms, int64_t cap, int64_t* n) {
+    return guard([&] {
+        if (!c || !n) throw ArgError{"NULL argument"};
+        DeviceScope ds(c->device);
+        const int64_t k = int64_t(c->ev_pairs.size());
+        *n = k;
+        if (!ms) return;  // count only
+        for (int64_t i = 0; i < k; ++i) {
+            auto [a, b] = c->ev_pairs[size_t(i)];
+            check_cuda(cudaEventSynchronize(b), "cudaEventSynchronize");
+            float t = 0.f;
+            check_cuda(cudaEventElapsedTime(&t, a, b), "cudaEventElapsedTime");
+            if (i < cap) ms[i] = double(t);
+            c->ev_pool.push_back(a);
+            c->ev_pool.push_back(b);
+        }
+        c->ev_pairs.clear();
     });
 }
 

@@ -984,6 +984,7 @@ void tree_query(Ctx& c, const T* q, int64_t Q, const sd_params& p, const Finaliz
         return v == "thread" ? 0 : (v == "packet" ? 1 : 2);
     }();
     int nsplits = 1;
+    KernelTimer timer(c, st);
     if (variant == 2) {
         // few / sparse queries: node-parallel K3F (one warp per query); dense
         // batches: K3 packets (tools/frontier_crossover.py: cfg4, 1k..262k
@@ -1003,6 +1004,7 @@ void tree_query(Ctx& c, const T* q, int64_t Q, const sd_params& p, const Finaliz
         check_cuda(cudaGetLastError(), "traverse kernel");
         ++launches;
     }
+    timer.stop();
     check_cuda(launch_finalize(a.part, nsplits, Q, p.alpha, p.epsilon, 0, a.leaves, a.far, a.hash, perm, out, st),
                "finalize");
     ++launches;

@@ -5,6 +5,7 @@
 
 #include <cstdint>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include <cuda_runtime.h>
@@ -144,6 +145,45 @@ struct Ctx {
     DevBuf qd, qT, part, out_d, out_g, out_c, out_gc, out_l, out_f, out_h;
     DevBuf perm, keys, tmp, tmp2, counters, polys, flag, qbox;
     int64_t last_launches = 0;
+
+    // kernel timing (sd_set_kernel_timing): one event pair on the launching
+    // stream around the dominant compute launches of every query call (the
+    // exact segment launches, or the tree traversal), read back and recycled
+    // by sd_kernel_times
+    bool timing = false;
+    std::vector<cudaEvent_t> ev_pool;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pairs;
+    cudaEvent_t take_event() {
+        cudaEvent_t e = nullptr;
+        if (!ev_pool.empty()) {
+            e = ev_pool.back();
+            ev_pool.pop_back();
+        } else {
+            check_cuda(cudaEventCreate(&e), "cudaEventCreate");
+        }
+        return e;
+    }
+};
+
+// Event pair around the dominant launches of one call (no-op unless the
+// context's kernel timing is on).
+struct KernelTimer {
+    Ctx& c;
+    cudaStream_t st;
+    cudaEvent_t a = nullptr;
+    KernelTimer(Ctx& ctx, cudaStream_t s) : c(ctx), st(s) {
+        if (c.timing) {
+            a = c.take_event();
+            check_cuda(cudaEventRecord(a, st), "cudaEventRecord");
+        }
+    }
+    void stop() {
+        if (!a) return;
+        cudaEvent_t b = c.take_event();
+        check_cuda(cudaEventRecord(b, st), "cudaEventRecord");
+        c.ev_pairs.emplace_back(a, b);
+        a = nullptr;
+    }
 };
 
 // Host helpers shared by api.cu / bvh.cu

@@ -20,9 +20,15 @@ __device__ __forceinline__ void finalize_write(double M, double s, double gx, do
                                                const uint64_t* __restrict__ hash_in, const int64_t* __restrict__ perm,
                                                const FinalizeOut& o) {
     const double scale = M > -INFINITY ? exp2(M) : 0.0;
-    const double c = s * scale;
-    const double cx = gx * scale, cy = gy * scale, cz = gz * scale;
+    double c = s * scale;
+    double cx = gx * scale, cy = gy * scale, cz = gz * scale;
     const int64_t j = perm ? perm[i] : i;  // tree path: undo the query sort
+    if (o.qf || o.qd) {
+        const double x = o.qf ? double(o.qf[3 * j]) : o.qd[3 * j];
+        const double y = o.qf ? double(o.qf[3 * j + 1]) : o.qd[3 * j + 1];
+        const double z = o.qf ? double(o.qf[3 * j + 2]) : o.qd[3 * j + 2];
+        if (isnan(x) || isnan(y) || isnan(z)) c = cx = cy = cz = NAN;
+    }
     if (o.peers) {  // fused exchange: NVLink stores into the owner's buffer
         const int64_t ow = j / o.peer_qown, k = j - ow * o.peer_qown;
         double* dst = o.peers[ow] + size_t(o.peer_rank) * 4 * o.peer_qown + k;
@@ -36,7 +42,7 @@ __device__ __forceinline__ void finalize_write(double M, double s, double gx, do
         return;
     }
     double d = INFINITY, ax = 0, ay = 0, az = 0;
-    if (c > 0.0) {
+    if (!(c <= 0.0)) {  // c > 0, or NaN (propagates like the reference's -log(NaN))
         d = -log(c) / alpha;
         const double den = c + eps;
         ax = cx / den;

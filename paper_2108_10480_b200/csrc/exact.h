@@ -54,6 +54,12 @@ struct FinalizeOut {
     double* const* peers = nullptr;
     int peer_rank = 0;
     int64_t peer_qown = 0;
+    // the batch's query points (context precision, input order): a query
+    // with a NaN coordinate reports NaN d_hat / grad / c / grad_c, as the
+    // reference's exp(NaN) does (the kernels mask NaN distances like
+    // overflowed ones, so the NaN is restored here)
+    const float* qf = nullptr;
+    const double* qd = nullptr;
 };
 
 cudaError_t launch_finalize(const double* part, int splits, int64_t Q, double alpha, double epsilon,

@@ -542,7 +542,10 @@ int launch_pair_traversal(Ctx& c, DeviceTree& t, TraverseArgs<T>& a, bool hash, 
                               : (hash ? pair_kernel<T, VIS, true, 0> : pair_kernel<T, VIS, false, 0>);
     if constexpr (VIS::kLeafBatch) {  // SDGPU_LEAF_BATCH = 1 turns leaf batching on (off: profiles/README.md)
         const char* lb = std::getenv("SDGPU_LEAF_BATCH");
+        // the leaf list sits after defer_cap deferred entries per warp
+        // (pair_walk): the two modes are exclusive, so defer_cap is 0 here
         if (!defer && lb && *lb == '1') {
+            if (a.defer_cap != 0) throw std::logic_error("leaf batching with a deferred list");
             smem += size_t(kLeafBatch) * (kTravThreads / 32) * sizeof(int2);
             kern = k > 0 ? (hash ? pair_kernel<T, VIS, true, 1, true> : pair_kernel<T, VIS, false, 1, true>)
                          : (hash ? pair_kernel<T, VIS, true, 0, true> : pair_kernel<T, VIS, false, 0, true>);

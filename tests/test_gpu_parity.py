@@ -282,9 +282,13 @@ def test_config4_tree_parity_subset(sd, oracle, builder, kernel, monkeypatch):
     this batch size, K3 the one the full-size bench runs)."""
     O = oracle
     monkeypatch.setenv("SDGPU_FRONTIER", "1" if kernel == "K3F" else "0")
-    if kernel in ("K3D", "K3LB"):  # the unsplit packet walk (the full-size default); K3LB: batched leaf terms
+    if kernel in ("K3D", "K3LB"):
+        # the unsplit packet walk (the full-size kernel); K3D with deferred
+        # per-lane tails (entries of <= 4 lanes), K3LB with batched leaf terms
         monkeypatch.setenv("SDGPU_SPLIT", "0")
         monkeypatch.setenv("SDGPU_LEAF_BATCH", "1" if kernel == "K3LB" else "0")
+        monkeypatch.setenv("SDGPU_DEFER", "4" if kernel == "K3D" else "0")
+        monkeypatch.setenv("SDGPU_DEFER_CAP", "64")
     m, q = _cfg(O, 4, 512, 0)
     w = O.Weights.build(m)
     if builder == "median":
@@ -303,6 +307,41 @@ def test_config4_tree_parity_subset(sd, oracle, builder, kernel, monkeypatch):
     assert_close(got, ref, 0, 200.0, "cfg4 bvh")
     ex = e.smooth_min_dist_flat(q[:64], sd.SmoothParams(alpha=200.0, beta=0.0))
     assert (got.d_hat[:64] <= ex.d_hat + 1e-5).all()
+
+
+@pytest.mark.parametrize("kernel", ["K3", "K3F"])
+def test_config4_parity_65536_queries(sd, oracle, kernel, monkeypatch):
+    """cfg4 at the scale BASELINE configs[3] names for its exact comparison:
+    65,536 queries (32,768 from each half of the distribution), the median
+    tree built on the GPU and exported to the oracle. Every query's decision
+    hash and counters equal the oracle's; d_hat / grad within the fp32
+    tolerance in both forms (max(1, |ref|) and the strict relative form
+    with a 1/alpha floor); Barnes-Hut below exact + 1e-5 on every query
+    (acceptance [1], T/acceptance.cpp:76-115). K3 = the packet walk of the
+    full-size batch, K3F = the node-parallel kernel this batch size picks
+    by default."""
+    O = oracle
+    monkeypatch.setenv("SDGPU_FRONTIER", "1" if kernel == "K3F" else "0")
+    monkeypatch.setenv("SDGPU_SPLIT", "0")
+    m = O.config_mesh(4).quantized()
+    qa = O.config_queries(4, m, 1 << 17)
+    q = np.concatenate([qa[:32768], qa[65536:65536 + 32768]]).astype(np.float32).astype(np.float64)
+    w = O.Weights.build(m)
+    e = engine_for(sd, O, m, w, 0)
+    e.build_bvh(sd.SD_BVH_MEDIAN)
+    t = O.Tree.from_nodes(e.export_bvh())
+    P = sd.SmoothParams(alpha=200.0, beta=0.5)
+    got = e.smooth_min_dist(q, P)
+    ref = O.query(m, w, q, O.Params(alpha=200.0, beta=0.5), tree=t)
+    assert (got.decision_hash == ref.decision_hash).all()
+    assert (got.leaves == ref.leaves).all() and (got.far_field == ref.far_field).all()
+    assert_close(got, ref, 0, 200.0, "cfg4 65536")
+    fin = np.isfinite(ref.d_hat)
+    strict = np.abs(got.d_hat[fin] - ref.d_hat[fin]) / np.maximum(np.abs(ref.d_hat[fin]), 1.0 / 200.0)
+    assert strict.max() <= 1e-5, strict.max()
+    ex = e.smooth_min_dist_flat(q, sd.SmoothParams(alpha=200.0, beta=0.0))
+    both = np.isfinite(ex.d_hat) & fin
+    assert (got.d_hat[both] <= ex.d_hat[both] + 1e-5).all()
 
 
 # ---------------------------------------------- full-size properties
@@ -883,3 +922,25 @@ def test_huge_query_coordinates_underflow_like_the_reference(sd, oracle, prec):
         assert not got.grad[-4:].any() and not np.isnan(got.grad).any()
         assert (got.leaves == ref.leaves).all() and (got.far_field == ref.far_field).all()
         assert_close(got, ref, prec, 100.0, f"huge coords beta {beta}")
+
+
+@pytest.mark.parametrize("prec", [0, 1])
+def test_nan_query_coordinates_propagate_like_the_reference(sd, oracle, prec):
+    """A query with a NaN coordinate gives NaN d_hat and gradient, as the
+    reference's exp(NaN) does (c = NaN skips the c <= 0 branch of
+    result_from_accum, smooth.hpp:151-157); exact and BVH, device and host
+    entry points; the other queries of the batch are unaffected."""
+    O = oracle
+    m0 = O.random_scene(6, 200)
+    qs = np.concatenate([O.QueryStream(56).draw_points(m0, 40), [[np.nan, 0.0, 0.0], [0.1, 0.2, np.nan]]])
+    m, q = prep(O, m0, qs, prec)
+    w, t = O.Weights.build(m), O.Tree.build(m)
+    e = engine_for(sd, O, m, w, prec, tree=t)
+    for beta in (0.0, 0.5):
+        p = O.Params(alpha=100.0, beta=beta)
+        ref = O.query(m, w, q[:-2], p, tree=t if beta > 0 else None)
+        got = e.smooth_min_dist(q, sd.SmoothParams(alpha=100.0, beta=beta)) if beta > 0 else \
+            e.smooth_min_dist_flat(q, sd.SmoothParams(alpha=100.0, beta=0.0))
+        assert np.isnan(got.d_hat[-2:]).all() and np.isnan(got.grad[-2:]).all()
+        sub = type(got)(got.d_hat[:-2], got.grad[:-2])
+        assert_close(sub, ref, prec, 100.0, f"nan batch beta {beta}")
