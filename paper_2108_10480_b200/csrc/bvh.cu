@@ -579,7 +579,7 @@ __device__ __forceinline__ void merge_partial(Acc<T>& acc, T m, T s, T gx, T gy,
 // 185-187): fp32 decides outside a 1e-5 relative band, fp64 re-decides in
 // the reference rounding inside it. On "far" also returns d_B, 1/d_B and
 // q - y_B for the far-field term.
-template <class T>
+template <class T, bool NEED_D = true>
 __device__ __forceinline__ bool point_far(const TraverseArgs<T>& a, const NodeT<T>& b, int32_t id, T qx, T qy, T qz,
                                           T& d, T& r, T& dx, T& dy, T& dz, unsigned long long& nre) {
     const T yx = fmin(fmax(qx, b.v[0]), b.v[4]);
@@ -601,7 +601,7 @@ __device__ __forceinline__ bool point_far(const TraverseArgs<T>& a, const NodeT<
             far = decide64(b, a.diam64[id], double(qx), double(qy), double(qz), a.beta64);
             ++nre;
         }
-        if (far) {  // s = 0 only for an fp64-confirmed box that the fp32 box contains; then dx = dy = dz = 0
+        if (NEED_D && far) {  // s = 0 only for an fp64-confirmed box that the fp32 box contains; then dx = dy = dz = 0
             r = Math<T>::rsqrt(fmax(s, T(1e-30)));
             d = s * r;
         }
@@ -617,7 +617,7 @@ __device__ __forceinline__ bool point_far(const TraverseArgs<T>& a, const NodeT<
             far = decide64(b, a.diam64[id], double(qx), double(qy), double(qz), a.beta64);
             ++nre;
         }
-        if (far) {
+        if (NEED_D && far) {
             r = Math<double>::rsqrt(s);
             d = s * r;
         }
@@ -651,6 +651,7 @@ __device__ __forceinline__ bool visit(const TraverseArgs<T>& a, const Poly<T>* p
 template <class T>
 struct PointVisit {
     static constexpr bool kLeafBatch = true;
+    static constexpr bool kLeafQueue = true;
     T qx, qy, qz;
     __device__ __forceinline__ void load(const TraverseArgs<T>& a, int64_t qi, bool valid) {
         qx = valid ? a.q[3 * qi] : T(0);
@@ -662,6 +663,50 @@ struct PointVisit {
                                           int32_t id, T lgc, Acc<T>& acc, CNT& nleaf, CNT& nfar, uint64_t& h,
                                           unsigned long long& nre) const {
         return sdgpu::visit<T, HASH, CNT>(a, polys, b, id, lgc, qx, qy, qz, acc, nleaf, nfar, h, nre);
+    }
+    // K3Q node test: a far-field node appends (q - y_B, log2 n_B) to this
+    // lane's far queue, an exact leaf its slot to the leaf queue; both are
+    // counted and hashed here, where the reference decides them (the terms
+    // come in far_round / leaf_round).
+    template <bool HASH, bool FARQ, class CNT>
+    __device__ __forceinline__ bool visit_q(const TraverseArgs<T>& a, const NodeT<T>& b, int32_t id, T lgc,
+                                            Acc<T>& acc, CNT& nleaf, CNT& nfar, uint64_t& h,
+                                            unsigned long long& nre, uint32_t lq0, int& nq, uint32_t fq0,
+                                            int& nf) const {
+        int32_t link;
+        memcpy(&link, &b.v[7], sizeof(int32_t));
+        {  // beta = 0 when there is no Barnes-Hut (see visit)
+            T d, r, dx, dy, dz;
+            if (point_far<T, !FARQ>(a, b, id, qx, qy, qz, d, r, dx, dy, dz, nre)) {
+                if constexpr (FARQ) {
+                    FarQ<T>::push(fq0, nf, dx, dy, dz, lgc);
+                    ++nf;
+                } else {
+                    far_term(a.ph, lgc + a.lw_ff, d, r, dx, dy, dz, acc);
+                }
+                ++nfar;
+                if constexpr (HASH) h += decision_mix(uint64_t(id), 1);
+                return false;
+            }
+        }
+        if (link >= 0) return true;
+        asm volatile("st.shared.s32 [%0], %1;" ::"r"(lq0 + uint32_t(nq) * kLeafStride), "r"(-link - 1) : "memory");
+        ++nq;
+        ++nleaf;
+        if constexpr (HASH) h += decision_mix(uint64_t(id), 2);
+        return false;
+    }
+    // one queued far-field term (smooth.hpp:67-75) of this lane
+    __device__ __forceinline__ void far_round(const TraverseArgs<T>& a, uint32_t fq0, int k, Acc<T>& acc) const {
+        T dx, dy, dz, lg;
+        FarQ<T>::pop(fq0, k, dx, dy, dz, lg);
+        const T s = fma(dx, dx, fma(dy, dy, dz * dz));
+        const T r = Math<T>::rsqrt(fmax(s, Tiny<T>::v));
+        far_term(a.ph, lg + a.lw_ff, s * r, r, dx, dy, dz, acc);
+    }
+    __device__ __forceinline__ void leaf_round(const TraverseArgs<T>& a, const Poly<T>* polys, int slot,
+                                               Acc<T>& acc) const {
+        leaf_term<T>(a, polys, slot, qx, qy, qz, acc);
     }
     template <bool HASH, class CNT>
     __device__ __forceinline__ bool far_test(const TraverseArgs<T>& a, const NodeT<T>& b, int32_t id, T lgc, bool emit,

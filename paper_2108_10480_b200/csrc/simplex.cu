@@ -595,6 +595,7 @@ __device__ __forceinline__ Geom load_query(const double* qg, const int32_t* qd, 
 // K3's per-lane query for simplex queries.
 struct SimplexVisit {
     static constexpr bool kLeafBatch = false;  // per-lane QP leaves: no batched flush
+    static constexpr bool kLeafQueue = false;  // (nor deferred leaf queues)
     sx::Geom g;
     __device__ __forceinline__ void load(const TraverseArgs<double>& a, int64_t qi, bool valid) {
         g = sx::load_query(a.qgeom, a.qdim, qi, valid);

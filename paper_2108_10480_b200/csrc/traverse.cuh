@@ -63,6 +63,8 @@ struct TraverseArgs {
     // pre-order subtree, the popcount threshold and the per-warp capacity
     const int32_t* esc = nullptr;
     int defer_t = 0, defer_cap = 0;
+    // K3Q queue capacities (entries per lane): exact leaves, far-field terms
+    int lq_cap = 0, fq_cap = 0;
 };
 
 constexpr int kTravThreads = 128;
@@ -348,6 +350,184 @@ __global__ void __launch_bounds__(kTravThreads, sizeof(T) == 4 ? 8 : 4)
     pair_walk<T, VIS, HASH, 0, true>(a);
 }
 
+// K3Q (default for dense point batches): the child-pair packet walk with
+// per-lane DEFERRED EXACT LEAVES. Inline, a leaf child costs the warp the
+// ~190-instruction triangle term for the ~3 lanes that reach it. Here a lane
+// that reaches an exact leaf counts and hashes it at once (the decision is
+// the reference's, made where the reference makes it) but only appends the
+// leaf slot to its own shared-memory queue (kLeafQ entries per lane, lane-
+// interleaved: entry k of a lane at [k][lane], conflict-free); the terms
+// are evaluated in ROUNDS in which every lane with a pending entry pops one
+// and adds its own term to its own accumulator -- no shuffles, each lane's
+// query and shift stay in registers. A round runs when some lane's queue
+// could overflow on the next step (>= kLeafQ - 1 pending; a step adds at
+// most two) and the queues are drained after the walk. Per lane the set of
+// terms is exactly collect_contributions'; only their summation order
+// changes (fp32 rounding).
+constexpr int kLeafQ = 16;  // default leaf queue entries per lane (SDGPU_LEAFQ)
+constexpr int kFarQ = 0;    // default far-field queue entries per lane (SDGPU_FARQ; 0 = far terms inline)
+constexpr uint32_t kLeafStride = kTravThreads * 4;  // bytes between a lane's leaf entries
+
+// Far queue entry (q - y_B, log2 n_B): 4 T per entry, lane-interleaved
+// ([k][128 threads]) so that a warp's accesses are contiguous.
+template <class T>
+struct FarQ;
+template <>
+struct FarQ<float> {
+    static constexpr uint32_t kStride = kTravThreads * 16;  // bytes between a lane's entries
+    __device__ __forceinline__ static void push(uint32_t q0, int k, float x, float y, float z, float w) {
+        asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(q0 + uint32_t(k) * kStride), "f"(x), "f"(y),
+                     "f"(z), "f"(w) : "memory");
+    }
+    __device__ __forceinline__ static void pop(uint32_t q0, int k, float& x, float& y, float& z, float& w) {
+        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(x), "=f"(y), "=f"(z), "=f"(w)
+                     : "r"(q0 + uint32_t(k) * kStride));
+    }
+};
+template <>
+struct FarQ<double> {
+    static constexpr uint32_t kStride = kTravThreads * 32;
+    __device__ __forceinline__ static void push(uint32_t q0, int k, double x, double y, double z, double w) {
+        const uint32_t p = q0 + uint32_t(k) * kStride;
+        asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(p), "d"(x), "d"(y) : "memory");
+        asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(p + 16), "d"(z), "d"(w) : "memory");
+    }
+    __device__ __forceinline__ static void pop(uint32_t q0, int k, double& x, double& y, double& z, double& w) {
+        const uint32_t p = q0 + uint32_t(k) * kStride;
+        asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(x), "=d"(y) : "r"(p));
+        asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(z), "=d"(w) : "r"(p + 16));
+    }
+};
+template <class T>
+__host__ __device__ constexpr size_t farq_bytes(int cap) {
+    return size_t(cap) * kTravThreads * 4 * sizeof(T);
+}
+
+template <class T, class VIS, bool HASH, bool FARQ>
+__device__ __forceinline__ void pair_walk_q(const TraverseArgs<T>& a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    Poly<T>* polys = reinterpret_cast<Poly<T>*>(smem_raw);
+    int4* stacks = reinterpret_cast<int4*>(smem_raw + poly_bytes<T>(a.npoly));
+    int32_t* lqs = reinterpret_cast<int32_t*>(stacks + (kTravThreads / 32) * a.stack_depth);
+    unsigned char* fqs = reinterpret_cast<unsigned char*>(lqs + a.lq_cap * kTravThreads);  // 16-B aligned
+    for (int i = threadIdx.x; i < a.npoly * kPolyCoefs; i += blockDim.x)
+        reinterpret_cast<T*>(polys)[i] = reinterpret_cast<const T*>(a.polys)[i];
+    __syncthreads();
+
+    constexpr unsigned FULL = 0xffffffffu;
+    const unsigned lane = threadIdx.x & 31u;
+    const unsigned lanebit = 1u << lane;
+    const unsigned warp = threadIdx.x >> 5;
+    int4* st = stacks + warp * a.stack_depth;
+    const uint32_t lq0 = smem_u32(lqs + threadIdx.x);  // this lane's entry 0 (entries kLeafStride apart)
+    const int lcap = a.lq_cap - 1, fcap = a.fq_cap - 1;  // a step appends at most two entries per lane
+    const uint32_t fq0 = smem_u32(fqs) + threadIdx.x * 4 * uint32_t(sizeof(T));
+    int nq = 0, nf = 0;  // pending leaf / far-field entries of this lane
+    const int64_t packet = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t i = packet * 32 + lane;
+    const bool valid = i < a.Q;
+    const int64_t qi = valid ? (a.perm ? a.perm[i] : i) : 0;
+    VIS qv;
+    qv.load(a, qi, valid);
+    unsigned mask = __ballot_sync(FULL, valid);
+    if (mask == 0u) return;
+    Acc<T> acc;
+    acc.init();
+    int32_t nleaf = 0, nfar = 0;  // per query: < 2^31 nodes
+    uint64_t h = 0;
+    unsigned long long nre = 0;
+    int32_t cur = 0, cur_link;
+    memcpy(&cur_link, &a.box[0].v[7], sizeof(int32_t));
+    {  // the root is popped alone
+        const NodeT<T> b0 = a.box[0];
+        const bool d = valid && qv.template visit_q<HASH, FARQ>(a, b0, 0, a.lgcount[0], acc, nleaf, nfar, h, nre, lq0,
+                                                                 nq, fq0, nf);
+        mask = __ballot_sync(FULL, d);
+    }
+    auto round = [&]() {
+        if (nq > 0) {
+            --nq;
+            int slot;
+            asm volatile("ld.shared.s32 %0, [%1];" : "=r"(slot) : "r"(lq0 + uint32_t(nq) * kLeafStride));
+            qv.leaf_round(a, polys, slot, acc);
+        }
+    };
+    auto fround = [&]() {
+        if constexpr (FARQ) {
+            if (nf > 0) qv.far_round(a, fq0, --nf, acc);
+        }
+    };
+    const uint32_t st0 = smem_u32(st);
+    uint32_t top = st0;
+    while (mask) {
+        const int32_t lid = cur + 1, rid = cur_link;
+        const PairT<T>& pr = a.pairs[uint32_t(cur)];  // warp-uniform: broadcast loads
+        const NodeT<T> bl = pr.l, br = pr.r;
+        const T lgl = pr.lgc[0], lgr = pr.lgc[1];
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(&pr + 1));  // = a.pairs + lid
+        bool dl = false, dr = false;
+        if (mask & lanebit) {
+            dl = qv.template visit_q<HASH, FARQ>(a, bl, lid, lgl, acc, nleaf, nfar, h, nre, lq0, nq, fq0, nf);
+            dr = qv.template visit_q<HASH, FARQ>(a, br, rid, lgr, acc, nleaf, nfar, h, nre, lq0, nq, fq0, nf);
+        }
+        const unsigned DL = __ballot_sync(FULL, dl), DR = __ballot_sync(FULL, dr);
+        int32_t llink, rlink;
+        memcpy(&llink, &bl.v[7], sizeof(int32_t));
+        memcpy(&rlink, &br.v[7], sizeof(int32_t));
+        if (DL) {
+            if (DR) {
+                if (lane == 0) st_shared_int4(top, rid, rlink, int(DR));
+                __syncwarp();
+                top += 16;
+            }
+            cur = lid;
+            cur_link = llink;
+            mask = DL;
+        } else if (DR) {
+            cur = rid;
+            cur_link = rlink;
+            mask = DR;
+        } else if (top != st0) {
+            top -= 16;
+            const int4 e = ld_shared_int4(top);
+            cur = e.x;
+            cur_link = e.y;
+            mask = unsigned(e.z);
+        } else {
+            mask = 0u;
+        }
+        if constexpr (FARQ) {
+            if (__any_sync(FULL, nq >= lcap || nf >= fcap)) {
+                while (__any_sync(FULL, nf >= fcap)) fround();
+                while (__any_sync(FULL, nq >= lcap)) round();
+            }
+        } else {
+            while (__any_sync(FULL, nq >= lcap)) round();
+        }
+    }
+    if constexpr (FARQ) {
+        while (__any_sync(FULL, nf > 0)) fround();
+    }
+    while (__any_sync(FULL, nq > 0)) round();
+    if (!valid) return;
+    Tot tot;
+    tot.init();
+    tot.flush(acc);
+    a.part[i] = tot.M;
+    a.part[a.Q + i] = tot.s;
+    a.part[2 * a.Q + i] = tot.gx;
+    a.part[3 * a.Q + i] = tot.gy;
+    a.part[4 * a.Q + i] = tot.gz;
+    a.leaves[i] = nleaf;
+    a.far[i] = nfar;
+    if (HASH) a.hash[i] = h;
+}
+
+template <class T, class VIS, bool HASH, bool FARQ>
+__global__ void __launch_bounds__(kTravThreads) pair_kernel_q(const __grid_constant__ TraverseArgs<T> a) {
+    pair_walk_q<T, VIS, HASH, FARQ>(a);
+}
+
 // K3F (few queries, node-parallel): a group of G lanes per query (32 / G
 // queries per warp); the lanes of a group test up to G nodes of their
 // query's walk at once. A group pops the top G (or fewer) entries of its
@@ -549,6 +729,26 @@ int launch_pair_traversal(Ctx& c, DeviceTree& t, TraverseArgs<T>& a, bool hash, 
             smem += size_t(kLeafBatch) * (kTravThreads / 32) * sizeof(int2);
             kern = k > 0 ? (hash ? pair_kernel<T, VIS, true, 1, true> : pair_kernel<T, VIS, false, 1, true>)
                          : (hash ? pair_kernel<T, VIS, true, 0, true> : pair_kernel<T, VIS, false, 0, true>);
+        }
+    }
+    if constexpr (VIS::kLeafQueue) {  // SDGPU_LEAF_QUEUE = 0 turns the deferred leaf queues off (A/B)
+        // SDGPU_LEAFQ / SDGPU_FARQ: queue entries per lane (>= 3 to be used;
+        // SDGPU_FARQ < 3 keeps the far-field terms inline)
+        auto cap = [](const char* name, int dflt) {
+            const char* e = std::getenv(name);
+            return e && *e ? std::max(0, std::min(64, std::atoi(e))) : dflt;
+        };
+        const char* lqe = std::getenv("SDGPU_LEAF_QUEUE");
+        const bool lq_on = !(lqe && *lqe == '0');
+        const char* lb = std::getenv("SDGPU_LEAF_BATCH");
+        a.lq_cap = cap("SDGPU_LEAFQ", kLeafQ);
+        a.fq_cap = cap("SDGPU_FARQ", kFarQ);
+        if (a.lq_cap < 3) a.lq_cap = 3;
+        if (a.fq_cap < 3) a.fq_cap = 0;
+        if (lq_on && k == 0 && !defer && !(lb && *lb == '1')) {
+            smem += size_t(a.lq_cap) * kTravThreads * sizeof(int32_t) + farq_bytes<T>(a.fq_cap);
+            kern = a.fq_cap ? (hash ? pair_kernel_q<T, VIS, true, true> : pair_kernel_q<T, VIS, false, true>)
+                            : (hash ? pair_kernel_q<T, VIS, true, false> : pair_kernel_q<T, VIS, false, false>);
         }
     }
     check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)), "smem attr");
