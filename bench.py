@@ -362,6 +362,34 @@ def oracle_objects(v, s, k, wt, nodes=None):
     return O, m, ws, t
 
 
+class CpuArm:
+    """The CPU implementation of the path timed beside ours: the reference
+    itself (oracle/_ref: its unmodified headers compiled with the Eigen
+    shim; kind "reference") when that library is present, else the oracle
+    restatement (kind "port"). The WeightSet table is fed in (the shim has
+    no SVD for the triangle polynomials); the tree is given or built."""
+
+    def __init__(self, v, s, k, wt, nodes=None, build_tree=False):
+        from oracle import reference as R
+        self.threads = os.cpu_count() or 1
+        if R.available():
+            self.kind = "reference"
+            self.sc = R.Scene(v, s, k, wt)
+            if nodes is not None or build_tree:
+                self.sc.set_bvh(nodes)
+            self.run = lambda q, p, tree: self.sc.query(q, p, tree=tree, threads=self.threads)
+        else:
+            O, m, ws, t = oracle_objects(v, s, k, wt, nodes)
+            if build_tree and t is None:
+                t = O.Tree.build(m)
+            self.kind, self.threads = "port", O.hardware_threads()
+            self.run = lambda q, p, tree: O.query(m, ws, q, p, tree=t if tree else None, threads=self.threads)
+
+    def query(self, q, alpha, alpha_u=600.0, beta=0.0, tree=False):
+        import oracle as O
+        return self.run(np.ascontiguousarray(q), O.Params(alpha=alpha, alpha_u=alpha_u, beta=beta), tree)
+
+
 # ------------------------------------------------------------- parity
 def parity_stats(got_d, got_g, ref_d, ref_g, alpha, dtype):
     """Both tolerance forms of north_star's relative bound on the same pairs:
@@ -447,16 +475,14 @@ def exact_leg(run, eng, q, prec, N, kind, P, steps, warmup, flush, stream, peaks
     return out, d_hat.cpu().numpy(), grad.cpu().numpy()
 
 
-def cpu_exact_sample(v, s, k, wt, q, alpha, threads, target_s):
-    """The oracle port on a bounded prefix of the queries, sized by a pilot
-    so the sample takes about target_s seconds."""
-    O, m, w, _ = oracle_objects(v, s, k, wt)
-    p = O.Params(alpha=alpha, alpha_u=600.0, beta=0.0)
-    pilot = max(threads * 2, 32)
-    r = O.query(m, w, q[:pilot], p, threads=threads)
+def cpu_exact_sample(arm, q, alpha, target_s):
+    """The CPU arm on a bounded prefix of the queries, sized by a pilot so
+    the sample takes about target_s seconds."""
+    pilot = max(arm.threads * 2, 32)
+    arm.query(q[:pilot], alpha)  # first touch of the scene
+    r = arm.query(q[:pilot], alpha)
     n = int(min(len(q), max(pilot, pilot * target_s / max(r.seconds, 1e-3))))
-    r = O.query(m, w, q[:n], p, threads=threads)
-    return n, r
+    return n, arm.query(q[:n], alpha)
 
 
 def run_exact_headline(args, run, peaks, stream, flush, line):
@@ -505,10 +531,11 @@ def run_exact_headline(args, run, peaks, stream, flush, line):
             par[f"cfg3_alpha{alpha:g}"] = parity_stats(d[idx], g[idx], ref.d_hat, ref.grad, alpha, "f32")
             par[f"cfg3_alpha{alpha:g}"]["sample"] = f"{nq} evenly spaced timed queries of rank 0's block"
         if world == 1:
-            n, r = cpu_exact_sample(v3, t3, k3, wt3, qb, 100.0, threads, 10.0)
-            line["cpu_baseline"] = {"value": n * N3 / r.seconds, "unit": "pair-evals/s", "cores": threads,
-                                    "kind": "port", "sample": f"first {n} of {len(qb)} cfg3 queries x {N3} "
-                                    f"triangles, alpha 100 ({r.seconds:.1f} s, fp64 oracle port)"}
+            arm = CpuArm(v3, t3, k3, wt3)
+            n, r = cpu_exact_sample(arm, qb, 100.0, 10.0)
+            line["cpu_baseline"] = {"value": n * N3 / r.seconds, "unit": "pair-evals/s", "cores": arm.threads,
+                                    "kind": arm.kind, "sample": f"first {n} of {len(qb)} cfg3 queries x {N3} "
+                                    f"triangles, alpha 100 ({r.seconds:.1f} s, fp64, {arm.kind})"}
     line.update({"metric": "exact pair-evals/s (value+grad)", "value": head["value"], "unit": "pair-evals/s",
                  "ms_per_step": head["ms_per_step"], "dtype": "f32",
                  "config": {"workload": "cfg3: torus R=1 r=0.3, 512x256 grid (262,144 triangles), vertex jitter, "
@@ -544,9 +571,10 @@ def run_exact_headline(args, run, peaks, stream, flush, line):
     if rank == 0 and not args.no_cpu:
         # the oracle port on a ~7 s prefix of the timed cfg2 queries: the cfg2
         # cpu baseline at the reference's precision and the parity reference
-        n, r = cpu_exact_sample(v2, w2.simplices, w2.kinds, wt2, qb2, 100.0, threads, 7.0)
-        cpu2 = {"value": n * N2 / r.seconds, "unit": "pair-evals/s", "cores": threads, "kind": "port",
-                "sample": f"first {n} of {len(qb2)} cfg2 queries x {N2} edges ({r.seconds:.1f} s, fp64 oracle port)"}
+        arm = CpuArm(v2, w2.simplices, w2.kinds, wt2)
+        n, r = cpu_exact_sample(arm, qb2, 100.0, 7.0)
+        cpu2 = {"value": n * N2 / r.seconds, "unit": "pair-evals/s", "cores": arm.threads, "kind": arm.kind,
+                "sample": f"first {n} of {len(qb2)} cfg2 queries x {N2} edges ({r.seconds:.1f} s, fp64, {arm.kind})"}
         for prec, key, dt in ((sd.SD_FP32, "exact_cfg2", "f32"), (sd.SD_FP64, "exact_cfg2_fp64", "f64")):
             d, g = res2[prec]
             par[key] = parity_stats(d[:n], g[:n], r.d_hat, r.grad, 100.0, dt)
@@ -720,9 +748,15 @@ def bvh_parity(eng, v, w, wt, qb, counted, got_d, got_g, P, full_batch, n_sample
            "far_field_mismatch": int((cf[idx] != ref.far_field).sum()),
            "timed_equals_counted_run": bool(np.array_equal(cd[idx], got_d[idx], equal_nan=True))}
     out.update(parity_stats(got_d[idx], got_g[idx], ref.d_hat, ref.grad, P.alpha, "f32"))
-    out["cpu_baseline"] = {"value": len(idx) / ref.seconds, "unit": "queries/s", "cores": threads, "kind": "port",
+    arm = CpuArm(v, w.simplices, w.kinds, wt, nodes=eng.export_bvh())
+    rr = arm.query(qb[idx], P.alpha, P.alpha_u, P.beta, tree=True)
+    if arm.kind == "reference":  # the oracle restatement against the reference itself on the same sample
+        out["oracle_equals_reference"] = bool(all(np.array_equal(getattr(ref, f), getattr(rr, f), equal_nan=True)
+                                                  for f in ("d_hat", "grad", "leaves", "far_field")))
+    out["cpu_baseline"] = {"value": len(idx) / rr.seconds, "unit": "queries/s", "cores": arm.threads,
+                           "kind": arm.kind,
                            "sample": f"{len(idx)} cfg4 queries (both halves) on the exported GPU-built tree, "
-                                     f"fp64 oracle port, {ref.seconds:.2f} s"}
+                                     f"fp64, {arm.kind}, {rr.seconds:.2f} s"}
     # Barnes-Hut vs exact on the same queries (GPU exact, checked below)
     ex = eng.query_points(qb[idx], sd.SmoothParams(alpha=P.alpha, alpha_u=P.alpha_u, beta=0.0), sd.SD_EXACT)
     fin = np.isfinite(ex.d_hat) & np.isfinite(got_d[idx])
@@ -770,28 +804,31 @@ def run_ours(args, rank, world, local):
 # ------------------------------------------------------ reference arm
 def run_reference(args, rank, world):
     """The reference's own CPU path, on our headline's config, metric and
-    unit: the oracle port (fp64, all host threads) builds the cfg3 WeightSet
-    the reference way and evaluates a bounded query sample per step; the
-    `bvh` object does the same for cfg4 on the host-built median tree."""
+    unit: the reference itself (oracle/_ref, its unmodified headers
+    compiled with the Eigen shim; else the oracle port), fp64, on all host
+    threads, a bounded query sample per step. The cfg3 WeightSet is the
+    reference construction restated by the oracle (the shim has no SVD);
+    the `bvh` object does the same for cfg4 on the reference's own
+    build_bvh tree."""
     if rank != 0:
         return
     import oracle as O
     O.build()
-    threads = O.hardware_threads()
     v3, t3, k3, q3 = cfg3_workload()
     m = O.Mesh.from_arrays(v3, t3, k3)
-    ws = O.Weights.build(m)
-    p = O.Params(alpha=100.0, alpha_u=600.0, beta=0.0)
+    wt = O.Weights.build(m).table
+    arm = CpuArm(v3, t3, k3, wt)
     N = len(k3)
-    pilot = max(threads * 2, 32)
-    r = O.query(m, ws, q3[:pilot], p, threads=threads)
+    pilot = max(arm.threads * 2, 32)
+    arm.query(q3[:pilot], 100.0)  # first touch of the scene
+    r = arm.query(q3[:pilot], 100.0)
     n = int(min(len(q3), max(pilot, pilot * 2.0 / max(r.seconds, 1e-3))))  # ~2 s per step
     for i in range(args.warmup):
-        O.query(m, ws, q3[:n], p, threads=threads)
+        arm.query(q3[:n], 100.0)
     times = []
     for i in range(args.steps):
         lo = (i * n) % max(1, len(q3) - n)
-        times.append(O.query(m, ws, q3[lo:lo + n], p, threads=threads).seconds)
+        times.append(arm.query(q3[lo:lo + n], 100.0).seconds)
     t = float(np.mean(times))
     value = n * N / t
     line = {
@@ -801,20 +838,24 @@ def run_reference(args, rank, world):
         "data": "synthetic (seeded generators of BASELINE configs[1..3])",
         "config": {"workload": "cfg3: torus 262,144 triangles, 1,048,576 queries, exact LSE, alpha=100 "
                                "(BASELINE configs[2]); a bounded sample of the batch per step",
-                   "queries_per_step": n, "primitives": N, "parallelism": f"{threads} host threads"},
-        "cpu_baseline": {"value": value, "unit": "pair-evals/s", "cores": threads, "kind": "port",
+                   "queries_per_step": n, "primitives": N, "parallelism": f"{arm.threads} host threads",
+                   "implementation": ("the reference's smooth_min_dist_flat (smooth.hpp:189-198) batched by its "
+                                      "parallel_for, unmodified headers compiled with an Eigen-subset shim "
+                                      "(oracle/_ref)") if arm.kind == "reference" else
+                                     "the oracle's fp64 restatement of the reference (oracle/)"},
+        "cpu_baseline": {"value": value, "unit": "pair-evals/s", "cores": arm.threads, "kind": arm.kind,
                          "sample": f"{n} of {len(q3)} cfg3 queries x {N} triangles per step"},
         "e2e": {"value": value, "unit": "pair-evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     if not args.no_bvh:
-        line["bvh"] = reference_bvh(threads)
+        line["bvh"] = reference_bvh()
     print(json.dumps(line), flush=True)
 
 
-def reference_bvh(threads, target_s=10.0):
-    """The reference's own CPU path for the BVH metric: the oracle port builds
-    the WeightSet and the median-split tree of cfg4 on the host
-    (build_weight_set / build_bvh restated) and evaluates a bounded query
+def reference_bvh(target_s=10.0):
+    """The reference's own CPU path for the BVH metric on cfg4: its
+    build_bvh tree (built here by the reference, or by the oracle port),
+    the WeightSet from the oracle's restated construction, a bounded query
     sample (both halves of the distribution) on all host threads."""
     import oracle as O
     from paper_2108_10480_b200 import configs
@@ -822,20 +863,20 @@ def reference_bvh(threads, target_s=10.0):
     w, q = configs.cfg4()
     v, q = configs.quantize(w.vertices), configs.quantize(q)
     m = O.Mesh.from_arrays(v, w.simplices, w.kinds)
-    ws = O.Weights.build(m)
-    tree = O.Tree.build(m)
+    wt = O.Weights.build(m).table
+    del m
+    arm = CpuArm(v, w.simplices, w.kinds, wt, build_tree=True)
     setup = time.perf_counter() - t0
-    p = O.Params(alpha=w.alpha, alpha_u=600.0, beta=w.beta)
     half = len(q) // 2
     pick = lambda n: np.concatenate([q[:n // 2], q[half:half + n - n // 2]])
-    pilot = max(threads * 16, 1024)
-    r = O.query(m, ws, pick(pilot), p, tree=tree, threads=threads)  # also warms the tree pages
+    pilot = max(arm.threads * 16, 1024)
+    r = arm.query(pick(pilot), w.alpha, 600.0, w.beta, tree=True)  # also warms the tree pages
     n = int(min(262144, max(pilot, pilot * target_s / max(r.seconds, 1e-3))))
-    r = O.query(m, ws, pick(n), p, tree=tree, threads=threads)
+    r = arm.query(pick(n), w.alpha, 600.0, w.beta, tree=True)
     return {"metric": "BVH queries/s (value+grad)", "value": n / r.seconds, "unit": "queries/s",
             "workload": "cfg4 (BASELINE configs[3]): icosphere(9), 5,242,880 triangles, alpha=200, beta=0.5, "
-                        "host-built median tree and WeightSet",
-            "cpu_baseline": {"value": n / r.seconds, "unit": "queries/s", "cores": threads, "kind": "port",
+                        "the reference's build_bvh tree, WeightSet from the restated construction",
+            "cpu_baseline": {"value": n / r.seconds, "unit": "queries/s", "cores": arm.threads, "kind": arm.kind,
                              "sample": f"{n} cfg4 queries (half from each half of the distribution), "
                                        f"{r.seconds:.1f} s"},
             "setup_s": setup}
