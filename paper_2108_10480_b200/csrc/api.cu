@@ -204,18 +204,43 @@ Poly<T> make_poly(const Ctx& c, int kind, int poly, const sd_params& p) {
     }
     double g[8][8];
     tri_grid(c, poly, g);
+    // w~ is symmetric in (x, y) (weights.hpp:155-170 mirrors every stored
+    // coefficient), so it is a polynomial in s = x + y and p = x y:
+    // c_jj x^j y^j = c_jj p^j and c_jk (x^j y^k + x^k y^j) = c_jk p^j P_{k-j}
+    // with the power sums P_0 = 2, P_1 = s, P_m = s P_{m-1} - p P_{m-2}.
+    // a[i][j] (coefficient of s^i p^j, i + 2 j <= 7): 20 terms instead of
+    // the 23 + 16 + 16 of the (x, y) rows, and the partials follow from
+    // d/dx = W_s + y W_p, d/dy = W_s + x W_p (tri_poly, pair.cuh).
+    double P[8][8][4] = {};  // P[m][i][j]
+    P[0][0][0] = 2.0;
+    P[1][1][0] = 1.0;
+    for (int m = 2; m < 8; ++m)
+        for (int i = 0; i < 8; ++i)
+            for (int j = 0; j < 4; ++j)
+                P[m][i][j] = (i > 0 ? P[m - 1][i - 1][j] : 0.0) - (j > 0 ? P[m - 2][i][j - 1] : 0.0);
+    double a[8][4] = {};
+    for (int j = 0; j < 8; ++j)
+        for (int k = j; j + k <= 7; ++k) {
+            if (k == j) {
+                a[0][j] += g[j][j];
+                continue;
+            }
+            for (int i = 0; i < 8; ++i)
+                for (int jj = 0; jj + j < 4; ++jj) a[i][jj + j] += g[j][k] * P[k - j][i][jj];
+        }
+    // layout (kTriSP*): value rows A_j(s) = sum_i a_ij s^i (x A) for j = 0..3
+    // (degrees 7, 5, 3, 1), then the s-derivative rows B_j(s) = sum_i i a_ij
+    // s^(i-1) (x K) (degrees 6, 4, 2, 0), then K / A, 2 K / A, 3 K / A
     int n = 0;
-    const int rows[7] = {0, 2, 3, 4, 5, 6, 7};
-    for (int j : rows)  // value rows
-        for (int k = 0; j + k <= 7; ++k)
-            if (k != 1) out.c[n++] = T(A * g[j][k]);
-    for (int j : rows)  // d/dx rows, j >= 2
-        if (j >= 2)
-            for (int k = 0; j + k <= 7; ++k)
-                if (k != 1) out.c[n++] = T(K * j * g[j][k]);
-    for (int j : rows)  // d/dy rows, k >= 2
-        for (int k = 2; j + k <= 7; ++k) out.c[n++] = T(K * k * g[j][k]);
-    if (n != kPolyCoefs) throw std::logic_error("triangle polynomial packing");
+    const int deg[4] = {7, 5, 3, 1};
+    for (int j = 0; j < 4; ++j)
+        for (int i = 0; i <= deg[j]; ++i) out.c[n++] = T(A * a[i][j]);
+    for (int j = 0; j < 4; ++j)
+        for (int i = 1; i <= deg[j]; ++i) out.c[n++] = T(K * i * a[i][j]);
+    out.c[n++] = T(K / A);
+    out.c[n++] = T(2.0 * K / A);
+    out.c[n++] = T(3.0 * K / A);
+    if (n != kTriSPCoefs) throw std::logic_error("triangle polynomial packing");
     return out;
 }
 template Poly<float> make_poly<float>(const Ctx&, int, int, const sd_params&);

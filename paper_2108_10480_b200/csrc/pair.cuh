@@ -47,7 +47,13 @@ struct Phys {
 //         [39..54] d/dy rows (k c_jk)  j=0:k{2..7} j=2:k{2..5} j=3:k{2..4}
 //                  j=4:k{2,3} j=5:k{2}                               (x K)
 // with K = S A / alpha^2; c_{1k} = c_{j1} = 0 exactly (weights.hpp:113-131).
+//   tri (s, p) form actually used (api.cu make_poly): w~ is symmetric, so
+//         it is a polynomial in s = x + y, p = x y with 20 terms:
+//         [0..19]  A_j(s) rows, j = 0..3, degrees 7, 5, 3, 1      (x A)
+//         [20..35] B_j(s) = dA_j/ds rows, degrees 6, 4, 2, 0      (x K)
+//         [36..38] K / A, 2 K / A, 3 K / A
 constexpr int kPolyCoefs = 55;
+constexpr int kTriSPCoefs = 39;
 template <class T>
 struct Poly {
     T c[kPolyCoefs];
@@ -201,33 +207,26 @@ __device__ __forceinline__ void tri_closest(const T* rec, T d1, T d2, T& u, T& v
     if (d1 <= T(0) && d2 <= T(0)) { u = T(0); v = T(0); }                       // vertex a
 }
 
-// base = A w~ and the K-scaled barycentric gradient of w~ (see Poly).
+// base = A w~ and the K-scaled barycentric gradient of w~ (see Poly), in
+// the symmetric (s, p) form: W = A_0 + p (A_1 + p (A_2 + p A_3)),
+// W_s = B_0 + p (B_1 + p (B_2 + p B_3)), W_p = A_1 + 2 p A_2 + 3 p^2 A_3,
+// d/dx = W_s + y W_p, d/dy = W_s + x W_p.
 template <class T>
-__device__ __forceinline__ void tri_poly(const Poly<T>& p, T x, T y, T& w, T& wx, T& wy) {
-    const T* c = p.c;
-    const T y2 = y * y, x2 = x * x;
-    // value rows P_j(y) = c_j0 + y^2 (c_j2 + y (c_j3 + ...))
-    const T P0 = fma(y2, fma(y, fma(y, fma(y, fma(y, fma(y, c[6], c[5]), c[4]), c[3]), c[2]), c[1]), c[0]);
-    const T P2 = fma(y2, fma(y, fma(y, fma(y, c[11], c[10]), c[9]), c[8]), c[7]);
-    const T P3 = fma(y2, fma(y, fma(y, c[15], c[14]), c[13]), c[12]);
-    const T P4 = fma(y2, fma(y, c[18], c[17]), c[16]);
-    const T P5 = fma(y2, c[20], c[19]);
-    const T P6 = c[21], P7 = c[22];
-    w = fma(x2, fma(x, fma(x, fma(x, fma(x, fma(x, P7, P6), P5), P4), P3), P2), P0);
-    // d/dx rows Q_j(y) (coefficients j c_jk)
-    const T Q2 = fma(y2, fma(y, fma(y, fma(y, c[27], c[26]), c[25]), c[24]), c[23]);
-    const T Q3 = fma(y2, fma(y, fma(y, c[31], c[30]), c[29]), c[28]);
-    const T Q4 = fma(y2, fma(y, c[34], c[33]), c[32]);
-    const T Q5 = fma(y2, c[36], c[35]);
-    const T Q6 = c[37], Q7 = c[38];
-    wx = x * fma(x, fma(x, fma(x, fma(x, fma(x, Q7, Q6), Q5), Q4), Q3), Q2);
-    // d/dy rows R_j(y) (coefficients k c_jk, powers k - 1)
-    const T R0 = y * fma(y, fma(y, fma(y, fma(y, fma(y, c[44], c[43]), c[42]), c[41]), c[40]), c[39]);
-    const T R2 = y * fma(y, fma(y, fma(y, c[48], c[47]), c[46]), c[45]);
-    const T R3 = y * fma(y, fma(y, c[51], c[50]), c[49]);
-    const T R4 = y * fma(y, c[53], c[52]);
-    const T R5 = y * c[54];
-    wy = fma(x2, fma(x, fma(x, fma(x, R5, R4), R3), R2), R0);
+__device__ __forceinline__ void tri_poly(const Poly<T>& pc, T x, T y, T& w, T& wx, T& wy) {
+    const T* c = pc.c;
+    const T s = x + y, p = x * y;
+    const T A0 = fma(s, fma(s, fma(s, fma(s, fma(s, fma(s, fma(s, c[7], c[6]), c[5]), c[4]), c[3]), c[2]), c[1]), c[0]);
+    const T A1 = fma(s, fma(s, fma(s, fma(s, fma(s, c[13], c[12]), c[11]), c[10]), c[9]), c[8]);
+    const T A2 = fma(s, fma(s, fma(s, c[17], c[16]), c[15]), c[14]);
+    const T A3 = fma(s, c[19], c[18]);
+    w = fma(p, fma(p, fma(p, A3, A2), A1), A0);
+    const T B0 = fma(s, fma(s, fma(s, fma(s, fma(s, fma(s, c[26], c[25]), c[24]), c[23]), c[22]), c[21]), c[20]);
+    const T B1 = fma(s, fma(s, fma(s, fma(s, c[31], c[30]), c[29]), c[28]), c[27]);
+    const T B2 = fma(s, fma(s, c[34], c[33]), c[32]);
+    const T Ws = fma(p, fma(p, fma(p, c[35], B2), B1), B0);
+    const T Wp = fma(p, fma(p, A3 * c[38], A2 * c[37]), A1 * c[36]);
+    wx = fma(y, Wp, Ws);
+    wy = fma(x, Wp, Ws);
 }
 
 // rec: see device_common.cuh (kRecTri)

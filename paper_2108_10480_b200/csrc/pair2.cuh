@@ -210,27 +210,23 @@ __device__ __forceinline__ void edge_term2(const Phys<float>& ph, const Poly<flo
 // ----------------------------------------------------------- triangles
 __device__ __forceinline__ f2 hz(f2 x, f2 acc, float c) { return fma2(x, acc, bcast(c)); }  // x acc + c
 
-// packed tri_poly (pair.cuh): base = A w~ and K-scaled d/dx, d/dy
-__device__ __forceinline__ void tri_poly2(const Poly<float>& p, f2 x, f2 y, f2& w, f2& wx, f2& wy) {
-    const float* c = p.c;
-    const f2 y2 = mul2(y, y), x2 = mul2(x, x);
-    const f2 P0 = hz(y2, hz(y, hz(y, hz(y, hz(y, fmas(y, c[6], bcast(c[5])), c[4]), c[3]), c[2]), c[1]), c[0]);
-    const f2 P2 = hz(y2, hz(y, hz(y, fmas(y, c[11], bcast(c[10])), c[9]), c[8]), c[7]);
-    const f2 P3 = hz(y2, hz(y, fmas(y, c[15], bcast(c[14])), c[13]), c[12]);
-    const f2 P4 = hz(y2, fmas(y, c[18], bcast(c[17])), c[16]);
-    const f2 P5 = fmas(y2, c[20], bcast(c[19]));
-    w = fma2(x2, fma2(x, fma2(x, fma2(x, fma2(x, fmas(x, c[22], bcast(c[21])), P5), P4), P3), P2), P0);
-    const f2 Q2 = hz(y2, hz(y, hz(y, fmas(y, c[27], bcast(c[26])), c[25]), c[24]), c[23]);
-    const f2 Q3 = hz(y2, hz(y, fmas(y, c[31], bcast(c[30])), c[29]), c[28]);
-    const f2 Q4 = hz(y2, fmas(y, c[34], bcast(c[33])), c[32]);
-    const f2 Q5 = fmas(y2, c[36], bcast(c[35]));
-    wx = mul2(x, fma2(x, fma2(x, fma2(x, fma2(x, fmas(x, c[38], bcast(c[37])), Q5), Q4), Q3), Q2));
-    const f2 R0 = mul2(y, hz(y, hz(y, hz(y, hz(y, fmas(y, c[44], bcast(c[43])), c[42]), c[41]), c[40]), c[39]));
-    const f2 R2 = mul2(y, hz(y, hz(y, fmas(y, c[48], bcast(c[47])), c[46]), c[45]));
-    const f2 R3 = mul2(y, hz(y, fmas(y, c[51], bcast(c[50])), c[49]));
-    const f2 R4 = mul2(y, fmas(y, c[53], bcast(c[52])));
-    const f2 R5 = muls(y, c[54]);
-    wy = fma2(x2, fma2(x, fma2(x, fma2(x, R5, R4), R3), R2), R0);
+// packed tri_poly (pair.cuh): base = A w~ and K-scaled d/dx, d/dy in the
+// symmetric (s, p) form
+__device__ __forceinline__ void tri_poly2(const Poly<float>& pc, f2 x, f2 y, f2& w, f2& wx, f2& wy) {
+    const float* c = pc.c;
+    const f2 s = add2(x, y), p = mul2(x, y);
+    const f2 A0 = hz(s, hz(s, hz(s, hz(s, hz(s, hz(s, fmas(s, c[7], bcast(c[6])), c[5]), c[4]), c[3]), c[2]), c[1]), c[0]);
+    const f2 A1 = hz(s, hz(s, hz(s, hz(s, fmas(s, c[13], bcast(c[12])), c[11]), c[10]), c[9]), c[8]);
+    const f2 A2 = hz(s, hz(s, fmas(s, c[17], bcast(c[16])), c[15]), c[14]);
+    const f2 A3 = fmas(s, c[19], bcast(c[18]));
+    w = fma2(p, fma2(p, fma2(p, A3, A2), A1), A0);
+    const f2 B0 = hz(s, hz(s, hz(s, hz(s, hz(s, fmas(s, c[26], bcast(c[25])), c[24]), c[23]), c[22]), c[21]), c[20]);
+    const f2 B1 = hz(s, hz(s, hz(s, fmas(s, c[31], bcast(c[30])), c[29]), c[28]), c[27]);
+    const f2 B2 = hz(s, fmas(s, c[34], bcast(c[33])), c[32]);
+    const f2 Ws = fma2(p, fma2(p, fmas(p, c[35], B2), B1), B0);
+    const f2 Wp = fma2(p, fma2(p, muls(A3, c[38]), muls(A2, c[37])), muls(A1, c[36]));
+    wx = fma2(y, Wp, Ws);
+    wy = fma2(x, Wp, Ws);
 }
 
 // packed Ericson regions: the dot products and candidates are packed, the
