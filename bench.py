@@ -425,7 +425,7 @@ def parity_stats(got_d, got_g, ref_d, ref_g, alpha, dtype):
 
 # ------------------------------------------------------------ exact legs
 def exact_leg(run, eng, q, prec, N, kind, P, steps, warmup, flush, stream, peaks, e2e_steps=0, q_total=None,
-              label=""):
+              stamp_key=None):
     """Times one exact configuration on this rank's query block q (fp32 /
     fp64 device buffer, inputs resident), optionally end to end through
     sd_query_points with pinned host buffers. Returns the result dict and
@@ -464,6 +464,14 @@ def exact_leg(run, eng, q, prec, N, kind, P, steps, warmup, flush, stream, peaks
             "kernel": f"exact_kernel<{'double' if fp64 else 'float'}, {['point', 'edge', 'triangle'][kind]}>"}
         if peaks and not fp64:
             out["roofline"]["mufu_frac"] = MUFU_PER_PAIR[kind] * pairs_rank / (kms * 1e-3) / 1e12 / peaks["mufu_tops"]
+        # bytes per launch: the queries in, the primitive records once per
+        # query block (staged through shared memory), the outputs out
+        out["roofline"]["algorithmic_bytes"] = Q * 12 + N * 4 * [4, 12, 24][kind] + Q * 32
+        out["roofline"]["traffic"] = None
+        st = ncu_stamp(f"exact_{stamp_key}") if stamp_key else None
+        if st:
+            out["roofline"]["traffic"] = st.get("dram_bytes")
+            out["roofline"]["ncu"] = st
     if e2e_steps:
         qh = torch.tensor(q, dtype=torch.float64).pin_memory().numpy()
         res = sd.SmoothResults(torch.empty(Q, dtype=torch.float64).pin_memory().numpy(),
@@ -501,7 +509,8 @@ def run_exact_headline(args, run, peaks, stream, flush, line):
     N3 = len(k3)
     P = sd.SmoothParams(alpha=100.0, alpha_u=600.0, beta=0.0)
     head, d100, g100 = exact_leg(run, eng, qb, sd.SD_FP32, N3, 2, P, args.steps, args.warmup, flush, stream, peaks,
-                                 e2e_steps=max(3, min(args.steps, 10)), q_total=len(q3))
+                                 e2e_steps=max(3, min(args.steps, 10)), q_total=len(q3),
+                                 stamp_key="cfg3_f32" if run.world == 1 else None)
     extra = {}
     outs = {100.0: (d100, g100)}
     for alpha in (10.0, 1000.0):
@@ -562,7 +571,8 @@ def run_exact_headline(args, run, peaks, stream, flush, line):
         e.set_geometry(v2, w2.simplices, w2.kinds)
         e.set_weights(wt2.A, wt2.sup_wtilde, wt2.edge_a, wt2.tri_stored, wt2.poly_index)
         r, d, g = exact_leg(run, e, qb2, prec, N2, 1, P2, args.steps, args.warmup, flush, stream, peaks,
-                            e2e_steps=3, q_total=len(q2))
+                            e2e_steps=3, q_total=len(q2),
+                            stamp_key=(f"cfg2_{'f64' if prec == sd.SD_FP64 else 'f32'}" if run.world == 1 else None))
         r["workload"] = ("cfg2: helix polyline 20,000 edges x 262,144 queries, exact LSE, alpha=100 "
                          "(BASELINE configs[1])")
         line[key] = r
@@ -693,7 +703,7 @@ def measure_bvh(args, run, stream, flush, peaks, fp64=False):
                 "modelled_l1l2_gbs": nbytes / (kms * 1e-3) / 1e9,
                 "modelled_bytes": "32 B per popped node + 100 B per exact leaf, served from L1/L2, not DRAM",
                 "traffic": None}
-        st = ncu_stamp("bvh_cfg4_f64" if fp64 else "bvh_cfg4_f32")
+        st = ncu_stamp("bvh_cfg4_f64" if fp64 else "bvh_cfg4_f32") if world == 1 else None
         if st:
             roof["traffic"] = st.get("dram_bytes")
             roof["ncu"] = st
