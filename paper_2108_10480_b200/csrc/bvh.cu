@@ -1038,7 +1038,7 @@ void tree_query(Ctx& c, const T* q, int64_t Q, const sd_params& p, const Finaliz
         if (!(use_frontier(Q, 65536) &&
               launch_frontier<T, PointVisit<T>>(c, c.dtree, a, out.hash != nullptr, st, launches, 32)))
             nsplits = launch_pair_traversal<T, PointVisit<T>>(c, c.dtree, a, out.hash != nullptr, st, launches, 1,
-                                                                 true);
+                                                                 true, out.leaves || out.far_field);
     } else {
         const size_t smem = poly_bytes<T>(npoly) +
                             (variant == 0 ? size_t(a.stack_depth) * kTravThreads * sizeof(int32_t)

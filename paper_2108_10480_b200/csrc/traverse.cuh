@@ -9,6 +9,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <stdexcept>
+#include <type_traits>
 
 #include "context.h"
 
@@ -364,7 +365,12 @@ __global__ void __launch_bounds__(kTravThreads, sizeof(T) == 4 ? 8 : 4)
 // most two) and the queues are drained after the walk. Per lane the set of
 // terms is exactly collect_contributions'; only their summation order
 // changes (fp32 rounding).
-constexpr int kLeafQ = 16;  // default leaf queue entries per lane (SDGPU_LEAFQ)
+constexpr int kLeafQ = 40;  // default leaf queue entries per lane (SDGPU_LEAFQ)
+
+// Counter type of walks whose per-query counters were not asked for.
+struct NoCount {
+    __device__ __forceinline__ NoCount& operator++() { return *this; }
+};
 constexpr int kFarQ = 0;    // default far-field queue entries per lane (SDGPU_FARQ; 0 = far terms inline)
 constexpr uint32_t kLeafStride = kTravThreads * 4;  // bytes between a lane's leaf entries
 
@@ -403,7 +409,7 @@ __host__ __device__ constexpr size_t farq_bytes(int cap) {
     return size_t(cap) * kTravThreads * 4 * sizeof(T);
 }
 
-template <class T, class VIS, bool HASH, bool FARQ>
+template <class T, class VIS, bool HASH, bool FARQ, bool COUNT>
 __device__ __forceinline__ void pair_walk_q(const TraverseArgs<T>& a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Poly<T>* polys = reinterpret_cast<Poly<T>*>(smem_raw);
@@ -433,7 +439,8 @@ __device__ __forceinline__ void pair_walk_q(const TraverseArgs<T>& a) {
     if (mask == 0u) return;
     Acc<T> acc;
     acc.init();
-    int32_t nleaf = 0, nfar = 0;  // per query: < 2^31 nodes
+    using CNT = std::conditional_t<COUNT, int32_t, NoCount>;  // per query: < 2^31 nodes
+    CNT nleaf{}, nfar{};
     uint64_t h = 0;
     unsigned long long nre = 0;
     int32_t cur = 0, cur_link;
@@ -471,6 +478,8 @@ __device__ __forceinline__ void pair_walk_q(const TraverseArgs<T>& a) {
             dr = qv.template visit_q<HASH, FARQ>(a, br, rid, lgr, acc, nleaf, nfar, h, nre, lq0, nq, fq0, nf);
         }
         const unsigned DL = __ballot_sync(FULL, dl), DR = __ballot_sync(FULL, dr);
+        // (one convergence point per step: the queue check with the ballots)
+        const bool full = FARQ ? __any_sync(FULL, nq >= lcap || nf >= fcap) : __any_sync(FULL, nq >= lcap);
         int32_t llink, rlink;
         memcpy(&llink, &bl.v[7], sizeof(int32_t));
         memcpy(&rlink, &br.v[7], sizeof(int32_t));
@@ -496,12 +505,10 @@ __device__ __forceinline__ void pair_walk_q(const TraverseArgs<T>& a) {
         } else {
             mask = 0u;
         }
-        if constexpr (FARQ) {
-            if (__any_sync(FULL, nq >= lcap || nf >= fcap)) {
+        if (full) {
+            if constexpr (FARQ) {
                 while (__any_sync(FULL, nf >= fcap)) fround();
-                while (__any_sync(FULL, nq >= lcap)) round();
             }
-        } else {
             while (__any_sync(FULL, nq >= lcap)) round();
         }
     }
@@ -518,14 +525,16 @@ __device__ __forceinline__ void pair_walk_q(const TraverseArgs<T>& a) {
     a.part[2 * a.Q + i] = tot.gx;
     a.part[3 * a.Q + i] = tot.gy;
     a.part[4 * a.Q + i] = tot.gz;
-    a.leaves[i] = nleaf;
-    a.far[i] = nfar;
+    if constexpr (COUNT) {
+        a.leaves[i] = nleaf;
+        a.far[i] = nfar;
+    }
     if (HASH) a.hash[i] = h;
 }
 
-template <class T, class VIS, bool HASH, bool FARQ>
+template <class T, class VIS, bool HASH, bool FARQ, bool COUNT>
 __global__ void __launch_bounds__(kTravThreads) pair_kernel_q(const __grid_constant__ TraverseArgs<T> a) {
-    pair_walk_q<T, VIS, HASH, FARQ>(a);
+    pair_walk_q<T, VIS, HASH, FARQ, COUNT || HASH>(a);
 }
 
 // K3F (few queries, node-parallel): a group of G lanes per query (32 / G
@@ -674,7 +683,7 @@ inline bool use_frontier(int64_t Q, int64_t limit) {
 // splitting. `weight` raises the warp target for expensive node tests.
 template <class T, class VIS>
 int launch_pair_traversal(Ctx& c, DeviceTree& t, TraverseArgs<T>& a, bool hash, cudaStream_t st, int64_t& launches,
-                          int weight = 1, bool allow_defer = false) {
+                          int weight = 1, bool allow_defer = false, bool count = true) {
     const int64_t Q = a.Q;
     size_t smem = poly_bytes<T>(a.npoly) + size_t(a.stack_depth) * (kTravThreads / 32) * sizeof(int4);
     const int64_t npackets = (Q + 31) / 32;
@@ -747,8 +756,12 @@ int launch_pair_traversal(Ctx& c, DeviceTree& t, TraverseArgs<T>& a, bool hash, 
         if (a.fq_cap < 3) a.fq_cap = 0;
         if (lq_on && k == 0 && !defer && !(lb && *lb == '1')) {
             smem += size_t(a.lq_cap) * kTravThreads * sizeof(int32_t) + farq_bytes<T>(a.fq_cap);
-            kern = a.fq_cap ? (hash ? pair_kernel_q<T, VIS, true, true> : pair_kernel_q<T, VIS, false, true>)
-                            : (hash ? pair_kernel_q<T, VIS, true, false> : pair_kernel_q<T, VIS, false, false>);
+            if (hash)
+                kern = a.fq_cap ? pair_kernel_q<T, VIS, true, true, true> : pair_kernel_q<T, VIS, true, false, true>;
+            else if (count)
+                kern = a.fq_cap ? pair_kernel_q<T, VIS, false, true, true> : pair_kernel_q<T, VIS, false, false, true>;
+            else
+                kern = a.fq_cap ? pair_kernel_q<T, VIS, false, true, false> : pair_kernel_q<T, VIS, false, false, false>;
         }
     }
     check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)), "smem attr");
