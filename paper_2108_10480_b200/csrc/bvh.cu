@@ -20,6 +20,7 @@
 
 #include <cub/cub.cuh>
 
+#include "pair2.cuh"
 #include "traverse.cuh"
 
 namespace sdgpu {
@@ -579,7 +580,7 @@ __device__ __forceinline__ void merge_partial(Acc<T>& acc, T m, T s, T gx, T gy,
 // 185-187): fp32 decides outside a 1e-5 relative band, fp64 re-decides in
 // the reference rounding inside it. On "far" also returns d_B, 1/d_B and
 // q - y_B for the far-field term.
-template <class T, bool NEED_D = true>
+template <class T>
 __device__ __forceinline__ bool point_far(const TraverseArgs<T>& a, const NodeT<T>& b, int32_t id, T qx, T qy, T qz,
                                           T& d, T& r, T& dx, T& dy, T& dz, unsigned long long& nre) {
     const T yx = fmin(fmax(qx, b.v[0]), b.v[4]);
@@ -601,7 +602,7 @@ __device__ __forceinline__ bool point_far(const TraverseArgs<T>& a, const NodeT<
             far = decide64(b, a.diam64[id], double(qx), double(qy), double(qz), a.beta64);
             ++nre;
         }
-        if (NEED_D && far) {  // s = 0 only for an fp64-confirmed box that the fp32 box contains; then dx = dy = dz = 0
+        if (far) {  // s = 0 only for an fp64-confirmed box that the fp32 box contains; then dx = dy = dz = 0
             r = Math<T>::rsqrt(fmax(s, T(1e-30)));
             d = s * r;
         }
@@ -617,7 +618,7 @@ __device__ __forceinline__ bool point_far(const TraverseArgs<T>& a, const NodeT<
             far = decide64(b, a.diam64[id], double(qx), double(qy), double(qz), a.beta64);
             ++nre;
         }
-        if (NEED_D && far) {
+        if (far) {
             r = Math<double>::rsqrt(s);
             d = s * r;
         }
@@ -664,26 +665,18 @@ struct PointVisit {
                                           unsigned long long& nre) const {
         return sdgpu::visit<T, HASH, CNT>(a, polys, b, id, lgc, qx, qy, qz, acc, nleaf, nfar, h, nre);
     }
-    // K3Q node test: a far-field node appends (q - y_B, log2 n_B) to this
-    // lane's far queue, an exact leaf its slot to the leaf queue; both are
-    // counted and hashed here, where the reference decides them (the terms
-    // come in far_round / leaf_round).
-    template <bool HASH, bool FARQ, class CNT>
+    // K3Q node test: far field inline; an exact leaf is counted, hashed and
+    // appended to this lane's leaf queue (its term comes in leaf_round).
+    template <bool HASH, class CNT>
     __device__ __forceinline__ bool visit_q(const TraverseArgs<T>& a, const NodeT<T>& b, int32_t id, T lgc,
                                             Acc<T>& acc, CNT& nleaf, CNT& nfar, uint64_t& h,
-                                            unsigned long long& nre, uint32_t lq0, int& nq, uint32_t fq0,
-                                            int& nf) const {
+                                            unsigned long long& nre, uint32_t lq0, int& nq) const {
         int32_t link;
         memcpy(&link, &b.v[7], sizeof(int32_t));
         {  // beta = 0 when there is no Barnes-Hut (see visit)
             T d, r, dx, dy, dz;
-            if (point_far<T, !FARQ>(a, b, id, qx, qy, qz, d, r, dx, dy, dz, nre)) {
-                if constexpr (FARQ) {
-                    FarQ<T>::push(fq0, nf, dx, dy, dz, lgc);
-                    ++nf;
-                } else {
-                    far_term(a.ph, lgc + a.lw_ff, d, r, dx, dy, dz, acc);
-                }
+            if (point_far(a, b, id, qx, qy, qz, d, r, dx, dy, dz, nre)) {
+                far_term(a.ph, lgc + a.lw_ff, d, r, dx, dy, dz, acc);
                 ++nfar;
                 if constexpr (HASH) h += decision_mix(uint64_t(id), 1);
                 return false;
@@ -696,13 +689,69 @@ struct PointVisit {
         if constexpr (HASH) h += decision_mix(uint64_t(id), 2);
         return false;
     }
-    // one queued far-field term (smooth.hpp:67-75) of this lane
-    __device__ __forceinline__ void far_round(const TraverseArgs<T>& a, uint32_t fq0, int k, Acc<T>& acc) const {
-        T dx, dy, dz, lg;
-        FarQ<T>::pop(fq0, k, dx, dy, dz, lg);
-        const T s = fma(dx, dx, fma(dy, dy, dz * dz));
-        const T r = Math<T>::rsqrt(fmax(s, Tiny<T>::v));
-        far_term(a.ph, lg + a.lw_ff, s * r, r, dx, dy, dz, acc);
+    // K3Q step: both children of a node. fp32: the box tests of the two
+    // children run as one packed fp32x2 sequence on the interleaved pair
+    // record (clamps and the decisions per child; each child's decision is
+    // point_far's, bit for bit -- the fp64 re-check band included); fp64:
+    // two visit_q calls. active = this lane reached the node.
+    template <bool HASH, class CNT>
+    __device__ __forceinline__ void visit_pair_q(const TraverseArgs<T>& a, const PairT<T>& pr, int32_t lid,
+                                                 int32_t rid, bool active, Acc<T>& acc, CNT& nleaf, CNT& nfar,
+                                                 uint64_t& h, unsigned long long& nre, uint32_t lq0, int& nq,
+                                                 bool& dl, bool& dr, int32_t& llink, int32_t& rlink) const {
+        if constexpr (sizeof(T) == 8) {
+            const NodeT<T> bl = pr.l(), br = pr.r();
+            memcpy(&llink, &bl.v[7], sizeof(int32_t));
+            memcpy(&rlink, &br.v[7], sizeof(int32_t));
+            if (active) {
+                dl = visit_q<HASH>(a, bl, lid, pr.lgc[0], acc, nleaf, nfar, h, nre, lq0, nq);
+                dr = visit_q<HASH>(a, br, rid, pr.lgc[1], acc, nleaf, nfar, h, nre, lq0, nq);
+            }
+        } else {
+            const float4* p4 = reinterpret_cast<const float4*>(pr.w);
+            // (lo.x, lo.y | lo.z, diam | hi.x, hi.y | hi.z, link) of (left, right)
+            const float4 w0 = p4[0], w1 = p4[1], w2 = p4[2], w3 = p4[3];
+            const float2 lg = *reinterpret_cast<const float2*>(pr.lgc);
+            memcpy(&llink, &w3.z, sizeof(int32_t));
+            memcpy(&rlink, &w3.w, sizeof(int32_t));
+            if (!active) return;
+            const f2 dx = sub2(bcast(qx), pack(fminf(fmaxf(qx, w0.x), w2.x), fminf(fmaxf(qx, w0.y), w2.y)));
+            const f2 dy = sub2(bcast(qy), pack(fminf(fmaxf(qy, w0.z), w2.z), fminf(fmaxf(qy, w0.w), w2.w)));
+            const f2 dz = sub2(bcast(qz), pack(fminf(fmaxf(qz, w1.x), w3.x), fminf(fmaxf(qz, w1.y), w3.y)));
+            const f2 s2 = fma2(dx, dx, fma2(dy, dy, mul2(dz, dz)));
+            const float b2 = a.ph.beta * a.ph.beta;
+            const f2 diam = pack(w1.z, w1.w);
+            const f2 gap = fma2(diam, diam, mul2(bcast(-b2), s2));  // diam^2 - beta^2 s
+            const f2 band = mul2(bcast(2e-5f * b2), s2);
+            auto child = [&](int hh, int32_t id, int32_t link, float lgc) -> bool {
+                const float g = hh ? hi(gap) : lo(gap), bd = hh ? hi(band) : lo(band), s = hh ? hi(s2) : lo(s2);
+                bool far;
+                if (fabsf(g) > bd) far = g < 0.f;
+                else if (s == 0.f && a.exact_boxes) far = false;
+                else {
+                    const NodeT<float> b = hh ? pr.r() : pr.l();
+                    far = decide64(b, a.diam64[id], double(qx), double(qy), double(qz), a.beta64);
+                    ++nre;
+                }
+                if (far) {
+                    const float r = Math<float>::rsqrt(fmaxf(s, 1e-30f));
+                    far_term(a.ph, lgc + a.lw_ff, s * r, r, hh ? hi(dx) : lo(dx), hh ? hi(dy) : lo(dy),
+                             hh ? hi(dz) : lo(dz), acc);
+                    ++nfar;
+                    if constexpr (HASH) h += decision_mix(uint64_t(id), 1);
+                    return false;
+                }
+                if (link >= 0) return true;
+                asm volatile("st.shared.s32 [%0], %1;" ::"r"(lq0 + uint32_t(nq) * kLeafStride), "r"(-link - 1)
+                             : "memory");
+                ++nq;
+                ++nleaf;
+                if constexpr (HASH) h += decision_mix(uint64_t(id), 2);
+                return false;
+            };
+            dl = child(0, lid, llink, lg.x);
+            dr = child(1, rid, rlink, lg.y);
+        }
     }
     __device__ __forceinline__ void leaf_round(const TraverseArgs<T>& a, const Poly<T>* polys, int slot,
                                                Acc<T>& acc) const {

@@ -151,12 +151,11 @@ __global__ void pair_records(const sd_bvh_node* __restrict__ nodes, int64_t n, c
     const sd_bvh_node& nd = nodes[id];
     PairT<T> pr;
     if (nd.left >= 0) {
-        pr.l = box[id + 1];
-        pr.r = box[nd.right];
+        pr.set(box[id + 1], box[nd.right]);
         pr.lgc[0] = lgc[id + 1];
         pr.lgc[1] = lgc[nd.right];
     } else {
-        for (int i = 0; i < 8; ++i) pr.l.v[i] = pr.r.v[i] = T(0);
+        for (int i = 0; i < 16; ++i) pr.w[i] = T(0);
         pr.lgc[0] = pr.lgc[1] = T(0);
     }
     pr.lgc[2] = pr.lgc[3] = T(0);

@@ -19,10 +19,33 @@ template <class T>
 struct alignas(16) NodeT {  // 2 x (4 T): (lo, diam) (hi, link)
     T v[8];
 };
+// Both children of an internal node + their log2 n_B, component-
+// interleaved (w[2k] = left.v[k], w[2k + 1] = right.v[k]) so that the fp32
+// walk tests both children with packed fp32x2 arithmetic straight from the
+// loaded registers.
 template <class T>
-struct alignas(16) PairT {  // both children of an internal node + their log2 n_B
-    NodeT<T> l, r;
+struct alignas(16) PairT {
+    T w[16];
     T lgc[4];
+    __host__ __device__ __forceinline__ NodeT<T> l() const {
+        NodeT<T> n;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) n.v[k] = w[2 * k];
+        return n;
+    }
+    __host__ __device__ __forceinline__ NodeT<T> r() const {
+        NodeT<T> n;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) n.v[k] = w[2 * k + 1];
+        return n;
+    }
+    __host__ __device__ __forceinline__ void set(const NodeT<T>& L, const NodeT<T>& R) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            w[2 * k] = L.v[k];
+            w[2 * k + 1] = R.v[k];
+        }
+    }
 };
 
 template <class T>
@@ -64,8 +87,8 @@ struct TraverseArgs {
     // pre-order subtree, the popcount threshold and the per-warp capacity
     const int32_t* esc = nullptr;
     int defer_t = 0, defer_cap = 0;
-    // K3Q queue capacities (entries per lane): exact leaves, far-field terms
-    int lq_cap = 0, fq_cap = 0;
+    // K3Q leaf-queue capacity (entries per lane)
+    int lq_cap = 0;
 };
 
 constexpr int kTravThreads = 128;
@@ -209,7 +232,7 @@ __device__ __forceinline__ void pair_walk(const TraverseArgs<T>& a) {
     while (mask) {
         const int32_t lid = cur + 1, rid = cur_link;
         const PairT<T>& pr = a.pairs[uint32_t(cur)];  // warp-uniform: broadcast loads
-        const NodeT<T> bl = pr.l, br = pr.r;
+        const NodeT<T> bl = pr.l(), br = pr.r();
         const T lgl = pr.lgc[0], lgr = pr.lgc[1];
         // the most likely next step descends into the left child: pull its
         // pair record into L1 while this one is being processed
@@ -371,51 +394,15 @@ constexpr int kLeafQ = 40;  // default leaf queue entries per lane (SDGPU_LEAFQ)
 struct NoCount {
     __device__ __forceinline__ NoCount& operator++() { return *this; }
 };
-constexpr int kFarQ = 0;    // default far-field queue entries per lane (SDGPU_FARQ; 0 = far terms inline)
 constexpr uint32_t kLeafStride = kTravThreads * 4;  // bytes between a lane's leaf entries
 
-// Far queue entry (q - y_B, log2 n_B): 4 T per entry, lane-interleaved
-// ([k][128 threads]) so that a warp's accesses are contiguous.
-template <class T>
-struct FarQ;
-template <>
-struct FarQ<float> {
-    static constexpr uint32_t kStride = kTravThreads * 16;  // bytes between a lane's entries
-    __device__ __forceinline__ static void push(uint32_t q0, int k, float x, float y, float z, float w) {
-        asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(q0 + uint32_t(k) * kStride), "f"(x), "f"(y),
-                     "f"(z), "f"(w) : "memory");
-    }
-    __device__ __forceinline__ static void pop(uint32_t q0, int k, float& x, float& y, float& z, float& w) {
-        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(x), "=f"(y), "=f"(z), "=f"(w)
-                     : "r"(q0 + uint32_t(k) * kStride));
-    }
-};
-template <>
-struct FarQ<double> {
-    static constexpr uint32_t kStride = kTravThreads * 32;
-    __device__ __forceinline__ static void push(uint32_t q0, int k, double x, double y, double z, double w) {
-        const uint32_t p = q0 + uint32_t(k) * kStride;
-        asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(p), "d"(x), "d"(y) : "memory");
-        asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(p + 16), "d"(z), "d"(w) : "memory");
-    }
-    __device__ __forceinline__ static void pop(uint32_t q0, int k, double& x, double& y, double& z, double& w) {
-        const uint32_t p = q0 + uint32_t(k) * kStride;
-        asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(x), "=d"(y) : "r"(p));
-        asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(z), "=d"(w) : "r"(p + 16));
-    }
-};
-template <class T>
-__host__ __device__ constexpr size_t farq_bytes(int cap) {
-    return size_t(cap) * kTravThreads * 4 * sizeof(T);
-}
 
-template <class T, class VIS, bool HASH, bool FARQ, bool COUNT>
+template <class T, class VIS, bool HASH, bool COUNT>
 __device__ __forceinline__ void pair_walk_q(const TraverseArgs<T>& a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Poly<T>* polys = reinterpret_cast<Poly<T>*>(smem_raw);
     int4* stacks = reinterpret_cast<int4*>(smem_raw + poly_bytes<T>(a.npoly));
     int32_t* lqs = reinterpret_cast<int32_t*>(stacks + (kTravThreads / 32) * a.stack_depth);
-    unsigned char* fqs = reinterpret_cast<unsigned char*>(lqs + a.lq_cap * kTravThreads);  // 16-B aligned
     for (int i = threadIdx.x; i < a.npoly * kPolyCoefs; i += blockDim.x)
         reinterpret_cast<T*>(polys)[i] = reinterpret_cast<const T*>(a.polys)[i];
     __syncthreads();
@@ -426,9 +413,8 @@ __device__ __forceinline__ void pair_walk_q(const TraverseArgs<T>& a) {
     const unsigned warp = threadIdx.x >> 5;
     int4* st = stacks + warp * a.stack_depth;
     const uint32_t lq0 = smem_u32(lqs + threadIdx.x);  // this lane's entry 0 (entries kLeafStride apart)
-    const int lcap = a.lq_cap - 1, fcap = a.fq_cap - 1;  // a step appends at most two entries per lane
-    const uint32_t fq0 = smem_u32(fqs) + threadIdx.x * 4 * uint32_t(sizeof(T));
-    int nq = 0, nf = 0;  // pending leaf / far-field entries of this lane
+    const int lcap = a.lq_cap - 1;  // a step appends at most two entries per lane
+    int nq = 0;  // pending leaf entries of this lane
     const int64_t packet = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int64_t i = packet * 32 + lane;
     const bool valid = i < a.Q;
@@ -447,8 +433,7 @@ __device__ __forceinline__ void pair_walk_q(const TraverseArgs<T>& a) {
     memcpy(&cur_link, &a.box[0].v[7], sizeof(int32_t));
     {  // the root is popped alone
         const NodeT<T> b0 = a.box[0];
-        const bool d = valid && qv.template visit_q<HASH, FARQ>(a, b0, 0, a.lgcount[0], acc, nleaf, nfar, h, nre, lq0,
-                                                                 nq, fq0, nf);
+        const bool d = valid && qv.template visit_q<HASH>(a, b0, 0, a.lgcount[0], acc, nleaf, nfar, h, nre, lq0, nq);
         mask = __ballot_sync(FULL, d);
     }
     auto round = [&]() {
@@ -459,30 +444,19 @@ __device__ __forceinline__ void pair_walk_q(const TraverseArgs<T>& a) {
             qv.leaf_round(a, polys, slot, acc);
         }
     };
-    auto fround = [&]() {
-        if constexpr (FARQ) {
-            if (nf > 0) qv.far_round(a, fq0, --nf, acc);
-        }
-    };
     const uint32_t st0 = smem_u32(st);
     uint32_t top = st0;
     while (mask) {
         const int32_t lid = cur + 1, rid = cur_link;
         const PairT<T>& pr = a.pairs[uint32_t(cur)];  // warp-uniform: broadcast loads
-        const NodeT<T> bl = pr.l, br = pr.r;
-        const T lgl = pr.lgc[0], lgr = pr.lgc[1];
         asm volatile("prefetch.global.L1 [%0];" ::"l"(&pr + 1));  // = a.pairs + lid
         bool dl = false, dr = false;
-        if (mask & lanebit) {
-            dl = qv.template visit_q<HASH, FARQ>(a, bl, lid, lgl, acc, nleaf, nfar, h, nre, lq0, nq, fq0, nf);
-            dr = qv.template visit_q<HASH, FARQ>(a, br, rid, lgr, acc, nleaf, nfar, h, nre, lq0, nq, fq0, nf);
-        }
+        int32_t llink, rlink;
+        qv.template visit_pair_q<HASH>(a, pr, lid, rid, (mask & lanebit) != 0u, acc, nleaf, nfar, h, nre, lq0, nq, dl,
+                                       dr, llink, rlink);
         const unsigned DL = __ballot_sync(FULL, dl), DR = __ballot_sync(FULL, dr);
         // (one convergence point per step: the queue check with the ballots)
-        const bool full = FARQ ? __any_sync(FULL, nq >= lcap || nf >= fcap) : __any_sync(FULL, nq >= lcap);
-        int32_t llink, rlink;
-        memcpy(&llink, &bl.v[7], sizeof(int32_t));
-        memcpy(&rlink, &br.v[7], sizeof(int32_t));
+        const bool full = __any_sync(FULL, nq >= lcap);
         if (DL) {
             if (DR) {
                 if (lane == 0) st_shared_int4(top, rid, rlink, int(DR));
@@ -506,14 +480,8 @@ __device__ __forceinline__ void pair_walk_q(const TraverseArgs<T>& a) {
             mask = 0u;
         }
         if (full) {
-            if constexpr (FARQ) {
-                while (__any_sync(FULL, nf >= fcap)) fround();
-            }
             while (__any_sync(FULL, nq >= lcap)) round();
         }
-    }
-    if constexpr (FARQ) {
-        while (__any_sync(FULL, nf > 0)) fround();
     }
     while (__any_sync(FULL, nq > 0)) round();
     if (!valid) return;
@@ -532,9 +500,9 @@ __device__ __forceinline__ void pair_walk_q(const TraverseArgs<T>& a) {
     if (HASH) a.hash[i] = h;
 }
 
-template <class T, class VIS, bool HASH, bool FARQ, bool COUNT>
+template <class T, class VIS, bool HASH, bool COUNT>
 __global__ void __launch_bounds__(kTravThreads) pair_kernel_q(const __grid_constant__ TraverseArgs<T> a) {
-    pair_walk_q<T, VIS, HASH, FARQ, COUNT || HASH>(a);
+    pair_walk_q<T, VIS, HASH, COUNT || HASH>(a);
 }
 
 // K3F (few queries, node-parallel): a group of G lanes per query (32 / G
@@ -741,8 +709,7 @@ int launch_pair_traversal(Ctx& c, DeviceTree& t, TraverseArgs<T>& a, bool hash, 
         }
     }
     if constexpr (VIS::kLeafQueue) {  // SDGPU_LEAF_QUEUE = 0 turns the deferred leaf queues off (A/B)
-        // SDGPU_LEAFQ / SDGPU_FARQ: queue entries per lane (>= 3 to be used;
-        // SDGPU_FARQ < 3 keeps the far-field terms inline)
+        // SDGPU_LEAFQ: leaf-queue entries per lane (>= 3)
         auto cap = [](const char* name, int dflt) {
             const char* e = std::getenv(name);
             return e && *e ? std::max(0, std::min(64, std::atoi(e))) : dflt;
@@ -750,18 +717,11 @@ int launch_pair_traversal(Ctx& c, DeviceTree& t, TraverseArgs<T>& a, bool hash, 
         const char* lqe = std::getenv("SDGPU_LEAF_QUEUE");
         const bool lq_on = !(lqe && *lqe == '0');
         const char* lb = std::getenv("SDGPU_LEAF_BATCH");
-        a.lq_cap = cap("SDGPU_LEAFQ", kLeafQ);
-        a.fq_cap = cap("SDGPU_FARQ", kFarQ);
-        if (a.lq_cap < 3) a.lq_cap = 3;
-        if (a.fq_cap < 3) a.fq_cap = 0;
+        a.lq_cap = std::max(3, cap("SDGPU_LEAFQ", kLeafQ));
         if (lq_on && k == 0 && !defer && !(lb && *lb == '1')) {
-            smem += size_t(a.lq_cap) * kTravThreads * sizeof(int32_t) + farq_bytes<T>(a.fq_cap);
-            if (hash)
-                kern = a.fq_cap ? pair_kernel_q<T, VIS, true, true, true> : pair_kernel_q<T, VIS, true, false, true>;
-            else if (count)
-                kern = a.fq_cap ? pair_kernel_q<T, VIS, false, true, true> : pair_kernel_q<T, VIS, false, false, true>;
-            else
-                kern = a.fq_cap ? pair_kernel_q<T, VIS, false, true, false> : pair_kernel_q<T, VIS, false, false, false>;
+            smem += size_t(a.lq_cap) * kTravThreads * sizeof(int32_t);
+            kern = hash ? pair_kernel_q<T, VIS, true, true>
+                        : (count ? pair_kernel_q<T, VIS, false, true> : pair_kernel_q<T, VIS, false, false>);
         }
     }
     check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)), "smem attr");

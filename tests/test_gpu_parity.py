@@ -141,7 +141,7 @@ def test_random_scene_tree_decisions(sd, oracle, prec, seed):
 @pytest.mark.parametrize("prec", [0, 1])
 @pytest.mark.parametrize("split", ["0", "1", "3", "6", "", "frontier", "frontier32",
                                    "defer0", "defer1", "defer32", "defer32cap1", "defer12cap3", "lb", "lb3",
-                                   "q3", "q3fq3", "q16fq8", "noq"])
+                                   "q3", "q16", "noq"])
 def test_split_traversal_decisions(sd, oracle, prec, split, monkeypatch):
     """The few-query traversal modes visit exactly the oracle's nodes:
     the slot split (one warp per (packet, depth-k slot) after re-testing the
@@ -151,17 +151,14 @@ def test_split_traversal_decisions(sd, oracle, prec, split, monkeypatch):
     handing entries of at most T lanes to per-lane stackless walks (a list
     of C entries per warp; a full list keeps the rest in the packet).
     "lb[k]": exact-leaf terms batched over the warp's lanes (split depth k).
-    "qL[fqF]": the unsplit walk with per-lane deferred queues of L exact
-    leaves [and F far-field terms] (K3Q; small queues force many rounds);
-    "noq": leaf terms inline."""
+    "qL": the unsplit walk with per-lane deferred queues of L exact leaves
+    (K3Q; small queues force many rounds); "noq": leaf terms inline."""
     O = oracle
     if split.startswith("q") or split == "noq":
         monkeypatch.setenv("SDGPU_FRONTIER", "0")
         monkeypatch.setenv("SDGPU_SPLIT", "0")
         monkeypatch.setenv("SDGPU_LEAF_QUEUE", "0" if split == "noq" else "1")
-        lq, _, fq = split[1:].partition("fq")
-        monkeypatch.setenv("SDGPU_LEAFQ", lq if split != "noq" else "16")
-        monkeypatch.setenv("SDGPU_FARQ", fq or "0")
+        monkeypatch.setenv("SDGPU_LEAFQ", split[1:] if split != "noq" else "16")
     elif split.startswith("frontier"):
         monkeypatch.setenv("SDGPU_FRONTIER", "1")
         monkeypatch.setenv("SDGPU_FRONTIER_G", split[8:] or "4")
@@ -283,8 +280,7 @@ def test_config_exact_parity(sd, oracle, cfg, prec, alphas, nq):
 
 
 @pytest.mark.parametrize("builder,kernel", [("median", "K3F"), ("lbvh", "K3F"), ("lbvh", "K3"), ("median", "K3D"),
-                                            ("median", "K3LB"), ("median", "K3"), ("median", "K3NQ"),
-                                            ("median", "K3FQ")])
+                                            ("median", "K3LB"), ("median", "K3"), ("median", "K3NQ")])
 def test_config4_tree_parity_subset(sd, oracle, builder, kernel, monkeypatch):
     """cfg4 (icosphere(9), 5.2M triangles, beta 0.5, alpha 200) on a query
     subset (both halves of the query distribution): decisions identical to
@@ -294,13 +290,11 @@ def test_config4_tree_parity_subset(sd, oracle, builder, kernel, monkeypatch):
     this batch size, K3 the one the full-size bench runs)."""
     O = oracle
     monkeypatch.setenv("SDGPU_FRONTIER", "1" if kernel == "K3F" else "0")
-    if kernel in ("K3", "K3NQ", "K3FQ"):
+    if kernel in ("K3", "K3NQ"):
         # the unsplit packet walk of the full-size batch: K3 = the default
-        # K3Q (deferred per-lane leaf queues), K3NQ = inline leaf terms, K3FQ
-        # = far-field terms queued too
+        # K3Q (deferred per-lane leaf queues), K3NQ = inline leaf terms
         monkeypatch.setenv("SDGPU_SPLIT", "0")
         monkeypatch.setenv("SDGPU_LEAF_QUEUE", "0" if kernel == "K3NQ" else "1")
-        monkeypatch.setenv("SDGPU_FARQ", "6" if kernel == "K3FQ" else "0")
     if kernel in ("K3D", "K3LB"):
         # the unsplit packet walk (the full-size kernel); K3D with deferred
         # per-lane tails (entries of <= 4 lanes), K3LB with batched leaf terms
