@@ -33,8 +33,8 @@ def val(name, scale=1.0):
         return None
     x = float(v.replace(",", ""))
     u = units.get(name, "")
-    mult = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "msecond": 1e-3, "usecond": 1e-6,
-            "nsecond": 1e-9, "second": 1}.get(u, 1)
+    mult = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12, "msecond": 1e-3, "ms": 1e-3,
+            "usecond": 1e-6, "us": 1e-6, "nsecond": 1e-9, "ns": 1e-9, "second": 1, "s": 1}.get(u, 1)
     return x * mult * scale
 
 
@@ -46,7 +46,8 @@ stamp = {
     "dram_bytes": (val("dram__bytes_read.sum") or 0) + (val("dram__bytes_write.sum") or 0),
     "dram_read_bytes": val("dram__bytes_read.sum"),
     "dram_write_bytes": val("dram__bytes_write.sum"),
-    "lts_bytes": val("lts__t_bytes.sum"),
+    "l2_hit_pct": val("lts__t_sector_hit_rate.pct"),
+    "l1_hit_pct": val("l1tex__t_sector_hit_rate.pct"),
     "warp_instructions": val("smsp__inst_executed.sum"),
     "issue_active_pct": val("smsp__issue_active.avg.pct_of_peak_sustained_active"),
     "avg_active_lanes": val("smsp__thread_inst_executed_per_inst_executed.ratio"),
