@@ -396,6 +396,8 @@ static void exact_query(Ctx& c, const T* q, int64_t Q, const sd_params& p, const
         if (score > best + 1e-9) best = score, splits = s;
         if (waves >= 1.0 && eff >= 0.97) break;
     }
+    if (const char* fs = std::getenv("SDGPU_EXACT_SPLITS"); fs && *fs)  // forced split count (tests, A/B)
+        splits = std::max<int64_t>(1, std::min<int64_t>(64, std::atoi(fs)));
     double* part = static_cast<double*>(c.part.ensure(size_t(splits) * 5 * Q * sizeof(double)));
     const Phys<T> ph = make_phys<T>(c, p);
     int64_t launches = 0;
@@ -405,6 +407,16 @@ static void exact_query(Ctx& c, const T* q, int64_t Q, const sd_params& p, const
     const int64_t* perm = sort_queries<T>(c, q, Q, c.scene_lo, c.scene_hi, st, launches, false);
     const double S = p.alpha / std::max(p.alpha, p.alpha_u);
     bool first = true;
+    // splits of a query block merge on chip (thread-block cluster, DSMEM)
+    // instead of each writing its fp64 partial state -- when each split's
+    // primitive range is short, so that the partial traffic is a visible
+    // share of the launch (cfg2: 20,000 edges / 8 splits; 168 -> 21 MB of
+    // partials, time unchanged). Long splits keep the free CTA scheduling:
+    // cfg3 (87k triangles per split) measured 974 ms without and 1021 ms
+    // with clusters. SDGPU_CLUSTER = 0 / 1 forces it off / on (2..8 splits).
+    const char* ce = std::getenv("SDGPU_CLUSTER");
+    const bool cluster = splits > 1 && splits <= 8 &&
+                         (ce && *ce ? *ce == '1' : maxcount / splits <= 4096);
     KernelTimer timer(c, st);
     for (const Segment& s : c.segs) {
         ExactLaunch<T> L;
@@ -414,6 +426,7 @@ static void exact_query(Ctx& c, const T* q, int64_t Q, const sd_params& p, const
         L.rec = c.rec[s.kind].as<T>() + s.offset * rec_size(s.kind);
         L.count = s.count;
         L.splits = int(splits);
+        L.cluster = cluster;
         const int64_t TILE = exact_tile_prims(s.kind);
         L.chunk = ((s.count + splits - 1) / splits + TILE - 1) / TILE * TILE;  // tile-aligned splits
         L.perm = perm;
@@ -438,7 +451,7 @@ static void exact_query(Ctx& c, const T* q, int64_t Q, const sd_params& p, const
         first = false;
     }
     timer.stop();
-    check_cuda(launch_finalize(part, int(splits), Q, p.alpha, p.epsilon, c.N, nullptr, nullptr, nullptr, perm,
+    check_cuda(launch_finalize(part, cluster ? 1 : int(splits), Q, p.alpha, p.epsilon, c.N, nullptr, nullptr, nullptr, perm,
                                   out, st),
                "finalize launch");
     c.last_launches = launches + 1;

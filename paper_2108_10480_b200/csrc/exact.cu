@@ -17,6 +17,7 @@
 #include "pair.cuh"
 #include "pair2.cuh"
 
+#include <cooperative_groups.h>
 #include <type_traits>
 
 namespace sdgpu {
@@ -35,7 +36,24 @@ struct ExactArgs {
     const int64_t* perm;  // sorted position -> query index
     const float4* tbox;   // tile boxes of the segment (null: no tile bounds)
     T lwmax, lwspan;      // log2 w upper bound and spread over the segment
+    int cluster;          // splits merged over DSMEM into split 0's partial
 };
+
+// Tot b folded into a (same anchor semantics as Tot::flush).
+__device__ __forceinline__ void tot_merge(Tot& a, const Tot& b) {
+    if (b.M == -INFINITY) return;
+    if (a.M == -INFINITY) {
+        a = b;
+        return;
+    }
+    const double M = fmax(a.M, b.M);
+    const double fa = exp2(a.M - M), fb = exp2(b.M - M);
+    a.s = fma(a.s, fa, b.s * fb);
+    a.gx = fma(a.gx, fa, b.gx * fb);
+    a.gy = fma(a.gy, fa, b.gy * fb);
+    a.gz = fma(a.gz, fa, b.gz * fb);
+    a.M = M;
+}
 
 // Tile bounds (per warp, per staged tile; see exact_kernel): terms of a
 // tile never exceed 2^kTileHeadroom relative to the shift after the
@@ -104,7 +122,7 @@ __global__ void __launch_bounds__(kThreads, MINB) exact_kernel(const __grid_cons
         acc[k].init();
         Tot& tk = tot[k * kThreads + threadIdx.x];
         tk.init();
-        if (!a.first) {
+        if (!a.first && (!a.cluster || split == 0)) {  // clusters: the merged state lives in split 0
             tk.M = part[qc];
             tk.s = part[a.Q + qc];
             tk.gx = part[2 * a.Q + qc];
@@ -243,6 +261,20 @@ __global__ void __launch_bounds__(kThreads, MINB) exact_kernel(const __grid_cons
         if (threadIdx.x == 0 && t + kStages < ntiles) issue(t + kStages);
     }
 
+    if (a.cluster) {  // fold the other splits' totals into split 0 over DSMEM
+        namespace cg = cooperative_groups;
+        cg::cluster_group cl = cg::this_cluster();
+        cl.sync();
+        if (split == 0) {
+            for (unsigned r = 1; r < cl.num_blocks(); ++r) {
+                const Tot* rt = cl.map_shared_rank(tot, r);
+#pragma unroll
+                for (int k = 0; k < QPT; ++k) tot_merge(tot[k * kThreads + threadIdx.x], rt[k * kThreads + threadIdx.x]);
+            }
+        }
+        cl.sync();  // the remote totals stay alive until split 0 has read them
+        if (split != 0) return;
+    }
 #pragma unroll
     for (int k = 0; k < QPT; ++k) {
         if (qi[k] >= a.Q) continue;
@@ -303,10 +335,26 @@ static cudaError_t launch_one(const ExactLaunch<T>& L, cudaStream_t st) {
         a.tbox = L.tbox;
         a.lwmax = L.lwmax;
         a.lwspan = L.lwspan;
+        a.cluster = L.cluster ? 1 : 0;
         const int64_t qblocks = (L.Q + int64_t(kThreads) * QPT - 1) / (int64_t(kThreads) * QPT);
         dim3 grid(unsigned(qblocks), unsigned(L.splits));
-        kern<<<grid, kThreads, smem, st>>>(a);
-        return cudaGetLastError();
+        if (!L.cluster) {
+            kern<<<grid, kThreads, smem, st>>>(a);
+            return cudaGetLastError();
+        }
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = grid;
+        cfg.blockDim = dim3(kThreads);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 1;
+        attr[0].val.clusterDim.y = unsigned(L.splits);
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        return cudaLaunchKernelEx(&cfg, kern, a);
     });
 }
 

@@ -18,6 +18,10 @@ struct ExactLaunch {
     int64_t count = 0;     // primitives in the segment
     int64_t chunk = 0;     // primitives per split
     int splits = 1;
+    // the split CTAs of a query block form one thread-block cluster and
+    // merge their per-query totals over distributed shared memory: only
+    // split 0's partial is written (splits <= 8)
+    bool cluster = false;
     const T* q = nullptr;
     int64_t Q = 0;
     double* part = nullptr;  // [splits][5][Q] fp64 partial state
