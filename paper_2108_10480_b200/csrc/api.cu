@@ -407,16 +407,15 @@ static void exact_query(Ctx& c, const T* q, int64_t Q, const sd_params& p, const
     const int64_t* perm = sort_queries<T>(c, q, Q, c.scene_lo, c.scene_hi, st, launches, false);
     const double S = p.alpha / std::max(p.alpha, p.alpha_u);
     bool first = true;
-    // splits of a query block merge on chip (thread-block cluster, DSMEM)
-    // instead of each writing its fp64 partial state -- when each split's
-    // primitive range is short, so that the partial traffic is a visible
-    // share of the launch (cfg2: 20,000 edges / 8 splits; 168 -> 21 MB of
-    // partials, time unchanged). Long splits keep the free CTA scheduling:
-    // cfg3 (87k triangles per split) measured 974 ms without and 1021 ms
-    // with clusters. SDGPU_CLUSTER = 0 / 1 forces it off / on (2..8 splits).
+    // SDGPU_CLUSTER=1: the split CTAs of a query block form one thread-block
+    // cluster (2..16 CTAs; more than 8 is a non-portable size, allowed on
+    // B200) and merge their fp64 totals over distributed shared memory, so
+    // that only split 0 writes a partial. Off by default: the partial round
+    // trip costs ~0.4 % of HBM bandwidth (cfg2: 252 MB over 6.9 ms), while
+    // cluster co-scheduling cost 32 % on cfg2 (12-CTA clusters: 9.19 vs
+    // 6.94 ms) and 5 % on cfg3 (3-CTA clusters: 1021 vs 974 ms).
     const char* ce = std::getenv("SDGPU_CLUSTER");
-    const bool cluster = splits > 1 && splits <= 8 &&
-                         (ce && *ce ? *ce == '1' : maxcount / splits <= 4096);
+    const bool cluster = splits > 1 && splits <= 16 && ce && *ce == '1';
     KernelTimer timer(c, st);
     for (const Segment& s : c.segs) {
         ExactLaunch<T> L;

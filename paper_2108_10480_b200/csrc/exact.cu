@@ -342,6 +342,10 @@ static cudaError_t launch_one(const ExactLaunch<T>& L, cudaStream_t st) {
             kern<<<grid, kThreads, smem, st>>>(a);
             return cudaGetLastError();
         }
+        if (L.splits > 8) {
+            e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+            if (e != cudaSuccess) return e;
+        }
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = grid;
         cfg.blockDim = dim3(kThreads);

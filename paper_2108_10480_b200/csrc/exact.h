@@ -20,7 +20,7 @@ struct ExactLaunch {
     int splits = 1;
     // the split CTAs of a query block form one thread-block cluster and
     // merge their per-query totals over distributed shared memory: only
-    // split 0's partial is written (splits <= 8)
+    // split 0's partial is written (splits <= 16)
     bool cluster = false;
     const T* q = nullptr;
     int64_t Q = 0;

@@ -959,16 +959,16 @@ def test_nan_query_coordinates_propagate_like_the_reference(sd, oracle, prec):
         assert_close(sub, ref, prec, 100.0, f"nan batch beta {beta}")
 
 
-@pytest.mark.parametrize("splits,cluster", [(1, "1"), (2, "1"), (3, "1"), (8, "1"), (9, "1"), (3, "0"), (8, "")])
+@pytest.mark.parametrize("splits,cluster", [(1, "1"), (2, "1"), (3, "1"), (8, "1"), (12, "1"), (16, "1"), (17, "1"),
+                                            (3, "0"), (8, "")])
 @pytest.mark.parametrize("cfg,prec", [(2, 0), (2, 1), (3, 0)])
 def test_exact_split_merge(sd, oracle, splits, cluster, cfg, prec, monkeypatch):
-    """The exact kernel's primitive splits: 2..8 split CTAs of a query block
+    """The exact kernel's primitive splits: 2..16 split CTAs of a query block
     form a thread-block cluster and merge their fp64 totals over distributed
     shared memory (only split 0 writes; the next segment launch continues
-    from it -- cfg2 has three weight-polynomial segments); 9 splits and
-    SDGPU_CLUSTER=0 write every split's partial for the finalize kernel;
-    "" = the automatic choice. Same results within the tolerance either
-    way."""
+    from it -- cfg2 has three weight-polynomial segments); 17 splits and
+    SDGPU_CLUSTER=0 (and "", the default) write every split's partial for
+    the finalize kernel. Same results within the tolerance either way."""
     O = oracle
     monkeypatch.setenv("SDGPU_EXACT_SPLITS", str(splits))
     monkeypatch.setenv("SDGPU_CLUSTER", cluster)
