@@ -753,6 +753,80 @@ struct PointVisit {
             dr = child(1, rid, rlink, lg.y);
         }
     }
+    // All pending leaf entries of the warp at once (called by the whole
+    // warp): item t (in the lanes' queue order) belongs to the owner lane o
+    // with excl[o] <= t < excl[o] + nq[o]; 32 items per round are spread
+    // over the 32 lanes, each evaluated for its owner's query (coordinates
+    // and shift by shuffle) into a partial relative to the owner's shift
+    // (raised only by a term above it). The items of one owner are
+    // contiguous, so a segmented max / sum over the lanes (starts known from
+    // excl) gives each owner one partial per round, merged into its
+    // accumulator. Per lane the terms are exactly the queued leaves'; only
+    // the summation order changes. lqw: the warp's lane-0 queue address.
+    __device__ __forceinline__ void leaf_flush_coop(const TraverseArgs<T>& a, const Poly<T>* polys, Acc<T>& acc,
+                                                    uint32_t lqw, int& nq, unsigned lane) const {
+        constexpr unsigned FULL = 0xffffffffu;
+        int incl = nq;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(FULL, incl, o);
+            if (int(lane) >= o) incl += y;
+        }
+        const int excl = incl - nq;
+        const int total = __shfl_sync(FULL, incl, 31);
+        for (int base = 0; base < total; base += 32) {
+            const int t = base + int(lane);
+            int o = 0;  // owner: the first lane whose inclusive count exceeds t
+#pragma unroll
+            for (int step = 16; step; step >>= 1)
+                if (__shfl_sync(FULL, incl, o + step - 1) <= t) o += step;
+            o &= 31;
+            const int oex = __shfl_sync(FULL, excl, o);
+            const T ox = __shfl_sync(FULL, qx, o), oy = __shfl_sync(FULL, qy, o), oz = __shfl_sync(FULL, qz, o);
+            Acc<T> it;
+            it.m = __shfl_sync(FULL, acc.m, o);
+            it.s = it.gx = it.gy = it.gz = T(0);
+            if (t < total) {
+                int slot;
+                asm volatile("ld.shared.s32 %0, [%1];"
+                             : "=r"(slot)
+                             : "r"(lqw + uint32_t(o) * 4u + uint32_t(t - oex) * kLeafStride));
+                leaf_term<T>(a, polys, slot, ox, oy, oz, it);
+            }
+            // segmented max of the shifts, then segmented sums, over the
+            // lanes of each owner's run in this round
+            const int s0 = max(oex - base, 0);  // this run's first lane
+            T m = it.m;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const T y = __shfl_up_sync(FULL, m, off);
+                if (int(lane) - off >= s0) m = fmax(m, y);
+            }
+            const int oend = min(__shfl_sync(FULL, incl, o), base + 32) - 1 - base;  // run's last lane
+            m = __shfl_sync(FULL, m, oend);
+            const T f = t >= total ? T(0) : (it.m == m ? T(1) : Math<T>::ex2(it.m - m));
+            T v0 = it.s * f, v1 = it.gx * f, v2 = it.gy * f, v3 = it.gz * f;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const T y0 = __shfl_up_sync(FULL, v0, off), y1 = __shfl_up_sync(FULL, v1, off),
+                        y2 = __shfl_up_sync(FULL, v2, off), y3 = __shfl_up_sync(FULL, v3, off);
+                if (int(lane) - off >= s0) {
+                    v0 += y0;
+                    v1 += y1;
+                    v2 += y2;
+                    v3 += y3;
+                }
+            }
+            // each owner collects its run's total from the run's last lane
+            const int my_lo = excl - base, my_hi = min(incl, base + 32) - 1 - base;
+            const bool mine = nq > 0 && my_lo < 32 && my_hi >= 0 && my_hi >= my_lo;
+            const int src = mine ? my_hi : 0;
+            const T rm = __shfl_sync(FULL, m, src), r0 = __shfl_sync(FULL, v0, src), r1 = __shfl_sync(FULL, v1, src),
+                    r2 = __shfl_sync(FULL, v2, src), r3 = __shfl_sync(FULL, v3, src);
+            if (mine && r0 != T(0)) merge_partial(acc, rm, r0, r1, r2, r3);
+        }
+        nq = 0;
+    }
     __device__ __forceinline__ void leaf_round(const TraverseArgs<T>& a, const Poly<T>* polys, int slot,
                                                Acc<T>& acc) const {
         leaf_term<T>(a, polys, slot, qx, qy, qz, acc);

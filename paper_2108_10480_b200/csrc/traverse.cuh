@@ -87,8 +87,11 @@ struct TraverseArgs {
     // pre-order subtree, the popcount threshold and the per-warp capacity
     const int32_t* esc = nullptr;
     int defer_t = 0, defer_cap = 0;
-    // K3Q leaf-queue capacity (entries per lane)
+    // K3Q leaf-queue capacity (entries per lane); leaf_coop: the queued
+    // terms are evaluated by the whole warp (leaf_flush_coop) instead of
+    // one per lane per round
     int lq_cap = 0;
+    int leaf_coop = 0;
 };
 
 constexpr int kTravThreads = 128;
@@ -388,7 +391,8 @@ __global__ void __launch_bounds__(kTravThreads, sizeof(T) == 4 ? 8 : 4)
 // most two) and the queues are drained after the walk. Per lane the set of
 // terms is exactly collect_contributions'; only their summation order
 // changes (fp32 rounding).
-constexpr int kLeafQ = 40;  // default leaf queue entries per lane (SDGPU_LEAFQ)
+constexpr int kLeafQ = 40;      // default leaf queue entries per lane (SDGPU_LEAFQ), per-lane rounds
+constexpr int kLeafQCoop = 24;  // the same with the warp-cooperative flush (fp32 default)
 
 // Counter type of walks whose per-query counters were not asked for.
 struct NoCount {
@@ -397,7 +401,7 @@ struct NoCount {
 constexpr uint32_t kLeafStride = kTravThreads * 4;  // bytes between a lane's leaf entries
 
 
-template <class T, class VIS, bool HASH, bool COUNT>
+template <class T, class VIS, bool HASH, bool COUNT, bool COOP>
 __device__ __forceinline__ void pair_walk_q(const TraverseArgs<T>& a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Poly<T>* polys = reinterpret_cast<Poly<T>*>(smem_raw);
@@ -413,6 +417,7 @@ __device__ __forceinline__ void pair_walk_q(const TraverseArgs<T>& a) {
     const unsigned warp = threadIdx.x >> 5;
     int4* st = stacks + warp * a.stack_depth;
     const uint32_t lq0 = smem_u32(lqs + threadIdx.x);  // this lane's entry 0 (entries kLeafStride apart)
+    const uint32_t lqw = smem_u32(lqs + (threadIdx.x & ~31u));  // the warp's lane 0
     const int lcap = a.lq_cap - 1;  // a step appends at most two entries per lane
     int nq = 0;  // pending leaf entries of this lane
     const int64_t packet = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
@@ -480,10 +485,14 @@ __device__ __forceinline__ void pair_walk_q(const TraverseArgs<T>& a) {
             mask = 0u;
         }
         if (full) {
-            while (__any_sync(FULL, nq >= lcap)) round();
+            if constexpr (COOP) qv.leaf_flush_coop(a, polys, acc, lqw, nq, lane);
+            else
+                while (__any_sync(FULL, nq >= lcap)) round();
         }
     }
-    while (__any_sync(FULL, nq > 0)) round();
+    if constexpr (COOP) qv.leaf_flush_coop(a, polys, acc, lqw, nq, lane);
+    else
+        while (__any_sync(FULL, nq > 0)) round();
     if (!valid) return;
     Tot tot;
     tot.init();
@@ -500,9 +509,9 @@ __device__ __forceinline__ void pair_walk_q(const TraverseArgs<T>& a) {
     if (HASH) a.hash[i] = h;
 }
 
-template <class T, class VIS, bool HASH, bool COUNT>
+template <class T, class VIS, bool HASH, bool COUNT, bool COOP = false>
 __global__ void __launch_bounds__(kTravThreads) pair_kernel_q(const __grid_constant__ TraverseArgs<T> a) {
-    pair_walk_q<T, VIS, HASH, COUNT || HASH>(a);
+    pair_walk_q<T, VIS, HASH, COUNT || HASH, COOP>(a);
 }
 
 // K3F (few queries, node-parallel): a group of G lanes per query (32 / G
@@ -717,11 +726,21 @@ int launch_pair_traversal(Ctx& c, DeviceTree& t, TraverseArgs<T>& a, bool hash, 
         const char* lqe = std::getenv("SDGPU_LEAF_QUEUE");
         const bool lq_on = !(lqe && *lqe == '0');
         const char* lb = std::getenv("SDGPU_LEAF_BATCH");
-        a.lq_cap = std::max(3, cap("SDGPU_LEAFQ", kLeafQ));
+        // SDGPU_LEAF_COOP = 1 / 0: queued leaf terms evaluated by the whole
+        // warp (leaf_flush_coop) / one per lane per round; default: the
+        // cooperative flush in fp32 (cfg4 21.9 -> 20.4 ms), per-lane rounds
+        // in fp64 (52.5 vs 55.5 ms)
+        const char* lce = std::getenv("SDGPU_LEAF_COOP");
+        a.leaf_coop = (lce && *lce) ? (*lce == '1' ? 1 : 0) : (sizeof(T) == 4 ? 1 : 0);
+        a.lq_cap = std::max(3, cap("SDGPU_LEAFQ", a.leaf_coop ? kLeafQCoop : kLeafQ));
         if (lq_on && k == 0 && !defer && !(lb && *lb == '1')) {
             smem += size_t(a.lq_cap) * kTravThreads * sizeof(int32_t);
-            kern = hash ? pair_kernel_q<T, VIS, true, true>
-                        : (count ? pair_kernel_q<T, VIS, false, true> : pair_kernel_q<T, VIS, false, false>);
+            if (a.leaf_coop)
+                kern = hash ? pair_kernel_q<T, VIS, true, true, true>
+                            : (count ? pair_kernel_q<T, VIS, false, true, true> : pair_kernel_q<T, VIS, false, false, true>);
+            else
+                kern = hash ? pair_kernel_q<T, VIS, true, true>
+                            : (count ? pair_kernel_q<T, VIS, false, true> : pair_kernel_q<T, VIS, false, false>);
         }
     }
     check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)), "smem attr");

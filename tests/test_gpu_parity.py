@@ -141,7 +141,7 @@ def test_random_scene_tree_decisions(sd, oracle, prec, seed):
 @pytest.mark.parametrize("prec", [0, 1])
 @pytest.mark.parametrize("split", ["0", "1", "3", "6", "", "frontier", "frontier32",
                                    "defer0", "defer1", "defer32", "defer32cap1", "defer12cap3", "lb", "lb3",
-                                   "q3", "q16", "noq"])
+                                   "q3", "q16", "noq", "coop3", "coop24", "lanes40"])
 def test_split_traversal_decisions(sd, oracle, prec, split, monkeypatch):
     """The few-query traversal modes visit exactly the oracle's nodes:
     the slot split (one warp per (packet, depth-k slot) after re-testing the
@@ -152,9 +152,16 @@ def test_split_traversal_decisions(sd, oracle, prec, split, monkeypatch):
     of C entries per warp; a full list keeps the rest in the packet).
     "lb[k]": exact-leaf terms batched over the warp's lanes (split depth k).
     "qL": the unsplit walk with per-lane deferred queues of L exact leaves
-    (K3Q; small queues force many rounds); "noq": leaf terms inline."""
+    (K3Q; small queues force many flushes); "noq": leaf terms inline;
+    "coopL" / "lanesL": the warp-cooperative flush / per-lane rounds."""
     O = oracle
-    if split.startswith("q") or split == "noq":
+    if split.startswith("coop") or split.startswith("lanes"):
+        monkeypatch.setenv("SDGPU_FRONTIER", "0")
+        monkeypatch.setenv("SDGPU_SPLIT", "0")
+        monkeypatch.setenv("SDGPU_LEAF_QUEUE", "1")
+        monkeypatch.setenv("SDGPU_LEAF_COOP", "1" if split.startswith("coop") else "0")
+        monkeypatch.setenv("SDGPU_LEAFQ", split.lstrip("coplanes"))
+    elif split.startswith("q") or split == "noq":
         monkeypatch.setenv("SDGPU_FRONTIER", "0")
         monkeypatch.setenv("SDGPU_SPLIT", "0")
         monkeypatch.setenv("SDGPU_LEAF_QUEUE", "0" if split == "noq" else "1")
