@@ -258,14 +258,25 @@ def compute_peak(peaks, sm_mhz, fp64: bool):
     return cands[src], src, cands
 
 
-def source_hash() -> str:
-    """Hash of the CUDA sources: ncu figures stamped with another hash are
-    stale and not reported."""
+# the CUDA sources each stamped kernel is built from
+STAMP_SOURCES = {
+    "exact": ("exact.cu", "exact.h", "pair.cuh", "pair2.cuh", "device_common.cuh", "api.cu", "context.h"),
+    "bvh": ("bvh.cu", "traverse.cuh", "layout.cu", "pair.cuh", "pair2.cuh", "device_common.cuh", "api.cu",
+            "context.h", "exact.h"),
+}
+
+
+def source_hash(kind: str | None = None) -> str:
+    """Hash of the CUDA sources of a kernel family (all of csrc/ without
+    `kind`): ncu figures stamped with another hash are stale and not
+    reported."""
     h = hashlib.sha256()
-    for p in sorted(glob.glob(os.path.join(ROOT, "paper_2108_10480_b200", "csrc", "*"))):
-        if p.endswith((".cu", ".cuh", ".h", ".cpp")):
-            with open(p, "rb") as f:
-                h.update(os.path.basename(p).encode() + f.read())
+    csrc = os.path.join(ROOT, "paper_2108_10480_b200", "csrc")
+    names = STAMP_SOURCES[kind] if kind else sorted(os.path.basename(p) for p in glob.glob(os.path.join(csrc, "*")))
+    for n in names:
+        if n.endswith((".cu", ".cuh", ".h", ".cpp")):
+            with open(os.path.join(csrc, n), "rb") as f:
+                h.update(n.encode() + f.read())
     return h.hexdigest()[:16]
 
 
@@ -279,7 +290,7 @@ def ncu_stamp(kernel_key: str):
     except (OSError, ValueError):
         return None
     e = st.get(kernel_key)
-    if not e or e.get("src_sha") != source_hash():
+    if not e or e.get("src_sha") != source_hash(kernel_key.split("_")[0]):
         return None
     return e
 

@@ -40,7 +40,7 @@ def val(name, scale=1.0):
 
 stamp = {
     "kernel": d["Kernel Name"],
-    "src_sha": bench.source_hash(),
+    "src_sha": bench.source_hash(key.split("_")[0]),
     "capture": os.path.relpath(rep, ROOT),
     "duration_s": val("gpu__time_duration.sum"),
     "dram_bytes": (val("dram__bytes_read.sum") or 0) + (val("dram__bytes_write.sum") or 0),
