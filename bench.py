@@ -411,7 +411,7 @@ def parity_stats(got_d, got_g, ref_d, ref_g, alpha, dtype):
     got_d, ref_d = np.asarray(got_d, np.float64), np.asarray(ref_d, np.float64)
     fr, fg = np.isfinite(ref_d), np.isfinite(got_d)
     both = fr & fg
-    dd = np.abs(got_d - ref_d)[both]
+    dd = np.abs(got_d[both] - ref_d[both])
     rd = np.abs(ref_d[both])
     out = {"n": int(len(ref_d)), "finite": int(both.sum()), "inf_mismatch": int((fr != fg).sum()),
            "tol_d_hat": td, "tol_grad": tg}
@@ -589,6 +589,31 @@ def run_exact_headline(args, run, peaks, stream, flush, line):
         line[key] = r
         res2[prec] = (d, g)
         e.close()
+    # ---- cfg1 point cloud (BASELINE configs[0]), fp64 as specified
+    from paper_2108_10480_b200 import configs as cf
+    w1, q1 = cf.cfg1()
+    lo, hi = strong_blocks(len(q1), world)[rank]
+    qb1 = q1[lo:hi]
+    wt1 = cf.weights_without_triangles(w1.simplices, w1.kinds, len(w1.vertices))
+    e1 = sd.Engine(run.local, sd.SD_FP64)
+    e1.set_geometry(w1.vertices, w1.simplices, w1.kinds)
+    e1.set_weights(wt1.A, wt1.sup_wtilde, wt1.edge_a, wt1.tri_stored, wt1.poly_index)
+    P1 = sd.SmoothParams(alpha=w1.alpha, alpha_u=600.0, beta=0.0)
+    r1, d1, g1 = exact_leg(run, e1, qb1, sd.SD_FP64, len(w1.kinds), 0, P1, args.steps, args.warmup, flush, stream, peaks,
+                           e2e_steps=3, q_total=len(q1))
+    r1["workload"] = "cfg1: 4,096 unit-sphere points x 65,536 queries, exact LSE, alpha=50, fp64 (BASELINE configs[0])"
+    line["exact_cfg1_fp64"] = r1
+    e1.close()
+    if rank == 0 and not args.no_cpu:
+        arm1 = CpuArm(w1.vertices, w1.simplices, w1.kinds, wt1)
+        n1, rr1 = cpu_exact_sample(arm1, qb1, w1.alpha, 4.0)
+        par["exact_cfg1_fp64"] = parity_stats(d1[:n1], g1[:n1], rr1.d_hat, rr1.grad, w1.alpha, "f64")
+        par["exact_cfg1_fp64"]["sample"] = f"first {n1} timed queries of rank 0's block"
+        cpu1 = {"value": n1 * len(w1.kinds) / rr1.seconds, "unit": "pair-evals/s", "cores": arm1.threads,
+                "kind": arm1.kind, "sample": f"first {n1} cfg1 queries x 4,096 points ({rr1.seconds:.1f} s, fp64)"}
+        line["exact_cfg1_fp64"]["cpu_baseline"] = cpu1
+        if world == 1:
+            line["exact_cfg1_fp64"]["vs_cpu_baseline"] = r1["value"] / cpu1["value"]
     if rank == 0 and not args.no_cpu:
         # the oracle port on a ~7 s prefix of the timed cfg2 queries: the cfg2
         # cpu baseline at the reference's precision and the parity reference
