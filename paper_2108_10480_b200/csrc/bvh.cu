@@ -648,11 +648,19 @@ __device__ __forceinline__ bool visit(const TraverseArgs<T>& a, const Poly<T>* p
     return false;
 }
 
+// The fp32 K3Q walk keeps each lane's shift relative to log2 w_ff (the
+// far-field weight), so that a far-field term's exponent is kappa d +
+// log2 n_B - m without adding log2 w_ff per term; leaf terms convert.
+template <class T>
+constexpr bool kFarFrame = sizeof(T) == 4;
+
 // The point query of one lane (K3's VIS for bvh.cu).
 template <class T>
 struct PointVisit {
     static constexpr bool kLeafBatch = true;
     static constexpr bool kLeafQueue = true;
+    template <class U>
+    static constexpr bool kFrame = kFarFrame<U>;
     T qx, qy, qz;
     __device__ __forceinline__ void load(const TraverseArgs<T>& a, int64_t qi, bool valid) {
         qx = valid ? a.q[3 * qi] : T(0);
@@ -735,7 +743,7 @@ struct PointVisit {
                 }
                 if (far) {
                     const float r = Math<float>::rsqrt(fmaxf(s, 1e-30f));
-                    far_term(a.ph, lgc + a.lw_ff, s * r, r, hh ? hi(dx) : lo(dx), hh ? hi(dy) : lo(dy),
+                    far_term(a.ph, lgc, s * r, r, hh ? hi(dx) : lo(dx), hh ? hi(dy) : lo(dy),
                              hh ? hi(dz) : lo(dz), acc);
                     ++nfar;
                     if constexpr (HASH) h += decision_mix(uint64_t(id), 1);
@@ -766,6 +774,7 @@ struct PointVisit {
     __device__ __forceinline__ void leaf_flush_coop(const TraverseArgs<T>& a, const Poly<T>* polys, Acc<T>& acc,
                                                     uint32_t lqw, int& nq, unsigned lane) const {
         constexpr unsigned FULL = 0xffffffffu;
+        const T frame = kFarFrame<T> ? a.lw_ff : T(0);  // acc.m is kept relative to log2 w_ff (fp32 walk)
         int incl = nq;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -784,7 +793,7 @@ struct PointVisit {
             const int oex = __shfl_sync(FULL, excl, o);
             const T ox = __shfl_sync(FULL, qx, o), oy = __shfl_sync(FULL, qy, o), oz = __shfl_sync(FULL, qz, o);
             Acc<T> it;
-            it.m = __shfl_sync(FULL, acc.m, o);
+            it.m = __shfl_sync(FULL, acc.m, o) + frame;
             it.s = it.gx = it.gy = it.gz = T(0);
             if (t < total) {
                 int slot;
@@ -823,13 +832,15 @@ struct PointVisit {
             const int src = mine ? my_hi : 0;
             const T rm = __shfl_sync(FULL, m, src), r0 = __shfl_sync(FULL, v0, src), r1 = __shfl_sync(FULL, v1, src),
                     r2 = __shfl_sync(FULL, v2, src), r3 = __shfl_sync(FULL, v3, src);
-            if (mine && r0 != T(0)) merge_partial(acc, rm, r0, r1, r2, r3);
+            if (mine && r0 != T(0)) merge_partial(acc, rm - frame, r0, r1, r2, r3);
         }
         nq = 0;
     }
     __device__ __forceinline__ void leaf_round(const TraverseArgs<T>& a, const Poly<T>* polys, int slot,
                                                Acc<T>& acc) const {
+        if constexpr (kFarFrame<T>) acc.m += a.lw_ff;
         leaf_term<T>(a, polys, slot, qx, qy, qz, acc);
+        if constexpr (kFarFrame<T>) acc.m -= a.lw_ff;
     }
     template <bool HASH, class CNT>
     __device__ __forceinline__ bool far_test(const TraverseArgs<T>& a, const NodeT<T>& b, int32_t id, T lgc, bool emit,

@@ -596,6 +596,8 @@ __device__ __forceinline__ Geom load_query(const double* qg, const int32_t* qd, 
 struct SimplexVisit {
     static constexpr bool kLeafBatch = false;  // per-lane QP leaves: no batched flush
     static constexpr bool kLeafQueue = false;  // (nor deferred leaf queues)
+    template <class U>
+    static constexpr bool kFrame = false;
     sx::Geom g;
     __device__ __forceinline__ void load(const TraverseArgs<double>& a, int64_t qi, bool valid) {
         g = sx::load_query(a.qgeom, a.qdim, qi, valid);

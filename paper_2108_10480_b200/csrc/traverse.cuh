@@ -441,6 +441,7 @@ __device__ __forceinline__ void pair_walk_q(const TraverseArgs<T>& a) {
         const bool d = valid && qv.template visit_q<HASH>(a, b0, 0, a.lgcount[0], acc, nleaf, nfar, h, nre, lq0, nq);
         mask = __ballot_sync(FULL, d);
     }
+    if constexpr (VIS::template kFrame<T>) acc.m -= a.lw_ff;  // see PointVisit (-inf stays -inf)
     auto round = [&]() {
         if (nq > 0) {
             --nq;
@@ -494,6 +495,7 @@ __device__ __forceinline__ void pair_walk_q(const TraverseArgs<T>& a) {
     else
         while (__any_sync(FULL, nq > 0)) round();
     if (!valid) return;
+    if constexpr (VIS::template kFrame<T>) acc.m += a.lw_ff;
     Tot tot;
     tot.init();
     tot.flush(acc);
