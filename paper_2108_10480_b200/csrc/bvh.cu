@@ -691,7 +691,7 @@ struct PointVisit {
             }
         }
         if (link >= 0) return true;
-        asm volatile("st.shared.s32 [%0], %1;" ::"r"(lq0 + uint32_t(nq) * kLeafStride), "r"(-link - 1) : "memory");
+        asm volatile("st.shared.s32 [%0], %1;" ::"r"(lq0 + uint32_t(nq) * kLeafStride), "r"(link) : "memory");
         ++nq;
         ++nleaf;
         if constexpr (HASH) h += decision_mix(uint64_t(id), 2);
@@ -750,7 +750,7 @@ struct PointVisit {
                     return false;
                 }
                 if (link >= 0) return true;
-                asm volatile("st.shared.s32 [%0], %1;" ::"r"(lq0 + uint32_t(nq) * kLeafStride), "r"(-link - 1)
+                asm volatile("st.shared.s32 [%0], %1;" ::"r"(lq0 + uint32_t(nq) * kLeafStride), "r"(link)
                              : "memory");
                 ++nq;
                 ++nleaf;
@@ -800,7 +800,7 @@ struct PointVisit {
                 asm volatile("ld.shared.s32 %0, [%1];"
                              : "=r"(slot)
                              : "r"(lqw + uint32_t(o) * 4u + uint32_t(t - oex) * kLeafStride));
-                leaf_term<T>(a, polys, slot, ox, oy, oz, it);
+                leaf_term<T>(a, polys, -slot - 1, ox, oy, oz, it);  // queued: the leaf link -(slot + 1)
             }
             // segmented max of the shifts, then segmented sums, over the
             // lanes of each owner's run in this round
@@ -836,10 +836,10 @@ struct PointVisit {
         }
         nq = 0;
     }
-    __device__ __forceinline__ void leaf_round(const TraverseArgs<T>& a, const Poly<T>* polys, int slot,
+    __device__ __forceinline__ void leaf_round(const TraverseArgs<T>& a, const Poly<T>* polys, int link,
                                                Acc<T>& acc) const {
         if constexpr (kFarFrame<T>) acc.m += a.lw_ff;
-        leaf_term<T>(a, polys, slot, qx, qy, qz, acc);
+        leaf_term<T>(a, polys, -link - 1, qx, qy, qz, acc);  // queued: the leaf link -(slot + 1)
         if constexpr (kFarFrame<T>) acc.m -= a.lw_ff;
     }
     template <bool HASH, class CNT>
