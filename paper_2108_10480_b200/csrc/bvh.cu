@@ -281,248 +281,6 @@ __device__ __forceinline__ bool decide64(const NodeT<T>& b, double d64, double q
     return d > 0.0 && d64 < __dmul_rn(beta, d);
 }
 
-template <class T>
-__global__ void __launch_bounds__(kTravThreads) traverse_kernel(const __grid_constant__ TraverseArgs<T> a) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    // polynomial table first, then the per-thread stacks [depth][threads]
-    Poly<T>* polys = reinterpret_cast<Poly<T>*>(smem_raw);
-    int32_t* stack = reinterpret_cast<int32_t*>(smem_raw + poly_bytes<T>(a.npoly));
-    for (int i = threadIdx.x; i < a.npoly * kPolyCoefs; i += blockDim.x)
-        reinterpret_cast<T*>(polys)[i] = reinterpret_cast<const T*>(a.polys)[i];
-    __syncthreads();
-
-    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i >= a.Q) return;
-    const int64_t qi = a.perm ? a.perm[i] : i;
-    const T qx = a.q[3 * qi], qy = a.q[3 * qi + 1], qz = a.q[3 * qi + 2];
-    Acc<T> acc;
-    acc.init();
-    int32_t nleaf = 0, nfar = 0;  // per query: < 2^31 nodes
-    uint64_t h = 0;
-    unsigned long long nre = 0;
-    int sp = 0;
-    int32_t id = 0;
-    const T beta = a.ph.beta;
-    while (true) {
-        const NodeT<T> b = a.box[id];
-        int32_t link;
-        memcpy(&link, &b.v[7], sizeof(int32_t));
-        if (a.use_bh) {
-            const T yx = fmin(fmax(qx, b.v[0]), b.v[4]);
-            const T yy = fmin(fmax(qy, b.v[1]), b.v[5]);
-            const T yz = fmin(fmax(qz, b.v[2]), b.v[6]);
-            const T dx = qx - yx, dy = qy - yy, dz = qz - yz;
-            const T s = fma(dx, dx, fma(dy, dy, dz * dz));
-            bool far;
-            if constexpr (sizeof(T) == 4) {
-                const T r = s > T(0) ? Math<T>::rsqrt(s) : T(0);
-                const T d = s * r;
-                const T rhs = beta * d;
-                const T band = T(1e-5) * rhs;
-                if (s == T(0) && a.exact_boxes) far = false;  // contact: d_B = 0 exactly
-                else if (b.v[3] < rhs - band) far = true;
-                else if (b.v[3] > rhs + band) far = false;
-                else {
-                    far = decide64(b, a.diam64[id], double(qx), double(qy), double(qz), a.beta64);
-                    ++nre;
-                }
-                if (far) far_term(a.ph, a.lgcount[id] + a.lw_ff, d, r, dx, dy, dz, acc);
-            } else {
-                far = decide64(b, a.diam64[id], double(qx), double(qy), double(qz), a.beta64);
-                if (far) {
-                    const T d = sqrt(s);
-                    far_term(a.ph, a.lgcount[id] + a.lw_ff, d, T(1) / d, dx, dy, dz, acc);
-                }
-            }
-            if (far) {
-                ++nfar;
-                h += decision_mix(uint64_t(id), 1);
-                if (sp == 0) break;
-                id = stack[(--sp) * kTravThreads + threadIdx.x];
-                continue;
-            }
-        }
-        if (link < 0) {  // exact leaf (smooth.hpp:122-124)
-            const int slot = -link - 1;
-            const int meta = a.leafmeta[slot];
-            const int kind = meta & 3, poly = (meta >> 2) - 1;
-            T rec[kRecTri];
-            using V = typename Vec4<T>::type;
-            const V* src = reinterpret_cast<const V*>(a.leafrec + size_t(slot) * kRecTri);
-            if (kind == 0) {
-                for (int j = 0; j < kRecPoint * int(sizeof(T)) / int(sizeof(V)); ++j) reinterpret_cast<V*>(rec)[j] = src[j];
-                acc.m -= a.ph.lw_unit;  // unit-weight terms take the shift relative to S log2 A
-                point_term(a.ph, qx, qy, qz, rec[0], rec[1], rec[2], acc);
-                acc.m += a.ph.lw_unit;
-            } else if (kind == 1) {
-#pragma unroll
-                for (int j = 0; j < kRecEdge * int(sizeof(T)) / int(sizeof(V)); ++j) reinterpret_cast<V*>(rec)[j] = src[j];
-                if (poly >= 0) edge_term<T, true, false>(a.ph, polys[poly], qx, qy, qz, rec, acc);
-                else unit_term<T, 1>(a.ph, polys[0], qx, qy, qz, rec, acc);
-            } else {
-#pragma unroll
-                for (int j = 0; j < kRecTri * int(sizeof(T)) / int(sizeof(V)); ++j) reinterpret_cast<V*>(rec)[j] = src[j];
-                if (poly >= 0) tri_term<T, true, false>(a.ph, polys[a.ne + poly], qx, qy, qz, rec, acc);
-                else unit_term<T, 2>(a.ph, polys[0], qx, qy, qz, rec, acc);
-            }
-            ++nleaf;
-            h += decision_mix(uint64_t(id), 2);
-            if (sp == 0) break;
-            id = stack[(--sp) * kTravThreads + threadIdx.x];
-        } else {  // descend: left (id + 1) next, right on the stack
-            stack[(sp++) * kTravThreads + threadIdx.x] = link;
-            id = id + 1;
-        }
-    }
-    Tot tot;
-    tot.init();
-    tot.flush(acc);
-    a.part[i] = tot.M;
-    a.part[a.Q + i] = tot.s;
-    a.part[2 * a.Q + i] = tot.gx;
-    a.part[3 * a.Q + i] = tot.gy;
-    a.part[4 * a.Q + i] = tot.gz;
-    a.leaves[i] = nleaf;
-    a.far[i] = nfar;
-    a.hash[i] = h;
-    if (nre) atomicAdd(a.rechecks, nre);
-}
-
-// K3 (default): warp-coherent packet traversal. The 32 Morton-adjacent
-// queries of a warp walk ONE node sequence; each node carries the mask of
-// lanes whose own traversal reaches it, every active lane makes exactly its
-// reference decision at that node (far field / exact leaf / descend), and
-// the warp descends into a child iff some lane descends. So each lane
-// visits precisely the nodes collect_contributions (smooth.hpp:101-131)
-// visits for its query, while node and leaf records are fetched once per
-// warp (broadcast loads) and control flow stays warp-uniform. The stack of
-// (node, lane mask) pairs lives in shared memory, one per warp.
-template <class T, bool HASH>
-__global__ void __launch_bounds__(kTravThreads) packet_kernel(const __grid_constant__ TraverseArgs<T> a) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    Poly<T>* polys = reinterpret_cast<Poly<T>*>(smem_raw);
-    int2* stacks = reinterpret_cast<int2*>(smem_raw + poly_bytes<T>(a.npoly));
-    for (int i = threadIdx.x; i < a.npoly * kPolyCoefs; i += blockDim.x)
-        reinterpret_cast<T*>(polys)[i] = reinterpret_cast<const T*>(a.polys)[i];
-    __syncthreads();
-
-    const unsigned lane = threadIdx.x & 31u;
-    int2* st = stacks + (threadIdx.x >> 5) * a.stack_depth;
-    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    const bool valid = i < a.Q;
-    const int64_t qi = valid ? (a.perm ? a.perm[i] : i) : 0;
-    const T qx = valid ? a.q[3 * qi] : T(0), qy = valid ? a.q[3 * qi + 1] : T(0), qz = valid ? a.q[3 * qi + 2] : T(0);
-    unsigned mask = __ballot_sync(0xffffffffu, valid);
-    if (mask == 0u) return;
-    Acc<T> acc;
-    acc.init();
-    int32_t nleaf = 0, nfar = 0;  // per query: < 2^31 nodes
-    uint64_t h = 0;
-    unsigned long long nre = 0;
-    int sp = 0;
-    int32_t id = 0;
-    const T beta = a.ph.beta;
-    while (true) {
-        const NodeT<T> b = a.box[id];  // warp-uniform address: one broadcast
-        int32_t link;
-        memcpy(&link, &b.v[7], sizeof(int32_t));
-        bool desc = false;
-        if ((mask >> lane) & 1u) {
-            bool far = false;
-            if (a.use_bh) {
-                const T yx = fmin(fmax(qx, b.v[0]), b.v[4]);
-                const T yy = fmin(fmax(qy, b.v[1]), b.v[5]);
-                const T yz = fmin(fmax(qz, b.v[2]), b.v[6]);
-                const T dx = qx - yx, dy = qy - yy, dz = qz - yz;
-                const T s = fma(dx, dx, fma(dy, dy, dz * dz));
-                if constexpr (sizeof(T) == 4) {
-                    const T r = s > T(0) ? Math<T>::rsqrt(s) : T(0);
-                    const T d = s * r;
-                    const T rhs = beta * d;
-                    const T band = T(1e-5) * rhs;
-                    if (s == T(0) && a.exact_boxes) far = false;
-                    else if (b.v[3] < rhs - band) far = true;
-                    else if (b.v[3] > rhs + band) far = false;
-                    else {
-                        far = decide64(b, a.diam64[id], double(qx), double(qy), double(qz), a.beta64);
-                        ++nre;
-                    }
-                    if (far) far_term(a.ph, a.lgcount[id] + a.lw_ff, d, r, dx, dy, dz, acc);
-                } else {
-                    far = decide64(b, a.diam64[id], double(qx), double(qy), double(qz), a.beta64);
-                    if (far) {
-                        const T d = sqrt(s);
-                        far_term(a.ph, a.lgcount[id] + a.lw_ff, d, T(1) / d, dx, dy, dz, acc);
-                    }
-                }
-                if (far) {
-                    ++nfar;
-                    if constexpr (HASH) h += decision_mix(uint64_t(id), 1);
-                }
-            }
-            if (!far) {
-                if (link < 0) {  // exact leaf: the record is the same for every lane
-                    const int slot = -link - 1;
-                    const int meta = a.leafmeta[slot];
-                    const int kind = meta & 3, poly = (meta >> 2) - 1;
-                    T rec[kRecTri];
-                    using V = typename Vec4<T>::type;
-                    const V* src = reinterpret_cast<const V*>(a.leafrec + size_t(slot) * kRecTri);
-                    if (kind == 0) {
-                        for (int j = 0; j < kRecPoint * int(sizeof(T)) / int(sizeof(V)); ++j) reinterpret_cast<V*>(rec)[j] = src[j];
-                        acc.m -= a.ph.lw_unit;
-                        point_term(a.ph, qx, qy, qz, rec[0], rec[1], rec[2], acc);
-                        acc.m += a.ph.lw_unit;
-                    } else if (kind == 1) {
-#pragma unroll
-                        for (int j = 0; j < kRecEdge * int(sizeof(T)) / int(sizeof(V)); ++j)
-                            reinterpret_cast<V*>(rec)[j] = src[j];
-                        if (poly >= 0) edge_term<T, true, false>(a.ph, polys[poly], qx, qy, qz, rec, acc);
-                        else unit_term<T, 1>(a.ph, polys[0], qx, qy, qz, rec, acc);
-                    } else {
-#pragma unroll
-                        for (int j = 0; j < kRecTri * int(sizeof(T)) / int(sizeof(V)); ++j)
-                            reinterpret_cast<V*>(rec)[j] = src[j];
-                        if (poly >= 0) tri_term<T, true, false>(a.ph, polys[a.ne + poly], qx, qy, qz, rec, acc);
-                        else unit_term<T, 2>(a.ph, polys[0], qx, qy, qz, rec, acc);
-                    }
-                    ++nleaf;
-                    if constexpr (HASH) h += decision_mix(uint64_t(id), 2);
-                } else {
-                    desc = true;
-                }
-            }
-        }
-        const unsigned D = __ballot_sync(0xffffffffu, desc);
-        if (D) {  // descend: left child next, right child (same lanes) on the stack
-            if (lane == 0) st[sp] = make_int2(link, int(D));
-            __syncwarp();
-            ++sp;
-            id = id + 1;
-            mask = D;
-        } else {
-            if (sp == 0) break;
-            --sp;
-            const int2 e = st[sp];
-            id = e.x;
-            mask = unsigned(e.y);
-        }
-    }
-    if (!valid) return;
-    Tot tot;
-    tot.init();
-    tot.flush(acc);
-    a.part[i] = tot.M;
-    a.part[a.Q + i] = tot.s;
-    a.part[2 * a.Q + i] = tot.gx;
-    a.part[3 * a.Q + i] = tot.gy;
-    a.part[4 * a.Q + i] = tot.gz;
-    a.leaves[i] = nleaf;
-    a.far[i] = nfar;
-    if (HASH) a.hash[i] = h;
-    if (nre) atomicAdd(a.rechecks, nre);
-}
-
 // Exact leaf term (smooth.hpp:51-61) of the primitive in leaf slot `slot`
 // for query q, added to acc.
 template <class T>
@@ -657,7 +415,6 @@ constexpr bool kFarFrame = sizeof(T) == 4;
 // The point query of one lane (K3's VIS for bvh.cu).
 template <class T>
 struct PointVisit {
-    static constexpr bool kLeafBatch = true;
     static constexpr bool kLeafQueue = true;
     template <class U>
     static constexpr bool kFrame = kFarFrame<U>;
@@ -856,101 +613,8 @@ struct PointVisit {
         return true;
     }
 
-    // Both children of a node (K3's child-pair step): two scalar tests. (A
-    // packed fp32x2 variant with a branch-free far-field path measured
-    // slower on cfg4 -- 33.0 ms vs 29.7 ms: 80 registers and an exponential
-    // for every child -- and was dropped.)
-    // Leaf-batching variants (pair_walk LB): returns "reached" -- descend
-    // into an internal node, or an exact leaf, which is counted (and hashed)
-    // at once but whose term is left to flush_leaves (the caller knows from
-    // the node's link which of the two it is).
-    template <bool HASH, class CNT>
-    __device__ __forceinline__ bool visit_nl(const TraverseArgs<T>& a, const NodeT<T>& b, int32_t id, T lgc,
-                                             Acc<T>& acc, CNT& nleaf, CNT& nfar, uint64_t& h,
-                                             unsigned long long& nre) const {
-        int32_t link;
-        memcpy(&link, &b.v[7], sizeof(int32_t));
-        {  // beta = 0 when there is no Barnes-Hut (see visit)
-            T d, r, dx, dy, dz;
-            if (point_far(a, b, id, qx, qy, qz, d, r, dx, dy, dz, nre)) {
-                far_term(a.ph, lgc + a.lw_ff, d, r, dx, dy, dz, acc);
-                ++nfar;
-                if constexpr (HASH) h += decision_mix(uint64_t(id), 1);
-                return false;
-            }
-        }
-        if (link >= 0) return true;
-        ++nleaf;
-        if constexpr (HASH) h += decision_mix(uint64_t(id), 2);
-        return true;
-    }
-    template <bool HASH, class CNT>
-    __device__ __forceinline__ void visit_pair_nl(const TraverseArgs<T>& a, const NodeT<T>& bl, const NodeT<T>& br,
-                                                  int32_t lid, int32_t rid, T lgl, T lgr, Acc<T>& acc, CNT& nleaf,
-                                                  CNT& nfar, uint64_t& h, unsigned long long& nre, bool& dl,
-                                                  bool& dr) const {
-        dl = visit_nl<HASH>(a, bl, lid, lgl, acc, nleaf, nfar, h, nre);
-        dr = visit_nl<HASH>(a, br, rid, lgr, acc, nleaf, nfar, h, nre);
-    }
-    // Evaluates the batched leaf entries of a warp -- entry k = list[k] =
-    // (leaf link, mask of the lanes that reached the leaf), k < nl -- with
-    // the (leaf, query) items spread over all 32 lanes, 32 per round: item
-    // t belongs to the entry with the largest exclusive popcount prefix
-    // <= t and to that entry's (t - prefix)-th lane, whose query and shift
-    // are fetched by shuffle. Each item is a partial relative to its
-    // owner's shift; the owners then merge theirs (merge_partial). Called
-    // by the whole warp.
-    __device__ __forceinline__ void flush_leaves(const TraverseArgs<T>& a, const Poly<T>* polys, Acc<T>& acc,
-                                                 const int2* list, int nl, unsigned lane) const {
-        constexpr unsigned FULL = 0xffffffffu;
-        __syncwarp();
-        const int2 ent = int(lane) < nl ? list[lane] : make_int2(0, 0);
-        const int32_t e_link = ent.x;
-        const unsigned e_mask = unsigned(ent.y);
-        const unsigned cnt = int(lane) < nl ? unsigned(__popc(e_mask)) : 0u;
-        unsigned incl = cnt;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const unsigned t = __shfl_up_sync(FULL, incl, o);
-            if (int(lane) >= o) incl += t;
-        }
-        const unsigned pre = incl - cnt;
-        const unsigned total = __shfl_sync(FULL, incl, nl - 1);
-        const unsigned pkey = int(lane) < nl ? pre : 0xffffffffu;
-        const unsigned lt = (1u << lane) - 1u;
-        for (unsigned base = 0; base < total; base += 32) {
-            const unsigned t = base + lane;
-            int k = 0;
-#pragma unroll
-            for (int step = 16; step; step >>= 1) {
-                const unsigned p = __shfl_sync(FULL, pkey, k + step);
-                if (p <= t) k += step;
-            }
-            const unsigned mk = __shfl_sync(FULL, e_mask, k);
-            const int32_t lk = __shfl_sync(FULL, e_link, k);
-            const unsigned pk = __shfl_sync(FULL, pre, k);
-            const int owner = int(__fns(mk, 0, int(t - pk) + 1)) & 31;
-            const T ox = __shfl_sync(FULL, qx, owner), oy = __shfl_sync(FULL, qy, owner),
-                    oz = __shfl_sync(FULL, qz, owner);
-            Acc<T> it;
-            it.m = __shfl_sync(FULL, acc.m, owner);
-            it.s = it.gx = it.gy = it.gz = T(0);
-            if (t < total) leaf_term<T>(a, polys, -lk - 1, ox, oy, oz, it);
-            const int kl = __shfl_sync(FULL, k, 0);
-            const int kh = __shfl_sync(FULL, k, int(min(31u, total - 1u - base)));
-            for (int kk = kl; kk <= kh; ++kk) {  // the owners collect their items of this round
-                const unsigned m2 = __shfl_sync(FULL, e_mask, kk), p2 = __shfl_sync(FULL, pre, kk);
-                const int src = int(p2 + unsigned(__popc(m2 & lt))) - int(base);
-                const bool have = ((m2 >> lane) & 1u) && src >= 0 && src < 32;
-                const int s2 = src & 31;
-                const T im = __shfl_sync(FULL, it.m, s2), is = __shfl_sync(FULL, it.s, s2),
-                        ix = __shfl_sync(FULL, it.gx, s2), iy = __shfl_sync(FULL, it.gy, s2),
-                        iz = __shfl_sync(FULL, it.gz, s2);
-                if (have && is != T(0)) merge_partial(acc, im, is, ix, iy, iz);
-            }
-        }
-    }
-
+    // Both children of a node (K3's child-pair step in the split walk): two
+    // scalar tests.
     template <bool HASH, class CNT>
     __device__ __forceinline__ void visit_pair(const TraverseArgs<T>& a, const Poly<T>* polys, const NodeT<T>& bl,
                                                const NodeT<T>& br, int32_t lid, int32_t rid, T lgl, T lgr,
@@ -1084,11 +748,7 @@ template const int64_t* sort_queries<float>(Ctx&, const float*, int64_t, const d
 template const int64_t* sort_queries<double>(Ctx&, const double*, int64_t, const double*, const double*,
                                              cudaStream_t, int64_t&, bool);
 
-static bool variant_is_frontier(int64_t Q) {
-    const char* e = std::getenv("SDGPU_TRAVERSAL");
-    if (e && std::string(e) != "pair") return false;
-    return use_frontier(Q, 65536);
-}
+static bool variant_is_frontier(int64_t Q) { return use_frontier(Q, 65536); }
 
 template <class T>
 void tree_query(Ctx& c, const T* q, int64_t Q, const sd_params& p, const FinalizeOut& out, cudaStream_t st) {
@@ -1156,33 +816,16 @@ void tree_query(Ctx& c, const T* q, int64_t Q, const sd_params& p, const Finaliz
     a.qgeom = nullptr;
     a.qdim = nullptr;
     a.leafgeom = nullptr;
-    // SDGPU_TRAVERSAL = thread | packet | pair (default) selects the kernel (A/B runs)
-    static const int variant = [] {
-        const char* e = std::getenv("SDGPU_TRAVERSAL");
-        const std::string v = e ? e : "pair";
-        return v == "thread" ? 0 : (v == "packet" ? 1 : 2);
-    }();
     int nsplits = 1;
     KernelTimer timer(c, st);
-    if (variant == 2) {
-        // few / sparse queries: node-parallel K3F (one warp per query); dense
-        // batches: K3 packets (tools/frontier_crossover.py: cfg4, 1k..262k
-        // queries: K3F 0.10 / 0.32 / 0.73 / 2.06 / 6.8 ms vs K3 2.8 / 7.0 / 7.7 /
-        // 6.3 / 7.3 ms; the full dense 4.19M batch: K3 29.7 ms)
-        if (!(use_frontier(Q, 65536) &&
-              launch_frontier<T, PointVisit<T>>(c, c.dtree, a, out.hash != nullptr, st, launches, 32)))
-            nsplits = launch_pair_traversal<T, PointVisit<T>>(c, c.dtree, a, out.hash != nullptr, st, launches, 1,
-                                                                 true, out.leaves || out.far_field);
-    } else {
-        const size_t smem = poly_bytes<T>(npoly) +
-                            (variant == 0 ? size_t(a.stack_depth) * kTravThreads * sizeof(int32_t)
-                                          : size_t(a.stack_depth) * (kTravThreads / 32) * sizeof(int4));
-        auto kern = variant == 0 ? traverse_kernel<T> : (out.hash ? packet_kernel<T, true> : packet_kernel<T, false>);
-        check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)), "smem attr");
-        kern<<<unsigned((Q + kTravThreads - 1) / kTravThreads), kTravThreads, smem, st>>>(a);
-        check_cuda(cudaGetLastError(), "traverse kernel");
-        ++launches;
-    }
+    // few / sparse queries: node-parallel K3F (one warp per query); dense
+    // batches: K3 packets (tools/frontier_crossover.py: cfg4, 1k..262k
+    // queries: K3F 0.10 / 0.32 / 0.73 / 2.06 / 6.8 ms vs K3 2.8 / 7.0 / 7.7 /
+    // 6.3 / 7.3 ms; the full dense 4.19M batch: K3 29.7 ms in round 1)
+    if (!(use_frontier(Q, 65536) &&
+          launch_frontier<T, PointVisit<T>>(c, c.dtree, a, out.hash != nullptr, st, launches, 32)))
+        nsplits = launch_pair_traversal<T, PointVisit<T>>(c, c.dtree, a, out.hash != nullptr, st, launches, 1,
+                                                             out.leaves || out.far_field);
     timer.stop();
     check_cuda(launch_finalize(a.part, nsplits, Q, p.alpha, p.epsilon, 0, a.leaves, a.far, a.hash, perm, out, st),
                "finalize");

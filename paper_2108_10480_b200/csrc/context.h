@@ -88,8 +88,6 @@ struct DeviceTree {
     int depth = 0;
     bool exact_boxes = true;
     DevBuf box, pairs, count, lgcount, diam64, leafrec, leafmeta;
-    DevBuf esc;             // end of each node's pre-order subtree (deferred walks)
-    bool has_esc = false;
     int split_k = -1;         // depth of the cached split tables
     int64_t split_count = 0;  // slots at that depth
     DevBuf split_meta, split_path;  // see split_tables (bvh.cu)

@@ -162,18 +162,6 @@ __global__ void pair_records(const sd_bvh_node* __restrict__ nodes, int64_t n, c
     pairs[id] = pr;
 }
 
-// end of the pre-order subtree of every node: one past its rightmost leaf
-// (the deferred per-lane walks of pair_kernel skip a subtree by jumping
-// there); O(depth) per node, used for trees of depth <= kEscMaxDepth
-constexpr int kEscMaxDepth = 64;
-__global__ void subtree_end(const sd_bvh_node* __restrict__ nodes, int64_t n, int32_t* esc) {
-    const int64_t id = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (id >= n) return;
-    int32_t x = int32_t(id);
-    for (int k = 0; k <= kEscMaxDepth && nodes[x].left >= 0; ++k) x = nodes[x].right;
-    esc[id] = x + 1;
-}
-
 }  // namespace
 
 template <class T>
@@ -217,11 +205,6 @@ void upload_tree_device(Ctx& c, DeviceTree& t, int depth) {
     auto* pairs = static_cast<PairT<T>*>(t.pairs.ensure(size_t(n) * sizeof(PairT<T>)));
     pair_records<T><<<G, B, 0, st>>>(nodes, n, box, lgc, pairs);
     check_cuda(cudaGetLastError(), "tree pair records");
-    t.has_esc = depth <= kEscMaxDepth;
-    if (t.has_esc) {
-        subtree_end<<<G, B, 0, st>>>(nodes, n, static_cast<int32_t*>(t.esc.ensure(size_t(n) * sizeof(int32_t))));
-        check_cuda(cudaGetLastError(), "tree subtree ends");
-    }
     int hf[2] = {0, 0};
     check_cuda(cudaMemcpyAsync(hf, flags, sizeof(hf), cudaMemcpyDeviceToHost, st), "D2H");
     check_cuda(cudaStreamSynchronize(st), "tree layout");

@@ -594,8 +594,7 @@ __device__ __forceinline__ Geom load_query(const double* qg, const int32_t* qd, 
 
 // K3's per-lane query for simplex queries.
 struct SimplexVisit {
-    static constexpr bool kLeafBatch = false;  // per-lane QP leaves: no batched flush
-    static constexpr bool kLeafQueue = false;  // (nor deferred leaf queues)
+    static constexpr bool kLeafQueue = false;  // per-lane QP leaves: no deferred leaf queues
     template <class U>
     static constexpr bool kFrame = false;
     sx::Geom g;

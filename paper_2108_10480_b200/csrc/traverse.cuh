@@ -83,10 +83,6 @@ struct TraverseArgs {
     const double* qgeom;
     const int32_t* qdim;
     const double* leafgeom;
-    // deferred sparse entries (pair_kernel DEFER): the end of each node's
-    // pre-order subtree, the popcount threshold and the per-warp capacity
-    const int32_t* esc = nullptr;
-    int defer_t = 0, defer_cap = 0;
     // K3Q leaf-queue capacity (entries per lane); leaf_coop: the queued
     // terms are evaluated by the whole warp (leaf_flush_coop) instead of
     // one per lane per round
@@ -95,9 +91,6 @@ struct TraverseArgs {
 };
 
 constexpr int kTravThreads = 128;
-constexpr int kDeferDefault = 0;  // pair_kernel DEFER threshold (SDGPU_DEFER); off: see profiles/README.md
-constexpr int kDeferCap = 64;     // deferred entries per warp (SDGPU_DEFER_CAP)
-constexpr int kLeafBatch = 32;    // batched leaf entries per warp (pair_walk LB)
 
 // shared-memory bytes of the polynomial table, padded so the stacks after it
 // stay 16-byte aligned
@@ -144,22 +137,6 @@ __device__ __forceinline__ void far_term(const Phys<T>& ph, T lw, T d, T r, T dx
 // tests one node for it (point queries: bvh.cu; simplex queries:
 // simplex.cu) and returns "descend"; far_test<HASH>(...) is the
 // admissibility test alone (emitting the far-field term only when asked).
-//
-// DEFER (unsplit point queries): an entry whose lane mask has at most
-// a.defer_t lanes -- the deep, query-specific tails of the walk, where a
-// packet step would run with most lanes idle -- is not walked by the packet
-// but appended to a per-warp list (while it has room). Once the packet walk
-// is over, every lane walks the subtrees of the listed entries that carry
-// its bit on its own, stackless in pre-order (descend: id + 1; far field or
-// leaf: a.esc[id], the end of id's subtree), all lanes at once. Per lane
-// the visited node set is still exactly collect_contributions'; only the
-// order of the terms changes.
-//
-// LB (leaf batching, point queries): a lane that reaches an exact leaf
-// counts it at once, but the warp only records (leaf, lane mask) -- lane k
-// of the warp holds entry k -- and evaluates 32 entries at a time with the
-// (leaf, query) items spread over all lanes (VIS::flush_leaves). Inline, a
-// leaf step runs the ~190-instruction triangle term for ~3.6 of 32 lanes.
 __device__ __forceinline__ void st_shared_int4(uint32_t addr, int x, int y, int z) {
     asm volatile("st.shared.v4.s32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(x), "r"(y), "r"(z), "r"(0) : "memory");
 }
@@ -169,7 +146,7 @@ __device__ __forceinline__ int4 ld_shared_int4(uint32_t addr) {
     return v;
 }
 
-template <class T, class VIS, bool HASH, int SPLIT, bool DEFER, bool LB = false>
+template <class T, class VIS, bool HASH, int SPLIT>
 __device__ __forceinline__ void pair_walk(const TraverseArgs<T>& a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Poly<T>* polys = reinterpret_cast<Poly<T>*>(smem_raw);
@@ -181,12 +158,6 @@ __device__ __forceinline__ void pair_walk(const TraverseArgs<T>& a) {
     const unsigned lane = threadIdx.x & 31u;
     const unsigned lanebit = 1u << lane;
     int4* st = stacks + (threadIdx.x >> 5) * a.stack_depth;
-    int2* dlist = reinterpret_cast<int2*>(stacks + (kTravThreads / 32) * a.stack_depth) + (threadIdx.x >> 5) * a.defer_cap;
-    int nd = 0;  // deferred entries (warp-uniform)
-    // LB: batched leaf entries (leaf link, lane mask), after the deferred list
-    [[maybe_unused]] int2* llist = reinterpret_cast<int2*>(stacks + (kTravThreads / 32) * a.stack_depth) +
-                                   (kTravThreads / 32) * a.defer_cap + (threadIdx.x >> 5) * kLeafBatch;
-    [[maybe_unused]] int nl = 0;  // batched leaf entries (warp-uniform)
     // packet (32 sorted queries) and, when split, the slot
     const int64_t gwarp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int64_t packet = SPLIT ? gwarp / a.nslots : gwarp;
@@ -241,43 +212,13 @@ __device__ __forceinline__ void pair_walk(const TraverseArgs<T>& a) {
         // pair record into L1 while this one is being processed
         asm volatile("prefetch.global.L1 [%0];" ::"l"(&pr + 1));  // = a.pairs + lid (one request per warp)
         bool dl = false, dr = false;
-        if (mask & lanebit) {
-            if constexpr (LB)
-                qv.template visit_pair_nl<HASH>(a, bl, br, lid, rid, lgl, lgr, acc, nleaf, nfar, h, nre, dl, dr);
-            else
-                qv.template visit_pair<HASH>(a, polys, bl, br, lid, rid, lgl, lgr, acc, nleaf, nfar, h, nre, dl, dr);
-        }
-        unsigned DL = __ballot_sync(0xffffffffu, dl), DR = __ballot_sync(0xffffffffu, dr);
+        if (mask & lanebit) qv.template visit_pair<HASH>(a, polys, bl, br, lid, rid, lgl, lgr, acc, nleaf, nfar, h, nre, dl, dr);
+        const unsigned DL = __ballot_sync(0xffffffffu, dl), DR = __ballot_sync(0xffffffffu, dr);
         int32_t llink, rlink;
         memcpy(&llink, &bl.v[7], sizeof(int32_t));
         memcpy(&rlink, &br.v[7], sizeof(int32_t));
-        if constexpr (LB) {  // a leaf child's "reached" mask is a batch entry, not a descent
-            if (llink < 0) {
-                if (DL) {
-                    if (lane == 0) llist[nl] = make_int2(llink, int(DL));
-                    if (++nl == kLeafBatch) {
-                        qv.flush_leaves(a, polys, acc, llist, nl, lane);
-                        nl = 0;
-                    }
-                }
-                DL = 0u;
-            }
-            if (rlink < 0) {
-                if (DR) {
-                    if (lane == 0) llist[nl] = make_int2(rlink, int(DR));
-                    if (++nl == kLeafBatch) {
-                        qv.flush_leaves(a, polys, acc, llist, nl, lane);
-                        nl = 0;
-                    }
-                }
-                DR = 0u;
-            }
-        }
         if (DL) {
-            if (DEFER && DR && __popc(DR) <= a.defer_t && nd < a.defer_cap) {
-                if (lane == 0) dlist[nd] = make_int2(rid, int(DR));
-                ++nd;
-            } else if (DR) {
+            if (DR) {
                 if (lane == 0) st_shared_int4(top, rid, rlink, int(DR));
                 __syncwarp();
                 top += 16;
@@ -298,49 +239,6 @@ __device__ __forceinline__ void pair_walk(const TraverseArgs<T>& a) {
         } else {
             mask = 0u;
         }
-        if constexpr (DEFER) {
-            while (mask && __popc(mask) <= a.defer_t && nd < a.defer_cap) {
-                if (lane == 0) dlist[nd] = make_int2(cur, int(mask));
-                ++nd;
-                if (top != st0) {
-                    top -= 16;
-                    const int4 e = ld_shared_int4(top);
-                    cur = e.x;
-                    cur_link = e.y;
-                    mask = unsigned(e.z);
-                        } else {
-                    mask = 0u;
-                }
-            }
-        }
-    }
-    if constexpr (LB) {
-        if (nl > 0) qv.flush_leaves(a, polys, acc, llist, nl, lane);
-    }
-    if constexpr (DEFER) {
-        if (nd > 0) {  // per-lane stackless walks of the deferred subtrees
-            __syncwarp();
-            int j = 0;
-            int32_t n = 0, end = 0;
-            auto next = [&]() {
-                while (j < nd) {
-                    const int2 e = dlist[j++];
-                    if ((unsigned(e.y) >> lane) & 1u) {
-                        n = e.x + 1;
-                        end = a.esc[e.x];
-                        return true;
-                    }
-                }
-                return false;
-            };
-            bool act = valid && next();
-            while (act) {
-                const NodeT<T> b = a.box[n];
-                const bool d = qv.template visit<HASH>(a, polys, b, n, a.lgcount[n], acc, nleaf, nfar, h, nre);
-                n = d ? n + 1 : a.esc[n];
-                if (n == end) act = next();
-            }
-        }
     }
     if (!valid) return;
     Tot tot;
@@ -360,21 +258,12 @@ __device__ __forceinline__ void pair_walk(const TraverseArgs<T>& a) {
         a.far[i] = nfar;
         if (HASH) a.hash[i] = h;
     }
-    // (the fp64 re-decision count nre is not reported by the packet walk: its
-    // two registers cost the fp32 leaf-batching kernel a spill of the
-    // far-field counter)
+    // (the fp64 re-decision count nre is not reported by the packet walk)
 }
 
-template <class T, class VIS, bool HASH, int SPLIT, bool LB = false>
+template <class T, class VIS, bool HASH, int SPLIT>
 __global__ void __launch_bounds__(kTravThreads) pair_kernel(const __grid_constant__ TraverseArgs<T> a) {
-    pair_walk<T, VIS, HASH, SPLIT, false, LB>(a);
-}
-// the deferring walk holds the packet state and the per-lane walk state:
-// pinned to the packet kernel's register budget (fp32 64, fp64 124)
-template <class T, class VIS, bool HASH>
-__global__ void __launch_bounds__(kTravThreads, sizeof(T) == 4 ? 8 : 4)
-    pair_kernel_defer(const __grid_constant__ TraverseArgs<T> a) {
-    pair_walk<T, VIS, HASH, 0, true>(a);
+    pair_walk<T, VIS, HASH, SPLIT>(a);
 }
 
 // K3Q (default for dense point batches): the child-pair packet walk with
@@ -662,7 +551,7 @@ inline bool use_frontier(int64_t Q, int64_t limit) {
 // splitting. `weight` raises the warp target for expensive node tests.
 template <class T, class VIS>
 int launch_pair_traversal(Ctx& c, DeviceTree& t, TraverseArgs<T>& a, bool hash, cudaStream_t st, int64_t& launches,
-                          int weight = 1, bool allow_defer = false, bool count = true) {
+                          int weight = 1, bool count = true) {
     const int64_t Q = a.Q;
     size_t smem = poly_bytes<T>(a.npoly) + size_t(a.stack_depth) * (kTravThreads / 32) * sizeof(int4);
     const int64_t npackets = (Q + 31) / 32;
@@ -694,31 +583,8 @@ int launch_pair_traversal(Ctx& c, DeviceTree& t, TraverseArgs<T>& a, bool hash, 
         nsplits = a.nslots;
         a.part = static_cast<double*>(c.part.ensure(size_t(nsplits) * 5 * Q * sizeof(double)));
     }
-    // deferred sparse entries (unsplit point walks): SDGPU_DEFER = popcount
-    // threshold (0 = off), SDGPU_DEFER_CAP = entries per warp
-    const char* de = std::getenv("SDGPU_DEFER");
-    const char* dc = std::getenv("SDGPU_DEFER_CAP");
-    const int defer_t = de && *de ? std::max(0, std::min(32, std::atoi(de))) : kDeferDefault;
-    const int defer_cap = dc && *dc ? std::max(1, std::min(1024, std::atoi(dc))) : kDeferCap;
-    const bool defer = allow_defer && k == 0 && defer_t > 0 && t.has_esc;
-    a.esc = defer ? t.esc.as<int32_t>() : nullptr;
-    a.defer_t = defer ? defer_t : 0;
-    a.defer_cap = defer ? defer_cap : 0;
-    if (defer) smem += size_t(defer_cap) * (kTravThreads / 32) * sizeof(int2);
     auto kern = k > 0 ? (hash ? pair_kernel<T, VIS, true, 1> : pair_kernel<T, VIS, false, 1>)
-                      : defer ? (hash ? pair_kernel_defer<T, VIS, true> : pair_kernel_defer<T, VIS, false>)
-                              : (hash ? pair_kernel<T, VIS, true, 0> : pair_kernel<T, VIS, false, 0>);
-    if constexpr (VIS::kLeafBatch) {  // SDGPU_LEAF_BATCH = 1 turns leaf batching on (off: profiles/README.md)
-        const char* lb = std::getenv("SDGPU_LEAF_BATCH");
-        // the leaf list sits after defer_cap deferred entries per warp
-        // (pair_walk): the two modes are exclusive, so defer_cap is 0 here
-        if (!defer && lb && *lb == '1') {
-            if (a.defer_cap != 0) throw std::logic_error("leaf batching with a deferred list");
-            smem += size_t(kLeafBatch) * (kTravThreads / 32) * sizeof(int2);
-            kern = k > 0 ? (hash ? pair_kernel<T, VIS, true, 1, true> : pair_kernel<T, VIS, false, 1, true>)
-                         : (hash ? pair_kernel<T, VIS, true, 0, true> : pair_kernel<T, VIS, false, 0, true>);
-        }
-    }
+                      : (hash ? pair_kernel<T, VIS, true, 0> : pair_kernel<T, VIS, false, 0>);
     if constexpr (VIS::kLeafQueue) {  // SDGPU_LEAF_QUEUE = 0 turns the deferred leaf queues off (A/B)
         // SDGPU_LEAFQ: leaf-queue entries per lane (>= 3)
         auto cap = [](const char* name, int dflt) {
@@ -727,7 +593,6 @@ int launch_pair_traversal(Ctx& c, DeviceTree& t, TraverseArgs<T>& a, bool hash, 
         };
         const char* lqe = std::getenv("SDGPU_LEAF_QUEUE");
         const bool lq_on = !(lqe && *lqe == '0');
-        const char* lb = std::getenv("SDGPU_LEAF_BATCH");
         // SDGPU_LEAF_COOP = 1 / 0: queued leaf terms evaluated by the whole
         // warp (leaf_flush_coop) / one per lane per round; default: the
         // cooperative flush in fp32 (cfg4 21.9 -> 20.4 ms), per-lane rounds
@@ -735,7 +600,7 @@ int launch_pair_traversal(Ctx& c, DeviceTree& t, TraverseArgs<T>& a, bool hash, 
         const char* lce = std::getenv("SDGPU_LEAF_COOP");
         a.leaf_coop = (lce && *lce) ? (*lce == '1' ? 1 : 0) : (sizeof(T) == 4 ? 1 : 0);
         a.lq_cap = std::max(3, cap("SDGPU_LEAFQ", a.leaf_coop ? kLeafQCoop : kLeafQ));
-        if (lq_on && k == 0 && !defer && !(lb && *lb == '1')) {
+        if (lq_on && k == 0) {
             smem += size_t(a.lq_cap) * kTravThreads * sizeof(int32_t);
             if (a.leaf_coop)
                 kern = hash ? pair_kernel_q<T, VIS, true, true, true>

@@ -140,17 +140,13 @@ def test_random_scene_tree_decisions(sd, oracle, prec, seed):
 
 @pytest.mark.parametrize("prec", [0, 1])
 @pytest.mark.parametrize("split", ["0", "1", "3", "6", "", "frontier", "frontier32",
-                                   "defer0", "defer1", "defer32", "defer32cap1", "defer12cap3", "lb", "lb3",
                                    "q3", "q16", "noq", "coop3", "coop24", "lanes40"])
 def test_split_traversal_decisions(sd, oracle, prec, split, monkeypatch):
     """The few-query traversal modes visit exactly the oracle's nodes:
     the slot split (one warp per (packet, depth-k slot) after re-testing the
     slot's ancestors, merged in fp64) at every depth k, none ("0"), the
     automatic choice (""), and the node-parallel frontier kernel: counters
-    and decision hash identical. "deferT[capC]": the unsplit packet walk
-    handing entries of at most T lanes to per-lane stackless walks (a list
-    of C entries per warp; a full list keeps the rest in the packet).
-    "lb[k]": exact-leaf terms batched over the warp's lanes (split depth k).
+    and decision hash identical.
     "qL": the unsplit walk with per-lane deferred queues of L exact leaves
     (K3Q; small queues force many flushes); "noq": leaf terms inline;
     "coopL" / "lanesL": the warp-cooperative flush / per-lane rounds."""
@@ -169,16 +165,6 @@ def test_split_traversal_decisions(sd, oracle, prec, split, monkeypatch):
     elif split.startswith("frontier"):
         monkeypatch.setenv("SDGPU_FRONTIER", "1")
         monkeypatch.setenv("SDGPU_FRONTIER_G", split[8:] or "4")
-    elif split.startswith("defer"):
-        t, _, cap = split[5:].partition("cap")
-        monkeypatch.setenv("SDGPU_FRONTIER", "0")
-        monkeypatch.setenv("SDGPU_SPLIT", "0")
-        monkeypatch.setenv("SDGPU_DEFER", t)
-        monkeypatch.setenv("SDGPU_DEFER_CAP", cap or "64")
-    elif split.startswith("lb"):  # leaf terms batched across the warp (SDGPU_LEAF_BATCH=1)
-        monkeypatch.setenv("SDGPU_FRONTIER", "0")
-        monkeypatch.setenv("SDGPU_SPLIT", split[2:] or "0")
-        monkeypatch.setenv("SDGPU_LEAF_BATCH", "1")
     else:
         monkeypatch.setenv("SDGPU_FRONTIER", "0")
         monkeypatch.setenv("SDGPU_SPLIT", split)
@@ -286,8 +272,8 @@ def test_config_exact_parity(sd, oracle, cfg, prec, alphas, nq):
         assert_close(got, ref, prec, alpha, f"cfg{cfg} alpha {alpha}")
 
 
-@pytest.mark.parametrize("builder,kernel", [("median", "K3F"), ("lbvh", "K3F"), ("lbvh", "K3"), ("median", "K3D"),
-                                            ("median", "K3LB"), ("median", "K3"), ("median", "K3NQ")])
+@pytest.mark.parametrize("builder,kernel", [("median", "K3F"), ("lbvh", "K3F"), ("lbvh", "K3"), ("median", "K3"),
+                                            ("median", "K3NQ"), ("median", "K3L")])
 def test_config4_tree_parity_subset(sd, oracle, builder, kernel, monkeypatch):
     """cfg4 (icosphere(9), 5.2M triangles, beta 0.5, alpha 200) on a query
     subset (both halves of the query distribution): decisions identical to
@@ -297,18 +283,13 @@ def test_config4_tree_parity_subset(sd, oracle, builder, kernel, monkeypatch):
     this batch size, K3 the one the full-size bench runs)."""
     O = oracle
     monkeypatch.setenv("SDGPU_FRONTIER", "1" if kernel == "K3F" else "0")
-    if kernel in ("K3", "K3NQ"):
+    if kernel in ("K3", "K3NQ", "K3L"):
         # the unsplit packet walk of the full-size batch: K3 = the default
-        # K3Q (deferred per-lane leaf queues), K3NQ = inline leaf terms
+        # K3Q (deferred leaf queues, cooperative flush in fp32), K3NQ =
+        # inline leaf terms, K3L = per-lane leaf rounds
         monkeypatch.setenv("SDGPU_SPLIT", "0")
         monkeypatch.setenv("SDGPU_LEAF_QUEUE", "0" if kernel == "K3NQ" else "1")
-    if kernel in ("K3D", "K3LB"):
-        # the unsplit packet walk (the full-size kernel); K3D with deferred
-        # per-lane tails (entries of <= 4 lanes), K3LB with batched leaf terms
-        monkeypatch.setenv("SDGPU_SPLIT", "0")
-        monkeypatch.setenv("SDGPU_LEAF_BATCH", "1" if kernel == "K3LB" else "0")
-        monkeypatch.setenv("SDGPU_DEFER", "4" if kernel == "K3D" else "0")
-        monkeypatch.setenv("SDGPU_DEFER_CAP", "64")
+        monkeypatch.setenv("SDGPU_LEAF_COOP", "0" if kernel == "K3L" else "1")
     m, q = _cfg(O, 4, 512, 0)
     w = O.Weights.build(m)
     if builder == "median":

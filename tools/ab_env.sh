@@ -1,10 +1,10 @@
 #!/bin/bash
 # A/B of traversal switches on the cfg4 BVH leg of bench.py (run under
-# gpurun, 1 GPU). Usage: AB="SDGPU_LEAF_BATCH=0 SDGPU_LEAF_BATCH=1" tools/ab_env.sh
+# gpurun, 1 GPU). Usage: AB="SDGPU_LEAF_QUEUE=0 SDGPU_LEAF_QUEUE=1" tools/ab_env.sh
 # (each word is one run's environment; '+' joins several variables).
 cd "${GRAFT_REPO_ROOT:-$(dirname "$0")/..}"
 mkdir -p gpurun_out
-for cfg in ${AB:-SDGPU_LEAF_BATCH=0 SDGPU_LEAF_BATCH=1}; do
+for cfg in ${AB:-SDGPU_LEAF_QUEUE=0 SDGPU_LEAF_QUEUE=1}; do
   for rep in $(seq ${REPS:-1}); do
     log=gpurun_out/ab_${cfg//[^A-Za-z0-9_]/_}_$rep.log
     env ${cfg//+/ } timeout 300 python bench.py --steps ${STEPS:-5} --warmup 3 --no-cpu ${BENCH_ARGS} > $log 2>&1
