@@ -354,8 +354,9 @@ __device__ __forceinline__ void pair_walk_q(const TraverseArgs<T>& a) {
         const bool full = __any_sync(FULL, nq >= lcap);
         if (DL) {
             if (DR) {
-                if (lane == 0) st_shared_int4(top, rid, rlink, int(DR));
-                __syncwarp();
+                // every lane stores the same entry (one same-address write):
+                // each lane later reads back its own store, no warp barrier
+                st_shared_int4(top, rid, rlink, int(DR));
                 top += 16;
             }
             cur = lid;
