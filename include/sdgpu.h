@@ -149,6 +149,19 @@ int sd_export_bvh(sd_ctx* ctx, sd_bvh_node* out, int64_t cap);
  * (blocking). mode SD_EXACT ignores beta; SD_BVH uses the tree. */
 int sd_query_points(sd_ctx* ctx, const double* q, int64_t Q, const sd_params* p, int mode, const sd_outputs* out);
 
+/* Pipelined HOST-buffer queries (serving loops): enqueue one batch -- H2D
+ * of q on a copy stream, the evaluation on the context's stream, D2H of
+ * the requested outputs on a second copy stream -- and return at once with
+ * a ticket. Batches submitted back to back overlap one batch's copies with
+ * its neighbours' evaluation. Two batches are in flight at most: a third
+ * submission first waits for the oldest. q and the output arrays must stay
+ * valid and untouched until sd_query_wait(ticket) (ticket < 0: every
+ * batch) returns; pinned host memory gives real overlap. Results are those
+ * of sd_query_points. */
+int sd_query_points_async(sd_ctx* ctx, const double* q, int64_t Q, const sd_params* p, int mode,
+                          const sd_outputs* out, int64_t* ticket);
+int sd_query_wait(sd_ctx* ctx, int64_t ticket);
+
 /* Same with DEVICE buffers on the caller's stream (cudaStream_t, may be
  * NULL): q_dev is Q x 3 float (SD_FP32) or double (SD_FP64); outputs are
  * device pointers. Asynchronous. */

@@ -36,7 +36,7 @@ assert NODE_DTYPE.itemsize == 72
 EXPORTED_SYMBOLS = (
     "sd_last_error", "sd_abi_version", "sd_create", "sd_destroy", "sd_set_geometry", "sd_set_weights",
     "sd_set_bvh", "sd_build_bvh", "sd_bvh_size", "sd_export_bvh", "sd_query_points", "sd_query_points_device",
-    "sd_finalize_device", "sd_last_launch_count", "sd_set_kernel_timing", "sd_kernel_times", "sd_build_weights", "sd_weights_info", "sd_export_weights",
+    "sd_finalize_device", "sd_query_points_async", "sd_query_wait", "sd_last_launch_count", "sd_set_kernel_timing", "sd_kernel_times", "sd_build_weights", "sd_weights_info", "sd_export_weights",
     "sd_mesh_dist_points",
     "sd_query_simplices",
     "sd_mesh_dist",
@@ -112,6 +112,8 @@ def lib():
             "sd_export_bvh": (C.c_int, [vp, vp, i64]),
             "sd_query_points": (C.c_int, [vp, vp, i64, P(_Params), C.c_int, P(_Outputs)]),
             "sd_query_points_device": (C.c_int, [vp, vp, i64, P(_Params), C.c_int, P(_Outputs), vp]),
+            "sd_query_points_async": (C.c_int, [vp, vp, i64, P(_Params), C.c_int, P(_Outputs), P(i64)]),
+            "sd_query_wait": (C.c_int, [vp, i64]),
             "sd_finalize_device": (C.c_int, [vp, vp, vp, i64, P(_Params), vp, vp, vp]),
             "sd_last_launch_count": (C.c_int, [vp, P(i64)]),
             "sd_set_kernel_timing": (C.c_int, [vp, C.c_int]),
@@ -296,6 +298,23 @@ class Engine:
                        (r.d_hat, r.grad, r.c, r.grad_c, r.leaves, r.far_field, r.decision_hash)))
         _check(lib().sd_query_points(self.h, _ptr(q), n, C.byref(params._c()), mode, C.byref(o)))
         return r
+
+    def query_points_async(self, q, params: SmoothParams, mode: int, out: SmoothResults) -> int:
+        """Pipelined host-buffer batch (sd_query_points_async): returns a
+        ticket at once; q and out must stay alive and untouched until
+        wait(ticket). Use pinned arrays for copy / compute overlap."""
+        assert q.dtype == np.float64 and q.flags.c_contiguous
+        r = out
+        o = _Outputs(*(None if a is None else a.ctypes.data for a in
+                       (r.d_hat, r.grad, r.c, r.grad_c, r.leaves, r.far_field, r.decision_hash)))
+        t = C.c_int64()
+        _check(lib().sd_query_points_async(self.h, _ptr(q), len(q), C.byref(params._c()), mode, C.byref(o),
+                                           C.byref(t)))
+        return t.value
+
+    def wait(self, ticket: int = -1):
+        """Wait for one pipelined batch (or every batch in flight)."""
+        _check(lib().sd_query_wait(self.h, ticket))
 
     def query_points_device(self, q_ptr: int, n: int, params: SmoothParams, mode: int, d_hat_ptr: int,
                             grad_ptr: int | None = None, c_ptr: int | None = None, grad_c_ptr: int | None = None,

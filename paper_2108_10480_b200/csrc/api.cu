@@ -606,6 +606,11 @@ int sd_destroy(sd_ctx* c) {
             c->stream = c->copy_stream = nullptr;
             for (auto& pr : c->ev_pairs) c->ev_pool.insert(c->ev_pool.end(), {pr.first, pr.second});
             for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
+            for (auto& sl : c->slots)
+                for (cudaEvent_t e : {sl.in, sl.done, sl.out})
+                    if (e) cudaEventDestroy(e);
+            if (c->in_stream) cudaStreamDestroy(c->in_stream);
+            if (c->out_stream) cudaStreamDestroy(c->out_stream);
         }
         delete c;
     });
@@ -1377,6 +1382,81 @@ int sd_write_grid_csv(const double* d, const int64_t* leaves, const int64_t* far
             out << buf;
         }
         if (!out) throw ArgError{std::string("write failed: ") + path};
+    });
+}
+
+int sd_query_points_async(sd_ctx* c, const double* q, int64_t Q, const sd_params* p, int mode, const sd_outputs* o,
+                          int64_t* ticket) {
+    return guard([&] {
+        if (!c || !ticket) throw ArgError{"NULL argument"};
+        check_params(p);
+        check_ready(*c, mode);
+        if (Q < 0 || (Q > 0 && (!q || !o || !o->d_hat))) throw ArgError{"bad query / output pointers"};
+        DeviceScope ds(c->device);
+        if (!c->in_stream) {
+            check_cuda(cudaStreamCreateWithFlags(&c->in_stream, cudaStreamNonBlocking), "stream");
+            check_cuda(cudaStreamCreateWithFlags(&c->out_stream, cudaStreamNonBlocking), "stream");
+            for (auto& sl : c->slots)
+                for (cudaEvent_t* e : {&sl.in, &sl.done, &sl.out})
+                    check_cuda(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "event");
+        }
+        Ctx::AsyncSlot& sl = c->slots[c->next_ticket % 2];
+        // the slot's previous batch has left the device (its buffers are free)
+        if (sl.ticket >= 0) check_cuda(cudaEventSynchronize(sl.out), "wait slot");
+        sl.ticket = c->next_ticket;
+        *ticket = c->next_ticket++;
+        if (Q == 0) {
+            check_cuda(cudaEventRecord(sl.out, c->out_stream), "event");
+            return;
+        }
+        cudaStream_t st = c->stream;
+        double* qd = static_cast<double*>(sl.qd.ensure(size_t(Q) * 3 * sizeof(double)));
+        check_cuda(cudaMemcpyAsync(qd, q, size_t(Q) * 3 * sizeof(double), cudaMemcpyHostToDevice, c->in_stream),
+                   "H2D queries");
+        check_cuda(cudaEventRecord(sl.in, c->in_stream), "event");
+        check_cuda(cudaStreamWaitEvent(st, sl.in, 0), "wait");
+        FinalizeOut out;
+        out.d_hat = static_cast<double*>(sl.d.ensure(size_t(Q) * sizeof(double)));
+        if (o->grad) out.grad = static_cast<double*>(sl.g.ensure(size_t(Q) * 3 * sizeof(double)));
+        if (o->c) out.c = static_cast<double*>(sl.c.ensure(size_t(Q) * sizeof(double)));
+        if (o->grad_c) out.grad_c = static_cast<double*>(sl.gc.ensure(size_t(Q) * 3 * sizeof(double)));
+        if (o->leaves) out.leaves = static_cast<int64_t*>(sl.l.ensure(size_t(Q) * sizeof(int64_t)));
+        if (o->far_field) out.far_field = static_cast<int64_t*>(sl.f.ensure(size_t(Q) * sizeof(int64_t)));
+        if (o->decision_hash) out.hash = static_cast<uint64_t*>(sl.h.ensure(size_t(Q) * sizeof(uint64_t)));
+        // the evaluation itself (stream-ordered after the previous batch's,
+        // so the shared scratch -- converted queries, sort, partials -- is free)
+        if (c->precision == SD_FP32) {
+            float* qf = static_cast<float*>(c->qT.ensure(size_t(Q) * 3 * sizeof(float)));
+            convert_queries<float><<<unsigned((3 * Q + 255) / 256), 256, 0, st>>>(qd, qf, 3 * Q);
+            check_cuda(cudaGetLastError(), "convert queries");
+            dispatch<float>(*c, qf, Q, *p, mode, out, st);
+            c->last_launches += 1;
+        } else {
+            dispatch<double>(*c, qd, Q, *p, mode, out, st);
+        }
+        check_cuda(cudaEventRecord(sl.done, st), "event");
+        check_cuda(cudaStreamWaitEvent(c->out_stream, sl.done, 0), "wait");
+        auto d2h = [&](void* dst, const void* src, size_t bytes) {
+            if (dst) check_cuda(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, c->out_stream), "D2H results");
+        };
+        d2h(o->d_hat, out.d_hat, size_t(Q) * sizeof(double));
+        d2h(o->grad, out.grad, size_t(Q) * 3 * sizeof(double));
+        d2h(o->c, out.c, size_t(Q) * sizeof(double));
+        d2h(o->grad_c, out.grad_c, size_t(Q) * 3 * sizeof(double));
+        d2h(o->leaves, out.leaves, size_t(Q) * sizeof(int64_t));
+        d2h(o->far_field, out.far_field, size_t(Q) * sizeof(int64_t));
+        d2h(o->decision_hash, out.hash, size_t(Q) * sizeof(uint64_t));
+        check_cuda(cudaEventRecord(sl.out, c->out_stream), "event");
+    });
+}
+
+int sd_query_wait(sd_ctx* c, int64_t ticket) {
+    return guard([&] {
+        if (!c) throw ArgError{"ctx is NULL"};
+        DeviceScope ds(c->device);
+        for (auto& sl : c->slots)
+            if (sl.ticket >= 0 && (ticket < 0 || sl.ticket == ticket))
+                check_cuda(cudaEventSynchronize(sl.out), "wait batch");
     });
 }
 

@@ -139,6 +139,18 @@ struct Ctx {
     DevBuf leafgeom, primgeom, primmeta, qgeom, qdim;
     bool sx_tree_ready = false, sx_prim_ready = false;
 
+    // pipelined host-buffer batches (sd_query_points_async): two slots, each
+    // with its own device copies of a batch's queries and outputs; H2D on
+    // in_stream, evaluation on `stream`, D2H on out_stream
+    struct AsyncSlot {
+        DevBuf qd, d, g, c, gc, l, f, h;
+        cudaEvent_t in = nullptr, done = nullptr, out = nullptr;
+        int64_t ticket = -1;
+    };
+    AsyncSlot slots[2];
+    cudaStream_t in_stream = nullptr, out_stream = nullptr;
+    int64_t next_ticket = 0;
+
     // scratch
     DevBuf qd, qT, part, out_d, out_g, out_c, out_gc, out_l, out_f, out_h;
     DevBuf perm, keys, tmp, tmp2, counters, polys, flag, qbox;

@@ -966,3 +966,31 @@ def test_exact_split_merge(sd, oracle, splits, cluster, cfg, prec, monkeypatch):
     ref = O.query(m, w, q, O.Params(alpha=100.0, beta=0.0))
     got = e.smooth_min_dist_flat(q, sd.SmoothParams(alpha=100.0, beta=0.0))
     assert_close(got, ref, prec, 100.0, f"cfg{cfg} splits {splits} cluster {cluster}")
+
+
+@pytest.mark.parametrize("prec", [0, 1])
+def test_pipelined_host_batches_equal_blocking_calls(sd, oracle, prec):
+    """sd_query_points_async: five batches of different sizes submitted back
+    to back (two in flight, a third submission waits for the oldest), exact
+    and tree mode alternating, results bit-equal to the blocking
+    sd_query_points calls; wait(ticket) and wait() semantics."""
+    O = oracle
+    m0 = O.random_scene(9, 300)
+    m, _ = prep(O, m0, np.zeros((1, 3)), prec)
+    w, t = O.Weights.build(m), O.Tree.build(m)
+    e = engine_for(sd, O, m, w, prec, tree=t)
+    P = sd.SmoothParams(alpha=120.0, beta=0.4)
+    batches = []
+    for k, n in enumerate((700, 33, 2048, 1, 517)):
+        q = O.QueryStream(900 + k).draw_points(m0, n)
+        if prec == 0:
+            q = q.astype(np.float32).astype(np.float64)
+        batches.append((np.ascontiguousarray(q), sd.SD_BVH if k % 2 else sd.SD_EXACT))
+    outs = [sd.SmoothResults(np.empty(len(q)), np.empty((len(q), 3))) for q, _ in batches]
+    tickets = [e.query_points_async(q, P, mode, outs[k]) for k, (q, mode) in enumerate(batches)]
+    assert tickets == sorted(tickets) and len(set(tickets)) == len(tickets)
+    e.wait(tickets[-1])
+    e.wait()
+    for (q, mode), got in zip(batches, outs):
+        ref = e.query_points(q, P, mode)
+        assert np.array_equal(got.d_hat, ref.d_hat) and np.array_equal(got.grad, ref.grad)
