@@ -109,6 +109,24 @@ class Backend {
         return smooth_min_dist(q, p, true);
     }
 
+    // Pipelined batches (sd_query_points_async): submit() enqueues the H2D,
+    // the evaluation and the D2H of one batch of points and returns at once;
+    // d_hat / grad (n and 3 n doubles, pinned memory for real overlap) must
+    // stay alive until wait(ticket). Two batches are in flight.
+    std::int64_t submit(const std::vector<Vec3>& q, const SmoothParams& p, double* d_hat, double* grad,
+                        bool exact = false) const {
+        sd_outputs o{d_hat, grad, nullptr, nullptr, nullptr, nullptr, nullptr};
+        const sd_params sp = params(p);
+        std::int64_t t = -1;
+        if (sd_query_points_async(ctx_, q.data()->data(), std::int64_t(q.size()), &sp,
+                                  (exact || !(p.beta > 0.0)) ? SD_EXACT : SD_BVH, &o, &t))
+            fail(sd_last_error());
+        return t;
+    }
+    void wait(std::int64_t ticket = -1) const {
+        if (sd_query_wait(ctx_, ticket)) fail(sd_last_error());
+    }
+
     // A batch of smooth_min_dist(mesh, bvh, ws, SimplexGeom g, params) over
     // query points / edges / triangles (gradient: rigid translation of g).
     std::vector<SmoothResult> smooth_min_dist(const std::vector<SimplexGeom>& g, const SmoothParams& p,

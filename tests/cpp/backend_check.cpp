@@ -73,6 +73,19 @@ int main(int argc, char** argv) {
         acc(ge[i], re, edx, egx);
     }
     check(counters, "tree counters = reference, exact leaves = N", double(q.size()));
+    {  // pipelined submission: the same results as the blocking batch
+        std::vector<double> d0(q.size()), g0(3 * q.size()), d1(q.size()), g1(3 * q.size());
+        const std::int64_t t0 = gpu.submit(q, p, d0.data(), g0.data());
+        const std::int64_t t1 = gpu.submit(q, p, d1.data(), g1.data(), true);
+        gpu.wait(t0);
+        gpu.wait(t1);
+        bool same = true;
+        for (std::size_t i = 0; i < q.size(); ++i) {
+            same &= (d0[i] == gt[i].d_hat || (std::isnan(d0[i]) && std::isnan(gt[i].d_hat))) && d1[i] == ge[i].d_hat;
+            for (int a = 0; a < 3; ++a) same &= g0[3 * i + a] == gt[i].grad(a) && g1[3 * i + a] == ge[i].grad(a);
+        }
+        check(same, "submit / wait = the blocking batches", 0.0);
+    }
     check(inf_ok, "+inf agrees", 0.0);
     check(ed <= td && eg <= tg, "smooth_min_dist (tree) d_hat / grad", std::max(ed, eg));
     check(edx <= td && egx <= tg, "smooth_min_dist_flat d_hat / grad", std::max(edx, egx));
