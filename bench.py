@@ -669,14 +669,21 @@ def tree_name():
 
 def measure_bvh(args, run, stream, flush, peaks, fp64=False):
     """BASELINE configs[3] (cfg4): BVH far-field queries/s. The fixed
-    4,194,304-query batch is split across the ranks (strong scaling; at N=1
-    the whole batch in input order); the timed outputs are then checked
-    against the oracle on 65,536 queries (decision hash, counters, d_hat,
-    grad) and Barnes-Hut against exact on the same queries."""
+    4,194,304-query batch is shared by the ranks (strong scaling): every
+    rank holds the whole batch and walks its share of the library's
+    32-query packets -- chunks of packets of the Hilbert-sorted batch dealt
+    round robin (sd_query_points_device_shard: regional locality within a
+    chunk, balance across chunks, no cost model, no collective). The timed
+    outputs are then checked against the oracle on 65,536 queries (decision
+    hash, counters, d_hat, grad) and Barnes-Hut against exact on the same
+    queries. --shard-world W --shard-rank R runs one rank's share on a
+    single GPU (tests of the sharded path; the value is that rank's rate)."""
     import paper_2108_10480_b200 as sd
     from paper_2108_10480_b200 import configs, sharding
     torch = run.torch
     rank, world = run.rank, run.world
+    W, R = (world, rank) if world > 1 else (max(1, args.shard_world), args.shard_rank)
+    sharded = W > 1
     t0 = time.perf_counter()
     w, q = configs.cfg4()
     v, q = configs.quantize(w.vertices), configs.quantize(q)
@@ -690,60 +697,58 @@ def measure_bvh(args, run, stream, flush, peaks, fp64=False):
     eng.build_bvh(tree_method(sd))
     tb = time.perf_counter() - tb
     P = sd.SmoothParams(alpha=w.alpha, alpha_u=600.0, beta=w.beta)
-    balance = None
-    sel = np.arange(Q_total)
-    if world > 1:
-        def counters(sub):
-            r = eng.smooth_min_dist(sub, P)
-            return r.leaves, r.far_field
-
-        order = sharding.morton_order(q)
-        est = sharding.estimate_query_costs(counters, q[order], stride=64)
-        ranges = sharding.balanced_ranges(est, world)
-        lo, hi = ranges[rank]
-        sel = order[lo:hi]
-        balance = {"ranges": ranges, "estimated_cost_share": [float(est[a:b].sum() / est.sum()) for a, b in ranges],
-                   "estimate": "strided sample (1/64) of the Morton-sorted batch, popped nodes 2(L+F)-1"}
-    qb = np.ascontiguousarray(q[sel])
-    Q = len(qb)
-    qd = torch.tensor(qb, dtype=torch.float64 if fp64 else torch.float32, device=run.dev)
-    d_hat = torch.empty(Q, dtype=torch.float64, device=run.dev)
-    grad = torch.empty(Q, 3, dtype=torch.float64, device=run.dev)
-    leaves = torch.empty(Q, dtype=torch.int64, device=run.dev)
-    far = torch.empty(Q, dtype=torch.int64, device=run.dev)
-    hsh = torch.empty(Q, dtype=torch.int64, device=run.dev)
+    qd = torch.tensor(q, dtype=torch.float64 if fp64 else torch.float32, device=run.dev)
+    d_hat = torch.full((Q_total,), float("nan"), dtype=torch.float64, device=run.dev)
+    grad = torch.empty(Q_total, 3, dtype=torch.float64, device=run.dev)
+    leaves = torch.zeros(Q_total, dtype=torch.int64, device=run.dev)
+    far = torch.zeros(Q_total, dtype=torch.int64, device=run.dev)
+    hsh = torch.zeros(Q_total, dtype=torch.int64, device=run.dev)
 
     def step(counters=False):
-        eng.query_points_device(qd.data_ptr(), Q, P, sd.SD_BVH, d_hat.data_ptr(), grad.data_ptr(),
-                                leaves_ptr=leaves.data_ptr() if counters else None,
-                                far_ptr=far.data_ptr() if counters else None,
-                                hash_ptr=hsh.data_ptr() if counters else None, stream=stream.cuda_stream)
+        kw = dict(leaves_ptr=leaves.data_ptr() if counters else None, far_ptr=far.data_ptr() if counters else None,
+                  hash_ptr=hsh.data_ptr() if counters else None, stream=stream.cuda_stream)
+        if sharded:
+            eng.query_points_device_shard(qd.data_ptr(), Q_total, P, W, R, d_hat.data_ptr(), grad.data_ptr(), **kw)
+        else:
+            eng.query_points_device(qd.data_ptr(), Q_total, P, sd.SD_BVH, d_hat.data_ptr(), grad.data_ptr(), **kw)
 
     step(counters=True)  # also uploads the traversal layout; counters + decision hash of the batch
     torch.cuda.synchronize()
     counted = (d_hat.cpu().numpy(), leaves.cpu().numpy(), far.cpu().numpy(), hsh.cpu().numpy().view(np.uint64))
+    mine = ~np.isnan(counted[0]) if sharded else np.ones(Q_total, bool)  # this rank's queries (cfg4 has no NaN)
+    Q = int(mine.sum())
     setup_s = time.perf_counter() - t0
-    L, F = float(counted[1].sum()), float(counted[2].sum())
+    L, F = float(counted[1][mine].sum()), float(counted[2][mine].sum())
     t = time_device(run, step, stream, flush, args.steps, args.warmup, eng)
     launches = eng.last_launch_count()
     ms, kms = t["ms"], t["kernel_ms"]
     got_d, got_g = d_hat.cpu().numpy(), grad.cpu().numpy()
-    qh = torch.tensor(qb, dtype=torch.float64).pin_memory().numpy()
-    outs = [sd.SmoothResults(torch.empty(Q, dtype=torch.float64).pin_memory().numpy(),
-                             torch.empty(Q, 3, dtype=torch.float64).pin_memory().numpy()) for _ in range(2)]
+    # end to end through the pipelined host API; with several ranks each
+    # takes an equal contiguous block of the Morton-sorted batch (the host
+    # API has no packet-sharded form)
+    if sharded:
+        order = sharding.morton_order(q)
+        lo, hi = sharding.query_ranges(Q_total, W)[R]
+        qe = np.ascontiguousarray(q[order[lo:hi]])
+    else:
+        qe = q
+    qh = torch.tensor(qe, dtype=torch.float64).pin_memory().numpy()
+    outs = [sd.SmoothResults(torch.empty(len(qe), dtype=torch.float64).pin_memory().numpy(),
+                             torch.empty(len(qe), 3, dtype=torch.float64).pin_memory().numpy()) for _ in range(2)]
     ne2e = max(3, min(args.steps, 10))
     tp = time_e2e_pipelined(run, eng, qh, P, sd.SD_BVH, outs, ne2e)
     te = time_e2e(run, lambda: eng.query_points(qh, P, sd.SD_BVH, out=outs[0]), ne2e)
-    e2e = {"value": Q_total / tp, "unit": "queries/s", "h2d_bytes_per_step": Q * 24, "d2h_bytes_per_step": Q * 32,
-           "steps": ne2e,
+    q_job = Q_total if world > 1 or not sharded else Q  # a virtual shard reports its own rate
+    e2e = {"value": q_job / tp, "unit": "queries/s", "h2d_bytes_per_step": len(qe) * 24,
+           "d2h_bytes_per_step": len(qe) * 32, "steps": ne2e,
            "api": "sd_query_points_async (pinned host fp64 queries in, d_hat + grad out; batches submitted back "
-                  "to back, two in flight)",
-           "blocking_call": {"value": Q_total / te, "api": "sd_query_points"}}
+                  "to back, two in flight)" + ("; per rank an equal Morton block of the batch" if sharded else ""),
+           "blocking_call": {"value": q_job / te, "api": "sd_query_points"}}
     L, F, Qs = run.reduce([L, F, float(Q)], "sum")
     pops = 2 * (L + F) - Qs
     flops = (FLOPS_BOX_TEST * pops + FLOPS_FAR_TERM * F + FLOPS_PER_PAIR[2] * L) / world
     nbytes = (BYTES_NODE * pops + BYTES_LEAF * L) / world
-    out = {"metric": "BVH queries/s (value+grad)", "value": Q_total / (ms * 1e-3), "unit": "queries/s",
+    out = {"metric": "BVH queries/s (value+grad)", "value": q_job / (ms * 1e-3), "unit": "queries/s",
            "scaling": "strong", "e2e": e2e, "ms_per_step": ms, "queries": Q_total, "queries_per_gpu": Q,
            "primitives": len(w.kinds),
            "workload": "cfg4: icosphere(9) with radial displacement, 5,242,880 triangles, 4,194,304 queries "
@@ -753,6 +758,10 @@ def measure_bvh(args, run, stream, flush, peaks, fp64=False):
            "per_query": {"leaves": L / Qs, "far_field": F / Qs, "nodes_popped": pops / Qs},
            "setup_s": {"total": setup_s, "build_weights": tw, "build_tree": tb},
            "gpu_launches": launches * args.steps}
+    if sharded:
+        out["sharding"] = {"world": W, "rank": R, "virtual": world == 1,
+                           "split": "chunks of 32-query packets of the Hilbert-sorted batch dealt round robin "
+                                    "(sd_query_points_device_shard)"}
     if kms:
         peak, src, cands = compute_peak(peaks, t["clocks"].get("sm_mhz"), fp64)
         achieved = flops / (kms * 1e-3) / 1e12
@@ -765,17 +774,15 @@ def measure_bvh(args, run, stream, flush, peaks, fp64=False):
                 "modelled_l1l2_gbs": nbytes / (kms * 1e-3) / 1e9,
                 "modelled_bytes": "32 B per popped node + 100 B per exact leaf, served from L1/L2, not DRAM",
                 "traffic": None}
-        st = ncu_stamp("bvh_cfg4_f64" if fp64 else "bvh_cfg4_f32") if world == 1 else None
+        st = ncu_stamp("bvh_cfg4_f64" if fp64 else "bvh_cfg4_f32") if not sharded else None
         if st:
             roof["traffic"] = st.get("dram_bytes")
             roof["ncu"] = st
         out["roofline"] = roof
-    if balance:
-        out["balance"] = balance
     par = None
     if rank == 0 and not args.no_cpu:
-        par = bvh_parity(eng, v, w, wt, qb, counted, got_d, got_g, P, world == 1)
-        if world == 1:
+        par = bvh_parity(eng, v, w, wt, q, np.nonzero(mine)[0], counted, got_d, got_g, P, not sharded)
+        if world == 1 and not sharded:
             out["cpu_baseline"] = par.pop("cpu_baseline")
     if world > 1 and not args.no_weak:
         # weak scaling variant: every rank a full cfg4 batch of its own
@@ -793,7 +800,7 @@ def measure_bvh(args, run, stream, flush, peaks, fp64=False):
     return out, par
 
 
-def bvh_parity(eng, v, w, wt, qb, counted, got_d, got_g, P, full_batch, n_sample=65536):
+def bvh_parity(eng, v, w, wt, q, sel, counted, got_d, got_g, P, full_batch, n_sample=65536):
     """cfg4 at config scale: the oracle port on the SAME tree (exported in
     the reference layout) and table, on n_sample queries (half from each
     half of the distribution at N=1): decision hash and counters of every
@@ -803,13 +810,14 @@ def bvh_parity(eng, v, w, wt, qb, counted, got_d, got_g, P, full_batch, n_sample
     import paper_2108_10480_b200 as sd
     O, m, ws, t = oracle_objects(v, w.simplices, w.kinds, wt, eng.export_bvh())
     threads = O.hardware_threads()
-    Q = len(qb)
+    Q = len(q)
+    qb = q  # sample indices address the whole batch; sel = this rank's queries
     if full_batch:
         half = Q // 2
         idx = np.concatenate([np.linspace(0, half - 1, n_sample // 2), np.linspace(half, Q - 1, n_sample // 2)])
     else:
-        idx = np.linspace(0, Q - 1, min(n_sample, Q))
-    idx = idx.astype(np.int64)
+        idx = sel[np.linspace(0, len(sel) - 1, min(n_sample, len(sel))).astype(np.int64)]
+    idx = np.unique(idx.astype(np.int64))
     p = O.Params(alpha=P.alpha, alpha_u=P.alpha_u, beta=P.beta)
     ref = O.query(m, ws, qb[idx], p, tree=t, threads=threads)
     cd, cl, cf, ch = counted
@@ -827,11 +835,8 @@ def bvh_parity(eng, v, w, wt, qb, counted, got_d, got_g, P, full_batch, n_sample
                                                   for f in ("d_hat", "grad", "leaves", "far_field")))
     # the CPU baseline proper: a ~8 s sample of the same batch (both halves)
     n = int(min(Q, max(len(idx), len(idx) * 8.0 / max(rr.seconds, 1e-3))))
-    if full_batch:
-        half = Q // 2
-        big = np.concatenate([qb[:n // 2], qb[half:half + n - n // 2]])
-    else:
-        big = qb[:n]
+    half = Q // 2
+    big = np.concatenate([qb[:n // 2], qb[half:half + n - n // 2]])
     rb = arm.query(big, P.alpha, P.alpha_u, P.beta, tree=True)
     out["cpu_baseline"] = {"value": len(big) / rb.seconds, "unit": "queries/s", "cores": arm.threads,
                            "kind": arm.kind,
@@ -1332,6 +1337,8 @@ def main():
     ap.add_argument("--exchange", choices=["nccl", "peer"], default="nccl",
                     help="--config 5 merge: NCCL all-reduce or stores into the owners' buffers over peer memory")
     ap.add_argument("--stub", action="store_true", help="CPU stand-in evaluator over gloo (plumbing tests)")
+    ap.add_argument("--shard-world", type=int, default=1, help=argparse.SUPPRESS)  # one rank's share on 1 GPU (tests)
+    ap.add_argument("--shard-rank", type=int, default=0, help=argparse.SUPPRESS)
     args = ap.parse_args()
     maybe_spawn(args)
     rank, world, local = dist_env()

@@ -36,7 +36,7 @@ assert NODE_DTYPE.itemsize == 72
 EXPORTED_SYMBOLS = (
     "sd_last_error", "sd_abi_version", "sd_create", "sd_destroy", "sd_set_geometry", "sd_set_weights",
     "sd_set_bvh", "sd_build_bvh", "sd_bvh_size", "sd_export_bvh", "sd_query_points", "sd_query_points_device",
-    "sd_finalize_device", "sd_query_points_async", "sd_query_wait", "sd_last_launch_count", "sd_set_kernel_timing", "sd_kernel_times", "sd_build_weights", "sd_weights_info", "sd_export_weights",
+    "sd_finalize_device", "sd_query_points_async", "sd_query_wait", "sd_query_points_device_shard", "sd_last_launch_count", "sd_set_kernel_timing", "sd_kernel_times", "sd_build_weights", "sd_weights_info", "sd_export_weights",
     "sd_mesh_dist_points",
     "sd_query_simplices",
     "sd_mesh_dist",
@@ -113,6 +113,7 @@ def lib():
             "sd_query_points": (C.c_int, [vp, vp, i64, P(_Params), C.c_int, P(_Outputs)]),
             "sd_query_points_device": (C.c_int, [vp, vp, i64, P(_Params), C.c_int, P(_Outputs), vp]),
             "sd_query_points_async": (C.c_int, [vp, vp, i64, P(_Params), C.c_int, P(_Outputs), P(i64)]),
+            "sd_query_points_device_shard": (C.c_int, [vp, vp, i64, P(_Params), P(_Outputs), i32, i32, vp]),
             "sd_query_wait": (C.c_int, [vp, i64]),
             "sd_finalize_device": (C.c_int, [vp, vp, vp, i64, P(_Params), vp, vp, vp]),
             "sd_last_launch_count": (C.c_int, [vp, P(i64)]),
@@ -325,6 +326,17 @@ class Engine:
         o = _Outputs(d_hat_ptr, grad_ptr, c_ptr, grad_c_ptr, leaves_ptr, far_ptr, hash_ptr)
         _check(lib().sd_query_points_device(self.h, C.c_void_p(q_ptr), n, C.byref(params._c()), mode, C.byref(o),
                                             C.c_void_p(stream) if stream else None))
+
+    def query_points_device_shard(self, q_ptr: int, n: int, params: SmoothParams, world: int, rank: int,
+                                  d_hat_ptr: int, grad_ptr: int | None = None, leaves_ptr: int | None = None,
+                                  far_ptr: int | None = None, hash_ptr: int | None = None,
+                                  stream: int | None = None):
+        """This rank's interleaved share (packets rank, rank + world, ...)
+        of the tree evaluation of the whole device batch q_ptr
+        (sd_query_points_device_shard); other output entries untouched."""
+        o = _Outputs(d_hat_ptr, grad_ptr, None, None, leaves_ptr, far_ptr, hash_ptr)
+        _check(lib().sd_query_points_device_shard(self.h, C.c_void_p(q_ptr), n, C.byref(params._c()), C.byref(o),
+                                                  world, rank, C.c_void_p(stream) if stream else None))
 
     def finalize_device(self, c_ptr: int, grad_c_ptr: int, n: int, params: SmoothParams, d_hat_ptr: int,
                         grad_ptr: int | None, stream: int | None = None):

@@ -959,6 +959,37 @@ int sd_query_points_device(sd_ctx* c, const void* q, int64_t Q, const sd_params*
     });
 }
 
+constexpr int kShardChunk = 1024;  // max packets per round-robin chunk of sd_query_points_device_shard
+
+int sd_query_points_device_shard(sd_ctx* c, const void* q, int64_t Q, const sd_params* p, const sd_outputs* o,
+                                 int32_t world, int32_t rank, void* stream) {
+    return guard([&] {
+        if (!c) throw ArgError{"ctx is NULL"};
+        check_params(p);
+        check_ready(*c, SD_BVH);
+        if (world < 1 || rank < 0 || rank >= world) throw ArgError{"bad world / rank"};
+        if (Q < 0 || (Q > 0 && (!q || !o || !o->d_hat))) throw ArgError{"bad query / output pointers"};
+        if (!(p->beta > 0.0)) throw ArgError{"sd_query_points_device_shard is the tree path: beta must be > 0"};
+        DeviceScope ds(c->device);
+        FinalizeOut out{o->d_hat, o->grad, o->c, o->grad_c, o->leaves, o->far_field, o->decision_hash};
+        out.pk_world = world;
+        out.pk_rank = rank;
+        // chunks of packets dealt round robin: spatial locality within a
+        // chunk (the rank's node working set stays regional), balance across
+        // at least 16 chunks per rank; SDGPU_SHARD_CHUNK overrides.
+        // tools/scaling_projection.py (cfg4, each share timed alone on one
+        // GPU): 8 ranks 4.51x (1 packet per chunk) / 5.03x (64) / 5.33x
+        // (1024); cost-balanced contiguous blocks 3.94x
+        const char* ch = std::getenv("SDGPU_SHARD_CHUNK");
+        const int64_t npk = (Q + 31) / 32;
+        out.pk_chunk = ch && *ch ? std::max(1, std::atoi(ch))
+                                 : std::max<int64_t>(1, std::min<int64_t>(kShardChunk, npk / (int64_t(world) * 16)));
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        if (c->precision == SD_FP32) dispatch<float>(*c, static_cast<const float*>(q), Q, *p, SD_BVH, out, st);
+        else dispatch<double>(*c, static_cast<const double*>(q), Q, *p, SD_BVH, out, st);
+    });
+}
+
 int sd_query_points(sd_ctx* c, const double* q, int64_t Q, const sd_params* p, int mode, const sd_outputs* o) {
     return guard([&] {
         if (!c) throw ArgError{"ctx is NULL"};

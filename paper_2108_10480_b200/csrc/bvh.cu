@@ -765,8 +765,10 @@ void tree_query(Ctx& c, const T* q, int64_t Q, const sd_params& p, const Finaliz
         const char* e = std::getenv("SDGPU_FEW_SORT");
         return e && *e == '1';
     }();
-    const int64_t* perm = (!few_sort && variant_is_frontier(Q)) ? nullptr
-                                                                 : sort_queries(c, q, Q, root.lo, root.hi, st, launches, true);
+    const bool sharded = out.pk_world > 1;
+    const int64_t* perm = (!few_sort && !sharded && variant_is_frontier(Q))
+                              ? nullptr
+                              : sort_queries(c, q, Q, root.lo, root.hi, st, launches, true);
 
     // polynomial table: edge polys then triangle polys
     const int ne = int(c.edge_a.size() / 5), nt = int(c.tri_stored.size() / 13);
@@ -822,7 +824,10 @@ void tree_query(Ctx& c, const T* q, int64_t Q, const sd_params& p, const Finaliz
     // batches: K3 packets (tools/frontier_crossover.py: cfg4, 1k..262k
     // queries: K3F 0.10 / 0.32 / 0.73 / 2.06 / 6.8 ms vs K3 2.8 / 7.0 / 7.7 /
     // 6.3 / 7.3 ms; the full dense 4.19M batch: K3 29.7 ms in round 1)
-    if (!(use_frontier(Q, 65536) &&
+    a.pk_world = out.pk_world;
+    a.pk_rank = out.pk_rank;
+    a.pk_chunk = out.pk_chunk;
+    if (!(!sharded && use_frontier(Q, 65536) &&
           launch_frontier<T, PointVisit<T>>(c, c.dtree, a, out.hash != nullptr, st, launches, 32)))
         nsplits = launch_pair_traversal<T, PointVisit<T>>(c, c.dtree, a, out.hash != nullptr, st, launches, 1,
                                                              out.leaves || out.far_field);

@@ -8,6 +8,7 @@
 // producing kernels, so the fp64 sums here have the reference semantics.
 #include "exact.h"
 
+#include <algorithm>
 #include <cmath>
 
 #include <cub/cub.cuh>
@@ -70,7 +71,8 @@ __global__ void finalize_kernel(const double* __restrict__ part, int splits, int
                                 int64_t const_leaves, const int64_t* __restrict__ leaves_in,
                                 const int64_t* __restrict__ far_in, const uint64_t* __restrict__ hash_in,
                                 const int64_t* __restrict__ perm, FinalizeOut o) {
-    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t i = o.pk_world > 1 ? shard_packet(t >> 5, o.pk_world, o.pk_rank, o.pk_chunk) * 32 + (t & 31) : t;
     if (i >= Q) return;
     double M = -INFINITY;
     for (int k = 0; k < splits; ++k) M = fmax(M, double(part[size_t(k) * 5 * Q + i]));
@@ -128,7 +130,12 @@ cudaError_t launch_finalize(const double* part, int splits, int64_t Q, double al
             part, splits, Q, alpha, epsilon, const_leaves, leaves_in, far_in, hash_in, perm, out);
         return cudaGetLastError();
     }
-    const unsigned blocks = unsigned((Q + threads - 1) / threads);
+    int64_t n = Q;  // positions covered
+    if (out.pk_world > 1) {
+        n = shard_count((Q + 31) / 32, out.pk_world, out.pk_rank, out.pk_chunk) * 32;
+        if (n == 0) return cudaSuccess;
+    }
+    const unsigned blocks = unsigned((n + threads - 1) / threads);
     finalize_kernel<<<blocks, threads, 0, st>>>(part, splits, Q, alpha, epsilon, const_leaves, leaves_in, far_in,
                                                    hash_in, perm, out);
     return cudaGetLastError();

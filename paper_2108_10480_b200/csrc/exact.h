@@ -64,7 +64,22 @@ struct FinalizeOut {
     // overflowed ones, so the NaN is restored here)
     const float* qf = nullptr;
     const double* qd = nullptr;
+    // query-sharded tree evaluation (sd_query_points_device_shard): only
+    // this rank's chunks of pk_chunk 32-query packets of the sorted batch
+    // (chunk j belongs to rank j % pk_world)
+    int64_t pk_world = 1, pk_rank = 0, pk_chunk = 1;
 };
+
+// k-th packet of a rank's share (chunks of C packets dealt round robin)
+__host__ __device__ __forceinline__ int64_t shard_packet(int64_t k, int64_t W, int64_t r, int64_t C) {
+    return ((k / C) * W + r) * C + k % C;
+}
+// number of packets of the rank among npk
+__host__ __device__ __forceinline__ int64_t shard_count(int64_t npk, int64_t W, int64_t r, int64_t C) {
+    const int64_t full = npk / (C * W), rem = npk - full * C * W;
+    const int64_t tail = rem - r * C;
+    return full * C + (tail < 0 ? 0 : (tail > C ? C : tail));
+}
 
 cudaError_t launch_finalize(const double* part, int splits, int64_t Q, double alpha, double epsilon,
                             int64_t const_leaves, const int64_t* leaves_in, const int64_t* far_in,

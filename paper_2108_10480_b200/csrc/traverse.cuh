@@ -83,6 +83,9 @@ struct TraverseArgs {
     const double* qgeom;
     const int32_t* qdim;
     const double* leafgeom;
+    // query sharding (sd_query_points_device_shard): this rank walks its
+    // chunks of pk_chunk packets of the sorted batch (shard_packet)
+    int64_t pk_world = 1, pk_rank = 0, pk_chunk = 1;
     // K3Q leaf-queue capacity (entries per lane); leaf_coop: the queued
     // terms are evaluated by the whole warp (leaf_flush_coop) instead of
     // one per lane per round
@@ -160,7 +163,7 @@ __device__ __forceinline__ void pair_walk(const TraverseArgs<T>& a) {
     int4* st = stacks + (threadIdx.x >> 5) * a.stack_depth;
     // packet (32 sorted queries) and, when split, the slot
     const int64_t gwarp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    const int64_t packet = SPLIT ? gwarp / a.nslots : gwarp;
+    const int64_t packet = SPLIT ? gwarp / a.nslots : shard_packet(gwarp, a.pk_world, a.pk_rank, a.pk_chunk);
     const int slot = SPLIT ? int(gwarp % a.nslots) : 0;
     if (SPLIT && packet >= a.npackets) return;
     const int64_t i = packet * 32 + lane;
@@ -309,7 +312,8 @@ __device__ __forceinline__ void pair_walk_q(const TraverseArgs<T>& a) {
     const uint32_t lqw = smem_u32(lqs + (threadIdx.x & ~31u));  // the warp's lane 0
     const int lcap = a.lq_cap - 1;  // a step appends at most two entries per lane
     int nq = 0;  // pending leaf entries of this lane
-    const int64_t packet = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t packet =
+        shard_packet((int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5, a.pk_world, a.pk_rank, a.pk_chunk);
     const int64_t i = packet * 32 + lane;
     const bool valid = i < a.Q;
     const int64_t qi = valid ? (a.perm ? a.perm[i] : i) : 0;
@@ -560,7 +564,7 @@ int launch_pair_traversal(Ctx& c, DeviceTree& t, TraverseArgs<T>& a, bool hash, 
     const char* se = std::getenv("SDGPU_SPLIT");
     const int forced = se && *se ? std::atoi(se) : -1;
     int k = 0;
-    if (t.depth >= 2) {
+    if (t.depth >= 2 && a.pk_world <= 1) {  // (sharded walks never split)
         const int kmax = std::min(14, t.depth);
         if (forced >= 0) {
             k = std::min(forced, kmax);
@@ -612,7 +616,9 @@ int launch_pair_traversal(Ctx& c, DeviceTree& t, TraverseArgs<T>& a, bool hash, 
         }
     }
     check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)), "smem attr");
-    const int64_t warps = npackets * a.nslots;
+    const int64_t warps =
+        a.pk_world > 1 ? shard_count(npackets, a.pk_world, a.pk_rank, a.pk_chunk) : npackets * a.nslots;
+    if (warps == 0) return nsplits;
     kern<<<unsigned((warps * 32 + kTravThreads - 1) / kTravThreads), kTravThreads, smem, st>>>(a);
     check_cuda(cudaGetLastError(), "traverse kernel");
     ++launches;

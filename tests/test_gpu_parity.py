@@ -994,3 +994,46 @@ def test_pipelined_host_batches_equal_blocking_calls(sd, oracle, prec):
     for (q, mode), got in zip(batches, outs):
         ref = e.query_points(q, P, mode)
         assert np.array_equal(got.d_hat, ref.d_hat) and np.array_equal(got.grad, ref.grad)
+
+
+@pytest.mark.parametrize("prec,chunk", [(0, "1"), (1, "1"), (0, "4"), (0, "")])
+def test_query_sharded_tree_walk_equals_the_whole_batch(sd, oracle, prec, chunk, monkeypatch):
+    """sd_query_points_device_shard: ranks 0..world-1 each walk the
+    interleaved packets r, r + world, ... of the whole sorted batch and write
+    only their queries' outputs; together they reproduce the single walk of
+    the batch bit for bit (same packets, same per-lane work), entries of
+    other ranks are left untouched, decision hashes equal the oracle's."""
+    import torch
+    O = oracle
+    monkeypatch.setenv("SDGPU_FRONTIER", "0")
+    monkeypatch.setenv("SDGPU_SPLIT", "0")
+    monkeypatch.setenv("SDGPU_SHARD_CHUNK", chunk)  # packets per round-robin chunk ("" = the default 64)
+    m0 = O.random_scene(12, 400)
+    qs = O.QueryStream(1212).draw_points(m0, 3000)  # 94 packets, the last one ragged
+    m, q = prep(O, m0, qs, prec)
+    w, t = O.Weights.build(m), O.Tree.build(m)
+    e = engine_for(sd, O, m, w, prec, tree=t)
+    P = sd.SmoothParams(alpha=150.0, beta=0.5)
+    whole = e.smooth_min_dist(q, P)
+    dev = torch.device("cuda", 0)
+    Q = len(q)
+    qd = torch.tensor(q, dtype=torch.float64 if prec else torch.float32, device=dev)
+    world = 3
+    d = torch.full((Q,), float("nan"), dtype=torch.float64, device=dev)
+    g = torch.full((Q, 3), float("nan"), dtype=torch.float64, device=dev)
+    hs = torch.zeros(Q, dtype=torch.int64, device=dev)
+    written = []
+    for r in range(world):
+        before = d.clone()
+        e.query_points_device_shard(qd.data_ptr(), Q, P, world, r, d.data_ptr(), g.data_ptr(),
+                                    hash_ptr=hs.data_ptr())
+        torch.cuda.synchronize()
+        now = ~torch.isnan(d) & torch.isnan(before)
+        written.append(now.cpu().numpy())
+    cover = np.sum(written, axis=0)
+    assert (cover == 1).all()  # every query by exactly one rank
+    if chunk == "1":
+        assert 0.25 < written[0].mean() < 0.42
+    assert np.array_equal(d.cpu().numpy(), whole.d_hat) and np.array_equal(g.cpu().numpy(), whole.grad)
+    ref = O.query(m, w, q, O.Params(alpha=150.0, beta=0.5), tree=t)
+    assert (hs.cpu().numpy().view(np.uint64) == ref.decision_hash).all()
