@@ -20,7 +20,8 @@ from dataclasses import dataclass, field
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsdgpu.so")
+# SDGPU_LIB: another build of the same library (A/B timing, tools/lib_ab.py)
+LIB_PATH = os.environ.get("SDGPU_LIB") or os.path.join(_HERE, "libsdgpu.so")
 
 SD_FP32, SD_FP64 = 0, 1
 SD_EXACT, SD_BVH = 0, 1

@@ -355,9 +355,6 @@ static void prepare_exact(Ctx& c) {
     c.exact_ready = true;
 }
 
-// smallest Bernstein coefficient (certified lower bound of w~), 0 if none
-static double poly_lower_bound(const Ctx& c, int kind, int poly);
-
 template <class T>
 __global__ void convert_queries(const double* __restrict__ in, T* __restrict__ out, int64_t n) {
     const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -611,6 +608,9 @@ int sd_destroy(sd_ctx* c) {
                     if (e) cudaEventDestroy(e);
             if (c->in_stream) cudaStreamDestroy(c->in_stream);
             if (c->out_stream) cudaStreamDestroy(c->out_stream);
+            if (c->aux_stream) cudaStreamDestroy(c->aux_stream);
+            if (c->aux_fork) cudaEventDestroy(c->aux_fork);
+            if (c->aux_join) cudaEventDestroy(c->aux_join);
         }
         delete c;
     });

@@ -224,6 +224,7 @@ void split_tables(Ctx& c, DeviceTree& t, int k) {
 }
 
 void tree_upload(Ctx& c) {
+    c.dtree.contact_rc2 = -1.f;
     if (c.precision == SD_FP32) upload_tree_T<float>(c, c.dtree);
     else upload_tree_T<double>(c, c.dtree);
     c.dtree_ready = true;
@@ -259,12 +260,12 @@ __global__ void query_morton(const T* __restrict__ q, int64_t Q, double3 lo, dou
 
 // ------------------------------------------------------------ traversal
 // Unit-weight edge / triangle leaf (poly_index < 0): w = A^S.
-template <class T, int KIND>
+template <class T, int KIND, bool FIX>
 __device__ __forceinline__ void unit_term(const Phys<T>& ph, const Poly<T>& pc, T qx, T qy, T qz, const T* rec,
-                                          Acc<T>& acc) {
+                                          Acc<T>& acc, bool* contact) {
     acc.m -= ph.lw_unit;
     if constexpr (KIND == 1) edge_term<T, false, false>(ph, pc, qx, qy, qz, rec, acc);
-    else tri_term<T, false, false>(ph, pc, qx, qy, qz, rec, acc);
+    else tri_term<T, false, false, FIX>(ph, pc, qx, qy, qz, rec, acc, contact);
     acc.m += ph.lw_unit;
 }
 
@@ -283,9 +284,12 @@ __device__ __forceinline__ bool decide64(const NodeT<T>& b, double d64, double q
 
 // Exact leaf term (smooth.hpp:51-61) of the primitive in leaf slot `slot`
 // for query q, added to acc.
-template <class T>
+// FIX / contact: see tri_contact (pair.cuh). K3 and K3F add the exact-
+// normal form inline (FIX); K3Q's cooperative flush adds the term as is
+// (FIX off) and K3C (contact_search) corrects it after the walk.
+template <class T, bool FIX = true>
 __device__ __forceinline__ void leaf_term(const TraverseArgs<T>& a, const Poly<T>* polys, int slot, T qx, T qy, T qz,
-                                          Acc<T>& acc) {
+                                          Acc<T>& acc, bool* contact = nullptr) {
     const int meta = a.leafmeta[slot];
     const int kind = meta & 3, poly = (meta >> 2) - 1;
     T rec[kRecTri];
@@ -300,12 +304,12 @@ __device__ __forceinline__ void leaf_term(const TraverseArgs<T>& a, const Poly<T
 #pragma unroll
         for (int j = 0; j < kRecEdge * int(sizeof(T)) / int(sizeof(V)); ++j) reinterpret_cast<V*>(rec)[j] = src[j];
         if (poly >= 0) edge_term<T, true, false>(a.ph, polys[poly], qx, qy, qz, rec, acc);
-        else unit_term<T, 1>(a.ph, polys[0], qx, qy, qz, rec, acc);
+        else unit_term<T, 1, FIX>(a.ph, polys[0], qx, qy, qz, rec, acc, contact);
     } else {
 #pragma unroll
         for (int j = 0; j < kRecTri * int(sizeof(T)) / int(sizeof(V)); ++j) reinterpret_cast<V*>(rec)[j] = src[j];
-        if (poly >= 0) tri_term<T, true, false>(a.ph, polys[a.ne + poly], qx, qy, qz, rec, acc);
-        else unit_term<T, 2>(a.ph, polys[0], qx, qy, qz, rec, acc);
+        if (poly >= 0) tri_term<T, true, false, FIX>(a.ph, polys[a.ne + poly], qx, qy, qz, rec, acc, contact);
+        else unit_term<T, 2, FIX>(a.ph, polys[0], qx, qy, qz, rec, acc, contact);
     }
 }
 
@@ -557,7 +561,9 @@ struct PointVisit {
                 asm volatile("ld.shared.s32 %0, [%1];"
                              : "=r"(slot)
                              : "r"(lqw + uint32_t(o) * 4u + uint32_t(t - oex) * kLeafStride));
-                leaf_term<T>(a, polys, -slot - 1, ox, oy, oz, it);  // queued: the leaf link -(slot + 1)
+                // (FIX off: near-contact face terms are corrected after the
+                // walk by K3C, contact_search, to keep this loop's registers)
+                leaf_term<T, false>(a, polys, -slot - 1, ox, oy, oz, it);  // the leaf link -(slot + 1)
             }
             // segmented max of the shifts, then segmented sums, over the
             // lanes of each owner's run in this round
@@ -750,6 +756,149 @@ template const int64_t* sort_queries<double>(Ctx&, const double*, int64_t, const
 
 static bool variant_is_frontier(int64_t Q) { return use_frontier(Q, 65536); }
 
+// K3C (fp32, with K3Q): the near-contact face terms. K3Q's cooperative
+// leaf flush adds every exact leaf term as evaluated (tri_term with FIX off,
+// pair.cuh: for a query within |ab| / 128 of a face's interior the fp32
+// offset ap - u ab - v ac is rounding noise in direction); adding the
+// exact-normal form inline costs the walk its register budget (56 -> 64+
+// registers, 5 % at cfg4), so K3C finds those terms on the side:
+//   contact_search -- on a second stream, concurrently with the walk: per
+//     query (the same sorted packets and shard) a depth-first walk over the
+//     boxes within r_c of the query (r_c = the largest |ab| / 128 of the
+//     mesh, x sqrt 2); at each triangle leaf tri_contact's own test
+//     (tri_near_contact); hits go to a list (sorted position, leaf slot);
+//   contact_apply -- after the walk: each hit's term evaluated as the walk
+//     did and in the exact-normal form, the difference added to the
+//     query's fp64 partial.
+// A face within |ab| / 128 of the query is always an exact leaf of the
+// walk (its box and every ancestor's is at distance <= d, never admissible
+// for beta < 128), so the corrected terms are exactly the walk's
+// near-contact terms.
+__global__ void __launch_bounds__(kTravThreads) contact_search(const __grid_constant__ TraverseArgs<float> a,
+                                                               float rc2, uint64_t* hits, unsigned* nhits,
+                                                               unsigned cap) {
+    extern __shared__ __align__(16) int32_t cstk[];  // per thread: entry k at [k * kTravThreads + tid]
+    const int64_t packet =
+        shard_packet((int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5, a.pk_world, a.pk_rank, a.pk_chunk);
+    const int64_t i = packet * 32 + (threadIdx.x & 31u);
+    if (i >= a.Q) return;
+    const int64_t qi = a.perm ? a.perm[i] : i;
+    const float qx = a.q[3 * qi], qy = a.q[3 * qi + 1], qz = a.q[3 * qi + 2];
+    auto near = [&](int32_t id) {
+        const NodeT<float> b = a.box[id];
+        const float dx = fmaxf(fmaxf(b.v[0] - qx, qx - b.v[4]), 0.f);
+        const float dy = fmaxf(fmaxf(b.v[1] - qy, qy - b.v[5]), 0.f);
+        const float dz = fmaxf(fmaxf(b.v[2] - qz, qz - b.v[6]), 0.f);
+        return fmaf(dx, dx, fmaf(dy, dy, dz * dz)) <= rc2;
+    };
+    // (per lane: each lane its own few root-to-leaf paths, far cheaper here
+    // than a packet walk over the union of 32 neighbourhoods)
+    int32_t* stk = cstk + threadIdx.x;
+    int sp = 0;
+    if (near(0)) stk[sp++ * kTravThreads] = 0;
+    while (sp > 0) {
+        const int32_t id = stk[--sp * kTravThreads];
+        int32_t link;
+        memcpy(&link, &a.box[id].v[7], sizeof(int32_t));
+        if (link >= 0) {  // internal: push the children within r_c (left on top)
+            if (near(link)) stk[sp++ * kTravThreads] = link;
+            if (near(id + 1)) stk[sp++ * kTravThreads] = id + 1;
+            continue;
+        }
+        const int slot = -link - 1;
+        if ((a.leafmeta[slot] & 3) != SD_TRIANGLE) continue;
+        float rec[16];
+        const float4* src = reinterpret_cast<const float4*>(a.leafrec + size_t(slot) * kRecTri);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) reinterpret_cast<float4*>(rec)[j] = src[j];  // a, ab, ac, A B C, 1/A 1/C 1/|bc|^2 1/det
+        if (!tri_near_contact(rec, qx, qy, qz)) continue;
+        const unsigned k = atomicAdd(nhits, 1u);
+        if (k < cap) hits[k] = (uint64_t(i) << 32) | uint32_t(slot);
+    }
+}
+
+__global__ void contact_apply(const __grid_constant__ TraverseArgs<float> a, const uint64_t* hits,
+                              const unsigned* nhits, unsigned cap) {
+    const unsigned n = min(*nhits, cap);
+    for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+        const int64_t i = int64_t(hits[k] >> 32);
+        const int slot = int(hits[k] & 0xffffffffu);
+        const int64_t qi = a.perm ? a.perm[i] : i;
+        const float qx = a.q[3 * qi], qy = a.q[3 * qi + 1], qz = a.q[3 * qi + 2];
+        Acc<float> was, fix;
+        was.init();
+        fix.init();
+        bool contact = false;
+        leaf_term<float, false>(a, a.polys, slot, qx, qy, qz, was, &contact);
+        if (!contact) continue;
+        leaf_term<float, true>(a, a.polys, slot, qx, qy, qz, fix);
+        const double M = a.part[i];  // the walk's anchor (finite: the term itself is in the sum)
+        const double fw = was.s != 0.f ? exp2(double(was.m) - M) : 0.0;
+        const double ff = fix.s != 0.f ? exp2(double(fix.m) - M) : 0.0;
+        atomicAdd(a.part + a.Q + i, double(fix.s) * ff - double(was.s) * fw);
+        atomicAdd(a.part + 2 * a.Q + i, double(fix.gx) * ff - double(was.gx) * fw);
+        atomicAdd(a.part + 3 * a.Q + i, double(fix.gy) * ff - double(was.gy) * fw);
+        atomicAdd(a.part + 4 * a.Q + i, double(fix.gz) * ff - double(was.gz) * fw);
+    }
+}
+
+// K3C search radius (2 x the largest |ab|^2 / 16384 of the mesh's
+// triangles: tri_contact's threshold with margin for the fp32 distance),
+// cached per tree upload; 0: no triangles.
+static float contact_radius2(Ctx& c) {
+    DeviceTree& t = c.dtree;
+    if (t.contact_rc2 < 0.f) {
+        double m = 0.0;
+        for (int64_t p = 0; p < c.N; ++p) {
+            if (c.kind[p] != SD_TRIANGLE) continue;
+            const double* x0 = &c.xyz[3 * size_t(c.sv[3 * p])];
+            const double* x1 = &c.xyz[3 * size_t(c.sv[3 * p + 1])];
+            const double dx = x1[0] - x0[0], dy = x1[1] - x0[1], dz = x1[2] - x0[2];
+            m = std::max(m, dx * dx + dy * dy + dz * dz);
+        }
+        t.contact_rc2 = float(2.0 * m / 16384.0);
+    }
+    return t.contact_rc2;
+}
+
+// Fork: contact_search on c.aux_stream once the sorted order exists on st
+// (call right before the walk's launch). Returns false if nothing to do.
+static bool contact_fork(Ctx& c, TraverseArgs<float>& a, cudaStream_t st, int64_t& launches) {
+    const float rc2 = contact_radius2(c);
+    if (rc2 == 0.f || a.Q == 0) return false;
+    const int64_t npackets = (a.Q + 31) / 32;
+    const int64_t warps = a.pk_world > 1 ? shard_count(npackets, a.pk_world, a.pk_rank, a.pk_chunk) : npackets;
+    if (warps == 0) return false;
+    if (!c.aux_stream) {
+        check_cuda(cudaStreamCreateWithFlags(&c.aux_stream, cudaStreamNonBlocking), "stream");
+        check_cuda(cudaEventCreateWithFlags(&c.aux_fork, cudaEventDisableTiming), "event");
+        check_cuda(cudaEventCreateWithFlags(&c.aux_join, cudaEventDisableTiming), "event");
+    }
+    c.contact_cap = unsigned(std::min<int64_t>(std::max<int64_t>(65536, a.Q / 64), int64_t(1) << 30));
+    uint64_t* hits = static_cast<uint64_t*>(c.contact_hits.ensure(size_t(c.contact_cap) * sizeof(uint64_t) + 64));
+    unsigned* nhits = reinterpret_cast<unsigned*>(hits + c.contact_cap);
+    check_cuda(cudaMemsetAsync(nhits, 0, sizeof(unsigned), st), "memset");
+    check_cuda(cudaEventRecord(c.aux_fork, st), "event");
+    check_cuda(cudaStreamWaitEvent(c.aux_stream, c.aux_fork, 0), "wait");
+    const size_t smem = size_t(a.stack_depth + 1) * kTravThreads * sizeof(int32_t);
+    contact_search<<<unsigned((warps * 32 + kTravThreads - 1) / kTravThreads), kTravThreads, smem, c.aux_stream>>>(
+        a, rc2, hits, nhits, c.contact_cap);
+    check_cuda(cudaGetLastError(), "contact search");
+    check_cuda(cudaEventRecord(c.aux_join, c.aux_stream), "event");
+    ++launches;
+    return true;
+}
+
+// Join: after the walk, st waits for the search and applies the hits.
+static void contact_join(Ctx& c, TraverseArgs<float>& a, cudaStream_t st, int64_t& launches) {
+    uint64_t* hits = c.contact_hits.as<uint64_t>();
+    unsigned* nhits = reinterpret_cast<unsigned*>(hits + c.contact_cap);
+    check_cuda(cudaStreamWaitEvent(st, c.aux_join, 0), "wait");
+    contact_apply<<<148, 128, 0, st>>>(a, hits, nhits, c.contact_cap);
+    check_cuda(cudaGetLastError(), "contact apply");
+    ++launches;
+}
+
 template <class T>
 void tree_query(Ctx& c, const T* q, int64_t Q, const sd_params& p, const FinalizeOut& out, cudaStream_t st) {
     if (!c.dtree_ready) tree_upload(c);
@@ -827,10 +976,22 @@ void tree_query(Ctx& c, const T* q, int64_t Q, const sd_params& p, const Finaliz
     a.pk_world = out.pk_world;
     a.pk_rank = out.pk_rank;
     a.pk_chunk = out.pk_chunk;
+    bool contact = false;  // K3C forked (fp32 K3Q walks)
     if (!(!sharded && use_frontier(Q, 65536) &&
-          launch_frontier<T, PointVisit<T>>(c, c.dtree, a, out.hash != nullptr, st, launches, 32)))
+          launch_frontier<T, PointVisit<T>>(c, c.dtree, a, out.hash != nullptr, st, launches, 32))) {
+        if constexpr (sizeof(T) == 4) {
+            static const bool no_contact = [] {  // SDGPU_NO_CONTACT=1 skips K3C (A/B timing only)
+                const char* e = std::getenv("SDGPU_NO_CONTACT");
+                return e && *e == '1';
+            }();
+            // (K3Q runs its cooperative flush exactly when these hold: see launch_pair_traversal)
+            if (!no_contact && will_use_coop_flush<T>(c.dtree, a)) contact = contact_fork(c, a, st, launches);
+        }
         nsplits = launch_pair_traversal<T, PointVisit<T>>(c, c.dtree, a, out.hash != nullptr, st, launches, 1,
                                                              out.leaves || out.far_field);
+    }
+    if constexpr (sizeof(T) == 4)
+        if (contact) contact_join(c, a, st, launches);  // K3C: K3Q's near-contact face terms
     timer.stop();
     check_cuda(launch_finalize(a.part, nsplits, Q, p.alpha, p.epsilon, 0, a.leaves, a.far, a.hash, perm, out, st),
                "finalize");

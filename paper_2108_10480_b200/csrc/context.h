@@ -88,6 +88,7 @@ struct DeviceTree {
     int depth = 0;
     bool exact_boxes = true;
     DevBuf box, pairs, count, lgcount, diam64, leafrec, leafmeta;
+    float contact_rc2 = -1.f;  // K3C search radius^2 (bvh.cu launch_contact_search); < 0: not computed
     int split_k = -1;         // depth of the cached split tables
     int64_t split_count = 0;  // slots at that depth
     DevBuf split_meta, split_path;  // see split_tables (bvh.cu)
@@ -150,6 +151,13 @@ struct Ctx {
     AsyncSlot slots[2];
     cudaStream_t in_stream = nullptr, out_stream = nullptr;
     int64_t next_ticket = 0;
+
+    // K3C (bvh.cu): side stream of the near-contact search, fork / join
+    // events, hit list
+    cudaStream_t aux_stream = nullptr;
+    cudaEvent_t aux_fork = nullptr, aux_join = nullptr;
+    DevBuf contact_hits;
+    unsigned contact_cap = 0;
 
     // scratch
     DevBuf qd, qT, part, out_d, out_g, out_c, out_gc, out_l, out_f, out_h;

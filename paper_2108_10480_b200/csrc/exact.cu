@@ -59,8 +59,13 @@ __device__ __forceinline__ void tot_merge(Tot& a, const Tot& b) {
 // tile never exceed 2^kTileHeadroom relative to the shift after the
 // proactive raise, and tiles whose bound is too loose for the fp32 range
 // (|kappa| diag + spread of log2 w > kLooseTile) keep the per-term checks.
-constexpr float kTileHeadroom = 100.0f;
-constexpr float kLooseTile = 200.0f;
+// The headroom leaves room for the gradient products: e r with r = 1/d up
+// to 2^50 (d >= 1e-15, the rsqrt floor) summed over a 768-term tile stays
+// below 2^64 + 50 + 10 = 2^124 (at 2^100 a query within ~4e-9 of a face
+// overflowed its gradient to -inf); the looseness cut keeps the tile's
+// largest term above 2^(64 - 164) = 2^-100, 26 bits clear of fp32 flush.
+constexpr float kTileHeadroom = 64.0f;
+constexpr float kLooseTile = 164.0f;
 
 constexpr int kThreads = 256;
 constexpr int kStages = 3;

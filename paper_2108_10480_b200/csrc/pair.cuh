@@ -189,7 +189,7 @@ __device__ __forceinline__ void edge_term(const Phys<T>& ph, const Poly<T>& pc, 
 // C = |ac|^2 the remaining dot products are d3 = d1 - A, d4 = d2 - B,
 // d5 = d1 - B, d6 = d2 - C, and va + vb + vc = AC - B^2.
 template <class T>
-__device__ __forceinline__ void tri_closest(const T* rec, T d1, T d2, T& u, T& v) {
+__device__ __forceinline__ void tri_closest(const T* rec, T d1, T d2, T& u, T& v, bool& inner) {
     const T A = rec[9], B = rec[10], C = rec[11];
     const T d3 = d1 - A, d4 = d2 - B, d5 = d1 - B, d6 = d2 - C;
     const T vc = fma(d1, d4, -d3 * d2);
@@ -199,12 +199,65 @@ __device__ __forceinline__ void tri_closest(const T* rec, T d1, T d2, T& u, T& v
     u = vb * rec[15];  // interior
     v = vc * rec[15];
     const T t6 = e43 * rec[14];  // edge bc
-    if (va <= T(0) && e43 >= T(0) && e56 >= T(0)) { u = T(1) - t6; v = t6; }
-    if (vb <= T(0) && d2 >= T(0) && d6 <= T(0)) { u = T(0); v = d2 * rec[13]; }  // edge ac
-    if (vc <= T(0) && d1 >= T(0) && d3 <= T(0)) { u = d1 * rec[12]; v = T(0); }  // edge ab
-    if (d6 >= T(0) && d5 <= d6) { u = T(0); v = T(1); }                         // vertex c
-    if (d3 >= T(0) && d4 <= d3) { u = T(1); v = T(0); }                         // vertex b
-    if (d1 <= T(0) && d2 <= T(0)) { u = T(0); v = T(0); }                       // vertex a
+    inner = true;
+    if (va <= T(0) && e43 >= T(0) && e56 >= T(0)) { u = T(1) - t6; v = t6; inner = false; }
+    if (vb <= T(0) && d2 >= T(0) && d6 <= T(0)) { u = T(0); v = d2 * rec[13]; inner = false; }  // edge ac
+    if (vc <= T(0) && d1 >= T(0) && d3 <= T(0)) { u = d1 * rec[12]; v = T(0); inner = false; }  // edge ab
+    if (d6 >= T(0) && d5 <= d6) { u = T(0); v = T(1); inner = false; }                         // vertex c
+    if (d3 >= T(0) && d4 <= d3) { u = T(1); v = T(0); inner = false; }                         // vertex b
+    if (d1 <= T(0) && d2 <= T(0)) { u = T(0); v = T(0); inner = false; }                       // vertex a
+}
+
+// Near-contact interior pairs in fp32 (the tree's exact leaves): q - p formed
+// as ap - u ab - v ac cancels down to a few ulps of |ap|, so for a query
+// within ~1e-8 of a face its direction -- the term's distance gradient
+// (exact.hpp:59-63) -- is rounding noise, while the reference (fp64) still
+// resolves it. Below d < |ab| / 128 the interior offset is taken as the
+// orthogonal projection onto the face normal instead, m (m . ap) / |m|^2
+// with m = G1 x G2 = n / |n|^2 (the record's shape gradients, exactly
+// parallel to n): its direction is exact to fp32 rounding of m whatever d.
+// Rare: cfg4's on-surface queries (d ~ 2e-9) had gradient errors up to
+// 4.6e-4 without it (1e-6 relative at most with it, the whole batch).
+// FIX: apply it (inline); otherwise *contact (if given) reports that it
+// would apply, so a register-tight caller can redo the term with FIX on a
+// rare, separate path (the cooperative leaf flush of K3Q).
+template <class T, bool FIX>
+__device__ __forceinline__ void tri_contact(const T* rec, bool inner, T apx, T apy, T apz, T& dx, T& dy, T& dz,
+                                            T& s, bool* contact) {
+    if constexpr (sizeof(T) == 4) {
+        const bool c = inner && s < rec[9] * T(1.0 / 16384.0);
+        if constexpr (FIX) {
+            if (c) {
+                const T mx = fma(rec[17], rec[21], -rec[18] * rec[20]);
+                const T my = fma(rec[18], rec[19], -rec[16] * rec[21]);
+                const T mz = fma(rec[16], rec[20], -rec[17] * rec[19]);
+                const T t = fma(mx, apx, fma(my, apy, mz * apz)) / fma(mx, mx, fma(my, my, mz * mz));
+                dx = t * mx;
+                dy = t * my;
+                dz = t * mz;
+                s = fma(dx, dx, fma(dy, dy, dz * dz));
+            }
+        } else if (contact) {
+            *contact = c;
+        }
+    }
+}
+
+// tri_contact's condition alone (the same operations as tri_term's
+// closest point, so the same decision): K3C's cheap test before it
+// re-evaluates a leaf term.
+__device__ __forceinline__ bool tri_near_contact(const float* rec, float qx, float qy, float qz) {
+    const float apx = qx - rec[0], apy = qy - rec[1], apz = qz - rec[2];
+    const float d1 = fmaf(rec[3], apx, fmaf(rec[4], apy, rec[5] * apz));
+    const float d2 = fmaf(rec[6], apx, fmaf(rec[7], apy, rec[8] * apz));
+    float u, v;
+    bool inner;
+    tri_closest(rec, d1, d2, u, v, inner);
+    const float dx = fmaf(-v, rec[6], fmaf(-u, rec[3], apx));
+    const float dy = fmaf(-v, rec[7], fmaf(-u, rec[4], apy));
+    const float dz = fmaf(-v, rec[8], fmaf(-u, rec[5], apz));
+    const float s = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+    return inner && s < rec[9] * (1.0f / 16384.0f);
 }
 
 // base = A w~ and the K-scaled barycentric gradient of w~ (see Poly), in
@@ -230,20 +283,22 @@ __device__ __forceinline__ void tri_poly(const Poly<T>& pc, T x, T y, T& w, T& w
 }
 
 // rec: see device_common.cuh (kRecTri)
-template <class T, bool POLY, bool SAFE>
+template <class T, bool POLY, bool SAFE, bool FIX = false>
 __device__ __forceinline__ void tri_term(const Phys<T>& ph, const Poly<T>& pc, T qx, T qy, T qz, const T* rec,
-                                         Acc<T>& acc) {
+                                         Acc<T>& acc, bool* contact = nullptr) {
     const T apx = qx - rec[0], apy = qy - rec[1], apz = qz - rec[2];
     const T abx = rec[3], aby = rec[4], abz = rec[5];
     const T acx = rec[6], acy = rec[7], acz = rec[8];
     const T d1 = fma(abx, apx, fma(aby, apy, abz * apz));
     const T d2 = fma(acx, apx, fma(acy, apy, acz * apz));
     T u, v;
-    tri_closest(rec, d1, d2, u, v);
-    const T dx = fma(-v, acx, fma(-u, abx, apx));
-    const T dy = fma(-v, acy, fma(-u, aby, apy));
-    const T dz = fma(-v, acz, fma(-u, abz, apz));
-    const T s = fma(dx, dx, fma(dy, dy, dz * dz));
+    bool inner;
+    tri_closest(rec, d1, d2, u, v, inner);
+    T dx = fma(-v, acx, fma(-u, abx, apx));
+    T dy = fma(-v, acy, fma(-u, aby, apy));
+    T dz = fma(-v, acz, fma(-u, abz, apz));
+    T s = fma(dx, dx, fma(dy, dy, dz * dz));
+    tri_contact<T, FIX>(rec, inner, apx, apy, apz, dx, dy, dz, s, contact);
     const T r = Math<T>::rsqrt(fmax(s, Tiny<T>::v));
     const T d = s * r;
     if constexpr (POLY && SAFE) {  // no reciprocal: see edge_term

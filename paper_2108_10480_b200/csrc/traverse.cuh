@@ -94,6 +94,17 @@ struct TraverseArgs {
 };
 
 constexpr int kTravThreads = 128;
+// K3Q launch bounds; A/B builds (tools/build_ab.sh): EXTRA=-DSD_TRAV_MINB=k
+// (CTA floor) or -DSD_TRAV_MAXNREG=n. Measured (cfg4): both caps at 56
+// registers run ~4 % slower than the unconstrained build, which lands on
+// 56 by itself -- and any code added to the walk's loop takes it to 64+.
+#ifdef SD_TRAV_MINB
+#define SD_TRAV_BOUNDS __launch_bounds__(kTravThreads, SD_TRAV_MINB)
+#elif defined(SD_TRAV_MAXNREG)
+#define SD_TRAV_BOUNDS __maxnreg__(SD_TRAV_MAXNREG)
+#else
+#define SD_TRAV_BOUNDS __launch_bounds__(kTravThreads)
+#endif
 
 // shared-memory bytes of the polynomial table, padded so the stacks after it
 // stay 16-byte aligned
@@ -406,7 +417,7 @@ __device__ __forceinline__ void pair_walk_q(const TraverseArgs<T>& a) {
 }
 
 template <class T, class VIS, bool HASH, bool COUNT, bool COOP = false>
-__global__ void __launch_bounds__(kTravThreads) pair_kernel_q(const __grid_constant__ TraverseArgs<T> a) {
+__global__ void SD_TRAV_BOUNDS pair_kernel_q(const __grid_constant__ TraverseArgs<T> a) {
     pair_walk_q<T, VIS, HASH, COUNT || HASH, COOP>(a);
 }
 
@@ -550,17 +561,11 @@ inline bool use_frontier(int64_t Q, int64_t limit) {
     return Q <= limit;
 }
 
-// Launches K3 (unsplit, or split at depth k for few queries) for VIS over
-// the tree t and returns the number of fp64 partial slots written to a.part
-// (merged by K4). a.part must hold 5 Q doubles; it is re-pointed when
-// splitting. `weight` raises the warp target for expensive node tests.
-template <class T, class VIS>
-int launch_pair_traversal(Ctx& c, DeviceTree& t, TraverseArgs<T>& a, bool hash, cudaStream_t st, int64_t& launches,
-                          int weight = 1, bool count = true) {
-    const int64_t Q = a.Q;
-    size_t smem = poly_bytes<T>(a.npoly) + size_t(a.stack_depth) * (kTravThreads / 32) * sizeof(int4);
-    const int64_t npackets = (Q + 31) / 32;
-    // SDGPU_SPLIT = 0 disables, = k forces depth k (A/B runs and tests)
+// Split depth of launch_pair_traversal (0: unsplit). SDGPU_SPLIT = 0
+// disables, = k forces depth k (A/B runs and tests).
+template <class T>
+int pair_split_depth(const DeviceTree& t, const TraverseArgs<T>& a, int weight = 1) {
+    const int64_t npackets = (a.Q + 31) / 32;
     const char* se = std::getenv("SDGPU_SPLIT");
     const int forced = se && *se ? std::atoi(se) : -1;
     int k = 0;
@@ -571,8 +576,45 @@ int launch_pair_traversal(Ctx& c, DeviceTree& t, TraverseArgs<T>& a, bool hash, 
         } else {  // >= ~32 (x weight) warps per SM
             while (k < kmax && npackets * (int64_t(1) << k) < int64_t(148) * 32 * weight) ++k;
         }
-        while (k > 0 && (size_t(1) << k) * 5 * size_t(Q) * sizeof(double) > (size_t(1) << 31)) --k;
+        while (k > 0 && (size_t(1) << k) * 5 * size_t(a.Q) * sizeof(double) > (size_t(1) << 31)) --k;
     }
+    return k;
+}
+
+// Leaf-queue switches of K3Q: SDGPU_LEAF_QUEUE = 0 turns the deferred leaf
+// queues off (A/B); SDGPU_LEAF_COOP = 1 / 0: queued leaf terms evaluated by
+// the whole warp (leaf_flush_coop) / one per lane per round; default: the
+// cooperative flush in fp32 (cfg4 21.9 -> 20.4 ms), per-lane rounds in fp64
+// (52.5 vs 55.5 ms).
+inline bool leaf_queue_on() {
+    const char* e = std::getenv("SDGPU_LEAF_QUEUE");
+    return !(e && *e == '0');
+}
+template <class T>
+int leaf_coop_default() {
+    const char* e = std::getenv("SDGPU_LEAF_COOP");
+    return (e && *e) ? (*e == '1' ? 1 : 0) : (sizeof(T) == 4 ? 1 : 0);
+}
+
+// True when launch_pair_traversal (point queries, weight 1) will run K3Q
+// with the cooperative leaf flush -- the walk whose near-contact face terms
+// K3C corrects (bvh.cu).
+template <class T>
+bool will_use_coop_flush(const DeviceTree& t, const TraverseArgs<T>& a) {
+    return leaf_queue_on() && leaf_coop_default<T>() == 1 && pair_split_depth(t, a, 1) == 0;
+}
+
+// Launches K3 (unsplit, or split at depth k for few queries) for VIS over
+// the tree t and returns the number of fp64 partial slots written to a.part
+// (merged by K4). a.part must hold 5 Q doubles; it is re-pointed when
+// splitting. `weight` raises the warp target for expensive node tests.
+template <class T, class VIS>
+int launch_pair_traversal(Ctx& c, DeviceTree& t, TraverseArgs<T>& a, bool hash, cudaStream_t st, int64_t& launches,
+                          int weight = 1, bool count = true) {
+    const int64_t Q = a.Q;
+    size_t smem = poly_bytes<T>(a.npoly) + size_t(a.stack_depth) * (kTravThreads / 32) * sizeof(int4);
+    const int64_t npackets = (Q + 31) / 32;
+    const int k = pair_split_depth(t, a, weight);
     a.split_depth = k;
     a.npackets = npackets;
     a.nslots = 1;
@@ -590,20 +632,14 @@ int launch_pair_traversal(Ctx& c, DeviceTree& t, TraverseArgs<T>& a, bool hash, 
     }
     auto kern = k > 0 ? (hash ? pair_kernel<T, VIS, true, 1> : pair_kernel<T, VIS, false, 1>)
                       : (hash ? pair_kernel<T, VIS, true, 0> : pair_kernel<T, VIS, false, 0>);
-    if constexpr (VIS::kLeafQueue) {  // SDGPU_LEAF_QUEUE = 0 turns the deferred leaf queues off (A/B)
+    if constexpr (VIS::kLeafQueue) {  // leaf queues: see leaf_queue_on / leaf_coop_default
         // SDGPU_LEAFQ: leaf-queue entries per lane (>= 3)
         auto cap = [](const char* name, int dflt) {
             const char* e = std::getenv(name);
             return e && *e ? std::max(0, std::min(64, std::atoi(e))) : dflt;
         };
-        const char* lqe = std::getenv("SDGPU_LEAF_QUEUE");
-        const bool lq_on = !(lqe && *lqe == '0');
-        // SDGPU_LEAF_COOP = 1 / 0: queued leaf terms evaluated by the whole
-        // warp (leaf_flush_coop) / one per lane per round; default: the
-        // cooperative flush in fp32 (cfg4 21.9 -> 20.4 ms), per-lane rounds
-        // in fp64 (52.5 vs 55.5 ms)
-        const char* lce = std::getenv("SDGPU_LEAF_COOP");
-        a.leaf_coop = (lce && *lce) ? (*lce == '1' ? 1 : 0) : (sizeof(T) == 4 ? 1 : 0);
+        const bool lq_on = leaf_queue_on();
+        a.leaf_coop = leaf_coop_default<T>();
         a.lq_cap = std::max(3, cap("SDGPU_LEAFQ", a.leaf_coop ? kLeafQCoop : kLeafQ));
         if (lq_on && k == 0) {
             smem += size_t(a.lq_cap) * kTravThreads * sizeof(int32_t);

@@ -340,9 +340,77 @@ def test_config4_parity_65536_queries(sd, oracle, kernel, monkeypatch):
     fin = np.isfinite(ref.d_hat)
     strict = np.abs(got.d_hat[fin] - ref.d_hat[fin]) / np.maximum(np.abs(ref.d_hat[fin]), 1.0 / 200.0)
     assert strict.max() <= 1e-5, strict.max()
+    gs = np.linalg.norm(got.grad[fin] - ref.grad[fin], axis=1) / np.maximum(np.linalg.norm(ref.grad[fin], axis=1), 1e-3)
+    assert gs.max() <= 1e-4, gs.max()
     ex = e.smooth_min_dist_flat(q, sd.SmoothParams(alpha=200.0, beta=0.0))
     both = np.isfinite(ex.d_hat) & fin
     assert (got.d_hat[both] <= ex.d_hat[both] + 1e-5).all()
+
+
+def test_config4_whole_batch_fp32_against_fp64(sd):
+    """The whole cfg4 batch (4,194,304 queries, the bench's BVH leg): the
+    fp32 tree path (K3Q + the K3C near-contact correction) against the fp64
+    tree path, which matches the compiled reference to ~1e-13 (bench parity,
+    test_config4_parity_65536_queries at fp64). Same decisions and counters
+    on every query; d_hat within 1e-5 and grad within 1e-4 in the STRICT
+    relative forms (floors 1/alpha and 1e-3). Without K3C, 110 queries
+    within ~1e-6 of a face failed the gradient bound (up to 2e-2 relative:
+    their fp32 face offsets are rounding noise in direction)."""
+    from paper_2108_10480_b200 import configs
+    w, q = configs.cfg4()
+    v, q = configs.quantize(w.vertices), configs.quantize(q)
+    P = sd.SmoothParams(alpha=w.alpha, alpha_u=600.0, beta=w.beta)
+    res = {}
+    for prec in (sd.SD_FP32, sd.SD_FP64):
+        e = sd.Engine(0, prec)
+        e.set_geometry(v, w.simplices, w.kinds)
+        e.build_weights()
+        e.build_bvh(sd.SD_BVH_MEDIAN)
+        res[prec] = e.smooth_min_dist(q, P)
+        e.close()
+    a, b = res[sd.SD_FP32], res[sd.SD_FP64]
+    assert (a.decision_hash == b.decision_hash).all()
+    assert (a.leaves == b.leaves).all() and (a.far_field == b.far_field).all()
+    fin = np.isfinite(b.d_hat)
+    assert (np.isfinite(a.d_hat) == fin).all()
+    dd = np.abs(a.d_hat[fin] - b.d_hat[fin]) / np.maximum(np.abs(b.d_hat[fin]), 1.0 / w.alpha)
+    assert dd.max() <= 1e-5, dd.max()
+    gn = np.linalg.norm(b.grad[fin], axis=1)
+    gs = np.linalg.norm(a.grad[fin] - b.grad[fin], axis=1) / np.maximum(gn, 1e-3)
+    assert gs.max() <= 1e-4, (gs.max(), int((gs > 1e-4).sum()))
+
+
+@pytest.mark.parametrize("kernel", ["K3Q", "K3F"])
+def test_exact_gradient_finite_at_contact(sd, oracle, kernel, monkeypatch):
+    """A query within ~1e-9 of a face (cfg4 has ~100 such queries): the fp32
+    exact kernel's tile shift allows terms up to 2^kTileHeadroom, and with
+    r = 1/d ~ 4e8 the gradient product overflowed to -inf at a headroom of
+    2^100 (exact.cu); it must stay finite, and the tree path (K3C) must
+    resolve the direction like the fp64 path (K3Q + K3C, or K3F inline)."""
+    O = oracle
+    monkeypatch.setenv("SDGPU_FRONTIER", "1" if kernel == "K3F" else "0")
+    monkeypatch.setenv("SDGPU_SPLIT", "0")
+    m = O.icosphere(4).quantized()
+    w = O.Weights.build(m)
+    V = m.vertices
+    f = m.simplices[7]
+    p = (V[f[0]] + V[f[1]] + V[f[2]]) / 3.0
+    n = np.cross(V[f[1]] - V[f[0]], V[f[2]] - V[f[0]])
+    n /= np.linalg.norm(n)
+    q = np.array([p + t * n for t in (2e-9, -3e-9, 1e-7, 5e-6)], np.float32).astype(np.float64)
+    out = {}
+    for prec in (0, 1):
+        e = engine_for(sd, O, m, w, prec)
+        e.build_bvh(sd.SD_BVH_MEDIAN)
+        out[prec, "exact"] = e.smooth_min_dist_flat(q, sd.SmoothParams(alpha=200.0, beta=0.0))
+        out[prec, "tree"] = e.query_points(q, sd.SmoothParams(alpha=200.0, beta=0.5), sd.SD_BVH, want_c=True)
+    for mode in ("exact", "tree"):
+        g32, g64 = out[0, mode].grad, out[1, mode].grad
+        assert np.isfinite(g32).all(), (mode, g32)
+    # the tree path (K3Q + K3C): strict gradient parity with fp64
+    gs = np.linalg.norm(out[0, "tree"].grad - out[1, "tree"].grad, axis=1) / np.maximum(
+        np.linalg.norm(out[1, "tree"].grad, axis=1), 1e-3)
+    assert gs.max() <= 1e-4, gs
 
 
 # ---------------------------------------------- full-size properties
