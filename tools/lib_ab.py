@@ -1,5 +1,6 @@
 """A/B timing of libsdgpu.so builds (tools/build_ab.sh) on the bench's BVH
-leg (cfg4, 4,194,304 queries, L2 flushed, CUDA events, median of REPS):
+leg (cfg4, 4,194,304 queries, L2 flushed, CUDA events, median of REPS;
+AB_SHARD=W: rank 0's share of a W-way sharded call; AB_CFG=3: exact cfg3):
   python tools/lib_ab.py ablibs/base ablibs/x[:ENV=VAL,...] ...   (rounds alternate)
 Each variant runs in its own process (one library per process)."""
 import json
@@ -30,7 +31,11 @@ eng = sd.Engine(0, sd.SD_FP32); eng.set_geometry(v, w.simplices, w.kinds); eng.b
 if mode == sd.SD_BVH: eng.build_bvh(sd.SD_BVH_AUTO)
 QD = torch.tensor(q, dtype=torch.float32, device=dev)
 D = torch.empty(len(q), dtype=torch.float64, device=dev); G = torch.empty(len(q), 3, dtype=torch.float64, device=dev)
-run = lambda: eng.query_points_device(QD.data_ptr(), len(q), P, mode, D.data_ptr(), G.data_ptr(), stream=st.cuda_stream)
+W = int(os.environ.get("AB_SHARD", "1"))  # > 1: rank 0's share of a W-way query-sharded call
+if W > 1:
+    run = lambda: eng.query_points_device_shard(QD.data_ptr(), len(q), P, W, 0, D.data_ptr(), G.data_ptr(), stream=st.cuda_stream)
+else:
+    run = lambda: eng.query_points_device(QD.data_ptr(), len(q), P, mode, D.data_ptr(), G.data_ptr(), stream=st.cuda_stream)
 for _ in range(3): run()
 ts = []
 for _ in range(int(os.environ.get("REPS", "9"))):
