@@ -854,6 +854,20 @@ def bvh_parity(eng, v, w, wt, q, sel, counted, got_d, got_g, P, full_batch, n_sa
     pos = np.searchsorted(idx, sub)
     out["gpu_exact_vs_oracle_exact"] = parity_stats(ex.d_hat[pos], ex.grad[pos], rex.d_hat, rex.grad, P.alpha, "f32")
     out["gpu_exact_vs_oracle_exact"]["sample"] = "32 of the sample queries x 5,242,880 triangles"
+    if eng.precision == sd.SD_FP32:
+        # every timed output of this rank against the fp64 tree path on the
+        # same tree (pinned to the reference by the sample above at fp64:
+        # test_config4_parity_65536_queries), decisions included
+        e64 = sd.Engine(eng.device, sd.SD_FP64)
+        e64.set_geometry(v, w.simplices, w.kinds)
+        e64.set_weight_table(wt)
+        e64.set_bvh(eng.export_bvh())
+        r64 = e64.smooth_min_dist(qb[sel], P)
+        e64.close()
+        wb = parity_stats(got_d[sel], got_g[sel], r64.d_hat, r64.grad, P.alpha, "f32")
+        wb.update({"n": int(len(sel)), "hash_mismatch": int((ch[sel] != r64.decision_hash).sum()),
+                   "sample": "every timed query of this rank (whole batch at N=1) vs the fp64 GPU tree path"})
+        out["whole_batch_vs_fp64"] = wb
     return out
 
 
