@@ -68,7 +68,10 @@ constexpr float kTileHeadroom = 64.0f;
 constexpr float kLooseTile = 164.0f;
 
 constexpr int kThreads = 256;
-constexpr int kStages = 3;
+#ifndef SD_K1_STAGES  // A/B builds (tools/build_ab.sh): EXTRA=-DSD_K1_STAGES=n -DSD_K1_MINB=k
+#define SD_K1_STAGES 3
+#endif
+constexpr int kStages = SD_K1_STAGES;
 
 template <class T, int KIND>
 constexpr int tile_prims() {
@@ -307,6 +310,9 @@ template <class T, int KIND>
 constexpr int minb_for() {
     // fp32: 3 CTAs/SM (<= 85 registers): cfg2 6.89 ms vs 6.92 at one CTA floor
     // (126 registers), cfg3 1.113 s vs 1.128 s
+#ifdef SD_K1_MINB
+    if constexpr (sizeof(T) == 4) return SD_K1_MINB;
+#endif
     return sizeof(T) == 4 ? 3 : (KIND != 0 ? 2 : 1);
 }
 

@@ -23,9 +23,11 @@ if cfg == "4":
     w, q = configs.cfg4(); mode = sd.SD_BVH
     P = sd.SmoothParams(alpha=w.alpha, alpha_u=600.0, beta=w.beta)
 else:
-    w, q = configs.cfg3(); mode = sd.SD_EXACT
+    import bench
+    v, T, K, q = bench.cfg3_workload(); mode = sd.SD_EXACT
     q = q[: int(os.environ.get("AB_NQ", "131072"))]
     P = sd.SmoothParams(alpha=100.0, alpha_u=600.0, beta=0.0)
+    w = type("W", (), {"vertices": v, "simplices": T, "kinds": K})
 v, q = configs.quantize(w.vertices), configs.quantize(q)
 eng = sd.Engine(0, sd.SD_FP32); eng.set_geometry(v, w.simplices, w.kinds); eng.build_weights()
 if mode == sd.SD_BVH: eng.build_bvh(sd.SD_BVH_AUTO)
