@@ -56,16 +56,20 @@ __device__ __forceinline__ void tot_merge(Tot& a, const Tot& b) {
 }
 
 // Tile bounds (per warp, per staged tile; see exact_kernel): terms of a
-// tile never exceed 2^kTileHeadroom relative to the shift after the
-// proactive raise, and tiles whose bound is too loose for the fp32 range
-// (|kappa| diag + spread of log2 w > kLooseTile) keep the per-term checks.
-// The headroom leaves room for the gradient products: e r with r = 1/d up
-// to 2^50 (d >= 1e-15, the rsqrt floor) summed over a 768-term tile stays
-// below 2^64 + 50 + 10 = 2^124 (at 2^100 a query within ~4e-9 of a face
-// overflowed its gradient to -inf); the looseness cut keeps the tile's
-// largest term above 2^(64 - 164) = 2^-100, 26 bits clear of fp32 flush.
-constexpr float kTileHeadroom = 64.0f;
-constexpr float kLooseTile = 164.0f;
+// tile never exceed 2^H relative to the shift after the proactive raise,
+// and tiles whose bound is too loose for the fp32 range (|kappa| diag +
+// spread of log2 w > H + kLooseMargin: the tile's largest term could sit
+// below 2^-100 of the shift, within 26 bits of fp32 flush) keep the
+// per-term checks. H leaves room for the gradient products e r, r = 1/d:
+// H = 96 while the query is at least 2^-20 from the tile's box (r <= 2^20:
+// e r summed over a 768-term tile < 2^126), H = 64 closer (r up to 2^50,
+// the rsqrt floor: < 2^124). (A single H = 100 overflowed the gradient of
+// a query within ~4e-9 of a face to -inf; a single H = 64 made cfg2 tiles
+// loose and cost 9 %.)
+constexpr float kTileHeadroom = 96.0f;
+constexpr float kTileHeadroomNear = 64.0f;
+constexpr float kNearBox = 9.5367431640625e-07f;  // 2^-20
+constexpr float kLooseMargin = 100.0f;
 
 constexpr int kThreads = 256;
 #ifndef SD_K1_STAGES  // A/B builds (tools/build_ab.sh): EXTRA=-DSD_K1_STAGES=n -DSD_K1_MINB=k
@@ -204,8 +208,8 @@ __global__ void __launch_bounds__(kThreads, MINB) exact_kernel(const __grid_cons
             // bounds every exponent: the shift is raised once here.
             const int64_t g = (p0 + int64_t(t) * TILE) / TILE;
             const float4 lo4 = __ldg(a.tbox + 2 * g), hi4 = __ldg(a.tbox + 2 * g + 1);
-            const bool loose = float(-a.ph.kappa) * lo4.w + float(a.lwspan) > kLooseTile;
-            bool all_skip = true, all_inside = true;
+            const float span = float(-a.ph.kappa) * lo4.w + float(a.lwspan);
+            bool all_skip = true, all_inside = true, any_loose = false;
 #pragma unroll
             for (int k = 0; k < QPT; ++k) {
                 const float x = float(qx[k]), y = float(qy[k]), z = float(qz[k]);
@@ -219,8 +223,11 @@ __global__ void __launch_bounds__(kThreads, MINB) exact_kernel(const __grid_cons
                 const bool sk = qi[k] >= a.Q || dlo > float(a.ph.dmax);
                 all_skip = all_skip && sk;
                 all_inside = all_inside && (qi[k] >= a.Q || dhi < float(a.ph.dmax));
+                const float H = dlo < kNearBox ? kTileHeadroomNear : kTileHeadroom;
+                const bool loose = !sk && span > H + kLooseMargin;
+                any_loose = any_loose || loose;
                 if (!loose && !sk) {  // raise the shift to the tile's exponent bound
-                    const T up = T(fmaf(float(a.ph.kappa), dlo, float(a.lwmax))) - T(kTileHeadroom);
+                    const T up = T(fmaf(float(a.ph.kappa), dlo, float(a.lwmax))) - T(H);
                     if constexpr (PACKED) {
                         Acc2& a2 = acc2[k / 2];
                         const float mk = (k & 1) ? hi(a2.m) : lo(a2.m);
@@ -240,7 +247,7 @@ __global__ void __launch_bounds__(kThreads, MINB) exact_kernel(const __grid_cons
             }
             skip = __all_sync(0xffffffffu, all_skip);
             const bool inside = __all_sync(0xffffffffu, all_inside);
-            mode = loose ? 0 : (inside ? 2 : 1);
+            mode = __any_sync(0xffffffffu, any_loose) ? 0 : (inside ? 2 : 1);
         }
         if (!skip) {
             if constexpr (PACKED) {

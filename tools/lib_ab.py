@@ -1,6 +1,6 @@
 """A/B timing of libsdgpu.so builds (tools/build_ab.sh) on the bench's BVH
 leg (cfg4, 4,194,304 queries, L2 flushed, CUDA events, median of REPS;
-AB_SHARD=W: rank 0's share of a W-way sharded call; AB_CFG=3: exact cfg3):
+AB_SHARD=W: rank 0's share of a W-way sharded call; AB_CFG=3 / 2: exact cfg3 / cfg2):
   python tools/lib_ab.py ablibs/base ablibs/x[:ENV=VAL,...] ...   (rounds alternate)
 Each variant runs in its own process (one library per process)."""
 import json
@@ -22,6 +22,10 @@ flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 if cfg == "4":
     w, q = configs.cfg4(); mode = sd.SD_BVH
     P = sd.SmoothParams(alpha=w.alpha, alpha_u=600.0, beta=w.beta)
+elif cfg == "2":
+    import bench
+    w, wt, q = bench.cfg2_workload(); mode = sd.SD_EXACT
+    P = sd.SmoothParams(alpha=100.0, alpha_u=600.0, beta=0.0)
 else:
     import bench
     v, T, K, q = bench.cfg3_workload(); mode = sd.SD_EXACT
@@ -29,7 +33,9 @@ else:
     P = sd.SmoothParams(alpha=100.0, alpha_u=600.0, beta=0.0)
     w = type("W", (), {"vertices": v, "simplices": T, "kinds": K})
 v, q = configs.quantize(w.vertices), configs.quantize(q)
-eng = sd.Engine(0, sd.SD_FP32); eng.set_geometry(v, w.simplices, w.kinds); eng.build_weights()
+eng = sd.Engine(0, sd.SD_FP32); eng.set_geometry(v, w.simplices, w.kinds)
+if cfg == "2": eng.set_weights(wt.A, wt.sup_wtilde, wt.edge_a, wt.tri_stored, wt.poly_index)
+else: eng.build_weights()
 if mode == sd.SD_BVH: eng.build_bvh(sd.SD_BVH_AUTO)
 QD = torch.tensor(q, dtype=torch.float32, device=dev)
 D = torch.empty(len(q), dtype=torch.float64, device=dev); G = torch.empty(len(q), 3, dtype=torch.float64, device=dev)
