@@ -631,44 +631,73 @@ struct PointVisit {
     }
 };
 
-struct QBox {
-    float lo[3], hi[3];
-};
-struct QBoxUnion {
-    __device__ __forceinline__ QBox operator()(const QBox& a, const QBox& b) const {
-        QBox r;
-        for (int k = 0; k < 3; ++k) {
-            r.lo[k] = fminf(a.lo[k], b.lo[k]);
-            r.hi[k] = fmaxf(a.hi[k], b.hi[k]);
-        }
-        return r;
-    }
-};
+// The queries' bounding box as order-preserving uint32 images of the
+// fp32 coordinates (min in [0..2], max in [3..5]): one pass, a warp / block
+// reduction and one atomic per block and component (was a CUB reduce over
+// a 24-byte struct: 25 us at cfg4, now a few).
+__device__ __forceinline__ uint32_t ord_f32(float f) {
+    const uint32_t b = __float_as_uint(f);
+    return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ float unord_f32(uint32_t o) {
+    return __uint_as_float((o & 0x80000000u) ? (o & 0x7fffffffu) : ~o);
+}
+__global__ void qbox_init(uint32_t* ob) {
+    if (threadIdx.x < 6) ob[threadIdx.x] = threadIdx.x < 3 ? 0xffffffffu : 0u;
+}
 template <class T>
-struct QBoxOf {
-    const T* q;
-    __device__ __forceinline__ QBox operator()(int64_t i) const {
-        QBox r;
-        for (int k = 0; k < 3; ++k) r.lo[k] = r.hi[k] = float(q[3 * i + k]);
-        return r;
+__global__ void __launch_bounds__(256) qbox_reduce(const T* __restrict__ q, int64_t Q, uint32_t* ob) {
+    uint32_t lo[3] = {0xffffffffu, 0xffffffffu, 0xffffffffu}, hi[3] = {0u, 0u, 0u};
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < Q; i += int64_t(gridDim.x) * blockDim.x)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const float f = float(q[3 * i + k]);
+            if (f == f) {  // (NaN coordinates do not widen the box)
+                const uint32_t o = ord_f32(f);
+                lo[k] = min(lo[k], o);
+                hi[k] = max(hi[k], o);
+            }
+        }
+    __shared__ uint32_t red[6][8];
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+        for (int off = 16; off; off >>= 1) {
+            lo[k] = min(lo[k], __shfl_xor_sync(0xffffffffu, lo[k], off));
+            hi[k] = max(hi[k], __shfl_xor_sync(0xffffffffu, hi[k], off));
+        }
+    const int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0)
+        for (int k = 0; k < 3; ++k) {
+            red[k][w] = lo[k];
+            red[3 + k][w] = hi[k];
+        }
+    __syncthreads();
+    if (threadIdx.x < 3) {
+        uint32_t a = red[threadIdx.x][0], b = red[3 + threadIdx.x][0];
+        for (int j = 1; j < int(blockDim.x >> 5); ++j) {
+            a = min(a, red[threadIdx.x][j]);
+            b = max(b, red[3 + threadIdx.x][j]);
+        }
+        atomicMin(ob + threadIdx.x, a);
+        atomicMax(ob + 3 + threadIdx.x, b);
     }
-};
+}
 
 // Hilbert (or Morton) keys over the union of [lo, hi] (the root box) and
 // the queries' own box, read from device memory (no host round trip):
 // queries outside the scene keep distinct cells instead of piling up on its
-// faces
+// faces. Cells in fp32 (the order only shapes the packets, not the results).
 template <class T>
-__global__ void query_morton_union(const T* __restrict__ q, int64_t Q, double3 lo, double3 hi,
-                                   const QBox* __restrict__ qb, int hilbert, uint32_t* keys, int64_t* idx) {
+__global__ void query_morton_union(const T* __restrict__ q, int64_t Q, float3 lo, float3 hi,
+                                   const uint32_t* __restrict__ ob, int hilbert, uint32_t* keys, int64_t* idx) {
     const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= Q) return;
-    const double l[3] = {fmin(lo.x, double(qb->lo[0])), fmin(lo.y, double(qb->lo[1])), fmin(lo.z, double(qb->lo[2]))};
-    const double h[3] = {fmax(hi.x, double(qb->hi[0])), fmax(hi.y, double(qb->hi[1])), fmax(hi.z, double(qb->hi[2]))};
+    const float l[3] = {fminf(lo.x, unord_f32(ob[0])), fminf(lo.y, unord_f32(ob[1])), fminf(lo.z, unord_f32(ob[2]))};
+    const float h[3] = {fmaxf(hi.x, unord_f32(ob[3])), fmaxf(hi.y, unord_f32(ob[4])), fmaxf(hi.z, unord_f32(ob[5]))};
     uint32_t cell[3];
     for (int a = 0; a < 3; ++a) {
-        const double s = h[a] > l[a] ? 1024.0 / (h[a] - l[a]) : 0.0;
-        cell[a] = uint32_t(fmin(fmax((double(q[3 * i + a]) - l[a]) * s, 0.0), 1023.0));
+        const float s = h[a] > l[a] ? 1024.0f / (h[a] - l[a]) : 0.0f;
+        cell[a] = uint32_t(fminf(fmaxf((float(q[3 * i + a]) - l[a]) * s, 0.0f), 1023.0f));
     }
     uint32_t key = 0;
     if (hilbert) {
@@ -713,26 +742,23 @@ const int64_t* sort_queries(Ctx& c, const T* q, int64_t Q, const double lo[3], c
         return !(e && *e == '0');
     }();
     if (union_box && union_hilbert) {
-        QBox* qb = static_cast<QBox*>(c.qbox.ensure(sizeof(QBox)));
-        QBox init;
-        for (int k = 0; k < 3; ++k) {
-            init.lo[k] = INFINITY;
-            init.hi[k] = -INFINITY;
-        }
-        cub::CountingInputIterator<int64_t> cnt(0);
-        cub::TransformInputIterator<QBox, QBoxOf<T>, cub::CountingInputIterator<int64_t>> in(cnt, QBoxOf<T>{q});
-        size_t tb = 0;
-        cub::DeviceReduce::Reduce(nullptr, tb, in, qb, Q, QBoxUnion{}, init, st);
-        check_cuda(cub::DeviceReduce::Reduce(c.tmp.ensure(tb), tb, in, qb, Q, QBoxUnion{}, init, st), "query box");
+        uint32_t* ob = static_cast<uint32_t*>(c.qbox.ensure(6 * sizeof(uint32_t)));
+        qbox_init<<<1, 32, 0, st>>>(ob);
+        qbox_reduce<T><<<unsigned(std::min<int64_t>(148 * 8, std::max<int64_t>(1, (Q + 255) / 256))), 256, 0, st>>>(
+            q, Q, ob);
         // Hilbert order by default (SDGPU_HILBERT=0: Morton): no long jumps
         // inside a 32-query packet (cfg4 26.9 -> 26.2 ms)
         static const int hilbert = [] {
             const char* e = std::getenv("SDGPU_HILBERT");
             return e && *e == '0' ? 0 : 1;
         }();
-        query_morton_union<T><<<blocks, 256, 0, st>>>(q, Q, make_double3(lo[0], lo[1], lo[2]),
-                                                      make_double3(hi[0], hi[1], hi[2]), qb, hilbert, keys, idx);
-        launches += 2;
+        // (the root box rounded outward to fp32)
+        auto dn = [](double x) { return std::nextafter(float(x), -INFINITY); };
+        auto up = [](double x) { return std::nextafter(float(x), INFINITY); };
+        query_morton_union<T><<<blocks, 256, 0, st>>>(q, Q, make_float3(dn(lo[0]), dn(lo[1]), dn(lo[2])),
+                                                      make_float3(up(hi[0]), up(hi[1]), up(hi[2])), ob, hilbert, keys,
+                                                      idx);
+        launches += 3;
     } else {
         auto inv = [](double l, double h) { return h > l ? 1024.0 / (h - l) : 0.0; };
         const double3 dlo = make_double3(lo[0], lo[1], lo[2]);
@@ -741,10 +767,17 @@ const int64_t* sort_queries(Ctx& c, const T* q, int64_t Q, const double lo[3], c
         ++launches;
     }
     check_cuda(cudaGetLastError(), "query morton");
+    // SDGPU_SORT_BITS = b: order by the top b bits of the 30-bit key only
+    // (a coarser curve, fewer radix passes; A/B)
+    static const int lo_bit = [] {
+        const char* e = std::getenv("SDGPU_SORT_BITS");
+        const int b = e && *e ? std::atoi(e) : 30;
+        return 30 - std::min(30, std::max(6, b));
+    }();
     size_t tmp_bytes = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys, keys + Q, idx, idx + Q, int(Q), 0, 30, st);
+    cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys, keys + Q, idx, idx + Q, int(Q), lo_bit, 30, st);
     void* tmp = c.tmp.ensure(tmp_bytes);
-    check_cuda(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, keys + Q, idx, idx + Q, int(Q), 0, 30, st),
+    check_cuda(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, keys + Q, idx, idx + Q, int(Q), lo_bit, 30, st),
                "radix sort queries");
     launches += 4;  // onesweep histogram + passes (approximate count of CUB kernels)
     return idx + Q;
