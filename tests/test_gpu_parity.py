@@ -383,10 +383,10 @@ def test_config4_whole_batch_fp32_against_fp64(sd):
 @pytest.mark.parametrize("kernel", ["K3Q", "K3F"])
 def test_exact_gradient_finite_at_contact(sd, oracle, kernel, monkeypatch):
     """A query within ~1e-9 of a face (cfg4 has ~100 such queries): the fp32
-    exact kernel's tile shift allows terms up to 2^kTileHeadroom, and with
-    r = 1/d ~ 4e8 the gradient product overflowed to -inf at a headroom of
-    2^100 (exact.cu); it must stay finite, and the tree path (K3C) must
-    resolve the direction like the fp64 path (K3Q + K3C, or K3F inline)."""
+    exact kernel's tile shift allows terms up to 2^H, and with r = 1/d ~ 4e8
+    the gradient product overflowed to -inf at H = 100 (exact.cu); it must
+    stay finite; the tree path must resolve the offset direction like the
+    fp64 path (tri_contact: K3Q + K3C or K3F inline)."""
     O = oracle
     monkeypatch.setenv("SDGPU_FRONTIER", "1" if kernel == "K3F" else "0")
     monkeypatch.setenv("SDGPU_SPLIT", "0")
@@ -407,10 +407,11 @@ def test_exact_gradient_finite_at_contact(sd, oracle, kernel, monkeypatch):
     for mode in ("exact", "tree"):
         g32, g64 = out[0, mode].grad, out[1, mode].grad
         assert np.isfinite(g32).all(), (mode, g32)
-    # the tree path (K3Q + K3C): strict gradient parity with fp64
-    gs = np.linalg.norm(out[0, "tree"].grad - out[1, "tree"].grad, axis=1) / np.maximum(
-        np.linalg.norm(out[1, "tree"].grad, axis=1), 1e-3)
-    assert gs.max() <= 1e-4, gs
+        gs = np.linalg.norm(g32 - g64, axis=1) / np.maximum(np.linalg.norm(g64, axis=1), 1e-3)
+        # strict parity on the tree path (K3Q + K3C, or K3F inline); K1 keeps
+        # the cancelling offset form (DESIGN: near-contact faces): finite only
+        if mode == "tree":
+            assert gs.max() <= 1e-4, (mode, gs)
 
 
 # ---------------------------------------------- full-size properties
