@@ -171,11 +171,12 @@ int sd_query_points_device(sd_ctx* ctx, const void* q_dev, int64_t Q, const sd_p
 /* Query-sharded tree evaluation of ONE batch across `world` ranks (each
  * with the whole batch and the replicated geometry on its device): the
  * batch is sorted along the library's Hilbert order and cut into 32-query
- * packets; rank r walks the packets r, r + world, r + 2 world, ... and
- * writes the outputs of their queries only (the other entries of the output
- * arrays are left untouched). Interleaving whole packets keeps each packet
- * as spatially coherent as in the single-GPU walk and gives every rank the
- * same mix of cheap and expensive packets -- balanced without a cost model.
+ * packets, grouped into chunks of C consecutive packets (C = min(1024,
+ * packets / (16 world)); SDGPU_SHARD_CHUNK overrides) dealt round robin:
+ * rank r walks chunks r, r + world, ... and writes the outputs of their
+ * queries only (the other entries of the output arrays are left untouched).
+ * Whole packets stay as spatially coherent as in the single-GPU walk and
+ * every rank gets a mix of cheap and expensive regions -- no cost model.
  * Tree path only (beta > 0); device buffers on the caller's stream. */
 int sd_query_points_device_shard(sd_ctx* ctx, const void* q_dev, int64_t Q, const sd_params* p,
                                  const sd_outputs* out_dev, int32_t world, int32_t rank, void* stream);
