@@ -254,7 +254,8 @@ __global__ void query_morton(const T* __restrict__ q, int64_t Q, double3 lo, dou
     const uint32_t x = cell(double(q[3 * i]), lo.x, inv.x);
     const uint32_t y = cell(double(q[3 * i + 1]), lo.y, inv.y);
     const uint32_t z = cell(double(q[3 * i + 2]), lo.z, inv.z);
-    keys[i] = (spread10(x) << 2) | (spread10(y) << 1) | spread10(z);
+    const T a = q[3 * i], b = q[3 * i + 1], d = q[3 * i + 2];
+    keys[i] = (a == a && b == b && d == d) ? (spread10(x) << 2) | (spread10(y) << 1) | spread10(z) : 0xffffffffu;
     idx[i] = i;
 }
 
@@ -724,7 +725,8 @@ __global__ void query_morton_union(const T* __restrict__ q, int64_t Q, float3 lo
     } else {
         for (int a = 0; a < 3; ++a) key |= spread10(cell[a]) << (2 - a);
     }
-    keys[i] = key;
+    const T x = q[3 * i], y = q[3 * i + 1], z = q[3 * i + 2];
+    keys[i] = (x == x && y == y && z == z) ? key : 0xffffffffu;  // NaN: last, and flagged for K4
     idx[i] = i;
 }
 
@@ -1026,7 +1028,13 @@ void tree_query(Ctx& c, const T* q, int64_t Q, const sd_params& p, const Finaliz
     if constexpr (sizeof(T) == 4)
         if (contact) contact_join(c, a, st, launches);  // K3C: K3Q's near-contact face terms
     timer.stop();
-    check_cuda(launch_finalize(a.part, nsplits, Q, p.alpha, p.epsilon, 0, a.leaves, a.far, a.hash, perm, out, st),
+    FinalizeOut fo = out;
+    if (perm) {  // NaN queries flagged in the sorted keys (coalesced, no scattered query re-read)
+        fo.nan_keys = static_cast<const uint32_t*>(c.keys.p) + Q;
+        fo.qf = nullptr;
+        fo.qd = nullptr;
+    }
+    check_cuda(launch_finalize(a.part, nsplits, Q, p.alpha, p.epsilon, 0, a.leaves, a.far, a.hash, perm, fo, st),
                "finalize");
     ++launches;
     c.last_launches = launches;

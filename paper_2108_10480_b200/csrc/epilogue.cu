@@ -24,7 +24,9 @@ __device__ __forceinline__ void finalize_write(double M, double s, double gx, do
     double c = s * scale;
     double cx = gx * scale, cy = gy * scale, cz = gz * scale;
     const int64_t j = perm ? perm[i] : i;  // tree path: undo the query sort
-    if (o.qf || o.qd) {
+    if (o.nan_keys) {
+        if (o.nan_keys[i] == 0xffffffffu) c = cx = cy = cz = NAN;
+    } else if (o.qf || o.qd) {
         const double x = o.qf ? double(o.qf[3 * j]) : o.qd[3 * j];
         const double y = o.qf ? double(o.qf[3 * j + 1]) : o.qd[3 * j + 1];
         const double z = o.qf ? double(o.qf[3 * j + 2]) : o.qd[3 * j + 2];

@@ -64,6 +64,10 @@ struct FinalizeOut {
     // overflowed ones, so the NaN is restored here)
     const float* qf = nullptr;
     const double* qd = nullptr;
+    // or, for sorted tree batches: the sorted Hilbert keys, 0xffffffff
+    // marking a query with a NaN coordinate (query_morton*): read in sorted
+    // order instead of the scattered re-read of the query
+    const uint32_t* nan_keys = nullptr;
     // query-sharded tree evaluation (sd_query_points_device_shard): only
     // this rank's chunks of pk_chunk 32-query packets of the sorted batch
     // (chunk j belongs to rank j % pk_world)
