@@ -1033,6 +1033,8 @@ void tree_query(Ctx& c, const T* q, int64_t Q, const sd_params& p, const Finaliz
         fo.nan_keys = static_cast<const uint32_t*>(c.keys.p) + Q;
         fo.qf = nullptr;
         fo.qd = nullptr;
+        if (out.grad && !out.peers && out.pk_world <= 1)
+            fo.aos = static_cast<double*>(c.aos.ensure(size_t(Q) * 4 * sizeof(double)));
     }
     check_cuda(launch_finalize(a.part, nsplits, Q, p.alpha, p.epsilon, 0, a.leaves, a.far, a.hash, perm, fo, st),
                "finalize");

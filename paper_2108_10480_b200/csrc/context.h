@@ -161,7 +161,7 @@ struct Ctx {
 
     // scratch
     DevBuf qd, qT, part, out_d, out_g, out_c, out_gc, out_l, out_f, out_h;
-    DevBuf perm, keys, tmp, tmp2, counters, polys, flag, qbox;
+    DevBuf perm, keys, tmp, tmp2, counters, polys, flag, qbox, aos;
     int64_t last_launches = 0;
 
     // kernel timing (sd_set_kernel_timing): one event pair on the launching

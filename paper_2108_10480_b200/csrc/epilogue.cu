@@ -52,8 +52,13 @@ __device__ __forceinline__ void finalize_write(double M, double s, double gx, do
         ay = cy / den;
         az = cz / den;
     }
-    o.d_hat[j] = d;
-    if (o.grad) {
+    if (o.aos) {  // one full sector; split_aos writes d_hat / grad
+        double4* dst = reinterpret_cast<double4*>(o.aos) + j;
+        *dst = make_double4(d, ax, ay, az);
+    } else {
+        o.d_hat[j] = d;
+    }
+    if (o.grad && !o.aos) {
         o.grad[3 * j] = ax;
         o.grad[3 * j + 1] = ay;
         o.grad[3 * j + 2] = az;
@@ -122,10 +127,27 @@ __global__ void finalize_warp_kernel(const double* __restrict__ part, int splits
     if (lane == 0) finalize_write(M, s, gx, gy, gz, i, alpha, eps, const_leaves, leaves_in, far_in, hash_in, perm, o);
 }
 
+// (d_hat, grad) of the queries in original order from the AoS scratch
+__global__ void split_aos(const double4* __restrict__ aos, int64_t Q, double* __restrict__ d_hat,
+                          double* __restrict__ grad) {
+    const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (j >= Q) return;
+    const double4 v = aos[j];
+    d_hat[j] = v.x;
+    grad[3 * j] = v.y;
+    grad[3 * j + 1] = v.z;
+    grad[3 * j + 2] = v.w;
+}
+
 cudaError_t launch_finalize(const double* part, int splits, int64_t Q, double alpha, double epsilon,
                             int64_t const_leaves, const int64_t* leaves_in, const int64_t* far_in,
                             const uint64_t* hash_in, const int64_t* perm, const FinalizeOut& out, cudaStream_t st) {
     if (Q <= 0) return cudaSuccess;
+    if (out.aos && (!out.grad || out.peers || out.pk_world > 1)) {  // the AoS route only for whole batches
+        FinalizeOut o = out;
+        o.aos = nullptr;
+        return launch_finalize(part, splits, Q, alpha, epsilon, const_leaves, leaves_in, far_in, hash_in, perm, o, st);
+    }
     const int threads = 256;
     if (splits >= 32) {
         finalize_warp_kernel<<<unsigned((Q * 32 + threads - 1) / threads), threads, 0, st>>>(
@@ -140,6 +162,12 @@ cudaError_t launch_finalize(const double* part, int splits, int64_t Q, double al
     const unsigned blocks = unsigned((n + threads - 1) / threads);
     finalize_kernel<<<blocks, threads, 0, st>>>(part, splits, Q, alpha, epsilon, const_leaves, leaves_in, far_in,
                                                    hash_in, perm, out);
+    if (out.aos) {
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+        split_aos<<<unsigned((Q + threads - 1) / threads), threads, 0, st>>>(reinterpret_cast<const double4*>(out.aos),
+                                                                             Q, out.d_hat, out.grad);
+    }
     return cudaGetLastError();
 }
 __global__ void finalize_sums_kernel(const double* __restrict__ c, const double* __restrict__ gc, int64_t Q,

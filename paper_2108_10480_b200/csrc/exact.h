@@ -68,6 +68,11 @@ struct FinalizeOut {
     // marking a query with a NaN coordinate (query_morton*): read in sorted
     // order instead of the scattered re-read of the query
     const uint32_t* nan_keys = nullptr;
+    // scratch of 4 doubles per query (sorted tree batches): K4 scatters
+    // (d_hat, grad) as ONE 32-byte sector per query into it, and a
+    // coalesced pass splits it into d_hat / grad (instead of partial-sector
+    // scatters into both arrays)
+    double* aos = nullptr;
     // query-sharded tree evaluation (sd_query_points_device_shard): only
     // this rank's chunks of pk_chunk 32-query packets of the sorted batch
     // (chunk j belongs to rank j % pk_world)
