@@ -72,6 +72,19 @@ constexpr float kNearBox = 9.5367431640625e-07f;  // 2^-20
 constexpr float kLooseMargin = 100.0f;
 
 constexpr int kThreads = 256;
+// Staged primitives per unrolled step of K1's inner loop: fp32 triangles
+// 6 (cfg3, 131,072 queries: 122.5 ms at 2, 120.8 at 4, 119.9 at 6, 120.1
+// at 8 -- more independent pair chains per warp at the same 80 registers),
+// else 2 (cfg2 edges: flat from 2 to 4, +0.2 % at 8). A/B builds:
+// EXTRA=-DSD_K1_UNROLL=k forces k for every kind.
+template <class T, int KIND>
+constexpr int unroll_prims() {
+#ifdef SD_K1_UNROLL
+    return SD_K1_UNROLL;
+#else
+    return sizeof(T) == 4 && KIND == 2 ? 6 : 2;
+#endif
+}
 #ifndef SD_K1_STAGES  // A/B builds (tools/build_ab.sh): EXTRA=-DSD_K1_STAGES=n -DSD_K1_MINB=k
 #define SD_K1_STAGES 3
 #endif
@@ -164,7 +177,7 @@ __global__ void __launch_bounds__(kThreads, MINB) exact_kernel(const __grid_cons
     // pair2.cuh exp_terms (fp64 always runs MODE 0).
     auto compute = [&](const T* tile, int n, auto mode) {
         constexpr int MODE = decltype(mode)::value;
-#pragma unroll 2
+#pragma unroll unroll_prims<T, KIND>()
         for (int i = 0; i < n; ++i) {
             T rec[R];
             using V = typename Vec4<T>::type;
