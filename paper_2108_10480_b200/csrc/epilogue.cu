@@ -152,16 +152,16 @@ cudaError_t launch_finalize(const double* part, int splits, int64_t Q, double al
     if (splits >= 32) {
         finalize_warp_kernel<<<unsigned((Q * 32 + threads - 1) / threads), threads, 0, st>>>(
             part, splits, Q, alpha, epsilon, const_leaves, leaves_in, far_in, hash_in, perm, out);
-        return cudaGetLastError();
+    } else {
+        int64_t n = Q;  // positions covered
+        if (out.pk_world > 1) {
+            n = shard_count((Q + 31) / 32, out.pk_world, out.pk_rank, out.pk_chunk) * 32;
+            if (n == 0) return cudaSuccess;
+        }
+        const unsigned blocks = unsigned((n + threads - 1) / threads);
+        finalize_kernel<<<blocks, threads, 0, st>>>(part, splits, Q, alpha, epsilon, const_leaves, leaves_in, far_in,
+                                                       hash_in, perm, out);
     }
-    int64_t n = Q;  // positions covered
-    if (out.pk_world > 1) {
-        n = shard_count((Q + 31) / 32, out.pk_world, out.pk_rank, out.pk_chunk) * 32;
-        if (n == 0) return cudaSuccess;
-    }
-    const unsigned blocks = unsigned((n + threads - 1) / threads);
-    finalize_kernel<<<blocks, threads, 0, st>>>(part, splits, Q, alpha, epsilon, const_leaves, leaves_in, far_in,
-                                                   hash_in, perm, out);
     if (out.aos) {
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;

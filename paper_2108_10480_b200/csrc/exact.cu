@@ -323,6 +323,9 @@ __global__ void __launch_bounds__(kThreads, MINB) exact_kernel(const __grid_cons
 // 109.5 ms vs 114.7-125.6).
 template <class T, int KIND>
 constexpr int qpt_for() {
+#ifdef SD_K1_QPT_TRI  // A/B: queries per thread of the fp32 triangle kernel
+    if constexpr (sizeof(T) == 4 && KIND == 2) return SD_K1_QPT_TRI;
+#endif
     if constexpr (sizeof(T) == 4) return KIND == 2 ? 2 : 4;
     else return KIND == 2 ? 1 : 2;
 }
