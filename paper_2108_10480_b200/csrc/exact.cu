@@ -75,14 +75,18 @@ constexpr int kThreads = 256;
 // Staged primitives per unrolled step of K1's inner loop: fp32 triangles
 // 6 (cfg3, 131,072 queries: 122.5 ms at 2, 120.8 at 4, 119.9 at 6, 120.1
 // at 8 -- more independent pair chains per warp at the same 80 registers),
-// else 2 (cfg2 edges: flat from 2 to 4, +0.2 % at 8). A/B builds:
-// EXTRA=-DSD_K1_UNROLL=k forces k for every kind.
+// fp64 6 (cfg1 points 0.876 -> 0.827 ms, cfg2 edges 31.45 -> 30.49 ms;
+// 8: 0.822 / 30.60, 12: 0.838 / 32.41), fp32 points and edges 2 (cfg2:
+// flat from 2 to 4, +0.2 % at 8). A/B builds: EXTRA=-DSD_K1_UNROLL=k forces
+// k for every kind, -DSD_K1_UNROLL64=k for fp64.
 template <class T, int KIND>
 constexpr int unroll_prims() {
 #ifdef SD_K1_UNROLL
     return SD_K1_UNROLL;
+#elif defined(SD_K1_UNROLL64)
+    return sizeof(T) == 4 && KIND == 2 ? 6 : (sizeof(T) == 8 ? SD_K1_UNROLL64 : 2);
 #else
-    return sizeof(T) == 4 && KIND == 2 ? 6 : 2;
+    return (sizeof(T) == 4 && KIND == 2) || sizeof(T) == 8 ? 6 : 2;
 #endif
 }
 #ifndef SD_K1_STAGES  // A/B builds (tools/build_ab.sh): EXTRA=-DSD_K1_STAGES=n -DSD_K1_MINB=k

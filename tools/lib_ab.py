@@ -1,6 +1,6 @@
 """A/B timing of libsdgpu.so builds (tools/build_ab.sh) on the bench's BVH
 leg (cfg4, 4,194,304 queries, L2 flushed, CUDA events, median of REPS;
-AB_SHARD=W: rank 0's share of a W-way sharded call; AB_CFG=3 / 2: exact cfg3 / cfg2):
+AB_SHARD=W: rank 0's share of a W-way sharded call; AB_CFG=3 / 2 / 1: exact cfg3 / cfg2 / cfg1 (fp64); AB_PREC=64: fp64):
   python tools/lib_ab.py ablibs/base ablibs/x[:ENV=VAL,...] ...   (rounds alternate)
 Each variant runs in its own process (one library per process)."""
 import json
@@ -26,18 +26,24 @@ elif cfg == "2":
     import bench
     w, wt, q = bench.cfg2_workload(); mode = sd.SD_EXACT
     P = sd.SmoothParams(alpha=100.0, alpha_u=600.0, beta=0.0)
+elif cfg == "1":
+    w, q = configs.cfg1(); mode = sd.SD_EXACT
+    P = sd.SmoothParams(alpha=w.alpha, alpha_u=600.0, beta=0.0)
 else:
     import bench
     v, T, K, q = bench.cfg3_workload(); mode = sd.SD_EXACT
     q = q[: int(os.environ.get("AB_NQ", "131072"))]
     P = sd.SmoothParams(alpha=100.0, alpha_u=600.0, beta=0.0)
     w = type("W", (), {"vertices": v, "simplices": T, "kinds": K})
-v, q = configs.quantize(w.vertices), configs.quantize(q)
-eng = sd.Engine(0, sd.SD_FP32); eng.set_geometry(v, w.simplices, w.kinds)
-if cfg == "2": eng.set_weights(wt.A, wt.sup_wtilde, wt.edge_a, wt.tri_stored, wt.poly_index)
+prec = sd.SD_FP64 if os.environ.get("AB_PREC") == "64" or cfg == "1" else sd.SD_FP32
+v = w.vertices if prec == sd.SD_FP64 else configs.quantize(w.vertices)
+q = q if prec == sd.SD_FP64 else configs.quantize(q)
+eng = sd.Engine(0, prec); eng.set_geometry(v, w.simplices, w.kinds)
+if cfg == "1": wt = configs.weights_without_triangles(w.simplices, w.kinds, len(w.vertices))
+if cfg in ("1", "2"): eng.set_weights(wt.A, wt.sup_wtilde, wt.edge_a, wt.tri_stored, wt.poly_index)
 else: eng.build_weights()
 if mode == sd.SD_BVH: eng.build_bvh(sd.SD_BVH_AUTO)
-QD = torch.tensor(q, dtype=torch.float32, device=dev)
+QD = torch.tensor(q, dtype=torch.float64 if prec == sd.SD_FP64 else torch.float32, device=dev)
 D = torch.empty(len(q), dtype=torch.float64, device=dev); G = torch.empty(len(q), 3, dtype=torch.float64, device=dev)
 W = int(os.environ.get("AB_SHARD", "1"))  # > 1: rank 0's share of a W-way query-sharded call
 if W > 1:
