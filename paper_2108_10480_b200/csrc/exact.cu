@@ -76,17 +76,21 @@ constexpr int kThreads = 256;
 // 6 (cfg3, 131,072 queries: 122.5 ms at 2, 120.8 at 4, 119.9 at 6, 120.1
 // at 8 -- more independent pair chains per warp at the same 80 registers),
 // fp64 6 (cfg1 points 0.876 -> 0.827 ms, cfg2 edges 31.45 -> 30.49 ms;
-// 8: 0.822 / 30.60, 12: 0.838 / 32.41), fp32 points and edges 2 (cfg2:
-// flat from 2 to 4, +0.2 % at 8). A/B builds: EXTRA=-DSD_K1_UNROLL=k forces
-// k for every kind, -DSD_K1_UNROLL64=k for fp64.
+// 8: 0.822 / 30.60, 12: 0.838 / 32.41), fp32 edges 8 with 2 queries per
+// thread (cfg2: 6.96 ms at 4 queries x 2 primitives; 2 queries x 2 / 3 /
+// 4 / 5 / 8 primitives: 6.82 / 6.92 / 6.80 / 6.89 / 6.79 ms), fp32 points
+// 2. A/B builds: EXTRA=-DSD_K1_UNROLL=k forces k for every kind,
+// -DSD_K1_UNROLL64=k for fp64, -DSD_K1_UNROLL_EDGE / -DSD_K1_QPT_EDGE.
 template <class T, int KIND>
 constexpr int unroll_prims() {
 #ifdef SD_K1_UNROLL
     return SD_K1_UNROLL;
+#elif defined(SD_K1_UNROLL_EDGE)
+    return sizeof(T) == 4 && KIND == 1 ? SD_K1_UNROLL_EDGE : ((sizeof(T) == 4 && KIND == 2) || sizeof(T) == 8 ? 6 : 2);
 #elif defined(SD_K1_UNROLL64)
     return sizeof(T) == 4 && KIND == 2 ? 6 : (sizeof(T) == 8 ? SD_K1_UNROLL64 : 2);
 #else
-    return (sizeof(T) == 4 && KIND == 2) || sizeof(T) == 8 ? 6 : 2;
+    return sizeof(T) == 4 && KIND == 1 ? 8 : ((sizeof(T) == 4 && KIND == 2) || sizeof(T) == 8 ? 6 : 2);
 #endif
 }
 #ifndef SD_K1_STAGES  // A/B builds (tools/build_ab.sh): EXTRA=-DSD_K1_STAGES=n -DSD_K1_MINB=k
@@ -330,7 +334,10 @@ constexpr int qpt_for() {
 #ifdef SD_K1_QPT_TRI  // A/B: queries per thread of the fp32 triangle kernel
     if constexpr (sizeof(T) == 4 && KIND == 2) return SD_K1_QPT_TRI;
 #endif
-    if constexpr (sizeof(T) == 4) return KIND == 2 ? 2 : 4;
+#ifdef SD_K1_QPT_EDGE  // A/B: queries per thread of the fp32 edge kernel
+    if constexpr (sizeof(T) == 4 && KIND == 1) return SD_K1_QPT_EDGE;
+#endif
+    if constexpr (sizeof(T) == 4) return KIND == 0 ? 4 : 2;  // (edges: 2 since round 2, see unroll_prims)
     else return KIND == 2 ? 1 : 2;
 }
 template <class T, int KIND>
