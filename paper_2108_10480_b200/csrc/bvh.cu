@@ -242,9 +242,9 @@ __device__ __forceinline__ uint32_t spread10(uint32_t v) {
     return v;
 }
 
-template <class T>
+template <class T, class I>
 __global__ void query_morton(const T* __restrict__ q, int64_t Q, double3 lo, double3 inv, uint32_t* keys,
-                             int64_t* idx) {
+                             I* idx) {
     const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= Q) return;
     auto cell = [](double x, double l, double s) {
@@ -256,7 +256,7 @@ __global__ void query_morton(const T* __restrict__ q, int64_t Q, double3 lo, dou
     const uint32_t z = cell(double(q[3 * i + 2]), lo.z, inv.z);
     const T a = q[3 * i], b = q[3 * i + 1], d = q[3 * i + 2];
     keys[i] = (a == a && b == b && d == d) ? (spread10(x) << 2) | (spread10(y) << 1) | spread10(z) : 0xffffffffu;
-    idx[i] = i;
+    idx[i] = I(i);
 }
 
 // ------------------------------------------------------------ traversal
@@ -688,9 +688,9 @@ __global__ void __launch_bounds__(256) qbox_reduce(const T* __restrict__ q, int6
 // the queries' own box, read from device memory (no host round trip):
 // queries outside the scene keep distinct cells instead of piling up on its
 // faces. Cells in fp32 (the order only shapes the packets, not the results).
-template <class T>
+template <class T, class I>
 __global__ void query_morton_union(const T* __restrict__ q, int64_t Q, float3 lo, float3 hi,
-                                   const uint32_t* __restrict__ ob, int hilbert, uint32_t* keys, int64_t* idx) {
+                                   const uint32_t* __restrict__ ob, int hilbert, uint32_t* keys, I* idx) {
     const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= Q) return;
     const float l[3] = {fminf(lo.x, unord_f32(ob[0])), fminf(lo.y, unord_f32(ob[1])), fminf(lo.z, unord_f32(ob[2]))};
@@ -727,17 +727,32 @@ __global__ void query_morton_union(const T* __restrict__ q, int64_t Q, float3 lo
     }
     const T x = q[3 * i], y = q[3 * i + 1], z = q[3 * i + 2];
     keys[i] = (x == x && y == y && z == z) ? key : 0xffffffffu;  // NaN: last, and flagged for K4
-    idx[i] = i;
+    idx[i] = I(i);
 }
 
 // Morton codes (10 bits per axis over [lo, hi] joined with the queries'
 // box) + CUB radix sort: the returned permutation lists query indices in
 // spatial order (device memory owned by the context).
+// sorted 32-bit query indices -> the int64 perm (grid-stride, coalesced)
+__global__ void widen_perm(const uint32_t* __restrict__ in, int64_t n, int64_t* __restrict__ out) {
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+        out[i] = in[i];
+}
+
 template <class T>
 const int64_t* sort_queries(Ctx& c, const T* q, int64_t Q, const double lo[3], const double hi[3], cudaStream_t st,
                             int64_t& launches, bool union_hilbert) {
     uint32_t* keys = static_cast<uint32_t*>(c.keys.ensure(size_t(Q) * 2 * sizeof(uint32_t)));
     int64_t* idx = static_cast<int64_t*>(c.perm.ensure(size_t(Q) * 2 * sizeof(int64_t)));
+    // batches below 2^31 queries sort 32-bit indices (8 instead of 12 bytes
+    // per element and radix pass; the same stable order) in the first half
+    // of the perm buffer and widen them into the int64 perm (second half)
+    static const bool idx64 = [] {  // SDGPU_SORT_IDX64=1: sort the int64 indices (A/B)
+        const char* e = std::getenv("SDGPU_SORT_IDX64");
+        return e && *e == '1';
+    }();
+    const bool narrow = !idx64 && Q < (int64_t(1) << 31);
+    uint32_t* idx32 = reinterpret_cast<uint32_t*>(idx);  // [0, Q) in, [Q, 2Q) sorted
     const unsigned blocks = unsigned((Q + 255) / 256);
     static const bool union_box = [] {
         const char* e = std::getenv("SDGPU_QBOX");
@@ -757,15 +772,17 @@ const int64_t* sort_queries(Ctx& c, const T* q, int64_t Q, const double lo[3], c
         // (the root box rounded outward to fp32)
         auto dn = [](double x) { return std::nextafter(float(x), -INFINITY); };
         auto up = [](double x) { return std::nextafter(float(x), INFINITY); };
-        query_morton_union<T><<<blocks, 256, 0, st>>>(q, Q, make_float3(dn(lo[0]), dn(lo[1]), dn(lo[2])),
-                                                      make_float3(up(hi[0]), up(hi[1]), up(hi[2])), ob, hilbert, keys,
-                                                      idx);
+        const float3 flo = make_float3(dn(lo[0]), dn(lo[1]), dn(lo[2]));
+        const float3 fhi = make_float3(up(hi[0]), up(hi[1]), up(hi[2]));
+        if (narrow) query_morton_union<T, uint32_t><<<blocks, 256, 0, st>>>(q, Q, flo, fhi, ob, hilbert, keys, idx32);
+        else query_morton_union<T, int64_t><<<blocks, 256, 0, st>>>(q, Q, flo, fhi, ob, hilbert, keys, idx);
         launches += 3;
     } else {
         auto inv = [](double l, double h) { return h > l ? 1024.0 / (h - l) : 0.0; };
         const double3 dlo = make_double3(lo[0], lo[1], lo[2]);
         const double3 iv = make_double3(inv(lo[0], hi[0]), inv(lo[1], hi[1]), inv(lo[2], hi[2]));
-        query_morton<T><<<blocks, 256, 0, st>>>(q, Q, dlo, iv, keys, idx);
+        if (narrow) query_morton<T, uint32_t><<<blocks, 256, 0, st>>>(q, Q, dlo, iv, keys, idx32);
+        else query_morton<T, int64_t><<<blocks, 256, 0, st>>>(q, Q, dlo, iv, keys, idx);
         ++launches;
     }
     check_cuda(cudaGetLastError(), "query morton");
@@ -777,10 +794,22 @@ const int64_t* sort_queries(Ctx& c, const T* q, int64_t Q, const double lo[3], c
         return 30 - std::min(30, std::max(6, b));
     }();
     size_t tmp_bytes = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys, keys + Q, idx, idx + Q, int(Q), lo_bit, 30, st);
-    void* tmp = c.tmp.ensure(tmp_bytes);
-    check_cuda(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, keys + Q, idx, idx + Q, int(Q), lo_bit, 30, st),
-               "radix sort queries");
+    if (narrow) {
+        cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys, keys + Q, idx32, idx32 + Q, int(Q), lo_bit, 30, st);
+        void* tmp = c.tmp.ensure(tmp_bytes);
+        check_cuda(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, keys + Q, idx32, idx32 + Q, int(Q), lo_bit,
+                                                   30, st),
+                   "radix sort queries");
+        widen_perm<<<unsigned(std::min<int64_t>(148 * 16, (Q + 255) / 256)), 256, 0, st>>>(idx32 + Q, Q, idx + Q);
+        check_cuda(cudaGetLastError(), "widen perm");
+        ++launches;
+    } else {
+        cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys, keys + Q, idx, idx + Q, int(Q), lo_bit, 30, st);
+        void* tmp = c.tmp.ensure(tmp_bytes);
+        check_cuda(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, keys + Q, idx, idx + Q, int(Q), lo_bit, 30,
+                                                   st),
+                   "radix sort queries");
+    }
     launches += 4;  // onesweep histogram + passes (approximate count of CUB kernels)
     return idx + Q;
 }
