@@ -515,6 +515,37 @@ def exact_leg(run, eng, q, prec, N, kind, P, steps, warmup, flush, stream, peaks
     return out, d_hat.cpu().numpy(), grad.cpu().numpy()
 
 
+PRUNE_BITS = 48.0
+
+
+def pruned_leg(run, eng, q, prec, N, kind, P, steps, flush, stream, peaks, q_total, full, base_ms):
+    """The same exact configuration with sd_set_exact_pruning(48): an extra
+    key, never the headline. Tiles whose terms are below 2^-48 of a lower
+    bound of the query's sum are skipped, so `value` is the all-pairs
+    EQUIVALENT rate (Q x N / time, skipped pairs counted); every timed
+    answer of this rank is compared with the all-pairs kernel's."""
+    eng.set_exact_pruning(PRUNE_BITS)
+    try:
+        r, d, g = exact_leg(run, eng, q, prec, N, kind, P, steps, 3, flush, stream, peaks, q_total=q_total)
+    finally:
+        eng.set_exact_pruning(0.0)
+    if "roofline" in r:
+        r["roofline_all_pairs"] = r.pop("roofline")
+        r["roofline_all_pairs"]["note"] = "counts skipped pairs too; not a pipe utilisation"
+    r["unit"] = "pair-evals/s (all-pairs equivalent)"
+    r["pruning_bits"] = PRUNE_BITS
+    r["speedup_over_all_pairs"] = base_ms / r["ms_per_step"]
+    d0, g0 = full
+    fin = np.isfinite(d0)
+    r["vs_all_pairs_kernel"] = {
+        "n": int(len(d0)), "inf_mismatch": int((np.isfinite(d) != fin).sum()),
+        "d_hat_max_abs": float(np.abs(d[fin] - d0[fin]).max()) if fin.any() else 0.0,
+        "grad_max_abs": float(np.abs(g[fin] - g0[fin]).max()) if fin.any() else 0.0,
+        "bound": f"relative error of c < N 2^-{PRUNE_BITS:g} = {N * 2.0 ** -PRUNE_BITS:.1e} (include/sdgpu.h); the rest "
+                 "is fp32 regrouping of the tile sums"}
+    return r, d, g
+
+
 def cpu_exact_sample(arm, q, alpha, target_s):
     """The CPU arm on a bounded prefix of the queries, sized by a pilot so
     the sample takes about target_s seconds."""
@@ -557,6 +588,10 @@ def run_exact_headline(args, run, peaks, stream, flush, line):
                                                "masked (alpha d > 708) are skipped exactly, so frac > 1 is expected")
         extra[f"exact_cfg3_alpha{alpha:g}"] = r
         outs[alpha] = (d, g)
+    rp, dp, gp = pruned_leg(run, eng, qb, sd.SD_FP32, N3, 2, P, max(1, min(args.steps, 5)), flush, stream, peaks,
+                            len(q3), (d100, g100), head["ms_per_step"])
+    extra["exact_cfg3_pruned"] = rp
+    outs["pruned"] = (dp, gp)
     eng.close()
     threads = None
     if rank == 0 and not args.no_cpu:
@@ -571,6 +606,10 @@ def run_exact_headline(args, run, peaks, stream, flush, line):
             d, g = outs[alpha]
             par[f"cfg3_alpha{alpha:g}"] = parity_stats(d[idx], g[idx], ref.d_hat, ref.grad, alpha, "f32")
             par[f"cfg3_alpha{alpha:g}"]["sample"] = f"{nq} evenly spaced timed queries of rank 0's block"
+            if alpha == 100.0:
+                d, g = outs["pruned"]
+                par["cfg3_alpha100_pruned"] = parity_stats(d[idx], g[idx], ref.d_hat, ref.grad, alpha, "f32")
+                par["cfg3_alpha100_pruned"]["sample"] = f"the same {nq} queries, sd_set_exact_pruning({PRUNE_BITS:g})"
         if world == 1:
             arm = CpuArm(v3, t3, k3, wt3)
             n, r = cpu_exact_sample(arm, qb, 100.0, 10.0)
@@ -609,6 +648,11 @@ def run_exact_headline(args, run, peaks, stream, flush, line):
                          "(BASELINE configs[1])")
         line[key] = r
         res2[prec] = (d, g)
+        if prec == sd.SD_FP32:
+            rp, dp, gp = pruned_leg(run, e, qb2, prec, N2, 1, P2, args.steps, flush, stream, peaks, len(q2), (d, g),
+                                    r["ms_per_step"])
+            line["exact_cfg2_pruned"] = rp
+            res2["pruned"] = (dp, gp)
         e.close()
     # ---- cfg1 point cloud (BASELINE configs[0]), fp64 as specified
     from paper_2108_10480_b200 import configs as cf
@@ -642,7 +686,8 @@ def run_exact_headline(args, run, peaks, stream, flush, line):
         n, r = cpu_exact_sample(arm, qb2, 100.0, 7.0)
         cpu2 = {"value": n * N2 / r.seconds, "unit": "pair-evals/s", "cores": arm.threads, "kind": arm.kind,
                 "sample": f"first {n} of {len(qb2)} cfg2 queries x {N2} edges ({r.seconds:.1f} s, fp64, {arm.kind})"}
-        for prec, key, dt in ((sd.SD_FP32, "exact_cfg2", "f32"), (sd.SD_FP64, "exact_cfg2_fp64", "f64")):
+        for prec, key, dt in ((sd.SD_FP32, "exact_cfg2", "f32"), (sd.SD_FP64, "exact_cfg2_fp64", "f64"),
+                              ("pruned", "exact_cfg2_pruned", "f32")):
             d, g = res2[prec]
             par[key] = parity_stats(d[:n], g[:n], r.d_hat, r.grad, 100.0, dt)
             par[key]["sample"] = f"first {n} timed queries of rank 0's block"

@@ -287,6 +287,20 @@ int sd_load_bvh_cache(sd_ctx* ctx, const char* path);
 int sd_save_weight_cache(sd_ctx* ctx, const char* path);
 int sd_load_weight_cache(sd_ctx* ctx, const char* path);
 
+/* Pruned exact evaluation (not in the reference; off by default). With
+ * bits > 0 the SD_EXACT path (smooth_min_dist_flat, smooth.hpp:189-198)
+ * still visits every primitive tile but skips a tile for a warp of queries
+ * when every term of it is provably below 2^-bits of a lower bound of each
+ * query's sum c (the sum's terms are positive, so its largest term bounds it
+ * from below; both bounds come from the tile's box). Each dropped term is
+ * < 2^-bits c, so the relative error of c is < N 2^-bits over N primitives
+ * (bits = 48, N = 2^18: 2^-30, |delta d_hat| < 1e-9 / alpha) -- below the
+ * fp32 path's own rounding, within the fp64 path's 1e-10 only for bits >=
+ * 56. bits = 0 restores the reference's sum over all pairs; 0 < bits < 24
+ * is rejected (SD_E_ARG). Applies to the exact kernels of both precisions;
+ * the tree path and simplex queries are unaffected. */
+int sd_set_exact_pruning(sd_ctx* ctx, double bits);
+
 /* Kernel timing (measurement support, not in the reference): with timing
  * on, every query call records a CUDA event pair on its launching stream
  * around its dominant compute launches (the exact segment launches, or the

@@ -37,7 +37,7 @@ assert NODE_DTYPE.itemsize == 72
 EXPORTED_SYMBOLS = (
     "sd_last_error", "sd_abi_version", "sd_create", "sd_destroy", "sd_set_geometry", "sd_set_weights",
     "sd_set_bvh", "sd_build_bvh", "sd_bvh_size", "sd_export_bvh", "sd_query_points", "sd_query_points_device",
-    "sd_finalize_device", "sd_query_points_async", "sd_query_wait", "sd_query_points_device_shard", "sd_last_launch_count", "sd_set_kernel_timing", "sd_kernel_times", "sd_build_weights", "sd_weights_info", "sd_export_weights",
+    "sd_finalize_device", "sd_query_points_async", "sd_query_wait", "sd_query_points_device_shard", "sd_last_launch_count", "sd_set_kernel_timing", "sd_set_exact_pruning", "sd_kernel_times", "sd_build_weights", "sd_weights_info", "sd_export_weights",
     "sd_mesh_dist_points",
     "sd_query_simplices",
     "sd_mesh_dist",
@@ -119,6 +119,7 @@ def lib():
             "sd_finalize_device": (C.c_int, [vp, vp, vp, i64, P(_Params), vp, vp, vp]),
             "sd_last_launch_count": (C.c_int, [vp, P(i64)]),
             "sd_set_kernel_timing": (C.c_int, [vp, C.c_int]),
+            "sd_set_exact_pruning": (C.c_int, [vp, C.c_double]),
             "sd_kernel_times": (C.c_int, [vp, vp, i64, P(i64)]),
             "sd_build_weights": (C.c_int, [vp]),
             "sd_weights_info": (C.c_int, [vp, P(f64), P(f64), P(i32), P(i32)]),
@@ -372,6 +373,12 @@ class Engine:
         _check(lib().sd_reduce_owned(self.h, C.c_void_p(sbuf_ptr), q_per_owner, n_owned, world, C.byref(params._c()),
                                      C.c_void_p(d_hat_ptr), C.c_void_p(grad_ptr) if grad_ptr else None,
                                      C.c_void_p(stream) if stream else None))
+
+    def set_exact_pruning(self, bits: float = 48.0):
+        """Pruned exact evaluation (sd_set_exact_pruning): tiles whose terms are
+        below 2^-bits of a lower bound of the query's sum are skipped; 0
+        restores the sum over all pairs (smooth.hpp:189-198)."""
+        _check(lib().sd_set_exact_pruning(self.h, float(bits)))
 
     def set_kernel_timing(self, on: bool = True):
         """Record a CUDA event pair around the dominant compute launches of

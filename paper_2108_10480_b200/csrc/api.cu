@@ -436,6 +436,7 @@ static void exact_query(Ctx& c, const T* q, int64_t Q, const sd_params& p, const
             L.lwmax = T(hi);
             L.lwspan = T(hi - lo);
         }
+        L.prune = float(c.exact_prune_bits);
         L.q = q;
         L.Q = Q;
         L.part = part;
@@ -1488,6 +1489,15 @@ int sd_query_wait(sd_ctx* c, int64_t ticket) {
         for (auto& sl : c->slots)
             if (sl.ticket >= 0 && (ticket < 0 || sl.ticket == ticket))
                 check_cuda(cudaEventSynchronize(sl.out), "wait batch");
+    });
+}
+
+int sd_set_exact_pruning(sd_ctx* c, double bits) {
+    return guard([&] {
+        if (!c) throw ArgError{"ctx is NULL"};
+        if (!(bits >= 0) || !std::isfinite(bits)) throw ArgError{"pruning threshold must be >= 0 bits and finite"};
+        if (bits > 0 && bits < 24) throw ArgError{"pruning threshold below 24 bits would show in the fp32 results"};
+        c->exact_prune_bits = bits;
     });
 }
 

@@ -164,6 +164,10 @@ struct Ctx {
     DevBuf perm, keys, tmp, tmp2, counters, polys, flag, qbox, aos;
     int64_t last_launches = 0;
 
+    // sd_set_exact_pruning: 0 = every pair evaluated (the reference's sum),
+    // > 0 = K1 skips tiles whose terms are below 2^-bits of the query's sum
+    double exact_prune_bits = 0.0;
+
     // kernel timing (sd_set_kernel_timing): one event pair on the launching
     // stream around the dominant compute launches of every query call (the
     // exact segment launches, or the tree traversal), read back and recycled

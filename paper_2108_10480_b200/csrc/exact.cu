@@ -37,6 +37,7 @@ struct ExactArgs {
     const float4* tbox;   // tile boxes of the segment (null: no tile bounds)
     T lwmax, lwspan;      // log2 w upper bound and spread over the segment
     int cluster;          // splits merged over DSMEM into split 0's partial
+    float prune;          // PRUNE kernels: negligibility threshold in bits
 };
 
 // Tot b folded into a (same anchor semantics as Tot::flush).
@@ -105,7 +106,17 @@ constexpr int tile_prims() {
     return KIND == 0 ? 512 : 128;
 }
 
-template <class T, int KIND, bool POLY, bool SAFE, int QPT, int MINB>
+// PRUNE (sd_set_exact_pruning, off by default): the positive terms of the
+// sum let any single term bound it from below, so before the tile loop each
+// query takes, over the tile boxes of the whole segment, the largest
+// kappa d_hi + min log2 w -- a lower bound of log2 of its largest term and
+// hence of log2 c. A tile whose upper bound kappa d_lo + max log2 w lies
+// more than `prune` bits below that bound for every query of the warp is
+// skipped: each dropped term is < 2^-prune c, N of them < N 2^-prune c
+// (2^-30 relative at 48 bits and 2^18 primitives, far inside the fp32
+// path's own rounding). Not the reference's sum term for term, so it is a
+// separate kernel instance behind its own switch.
+template <class T, int KIND, bool POLY, bool SAFE, int QPT, int MINB, bool PRUNE = false>
 __global__ void __launch_bounds__(kThreads, MINB) exact_kernel(const __grid_constant__ ExactArgs<T> a) {
     constexpr int R = rec_size(KIND);
     constexpr int TILE = tile_prims<T, KIND>();
@@ -214,6 +225,28 @@ __global__ void __launch_bounds__(kThreads, MINB) exact_kernel(const __grid_cons
         }
     };
 
+    [[maybe_unused]] float seed[QPT];
+    if constexpr (PRUNE) {
+        const int64_t ntall = (a.count + TILE - 1) / TILE;
+        float dmin2[QPT];
+#pragma unroll
+        for (int k = 0; k < QPT; ++k) dmin2[k] = INFINITY;
+        for (int64_t g = 0; g < ntall; ++g) {  // warp-uniform addresses: broadcast loads
+            const float4 lo4 = __ldg(a.tbox + 2 * g), hi4 = __ldg(a.tbox + 2 * g + 1);
+#pragma unroll
+            for (int k = 0; k < QPT; ++k) {
+                const float x = float(qx[k]), y = float(qy[k]), z = float(qz[k]);
+                const float fx = fmaxf(fabsf(x - lo4.x), fabsf(x - hi4.x)),
+                            fy = fmaxf(fabsf(y - lo4.y), fabsf(y - hi4.y)),
+                            fz = fmaxf(fabsf(z - lo4.z), fabsf(z - hi4.z));
+                dmin2[k] = fminf(dmin2[k], fmaf(fx, fx, fmaf(fy, fy, fz * fz)));
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < QPT; ++k)  // (NaN queries: NaN seed, no tile is pruned)
+            seed[k] = fmaf(float(a.ph.kappa), sqrtf(dmin2[k]) * (1.f + 1e-5f), float(a.lwmax) - float(a.lwspan)) - a.prune;
+    }
+
     for (int t = 0; t < ntiles; ++t) {
         const int s = t % kStages;
         mbar_wait(&full[s], (t / kStages) & 1);
@@ -242,7 +275,8 @@ __global__ void __launch_bounds__(kThreads, MINB) exact_kernel(const __grid_cons
                 const float dlo = sqrtf(fmaf(ex, ex, fmaf(ey, ey, ez * ez))) * (1.f - 1e-5f);
                 const float dhi = sqrtf(fmaf(fx, fx, fmaf(fy, fy, fz * fz))) * (1.f + 1e-5f);
                 const bool sk = qi[k] >= a.Q || dlo > float(a.ph.dmax);
-                all_skip = all_skip && sk;
+                if constexpr (PRUNE) all_skip = all_skip && (sk || fmaf(float(a.ph.kappa), dlo, float(a.lwmax)) < seed[k]);
+                else all_skip = all_skip && sk;
                 all_inside = all_inside && (qi[k] >= a.Q || dhi < float(a.ph.dmax));
                 const float H = dlo < kNearBox ? kTileHeadroomNear : kTileHeadroom;
                 const bool loose = !sk && span > H + kLooseMargin;
@@ -288,6 +322,23 @@ __global__ void __launch_bounds__(kThreads, MINB) exact_kernel(const __grid_cons
             if constexpr (!POLY) acc[k].m += a.ph.lw_unit;  // totals are absolute
             tot[k * kThreads + threadIdx.x].flush(acc[k]);
             if constexpr (!POLY) acc[k].m -= a.ph.lw_unit;
+        }
+        if constexpr (PRUNE) {
+            // the running total is a lower bound of c as well (floor of its
+            // log2 from the fp64 exponent field): usually tighter than the
+            // box seed once a near tile has been summed
+            if (!skip) {
+#pragma unroll
+                for (int k = 0; k < QPT; ++k) {
+                    const Tot& tk = tot[k * kThreads + threadIdx.x];
+                    if (tk.s > 0.0) {
+                        const int ex = ((__double2hiint(tk.s) >> 20) & 0x7ff) - 1023;
+                        float lc = float(tk.M) + float(ex) - 1.f;  // (-1: float(M) may round up)
+                        if constexpr (!POLY) lc -= float(a.ph.lw_unit);
+                        seed[k] = fmaxf(seed[k], lc - a.prune);
+                    }
+                }
+            }
         }
         if constexpr (PACKED) {
 #pragma unroll
@@ -356,8 +407,9 @@ static size_t smem_bytes() {
 }
 
 template <class T, int KIND, bool POLY, bool SAFE, class F>
-static auto with_kernel(F&& f) {
+static auto with_kernel(F&& f, bool prune = false) {
     constexpr int QPT = qpt_for<T, KIND>();
+    if (prune) return f(exact_kernel<T, KIND, POLY, SAFE, QPT, minb_for<T, KIND>(), true>, smem_bytes<T, KIND, QPT>(), QPT);
     return f(exact_kernel<T, KIND, POLY, SAFE, QPT, minb_for<T, KIND>()>, smem_bytes<T, KIND, QPT>(), QPT);
 }
 
@@ -381,6 +433,7 @@ static cudaError_t launch_one(const ExactLaunch<T>& L, cudaStream_t st) {
         a.lwmax = L.lwmax;
         a.lwspan = L.lwspan;
         a.cluster = L.cluster ? 1 : 0;
+        a.prune = L.prune;
         const int64_t qblocks = (L.Q + int64_t(kThreads) * QPT - 1) / (int64_t(kThreads) * QPT);
         dim3 grid(unsigned(qblocks), unsigned(L.splits));
         if (!L.cluster) {
@@ -404,7 +457,7 @@ static cudaError_t launch_one(const ExactLaunch<T>& L, cudaStream_t st) {
         cfg.attrs = attr;
         cfg.numAttrs = 1;
         return cudaLaunchKernelEx(&cfg, kern, a);
-    });
+    }, L.prune > 0.f && L.tbox != nullptr);
 }
 
 template <class T, int KIND, bool POLY, bool SAFE>

@@ -32,6 +32,9 @@ struct ExactLaunch {
     const float4* tbox = nullptr;   // tile boxes of this segment (2 float4 per tile), or null
     T lwmax = T(0);                 // upper bound of log2 w over the segment (unit: 0, shift-relative)
     T lwspan = T(0);                // lwmax - lower bound of log2 w
+    // > 0: pruned evaluation (sd_set_exact_pruning): a warp skips a tile when
+    // every term of it is below 2^-prune of a lower bound of the query's sum
+    float prune = 0.f;
 };
 
 template <class T>

@@ -1106,3 +1106,74 @@ def test_query_sharded_tree_walk_equals_the_whole_batch(sd, oracle, prec, chunk,
     assert np.array_equal(d.cpu().numpy(), whole.d_hat) and np.array_equal(g.cpu().numpy(), whole.grad)
     ref = O.query(m, w, q, O.Params(alpha=150.0, beta=0.5), tree=t)
     assert (hs.cpu().numpy().view(np.uint64) == ref.decision_hash).all()
+
+
+# ------------------------------------------------- pruned exact evaluation
+def _prune_bound(n_prims, bits):
+    """Relative bound on c of sd_set_exact_pruning (include/sdgpu.h)."""
+    return n_prims * 2.0 ** -bits
+
+
+@pytest.mark.parametrize("prec,bits", [(0, 48.0), (0, 32.0), (1, 64.0)])
+@pytest.mark.parametrize("seed", [1, 4, 7, 10])
+def test_pruned_exact_on_random_scenes(sd, oracle, prec, bits, seed):
+    """sd_set_exact_pruning on mixed point / edge / triangle scenes: oracle
+    parity at the unpruned tolerances, and the documented bound against
+    the engine's own all-pairs sum (c, grad_c compared directly)."""
+    O = oracle
+    m0 = O.random_scene(seed, 400)
+    qs = O.QueryStream(2000 + seed).draw_points(m0, 700)
+    m, q = prep(O, m0, qs, prec)
+    w = O.Weights.build(m)
+    e = engine_for(sd, O, m, w, prec)
+    for alpha in (100.0, 900.0, 20.0):
+        P = sd.SmoothParams(alpha=alpha, alpha_u=600.0, beta=0.0)
+        e.set_exact_pruning(0.0)
+        full = e.query_points(q, P, sd.SD_EXACT, want_c=True)
+        e.set_exact_pruning(bits)
+        got = e.query_points(q, P, sd.SD_EXACT, want_c=True)
+        ref = O.query(m, w, q, O.Params(alpha=alpha, alpha_u=600.0, beta=0.0))
+        assert_close(got, ref, prec, alpha, f"pruned seed {seed} alpha {alpha}")
+        assert (np.isfinite(got.d_hat) == np.isfinite(full.d_hat)).all()
+        pos = full.c > 0
+        rel = np.abs(got.c[pos] - full.c[pos]) / full.c[pos]
+        # the fp32 tile sums regroup when tiles drop out: allow their rounding
+        slack = 5e-6 if prec == 0 else 1e-13
+        assert rel.max() <= _prune_bound(m.num_simplices, bits) + slack, rel.max()
+        assert (got.c[pos] <= full.c[pos] * (1 + slack)).all()  # pruning only removes positive terms
+    e.set_exact_pruning(0.0)
+    again = e.query_points(q, P, sd.SD_EXACT, want_c=True)
+    assert np.array_equal(again.d_hat, full.d_hat) and np.array_equal(again.grad, full.grad)
+
+
+def test_pruned_exact_config3_subset(sd, oracle):
+    """cfg3 (262,144 triangles), 4,096 queries, alpha in {10, 100, 1000}:
+    pruned at 48 bits against the oracle and against the all-pairs kernel."""
+    O = oracle
+    m, q = _cfg(O, 3, 4096, 0)
+    w = O.Weights.build(m)
+    e = engine_for(sd, O, m, w, 0)
+    idx = np.arange(0, len(q), 16)
+    for alpha in (10.0, 100.0, 1000.0):
+        P = sd.SmoothParams(alpha=alpha, beta=0.0)
+        e.set_exact_pruning(0.0)
+        full = e.query_points(q, P, sd.SD_EXACT)
+        e.set_exact_pruning(48.0)
+        got = e.query_points(q, P, sd.SD_EXACT)
+        fin = np.isfinite(full.d_hat)
+        assert (np.isfinite(got.d_hat) == fin).all()
+        assert np.abs(got.d_hat[fin] - full.d_hat[fin]).max() <= 2e-6 / alpha + 1e-7
+        assert np.abs(got.grad[fin] - full.grad[fin]).max() <= 1e-5
+        ref = O.query(m, w, q[idx], O.Params(alpha=alpha, beta=0.0))
+        assert_close(type(got)(got.d_hat[idx], got.grad[idx]), ref, 0, alpha, f"pruned cfg3 alpha {alpha}")
+
+
+def test_pruning_threshold_is_validated(sd, oracle):
+    O = oracle
+    m = O.random_scene(3, 50)
+    e = engine_for(sd, O, m, O.Weights.build(m), 0)
+    for bad in (-1.0, 8.0, float("nan"), float("inf")):
+        with pytest.raises(sd.SdError):
+            e.set_exact_pruning(bad)
+    e.set_exact_pruning(24.0)
+    e.set_exact_pruning(0.0)

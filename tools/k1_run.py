@@ -1,5 +1,6 @@
 """One exact pass of a BASELINE config on cuda:0 (ncu target for K1):
-  python tools/k1_run.py [cfg=3] [alpha=100] [queries]"""
+  python tools/k1_run.py [cfg=3] [alpha=100] [queries]
+K1_TIME=reps times it; K1_PRUNE=bits turns the pruned evaluation on."""
 import os
 import sys
 
@@ -31,6 +32,8 @@ qd = torch.tensor(q, dtype=torch.float32, device=dev)
 d = torch.empty(len(q), dtype=torch.float64, device=dev)
 g = torch.empty(len(q), 3, dtype=torch.float64, device=dev)
 P = sd.SmoothParams(alpha=alpha, alpha_u=600.0, beta=0.0)
+if os.environ.get("K1_PRUNE"):  # sd_set_exact_pruning bits
+    eng.set_exact_pruning(float(os.environ["K1_PRUNE"]))
 run = lambda: eng.query_points_device(qd.data_ptr(), len(q), P, sd.SD_EXACT, d.data_ptr(), g.data_ptr())
 for _ in range(2):
     run()
