@@ -133,6 +133,9 @@ public:
         return w;
     }
 
+    // sd_set_exact_pruning: 0 (default) sums every pair like smooth_min_dist_flat
+    void set_exact_pruning(double bits) { check(sd_set_exact_pruning(ctx_, bits)); }
+
     void build_bvh(int method = SD_BVH_LBVH) { check(sd_build_bvh(ctx_, method)); }
     void set_bvh(const std::vector<BvhNode>& nodes) {
         check(sd_set_bvh(ctx_, nodes.data(), static_cast<std::int64_t>(nodes.size())));

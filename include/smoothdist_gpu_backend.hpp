@@ -72,6 +72,13 @@ class Backend {
         }
     }
 
+    // Pruned exact evaluation (sd_set_exact_pruning; 0 = the reference's sum
+    // over all pairs, the default): smooth_min_dist_flat skips primitive
+    // tiles whose terms are below 2^-bits of a lower bound of the sum.
+    void set_exact_pruning(double bits) {
+        if (sd_set_exact_pruning(ctx_, bits)) fail(sd_last_error());
+    }
+
     // The tree the engine traverses, as the reference's Bvh.
     Bvh tree() const {
         std::int64_t n = 0;

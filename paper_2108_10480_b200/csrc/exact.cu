@@ -137,16 +137,24 @@ __global__ void __launch_bounds__(kThreads, MINB) exact_kernel(const __grid_cons
         fence_mbar_init();
     }
     __syncthreads();
+    // PRUNE: the split's tiles are visited from the tile nearest the CTA's
+    // first query (t0, wrapping around), so the running totals bound the
+    // sums tightly from the first tiles on
+    [[maybe_unused]] __shared__ int t0s;
+    int t0 = 0;
+    auto tile_of = [&](int t) { return PRUNE ? (t0 + t < ntiles ? t0 + t : t0 + t - ntiles) : t; };
     auto issue = [&](int t) {
         const int s = t % kStages;
-        const int64_t b = p0 + int64_t(t) * TILE;
+        const int64_t b = p0 + int64_t(tile_of(t)) * TILE;
         const int n = int(min(int64_t(TILE), p1 - b));
         const uint32_t bytes = uint32_t(n) * R * sizeof(T);
         mbar_arrive_expect_tx(&full[s], bytes);
         bulk_g2s(tiles + size_t(s) * TILE * R, a.rec + b * R, bytes, &full[s]);
     };
-    if (threadIdx.x == 0)
-        for (int t = 0; t < kStages && t < ntiles; ++t) issue(t);
+    if constexpr (!PRUNE) {
+        if (threadIdx.x == 0)
+            for (int t = 0; t < kStages && t < ntiles; ++t) issue(t);
+    }
 
     // queries of this thread
     T qx[QPT], qy[QPT], qz[QPT];
@@ -229,6 +237,7 @@ __global__ void __launch_bounds__(kThreads, MINB) exact_kernel(const __grid_cons
     if constexpr (PRUNE) {
         const int64_t ntall = (a.count + TILE - 1) / TILE;
         float dmin2[QPT];
+        int64_t gmin = 0;
 #pragma unroll
         for (int k = 0; k < QPT; ++k) dmin2[k] = INFINITY;
         for (int64_t g = 0; g < ntall; ++g) {  // warp-uniform addresses: broadcast loads
@@ -239,9 +248,19 @@ __global__ void __launch_bounds__(kThreads, MINB) exact_kernel(const __grid_cons
                 const float fx = fmaxf(fabsf(x - lo4.x), fabsf(x - hi4.x)),
                             fy = fmaxf(fabsf(y - lo4.y), fabsf(y - hi4.y)),
                             fz = fmaxf(fabsf(z - lo4.z), fabsf(z - hi4.z));
-                dmin2[k] = fminf(dmin2[k], fmaf(fx, fx, fmaf(fy, fy, fz * fz)));
+                const float d2 = fmaf(fx, fx, fmaf(fy, fy, fz * fz));
+                if (k == 0 && d2 < dmin2[0]) gmin = g;
+                dmin2[k] = fminf(dmin2[k], d2);
             }
         }
+        if (threadIdx.x == 0) {
+            const int64_t rel = gmin - p0 / TILE;  // (p0 is tile-aligned)
+            t0s = ntiles > 0 ? int(max(int64_t(0), min(int64_t(ntiles - 1), rel))) : 0;
+        }
+        __syncthreads();
+        t0 = t0s;
+        if (threadIdx.x == 0)
+            for (int t = 0; t < kStages && t < ntiles; ++t) issue(t);
 #pragma unroll
         for (int k = 0; k < QPT; ++k)  // (NaN queries: NaN seed, no tile is pruned)
             seed[k] = fmaf(float(a.ph.kappa), sqrtf(dmin2[k]) * (1.f + 1e-5f), float(a.lwmax) - float(a.lwspan)) - a.prune;
@@ -251,7 +270,7 @@ __global__ void __launch_bounds__(kThreads, MINB) exact_kernel(const __grid_cons
         const int s = t % kStages;
         mbar_wait(&full[s], (t / kStages) & 1);
         const T* tile = tiles + size_t(s) * TILE * R;
-        const int n = int(min(int64_t(TILE), p1 - (p0 + int64_t(t) * TILE)));
+        const int n = int(min(int64_t(TILE), p1 - (p0 + int64_t(tile_of(t)) * TILE)));
         int mode = 0;
         bool skip = false;
         if (a.tbox) {
@@ -260,7 +279,7 @@ __global__ void __launch_bounds__(kThreads, MINB) exact_kernel(const __grid_cons
             // every term (smooth.hpp:85-88 zeroes them): the warp skips the
             // tile. dhi < 708/alpha: nothing can be masked. kappa dlo + lwmax
             // bounds every exponent: the shift is raised once here.
-            const int64_t g = (p0 + int64_t(t) * TILE) / TILE;
+            const int64_t g = (p0 + int64_t(tile_of(t)) * TILE) / TILE;
             const float4 lo4 = __ldg(a.tbox + 2 * g), hi4 = __ldg(a.tbox + 2 * g + 1);
             const float span = float(-a.ph.kappa) * lo4.w + float(a.lwspan);
             bool all_skip = true, all_inside = true, any_loose = false;

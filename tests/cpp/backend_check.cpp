@@ -89,6 +89,21 @@ int main(int argc, char** argv) {
     check(inf_ok, "+inf agrees", 0.0);
     check(ed <= td && eg <= tg, "smooth_min_dist (tree) d_hat / grad", std::max(ed, eg));
     check(edx <= td && egx <= tg, "smooth_min_dist_flat d_hat / grad", std::max(edx, egx));
+    {  // pruned exact evaluation against the reference's flat sum, same tolerances
+        gpu.set_exact_pruning(prec == SD_FP64 ? 64.0 : 48.0);
+        const auto gp = gpu.smooth_min_dist_flat(q, p);
+        gpu.set_exact_pruning(0.0);
+        double epd = 0, epg = 0;
+        bool pinf = true;
+        for (std::size_t i = 0; i < q.size(); ++i) {
+            const SmoothResult re = smooth_min_dist_flat(mesh, ws, SimplexGeom::point(q[i]), p);
+            if (std::isfinite(re.d_hat) != std::isfinite(gp[i].d_hat)) pinf = false;
+            if (!std::isfinite(re.d_hat)) continue;
+            epd = std::max(epd, std::abs(gp[i].d_hat - re.d_hat) / std::max(1.0, std::abs(re.d_hat)));
+            epg = std::max(epg, (gp[i].grad - re.grad).norm() / std::max(1.0, re.grad.norm()));
+        }
+        check(pinf && epd <= td && epg <= tg, "pruned smooth_min_dist_flat d_hat / grad", std::max(epd, epg));
+    }
 
     // query simplices (edges / triangles from consecutive query points): fp64 path
     std::vector<SimplexGeom> g;
