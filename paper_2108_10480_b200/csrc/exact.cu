@@ -233,6 +233,14 @@ __global__ void __launch_bounds__(kThreads, MINB) exact_kernel(const __grid_cons
         }
     };
 
+    // log2 of a running fp64 total, rounded down (exponent field), in the
+    // launch's exponent frame (unit-weight launches: relative to lw_unit)
+    [[maybe_unused]] auto total_log2 = [&](const Tot& tk) {
+        const int ex = ((__double2hiint(tk.s) >> 20) & 0x7ff) - 1023;
+        float lc = float(tk.M) + float(ex) - 1.f;  // (-1: float(M) may round up)
+        if constexpr (!POLY) lc -= float(a.ph.lw_unit);
+        return lc;
+    };
     [[maybe_unused]] float seed[QPT];
     if constexpr (PRUNE) {
         const int64_t ntall = (a.count + TILE - 1) / TILE;
@@ -262,8 +270,12 @@ __global__ void __launch_bounds__(kThreads, MINB) exact_kernel(const __grid_cons
         if (threadIdx.x == 0)
             for (int t = 0; t < kStages && t < ntiles; ++t) issue(t);
 #pragma unroll
-        for (int k = 0; k < QPT; ++k)  // (NaN queries: NaN seed, no tile is pruned)
+        for (int k = 0; k < QPT; ++k) {  // (NaN queries: NaN seed, no tile is pruned)
             seed[k] = fmaf(float(a.ph.kappa), sqrtf(dmin2[k]) * (1.f + 1e-5f), float(a.lwmax) - float(a.lwspan)) - a.prune;
+            // later segments of a mixed mesh: the sum of the earlier ones bounds c too
+            const Tot& tk = tot[k * kThreads + threadIdx.x];
+            if (tk.s > 0.0) seed[k] = fmaxf(seed[k], total_log2(tk) - a.prune);
+        }
     }
 
     for (int t = 0; t < ntiles; ++t) {
@@ -350,12 +362,7 @@ __global__ void __launch_bounds__(kThreads, MINB) exact_kernel(const __grid_cons
 #pragma unroll
                 for (int k = 0; k < QPT; ++k) {
                     const Tot& tk = tot[k * kThreads + threadIdx.x];
-                    if (tk.s > 0.0) {
-                        const int ex = ((__double2hiint(tk.s) >> 20) & 0x7ff) - 1023;
-                        float lc = float(tk.M) + float(ex) - 1.f;  // (-1: float(M) may round up)
-                        if constexpr (!POLY) lc -= float(a.ph.lw_unit);
-                        seed[k] = fmaxf(seed[k], lc - a.prune);
-                    }
+                    if (tk.s > 0.0) seed[k] = fmaxf(seed[k], total_log2(tk) - a.prune);
                 }
             }
         }
