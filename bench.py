@@ -1096,6 +1096,8 @@ def run_cfg5(args, rank, world, local):
     eng = sd.Engine(local, sd.SD_FP32)
     eng.set_geometry(sh.vertices, sh.simplices, sh.kinds)
     eng.set_weights(wt.A, wt.sup_wtilde, wt.edge_a, wt.tri_stored, sh.poly_index)
+    if exact and args.prune > 0:
+        eng.set_exact_pruning(args.prune)
     tb = time.perf_counter()
     # BENCH_TREE=median builds the reference's median-split tree instead (A/B)
     if not exact:
@@ -1189,7 +1191,7 @@ def run_cfg5(args, rank, world, local):
         om = O.Mesh.from_arrays(v, w.simplices, w.kinds)
         ow = O.Weights.from_table(O.WeightTable(wt.A, wt.sup_wtilde, wt.edge_a, wt.tri_stored, wt.poly_index))
         ot = None if exact else O.Tree.from_nodes(eng.export_bvh())
-        nsamp = 16 if exact else 4096
+        nsamp = (64 if args.prune > 0 else 16) if exact else 4096
         sample = np.linspace(0, Q - 1, nsamp).astype(np.int64)
         r = O.query(om, ow, q[sample], O.Params(alpha=w.alpha, alpha_u=600.0, beta=0.0 if exact else w.beta),
                     tree=None if exact else ot, threads=threads)
@@ -1222,6 +1224,7 @@ def run_cfg5(args, rank, world, local):
                                              "owner-side reduce + finalize" if exchange == "peer" else
                                              f"one NCCL all_reduce(SUM) of 4 fp64 per query; exchange={exchange}"),
                            "primitives_per_gpu": len(sh.kinds), "l2": "flushed between timed steps"},
+                "pruning_bits": (args.prune if exact else None),
                 "finite_fraction": fin, "gpu_launches": launches[0] * args.steps, "cpu_baseline": cpu,
                 "setup_s": {"total": setup, "generate": tg, "build_weights": tw, "build_tree": tb},
                 "clocks": clk.summary()}
@@ -1388,6 +1391,8 @@ def main():
                     help="0 = the default line (cfg3 headline + cfg2 + cfg4), 5 = configs[4] primitive-sharded")
     ap.add_argument("--exact", action="store_true", help="--config 5: the exact path instead of the BVH path")
     ap.add_argument("--exact-queries", type=int, default=65536, help="--config 5 --exact: evenly spaced queries")
+    ap.add_argument("--prune", type=float, default=0.0,
+                    help="--config 5 --exact: sd_set_exact_pruning bits (0 = every pair, the default)")
     ap.add_argument("--bvh-fp64", action="store_true", help="run only the BVH leg, in fp64")
     ap.add_argument("--fp64", action="store_true", help="--render in fp64")
     ap.add_argument("--m2m", action="store_true", help="mesh-to-mesh evaluations of the paper's timing table rows")

@@ -20,9 +20,22 @@ __device__ __forceinline__ void finalize_write(double M, double s, double gx, do
                                                const int64_t* __restrict__ leaves_in, const int64_t* __restrict__ far_in,
                                                const uint64_t* __restrict__ hash_in, const int64_t* __restrict__ perm,
                                                const FinalizeOut& o) {
-    const double scale = M > -INFINITY ? exp2(M) : 0.0;
-    double c = s * scale;
-    double cx = gx * scale, cy = gy * scale, cz = gz * scale;
+    double c, cx, cy, cz;
+    if (M < -1000.0 && M > -INFINITY) {
+        // The anchor can sit below fp64's exponent range while the sum does
+        // not: the first tile with a nonzero sum anchors the totals at its
+        // shift (a far tile just inside the -708 mask: ~ -1021 - 96), and
+        // nearer tiles within 2^512 of it add to s without re-anchoring, so
+        // s 2^M is representable (2^-760, say) although 2^M alone is 0.
+        // Scale in two steps.
+        const double h = exp2(0.5 * M), h2 = exp2(M - 0.5 * M);
+        c = (s * h) * h2;
+        cx = (gx * h) * h2, cy = (gy * h) * h2, cz = (gz * h) * h2;
+    } else {
+        const double scale = M > -INFINITY ? exp2(M) : 0.0;
+        c = s * scale;
+        cx = gx * scale, cy = gy * scale, cz = gz * scale;
+    }
     const int64_t j = perm ? perm[i] : i;  // tree path: undo the query sort
     if (o.nan_keys) {
         if (o.nan_keys[i] == 0xffffffffu) c = cx = cy = cz = NAN;

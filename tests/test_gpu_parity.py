@@ -1177,3 +1177,36 @@ def test_pruning_threshold_is_validated(sd, oracle):
             e.set_exact_pruning(bad)
     e.set_exact_pruning(24.0)
     e.set_exact_pruning(0.0)
+
+
+@pytest.mark.parametrize("prec", [0, 1])
+@pytest.mark.parametrize("side", [1.0, -1.0])
+def test_far_tile_first_then_near_tiles(sd, oracle, prec, side, monkeypatch):
+    """A far cluster (alpha d = 700, just inside the -708 mask) summed before
+    a nearer one (alpha d = 530) by the same CTA: the totals stay anchored at
+    the far tile's shift (below 2^-1074), and the de-shift in K4 must still
+    return c ~ 600 e^-530 instead of 0 (found on cfg5: d_hat = +inf for
+    queries ~5.3 from the nearest primitive)."""
+    O = oracle
+    rng = np.random.default_rng(5)
+    far = np.array([3.0, 0.0, 0.0]) + 0.005 * rng.standard_normal((1024, 3))
+    near = np.array([4.7, 0.0, 0.0]) + 0.005 * rng.standard_normal((600, 3))
+    v = side * np.concatenate([far, near])
+    n = len(v)
+    simp = np.stack([np.arange(n), np.full(n, -1), np.full(n, -1)], axis=1).astype(np.int32)
+    m0 = O.Mesh.from_arrays(v, simp, np.zeros(n, np.uint8))
+    qs = side * (np.array([10.0, 0.0, 0.0]) + 0.01 * rng.standard_normal((70, 3)))
+    m, q = prep(O, m0, qs, prec)
+    w = O.Weights.build(m)
+    e = engine_for(sd, O, m, w, prec)
+    P = sd.SmoothParams(alpha=100.0, beta=0.0)
+    ref = O.query(m, w, q, O.Params(alpha=100.0, beta=0.0))
+    assert np.isfinite(ref.d_hat).all() and (ref.c < 1e-200).all()
+    for splits in ("1", "2", ""):
+        if splits:
+            monkeypatch.setenv("SDGPU_EXACT_SPLITS", splits)
+        else:
+            monkeypatch.delenv("SDGPU_EXACT_SPLITS", raising=False)
+        got = e.query_points(q, P, sd.SD_EXACT, want_c=True)
+        assert_close(got, ref, prec, 100.0, f"far tile first, splits {splits!r}")
+        assert np.abs(got.c / ref.c - 1).max() < (1e-3 if prec == 0 else 1e-9)
