@@ -518,13 +518,13 @@ def exact_leg(run, eng, q, prec, N, kind, P, steps, warmup, flush, stream, peaks
 PRUNE_BITS = 48.0
 
 
-def pruned_leg(run, eng, q, prec, N, kind, P, steps, flush, stream, peaks, q_total, full, base_ms):
+def pruned_leg(run, eng, q, prec, N, kind, P, steps, flush, stream, peaks, q_total, full, base_ms, bits=PRUNE_BITS):
     """The same exact configuration with sd_set_exact_pruning(48): an extra
     key, never the headline. Tiles whose terms are below 2^-48 of a lower
     bound of the query's sum are skipped, so `value` is the all-pairs
     EQUIVALENT rate (Q x N / time, skipped pairs counted); every timed
     answer of this rank is compared with the all-pairs kernel's."""
-    eng.set_exact_pruning(PRUNE_BITS)
+    eng.set_exact_pruning(bits)
     try:
         r, d, g = exact_leg(run, eng, q, prec, N, kind, P, steps, 3, flush, stream, peaks, q_total=q_total)
     finally:
@@ -533,7 +533,7 @@ def pruned_leg(run, eng, q, prec, N, kind, P, steps, flush, stream, peaks, q_tot
         r["roofline_all_pairs"] = r.pop("roofline")
         r["roofline_all_pairs"]["note"] = "counts skipped pairs too; not a pipe utilisation"
     r["unit"] = "pair-evals/s (all-pairs equivalent)"
-    r["pruning_bits"] = PRUNE_BITS
+    r["pruning_bits"] = bits
     r["speedup_over_all_pairs"] = base_ms / r["ms_per_step"]
     d0, g0 = full
     fin = np.isfinite(d0)
@@ -541,8 +541,8 @@ def pruned_leg(run, eng, q, prec, N, kind, P, steps, flush, stream, peaks, q_tot
         "n": int(len(d0)), "inf_mismatch": int((np.isfinite(d) != fin).sum()),
         "d_hat_max_abs": float(np.abs(d[fin] - d0[fin]).max()) if fin.any() else 0.0,
         "grad_max_abs": float(np.abs(g[fin] - g0[fin]).max()) if fin.any() else 0.0,
-        "bound": f"relative error of c < N 2^-{PRUNE_BITS:g} = {N * 2.0 ** -PRUNE_BITS:.1e} (include/sdgpu.h); the rest "
-                 "is fp32 regrouping of the tile sums"}
+        "bound": f"relative error of c < N 2^-{bits:g} = {N * 2.0 ** -bits:.1e} (include/sdgpu.h); the rest "
+                 "is regrouping of the tile sums (another tile order)"}
     return r, d, g
 
 
@@ -653,6 +653,11 @@ def run_exact_headline(args, run, peaks, stream, flush, line):
                                     r["ms_per_step"])
             line["exact_cfg2_pruned"] = rp
             res2["pruned"] = (dp, gp)
+        else:  # the reference's precision: 64 bits keep the fp64 path's 1e-10 bound
+            rp, dp, gp = pruned_leg(run, e, qb2, prec, N2, 1, P2, max(1, min(args.steps, 5)), flush, stream, peaks,
+                                    len(q2), (d, g), r["ms_per_step"], bits=64.0)
+            line["exact_cfg2_fp64_pruned"] = rp
+            res2["pruned64"] = (dp, gp)
         e.close()
     # ---- cfg1 point cloud (BASELINE configs[0]), fp64 as specified
     from paper_2108_10480_b200 import configs as cf
@@ -687,7 +692,7 @@ def run_exact_headline(args, run, peaks, stream, flush, line):
         cpu2 = {"value": n * N2 / r.seconds, "unit": "pair-evals/s", "cores": arm.threads, "kind": arm.kind,
                 "sample": f"first {n} of {len(qb2)} cfg2 queries x {N2} edges ({r.seconds:.1f} s, fp64, {arm.kind})"}
         for prec, key, dt in ((sd.SD_FP32, "exact_cfg2", "f32"), (sd.SD_FP64, "exact_cfg2_fp64", "f64"),
-                              ("pruned", "exact_cfg2_pruned", "f32")):
+                              ("pruned", "exact_cfg2_pruned", "f32"), ("pruned64", "exact_cfg2_fp64_pruned", "f64")):
             d, g = res2[prec]
             par[key] = parity_stats(d[:n], g[:n], r.d_hat, r.grad, 100.0, dt)
             par[key]["sample"] = f"first {n} timed queries of rank 0's block"
